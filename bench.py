@@ -1,0 +1,317 @@
+#!/usr/bin/env python3
+"""Benchmark of the hot path: minibatch SGD training of the paper's 784-30-10 MNIST net
+(BASELINE.json configs[1], "config 2"), synthetic digit-shaped data, on B200.
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference] [--config 2]
+
+A "step" is one SGD step (forward, backward, batch-summed tendencies, update) over one
+minibatch of B=1000 rows drawn at a random contiguous start from the resident 50000-row
+dataset.  K steps run as ONE nf_train_steps call (the fused persistent kernel
+for this config).  Timing: CUDA events on the launching stream around exactly K steps,
+barrier + synchronize on both sides, repeated R times (>= 1 s in total so nvidia-smi can
+sample clocks during the timed region); the median rep is reported, max over ranks.
+The dataset (157 MB) is larger than L2 (126 MB); L2 is not flushed between reps.
+
+Prints ONE JSON line (rank 0).  --impl reference times the CPU oracle (oracle/, fp32
+build = the paper's real32) on the same config instead.
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import threading
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+import synth  # noqa: E402
+
+BYTES_PER_SAMPLE = {  # algorithmic HBM bytes per training sample: x row + y row, fp32
+    cid: 4 * (c["dims"][0] + c["dims"][-1]) for cid, c in synth.CONFIGS.items()
+}
+
+
+def flops_per_sample(dims):
+    """Dense useful flops per training sample: forward 2*n_l*n_{l-1} per layer, backward delta
+    2*n_l*n_{l-1} for layers >= 2, weight gradient 2*n_l*n_{l-1} per layer."""
+    f = 0
+    for l in range(1, len(dims)):
+        mac = dims[l] * dims[l - 1]
+        f += 2 * mac + 2 * mac + (2 * mac if l >= 2 else 0)
+    return f
+
+
+def measured_peaks():
+    path = os.path.join(ROOT, "MEASURED_PEAKS.json")
+    try:
+        with open(path) as f:
+            return json.load(f), "measured"
+    except Exception:
+        return {"hbm_gbs": 6650.0, "bf16_tflops": 1590.0, "bf16_tflops_sustained": 1400.0}, "fallback"
+
+
+class ClockSampler:
+    """nvidia-smi clocks/throttle reasons sampled every 100 ms while the timed region runs."""
+
+    FIELDS = ("clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.hw_slowdown,"
+              "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
+              "clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, index: int):
+        self.index, self.rows, self.proc = index, [], None
+
+    def __enter__(self):
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", "-i", str(self.index), f"--query-gpu={self.FIELDS}",
+                 "--format=csv,noheader,nounits", "-lms", "100"],
+                stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            self.t = threading.Thread(target=self._read, daemon=True)
+            self.t.start()
+            time.sleep(0.3)
+        except FileNotFoundError:
+            self.proc = None
+        return self
+
+    def _read(self):
+        for line in self.proc.stdout:
+            parts = [p.strip() for p in line.split(",")]
+            if len(parts) == 7:
+                self.rows.append(parts)
+
+    def __exit__(self, *a):
+        if self.proc:
+            time.sleep(0.15)
+            self.proc.terminate()
+            self.proc.wait(timeout=5)
+
+    def summary(self):
+        if not self.rows:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"]}
+        sm = [float(r[0]) for r in self.rows if r[0].replace(".", "").isdigit()]
+        mx = [float(r[1]) for r in self.rows if r[1].replace(".", "").isdigit()]
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        reasons = sorted({names[i] for r in self.rows for i in range(4) if r[3 + i].lower() == "active"})
+        return {"sm_mhz": statistics.median(sm) if sm else None, "sm_max_mhz": max(mx) if mx else None,
+                "reasons": reasons, "samples": len(self.rows)}
+
+
+def dist_setup(n_gpus):
+    import torch
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    if world > 1:
+        import torch.distributed as dist
+        torch.cuda.set_device(local)
+        dist.init_process_group("nccl")
+    return world, rank, local
+
+
+def barrier(world):
+    if world > 1:
+        import torch.distributed as dist
+        dist.barrier()
+
+
+def max_over_ranks(v, world):
+    if world == 1:
+        return v
+    import torch
+    import torch.distributed as dist
+    t = torch.tensor([v], dtype=torch.float64, device="cuda")
+    dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    return float(t.item())
+
+
+def run_cpu_oracle(cid, steps, bits=32):
+    """The oracle as it stands (single-threaded C), `steps` SGD steps of config `cid`."""
+    import oracle
+    cfg = synth.CONFIGS[cid]
+    X, Y = synth.dataset(cid)
+    starts = synth.batch_starts(cid, steps=steps, N=len(X))
+    o = oracle.Oracle(cfg["dims"], cfg["act"], bits=bits)
+    p = synth.init_params(cid)
+    o.train_steps(p, X, Y, cfg["batch"], starts[:1], cfg["eta"])  # page in
+    t0 = time.perf_counter()
+    o.train_steps(p, X, Y, cfg["batch"], starts, cfg["eta"])
+    dt = time.perf_counter() - t0
+    return steps * cfg["batch"] / dt, dt
+
+
+def reference_arm(args):
+    """--impl reference: the CPU oracle on this config (rank 0 only)."""
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    if rank != 0:
+        return
+    cid = args.config
+    cfg = synth.CONFIGS[cid]
+    import oracle
+    X, Y = synth.dataset(cid)
+    starts = synth.batch_starts(cid, steps=args.warmup + args.steps, N=len(X))
+    o = oracle.Oracle(cfg["dims"], cfg["act"], bits=32)
+    p = synth.init_params(cid)
+    if args.warmup:
+        p, _ = o.train_steps(p, X, Y, cfg["batch"], starts[:args.warmup], cfg["eta"])
+    t0 = time.perf_counter()
+    o.train_steps(p, X, Y, cfg["batch"], starts[args.warmup:], cfg["eta"])
+    dt = time.perf_counter() - t0
+    v = args.steps * cfg["batch"] / dt
+    line = {
+        "impl": "reference", "metric": "training samples/sec (fwd+bwd+SGD)", "value": v,
+        "unit": "samples/s", "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
+        "ms_per_step": dt * 1e3 / args.steps, "higher_is_better": True, "scaling": "weak",
+        "vs_baseline": None, "dtype": "f32", "data": "synthetic",
+        "config": {"workload": cfg["name"], "dims": cfg["dims"], "batch": cfg["batch"]},
+        "cpu_baseline": {"value": v, "unit": "samples/s", "cores": 1, "kind": "oracle",
+                         "sample": f"{args.steps} full SGD steps of B={cfg['batch']} (fp32 build of "
+                                   f"oracle/nf_oracle.c, single thread)"},
+        "e2e": {"value": v, "unit": "samples/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+    }
+    print(json.dumps(line), flush=True)
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=500)
+    ap.add_argument("--warmup", type=int, default=50)
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--config", type=int, default=2)
+    ap.add_argument("--min-seconds", type=float, default=1.0)
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--no-e2e", action="store_true")
+    args = ap.parse_args()
+    if args.warmup < 3:
+        ap.error("--warmup must be >= 3")
+    if args.impl == "reference":
+        return reference_arm(args)
+
+    import torch
+    from paper_1902_06714_b200 import build as nfbuild
+    nfbuild.build()
+    import paper_1902_06714_b200 as nf
+
+    world, rank, local = dist_setup(args.gpus)
+    cid = args.config
+    cfg = synth.CONFIGS[cid]
+    B, K, W = cfg["batch"], args.steps, args.warmup
+    X, Y = synth.dataset(cid)
+    N = len(X)
+    starts = synth.batch_starts(cid, steps=W + K, N=N)
+    Xd, Yd = torch.from_numpy(X).cuda(), torch.from_numpy(Y).cuda()
+    stream = torch.cuda.current_stream()
+    net = nf.Net(cfg["dims"], cfg["act"], stream=stream)
+    net.set_params(torch.from_numpy(synth.init_params(cid)).cuda())
+    loss = torch.zeros(K, device="cuda")
+
+    # warm-up (W untimed steps)
+    net.train_steps(Xd, Yd, B, starts[:W], cfg["eta"])
+    torch.cuda.synchronize()
+
+    def timed_rep():
+        barrier(world)
+        torch.cuda.synchronize()
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record(stream)
+        net.train_steps(Xd, Yd, B, starts[W:], cfg["eta"], step_loss=loss)
+        e1.record(stream)
+        torch.cuda.synchronize()
+        barrier(world)
+        return e0.elapsed_time(e1) / 1e3
+
+    l0 = nf.nf_launch_count()
+    t_first = timed_rep()
+    launches = nf.nf_launch_count() - l0
+    reps = max(5, min(2000, int(args.min_seconds / max(t_first, 1e-6)) + 1))
+    times = []
+    with ClockSampler(local) as clk:
+        for _ in range(reps):
+            times.append(timed_rep())
+    t_med = statistics.median(times)
+    t_max = max_over_ranks(t_med, world)
+    value = world * K * B / t_max
+
+    peaks, peak_src = measured_peaks()
+    alg_bytes = K * B * BYTES_PER_SAMPLE[cid]
+    achieved = alg_bytes / t_med / 1e9
+    traffic = None
+    prof = os.path.join(ROOT, "profiles", f"traffic_c{cid}.json")
+    if os.path.exists(prof):
+        try:
+            traffic = json.load(open(prof)).get("bytes_per_launch")
+        except Exception:
+            traffic = None
+
+    # ---- e2e: same metric through the C-ABI with pinned HOST buffers; each step's batch
+    # is copied host->device inside the call, the step losses are read back to the host.
+    e2e = None
+    if not args.no_e2e:
+        Xh = torch.from_numpy(X).pin_memory()
+        Yh = torch.from_numpy(Y).pin_memory()
+        lh = torch.empty(K, dtype=torch.float32).pin_memory()
+
+        def e2e_rep():
+            barrier(world)
+            torch.cuda.synchronize()
+            e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            e0.record(stream)
+            net.train_steps(Xh, Yh, B, starts[W:], cfg["eta"], step_loss=loss)
+            lh.copy_(loss, non_blocking=True)
+            e1.record(stream)
+            torch.cuda.synchronize()
+            barrier(world)
+            return e0.elapsed_time(e1) / 1e3
+
+        e2e_rep()
+        te = statistics.median([e2e_rep() for _ in range(3)])
+        te = max_over_ranks(te, world)
+        e2e = {"value": world * K * B / te, "unit": "samples/s",
+               "h2d_bytes_per_step": B * BYTES_PER_SAMPLE[cid], "d2h_bytes_per_step": 4}
+
+    cpu = None
+    if rank == 0 and world == 1 and not args.no_cpu_baseline:
+        cpu_steps = {1: 20000, 2: 200, 3: 1, 4: 3, 5: 1}[cid]
+        v, dt = run_cpu_oracle(cid, cpu_steps)
+        cpu = {"value": v, "unit": "samples/s", "cores": 1, "kind": "oracle",
+               "sample": f"{cpu_steps} SGD steps of B={B} on config {cid} ({dt:.1f} s), fp32 build of "
+                         f"oracle/nf_oracle.c, single thread"}
+
+    if rank == 0:
+        fl = flops_per_sample(cfg["dims"])
+        line = {
+            "metric": "training samples/sec (fwd+bwd+SGD)",
+            "value": value, "unit": "samples/s", "n_gpus": world, "steps": K, "warmup": W,
+            "ms_per_step": t_max * 1e3 / K, "higher_is_better": True, "scaling": "weak",
+            "vs_baseline": None, "dtype": "f32", "data": "synthetic",
+            "config": {"workload": cfg["name"], "dims": cfg["dims"], "batch": B, "dataset_rows": N,
+                       "eta": cfg["eta"], "steps_per_timed_call": K, "reps": reps, "stat": "median rep",
+                       "l2": f"dataset {X.nbytes / 1e6:.0f} MB > 126 MB L2, not flushed",
+                       "parallelism": f"replicas x{world}" if world > 1 else "1 GPU"},
+            "roofline": {"bound": "hbm", "achieved": achieved, "peak": peaks["hbm_gbs"], "unit": "GB/s",
+                         "frac": achieved / peaks["hbm_gbs"], "traffic": traffic,
+                         "peak_source": f"MEASURED_PEAKS.json hbm_gbs ({peak_src})",
+                         "kernel": "fused_small_kernel" if len(cfg["dims"]) == 3 else "gemm_simt",
+                         "algorithmic_bytes_per_launch": alg_bytes},
+            "flops": {"per_sample": fl, "achieved_tflops": fl * K * B / t_med / 1e12},
+            "cpu_baseline": cpu,
+            "e2e": e2e,
+            "gpu_launches": launches,
+            "clocks": clk.summary(),
+        }
+        print(json.dumps(line), flush=True)
+    if world > 1:
+        import torch.distributed as dist
+        dist.destroy_process_group()
+
+
+if __name__ == "__main__":
+    main()

@@ -1,0 +1,146 @@
+/*
+ * nf.h -- C-ABI of the B200-native hot path of neural-fortran (Curcic,
+ * arXiv:1902.06714): minibatch SGD training of a dense feed-forward network.
+ *
+ * Citations: "P:n" = PAPER.md line n (the paper), "S:n" = SPEC.md line n.
+ * The entry points follow the paper's network interface: constructor
+ * network_type(dims, activation), output, train on a
+ * batch, accuracy and the quadratic cost.
+ *
+ * Conventions for every call
+ *   - All tensors are fp32, row-major [n][width] (one sample per row; the
+ *     paper's column-major x(:,i) has the same memory order).
+ *   - Caller buffers (x, y, out, grad, params) may be HOST pointers (pageable
+ *     or pinned) or CUDA DEVICE pointers; the library tells them apart with
+ *     cudaPointerGetAttributes.  Host inputs are copied to device staging
+ *     buffers on the net's stream; host outputs are copied back and the call
+ *     synchronises before returning.  With device pointers the call is
+ *     asynchronous on the net's stream (unless stated) and the caller keeps
+ *     the buffers alive until the stream reaches the call.
+ *   - Pointers must be 4-byte aligned.  No other alignment is required (the
+ *     runtime picks vector widths per pointer).
+ *   - Parameters, workspaces and staging buffers are owned by the library.
+ *   - Return value: NF_OK (0) or a negative NF_E* code; nf_last_error()
+ *     returns a thread-local text for the last failing call.
+ *   - A net is used by one stream (one host thread) at a time.
+ *
+ * Parameter layout ("flat"): for l = 1..L, W_l [n_l][n_{l-1}] row-major, then
+ * b_l [n_l].  W_l[i][k] connects input k of layer l-1 to neuron i of layer l;
+ * this is the paper's w(k,i) stored in layer l-1 in the same
+ * column-major memory order.  b_l lives with layer l.
+ */
+#ifndef NF_H
+#define NF_H
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+typedef struct nf_net nf_net;
+
+enum {
+    NF_OK = 0,
+    NF_EINVAL = -1,       /* bad argument: see nf_last_error()            */
+    NF_ECUDA = -2,        /* CUDA runtime error (message has its string)  */
+    NF_ENOMEM = -3,       /* device allocation failed                     */
+    NF_ENODEV = -4        /* no sm_100 device: there is NO CPU fallback   */
+};
+
+/* Numerics mode of the contractions (nf_set_math).
+ *   NF_MATH_FP32 : fp32 storage, fp32 FMA accumulation (default; the paper's
+ *                  real32).  Parity bar 1e-4 (BASELINE.json).
+ *   NF_MATH_TF32 : TF32 tensor-core tiles, fp32 accumulate, where a kernel
+ *                  has them (configs 3 and 5).  Parity bar 5e-3.           */
+enum { NF_MATH_FP32 = 0, NF_MATH_TF32 = 1 };
+
+/* Constructor (network_constructor_listing).
+ *   dims[0..n_dims-1] : neurons per layer incl. input and output;
+ *                       n_dims >= 2, every dim >= 1.
+ *   activation        : "sigmoid" | "tanh" | "relu" | "gaussian" | "step"
+ *                       (P:108-109), or "hidden,output" (e.g. "relu,sigmoid")
+ *                       to give the output layer its own activation (an
+ *                       extension, reading R7).  NULL means "sigmoid", the
+ *                       paper's default.  Unknown -> NF_EINVAL.
+ *   seed              : initial parameters are drawn on the host from a
+ *                       documented splitmix64/Box-Muller stream:
+ *                       W ~ N(0,1)/n_{l-1} ("normalized by the number of
+ *                       neurons in the layer"), b ~ N(0,1) (R2).
+ *                       Benchmarks and tests overwrite them with nf_set_params.
+ *   *out              : receives the new net (owned by the caller, release
+ *                       with nf_net_destroy).
+ * Fails with NF_ENODEV when no sm_100 GPU is present.                       */
+int nf_net_create(const int32_t *dims, int32_t n_dims, const char *activation,
+                  uint64_t seed, nf_net **out);
+
+/* Synchronises the net's stream and frees everything the net owns. */
+void nf_net_destroy(nf_net *net);
+
+/* Sets the CUDA stream (a cudaStream_t; NULL = legacy default stream) on
+ * which every later call of this net is ordered. */
+int nf_set_stream(nf_net *net, void *cuda_stream);
+
+/* NF_MATH_FP32 or NF_MATH_TF32 (see above). */
+int nf_set_math(nf_net *net, int mode);
+
+/* Number of parameters: sum_l n_l*n_{l-1} + n_l ([3,5,2] -> 32). */
+int64_t nf_param_count(const nf_net *net);
+
+/* Copies the flat parameters out (dst: count floats, host or device).
+ * count must equal nf_param_count.  Host dst: synchronous. */
+int nf_get_params(nf_net *net, float *dst, int64_t count);
+
+/* Replaces the flat parameters (src: count floats, host or device). */
+int nf_set_params(nf_net *net, const float *src, int64_t count);
+
+/* The paper's `output`: forward pass without caching.
+ *   x   [n][n_0]  inputs;  out [n][n_L] receives a_L.  n >= 0.            */
+int nf_output(nf_net *net, const float *x, int64_t n, float *out);
+
+/* One SGD step on a batch: the paper's train_batch with its
+ * fwdprop and backprop per sample, tendencies summed
+ * over the batch (the co_sum) and the update
+ *   W_l -= (eta/n) * sum_s delta_l(s) a_{l-1}(s)^T,  b_l -= (eta/n) sum_s delta_l(s)
+ * (reading R3).  Every sample sees the pre-step parameters.
+ *   x [n][n_0], y [n][n_L] (targets, e.g. one-hot labels), n >= 1,
+ *   eta finite.  eta = 0 leaves the parameters bitwise unchanged.          */
+int nf_train_batch(nf_net *net, const float *x, const float *y, int64_t n, float eta);
+
+/* The MNIST driver's minibatch loop moved on-device (extension):
+ * for s = 0..n_steps-1, nf_train_batch on rows [starts[s], starts[s]+batch)
+ * of the resident dataset X [N][n_0], Y [N][n_L].
+ *   starts     : HOST array of n_steps int64, each in [0, N-batch] (R11).
+ *   step_loss  : NULL or a DEVICE array of n_steps floats receiving the mean
+ *                quadratic cost of step s's batch under the pre-step
+ *                parameters (the cost evaluated by step 1 of SGD).
+ * Small nets (two layers, widths <= 32) run as ONE persistent kernel for all
+ * steps; others as a sequence of fused kernels per step.                    */
+int nf_train_steps(nf_net *net, const float *X, const float *Y, int64_t N, int64_t batch,
+                   const int64_t *starts, int64_t n_steps, float eta, float *step_loss);
+
+/* The paper's backprop + co_sum without the update: writes the
+ * batch-summed tendencies in the flat parameter layout (grad: count floats).
+ * Parameters are unchanged.  (Extension, for gradient parity.)             */
+int nf_grad(nf_net *net, const float *x, const float *y, int64_t n, float *grad);
+
+/* Mean quadratic cost (1/n) sum_s 1/2 ||a_L(x_s) - y_s||^2 (reading R9)
+ * written to *loss (host).  n = 0 -> 0.  Synchronises. */
+int nf_loss(nf_net *net, const float *x, const float *y, int64_t n, float *loss);
+
+/* Accuracy: fraction of samples with
+ * argmax a_L(x_s) == argmax y_s, first index on ties (R10), to *acc (host).
+ * n = 0 -> 0.0.  Synchronises. */
+int nf_accuracy(nf_net *net, const float *x, const float *y, int64_t n, float *acc);
+
+/* Thread-local text of the last error ("" if none). */
+const char *nf_last_error(void);
+
+/* Number of this library's kernels launched since load (for the bench's
+ * gpu_launches claim).  Counts launches, not graph replays. */
+int64_t nf_launch_count(void);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* NF_H */

@@ -1,0 +1,246 @@
+"""B200-native hot path of neural-fortran (Curcic, arXiv:1902.06714): minibatch SGD
+training of a dense feed-forward network, behind the C-ABI of ``include/nf.h``.
+
+This module is a thin ctypes binding: argument marshalling only.  Every step of
+the method runs in the CUDA kernels of ``libnf_b200.so`` (built in-tree by
+``paper_1902_06714_b200.build``).  There is no CPU fallback: if the library is
+missing, importing raises; if no sm_100 GPU is present, ``nf_net_create``
+fails with ``NF_ENODEV``.
+
+The functions carry the C names (``nf_net_create``, ``nf_output``,
+``nf_train_batch``, ``nf_train_steps``, ``nf_grad``, ``nf_loss``,
+``nf_accuracy``, ...).  Array arguments may be torch tensors (CUDA or CPU) or
+numpy arrays; they must be contiguous fp32 (int64 for ``starts``).
+``Net`` is a small object wrapper over the same calls.
+"""
+from __future__ import annotations
+
+import ctypes
+import os
+
+import numpy as np
+
+_PKG = os.path.dirname(os.path.abspath(__file__))
+LIB_PATH = os.path.join(_PKG, "libnf_b200.so")
+
+NF_OK, NF_EINVAL, NF_ECUDA, NF_ENOMEM, NF_ENODEV = 0, -1, -2, -3, -4
+NF_MATH_FP32, NF_MATH_TF32 = 0, 1
+
+
+class NFError(RuntimeError):
+    def __init__(self, code: int, msg: str):
+        super().__init__(f"nf error {code}: {msg}")
+        self.code = code
+
+
+def _load() -> ctypes.CDLL:
+    if not os.path.exists(LIB_PATH):
+        raise ImportError(f"{LIB_PATH} is missing: build it with `python -m paper_1902_06714_b200.build` "
+                          "(there is no CPU fallback)")
+    lib = ctypes.CDLL(LIB_PATH)
+    P, I64, I32, F, U64 = ctypes.c_void_p, ctypes.c_int64, ctypes.c_int32, ctypes.c_float, ctypes.c_uint64
+    sig = {
+        "nf_net_create": (ctypes.c_int, [P, I32, ctypes.c_char_p, U64, ctypes.POINTER(P)]),
+        "nf_net_destroy": (None, [P]),
+        "nf_set_stream": (ctypes.c_int, [P, P]),
+        "nf_set_math": (ctypes.c_int, [P, ctypes.c_int]),
+        "nf_param_count": (I64, [P]),
+        "nf_get_params": (ctypes.c_int, [P, P, I64]),
+        "nf_set_params": (ctypes.c_int, [P, P, I64]),
+        "nf_output": (ctypes.c_int, [P, P, I64, P]),
+        "nf_train_batch": (ctypes.c_int, [P, P, P, I64, F]),
+        "nf_train_steps": (ctypes.c_int, [P, P, P, I64, I64, P, I64, F, P]),
+        "nf_grad": (ctypes.c_int, [P, P, P, I64, P]),
+        "nf_loss": (ctypes.c_int, [P, P, P, I64, ctypes.POINTER(F)]),
+        "nf_accuracy": (ctypes.c_int, [P, P, P, I64, ctypes.POINTER(F)]),
+        "nf_last_error": (ctypes.c_char_p, []),
+        "nf_launch_count": (I64, []),
+    }
+    for name, (res, args) in sig.items():
+        fn = getattr(lib, name)
+        fn.restype, fn.argtypes = res, args
+    return lib
+
+
+_lib = _load()
+
+# Every symbol include/nf.h declares (checked by tests/test_abi.py).
+EXPORTS = ("nf_net_create", "nf_net_destroy", "nf_set_stream", "nf_set_math", "nf_param_count",
+           "nf_get_params", "nf_set_params", "nf_output", "nf_train_batch", "nf_train_steps",
+           "nf_grad", "nf_loss", "nf_accuracy", "nf_last_error", "nf_launch_count")
+
+
+def lib() -> ctypes.CDLL:
+    return _lib
+
+
+def _check(rc: int):
+    if rc != NF_OK:
+        raise NFError(rc, _lib.nf_last_error().decode())
+
+
+def _ptr(a, dtype=np.float32):
+    """Data pointer of a contiguous torch tensor or numpy array (no copies)."""
+    if a is None:
+        return None
+    if hasattr(a, "data_ptr"):          # torch.Tensor
+        import torch
+        want = {np.float32: torch.float32, np.int64: torch.int64}[dtype]
+        if a.dtype != want or not a.is_contiguous():
+            raise TypeError(f"expected a contiguous {want} tensor")
+        return ctypes.c_void_p(a.data_ptr())
+    if not isinstance(a, np.ndarray) or a.dtype != dtype or not a.flags.c_contiguous:
+        raise TypeError(f"expected a C-contiguous {np.dtype(dtype).name} array")
+    return a.ctypes.data_as(ctypes.c_void_p)
+
+
+# ---------------------------------------------------------------- C-named functions
+def nf_net_create(dims, activation: str = "sigmoid", seed: int = 0):
+    d = np.ascontiguousarray(np.asarray(dims, dtype=np.int32))
+    out = ctypes.c_void_p()
+    _check(_lib.nf_net_create(d.ctypes.data_as(ctypes.c_void_p), len(d),
+                              None if activation is None else activation.encode(), seed, ctypes.byref(out)))
+    return out
+
+
+def nf_net_destroy(net):
+    _lib.nf_net_destroy(net)
+
+
+def nf_set_stream(net, stream):
+    """stream: a torch.cuda.Stream, a raw cudaStream_t int, or None (legacy default)."""
+    h = getattr(stream, "cuda_stream", stream)
+    _check(_lib.nf_set_stream(net, ctypes.c_void_p(h or 0)))
+
+
+def nf_set_math(net, mode: int):
+    _check(_lib.nf_set_math(net, mode))
+
+
+def nf_param_count(net) -> int:
+    return int(_lib.nf_param_count(net))
+
+
+def nf_get_params(net, dst):
+    _check(_lib.nf_get_params(net, _ptr(dst), _numel(dst)))
+
+
+def nf_set_params(net, src):
+    _check(_lib.nf_set_params(net, _ptr(src), _numel(src)))
+
+
+def nf_output(net, x, n: int, out):
+    _check(_lib.nf_output(net, _ptr(x), n, _ptr(out)))
+
+
+def nf_train_batch(net, x, y, n: int, eta: float):
+    _check(_lib.nf_train_batch(net, _ptr(x), _ptr(y), n, eta))
+
+
+def nf_train_steps(net, X, Y, N: int, batch: int, starts, n_steps: int, eta: float, step_loss=None):
+    _check(_lib.nf_train_steps(net, _ptr(X), _ptr(Y), N, batch, _ptr(starts, np.int64), n_steps, eta,
+                               _ptr(step_loss)))
+
+
+def nf_grad(net, x, y, n: int, grad):
+    _check(_lib.nf_grad(net, _ptr(x), _ptr(y), n, _ptr(grad)))
+
+
+def nf_loss(net, x, y, n: int) -> float:
+    v = ctypes.c_float()
+    _check(_lib.nf_loss(net, _ptr(x), _ptr(y), n, ctypes.byref(v)))
+    return v.value
+
+
+def nf_accuracy(net, x, y, n: int) -> float:
+    v = ctypes.c_float()
+    _check(_lib.nf_accuracy(net, _ptr(x), _ptr(y), n, ctypes.byref(v)))
+    return v.value
+
+
+def nf_last_error() -> str:
+    return _lib.nf_last_error().decode()
+
+
+def nf_launch_count() -> int:
+    return int(_lib.nf_launch_count())
+
+
+def _numel(a) -> int:
+    return int(a.numel()) if hasattr(a, "numel") else int(a.size)
+
+
+# ---------------------------------------------------------------- object wrapper
+class Net:
+    """network_type(dims, activation) on the GPU."""
+
+    def __init__(self, dims, activation: str = "sigmoid", seed: int = 0, stream=None):
+        self.dims = [int(d) for d in dims]
+        self.activation = activation
+        self.h = nf_net_create(self.dims, activation, seed)
+        if stream is not None:
+            nf_set_stream(self.h, stream)
+
+    def close(self):
+        if getattr(self, "h", None):
+            nf_net_destroy(self.h)
+            self.h = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+    @property
+    def n_params(self) -> int:
+        return nf_param_count(self.h)
+
+    def set_stream(self, stream):
+        nf_set_stream(self.h, stream)
+
+    def set_math(self, mode: int):
+        nf_set_math(self.h, mode)
+
+    def get_params(self, out=None):
+        if out is None:
+            out = np.empty(self.n_params, np.float32)
+        nf_get_params(self.h, out)
+        return out
+
+    def set_params(self, p):
+        nf_set_params(self.h, p)
+
+    def output(self, x, out=None):
+        n = x.shape[0]
+        if out is None:
+            out = _empty_like_rows(x, n, self.dims[-1])
+        nf_output(self.h, x, n, out)
+        return out
+
+    def train_batch(self, x, y, eta: float):
+        nf_train_batch(self.h, x, y, x.shape[0], eta)
+
+    def train_steps(self, X, Y, batch: int, starts, eta: float, step_loss=None):
+        starts = np.ascontiguousarray(np.asarray(starts, dtype=np.int64))
+        nf_train_steps(self.h, X, Y, X.shape[0], batch, starts, len(starts), eta, step_loss)
+
+    def grad(self, x, y, out=None):
+        if out is None:
+            out = _empty_like_rows(x, self.n_params, None)
+        nf_grad(self.h, x, y, x.shape[0], out)
+        return out
+
+    def loss(self, x, y) -> float:
+        return nf_loss(self.h, x, y, x.shape[0])
+
+    def accuracy(self, x, y) -> float:
+        return nf_accuracy(self.h, x, y, x.shape[0])
+
+
+def _empty_like_rows(x, n, w):
+    shape = (n,) if w is None else (n, w)
+    if hasattr(x, "data_ptr"):
+        import torch
+        return torch.empty(shape, dtype=torch.float32, device=x.device)
+    return np.empty(shape, np.float32)

@@ -1,0 +1,507 @@
+// api.cu -- the C-ABI (include/nf.h) and the host runtime behind it: parameter
+// arena, activation/derivative stash, host<->device staging, and the launch
+// sequences of one SGD step.  Every arithmetic step of the method runs in this
+// library's CUDA kernels; there is no CPU fallback (NF_ENODEV without a GPU).
+#include <cmath>
+#include <cstdarg>
+#include <cstdio>
+#include <cstring>
+#include <string>
+#include <vector>
+
+#include "../../include/nf.h"
+#include "fused_small.cuh"
+#include "kernels.cuh"
+
+using namespace nf;
+
+namespace {
+
+thread_local std::string g_err;
+
+int fail(int code, const char *fmt, ...) {
+  char buf[512];
+  va_list ap;
+  va_start(ap, fmt);
+  vsnprintf(buf, sizeof buf, fmt, ap);
+  va_end(ap);
+  g_err = buf;
+  return code;
+}
+
+#define NF_CUDA(expr)                                                                  \
+  do {                                                                                 \
+    cudaError_t e_ = (expr);                                                           \
+    if (e_ != cudaSuccess)                                                             \
+      return fail(e_ == cudaErrorMemoryAllocation ? NF_ENOMEM : NF_ECUDA, "%s: %s (%s:%d)", \
+                  #expr, cudaGetErrorString(e_), __FILE__, __LINE__);                  \
+  } while (0)
+
+struct DevBuf {
+  void *p = nullptr;
+  size_t cap = 0;
+  cudaError_t ensure(size_t bytes) {
+    if (bytes <= cap) return cudaSuccess;
+    if (p) cudaFree(p);
+    p = nullptr;
+    cap = 0;
+    cudaError_t e = cudaMalloc(&p, bytes);
+    if (e == cudaSuccess) cap = bytes;
+    return e;
+  }
+  void release() {
+    if (p) cudaFree(p);
+    p = nullptr;
+    cap = 0;
+  }
+  template <class T> T *as() const { return static_cast<T *>(p); }
+};
+
+int parse_act(const std::string &s) {
+  static const char *names[] = {"sigmoid", "tanh", "relu", "gaussian", "step"};
+  for (int i = 0; i < 5; ++i)
+    if (s == names[i]) return i;
+  return -1;
+}
+
+bool is_device_ptr(const void *p) {
+  cudaPointerAttributes at;
+  if (cudaPointerGetAttributes(&at, p) != cudaSuccess) {
+    cudaGetLastError();
+    return false;
+  }
+  return at.type == cudaMemoryTypeDevice || at.type == cudaMemoryTypeManaged;
+}
+
+// splitmix64 + Box-Muller: the documented host stream of nf_net_create.
+struct HostRng {
+  uint64_t s;
+  uint64_t next() {
+    uint64_t z = (s += 0x9E3779B97F4A7C15ull);
+    z = (z ^ (z >> 30)) * 0xBF58476D1CE4E5B9ull;
+    z = (z ^ (z >> 27)) * 0x94D049BB133111EBull;
+    return z ^ (z >> 31);
+  }
+  double uniform() { return ((next() >> 11) + 0.5) * (1.0 / 9007199254740992.0); }
+  double normal() {
+    const double u1 = uniform(), u2 = uniform();
+    return std::sqrt(-2.0 * std::log(u1)) * std::cos(6.283185307179586 * u2);
+  }
+};
+
+}  // namespace
+
+struct nf_net {
+  std::vector<int> dims;
+  int L = 0;
+  int act_h = 0, act_o = 0;
+  int math = NF_MATH_FP32;
+  cudaStream_t stream = nullptr;
+  int64_t nparams = 0;
+  float *params = nullptr;               // device, flat layout of nf.h
+  std::vector<int64_t> offW, offB;       // index 1..L
+  // stash: A_l (activations) and S_l (sigma'(Z_l), overwritten by delta_l), l = 1..L
+  int64_t ws_rows = 0;
+  std::vector<float *> A, S;
+  DevBuf stash;
+  Workspace ws;
+  DevBuf partial;
+  DevBuf red;                            // loss/acc partials + results
+  DevBuf stage_x, stage_y, stage_o, stage_g;  // host-pointer staging
+  DevBuf d_starts;
+  FusedSmall fused;                      // persistent small-net kernel state
+
+  float *W(int l) const { return params + offW[l]; }
+  float *b(int l) const { return params + offB[l]; }
+  int act(int l) const { return l < L ? act_h : act_o; }
+};
+
+namespace {
+
+constexpr int64_t kEvalChunk = 32768;    // rows per forward chunk for eval calls
+
+int ensure_ws(nf_net *net, int64_t rows) {
+  if (rows <= net->ws_rows) return NF_OK;
+  int64_t per_row = 0;
+  for (int l = 1; l <= net->L; ++l) per_row += 2 * (int64_t)net->dims[l];
+  NF_CUDA(cudaStreamSynchronize(net->stream));
+  NF_CUDA(net->stash.ensure((size_t)(per_row * rows) * sizeof(float)));
+  float *p = net->stash.as<float>();
+  net->A.assign(net->L + 1, nullptr);
+  net->S.assign(net->L + 1, nullptr);
+  for (int l = 1; l <= net->L; ++l) {
+    net->A[l] = p; p += rows * net->dims[l];
+    net->S[l] = p; p += rows * net->dims[l];
+  }
+  net->ws_rows = rows;
+  return NF_OK;
+}
+
+// fwdprop over a batch.  mode: 0 train (stash A, S; output layer
+// S = delta_L), 2 inference (A only).  y only for mode 0.
+int forward(nf_net *net, const float *x, const float *y, int64_t n, int mode) {
+  const float *in = x;
+  for (int l = 1; l <= net->L; ++l) {
+    const int lm = (mode == 2) ? 2 : (l < net->L ? 0 : 1);
+    EpiFwd epi{net->b(l), net->A[l], net->S[l], y, net->dims[l], net->act(l), lm};
+    NF_CUDA(gemm_fwd(net->stream, (int)n, net->dims[l], net->dims[l - 1], in, net->W(l), epi, net->ws));
+    in = net->A[l];
+  }
+  return NF_OK;
+}
+
+// backprop + batch sum + update.  With
+// grad != nullptr the summed tendencies are stored there instead (nf_grad).
+// Order per layer: the delta of layer l-1 (reads W_l) BEFORE W_l is updated.
+int backward(nf_net *net, const float *x, int64_t n, float eta, float *grad) {
+  for (int l = net->L; l >= 1; --l) {
+    const int nl = net->dims[l], nk = net->dims[l - 1];
+    if (l > 1) {
+      EpiBwd eb{net->S[l - 1], nk};
+      NF_CUDA(gemm_bwd(net->stream, (int)n, nk, nl, net->S[l], net->W(l), eb, net->ws));
+    }
+    const float *aprev = l > 1 ? net->A[l - 1] : x;
+    EpiGrad eg = grad ? EpiGrad{grad + net->offW[l], grad + net->offB[l], nk, nk, 0.0f, 1}
+                      : EpiGrad{net->W(l), net->b(l), nk, nk, (float)((double)eta / (double)n), 0};
+    NF_CUDA(gemm_grad(net->stream, nl, nk, (int)n, net->S[l], aprev, eg, net->ws));
+  }
+  return NF_OK;
+}
+
+int train_batch_dev(nf_net *net, const float *x, const float *y, int64_t n, float eta,
+                    float *step_loss) {
+  int rc;
+  if ((rc = ensure_ws(net, n))) return rc;
+  if ((rc = forward(net, x, y, n, 0))) return rc;
+  if (step_loss) {
+    NF_CUDA(net->red.ensure(sizeof(double2) * loss_acc_parts() + 64));
+    NF_CUDA(loss_acc(net->stream, net->A[net->L], y, n, net->dims[net->L], net->red.as<double2>(),
+                     nullptr, step_loss));
+  }
+  return backward(net, x, n, eta, nullptr);
+}
+
+const float *stage_in(nf_net *net, const float *p, size_t count, DevBuf &buf, int *rc) {
+  *rc = NF_OK;
+  if (is_device_ptr(p)) return p;
+  cudaError_t e = buf.ensure(count * sizeof(float));
+  if (e == cudaSuccess) e = cudaMemcpyAsync(buf.p, p, count * sizeof(float), cudaMemcpyHostToDevice, net->stream);
+  if (e != cudaSuccess) {
+    *rc = fail(NF_ECUDA, "staging input: %s", cudaGetErrorString(e));
+    return nullptr;
+  }
+  return buf.as<float>();
+}
+
+int check_net(const nf_net *net) { return net ? NF_OK : fail(NF_EINVAL, "null net"); }
+
+int check_ptr(const void *p, const char *what) {
+  if (!p) return fail(NF_EINVAL, "%s is NULL", what);
+  if (reinterpret_cast<uintptr_t>(p) & 3) return fail(NF_EINVAL, "%s is not 4-byte aligned", what);
+  return NF_OK;
+}
+
+}  // namespace
+
+// ============================================================================ C-ABI
+extern "C" {
+
+const char *nf_last_error(void) { return g_err.c_str(); }
+
+int64_t nf_launch_count(void) { return __atomic_load_n(&g_launches, __ATOMIC_RELAXED); }
+
+int nf_net_create(const int32_t *dims, int32_t n_dims, const char *activation, uint64_t seed,
+                  nf_net **out) {
+  if (!out) return fail(NF_EINVAL, "out is NULL");
+  *out = nullptr;
+  if (!dims || n_dims < 2) return fail(NF_EINVAL, "need at least 2 dims (S:118-124)");
+  for (int i = 0; i < n_dims; ++i)
+    if (dims[i] < 1) return fail(NF_EINVAL, "dims[%d] = %d < 1", i, dims[i]);
+  std::string spec = activation ? activation : "sigmoid";
+  std::string h = spec, o = spec;
+  const size_t comma = spec.find(',');
+  if (comma != std::string::npos) { h = spec.substr(0, comma); o = spec.substr(comma + 1); }
+  const int ah = parse_act(h), ao = parse_act(o);
+  if (ah < 0 || ao < 0) return fail(NF_EINVAL, "unknown activation '%s' (S:32-33)", spec.c_str());
+
+  int ndev = 0;
+  if (cudaGetDeviceCount(&ndev) != cudaSuccess || ndev == 0) {
+    cudaGetLastError();
+    return fail(NF_ENODEV, "no CUDA device: this library has no CPU fallback");
+  }
+  int dev = 0, major = 0;
+  cudaGetDevice(&dev);
+  cudaDeviceGetAttribute(&major, cudaDevAttrComputeCapabilityMajor, dev);
+  if (major != 10) return fail(NF_ENODEV, "device %d is sm_%d0, this build targets sm_100a", dev, major);
+
+  nf_net *net = new nf_net();
+  net->dims.assign(dims, dims + n_dims);
+  net->L = n_dims - 1;
+  net->act_h = ah;
+  net->act_o = ao;
+  net->offW.assign(net->L + 1, 0);
+  net->offB.assign(net->L + 1, 0);
+  int64_t o_ = 0;
+  for (int l = 1; l <= net->L; ++l) {
+    net->offW[l] = o_; o_ += (int64_t)dims[l] * dims[l - 1];
+    net->offB[l] = o_; o_ += dims[l];
+  }
+  net->nparams = o_;
+  std::vector<float> host(o_);
+  HostRng rng{seed};
+  for (int l = 1; l <= net->L; ++l) {
+    for (int64_t i = 0; i < (int64_t)dims[l] * dims[l - 1]; ++i)
+      host[net->offW[l] + i] = (float)(rng.normal() / dims[l - 1]);
+    for (int i = 0; i < dims[l]; ++i) host[net->offB[l] + i] = (float)rng.normal();
+  }
+  cudaError_t e = cudaMalloc(&net->params, o_ * sizeof(float));
+  if (e == cudaSuccess) e = cudaMemcpy(net->params, host.data(), o_ * sizeof(float), cudaMemcpyHostToDevice);
+  if (e == cudaSuccess) e = net->partial.ensure(size_t(16) << 20 << 2);  // 16M floats
+  if (e != cudaSuccess) {
+    nf_net_destroy(net);
+    return fail(NF_ECUDA, "nf_net_create: %s", cudaGetErrorString(e));
+  }
+  net->ws.partial = net->partial.as<float>();
+  net->ws.partial_floats = size_t(16) << 20;
+  *out = net;
+  return NF_OK;
+}
+
+void nf_net_destroy(nf_net *net) {
+  if (!net) return;
+  cudaStreamSynchronize(net->stream);
+  if (net->params) cudaFree(net->params);
+  net->stash.release();
+  net->partial.release();
+  net->red.release();
+  net->stage_x.release();
+  net->stage_y.release();
+  net->stage_o.release();
+  net->stage_g.release();
+  net->d_starts.release();
+  fused_small_release(net->fused);
+  delete net;
+}
+
+int nf_set_stream(nf_net *net, void *s) {
+  if (int rc = check_net(net)) return rc;
+  net->stream = static_cast<cudaStream_t>(s);
+  return NF_OK;
+}
+
+int nf_set_math(nf_net *net, int mode) {
+  if (int rc = check_net(net)) return rc;
+  if (mode != NF_MATH_FP32 && mode != NF_MATH_TF32) return fail(NF_EINVAL, "unknown math mode %d", mode);
+  net->math = mode;
+  return NF_OK;
+}
+
+int64_t nf_param_count(const nf_net *net) { return net ? net->nparams : -1; }
+
+int nf_get_params(nf_net *net, float *dst, int64_t count) {
+  if (int rc = check_net(net)) return rc;
+  if (int rc = check_ptr(dst, "dst")) return rc;
+  if (count != net->nparams) return fail(NF_EINVAL, "count %lld != %lld", (long long)count, (long long)net->nparams);
+  const bool dev = is_device_ptr(dst);
+  NF_CUDA(cudaMemcpyAsync(dst, net->params, count * sizeof(float),
+                          dev ? cudaMemcpyDeviceToDevice : cudaMemcpyDeviceToHost, net->stream));
+  if (!dev) NF_CUDA(cudaStreamSynchronize(net->stream));
+  return NF_OK;
+}
+
+int nf_set_params(nf_net *net, const float *src, int64_t count) {
+  if (int rc = check_net(net)) return rc;
+  if (int rc = check_ptr(src, "src")) return rc;
+  if (count != net->nparams) return fail(NF_EINVAL, "count %lld != %lld", (long long)count, (long long)net->nparams);
+  const bool dev = is_device_ptr(src);
+  NF_CUDA(cudaMemcpyAsync(net->params, src, count * sizeof(float),
+                          dev ? cudaMemcpyDeviceToDevice : cudaMemcpyHostToDevice, net->stream));
+  if (!dev) NF_CUDA(cudaStreamSynchronize(net->stream));
+  fused_small_invalidate(net->fused);
+  return NF_OK;
+}
+
+int nf_output(nf_net *net, const float *x, int64_t n, float *out) {
+  if (int rc = check_net(net)) return rc;
+  if (n < 0) return fail(NF_EINVAL, "n < 0");
+  if (n == 0) return NF_OK;
+  if (int rc = check_ptr(x, "x")) return rc;
+  if (int rc = check_ptr(out, "out")) return rc;
+  const int n0 = net->dims[0], nL = net->dims[net->L];
+  int rc;
+  const float *dx = stage_in(net, x, (size_t)n * n0, net->stage_x, &rc);
+  if (rc) return rc;
+  const bool host_out = !is_device_ptr(out);
+  float *dout = out;
+  if (host_out) {
+    NF_CUDA(net->stage_o.ensure((size_t)n * nL * sizeof(float)));
+    dout = net->stage_o.as<float>();
+  }
+  const int64_t chunk = std::min<int64_t>(n, kEvalChunk);
+  if ((rc = ensure_ws(net, chunk))) return rc;
+  for (int64_t r = 0; r < n; r += chunk) {
+    const int64_t m = std::min(chunk, n - r);
+    if ((rc = forward(net, dx + r * n0, nullptr, m, 2))) return rc;
+    NF_CUDA(cudaMemcpyAsync(dout + r * nL, net->A[net->L], (size_t)m * nL * sizeof(float),
+                            cudaMemcpyDeviceToDevice, net->stream));
+  }
+  if (host_out) {
+    NF_CUDA(cudaMemcpyAsync(out, dout, (size_t)n * nL * sizeof(float), cudaMemcpyDeviceToHost, net->stream));
+    NF_CUDA(cudaStreamSynchronize(net->stream));
+  }
+  return NF_OK;
+}
+
+int nf_train_batch(nf_net *net, const float *x, const float *y, int64_t n, float eta) {
+  if (int rc = check_net(net)) return rc;
+  if (n <= 0) return fail(NF_EINVAL, "train needs n >= 1 (S:181)");
+  if (!std::isfinite(eta)) return fail(NF_EINVAL, "eta is not finite");
+  if (int rc = check_ptr(x, "x")) return rc;
+  if (int rc = check_ptr(y, "y")) return rc;
+  int rc;
+  const float *dx = stage_in(net, x, (size_t)n * net->dims[0], net->stage_x, &rc);
+  if (rc) return rc;
+  const float *dy = stage_in(net, y, (size_t)n * net->dims[net->L], net->stage_y, &rc);
+  if (rc) return rc;
+  fused_small_invalidate(net->fused);
+  rc = train_batch_dev(net, dx, dy, n, eta, nullptr);
+  if (rc == NF_OK && (dx != x || dy != y)) NF_CUDA(cudaStreamSynchronize(net->stream));
+  return rc;
+}
+
+int nf_train_steps(nf_net *net, const float *X, const float *Y, int64_t N, int64_t batch,
+                   const int64_t *starts, int64_t n_steps, float eta, float *step_loss) {
+  if (int rc = check_net(net)) return rc;
+  if (batch <= 0 || N < batch) return fail(NF_EINVAL, "need 1 <= batch <= N");
+  if (n_steps < 0) return fail(NF_EINVAL, "n_steps < 0");
+  if (n_steps == 0) return NF_OK;
+  if (!std::isfinite(eta)) return fail(NF_EINVAL, "eta is not finite");
+  if (int rc = check_ptr(X, "X")) return rc;
+  if (int rc = check_ptr(Y, "Y")) return rc;
+  if (!starts) return fail(NF_EINVAL, "starts is NULL");
+  if (is_device_ptr(starts)) return fail(NF_EINVAL, "starts must be a host array");
+  for (int64_t s = 0; s < n_steps; ++s)
+    if (starts[s] < 0 || starts[s] + batch > N)
+      return fail(NF_EINVAL, "starts[%lld] = %lld outside [0, N-batch]", (long long)s, (long long)starts[s]);
+  if (step_loss && !is_device_ptr(step_loss)) return fail(NF_EINVAL, "step_loss must be a device array");
+  const int n0 = net->dims[0], nL = net->dims[net->L];
+
+  // Host dataset: gather each step's batch into device staging (one H2D copy
+  // per step, the e2e path) and renumber the starts.
+  const bool host_in = !is_device_ptr(X) || !is_device_ptr(Y);
+  std::vector<int64_t> st(starts, starts + n_steps);
+  const float *dX = X, *dY = Y;
+  int64_t dN = N;
+  if (host_in) {
+    NF_CUDA(net->stage_x.ensure((size_t)n_steps * batch * n0 * sizeof(float)));
+    NF_CUDA(net->stage_y.ensure((size_t)n_steps * batch * nL * sizeof(float)));
+    for (int64_t s = 0; s < n_steps; ++s) {
+      NF_CUDA(cudaMemcpyAsync(net->stage_x.as<float>() + s * batch * n0, X + starts[s] * n0,
+                              (size_t)batch * n0 * sizeof(float), cudaMemcpyHostToDevice, net->stream));
+      NF_CUDA(cudaMemcpyAsync(net->stage_y.as<float>() + s * batch * nL, Y + starts[s] * nL,
+                              (size_t)batch * nL * sizeof(float), cudaMemcpyHostToDevice, net->stream));
+      st[s] = s * batch;
+    }
+    dX = net->stage_x.as<float>();
+    dY = net->stage_y.as<float>();
+    dN = n_steps * batch;
+  }
+
+  int rc = fused_small_train_steps(net->fused, net->stream, net->dims, net->act_h, net->act_o,
+                                   net->params, dX, dY, dN, batch, st.data(), n_steps, eta, step_loss);
+  if (rc == FUSED_NOT_APPLICABLE) {
+    for (int64_t s = 0; s < n_steps; ++s) {
+      rc = train_batch_dev(net, dX + st[s] * n0, dY + st[s] * nL, batch, eta,
+                           step_loss ? step_loss + s : nullptr);
+      if (rc) return rc;
+    }
+  } else if (rc != 0) {
+    return fail(NF_ECUDA, "fused small-net kernel: %s", fused_small_error());
+  }
+  if (host_in) NF_CUDA(cudaStreamSynchronize(net->stream));
+  return NF_OK;
+}
+
+int nf_grad(nf_net *net, const float *x, const float *y, int64_t n, float *grad) {
+  if (int rc = check_net(net)) return rc;
+  if (n <= 0) return fail(NF_EINVAL, "n must be >= 1");
+  if (int rc = check_ptr(x, "x")) return rc;
+  if (int rc = check_ptr(y, "y")) return rc;
+  if (int rc = check_ptr(grad, "grad")) return rc;
+  int rc;
+  const float *dx = stage_in(net, x, (size_t)n * net->dims[0], net->stage_x, &rc);
+  if (rc) return rc;
+  const float *dy = stage_in(net, y, (size_t)n * net->dims[net->L], net->stage_y, &rc);
+  if (rc) return rc;
+  const bool host_out = !is_device_ptr(grad);
+  float *dg = grad;
+  if (host_out) {
+    NF_CUDA(net->stage_g.ensure((size_t)net->nparams * sizeof(float)));
+    dg = net->stage_g.as<float>();
+  }
+  if ((rc = ensure_ws(net, n))) return rc;
+  if ((rc = forward(net, dx, dy, n, 0))) return rc;
+  if ((rc = backward(net, dx, n, 0.0f, dg))) return rc;
+  if (host_out) {
+    NF_CUDA(cudaMemcpyAsync(grad, dg, (size_t)net->nparams * sizeof(float), cudaMemcpyDeviceToHost, net->stream));
+    NF_CUDA(cudaStreamSynchronize(net->stream));
+  }
+  return NF_OK;
+}
+
+static int eval_loss_acc(nf_net *net, const float *x, const float *y, int64_t n, float *res2) {
+  res2[0] = res2[1] = 0.0f;
+  if (n == 0) return NF_OK;
+  if (int rc = check_ptr(x, "x")) return rc;
+  if (int rc = check_ptr(y, "y")) return rc;
+  const int n0 = net->dims[0], nL = net->dims[net->L];
+  int rc;
+  const float *dx = stage_in(net, x, (size_t)n * n0, net->stage_x, &rc);
+  if (rc) return rc;
+  const float *dy = stage_in(net, y, (size_t)n * nL, net->stage_y, &rc);
+  if (rc) return rc;
+  const int64_t chunk = std::min<int64_t>(n, kEvalChunk);
+  if ((rc = ensure_ws(net, chunk))) return rc;
+  const int64_t nchunks = (n + chunk - 1) / chunk;
+  NF_CUDA(net->red.ensure(sizeof(double2) * loss_acc_parts() + 64 + nchunks * 2 * sizeof(float)));
+  float *res = reinterpret_cast<float *>(net->red.as<char>() + sizeof(double2) * loss_acc_parts() + 64);
+  for (int64_t c = 0; c < nchunks; ++c) {
+    const int64_t r = c * chunk, m = std::min(chunk, n - r);
+    if ((rc = forward(net, dx + r * n0, nullptr, m, 2))) return rc;
+    NF_CUDA(loss_acc(net->stream, net->A[net->L], dy + r * nL, m, nL, net->red.as<double2>(), res + 2 * c, nullptr));
+  }
+  std::vector<float> h(2 * nchunks);
+  NF_CUDA(cudaMemcpyAsync(h.data(), res, h.size() * sizeof(float), cudaMemcpyDeviceToHost, net->stream));
+  NF_CUDA(cudaStreamSynchronize(net->stream));
+  double l = 0, a = 0;
+  for (int64_t c = 0; c < nchunks; ++c) {
+    const int64_t m = std::min(chunk, n - c * chunk);
+    l += (double)h[2 * c] * m;
+    a += (double)h[2 * c + 1] * m;
+  }
+  res2[0] = (float)(l / n);
+  res2[1] = (float)(a / n);
+  return NF_OK;
+}
+
+int nf_loss(nf_net *net, const float *x, const float *y, int64_t n, float *loss) {
+  if (int rc = check_net(net)) return rc;
+  if (!loss) return fail(NF_EINVAL, "loss is NULL");
+  if (n < 0) return fail(NF_EINVAL, "n < 0");
+  float r[2];
+  if (int rc = eval_loss_acc(net, x, y, n, r)) return rc;
+  *loss = r[0];
+  return NF_OK;
+}
+
+int nf_accuracy(nf_net *net, const float *x, const float *y, int64_t n, float *acc) {
+  if (int rc = check_net(net)) return rc;
+  if (!acc) return fail(NF_EINVAL, "acc is NULL");
+  if (n < 0) return fail(NF_EINVAL, "n < 0");
+  float r[2];
+  if (int rc = eval_loss_acc(net, x, y, n, r)) return rc;
+  *acc = r[1];
+  return NF_OK;
+}
+
+}  // extern "C"

@@ -1,0 +1,184 @@
+// gemm_simt.cuh -- fp32 FFMA tiled contraction with fused epilogues: the
+// generic-width path of the three GEMM-shaped steps of the method
+// (SURVEY 8(a) rows a1, a3, a4):
+//   K1 forward     Z_l = A_{l-1} W_l^T (+b_l, sigma, stash)      A K-major, B K-major
+//   K3 backward    D_l = (D_{l+1} W_{l+1}) .* sigma'(Z_l)        A K-major, B N-major
+//   K4 gradient    G_l = D_l^T [A_{l-1} | 1]  (+ SGD epilogue)    A M-major, B N-major
+// The bias gradient g_l = 1^T D_l rides along as an extra ones column of the
+// B operand (n == nb_real), so one kernel yields dW and db (the paper's
+// dw/db tendencies, summed over the batch = the co_sum).
+//
+// Tiles are staged through double-buffered shared memory (register prefetch
+// of tile t+1 while tile t is consumed), each thread owns a TMxTN register
+// micro-tile.  Optional split-K over gridDim.z writes partials that a second
+// kernel sums in a fixed order (deterministic) before the same epilogue.
+#pragma once
+#include "nf_common.cuh"
+
+namespace nf {
+
+struct GemmArgs {
+  int M, N, K;
+  const float *A; int64_t lda;
+  const float *B; int64_t ldb;
+  int nb_real;        // B(k, n) = 1 for nb_real <= n < N (ones column for db)
+  int kchunk;         // K range per blockIdx.z
+  float *partial;     // non-null: write raw partials [z][M][N] instead of the epilogue
+};
+
+// ---- epilogues ------------------------------------------------------------
+// Forward: mode 0 hidden (A = sigma(z), S = sigma'(z)); mode 1 output layer in
+// training (A = sigma(z), S = (sigma(z) - y) sigma'(z) = delta_L, S:150 /
+// quadratic cost P:111); mode 2 inference (A = sigma(z) only).
+struct EpiFwd {
+  const float *bias; float *A; float *S; const float *Y; int ld; int act; int mode;
+  __device__ __forceinline__ void operator()(int m, int n, float acc) const {
+    const float z = acc + bias[n];
+    const int64_t i = (int64_t)m * ld + n;
+    if (mode == 2) { A[i] = act_only(act, z); return; }
+    float a, s;
+    act_fwd(act, z, a, s);
+    A[i] = a;
+    S[i] = mode == 0 ? s : (a - Y[i]) * s;
+  }
+};
+
+// Backward: SD holds sigma'(Z_l) on entry and delta_l on exit.
+struct EpiBwd {
+  float *SD; int ld;
+  __device__ __forceinline__ void operator()(int m, int n, float acc) const {
+    const int64_t i = (int64_t)m * ld + n;
+    SD[i] = acc * SD[i];
+  }
+};
+
+// Gradient: store = 0 applies W -= scale*G, b -= scale*g (scale =
+// eta/B, reading R3); store = 1 writes G, g (nf_grad).
+struct EpiGrad {
+  float *W; float *b; int ldw; int nreal; float scale; int store;
+  __device__ __forceinline__ void operator()(int m, int n, float acc) const {
+    float *p = n < nreal ? W + (int64_t)m * ldw + n : b + m;
+    if (store) *p = acc;
+    else *p = *p - scale * acc;
+  }
+};
+
+// ---- the kernel -------------------------------------------------------------
+template <int BM, int BN, int BK, int TM, int TN, bool AK, bool BKM, class Epi>
+__global__ void __launch_bounds__((BM / TM) * (BN / TN))
+gemm_simt(GemmArgs g, Epi epi) {
+  constexpr int NT = (BM / TM) * (BN / TN);
+  constexpr int APT = BM * BK / NT;
+  constexpr int BPT = BN * BK / NT;
+  static_assert(APT * NT == BM * BK && BPT * NT == BN * BK, "tile/thread mismatch");
+  __shared__ __align__(16) float As[2][BK][BM + 4];
+  __shared__ __align__(16) float Bs[2][BK][BN + 4];
+
+  const int tid = threadIdx.x;
+  const int tx = tid % (BN / TN), ty = tid / (BN / TN);
+  const int m0 = blockIdx.y * BM, n0 = blockIdx.x * BN;
+  const int kbeg = blockIdx.z * g.kchunk;
+  const int kend = min(g.K, kbeg + g.kchunk);
+  const int nkt = (kend - kbeg + BK - 1) / BK;
+
+  float ra[APT], rb[BPT];
+  auto load = [&](int k0) {
+#pragma unroll
+    for (int i = 0; i < APT; ++i) {
+      const int idx = tid + i * NT;
+      const int mm = AK ? idx / BK : idx % BM;
+      const int kk = AK ? idx % BK : idx / BM;
+      const int m = m0 + mm, k = k0 + kk;
+      ra[i] = (m < g.M && k < kend) ? __ldg(AK ? g.A + (int64_t)m * g.lda + k
+                                               : g.A + (int64_t)k * g.lda + m) : 0.0f;
+    }
+#pragma unroll
+    for (int i = 0; i < BPT; ++i) {
+      const int idx = tid + i * NT;
+      const int nn = BKM ? idx / BK : idx % BN;
+      const int kk = BKM ? idx % BK : idx / BN;
+      const int n = n0 + nn, k = k0 + kk;
+      float v = 0.0f;
+      if (k < kend && n < g.N)
+        v = n < g.nb_real ? __ldg(BKM ? g.B + (int64_t)n * g.ldb + k : g.B + (int64_t)k * g.ldb + n)
+                          : 1.0f;
+      rb[i] = v;
+    }
+  };
+  auto store = [&](int buf) {
+#pragma unroll
+    for (int i = 0; i < APT; ++i) {
+      const int idx = tid + i * NT;
+      const int mm = AK ? idx / BK : idx % BM;
+      const int kk = AK ? idx % BK : idx / BM;
+      As[buf][kk][mm] = ra[i];
+    }
+#pragma unroll
+    for (int i = 0; i < BPT; ++i) {
+      const int idx = tid + i * NT;
+      const int nn = BKM ? idx / BK : idx % BN;
+      const int kk = BKM ? idx % BK : idx / BN;
+      Bs[buf][kk][nn] = rb[i];
+    }
+  };
+
+  float acc[TM][TN];
+#pragma unroll
+  for (int i = 0; i < TM; ++i)
+#pragma unroll
+    for (int j = 0; j < TN; ++j) acc[i][j] = 0.0f;
+
+  if (nkt > 0) {
+    load(kbeg);
+    store(0);
+  }
+  __syncthreads();
+  for (int t = 0; t < nkt; ++t) {
+    const int buf = t & 1;
+    if (t + 1 < nkt) load(kbeg + (t + 1) * BK);
+#pragma unroll
+    for (int kk = 0; kk < BK; ++kk) {
+      float a[TM], b[TN];
+#pragma unroll
+      for (int i = 0; i < TM; ++i) a[i] = As[buf][kk][ty * TM + i];
+#pragma unroll
+      for (int j = 0; j < TN; ++j) b[j] = Bs[buf][kk][tx * TN + j];
+#pragma unroll
+      for (int i = 0; i < TM; ++i)
+#pragma unroll
+        for (int j = 0; j < TN; ++j) acc[i][j] = fmaf(a[i], b[j], acc[i][j]);
+    }
+    if (t + 1 < nkt) store(buf ^ 1);
+    __syncthreads();
+  }
+
+#pragma unroll
+  for (int i = 0; i < TM; ++i) {
+    const int m = m0 + ty * TM + i;
+    if (m >= g.M) continue;
+#pragma unroll
+    for (int j = 0; j < TN; ++j) {
+      const int n = n0 + tx * TN + j;
+      if (n >= g.N) continue;
+      if (g.partial)
+        g.partial[((int64_t)blockIdx.z * g.M + m) * g.N + n] = acc[i][j];
+      else
+        epi(m, n, acc[i][j]);
+    }
+  }
+}
+
+// Sum split-K partials in z order (deterministic) and apply the epilogue.
+template <class Epi>
+__global__ void __launch_bounds__(256)
+splitk_epilogue(const float *__restrict__ partial, int splits, int M, int N, Epi epi) {
+  const int64_t MN = (int64_t)M * N;
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < MN;
+       i += (int64_t)gridDim.x * blockDim.x) {
+    float s = 0.0f;
+    for (int z = 0; z < splits; ++z) s += partial[z * MN + i];
+    epi((int)(i / N), (int)(i % N), s);
+  }
+}
+
+}  // namespace nf

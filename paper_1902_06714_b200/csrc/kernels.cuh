@@ -1,0 +1,38 @@
+// kernels.cuh -- host-side launchers of the hot-path kernels (internal, C++).
+#pragma once
+#include <cstddef>
+#include <cstdint>
+#include <cuda_runtime.h>
+
+#include "gemm_simt.cuh"
+
+namespace nf {
+
+extern int64_t g_launches;  // kernels launched by this library (nf_launch_count)
+inline void count_launch(int n = 1) { __atomic_add_fetch(&g_launches, n, __ATOMIC_RELAXED); }
+
+// Split-K partial workspace owned by the net (fixed capacity in floats).
+struct Workspace {
+  float *partial = nullptr;
+  size_t partial_floats = 0;
+};
+
+// K1: Z = A[M][K] * W[N][K]^T, epilogue EpiFwd.
+cudaError_t gemm_fwd(cudaStream_t st, int M, int N, int K, const float *A, const float *W,
+                     const EpiFwd &epi, const Workspace &ws);
+// K3: C[M][N] = D[M][K] * W[K][N], epilogue EpiBwd.
+cudaError_t gemm_bwd(cudaStream_t st, int M, int N, int K, const float *D, const float *W,
+                     const EpiBwd &epi, const Workspace &ws);
+// K4: C[M][N+1] = D^T (D is [K][M]) * [Aprev | 1] (Aprev is [K][N]), epilogue EpiGrad.
+cudaError_t gemm_grad(cudaStream_t st, int M, int N, int K, const float *D, const float *Aprev,
+                      const EpiGrad &epi, const Workspace &ws);
+
+// K5: mean quadratic cost and argmax-accuracy of A_L against Y over n rows of
+// width w.  part: scratch of >= loss_acc_parts() double2.  Results: out[0] =
+// mean loss, out[1] = accuracy (device floats); step_loss (nullable) gets the
+// mean loss too.
+int loss_acc_parts();
+cudaError_t loss_acc(cudaStream_t st, const float *A, const float *Y, int64_t n, int w,
+                     double2 *part, float *out, float *step_loss);
+
+}  // namespace nf

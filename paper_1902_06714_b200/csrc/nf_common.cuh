@@ -1,0 +1,68 @@
+// nf_common.cuh -- device helpers shared by the CUDA kernels of the hot path.
+// Activation pairs (sigma, sigma') of P:108-109 / S:40, evaluated from
+// z in numerically stable fp32 forms (reading R6 in DESIGN.md): sigma' is
+// computed from z inside the forward epilogue and stashed, so no cancellation
+// of the a(1-a) / 1-a^2 kind ever happens.
+#pragma once
+#include <cstdint>
+#include <cuda_runtime.h>
+
+namespace nf {
+
+enum Act : int { ACT_SIGMOID = 0, ACT_TANH = 1, ACT_RELU = 2, ACT_GAUSSIAN = 3, ACT_STEP = 4 };
+
+// a = sigma(z), s = sigma'(z).  Accurate libdevice expf/tanhf (no fast-math).
+__device__ __forceinline__ void act_fwd(int kind, float z, float &a, float &s) {
+  switch (kind) {
+    case ACT_SIGMOID: {            // t = e^{-|z|}:  sigma = 1/(1+t) or t/(1+t);  sigma' = t/(1+t)^2
+      const float t = expf(-fabsf(z));
+      const float r = 1.0f / (1.0f + t);
+      a = z >= 0.0f ? r : t * r;
+      s = t * r * r;
+      break;
+    }
+    case ACT_TANH: {               // sigma' = sech^2 z = 4t/(1+t)^2, t = e^{-2|z|}
+      a = tanhf(z);
+      const float t = expf(-2.0f * fabsf(z));
+      const float r = 1.0f / (1.0f + t);
+      s = 4.0f * t * r * r;
+      break;
+    }
+    case ACT_RELU:                 // relu'(0) = 0 (reading R8)
+      a = z > 0.0f ? z : 0.0f;
+      s = z > 0.0f ? 1.0f : 0.0f;
+      break;
+    case ACT_GAUSSIAN: {           // e^{-z^2}, -2z e^{-z^2}
+      const float e = expf(-z * z);
+      a = e;
+      s = -2.0f * z * e;
+      break;
+    }
+    default:                       // step: [z>0], derivative 0
+      a = z > 0.0f ? 1.0f : 0.0f;
+      s = 0.0f;
+      break;
+  }
+}
+
+__device__ __forceinline__ float act_only(int kind, float z) {
+  switch (kind) {
+    case ACT_SIGMOID: {
+      const float t = expf(-fabsf(z));
+      const float r = 1.0f / (1.0f + t);
+      return z >= 0.0f ? r : t * r;
+    }
+    case ACT_TANH: return tanhf(z);
+    case ACT_RELU: return z > 0.0f ? z : 0.0f;
+    case ACT_GAUSSIAN: return expf(-z * z);
+    default: return z > 0.0f ? 1.0f : 0.0f;
+  }
+}
+
+__device__ __forceinline__ float warp_sum(float v) {
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+  return v;
+}
+
+}  // namespace nf

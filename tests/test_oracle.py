@@ -317,7 +317,7 @@ def test_accuracy_pins():
     k = 5
     o = O64([k, k], "relu")
     p = np.concatenate([np.eye(k).ravel(), np.zeros(k)])
-    lab = np.array([0, 3, 4, 1, 1, 2])
+    lab = np.array([0, 3, 4, 1, 1, 2, 0])
     Y = synth.one_hot(lab, k)
     assert o.accuracy(p, Y, Y) == 1.0
     # predicting class (label+1) mod k everywhere -> 0.0

@@ -1,0 +1,282 @@
+"""GPU parity of the CUDA path (through the C-ABI) against the fp64 CPU oracle (-m gpu).
+
+Every input comes from synth/ (seeded); every expected value from oracle/.  Bars and the
+metric are in tests/parity.py (R14/R15).  Shapes span several tiles with ragged tails;
+the full-size configs are checked in the launch configuration bench.py times, on
+samples the oracle can compute (teacher-forced steps, sampled rows).
+"""
+import numpy as np
+import pytest
+import torch
+
+import oracle
+import synth
+from parity import FP32_BAR, argmax_agree, rel_err
+
+pytestmark = pytest.mark.gpu
+
+import paper_1902_06714_b200 as nf  # noqa: E402
+
+
+def dev(a):
+    return torch.from_numpy(np.ascontiguousarray(a)).cuda()
+
+
+def make_net(dims, act, params):
+    net = nf.Net(dims, act)
+    net.set_params(dev(params.astype(np.float32)))
+    return net
+
+
+def gpu_params(net):
+    out = torch.empty(net.n_params, dtype=torch.float32, device="cuda")
+    net.get_params(out)
+    torch.cuda.synchronize()
+    return out.cpu().numpy()
+
+
+SHAPES = [
+    ([3, 5, 2], "sigmoid", 8),
+    ([37, 45, 13], "tanh", 77),
+    ([784, 30, 10], "sigmoid", 1000),
+    ([64, 33, 129, 7], "relu,sigmoid", 130),
+    ([20, 200, 150, 5], "gaussian", 67),
+    ([300, 260, 1], "tanh,relu", 300),
+    ([1, 1], "sigmoid", 1),
+    ([5, 1, 3], "step,sigmoid", 9),
+]
+
+
+@pytest.mark.parametrize("dims,act,n", SHAPES)
+def test_output_parity(dims, act, n):
+    p = synth.random_params(len(dims) * 7 + n, dims, 0.5)
+    x, _ = synth.random_batch(n, n, dims[0], dims[-1], "normal")
+    net = make_net(dims, act, p)
+    out = net.output(dev(x)).cpu().numpy()
+    ref = oracle.Oracle(dims, act).output(p, x)
+    assert rel_err(out, ref) <= FP32_BAR
+    mism, _ = argmax_agree(out, ref)
+    assert mism == 0
+
+
+@pytest.mark.parametrize("dims,act,n", SHAPES)
+def test_grad_parity(dims, act, n):
+    p = synth.random_params(len(dims) * 11 + n, dims, 0.5)
+    x, y = synth.random_batch(n + 1, n, dims[0], dims[-1], "uniform")
+    net = make_net(dims, act, p)
+    g = net.grad(dev(x), dev(y)).cpu().numpy()
+    ref = oracle.Oracle(dims, act).grad(p, x, y)
+    o = oracle.Oracle(dims, act)
+    for (Wg, bg), (Wr, br) in zip(o.layers(g), o.layers(ref)):
+        assert rel_err(Wg, Wr) <= FP32_BAR
+        assert rel_err(bg, br) <= FP32_BAR
+
+
+@pytest.mark.parametrize("dims,act,n", SHAPES)
+def test_train_batch_parity(dims, act, n):
+    p = synth.random_params(len(dims) * 13 + n, dims, 0.5)
+    x, y = synth.random_batch(n + 2, n, dims[0], dims[-1], "uniform")
+    net = make_net(dims, act, p)
+    net.train_batch(dev(x), dev(y), 0.7)
+    got = gpu_params(net)
+    ref, _ = oracle.Oracle(dims, act).train_batch(p, x, y, 0.7)
+    o = oracle.Oracle(dims, act)
+    # compare the update itself (params move little; the update is what the step computes)
+    for (Wg, bg), (Wr, br), (W0, b0) in zip(o.layers(got), o.layers(ref), o.layers(p.astype(np.float64))):
+        assert rel_err(Wg, Wr) <= FP32_BAR
+        assert rel_err(Wg - W0, Wr - W0) <= 1e-3   # fp32 cancellation of W - W0 bounds this
+        assert rel_err(bg, br) <= FP32_BAR
+
+
+def test_eta_zero_is_bitwise_noop():
+    dims = [784, 30, 10]
+    p = synth.init_params(2)
+    X, Y = synth.dataset(2, N=2000)
+    net = make_net(dims, "sigmoid", p)
+    net.train_batch(dev(X[:1000]), dev(Y[:1000]), 0.0)
+    assert np.array_equal(gpu_params(net), p)
+    net.train_steps(dev(X), dev(Y), 1000, [0, 500, 1000], 0.0)   # fused path
+    assert np.array_equal(gpu_params(net), p)
+
+
+def test_split_batch_co_sum_on_gpu():
+    """tendencies of a batch == sum over any split (the co_sum property)."""
+    dims = [784, 30, 10]
+    p = synth.init_params(2)
+    X, Y = synth.dataset(2, N=1000)
+    net = make_net(dims, "sigmoid", p)
+    g = net.grad(dev(X), dev(Y)).cpu().numpy().astype(np.float64)
+    g1 = net.grad(dev(X[:377]), dev(Y[:377])).cpu().numpy().astype(np.float64)
+    g2 = net.grad(dev(X[377:]), dev(Y[377:])).cpu().numpy().astype(np.float64)
+    assert rel_err(g1 + g2, g) <= FP32_BAR
+
+
+def test_loss_accuracy_parity():
+    dims = [784, 30, 10]
+    p = synth.init_params(2)
+    X, Y = synth.dataset(2, N=10000)
+    net = make_net(dims, "sigmoid", p)
+    o = oracle.Oracle(dims, "sigmoid")
+    assert abs(net.loss(dev(X), dev(Y)) - o.loss(p, X, Y)) <= FP32_BAR * o.loss(p, X, Y)
+    out = net.output(dev(X)).cpu().numpy()
+    ref = o.output(p, X)
+    mism, ties = argmax_agree(out, ref)
+    assert mism == 0
+    acc_ref = o.accuracy(p, X, Y)
+    assert abs(net.accuracy(dev(X), dev(Y)) - acc_ref) <= ties / len(X) + 1e-7
+    assert 0.05 < acc_ref < 0.15          # untrained net = chance
+
+
+def test_degenerate_inputs():
+    net = make_net([4, 3, 2], "sigmoid", synth.random_params(1, [4, 3, 2]))
+    assert net.accuracy(dev(np.zeros((0, 4), np.float32)), dev(np.zeros((0, 2), np.float32))) == 0.0
+    out = torch.empty((0, 2), device="cuda")
+    nf.nf_output(net.h, dev(np.zeros((1, 4), np.float32)), 0, out)
+    with pytest.raises(nf.NFError):
+        nf.nf_train_batch(net.h, dev(np.zeros((1, 4), np.float32)), dev(np.zeros((1, 2), np.float32)), 0, 1.0)
+    with pytest.raises(nf.NFError):
+        nf.nf_train_batch(net.h, dev(np.zeros((1, 4), np.float32)), dev(np.zeros((1, 2), np.float32)), 1,
+                          float("nan"))
+
+
+def test_host_pointers_match_device_pointers():
+    dims = [37, 45, 13]
+    p = synth.random_params(5, dims, 0.5)
+    x, y = synth.random_batch(5, 50, 37, 13)
+    a = make_net(dims, "tanh", p)
+    b = make_net(dims, "tanh", p)
+    a.train_batch(x, y, 0.5)                      # numpy host buffers
+    b.train_batch(dev(x), dev(y), 0.5)
+    assert np.array_equal(gpu_params(a), gpu_params(b))
+    assert np.array_equal(a.output(x), b.output(dev(x)).cpu().numpy())
+    assert np.array_equal(a.grad(x, y), b.grad(dev(x), dev(y)).cpu().numpy())
+
+
+# ------------------------------------------------------------------ full configs
+def test_c1_full_trajectory():
+    """Config 1 in full: [3,5,2] sigmoid, 64 samples, B=8, eta=1, 100 steps (fused kernel)."""
+    cfg = synth.CONFIGS[1]
+    p = synth.init_params(1)
+    X, Y = synth.dataset(1)
+    starts = synth.batch_starts(1)
+    net = make_net(cfg["dims"], cfg["act"], p)
+    loss = torch.zeros(len(starts), device="cuda")
+    net.train_steps(dev(X), dev(Y), cfg["batch"], starts, cfg["eta"], step_loss=loss)
+    ref, ref_loss = oracle.Oracle(cfg["dims"], cfg["act"]).train_steps(p, X, Y, cfg["batch"], starts, cfg["eta"])
+    assert rel_err(gpu_params(net), ref) <= FP32_BAR
+    assert rel_err(loss.cpu().numpy(), ref_loss) <= FP32_BAR
+
+
+def test_c1_generic_path_equals_fused_semantics():
+    """The per-step kernels (nf_train_batch loop) and the fused kernel agree."""
+    cfg = synth.CONFIGS[1]
+    p = synth.init_params(1)
+    X, Y = synth.dataset(1)
+    starts = synth.batch_starts(1, steps=20)
+    a = make_net(cfg["dims"], cfg["act"], p)
+    b = make_net(cfg["dims"], cfg["act"], p)
+    a.train_steps(dev(X), dev(Y), 8, starts, 1.0)
+    for s in starts:
+        b.train_batch(dev(X[s:s + 8]), dev(Y[s:s + 8]), 1.0)
+    assert rel_err(gpu_params(a), gpu_params(b)) <= FP32_BAR
+
+
+@pytest.fixture(scope="module")
+def c2_trajectory():
+    """Oracle (fp64) run of config 2 in full: 500 steps, with fp32-rounded checkpoints."""
+    cfg = synth.CONFIGS[2]
+    p0 = synth.init_params(2)
+    X, Y = synth.dataset(2)
+    starts = synth.batch_starts(2)
+    o = oracle.Oracle(cfg["dims"], cfg["act"])
+    ckpt = {}
+    p = p0.astype(np.float64)
+    losses = []
+    for a, b in [(0, 100), (100, 250), (250, 490), (490, 500)]:
+        ckpt[a] = p.astype(np.float32)
+        p, l = o.train_steps(p, X, Y, cfg["batch"], starts[a:b], cfg["eta"])
+        losses.append(l)
+    ckpt[500] = p
+    return dict(cfg=cfg, X=X, Y=Y, starts=starts, ckpt=ckpt, p0=p0, loss=np.concatenate(losses))
+
+
+@pytest.mark.parametrize("at", [0, 100, 250, 490])
+def test_c2_teacher_forced_steps(c2_trajectory, at):
+    """Config 2 at full size, fused kernel in the bench's launch configuration: from the
+    oracle's fp32-rounded parameters at step `at`, 10 GPU steps vs 10 oracle steps."""
+    t = c2_trajectory
+    cfg, X, Y = t["cfg"], t["X"], t["Y"]
+    starts = t["starts"][at:at + 10]
+    p = t["ckpt"][at]
+    net = make_net(cfg["dims"], cfg["act"], p)
+    Xd, Yd = dev(X), dev(Y)
+    loss = torch.zeros(len(starts), device="cuda")
+    net.train_steps(Xd, Yd, cfg["batch"], starts, cfg["eta"], step_loss=loss)
+    o = oracle.Oracle(cfg["dims"], cfg["act"])
+    ref, ref_loss = o.train_steps(p, X, Y, cfg["batch"], starts, cfg["eta"])
+    got = gpu_params(net)
+    for (Wg, bg), (Wr, br) in zip(o.layers(got), o.layers(ref)):
+        assert rel_err(Wg, Wr) <= FP32_BAR
+        assert rel_err(bg, br) <= FP32_BAR
+    assert rel_err(loss.cpu().numpy(), ref_loss) <= FP32_BAR
+
+
+def test_c2_single_step_gradient_full_size(c2_trajectory):
+    """One full-size c2 step: the applied update (W_after - W_before) against the oracle's."""
+    t = c2_trajectory
+    cfg, X, Y = t["cfg"], t["X"], t["Y"]
+    s = int(t["starts"][0])
+    p = t["p0"]
+    net = make_net(cfg["dims"], cfg["act"], p)
+    net.train_steps(dev(X), dev(Y), cfg["batch"], [s], cfg["eta"])
+    o = oracle.Oracle(cfg["dims"], cfg["act"])
+    g = o.grad(p, X[s:s + 1000], Y[s:s + 1000]) * (cfg["eta"] / 1000)
+    upd = p.astype(np.float64) - gpu_params(net).astype(np.float64)
+    for (Ug, ub), (Ur, br) in zip(o.layers(upd), o.layers(g)):
+        assert rel_err(Ug, Ur) <= 5e-3   # W - W' in fp32 loses ~|W|/|dW| * 2^-24 relative
+        assert rel_err(ub, br) <= 5e-3
+
+
+def test_c2_free_running_500_steps(c2_trajectory):
+    """Whole config 2 (10 epochs) free-running on the GPU vs the fp64 oracle trajectory.
+    Reported bar 1e-3 on the final parameters, plus the per-step losses."""
+    t = c2_trajectory
+    cfg = t["cfg"]
+    net = make_net(cfg["dims"], cfg["act"], t["p0"])
+    loss = torch.zeros(500, device="cuda")
+    net.train_steps(dev(t["X"]), dev(t["Y"]), cfg["batch"], t["starts"], cfg["eta"], step_loss=loss)
+    err = rel_err(gpu_params(net), t["ckpt"][500])
+    print(f"c2 free-running final-param err {err:.3e}")
+    assert err <= 1e-3
+    assert rel_err(loss.cpu().numpy(), t["loss"]) <= 1e-3
+
+
+def test_c5_full_width_sampled():
+    """Config 5 widths [4096,4096,4096,4096,1024]: forward on sampled rows and one-step
+    tendencies on a small batch (the oracle's per-sample cost is batch independent)."""
+    cfg = synth.CONFIGS[5]
+    dims = cfg["dims"]
+    p = synth.init_params(5)
+    X, Y = synth.dataset(5, N=64)
+    net = make_net(dims, cfg["act"], p)
+    o = oracle.Oracle(dims, cfg["act"])
+    rows = np.arange(0, 64, 8)
+    out = net.output(dev(X)).cpu().numpy()
+    assert rel_err(out[rows], o.output(p, X[rows])) <= FP32_BAR
+    g = net.grad(dev(X[:6]), dev(Y[:6])).cpu().numpy()
+    ref = o.grad(p, X[:6], Y[:6])
+    for (Wg, bg), (Wr, br) in zip(o.layers(g), o.layers(ref)):
+        assert rel_err(Wg, Wr) <= FP32_BAR
+        assert rel_err(bg, br) <= FP32_BAR
+
+
+@pytest.mark.parametrize("cid,n", [(3, 64), (4, 256)])
+def test_c3_c4_full_width_one_step(cid, n):
+    cfg = synth.CONFIGS[cid]
+    dims = cfg["dims"]
+    p = synth.init_params(cid)
+    X, Y = synth.dataset(cid, N=n)
+    net = make_net(dims, cfg["act"], p)
+    net.train_batch(dev(X), dev(Y), cfg["eta"])
+    ref, _ = oracle.Oracle(dims, cfg["act"]).train_batch(p, X, Y, cfg["eta"])
+    assert rel_err(gpu_params(net), ref) <= FP32_BAR
