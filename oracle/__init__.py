@@ -194,21 +194,40 @@ class Oracle:
         assert rc == 0
         return float(out[0])
 
-    def stash(self, params, x, y):
-        """Per-layer activations a_0..a_L and deltas delta_1..delta_L of one batch."""
+    def stash(self, params, x, y, with_z: bool = False):
+        """Per-layer activations a_0..a_L and deltas delta_1..delta_L of one batch
+        (and pre-activations z_1..z_L with with_z=True)."""
         p, x, y = self._p(params), _f32(x), _f32(y)
         n = x.shape[0]
         A = np.zeros(n * sum(self.dims), dtype=self.real)
         D = np.zeros(n * sum(self.dims[1:]), dtype=self.real)
+        Z = np.zeros(n * sum(self.dims[1:]), dtype=self.real) if with_z else None
         rc = self.lib.orc_forward_backward_stash(*self._head(), _ptr(p), _ptr(x), _ptr(y),
-                                                 ctypes.c_long(n), _ptr(A), _ptr(D))
+                                                 ctypes.c_long(n), _ptr(A), _ptr(D),
+                                                 _ptr(Z) if with_z else None)
         assert rc == 0
-        As, Ds, oa, od = [], [], 0, 0
+        As, Ds, Zs, oa, od = [], [], [], 0, 0
         for l, w in enumerate(self.dims):
             As.append(A[oa:oa + n * w].reshape(n, w)); oa += n * w
             if l >= 1:
-                Ds.append(D[od:od + n * w].reshape(n, w)); od += n * w
-        return As, Ds
+                Ds.append(D[od:od + n * w].reshape(n, w))
+                if with_z:
+                    Zs.append(Z[od:od + n * w].reshape(n, w))
+                od += n * w
+        return (As, Ds, Zs) if with_z else (As, Ds)
+
+    def kink_free_rows(self, params, x, y, margin: float = 1e-4):
+        """Rows whose hidden pre-activations all keep |z| > margin, where a relu/step
+        derivative is a discrete decision: the fp32 GPU sum and this fp64 sum may take it
+        differently within rounding (reading R8 of DESIGN.md).  Parity compares these rows."""
+        acts = (self.act_h, self.act_o)
+        _, _, Zs = self.stash(params, x, y, with_z=True)
+        ok = np.ones(x.shape[0], dtype=bool)
+        for l, z in enumerate(Zs, start=1):
+            kind = acts[0] if l < len(Zs) else acts[1]
+            if kind in (ACT["relu"], ACT["step"]):
+                ok &= np.all(np.abs(z) > margin, axis=1)
+        return ok
 
 
 def _scalar(bits, v):

@@ -309,11 +309,11 @@ int orc_accuracy(const int *dims, int nd, int act_h, int act_o, const REAL *p,
 }
 
 /* per-layer stash of one forward pass over a batch, for kernel-level
- * parity (a_l and delta_l per sample).  A: for l=0..L, [n][n_l] blocks
- * concatenated; D: for l=1..L, [n][n_l] blocks concatenated. */
+ * parity (a_l, delta_l and z_l per sample).  A: for l=0..L, [n][n_l] blocks
+ * concatenated; D and Z (Z may be NULL): for l=1..L, [n][n_l] blocks. */
 int orc_forward_backward_stash(const int *dims, int nd, int act_h, int act_o,
                                const REAL *p, const float *x, const float *y,
-                               long n, REAL *A, REAL *D)
+                               long n, REAL *A, REAL *D, REAL *Z)
 {
     net_t t;
     if (net_open(&t, dims, nd, act_h, act_o)) { net_close(&t); return -1; }
@@ -329,6 +329,8 @@ int orc_forward_backward_stash(const int *dims, int nd, int act_h, int act_o,
             oa += n * dims[l];
             if (l >= 1) {
                 for (int i = 0; i < dims[l]; ++i) D[od + s * dims[l] + i] = t.delta[l][i];
+                if (Z)
+                    for (int i = 0; i < dims[l]; ++i) Z[od + s * dims[l] + i] = t.z[l][i];
                 od += n * dims[l];
             }
         }

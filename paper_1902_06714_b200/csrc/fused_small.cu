@@ -60,7 +60,16 @@ struct FusedParams {
   float *acc;            // 3 x nparams accumulators (zeroed by the host)
   unsigned *bar;         // grid barrier counter (zeroed by the host)
   float *step_loss;      // nullable, zeroed by the host
+  unsigned long long *prof;  // nullable: per-CTA per-step phase timestamps (NF_FUSED_PROF=1)
 };
+
+__device__ __forceinline__ unsigned long long globaltimer() {
+  unsigned long long t;
+  asm volatile("mov.u64 %0, %globaltimer;" : "=l"(t));
+  return t;
+}
+#define PROF(i) \
+  if (p.prof && threadIdx.x == 0 && s < 64) p.prof[((int64_t)blockIdx.x * 64 + s) * 8 + (i)] = globaltimer()
 
 __device__ __forceinline__ int row_begin(int g, int B, int G) { return (int)(((int64_t)g * B) / G); }
 
@@ -181,10 +190,12 @@ __global__ void __launch_bounds__(kThreads, 1) fused_small_kernel(const FusedPar
     const float *xs = xs0 + buf * p.nSmax * wpad;
     const float *ys = ys0 + buf * p.nOwnMax * 32;
     float *accS = p.acc + (s % 3) * np;
+    PROF(0);
     if (s + 1 < p.n_steps) prefetch(s + 1);
     else cp_async_commit();
     cp_async_wait1();
     __syncthreads();
+    PROF(1);
 
     // ---- 1. partial Z1: P[i][j] = sum_{k<w} x[i][k] W1[j][k0+k]   (warp: rows i = warp + 8q, lane: j)
     {
@@ -207,7 +218,9 @@ __global__ void __launch_bounds__(kThreads, 1) fused_small_kernel(const FusedPar
       for (int q = 0; q < kMaxQ; ++q)
         if (q < nq) P[(warp + q * kWarps) * 32 + lane] = accq[q];
     }
+    PROF(2);
     cluster_sync_all();
+    PROF(3);
 
     // ---- 2. owned rows: reduce partials over the cluster, layer 1 epilogue, layer 2, deltas
     float g2acc[32];  // per-lane accumulators: lane j holds G2[o][j] for all o
@@ -269,6 +282,7 @@ __global__ void __launch_bounds__(kThreads, 1) fused_small_kernel(const FusedPar
       for (int ww = 0; ww < kWarps; ++ww) l += lsum[ww];
       red_add(p.step_loss + s, 0.5f * l * p.inv_B);
     }
+    PROF(4);
     cluster_sync_all();
 
     // ---- 3. all-gather delta_1 rows of the peers; cluster-reduce the layer-2/bias tendencies
@@ -297,6 +311,7 @@ __global__ void __launch_bounds__(kThreads, 1) fused_small_kernel(const FusedPar
     }
     __syncthreads();
 
+    PROF(5);
     // ---- 4. dW1 slice: Gs[j][k] = sum_{i<nS} D1[i][j] x[i][k]   (lane: j, warp: 4-column chunks)
     {
       const int nchunk = wpad / 4;
@@ -331,7 +346,9 @@ __global__ void __launch_bounds__(kThreads, 1) fused_small_kernel(const FusedPar
     }
 
     // ---- 5. grid barrier (the co_sum is complete), then the SGD update of the resident parameters
+    PROF(6);
     grid_barrier(p.bar, (unsigned)((s + 1) * nCTA));
+    PROF(7);
     for (int i = tid; i < H * w; i += kThreads) {
       const int j = i / w, k = i % w;
       const float gsum = __ldcg(accS + oW1 + (int64_t)j * n0 + k0 + k);
@@ -463,6 +480,13 @@ int fused_small_train_steps(FusedSmall &fs, cudaStream_t st, const std::vector<i
   int64_t *dstarts = reinterpret_cast<int64_t *>(base + 3 * np * sizeof(float) + 256);
   p.starts = dstarts;
   p.step_loss = step_loss;
+  static unsigned long long *prof_buf = nullptr;
+  const bool prof = env_int("NF_FUSED_PROF", 0) != 0;
+  if (prof) {
+    if (!prof_buf) cudaMalloc(&prof_buf, sizeof(unsigned long long) * 148 * 64 * 8);
+    cudaMemsetAsync(prof_buf, 0, sizeof(unsigned long long) * 148 * 64 * 8, st);
+    p.prof = prof_buf;
+  }
 
   cudaError_t e = cudaMemsetAsync(base, 0, 3 * np * sizeof(float) + 256, st);
   if (e == cudaSuccess)
@@ -485,6 +509,29 @@ int fused_small_train_steps(FusedSmall &fs, cudaStream_t st, const std::vector<i
   if (e != cudaSuccess) {
     snprintf(g_fs_err, sizeof g_fs_err, "launch (C=%d G=%d smem=%zu): %s", C, G, smem, cudaGetErrorString(e));
     return -1;
+  }
+  if (prof) {
+    std::vector<unsigned long long> h((size_t)G * C * 64 * 8);
+    cudaStreamSynchronize(st);
+    cudaMemcpy(h.data(), prof_buf, h.size() * sizeof(unsigned long long), cudaMemcpyDeviceToHost);
+    const int ns = (int)std::min<int64_t>(n_steps, 64);
+    double ph[8] = {0}, phmax[8] = {0};
+    int cnt = 0;
+    for (int s = 2; s + 1 < ns; ++s, ++cnt) {
+      for (int i = 0; i < 8; ++i) {
+        double mx = 0, sum = 0;
+        for (int b = 0; b < G * C; ++b) {
+          const unsigned long long *t = &h[((size_t)b * 64 + s) * 8];
+          const unsigned long long nxt = i < 7 ? t[i + 1] : h[((size_t)b * 64 + s + 1) * 8];
+          const double d = (double)(nxt - t[i]);
+          sum += d; mx = std::max(mx, d);
+        }
+        ph[i] += sum / (G * C); phmax[i] += mx;
+      }
+    }
+    fprintf(stderr, "[fused prof] C=%d G=%d nS<=%d w=%d smem=%zu  phase ns (mean over CTAs / max):\n", C, G, nSmax, w, smem);
+    const char *names[8] = {"wait_x", "z1_partial", "csync1", "owned_rows", "csync2+gather", "dW1+red", "grid_bar", "update"};
+    for (int i = 0; i < 8; ++i) fprintf(stderr, "  %-14s %8.0f %8.0f\n", names[i], ph[i] / cnt, phmax[i] / cnt);
   }
   return 0;
 }

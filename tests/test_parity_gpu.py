@@ -272,11 +272,20 @@ def test_c5_full_width_sampled():
 
 @pytest.mark.parametrize("cid,n", [(3, 64), (4, 256)])
 def test_c3_c4_full_width_one_step(cid, n):
+    """One step at the full widths of configs 3 and 4.  Rows with a relu pre-activation
+    inside the fp32 rounding band (|z| <= 1e-4) are excluded: there relu' is a discrete
+    decision both sides may take differently (R8); the rest must match to 1e-4 per layer."""
     cfg = synth.CONFIGS[cid]
     dims = cfg["dims"]
     p = synth.init_params(cid)
     X, Y = synth.dataset(cid, N=n)
+    o = oracle.Oracle(dims, cfg["act"])
+    keep = o.kink_free_rows(p, X, Y)
+    assert keep.mean() > 0.5
+    X, Y = np.ascontiguousarray(X[keep]), np.ascontiguousarray(Y[keep])
     net = make_net(dims, cfg["act"], p)
     net.train_batch(dev(X), dev(Y), cfg["eta"])
-    ref, _ = oracle.Oracle(dims, cfg["act"]).train_batch(p, X, Y, cfg["eta"])
-    assert rel_err(gpu_params(net), ref) <= FP32_BAR
+    ref, _ = o.train_batch(p, X, Y, cfg["eta"])
+    for (Wg, bg), (Wr, br) in zip(o.layers(gpu_params(net)), o.layers(ref)):
+        assert rel_err(Wg, Wr) <= FP32_BAR
+        assert rel_err(bg, br) <= FP32_BAR
