@@ -41,7 +41,8 @@ namespace {
 
 constexpr int kThreads = 256;
 constexpr int kWarps = kThreads / 32;
-constexpr int kMaxQ = 16;  // samples per warp in the Z1 phase (nS <= kWarps * kMaxQ = 128)
+constexpr int kMaxQ = 16;  // nS <= kWarps * kMaxQ = 128 rows per cluster
+constexpr int kMaxC = 8;   // cluster size
 
 struct FusedParams {
   int n0, H, O;          // dims
@@ -124,16 +125,17 @@ __global__ void __launch_bounds__(kThreads, 1) fused_small_kernel(const FusedPar
 
   // ---- shared memory carve-up (floats)
   float *W1t = sm;                                  // [wpad][32]  W1[j][k0+k] at W1t[k*32+j]
-  float *W2s = W1t + wpad * 32;                     // [32][32]    W2[o][j]
-  float *b1s = W2s + 32 * 32;                       // [32]
+  float *W2s = W1t + wpad * 32;                     // [32][33]    W2[o][j] (padded rows)
+  float *b1s = W2s + 32 * 33;                       // [32]
   float *b2s = b1s + 32;                            // [32]
   float *xs0 = b2s + 32;                            // 2 x [nSmax][wpad]
   float *ys0 = xs0 + 2 * p.nSmax * wpad;            // 2 x [nOwnMax][32]
   float *P = ys0 + 2 * p.nOwnMax * 32;              // [nSmax][32] partial Z1
   float *D1 = P + p.nSmax * 32;                     // [nSmax][32] delta_1 of all cluster rows
   float *gpart = D1 + p.nSmax * 32;                 // [32*32 + 64]: G2[o][j], g1[j], g2[o]
-  float *Gs = gpart + 32 * 32 + 64;                 // [32][wpad] dW1 slice staging
-  float *wred = Gs + 32 * wpad;                     // [kWarps][32*32+64] warp partials
+  const int gsld = wpad + 1;                        // odd row stride: conflict-free row and column access
+  float *Gs = gpart + 32 * 32 + 64;                 // [32][gsld] dW1 slice staging
+  float *wred = Gs + 32 * gsld;                     // [kWarps][32*32+64] warp partials
   float *lsum = wred + kWarps * (32 * 32 + 64);     // [kWarps]
   const int GP = 32 * 32 + 64;
 
@@ -146,8 +148,8 @@ __global__ void __launch_bounds__(kThreads, 1) fused_small_kernel(const FusedPar
     const int k = i / 32, j = i % 32;
     W1t[i] = (j < H && k < w) ? p.params[oW1 + (int64_t)j * n0 + k0 + k] : 0.0f;
   }
-  for (int i = tid; i < 32 * 32; i += kThreads) {
-    const int o = i / 32, j = i % 32;
+  for (int i = tid; i < 32 * 33; i += kThreads) {
+    const int o = i / 33, j = i % 33;
     W2s[i] = (o < O && j < H) ? p.params[oW2 + (int64_t)o * H + j] : 0.0f;
   }
   for (int i = tid; i < 32; i += kThreads) {
@@ -161,15 +163,14 @@ __global__ void __launch_bounds__(kThreads, 1) fused_small_kernel(const FusedPar
     const int64_t row0 = p.starts[s] + r0;
     float *xs = xs0 + buf * p.nSmax * wpad;
     if (vec8) {
-      const int w2 = w >> 1;
-      for (int i = tid; i < nS * w2; i += kThreads) {
-        const int r = i / w2, c = (i % w2) * 2;
-        cp_async8(xs + r * wpad + c, p.X + (row0 + r) * n0 + k0 + c);
+      for (int r = warp; r < nS; r += kWarps) {
+        const float *src = p.X + (row0 + r) * n0 + k0;
+        for (int c = lane * 2; c < w; c += 64) cp_async8(xs + r * wpad + c, src + c);
       }
     } else {
-      for (int i = tid; i < nS * w; i += kThreads) {
-        const int r = i / w, c = i % w;
-        cp_async4(xs + r * wpad + c, p.X + (row0 + r) * n0 + k0 + c);
+      for (int r = warp; r < nS; r += kWarps) {
+        const float *src = p.X + (row0 + r) * n0 + k0;
+        for (int c = lane; c < w; c += 32) cp_async4(xs + r * wpad + c, src + c);
       }
     }
     float *ys = ys0 + buf * p.nOwnMax * 32;
@@ -197,26 +198,34 @@ __global__ void __launch_bounds__(kThreads, 1) fused_small_kernel(const FusedPar
     __syncthreads();
     PROF(1);
 
-    // ---- 1. partial Z1: P[i][j] = sum_{k<w} x[i][k] W1[j][k0+k]   (warp: rows i = warp + 8q, lane: j)
-    {
-      float accq[kMaxQ];
+    // ---- 1. partial Z1: P[i][j] = sum_{k<w} x[i][k] W1[j][k0+k]
+    //      warp: 8-row chunks (rows warp + 8u), lane: j; 8 independent FMA chains per lane
+    for (int rb = 0; rb * kWarps * 8 < nS; ++rb) {
+      const float *xr[8];
+      int rows[8];
 #pragma unroll
-      for (int q = 0; q < kMaxQ; ++q) accq[q] = 0.0f;
-      const int nq = (nS - warp + kWarps - 1) / kWarps;
+      for (int u = 0; u < 8; ++u) {
+        rows[u] = warp + kWarps * (rb * 8 + u);
+        xr[u] = xs + (rows[u] < nS ? rows[u] : 0) * wpad;
+      }
+      float a[8] = {0, 0, 0, 0, 0, 0, 0, 0};
       for (int k = 0; k < wpad; k += 4) {
         const float w0 = W1t[(k + 0) * 32 + lane], w1 = W1t[(k + 1) * 32 + lane];
         const float w2 = W1t[(k + 2) * 32 + lane], w3 = W1t[(k + 3) * 32 + lane];
+        float4 xv[8];
 #pragma unroll
-        for (int q = 0; q < kMaxQ; ++q) {
-          if (q < nq) {
-            const float4 xv = *reinterpret_cast<const float4 *>(xs + (warp + q * kWarps) * wpad + k);
-            accq[q] = fmaf(xv.x, w0, fmaf(xv.y, w1, fmaf(xv.z, w2, fmaf(xv.w, w3, accq[q]))));
-          }
+        for (int u = 0; u < 8; ++u) xv[u] = *reinterpret_cast<const float4 *>(xr[u] + k);
+#pragma unroll
+        for (int u = 0; u < 8; ++u) {
+          a[u] = fmaf(xv[u].x, w0, a[u]);
+          a[u] = fmaf(xv[u].y, w1, a[u]);
+          a[u] = fmaf(xv[u].z, w2, a[u]);
+          a[u] = fmaf(xv[u].w, w3, a[u]);
         }
       }
 #pragma unroll
-      for (int q = 0; q < kMaxQ; ++q)
-        if (q < nq) P[(warp + q * kWarps) * 32 + lane] = accq[q];
+      for (int u = 0; u < 8; ++u)
+        if (rows[u] < nS) P[rows[u] * 32 + lane] = a[u];
     }
     PROF(2);
     cluster_sync_all();
@@ -229,17 +238,21 @@ __global__ void __launch_bounds__(kThreads, 1) fused_small_kernel(const FusedPar
     float g1acc = 0.0f, gb2acc = 0.0f, lacc = 0.0f;
     for (int q = warp; q < nOwn; q += kWarps) {
       const int i = o0 + q;
+      float pv[kMaxC];
+#pragma unroll
+      for (int c = 0; c < kMaxC; ++c)   // all DSMEM loads in flight, then a fixed-order sum
+        pv[c] = c < C ? cl.map_shared_rank(P, c)[i * 32 + lane] : 0.0f;
       float z = b1s[lane];
-      for (int c = 0; c < C; ++c) {
-        const float *Pc = cl.map_shared_rank(P, c);
-        z += Pc[i * 32 + lane];
-      }
+#pragma unroll
+      for (int c = 0; c < kMaxC; ++c) z += pv[c];
       float a1, s1;
       act_fwd(p.act_h, z, a1, s1);
       if (lane >= H) { a1 = 0.0f; s1 = 0.0f; }
       // z2[o] at lane o
       float z2 = b2s[lane];
-      for (int j = 0; j < H; ++j) z2 = fmaf(W2s[lane * 32 + j], __shfl_sync(0xffffffffu, a1, j), z2);
+#pragma unroll
+      for (int j = 0; j < 32; ++j)
+        if (j < H) z2 = fmaf(W2s[lane * 33 + j], __shfl_sync(0xffffffffu, a1, j), z2);
       float a2, s2;
       act_fwd(p.act_o, z2, a2, s2);
       const float yv = lane < O ? ys[q * 32 + lane] : 0.0f;
@@ -252,7 +265,7 @@ __global__ void __launch_bounds__(kThreads, 1) fused_small_kernel(const FusedPar
       for (int o = 0; o < 32; ++o) {
         if (o < O) {
           const float d2o = __shfl_sync(0xffffffffu, d2, o);
-          t = fmaf(W2s[o * 32 + lane], d2o, t);
+          t = fmaf(W2s[o * 33 + lane], d2o, t);
           g2acc[o] = fmaf(d2o, a1, g2acc[o]);
         }
       }
@@ -274,6 +287,7 @@ __global__ void __launch_bounds__(kThreads, 1) fused_small_kernel(const FusedPar
     __syncthreads();
     for (int i = tid; i < GP; i += kThreads) {
       float v = 0.0f;
+#pragma unroll
       for (int ww = 0; ww < kWarps; ++ww) v += wred[ww * GP + i];
       gpart[i] = v;
     }
@@ -286,17 +300,34 @@ __global__ void __launch_bounds__(kThreads, 1) fused_small_kernel(const FusedPar
     cluster_sync_all();
 
     // ---- 3. all-gather delta_1 rows of the peers; cluster-reduce the layer-2/bias tendencies
-    for (int c = 0; c < C; ++c) {
-      if (c == rank) continue;
-      const int a0 = (c * nS) / C, a1r = ((c + 1) * nS) / C;
-      const float *Dc = cl.map_shared_rank(D1, c);
-      for (int i = a0 * 32 + tid; i < a1r * 32; i += kThreads) D1[i] = Dc[i];
+    for (int base = 0; base < nS * 32; base += 8 * kThreads) {
+      float v[8];
+      int own[8];
+#pragma unroll
+      for (int u = 0; u < 8; ++u) {
+        const int idx = base + u * kThreads + tid;
+        own[u] = -1;
+        v[u] = 0.0f;
+        if (idx < nS * 32) {
+          const int row = idx >> 5;
+          int c = 0;
+          while (c + 1 < C && ((c + 1) * nS) / C <= row) ++c;
+          if (c != rank) { own[u] = c; v[u] = cl.map_shared_rank(D1, c)[idx]; }
+        }
+      }
+#pragma unroll
+      for (int u = 0; u < 8; ++u)
+        if (own[u] >= 0) D1[base + u * kThreads + tid] = v[u];
     }
     {
       const int e0 = (rank * GP) / C, e1 = ((rank + 1) * GP) / C;
       for (int e = e0 + tid; e < e1; e += kThreads) {
+        float pv[kMaxC];
+#pragma unroll
+        for (int c = 0; c < kMaxC; ++c) pv[c] = c < C ? cl.map_shared_rank(gpart, c)[e] : 0.0f;
         float v = 0.0f;
-        for (int c = 0; c < C; ++c) v += cl.map_shared_rank(gpart, c)[e];
+#pragma unroll
+        for (int c = 0; c < kMaxC; ++c) v += pv[c];
         int64_t dst = -1;
         if (e < 1024) {
           const int o = e / 32, j = e % 32;
@@ -312,54 +343,83 @@ __global__ void __launch_bounds__(kThreads, 1) fused_small_kernel(const FusedPar
     __syncthreads();
 
     PROF(5);
-    // ---- 4. dW1 slice: Gs[j][k] = sum_{i<nS} D1[i][j] x[i][k]   (lane: j, warp: 4-column chunks)
+    // ---- 4. dW1 slice: Gs[j][k] = sum_{i<nS} D1[i][j] x[i][k]   (lane: j, warp: 16-column groups)
     {
-      const int nchunk = wpad / 4;
-      for (int c0 = warp; c0 < nchunk; c0 += 2 * kWarps) {
-        const int c1 = c0 + kWarps;
-        float a[8] = {0, 0, 0, 0, 0, 0, 0, 0};
-        const bool two = c1 < nchunk;
+      const int nchunk = wpad / 4;  // 4-column chunks
+      for (int cb = warp * 4; cb < nchunk; cb += kWarps * 4) {
+        int cc[4];
+#pragma unroll
+        for (int u = 0; u < 4; ++u) cc[u] = (cb + u < nchunk ? cb + u : cb) * 4;
+        float a[16];
+#pragma unroll
+        for (int u = 0; u < 16; ++u) a[u] = 0.0f;
         for (int i = 0; i < nS; ++i) {
           const float d = D1[i * 32 + lane];
-          const float4 x0 = *reinterpret_cast<const float4 *>(xs + i * wpad + c0 * 4);
-          a[0] = fmaf(d, x0.x, a[0]); a[1] = fmaf(d, x0.y, a[1]);
-          a[2] = fmaf(d, x0.z, a[2]); a[3] = fmaf(d, x0.w, a[3]);
-          if (two) {
-            const float4 x1 = *reinterpret_cast<const float4 *>(xs + i * wpad + c1 * 4);
-            a[4] = fmaf(d, x1.x, a[4]); a[5] = fmaf(d, x1.y, a[5]);
-            a[6] = fmaf(d, x1.z, a[6]); a[7] = fmaf(d, x1.w, a[7]);
+          const float *xr = xs + i * wpad;
+          float4 xv[4];
+#pragma unroll
+          for (int u = 0; u < 4; ++u) xv[u] = *reinterpret_cast<const float4 *>(xr + cc[u]);
+#pragma unroll
+          for (int u = 0; u < 4; ++u) {
+            a[4 * u + 0] = fmaf(d, xv[u].x, a[4 * u + 0]);
+            a[4 * u + 1] = fmaf(d, xv[u].y, a[4 * u + 1]);
+            a[4 * u + 2] = fmaf(d, xv[u].z, a[4 * u + 2]);
+            a[4 * u + 3] = fmaf(d, xv[u].w, a[4 * u + 3]);
           }
         }
         if (lane < H) {
 #pragma unroll
-          for (int u = 0; u < 4; ++u) Gs[lane * wpad + c0 * 4 + u] = a[u];
-          if (two)
+          for (int u = 0; u < 4; ++u)
+            if (cb + u < nchunk)
 #pragma unroll
-            for (int u = 0; u < 4; ++u) Gs[lane * wpad + c1 * 4 + u] = a[4 + u];
+              for (int e = 0; e < 4; ++e) Gs[lane * gsld + cc[u] + e] = a[4 * u + e];
         }
       }
     }
     __syncthreads();
-    for (int i = tid; i < H * w; i += kThreads) {
-      const int j = i / w, k = i % w;
-      red_add(accS + oW1 + (int64_t)j * n0 + k0 + k, Gs[j * wpad + k]);
+    // co_sum: add this CTA's slice partial into the L2 accumulator (rows j, lanes along k)
+    for (int j = warp; j < H; j += kWarps) {
+      float *dst = accS + oW1 + (int64_t)j * n0 + k0;
+      for (int k = lane; k < w; k += 32) red_add(dst + k, Gs[j * gsld + k]);
     }
 
     // ---- 5. grid barrier (the co_sum is complete), then the SGD update of the resident parameters
     PROF(6);
     grid_barrier(p.bar, (unsigned)((s + 1) * nCTA));
     PROF(7);
-    for (int i = tid; i < H * w; i += kThreads) {
-      const int j = i / w, k = i % w;
-      const float gsum = __ldcg(accS + oW1 + (int64_t)j * n0 + k0 + k);
-      W1t[k * 32 + j] -= p.scale * gsum;
+    // fetch the reduced slice rows (coalesced along k, all loads in flight) into Gs
+    for (int j = warp; j < H; j += kWarps) {
+      const float *src = accS + oW1 + (int64_t)j * n0 + k0;
+      float v[8];
+#pragma unroll
+      for (int u = 0; u < 8; ++u) {
+        const int k = lane + 32 * u;
+        v[u] = k < w ? __ldcg(src + k) : 0.0f;
+      }
+#pragma unroll
+      for (int u = 0; u < 8; ++u) {
+        const int k = lane + 32 * u;
+        if (k < w) Gs[j * gsld + k] = v[u];
+      }
+      for (int k = lane + 256; k < w; k += 32) Gs[j * gsld + k] = __ldcg(src + k);
     }
-    for (int i = tid; i < O * H; i += kThreads) {
-      const int o = i / H, j = i % H;
-      W2s[o * 32 + j] -= p.scale * __ldcg(accS + oW2 + i);
+    float gl2 = 0.0f, gl3 = 0.0f;
+    {
+      const int e = tid;  // O*H + H + O <= 32*32 + 64 entries of W2/b1/b2 (flat layout order b1, W2, b2)
+      if (e < H + O * H + O) gl2 = __ldcg(accS + ob1 + e);
+      if (e + kThreads < H + O * H + O) gl3 = __ldcg(accS + ob1 + e + kThreads);
     }
-    for (int i = tid; i < H; i += kThreads) b1s[i] -= p.scale * __ldcg(accS + ob1 + i);
-    for (int i = tid; i < O; i += kThreads) b2s[i] -= p.scale * __ldcg(accS + ob2 + i);
+    __syncthreads();
+    for (int i = tid; i < w * 32; i += kThreads) {
+      const int k = i >> 5, j = i & 31;
+      if (j < H) W1t[i] -= p.scale * Gs[j * gsld + k];
+    }
+    for (int e = tid; e < H + O * H + O; e += kThreads) {
+      const float gsum = e == tid ? gl2 : (e == tid + kThreads ? gl3 : __ldcg(accS + ob1 + e));
+      if (e < H) b1s[e] -= p.scale * gsum;
+      else if (e < H + O * H) { const int f = e - H; W2s[(f / H) * 33 + f % H] -= p.scale * gsum; }
+      else b2s[e - H - O * H] -= p.scale * gsum;
+    }
     // zero the accumulator used two steps ahead (its readers finished before this barrier)
     {
       float *z = p.acc + ((s + 2) % 3) * np;
@@ -377,7 +437,7 @@ __global__ void __launch_bounds__(kThreads, 1) fused_small_kernel(const FusedPar
       p.params[oW1 + (int64_t)j * n0 + k0 + k] = W1t[k * 32 + j];
     }
     if (rank == 0) {
-      for (int i = tid; i < O * H; i += kThreads) p.params[oW2 + i] = W2s[(i / H) * 32 + i % H];
+      for (int i = tid; i < O * H; i += kThreads) p.params[oW2 + i] = W2s[(i / H) * 33 + i % H];
       for (int i = tid; i < H; i += kThreads) p.params[ob1 + i] = b1s[i];
       for (int i = tid; i < O; i += kThreads) p.params[ob2 + i] = b2s[i];
     }
@@ -385,8 +445,8 @@ __global__ void __launch_bounds__(kThreads, 1) fused_small_kernel(const FusedPar
 }
 
 size_t smem_floats(int wpad, int nSmax, int nOwnMax) {
-  return (size_t)wpad * 32 + 32 * 32 + 64 + 2 * (size_t)nSmax * wpad + 2 * (size_t)nOwnMax * 32 +
-         2 * (size_t)nSmax * 32 + (32 * 32 + 64) + 32 * (size_t)wpad + kWarps * (32 * 32 + 64) + kWarps;
+  return (size_t)wpad * 32 + 32 * 33 + 64 + 2 * (size_t)nSmax * wpad + 2 * (size_t)nOwnMax * 32 +
+         2 * (size_t)nSmax * 32 + (32 * 32 + 64) + 32 * (size_t)(wpad + 1) + kWarps * (32 * 32 + 64) + kWarps + 8;
 }
 
 int env_int(const char *name, int dflt) {
@@ -412,6 +472,7 @@ int fused_small_train_steps(FusedSmall &fs, cudaStream_t st, const std::vector<i
     C = 8;
     while (C > 1 && n0 / C < 32) C /= 2;
   }
+  C = std::max(1, std::min(C, kMaxC));
   const int w = (n0 + C - 1) / C;
   const int wpad = (w + 3) / 4 * 4;
   // clusters: as many as co-reside (1 CTA per SM), rows per cluster <= 128
