@@ -43,6 +43,7 @@ constexpr int kThreads = 256;
 constexpr int kWarps = kThreads / 32;
 constexpr int kMaxQ = 16;  // nS <= kWarps * kMaxQ = 128 rows per cluster
 constexpr int kMaxC = 8;   // cluster size
+constexpr int kProf = 16;  // profiler slots per step
 
 struct FusedParams {
   int n0, H, O;          // dims
@@ -70,7 +71,7 @@ __device__ __forceinline__ unsigned long long globaltimer() {
   return t;
 }
 #define PROF(i) \
-  if (p.prof && threadIdx.x == 0 && s < 64) p.prof[((int64_t)blockIdx.x * 64 + s) * 8 + (i)] = globaltimer()
+  if (p.prof && threadIdx.x == 0 && s < 64) p.prof[((int64_t)blockIdx.x * 64 + s) * kProf + (i)] = globaltimer()
 
 __device__ __forceinline__ int row_begin(int g, int B, int G) { return (int)(((int64_t)g * B) / G); }
 
@@ -194,9 +195,10 @@ __global__ void __launch_bounds__(kThreads, 1) fused_small_kernel(const FusedPar
     PROF(0);
     if (s + 1 < p.n_steps) prefetch(s + 1);
     else cp_async_commit();
+    PROF(1);
     cp_async_wait1();
     __syncthreads();
-    PROF(1);
+    PROF(2);
 
     // ---- 1. partial Z1: P[i][j] = sum_{k<w} x[i][k] W1[j][k0+k]
     //      warp: 8-row chunks (rows warp + 8u), lane: j; 8 independent FMA chains per lane
@@ -227,9 +229,9 @@ __global__ void __launch_bounds__(kThreads, 1) fused_small_kernel(const FusedPar
       for (int u = 0; u < 8; ++u)
         if (rows[u] < nS) P[rows[u] * 32 + lane] = a[u];
     }
-    PROF(2);
-    cluster_sync_all();
     PROF(3);
+    cluster_sync_all();
+    PROF(4);
 
     // ---- 2. owned rows: reduce partials over the cluster, layer 1 epilogue, layer 2, deltas
     float g2acc[32];  // per-lane accumulators: lane j holds G2[o][j] for all o
@@ -274,6 +276,7 @@ __global__ void __launch_bounds__(kThreads, 1) fused_small_kernel(const FusedPar
       g1acc += d1;
       gb2acc += lane < O ? d2 : 0.0f;
     }
+    PROF(5);
     // warp partials -> smem
     {
       float *wr = wred + warp * GP;
@@ -296,8 +299,9 @@ __global__ void __launch_bounds__(kThreads, 1) fused_small_kernel(const FusedPar
       for (int ww = 0; ww < kWarps; ++ww) l += lsum[ww];
       red_add(p.step_loss + s, 0.5f * l * p.inv_B);
     }
-    PROF(4);
+    PROF(6);
     cluster_sync_all();
+    PROF(7);
 
     // ---- 3. all-gather delta_1 rows of the peers; cluster-reduce the layer-2/bias tendencies
     for (int base = 0; base < nS * 32; base += 8 * kThreads) {
@@ -319,6 +323,7 @@ __global__ void __launch_bounds__(kThreads, 1) fused_small_kernel(const FusedPar
       for (int u = 0; u < 8; ++u)
         if (own[u] >= 0) D1[base + u * kThreads + tid] = v[u];
     }
+    PROF(8);
     {
       const int e0 = (rank * GP) / C, e1 = ((rank + 1) * GP) / C;
       for (int e = e0 + tid; e < e1; e += kThreads) {
@@ -340,9 +345,10 @@ __global__ void __launch_bounds__(kThreads, 1) fused_small_kernel(const FusedPar
         if (dst >= 0) red_add(accS + dst, v);
       }
     }
+    PROF(9);
     __syncthreads();
 
-    PROF(5);
+    PROF(10);
     // ---- 4. dW1 slice: Gs[j][k] = sum_{i<nS} D1[i][j] x[i][k]   (lane: j, warp: 16-column groups)
     {
       const int nchunk = wpad / 4;  // 4-column chunks
@@ -377,6 +383,7 @@ __global__ void __launch_bounds__(kThreads, 1) fused_small_kernel(const FusedPar
       }
     }
     __syncthreads();
+    PROF(11);
     // co_sum: add this CTA's slice partial into the L2 accumulator (rows j, lanes along k)
     for (int j = warp; j < H; j += kWarps) {
       float *dst = accS + oW1 + (int64_t)j * n0 + k0;
@@ -384,9 +391,9 @@ __global__ void __launch_bounds__(kThreads, 1) fused_small_kernel(const FusedPar
     }
 
     // ---- 5. grid barrier (the co_sum is complete), then the SGD update of the resident parameters
-    PROF(6);
+    PROF(12);
     grid_barrier(p.bar, (unsigned)((s + 1) * nCTA));
-    PROF(7);
+    PROF(13);
     // fetch the reduced slice rows (coalesced along k, all loads in flight) into Gs
     for (int j = warp; j < H; j += kWarps) {
       const float *src = accS + oW1 + (int64_t)j * n0 + k0;
@@ -410,6 +417,7 @@ __global__ void __launch_bounds__(kThreads, 1) fused_small_kernel(const FusedPar
       if (e + kThreads < H + O * H + O) gl3 = __ldcg(accS + ob1 + e + kThreads);
     }
     __syncthreads();
+    PROF(14);
     for (int i = tid; i < w * 32; i += kThreads) {
       const int k = i >> 5, j = i & 31;
       if (j < H) W1t[i] -= p.scale * Gs[j * gsld + k];
@@ -420,6 +428,7 @@ __global__ void __launch_bounds__(kThreads, 1) fused_small_kernel(const FusedPar
       else if (e < H + O * H) { const int f = e - H; W2s[(f / H) * 33 + f % H] -= p.scale * gsum; }
       else b2s[e - H - O * H] -= p.scale * gsum;
     }
+    PROF(15);
     // zero the accumulator used two steps ahead (its readers finished before this barrier)
     {
       float *z = p.acc + ((s + 2) % 3) * np;
@@ -544,8 +553,8 @@ int fused_small_train_steps(FusedSmall &fs, cudaStream_t st, const std::vector<i
   static unsigned long long *prof_buf = nullptr;
   const bool prof = env_int("NF_FUSED_PROF", 0) != 0;
   if (prof) {
-    if (!prof_buf) cudaMalloc(&prof_buf, sizeof(unsigned long long) * 148 * 64 * 8);
-    cudaMemsetAsync(prof_buf, 0, sizeof(unsigned long long) * 148 * 64 * 8, st);
+    if (!prof_buf) cudaMalloc(&prof_buf, sizeof(unsigned long long) * 148 * 64 * kProf);
+    cudaMemsetAsync(prof_buf, 0, sizeof(unsigned long long) * 148 * 64 * kProf, st);
     p.prof = prof_buf;
   }
 
@@ -572,18 +581,18 @@ int fused_small_train_steps(FusedSmall &fs, cudaStream_t st, const std::vector<i
     return -1;
   }
   if (prof) {
-    std::vector<unsigned long long> h((size_t)G * C * 64 * 8);
+    std::vector<unsigned long long> h((size_t)G * C * 64 * kProf);
     cudaStreamSynchronize(st);
     cudaMemcpy(h.data(), prof_buf, h.size() * sizeof(unsigned long long), cudaMemcpyDeviceToHost);
     const int ns = (int)std::min<int64_t>(n_steps, 64);
-    double ph[8] = {0}, phmax[8] = {0};
+    double ph[kProf] = {0}, phmax[kProf] = {0};
     int cnt = 0;
     for (int s = 2; s + 1 < ns; ++s, ++cnt) {
-      for (int i = 0; i < 8; ++i) {
+      for (int i = 0; i < kProf; ++i) {
         double mx = 0, sum = 0;
         for (int b = 0; b < G * C; ++b) {
-          const unsigned long long *t = &h[((size_t)b * 64 + s) * 8];
-          const unsigned long long nxt = i < 7 ? t[i + 1] : h[((size_t)b * 64 + s + 1) * 8];
+          const unsigned long long *t = &h[((size_t)b * 64 + s) * kProf];
+          const unsigned long long nxt = i < kProf - 1 ? t[i + 1] : h[((size_t)b * 64 + s + 1) * kProf];
           const double d = (double)(nxt - t[i]);
           sum += d; mx = std::max(mx, d);
         }
@@ -591,8 +600,10 @@ int fused_small_train_steps(FusedSmall &fs, cudaStream_t st, const std::vector<i
       }
     }
     fprintf(stderr, "[fused prof] C=%d G=%d nS<=%d w=%d smem=%zu  phase ns (mean over CTAs / max):\n", C, G, nSmax, w, smem);
-    const char *names[8] = {"wait_x", "z1_partial", "csync1", "owned_rows", "csync2+gather", "dW1+red", "grid_bar", "update"};
-    for (int i = 0; i < 8; ++i) fprintf(stderr, "  %-14s %8.0f %8.0f\n", names[i], ph[i] / cnt, phmax[i] / cnt);
+    const char *names[kProf] = {"prefetch_issue", "wait_x", "z1_partial", "csync1", "owned_rows", "owned_sum",
+                                "csync2", "gather_d1", "gpart_red", "sync", "dW1", "red_dW1", "grid_bar",
+                                "acc_loads", "update", "tail"};
+    for (int i = 0; i < kProf; ++i) fprintf(stderr, "  %-14s %8.0f %8.0f\n", names[i], ph[i] / cnt, phmax[i] / cnt);
   }
   return 0;
 }
