@@ -4,7 +4,7 @@ training of a dense feed-forward network, behind the C-ABI of ``include/nf.h``.
 This module is a thin ctypes binding: argument marshalling only.  Every step of
 the method runs in the CUDA kernels of ``libnf_b200.so`` (built in-tree by
 ``paper_1902_06714_b200.build``).  There is no CPU fallback: if the library is
-missing, importing raises; if no sm_100 GPU is present, ``nf_net_create``
+missing, the first call raises ImportError; if no sm_100 GPU is present, ``nf_net_create``
 fails with ``NF_ENODEV``.
 
 The functions carry the C names (``nf_net_create``, ``nf_output``,
@@ -62,7 +62,17 @@ def _load() -> ctypes.CDLL:
     return lib
 
 
-_lib = _load()
+_lib = None
+
+
+def lib() -> ctypes.CDLL:
+    """The loaded libnf_b200.so.  Loaded on first use so that the build step can import
+    ``paper_1902_06714_b200.build`` before the library exists; every C call goes through
+    here and raises ImportError when the library is missing (no CPU fallback)."""
+    global _lib
+    if _lib is None:
+        _lib = _load()
+    return _lib
 
 # Every symbol include/nf.h declares (checked by tests/test_abi.py).
 EXPORTS = ("nf_net_create", "nf_net_destroy", "nf_set_stream", "nf_set_math", "nf_param_count",
@@ -70,13 +80,9 @@ EXPORTS = ("nf_net_create", "nf_net_destroy", "nf_set_stream", "nf_set_math", "n
            "nf_grad", "nf_loss", "nf_accuracy", "nf_last_error", "nf_launch_count")
 
 
-def lib() -> ctypes.CDLL:
-    return _lib
-
-
 def _check(rc: int):
     if rc != NF_OK:
-        raise NFError(rc, _lib.nf_last_error().decode())
+        raise NFError(rc, lib().nf_last_error().decode())
 
 
 def _ptr(a, dtype=np.float32):
@@ -98,72 +104,72 @@ def _ptr(a, dtype=np.float32):
 def nf_net_create(dims, activation: str = "sigmoid", seed: int = 0):
     d = np.ascontiguousarray(np.asarray(dims, dtype=np.int32))
     out = ctypes.c_void_p()
-    _check(_lib.nf_net_create(d.ctypes.data_as(ctypes.c_void_p), len(d),
+    _check(lib().nf_net_create(d.ctypes.data_as(ctypes.c_void_p), len(d),
                               None if activation is None else activation.encode(), seed, ctypes.byref(out)))
     return out
 
 
 def nf_net_destroy(net):
-    _lib.nf_net_destroy(net)
+    lib().nf_net_destroy(net)
 
 
 def nf_set_stream(net, stream):
     """stream: a torch.cuda.Stream, a raw cudaStream_t int, or None (legacy default)."""
     h = getattr(stream, "cuda_stream", stream)
-    _check(_lib.nf_set_stream(net, ctypes.c_void_p(h or 0)))
+    _check(lib().nf_set_stream(net, ctypes.c_void_p(h or 0)))
 
 
 def nf_set_math(net, mode: int):
-    _check(_lib.nf_set_math(net, mode))
+    _check(lib().nf_set_math(net, mode))
 
 
 def nf_param_count(net) -> int:
-    return int(_lib.nf_param_count(net))
+    return int(lib().nf_param_count(net))
 
 
 def nf_get_params(net, dst):
-    _check(_lib.nf_get_params(net, _ptr(dst), _numel(dst)))
+    _check(lib().nf_get_params(net, _ptr(dst), _numel(dst)))
 
 
 def nf_set_params(net, src):
-    _check(_lib.nf_set_params(net, _ptr(src), _numel(src)))
+    _check(lib().nf_set_params(net, _ptr(src), _numel(src)))
 
 
 def nf_output(net, x, n: int, out):
-    _check(_lib.nf_output(net, _ptr(x), n, _ptr(out)))
+    _check(lib().nf_output(net, _ptr(x), n, _ptr(out)))
 
 
 def nf_train_batch(net, x, y, n: int, eta: float):
-    _check(_lib.nf_train_batch(net, _ptr(x), _ptr(y), n, eta))
+    _check(lib().nf_train_batch(net, _ptr(x), _ptr(y), n, eta))
 
 
 def nf_train_steps(net, X, Y, N: int, batch: int, starts, n_steps: int, eta: float, step_loss=None):
-    _check(_lib.nf_train_steps(net, _ptr(X), _ptr(Y), N, batch, _ptr(starts, np.int64), n_steps, eta,
+    _check(lib().nf_train_steps(net, _ptr(X), _ptr(Y), N, batch, _ptr(starts, np.int64), n_steps, eta,
                                _ptr(step_loss)))
 
 
 def nf_grad(net, x, y, n: int, grad):
-    _check(_lib.nf_grad(net, _ptr(x), _ptr(y), n, _ptr(grad)))
+    _check(lib().nf_grad(net, _ptr(x), _ptr(y), n, _ptr(grad)))
 
 
 def nf_loss(net, x, y, n: int) -> float:
     v = ctypes.c_float()
-    _check(_lib.nf_loss(net, _ptr(x), _ptr(y), n, ctypes.byref(v)))
+    _check(lib().nf_loss(net, _ptr(x), _ptr(y), n, ctypes.byref(v)))
     return v.value
 
 
 def nf_accuracy(net, x, y, n: int) -> float:
     v = ctypes.c_float()
-    _check(_lib.nf_accuracy(net, _ptr(x), _ptr(y), n, ctypes.byref(v)))
+    _check(lib().nf_accuracy(net, _ptr(x), _ptr(y), n, ctypes.byref(v)))
     return v.value
 
 
 def nf_last_error() -> str:
-    return _lib.nf_last_error().decode()
+    return lib().nf_last_error().decode()
 
 
 def nf_launch_count() -> int:
-    return int(_lib.nf_launch_count())
+    return int(lib().nf_launch_count())
 
 
 def _numel(a) -> int:
