@@ -293,6 +293,7 @@ int nf_set_math(nf_net *net, int mode) {
   if (int rc = check_net(net)) return rc;
   if (mode != NF_MATH_FP32 && mode != NF_MATH_TF32) return fail(NF_EINVAL, "unknown math mode %d", mode);
   net->math = mode;
+  net->ws.math = mode;
   return NF_OK;
 }
 

@@ -1,17 +1,36 @@
-// gemm_tc.cuh -- tcgen05 (5th-gen tensor core) TF32 contraction for sm_100a with
-// fused epilogues: the wide-layer path of the three GEMM-shaped steps of the
-// method in NF_MATH_TF32 mode.
+// gemm_tc.cuh -- tcgen05 (5th-gen tensor core) contraction for sm_100a with fused
+// epilogues: the wide-layer path of the three GEMM-shaped steps of the method
+// (fwdprop P:324-361, backprop P:391-427, the batch-summed
+// tendencies of train_batch P:460-476):
 //
-//   C[M][N] = sum_k A[m][k] * B[n][k]      (both operands K-major, fp32 in HBM,
-//                                           TF32 multiply, fp32 accumulate in TMEM)
+//   C[m][n] = sum_k A(m,k) * B(n,k)        fp32 operands in HBM, TF32 tensor-core
+//                                           multiplies, fp32 accumulation in TMEM
 //
-// One CTA computes one BM x BN tile.  Warp roles (192 threads):
-//   warp 0      TMA producer: 2-D tensor-map loads of A/B K-blocks (SWIZZLE_128B)
-//               into a STAGES-deep shared-memory ring (mbarrier full/empty pairs)
-//   warp 1      TMEM allocator + single-thread tcgen05.mma issuer; tcgen05.commit
-//               releases ring slots and finally signals the accumulator
-//   warps 2..5  epilogue: tcgen05.ld 32x32b.x32 (one TMEM lane = one tile row per
-//               thread, 32 columns per load) -> functor(m, n, v[32])
+//   K1 forward   Z_l = A_{l-1} W_l^T       A K-major [M][K], B K-major [N][K]
+//   K3 backward  D_l = D_{l+1} W_{l+1}     A K-major,        B N-major [K][N]
+//   K4 gradient  G_l = D_l^T A_{l-1}       A M-major [K][M], B N-major [K][N]
+//
+// Numerics (reading R13 of DESIGN.md): SPLIT = 1 is plain TF32 (NF_MATH_TF32).
+// SPLIT = 3 is 3xTF32 for the fp32 mode: every staged tile x is split in shared memory
+// into hi = x with the low 13 mantissa bits cleared (an exact TF32 value, written back in
+// place) and lo = x - hi (exact in fp32), and each K-step issues hi*hi + hi*lo + lo*hi.
+//
+// One CTA computes one BM x BN tile (optionally one K-chunk of it: split-K writes raw
+// partials that splitk_epilogue sums in fixed order).  Warp roles (192 threads):
+//   warp 0      TMA producer: 2-D tensor-map loads (SWIZZLE_128B) into a STAGES-deep ring
+//   warp 1      TMEM allocator + single-thread tcgen05.mma issuer; tcgen05.commit frees
+//               ring slots and finally signals the accumulator
+//   warps 2..5  (SPLIT = 3) hi/lo splitters during the main loop; then the epilogue:
+//               tcgen05.ld 32x32b.x32 (thread = tile row), transpose through shared memory
+//               so that a warp touches 32 consecutive columns of one row per access
+//               (coalesced), then epi(m, n, value).
+//
+// Shared-memory operand layouts (UMMA canonical forms, SWIZZLE_128B):
+//   K-major : TMA box {32 k, rows}: row r at r*128 B, 8-row groups 1024 B apart (SBO);
+//             the MMA's K = 8 step advances the start address by 32 B inside the row.
+//   MN-major: rows/32 TMA boxes {32 mn, 32 k}, each 4 KB: k-row at k*128 B; 32-element
+//             MN blocks 4096 B apart (LBO); 8-k-row groups 1024 B apart (SBO); the K = 8
+//             step advances the start address by one 1024 B group.
 #pragma once
 #include <cstdint>
 
@@ -22,34 +41,45 @@ namespace nf {
 namespace tc {
 
 constexpr int BM = 128;
-constexpr int BK = 32;              // 32 fp32 = 128 B = one SWIZZLE_128B atom along K
+constexpr int BK = 32;              // 32 fp32 = 128 B = one SWIZZLE_128B row
 constexpr int kThreads = 192;
+constexpr int kSmemBudget = 232448; // max dynamic shared memory per CTA on sm_100
+constexpr int kEpiBytes = 4 * 32 * 33 * 4;
 
-template <int BN>
+template <int BN, int SPLIT>
 struct Cfg {
   static constexpr int A_BYTES = BM * BK * 4;
   static constexpr int B_BYTES = BN * BK * 4;
-  static constexpr int STAGE_BYTES = A_BYTES + B_BYTES;
-  static constexpr int STAGES = (200 * 1024) / STAGE_BYTES;  // 4 for BN=256, 6 for BN=128
-  static constexpr int TMEM_COLS = BN;                        // fp32 accumulator: 1 column per n
-  static constexpr int SMEM = STAGES * STAGE_BYTES + 1024 /*align*/ + 256 /*barriers*/;
+  static constexpr int RAW_BYTES = A_BYTES + B_BYTES;
+  static constexpr int STAGE_BYTES = SPLIT == 3 ? 2 * RAW_BYTES : RAW_BYTES;  // raw(hi) | lo
+  static constexpr int STAGES_FIT = (kSmemBudget - kEpiBytes - 1024 - 512) / STAGE_BYTES;
+  static constexpr int STAGES = STAGES_FIT > 6 ? 6 : STAGES_FIT;
+  static constexpr int TMEM_COLS = BN;
+  static constexpr int SMEM = STAGES * STAGE_BYTES + kEpiBytes + 1024 /*align*/ + 512 /*barriers*/;
+  static_assert(STAGES >= 2, "ring too shallow");
 };
 
-// ---- descriptors ------------------------------------------------------------------
-// Shared-memory matrix descriptor, K-major, SWIZZLE_128B: rows of 128 B, 8-row groups
-// 1024 B apart (SBO); LBO unused for swizzled K-major; version 1 (sm_100).
-__device__ __forceinline__ uint64_t smem_desc_k_sw128(uint32_t saddr) {
+// ---- descriptors ---------------------------------------------------------------------
+// Shared-memory matrix descriptor (sm_100 version 1), SWIZZLE_128B.
+__device__ __forceinline__ uint64_t smem_desc_sw128(uint32_t saddr, uint32_t lbo, uint32_t sbo) {
   uint64_t d = 0;
   d |= (uint64_t)((saddr >> 4) & 0x3FFF);
-  d |= (uint64_t)1 << 16;                    // LBO (ignored)
-  d |= (uint64_t)(1024 >> 4) << 32;          // SBO
+  d |= (uint64_t)((lbo >> 4) & 0x3FFF) << 16;
+  d |= (uint64_t)((sbo >> 4) & 0x3FFF) << 32;
   d |= (uint64_t)1 << 46;                    // version
   d |= (uint64_t)2 << 61;                    // SWIZZLE_128B
   return d;
 }
-// Instruction descriptor: D fp32, A/B tf32, both K-major, M x N.
-__host__ __device__ constexpr uint32_t idesc_tf32(int M, int N) {
-  return (1u << 4) | (2u << 7) | (2u << 10) | ((uint32_t)(N >> 3) << 17) | ((uint32_t)(M >> 4) << 24);
+// Operand descriptor for K-step `ks` (K = 8 tf32 each) of a staged tile.
+template <bool MN>
+__device__ __forceinline__ uint64_t op_desc(uint32_t base, int ks) {
+  if (MN) return smem_desc_sw128(base + 1024u * ks, BK * 128, 1024);
+  return smem_desc_sw128(base + 32u * ks, 16, 1024);
+}
+// Instruction descriptor: D fp32, A/B tf32, majors, M x N.
+__host__ __device__ constexpr uint32_t idesc_tf32(int M, int N, bool a_mn, bool b_mn) {
+  return (1u << 4) | (2u << 7) | (2u << 10) | ((a_mn ? 1u : 0u) << 15) | ((b_mn ? 1u : 0u) << 16) |
+         ((uint32_t)(N >> 3) << 17) | ((uint32_t)(M >> 4) << 24);
 }
 
 __device__ __forceinline__ void mma_tf32(uint32_t tmem_d, uint64_t da, uint64_t db, uint32_t idesc, uint32_t acc) {
@@ -81,35 +111,41 @@ __device__ __forceinline__ void tmem_ld32(uint32_t taddr, float (&v)[32]) {
   for (int i = 0; i < 32; ++i) v[i] = __uint_as_float(r[i]);
 }
 
-__device__ __forceinline__ float round_tf32(float x) {
-  uint32_t r;
-  asm("cvt.rna.tf32.f32 %0, %1;" : "=r"(r) : "f"(x));
-  return __uint_as_float(r);
-}
+// TF32 part of x by truncation (low 13 mantissa bits cleared): exact as a TF32 operand.
+__device__ __forceinline__ float tf32_hi(float x) { return __uint_as_float(__float_as_uint(x) & 0xFFFFE000u); }
+
+struct TileArgs {
+  int M, N, K;
+  int kchunk;          // K range per blockIdx.z (multiple of BK)
+  float *partial;      // non-null: write raw partials [z][M][N] (split-K) instead of epi
+};
 
 // ---- the kernel ------------------------------------------------------------------------
-// Epi: __device__ void operator()(int m, int n, const float (&v)[32]) const -- row m,
-// columns n..n+31 (caller guarantees m < M; columns >= N must be ignored by the functor).
-template <int BN, class Epi>
+template <int BN, bool A_MN, bool B_MN, int SPLIT, class Epi>
 __global__ void __launch_bounds__(kThreads, 1)
-gemm_tc_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB, int M, int N,
-               int K, Epi epi) {
-  using C = Cfg<BN>;
+gemm_tc_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB, TileArgs g,
+               Epi epi) {
+  using C = Cfg<BN, SPLIT>;
   extern __shared__ uint8_t smem_raw[];
   uint8_t *smem = reinterpret_cast<uint8_t *>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
-  uint64_t *full = reinterpret_cast<uint64_t *>(smem + C::STAGES * C::STAGE_BYTES);
+  float *epibuf = reinterpret_cast<float *>(smem + C::STAGES * C::STAGE_BYTES);
+  uint64_t *full = reinterpret_cast<uint64_t *>(smem + C::STAGES * C::STAGE_BYTES + kEpiBytes);
   uint64_t *empty = full + C::STAGES;
-  uint64_t *accum = empty + C::STAGES;
+  uint64_t *conv = empty + C::STAGES;
+  uint64_t *accum = conv + C::STAGES;
   uint32_t *tmem_slot = reinterpret_cast<uint32_t *>(accum + 1);
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int n0 = blockIdx.x * BN, m0 = blockIdx.y * BM;
-  const int nkb = (K + BK - 1) / BK;
+  const int kbeg = blockIdx.z * g.kchunk;
+  const int kend = min(g.K, kbeg + g.kchunk);
+  const int nkb = (kend - kbeg + BK - 1) / BK;
 
   if (threadIdx.x == 0) {
     for (int s = 0; s < C::STAGES; ++s) {
       ptx::mbar_init(&full[s], 1);
       ptx::mbar_init(&empty[s], 1);
+      ptx::mbar_init(&conv[s], 4);
     }
     ptx::mbar_init(accum, 1);
     ptx::fence_mbar_init();
@@ -128,45 +164,98 @@ gemm_tc_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ 
 
   if (warp == 0) {
     if (lane == 0) {  // ---- TMA producer
-      for (int kb = 0; kb < nkb; ++kb) {
-        const int s = kb % C::STAGES;
-        if (kb >= C::STAGES) ptx::mbar_wait(&empty[s], (uint32_t)(((kb / C::STAGES) - 1) & 1));
+      for (int it = 0; it < nkb; ++it) {
+        const int s = it % C::STAGES;
+        if (it >= C::STAGES) ptx::mbar_wait(&empty[s], (uint32_t)(((it / C::STAGES) - 1) & 1));
         uint8_t *sa = smem + s * C::STAGE_BYTES;
         uint8_t *sb = sa + C::A_BYTES;
-        ptx::mbar_arrive_expect_tx(&full[s], (uint32_t)C::STAGE_BYTES);
-        ptx::tma_load_2d(sa, &tmA, &full[s], kb * BK, m0);
-        ptx::tma_load_2d(sb, &tmB, &full[s], kb * BK, n0);
+        const int k = kbeg + it * BK;
+        ptx::mbar_arrive_expect_tx(&full[s], (uint32_t)C::RAW_BYTES);
+        if (A_MN) {
+#pragma unroll
+          for (int i = 0; i < BM / 32; ++i) ptx::tma_load_2d(sa + i * 4096, &tmA, &full[s], m0 + 32 * i, k);
+        } else {
+          ptx::tma_load_2d(sa, &tmA, &full[s], k, m0);
+        }
+        if (B_MN) {
+#pragma unroll
+          for (int i = 0; i < BN / 32; ++i) ptx::tma_load_2d(sb + i * 4096, &tmB, &full[s], n0 + 32 * i, k);
+        } else {
+          ptx::tma_load_2d(sb, &tmB, &full[s], k, n0);
+        }
       }
     }
   } else if (warp == 1) {
     if (lane == 0) {  // ---- MMA issuer
-      const uint32_t idesc = idesc_tf32(BM, BN);
-      for (int kb = 0; kb < nkb; ++kb) {
-        const int s = kb % C::STAGES;
-        ptx::mbar_wait(&full[s], (uint32_t)((kb / C::STAGES) & 1));
+      constexpr uint32_t idesc = idesc_tf32(BM, BN, A_MN, B_MN);
+      for (int it = 0; it < nkb; ++it) {
+        const int s = it % C::STAGES;
+        const uint32_t par = (uint32_t)((it / C::STAGES) & 1);
+        ptx::mbar_wait(SPLIT == 3 ? &conv[s] : &full[s], par);
         tc_fence_after();
         const uint32_t sa = ptx::smem_u32(smem + s * C::STAGE_BYTES);
         const uint32_t sb = sa + C::A_BYTES;
 #pragma unroll
-        for (int k = 0; k < BK / 8; ++k)  // K = 8 tf32 (32 B) per MMA: advance inside the 128-B atom
-          mma_tf32(tmem, smem_desc_k_sw128(sa + 32 * k), smem_desc_k_sw128(sb + 32 * k), idesc,
-                   (kb | k) != 0 ? 1u : 0u);
+        for (int ks = 0; ks < BK / 8; ++ks) {
+          const uint64_t ah = op_desc<A_MN>(sa, ks), bh = op_desc<B_MN>(sb, ks);
+          mma_tf32(tmem, ah, bh, idesc, (it | ks) != 0 ? 1u : 0u);
+          if (SPLIT == 3) {
+            const uint64_t al = op_desc<A_MN>(sa + C::RAW_BYTES, ks), bl = op_desc<B_MN>(sb + C::RAW_BYTES, ks);
+            mma_tf32(tmem, ah, bl, idesc, 1u);
+            mma_tf32(tmem, al, bh, idesc, 1u);
+          }
+        }
         mma_commit(&empty[s]);
       }
       mma_commit(accum);
     }
-  } else {  // ---- epilogue warps 2..5: TMEM lane quadrant = warp % 4
+  } else {
+    const int t = threadIdx.x - 64;  // 0..127
+    if (SPLIT == 3) {  // ---- hi/lo splitters
+      for (int it = 0; it < nkb; ++it) {
+        const int s = it % C::STAGES;
+        ptx::mbar_wait(&full[s], (uint32_t)((it / C::STAGES) & 1));
+        float4 *raw = reinterpret_cast<float4 *>(smem + s * C::STAGE_BYTES);
+        float4 *lo = reinterpret_cast<float4 *>(smem + s * C::STAGE_BYTES + C::RAW_BYTES);
+#pragma unroll 4
+        for (int i = t; i < C::RAW_BYTES / 16; i += 128) {
+          const float4 x = raw[i];
+          const float4 h = make_float4(tf32_hi(x.x), tf32_hi(x.y), tf32_hi(x.z), tf32_hi(x.w));
+          raw[i] = h;
+          lo[i] = make_float4(x.x - h.x, x.y - h.y, x.z - h.z, x.w - h.w);
+        }
+        ptx::fence_proxy_async_smem();
+        __syncwarp();
+        if (lane == 0) ptx::mbar_arrive(&conv[s]);
+      }
+    }
+    // ---- epilogue: TMEM lane quadrant = warp % 4
     const int q = warp & 3;
+    float *buf = epibuf + q * 32 * 33;
     ptx::mbar_wait(accum, 0);
     tc_fence_after();
-    const int m = m0 + q * 32 + lane;
+    const int mrow0 = m0 + q * 32;
+    const int64_t MN = (int64_t)g.M * g.N;
 #pragma unroll 1
     for (int c = 0; c < BN / 32; ++c) {
-      const int n = n0 + c * 32;
-      if (n >= N) break;  // warp-uniform
+      const int nc = n0 + c * 32;
+      if (nc >= g.N) break;  // warp-uniform
       float v[32];
       tmem_ld32(tmem + ((uint32_t)(q * 32) << 16) + (uint32_t)(c * 32), v);
-      if (m < M) epi(m, n, v);
+#pragma unroll
+      for (int j = 0; j < 32; ++j) buf[lane * 33 + j] = v[j];
+      __syncwarp();
+      const int n = nc + lane;
+#pragma unroll 4
+      for (int r = 0; r < 32; ++r) {
+        const int m = mrow0 + r;
+        if (m < g.M && n < g.N) {
+          const float val = buf[r * 33 + lane];
+          if (g.partial) g.partial[blockIdx.z * MN + (int64_t)m * g.N + n] = val;
+          else epi(m, n, val);
+        }
+      }
+      __syncwarp();
     }
   }
   tc_fence_before();

@@ -2,11 +2,17 @@
 // loss/accuracy reduction (K5).
 #include <algorithm>
 
+#include <cstdlib>
+#include <cstring>
+
+#include "gemm_tc.cuh"
 #include "kernels.cuh"
 
 namespace nf {
 
 int64_t g_launches = 0;
+static thread_local Engine g_last_engine = ENGINE_SIMT;
+Engine last_engine() { return g_last_engine; }
 
 namespace {
 
@@ -60,22 +66,159 @@ cudaError_t run_gemm(cudaStream_t st, GemmArgs g, const Epi &epi, const Workspac
   }
 }
 
+// ---------------------------------------------------------------------------
+// tcgen05 path.  An operand is K-major ([rows][ld], K contiguous) or MN-major
+// ([K][ld], M or N contiguous).  TMA needs 16-B aligned bases and row pitches.
+struct TcOp {
+  const float *p;
+  int64_t ld;
+  bool mn;
+};
+
+bool tc_enabled() {
+  static int v = -1;
+  if (v < 0) {
+    const char *e = getenv("NF_DISABLE_TC");
+    v = (e && atoi(e)) ? 0 : 1;
+  }
+  return v == 1;
+}
+
+bool tc_ok(const TcOp &o) { return (reinterpret_cast<uintptr_t>(o.p) & 15) == 0 && (o.ld * 4) % 16 == 0; }
+
+// The tensor-core path is used for contractions whose three extents are all >= 64
+// (the output layer's 10-wide GEMMs stay on the SIMT kernels).
+bool use_tc(int M, int N, int K, const TcOp &a, const TcOp &b) {
+  return tc_enabled() && M >= 64 && N >= 64 && K >= 64 && tc_ok(a) && tc_ok(b);
+}
+
+bool make_map(CUtensorMap *m, const TcOp &o, int rows, int K, int box_rows) {
+  if (o.mn)  // [K][rows] with rows contiguous: box {32 mn, 32 k}
+    return encode_tmap_2d_f32(m, o.p, (uint64_t)rows, (uint64_t)K, (uint64_t)o.ld * 4, 32, tc::BK,
+                              CU_TENSOR_MAP_SWIZZLE_128B);
+  return encode_tmap_2d_f32(m, o.p, (uint64_t)K, (uint64_t)rows, (uint64_t)o.ld * 4, tc::BK, (uint32_t)box_rows,
+                            CU_TENSOR_MAP_SWIZZLE_128B);
+}
+
+template <int BN, bool AMN, bool BMN, int SPLIT, class Epi>
+cudaError_t launch_tc(cudaStream_t st, int M, int N, int K, const TcOp &a, const TcOp &b, const Epi &epi,
+                      const Workspace &ws) {
+  using C = tc::Cfg<BN, SPLIT>;
+  auto kern = tc::gemm_tc_kernel<BN, AMN, BMN, SPLIT, Epi>;
+  static bool attr = false;
+  if (!attr) {
+    cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, C::SMEM);
+    if (e != cudaSuccess) return e;
+    attr = true;
+  }
+  CUtensorMap ta, tb;
+  if (!make_map(&ta, a, M, K, tc::BM) || !make_map(&tb, b, N, K, BN)) return cudaErrorInvalidValue;
+  const int tm = (M + tc::BM - 1) / tc::BM, tn = (N + BN - 1) / BN;
+  const int tiles = tm * tn;
+  const int nkb = (K + tc::BK - 1) / tc::BK;
+  int splits = 1;
+  if (tiles < kSMs && nkb >= 8) {
+    splits = std::min((kSMs + tiles - 1) / tiles, nkb / 4);
+    while (splits > 1 && (size_t)splits * M * N > ws.partial_floats) --splits;
+    splits = std::max(splits, 1);
+  }
+  const int kbper = (nkb + splits - 1) / splits;
+  splits = (nkb + kbper - 1) / kbper;  // no empty K-chunk
+  tc::TileArgs g{M, N, K, kbper * tc::BK, splits > 1 ? ws.partial : nullptr};
+  kern<<<dim3(tn, tm, splits), tc::kThreads, C::SMEM, st>>>(ta, tb, g, epi);
+  count_launch();
+  if (splits > 1) {
+    const int64_t MN = (int64_t)M * N;
+    const int blocks = (int)std::min<int64_t>((MN + 255) / 256, 4 * kSMs);
+    splitk_epilogue<Epi><<<blocks, 256, 0, st>>>(ws.partial, splits, M, N, epi);
+    count_launch();
+  }
+  return cudaGetLastError();
+}
+
+template <bool AMN, bool BMN, class Epi>
+cudaError_t run_tc(cudaStream_t st, int M, int N, int K, const TcOp &a, const TcOp &b, const Epi &epi,
+                   const Workspace &ws) {
+  if (ws.math == 1) {
+    g_last_engine = ENGINE_TC1;
+    if (N > 128) return launch_tc<256, AMN, BMN, 1>(st, M, N, K, a, b, epi, ws);
+    return launch_tc<128, AMN, BMN, 1>(st, M, N, K, a, b, epi, ws);
+  }
+  g_last_engine = ENGINE_TC3;
+  return launch_tc<128, AMN, BMN, 3>(st, M, N, K, a, b, epi, ws);
+}
+
+// Bias tendency g[i] = sum_r D[r][i] over n rows (the ones-column of the SIMT path),
+// row chunks summed in a fixed order, then the same EpiGrad bias element update.
+__global__ void __launch_bounds__(256)
+colsum_partial(const float *__restrict__ D, int64_t rows, int cols, int chunk, float *__restrict__ part) {
+  const int c = blockIdx.x * 256 + threadIdx.x;
+  if (c >= cols) return;
+  const int64_t r0 = (int64_t)blockIdx.y * chunk, r1 = min(rows, r0 + chunk);
+  float s0 = 0.f, s1 = 0.f, s2 = 0.f, s3 = 0.f;
+  int64_t r = r0;
+  for (; r + 4 <= r1; r += 4) {
+    s0 += D[r * cols + c];
+    s1 += D[(r + 1) * cols + c];
+    s2 += D[(r + 2) * cols + c];
+    s3 += D[(r + 3) * cols + c];
+  }
+  for (; r < r1; ++r) s0 += D[r * cols + c];
+  part[(int64_t)blockIdx.y * cols + c] = (s0 + s1) + (s2 + s3);
+}
+
+__global__ void __launch_bounds__(256)
+colsum_final(const float *__restrict__ part, int nchunks, int cols, EpiGrad epi) {
+  const int c = blockIdx.x * 256 + threadIdx.x;
+  if (c >= cols) return;
+  float s = 0.f;
+  for (int z = 0; z < nchunks; ++z) s += part[(int64_t)z * cols + c];
+  epi(c, epi.nreal, s);  // column nreal of the [M][N+1] gradient = the bias
+}
+
+cudaError_t bias_grad(cudaStream_t st, const float *D, int64_t rows, int cols, const EpiGrad &epi,
+                      float *part, size_t part_floats) {
+  int nchunks = (int)std::min<int64_t>((rows + 255) / 256, 64);
+  while (nchunks > 1 && (size_t)nchunks * cols > part_floats) --nchunks;
+  const int chunk = (int)((rows + nchunks - 1) / nchunks);
+  const dim3 grid((cols + 255) / 256, nchunks);
+  colsum_partial<<<grid, 256, 0, st>>>(D, rows, cols, chunk, part);
+  colsum_final<<<(cols + 255) / 256, 256, 0, st>>>(part, nchunks, cols, epi);
+  count_launch(2);
+  return cudaGetLastError();
+}
+
 }  // namespace
 
 cudaError_t gemm_fwd(cudaStream_t st, int M, int N, int K, const float *A, const float *W,
                      const EpiFwd &epi, const Workspace &ws) {
+  const TcOp a{A, K, false}, b{W, K, false};
+  if (use_tc(M, N, K, a, b)) return run_tc<false, false>(st, M, N, K, a, b, epi, ws);
+  g_last_engine = ENGINE_SIMT;
   GemmArgs g{M, N, K, A, K, W, K, N, 0, nullptr};
   return run_gemm<true, true>(st, g, epi, ws);
 }
 
 cudaError_t gemm_bwd(cudaStream_t st, int M, int N, int K, const float *D, const float *W,
                      const EpiBwd &epi, const Workspace &ws) {
+  const TcOp a{D, K, false}, b{W, N, true};
+  if (use_tc(M, N, K, a, b)) return run_tc<false, true>(st, M, N, K, a, b, epi, ws);
+  g_last_engine = ENGINE_SIMT;
   GemmArgs g{M, N, K, D, K, W, N, N, 0, nullptr};
   return run_gemm<true, false>(st, g, epi, ws);
 }
 
 cudaError_t gemm_grad(cudaStream_t st, int M, int N, int K, const float *D, const float *Aprev,
                       const EpiGrad &epi, const Workspace &ws) {
+  const TcOp a{D, M, true}, b{Aprev, N, true};
+  if (use_tc(M, N, K, a, b)) {
+    // bias tendencies first: they read D only, and the partial buffer is free again
+    // before the split-K GEMM uses it (same stream)
+    cudaError_t e = bias_grad(st, D, K, M, epi, ws.partial, ws.partial_floats);
+    if (e != cudaSuccess) return e;
+    return run_tc<true, true>(st, M, N, K, a, b, epi, ws);
+  }
+  g_last_engine = ENGINE_SIMT;
   // C[M][N+1]: column N is the ones column -> bias gradient.
   GemmArgs g{M, N + 1, K, D, M, Aprev, N, N, 0, nullptr};
   return run_gemm<false, false>(st, g, epi, ws);

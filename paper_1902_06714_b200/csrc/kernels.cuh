@@ -11,11 +11,18 @@ namespace nf {
 extern int64_t g_launches;  // kernels launched by this library (nf_launch_count)
 inline void count_launch(int n = 1) { __atomic_add_fetch(&g_launches, n, __ATOMIC_RELAXED); }
 
-// Split-K partial workspace owned by the net (fixed capacity in floats).
+// Split-K partial workspace owned by the net (fixed capacity in floats) and the numerics
+// mode of the contractions (NF_MATH_FP32 = 0: fp32 SIMT or 3xTF32 tensor cores;
+// NF_MATH_TF32 = 1: 1xTF32 tensor cores where a GEMM qualifies).
 struct Workspace {
   float *partial = nullptr;
   size_t partial_floats = 0;
+  int math = 0;
 };
+
+// Which engine ran the last gemm_* call (for tests / the bench's kernel attribution).
+enum Engine { ENGINE_SIMT = 0, ENGINE_TC1 = 1, ENGINE_TC3 = 3 };
+Engine last_engine();
 
 // K1: Z = A[M][K] * W[N][K]^T, epilogue EpiFwd.
 cudaError_t gemm_fwd(cudaStream_t st, int M, int N, int K, const float *A, const float *W,

@@ -1,0 +1,108 @@
+"""GPU parity of the tcgen05 tensor-core contractions (gemm_tc.cuh) through the C-ABI (-m gpu).
+
+Shapes are chosen so that every contraction with all extents >= 64 takes the tensor-core
+path: K1 (both operands K-major), K3 (B operand N-major), K4 (both operands MN-major),
+with ragged tile tails in M, N and K and split-K over the batch.  NF_MATH_FP32 runs them
+as 3xTF32 (bar 1e-4), NF_MATH_TF32 as 1xTF32 (bar 5e-3), both against the fp64 oracle.
+"""
+import numpy as np
+import pytest
+import torch
+
+import oracle
+import synth
+from parity import FP32_BAR, TF32_BAR, argmax_agree, rel_err
+
+pytestmark = pytest.mark.gpu
+
+import paper_1902_06714_b200 as nf  # noqa: E402
+
+TC_SHAPES = [
+    ([200, 136, 72, 5], "tanh", 300),          # ragged M/N/K tails in every GEMM
+    ([256, 128, 64], "sigmoid", 4096),         # K4: few tiles, K = 4096 -> split-K
+    ([516, 260, 132, 3], "gaussian,sigmoid", 333),
+    ([784, 1024, 1024, 10], "tanh", 256),      # config-3 widths
+]
+
+
+def dev(a):
+    return torch.from_numpy(np.ascontiguousarray(a)).cuda()
+
+
+def make_net(dims, act, params, math):
+    net = nf.Net(dims, act)
+    net.set_math(math)
+    net.set_params(dev(params.astype(np.float32)))
+    return net
+
+
+def gpu_params(net):
+    out = torch.empty(net.n_params, dtype=torch.float32, device="cuda")
+    net.get_params(out)
+    torch.cuda.synchronize()
+    return out.cpu().numpy()
+
+
+@pytest.mark.parametrize("math,bar", [(nf.NF_MATH_FP32, FP32_BAR), (nf.NF_MATH_TF32, TF32_BAR)])
+@pytest.mark.parametrize("dims,act,n", TC_SHAPES)
+def test_tc_output(dims, act, n, math, bar):
+    p = synth.random_params(len(dims) * 3 + n, dims, 1.0 / np.sqrt(max(dims)))
+    x, _ = synth.random_batch(n, n, dims[0], dims[-1], "normal")
+    net = make_net(dims, act, p, math)
+    out = net.output(dev(x)).cpu().numpy()
+    ref = oracle.Oracle(dims, act).output(p, x)
+    assert rel_err(out, ref) <= bar
+    if math == nf.NF_MATH_FP32:
+        assert argmax_agree(out, ref)[0] == 0
+
+
+@pytest.mark.parametrize("math,bar", [(nf.NF_MATH_FP32, FP32_BAR), (nf.NF_MATH_TF32, TF32_BAR)])
+@pytest.mark.parametrize("dims,act,n", TC_SHAPES)
+def test_tc_grad(dims, act, n, math, bar):
+    p = synth.random_params(len(dims) * 5 + n, dims, 1.0 / np.sqrt(max(dims)))
+    x, y = synth.random_batch(n + 3, n, dims[0], dims[-1], "uniform")
+    net = make_net(dims, act, p, math)
+    g = net.grad(dev(x), dev(y)).cpu().numpy()
+    o = oracle.Oracle(dims, act)
+    ref = o.grad(p, x, y)
+    for (Wg, bg), (Wr, br) in zip(o.layers(g), o.layers(ref)):
+        assert rel_err(Wg, Wr) <= bar
+        assert rel_err(bg, br) <= bar
+
+
+@pytest.mark.parametrize("math,bar", [(nf.NF_MATH_FP32, FP32_BAR), (nf.NF_MATH_TF32, TF32_BAR)])
+@pytest.mark.parametrize("dims,act,n", TC_SHAPES[:3])
+def test_tc_train_batch(dims, act, n, math, bar):
+    p = synth.random_params(len(dims) * 9 + n, dims, 1.0 / np.sqrt(max(dims)))
+    x, y = synth.random_batch(n + 4, n, dims[0], dims[-1], "uniform")
+    net = make_net(dims, act, p, math)
+    net.train_batch(dev(x), dev(y), 0.5)
+    o = oracle.Oracle(dims, act)
+    ref, _ = o.train_batch(p, x, y, 0.5)
+    got = gpu_params(net)
+    for (Wg, bg), (Wr, br) in zip(o.layers(got), o.layers(ref)):
+        assert rel_err(Wg, Wr) <= bar
+        assert rel_err(bg, br) <= bar
+    # the update itself (W' - W) carries the contraction error undiluted by W
+    for (Wg, _), (Wr, _), (W0, _) in zip(o.layers(got), o.layers(ref), o.layers(p.astype(np.float64))):
+        assert rel_err(Wg - W0, Wr - W0) <= (1e-3 if math == nf.NF_MATH_FP32 else 2e-2)
+
+
+def test_tc_c5_full_width_grad():
+    """Config-5 widths on 64 rows: every layer of K1/K3/K4 at 4096/1024 widths on the
+    tensor cores (3xTF32, fp32 mode); rows with relu pre-activations inside the rounding
+    band are excluded (R8)."""
+    cfg = synth.CONFIGS[5]
+    dims = cfg["dims"]
+    p = synth.init_params(5)
+    X, Y = synth.dataset(5, N=80)
+    o = oracle.Oracle(dims, cfg["act"])
+    keep = o.kink_free_rows(p, X, Y)
+    X, Y = np.ascontiguousarray(X[keep][:64]), np.ascontiguousarray(Y[keep][:64])
+    assert len(X) == 64
+    net = make_net(dims, cfg["act"], p, nf.NF_MATH_FP32)
+    g = net.grad(dev(X), dev(Y)).cpu().numpy()
+    ref = o.grad(p, X, Y)
+    for (Wg, bg), (Wr, br) in zip(o.layers(g), o.layers(ref)):
+        assert rel_err(Wg, Wr) <= FP32_BAR
+        assert rel_err(bg, br) <= FP32_BAR
