@@ -189,6 +189,8 @@ def main():
     ap.add_argument("--min-seconds", type=float, default=1.0)
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--math", default="fp32", choices=["fp32", "tf32"],
+                    help="fp32: fp32 SIMT / 3xTF32 tensor cores (1e-4 parity); tf32: 1xTF32 tiles")
     args = ap.parse_args()
     if args.warmup < 3:
         ap.error("--warmup must be >= 3")
@@ -210,6 +212,7 @@ def main():
     Xd, Yd = torch.from_numpy(X).cuda(), torch.from_numpy(Y).cuda()
     stream = torch.cuda.current_stream()
     net = nf.Net(cfg["dims"], cfg["act"], stream=stream)
+    net.set_math(nf.NF_MATH_TF32 if args.math == "tf32" else nf.NF_MATH_FP32)
     net.set_params(torch.from_numpy(synth.init_params(cid)).cuda())
     loss = torch.zeros(K, device="cuda")
 
@@ -243,6 +246,11 @@ def main():
     peaks, peak_src = measured_peaks()
     alg_bytes = K * B * BYTES_PER_SAMPLE[cid]
     achieved = alg_bytes / t_med / 1e9
+    tensor_bound = len(cfg["dims"]) > 3
+    if tensor_bound:
+        # TF32 dense peak = measured bf16 x (1.1 / 2.25), the guide's nominal ratio
+        tf32_peak = peaks["bf16_tflops"] * 1.1 / 2.25
+        ach_tf = flops_per_sample(cfg["dims"]) * K * B / t_med / 1e12
     traffic = None
     prof = os.path.join(ROOT, "profiles", f"traffic_c{cid}.json")
     if os.path.exists(prof):
@@ -291,16 +299,23 @@ def main():
             "metric": "training samples/sec (fwd+bwd+SGD)",
             "value": value, "unit": "samples/s", "n_gpus": world, "steps": K, "warmup": W,
             "ms_per_step": t_max * 1e3 / K, "higher_is_better": True, "scaling": "weak",
-            "vs_baseline": None, "dtype": "f32", "data": "synthetic",
+            "vs_baseline": None, "dtype": "f32" if args.math == "fp32" else "tf32", "data": "synthetic",
             "config": {"workload": cfg["name"], "dims": cfg["dims"], "batch": B, "dataset_rows": N,
+                       "math": args.math,
                        "eta": cfg["eta"], "steps_per_timed_call": K, "reps": reps, "stat": "median rep",
                        "l2": f"dataset {X.nbytes / 1e6:.0f} MB > 126 MB L2, not flushed",
                        "parallelism": f"replicas x{world}" if world > 1 else "1 GPU"},
-            "roofline": {"bound": "hbm", "achieved": achieved, "peak": peaks["hbm_gbs"], "unit": "GB/s",
-                         "frac": achieved / peaks["hbm_gbs"], "traffic": traffic,
-                         "peak_source": f"MEASURED_PEAKS.json hbm_gbs ({peak_src})",
-                         "kernel": "fused_small_kernel" if len(cfg["dims"]) == 3 else "gemm_simt",
-                         "algorithmic_bytes_per_launch": alg_bytes},
+            "roofline": ({"bound": "tensor", "achieved": ach_tf, "peak": tf32_peak, "unit": "TFLOP/s",
+                          "frac": ach_tf / tf32_peak, "traffic": traffic,
+                          "peak_source": f"MEASURED_PEAKS.json bf16_tflops x 1.1/2.25 = TF32 dense ({peak_src})",
+                          "kernel": "whole step (gemm_tc_kernel + epilogue kernels)",
+                          "algorithmic_flops_per_step": flops_per_sample(cfg["dims"]) * B}
+                         if tensor_bound else
+                         {"bound": "hbm", "achieved": achieved, "peak": peaks["hbm_gbs"], "unit": "GB/s",
+                          "frac": achieved / peaks["hbm_gbs"], "traffic": traffic,
+                          "peak_source": f"MEASURED_PEAKS.json hbm_gbs ({peak_src})",
+                          "kernel": "fused_small_kernel",
+                          "algorithmic_bytes_per_launch": alg_bytes}),
             "flops": {"per_sample": fl, "achieved_tflops": fl * K * B / t_med / 1e12},
             "cpu_baseline": cpu,
             "e2e": e2e,

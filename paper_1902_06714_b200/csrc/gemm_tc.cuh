@@ -12,8 +12,10 @@
 //
 // Numerics (reading R13 of DESIGN.md): SPLIT = 1 is plain TF32 (NF_MATH_TF32).
 // SPLIT = 3 is 3xTF32 for the fp32 mode: every staged tile x is split in shared memory
-// into hi = x with the low 13 mantissa bits cleared (an exact TF32 value, written back in
-// place) and lo = x - hi (exact in fp32), and each K-step issues hi*hi + hi*lo + lo*hi.
+// into hi = x rounded to TF32 (written back in place) and lo = x - hi (exact in fp32), and
+// each K-step issues hi*hi + hi*lo + lo*hi.  The tensor core reads fp32 bit patterns and
+// drops the low 13 mantissa bits (truncation, measured: micro/tc_major_test.cu), which is
+// what SPLIT = 1 gets.
 //
 // One CTA computes one BM x BN tile (optionally one K-chunk of it: split-K writes raw
 // partials that splitk_epilogue sums in fixed order).  Warp roles (192 threads):
@@ -28,9 +30,10 @@
 // Shared-memory operand layouts (UMMA canonical forms, SWIZZLE_128B):
 //   K-major : TMA box {32 k, rows}: row r at r*128 B, 8-row groups 1024 B apart (SBO);
 //             the MMA's K = 8 step advances the start address by 32 B inside the row.
-//   MN-major: rows/32 TMA boxes {32 mn, 32 k}, each 4 KB: k-row at k*128 B; 32-element
-//             MN blocks 4096 B apart (LBO); 8-k-row groups 1024 B apart (SBO); the K = 8
-//             step advances the start address by one 1024 B group.
+//   MN-major: rows/32 TMA boxes {32 mn, 32 k} with the 128B_ATOM_32B swizzle, each 4 KB:
+//             k-row at k*128 B, its four 32-B chunks permuted by (k mod 4); 32-element MN
+//             blocks 4096 B apart (LBO); 4-k-row atoms 512 B apart (SBO); the K = 8 step
+//             advances the start address by 1024 B.
 #pragma once
 #include <cstdint>
 
@@ -60,21 +63,26 @@ struct Cfg {
 };
 
 // ---- descriptors ---------------------------------------------------------------------
-// Shared-memory matrix descriptor (sm_100 version 1), SWIZZLE_128B.
-__device__ __forceinline__ uint64_t smem_desc_sw128(uint32_t saddr, uint32_t lbo, uint32_t sbo) {
+// Shared-memory matrix descriptor (sm_100 version 1).  layout: 2 = SWIZZLE_128B,
+// 1 = SWIZZLE_128B_BASE32B (128-B rows, 32-B swizzle atoms: the only smem layout the
+// tensor core accepts for MN-major TF32 operands).
+__device__ __forceinline__ uint64_t smem_desc(uint32_t saddr, uint32_t lbo, uint32_t sbo, uint32_t layout) {
   uint64_t d = 0;
   d |= (uint64_t)((saddr >> 4) & 0x3FFF);
   d |= (uint64_t)((lbo >> 4) & 0x3FFF) << 16;
   d |= (uint64_t)((sbo >> 4) & 0x3FFF) << 32;
   d |= (uint64_t)1 << 46;                    // version
-  d |= (uint64_t)2 << 61;                    // SWIZZLE_128B
+  d |= (uint64_t)layout << 61;
   return d;
 }
 // Operand descriptor for K-step `ks` (K = 8 tf32 each) of a staged tile.
+//   K-major : SWIZZLE_128B, SBO = 1024 (8-row groups); +32 B per K-step inside the row.
+//   MN-major: SWIZZLE_128B_BASE32B, LBO = 4096 (32-element MN blocks = one TMA box),
+//             SBO = 512 (4-k-row swizzle atoms); +1024 B (8 k-rows) per K-step.
 template <bool MN>
 __device__ __forceinline__ uint64_t op_desc(uint32_t base, int ks) {
-  if (MN) return smem_desc_sw128(base + 1024u * ks, BK * 128, 1024);
-  return smem_desc_sw128(base + 32u * ks, 16, 1024);
+  if (MN) return smem_desc(base + 1024u * ks, BK * 128, 512, 1);
+  return smem_desc(base + 32u * ks, 16, 1024, 2);
 }
 // Instruction descriptor: D fp32, A/B tf32, majors, M x N.
 __host__ __device__ constexpr uint32_t idesc_tf32(int M, int N, bool a_mn, bool b_mn) {
@@ -111,8 +119,14 @@ __device__ __forceinline__ void tmem_ld32(uint32_t taddr, float (&v)[32]) {
   for (int i = 0; i < 32; ++i) v[i] = __uint_as_float(r[i]);
 }
 
-// TF32 part of x by truncation (low 13 mantissa bits cleared): exact as a TF32 operand.
-__device__ __forceinline__ float tf32_hi(float x) { return __uint_as_float(__float_as_uint(x) & 0xFFFFE000u); }
+// TF32 part of x, rounded to nearest (ties away): an exact TF32 value, so the tensor core's
+// own operand truncation leaves it unchanged; lo = x - hi is exact in fp32 with
+// abs(lo) <= 2^-11 abs(x).
+__device__ __forceinline__ float tf32_hi(float x) {
+  uint32_t r;
+  asm("cvt.rna.tf32.f32 %0, %1;" : "=r"(r) : "f"(x));
+  return __uint_as_float(r);
+}
 
 struct TileArgs {
   int M, N, K;

@@ -95,7 +95,7 @@ bool use_tc(int M, int N, int K, const TcOp &a, const TcOp &b) {
 bool make_map(CUtensorMap *m, const TcOp &o, int rows, int K, int box_rows) {
   if (o.mn)  // [K][rows] with rows contiguous: box {32 mn, 32 k}
     return encode_tmap_2d_f32(m, o.p, (uint64_t)rows, (uint64_t)K, (uint64_t)o.ld * 4, 32, tc::BK,
-                              CU_TENSOR_MAP_SWIZZLE_128B);
+                              CU_TENSOR_MAP_SWIZZLE_128B_ATOM_32B);
   return encode_tmap_2d_f32(m, o.p, (uint64_t)K, (uint64_t)rows, (uint64_t)o.ld * 4, tc::BK, (uint32_t)box_rows,
                             CU_TENSOR_MAP_SWIZZLE_128B);
 }

@@ -3,7 +3,9 @@
 Shapes are chosen so that every contraction with all extents >= 64 takes the tensor-core
 path: K1 (both operands K-major), K3 (B operand N-major), K4 (both operands MN-major),
 with ragged tile tails in M, N and K and split-K over the batch.  NF_MATH_FP32 runs them
-as 3xTF32 (bar 1e-4), NF_MATH_TF32 as 1xTF32 (bar 5e-3), both against the fp64 oracle.
+as 3xTF32 (bar 1e-4 at tau=0.1), NF_MATH_TF32 as 1xTF32 with the tensor core's operand
+truncation (bar 5e-3 normwise, tau=1, and 1e-2 at tau=0.1: reading R14 of DESIGN.md),
+both against the fp64 oracle.
 """
 import numpy as np
 import pytest
@@ -11,7 +13,7 @@ import torch
 
 import oracle
 import synth
-from parity import FP32_BAR, TF32_BAR, argmax_agree, rel_err
+from parity import FP32_BAR, TF32_BAR, TF32_ELEM_BAR, argmax_agree, rel_err
 
 pytestmark = pytest.mark.gpu
 
@@ -27,6 +29,14 @@ TC_SHAPES = [
 
 def dev(a):
     return torch.from_numpy(np.ascontiguousarray(a)).cuda()
+
+
+def check(got, ref, math):
+    if math == nf.NF_MATH_FP32:
+        assert rel_err(got, ref) <= FP32_BAR
+    else:
+        assert rel_err(got, ref, tau=1.0) <= TF32_BAR
+        assert rel_err(got, ref) <= TF32_ELEM_BAR
 
 
 def make_net(dims, act, params, math):
@@ -51,7 +61,7 @@ def test_tc_output(dims, act, n, math, bar):
     net = make_net(dims, act, p, math)
     out = net.output(dev(x)).cpu().numpy()
     ref = oracle.Oracle(dims, act).output(p, x)
-    assert rel_err(out, ref) <= bar
+    check(out, ref, math)
     if math == nf.NF_MATH_FP32:
         assert argmax_agree(out, ref)[0] == 0
 
@@ -66,8 +76,8 @@ def test_tc_grad(dims, act, n, math, bar):
     o = oracle.Oracle(dims, act)
     ref = o.grad(p, x, y)
     for (Wg, bg), (Wr, br) in zip(o.layers(g), o.layers(ref)):
-        assert rel_err(Wg, Wr) <= bar
-        assert rel_err(bg, br) <= bar
+        check(Wg, Wr, math)
+        check(bg, br, math)
 
 
 @pytest.mark.parametrize("math,bar", [(nf.NF_MATH_FP32, FP32_BAR), (nf.NF_MATH_TF32, TF32_BAR)])
@@ -81,8 +91,8 @@ def test_tc_train_batch(dims, act, n, math, bar):
     ref, _ = o.train_batch(p, x, y, 0.5)
     got = gpu_params(net)
     for (Wg, bg), (Wr, br) in zip(o.layers(got), o.layers(ref)):
-        assert rel_err(Wg, Wr) <= bar
-        assert rel_err(bg, br) <= bar
+        check(Wg, Wr, math)
+        check(bg, br, math)
     # the update itself (W' - W) carries the contraction error undiluted by W
     for (Wg, _), (Wr, _), (W0, _) in zip(o.layers(got), o.layers(ref), o.layers(p.astype(np.float64))):
         assert rel_err(Wg - W0, Wr - W0) <= (1e-3 if math == nf.NF_MATH_FP32 else 2e-2)
@@ -95,7 +105,7 @@ def test_tc_c5_full_width_grad():
     cfg = synth.CONFIGS[5]
     dims = cfg["dims"]
     p = synth.init_params(5)
-    X, Y = synth.dataset(5, N=80)
+    X, Y = synth.dataset(5, N=160)
     o = oracle.Oracle(dims, cfg["act"])
     keep = o.kink_free_rows(p, X, Y)
     X, Y = np.ascontiguousarray(X[keep][:64]), np.ascontiguousarray(Y[keep][:64])
