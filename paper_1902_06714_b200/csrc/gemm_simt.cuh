@@ -27,39 +27,102 @@ struct GemmArgs {
 };
 
 // ---- epilogues ------------------------------------------------------------
+// Each epilogue is split into load(m, n) -> aux (the one global value the element update
+// reads, 0 if none) and store(m, n, acc, aux), so that the tensor-core epilogue can issue
+// all 32 loads of a tile column before any store (no load-after-store serialisation
+// through possibly aliasing pointers).  operator() = store(load()).
+//
 // Forward: mode 0 hidden (A = sigma(z), S = sigma'(z)); mode 1 output layer in
 // training (A = sigma(z), S = (sigma(z) - y) sigma'(z) = delta_L, S:150 /
 // quadratic cost P:111); mode 2 inference (A = sigma(z) only).
 struct EpiFwd {
   const float *bias; float *A; float *S; const float *Y; int ld; int act; int mode;
-  __device__ __forceinline__ void operator()(int m, int n, float acc) const {
+  __device__ __forceinline__ float load(int m, int n) const {
+    return mode == 1 ? Y[(int64_t)m * ld + n] : 0.0f;
+  }
+  __device__ __forceinline__ void store(int m, int n, float acc, float y) const {
     const float z = acc + bias[n];
     const int64_t i = (int64_t)m * ld + n;
     if (mode == 2) { A[i] = act_only(act, z); return; }
     float a, s;
     act_fwd(act, z, a, s);
     A[i] = a;
-    S[i] = mode == 0 ? s : (a - Y[i]) * s;
+    S[i] = mode == 0 ? s : (a - y) * s;
+  }
+  __device__ __forceinline__ void operator()(int m, int n, float acc) const { store(m, n, acc, load(m, n)); }
+
+  // Tensor-core epilogue strip: rows m0..m0+31 (valid while < mlim) of column n; value of
+  // row r at v[33 r].  One switch on the activation per strip, not per element.
+  template <int K>
+  __device__ __forceinline__ void strip_t(int m0, int mlim, int n, const float *v) const {
+    const float bn = bias[n];
+    float y[32];
+    if (mode == 1) {
+#pragma unroll
+      for (int r = 0; r < 32; ++r) y[r] = m0 + r < mlim ? Y[(int64_t)(m0 + r) * ld + n] : 0.0f;
+    }
+#pragma unroll
+    for (int r = 0; r < 32; ++r) {
+      if (m0 + r >= mlim) break;
+      const int64_t i = (int64_t)(m0 + r) * ld + n;
+      const float z = v[33 * r] + bn;
+      if (mode == 2) {
+        A[i] = act_only_t<K>(z);
+      } else {
+        float a, s;
+        act_fwd_t<K>(z, a, s);
+        A[i] = a;
+        S[i] = mode == 0 ? s : (a - y[r]) * s;
+      }
+    }
+  }
+  __device__ __forceinline__ void strip(int m0, int mlim, int n, const float *v) const {
+    switch (act) {
+      case ACT_SIGMOID: strip_t<ACT_SIGMOID>(m0, mlim, n, v); break;
+      case ACT_TANH: strip_t<ACT_TANH>(m0, mlim, n, v); break;
+      case ACT_RELU: strip_t<ACT_RELU>(m0, mlim, n, v); break;
+      case ACT_GAUSSIAN: strip_t<ACT_GAUSSIAN>(m0, mlim, n, v); break;
+      default: strip_t<ACT_STEP>(m0, mlim, n, v); break;
+    }
   }
 };
+
+// Generic strip for element-wise epilogues with one aux load: all loads first, then stores.
+template <class E>
+__device__ __forceinline__ void strip_generic(const E &e, int m0, int mlim, int n, const float *v) {
+  float aux[32];
+#pragma unroll
+  for (int r = 0; r < 32; ++r) aux[r] = m0 + r < mlim ? e.load(m0 + r, n) : 0.0f;
+#pragma unroll
+  for (int r = 0; r < 32; ++r)
+    if (m0 + r < mlim) e.store(m0 + r, n, v[33 * r], aux[r]);
+}
 
 // Backward: SD holds sigma'(Z_l) on entry and delta_l on exit.
 struct EpiBwd {
   float *SD; int ld;
-  __device__ __forceinline__ void operator()(int m, int n, float acc) const {
-    const int64_t i = (int64_t)m * ld + n;
-    SD[i] = acc * SD[i];
+  __device__ __forceinline__ float load(int m, int n) const { return SD[(int64_t)m * ld + n]; }
+  __device__ __forceinline__ void store(int m, int n, float acc, float s) const {
+    SD[(int64_t)m * ld + n] = acc * s;
+  }
+  __device__ __forceinline__ void operator()(int m, int n, float acc) const { store(m, n, acc, load(m, n)); }
+  __device__ __forceinline__ void strip(int m0, int mlim, int n, const float *v) const {
+    strip_generic(*this, m0, mlim, n, v);
   }
 };
 
 // Gradient: store = 0 applies W -= scale*G, b -= scale*g (scale =
-// eta/B, reading R3); store = 1 writes G, g (nf_grad).
+// eta/B, reading R3); store = 1 writes G, g (nf_grad).  Column n == nreal is the bias.
 struct EpiGrad {
-  float *W; float *b; int ldw; int nreal; float scale; int store;
-  __device__ __forceinline__ void operator()(int m, int n, float acc) const {
-    float *p = n < nreal ? W + (int64_t)m * ldw + n : b + m;
-    if (store) *p = acc;
-    else *p = *p - scale * acc;
+  float *W; float *b; int ldw; int nreal; float scale; int store_only;
+  __device__ __forceinline__ float *at(int m, int n) const { return n < nreal ? W + (int64_t)m * ldw + n : b + m; }
+  __device__ __forceinline__ float load(int m, int n) const { return store_only ? 0.0f : *at(m, n); }
+  __device__ __forceinline__ void store(int m, int n, float acc, float w) const {
+    *at(m, n) = store_only ? acc : w - scale * acc;
+  }
+  __device__ __forceinline__ void operator()(int m, int n, float acc) const { store(m, n, acc, load(m, n)); }
+  __device__ __forceinline__ void strip(int m0, int mlim, int n, const float *v) const {
+    strip_generic(*this, m0, mlim, n, v);
   }
 };
 

@@ -12,8 +12,9 @@
 //
 // Numerics (reading R13 of DESIGN.md): SPLIT = 1 is plain TF32 (NF_MATH_TF32).
 // SPLIT = 3 is 3xTF32 for the fp32 mode: every staged tile x is split in shared memory
-// into hi = x rounded to TF32 (written back in place) and lo = x - hi (exact in fp32), and
-// each K-step issues hi*hi + hi*lo + lo*hi.  The tensor core reads fp32 bit patterns and
+// into hi = x rounded to TF32 (written back in place) and lo = (x - hi) rounded to TF32
+// (x - hi is exact in fp32), and each K-step issues hi*hi + hi*lo + lo*hi: per-product error
+// <= 2^-23 (lo rounding) + 2^-22 (dropped lo*lo) relative.  The tensor core reads fp32 bit patterns and
 // drops the low 13 mantissa bits (truncation, measured: micro/tc_major_test.cu), which is
 // what SPLIT = 1 gets.
 //
@@ -57,7 +58,12 @@ struct Cfg {
   static constexpr int STAGE_BYTES = SPLIT == 3 ? 2 * RAW_BYTES : RAW_BYTES;  // raw(hi) | lo
   static constexpr int STAGES_FIT = (kSmemBudget - kEpiBytes - 1024 - 512) / STAGE_BYTES;
   static constexpr int STAGES = STAGES_FIT > 6 ? 6 : STAGES_FIT;
-  static constexpr int TMEM_COLS = BN;
+  // NACC accumulators (all 512 TMEM columns): K-step t accumulates into t % NACC, and
+  // the epilogue sums them in fp32.  The tensor core's fp32 accumulation truncates
+  // (measured error linear in K, micro/tc_major_test.cu); spreading the K-steps over
+  // NACC accumulators divides that error by NACC.
+  static constexpr int NACC = 512 / BN;
+  static constexpr int TMEM_COLS = 512;
   static constexpr int SMEM = STAGES * STAGE_BYTES + kEpiBytes + 1024 /*align*/ + 512 /*barriers*/;
   static_assert(STAGES >= 2, "ring too shallow");
 };
@@ -211,12 +217,15 @@ gemm_tc_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ 
         const uint32_t sb = sa + C::A_BYTES;
 #pragma unroll
         for (int ks = 0; ks < BK / 8; ++ks) {
+          const int t = it * (BK / 8) + ks;                  // global K-step
+          const uint32_t d = tmem + (uint32_t)((t % C::NACC) * BN);
+          const uint32_t acc = t >= C::NACC ? 1u : 0u;       // first use of each accumulator
           const uint64_t ah = op_desc<A_MN>(sa, ks), bh = op_desc<B_MN>(sb, ks);
-          mma_tf32(tmem, ah, bh, idesc, (it | ks) != 0 ? 1u : 0u);
+          mma_tf32(d, ah, bh, idesc, acc);
           if (SPLIT == 3) {
             const uint64_t al = op_desc<A_MN>(sa + C::RAW_BYTES, ks), bl = op_desc<B_MN>(sb + C::RAW_BYTES, ks);
-            mma_tf32(tmem, ah, bl, idesc, 1u);
-            mma_tf32(tmem, al, bh, idesc, 1u);
+            mma_tf32(d, ah, bl, idesc, 1u);
+            mma_tf32(d, al, bh, idesc, 1u);
           }
         }
         mma_commit(&empty[s]);
@@ -236,7 +245,7 @@ gemm_tc_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ 
           const float4 x = raw[i];
           const float4 h = make_float4(tf32_hi(x.x), tf32_hi(x.y), tf32_hi(x.z), tf32_hi(x.w));
           raw[i] = h;
-          lo[i] = make_float4(x.x - h.x, x.y - h.y, x.z - h.z, x.w - h.w);
+          lo[i] = make_float4(tf32_hi(x.x - h.x), tf32_hi(x.y - h.y), tf32_hi(x.z - h.z), tf32_hi(x.w - h.w));
         }
         ptx::fence_proxy_async_smem();
         __syncwarp();
@@ -255,19 +264,29 @@ gemm_tc_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ 
       const int nc = n0 + c * 32;
       if (nc >= g.N) break;  // warp-uniform
       float v[32];
-      tmem_ld32(tmem + ((uint32_t)(q * 32) << 16) + (uint32_t)(c * 32), v);
+      const uint32_t trow = tmem + ((uint32_t)(q * 32) << 16) + (uint32_t)(c * 32);
+      tmem_ld32(trow, v);
+      const int nk = nkb * (BK / 8);                 // K-steps issued: accumulators in use
+#pragma unroll 1
+      for (int a = 1; a < C::NACC && a < nk; ++a) {   // fixed order: acc 0 + 1 + ... (RN fp32)
+        float w[32];
+        tmem_ld32(trow + (uint32_t)(a * BN), w);
+#pragma unroll
+        for (int j = 0; j < 32; ++j) v[j] += w[j];
+      }
 #pragma unroll
       for (int j = 0; j < 32; ++j) buf[lane * 33 + j] = v[j];
       __syncwarp();
       const int n = nc + lane;
+      const bool nok = n < g.N;
+      if (g.partial) {
 #pragma unroll 4
-      for (int r = 0; r < 32; ++r) {
-        const int m = mrow0 + r;
-        if (m < g.M && n < g.N) {
-          const float val = buf[r * 33 + lane];
-          if (g.partial) g.partial[blockIdx.z * MN + (int64_t)m * g.N + n] = val;
-          else epi(m, n, val);
+        for (int r = 0; r < 32; ++r) {
+          const int m = mrow0 + r;
+          if (m < g.M && nok) g.partial[blockIdx.z * MN + (int64_t)m * g.N + n] = buf[r * 33 + lane];
         }
+      } else if (nok) {
+        epi.strip(mrow0, g.M, n, buf + lane);  // 32 rows of column n, loads before stores
       }
       __syncwarp();
     }

@@ -117,7 +117,7 @@ cudaError_t launch_tc(cudaStream_t st, int M, int N, int K, const TcOp &a, const
   const int tiles = tm * tn;
   const int nkb = (K + tc::BK - 1) / tc::BK;
   int splits = 1;
-  if (tiles < kSMs && nkb >= 8) {
+  if (2 * tiles < kSMs && nkb >= 8) {  // split-K only when under half a wave
     splits = std::min((kSMs + tiles - 1) / tiles, nkb / 4);
     while (splits > 1 && (size_t)splits * M * N > ws.partial_floats) --splits;
     splits = std::max(splits, 1);
@@ -139,13 +139,20 @@ cudaError_t launch_tc(cudaStream_t st, int M, int N, int K, const TcOp &a, const
 template <bool AMN, bool BMN, class Epi>
 cudaError_t run_tc(cudaStream_t st, int M, int N, int K, const TcOp &a, const TcOp &b, const Epi &epi,
                    const Workspace &ws) {
+  // Tile width: the widest BN whose tile count still fills the GPU (>= ~0.8 of the SMs);
+  // otherwise BN = 64 and split-K over the reduction dimension.
+  const int tm = (M + tc::BM - 1) / tc::BM;
+  auto tiles = [&](int bn) { return tm * ((N + bn - 1) / bn); };
+  const int fill = kSMs * 4 / 5;
   if (ws.math == 1) {
     g_last_engine = ENGINE_TC1;
-    if (N > 128) return launch_tc<256, AMN, BMN, 1>(st, M, N, K, a, b, epi, ws);
-    return launch_tc<128, AMN, BMN, 1>(st, M, N, K, a, b, epi, ws);
+    if (N > 128 && tiles(256) >= fill) return launch_tc<256, AMN, BMN, 1>(st, M, N, K, a, b, epi, ws);
+    if (N > 64 && tiles(128) >= fill) return launch_tc<128, AMN, BMN, 1>(st, M, N, K, a, b, epi, ws);
+    return launch_tc<64, AMN, BMN, 1>(st, M, N, K, a, b, epi, ws);
   }
   g_last_engine = ENGINE_TC3;
-  return launch_tc<128, AMN, BMN, 3>(st, M, N, K, a, b, epi, ws);
+  if (N > 64 && tiles(128) >= fill) return launch_tc<128, AMN, BMN, 3>(st, M, N, K, a, b, epi, ws);
+  return launch_tc<64, AMN, BMN, 3>(st, M, N, K, a, b, epi, ws);
 }
 
 // Bias tendency g[i] = sum_r D[r][i] over n rows (the ones-column of the SIMT path),
@@ -178,7 +185,8 @@ colsum_final(const float *__restrict__ part, int nchunks, int cols, EpiGrad epi)
 
 cudaError_t bias_grad(cudaStream_t st, const float *D, int64_t rows, int cols, const EpiGrad &epi,
                       float *part, size_t part_floats) {
-  int nchunks = (int)std::min<int64_t>((rows + 255) / 256, 64);
+  // ~4 column blocks x 64+ row chunks of <= 64 rows: enough CTAs to stream D at HBM rate
+  int nchunks = (int)std::min<int64_t>((rows + 63) / 64, 256);
   while (nchunks > 1 && (size_t)nchunks * cols > part_floats) --nchunks;
   const int chunk = (int)((rows + nchunks - 1) / nchunks);
   const dim3 grid((cols + 255) / 256, nchunks);
@@ -271,11 +279,19 @@ loss_acc_partial(const float *__restrict__ A, const float *__restrict__ Y, int64
   }
 }
 
+// One warp: lane j sums partials j, j+32, ... in order, then a fixed shuffle tree
+// (deterministic for a given nparts).
 __global__ void loss_acc_final(const double2 *__restrict__ part, int nparts, int64_t n,
                                float *out, float *step_loss) {
-  if (threadIdx.x != 0) return;
+  const int lane = threadIdx.x;
   double l = 0.0, c = 0.0;
-  for (int i = 0; i < nparts; ++i) { l += part[i].x; c += part[i].y; }
+  for (int i = lane; i < nparts; i += 32) { l += part[i].x; c += part[i].y; }
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) {
+    l += __shfl_xor_sync(0xffffffffu, l, o);
+    c += __shfl_xor_sync(0xffffffffu, c, o);
+  }
+  if (lane != 0) return;
   const float loss = n > 0 ? (float)(l / (double)n) : 0.0f;
   const float acc = n > 0 ? (float)(c / (double)n) : 0.0f;
   if (out) { out[0] = loss; out[1] = acc; }

@@ -45,6 +45,16 @@ __device__ __forceinline__ void act_fwd(int kind, float z, float &a, float &s) {
   }
 }
 
+// Compile-time-activation forms (same arithmetic) for unrolled epilogue strips.
+template <int K>
+__device__ __forceinline__ void act_fwd_t(float z, float &a, float &s) { act_fwd(K, z, a, s); }
+template <int K>
+__device__ __forceinline__ float act_only_t(float z) {
+  float a, s;
+  act_fwd(K, z, a, s);
+  return a;
+}
+
 __device__ __forceinline__ float act_only(int kind, float z) {
   switch (kind) {
     case ACT_SIGMOID: {
