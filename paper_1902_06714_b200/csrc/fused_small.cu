@@ -1,27 +1,33 @@
-// fused_small.cu -- ONE persistent kernel running many SGD steps of a two-layer
-// net with narrow hidden and output layers (H, O <= 32): configs 1 and 2
-// ([3,5,2] and the paper's MNIST net [784,30,10]).
+// fused_small.cu -- ONE persistent kernel running many SGD steps of a two-layer net with
+// narrow hidden and output layers (H, O <= 32): configs 1 and 2 ([3,5,2] and the paper's
+// MNIST net [784,30,10]).  Every step is the paper's train_batch:
+// fwdprop, backprop, tendencies summed over the batch (the co_sum
+// of P:536-556) and the update W -= eta/B dW (reading R3).
 //
-// Decomposition (DESIGN.md "K6 fused small-net kernel"):
+// Decomposition (DESIGN.md "K6"):
 //   * G clusters x C CTAs, all co-resident (1 CTA per SM).  Cluster g owns rows
-//     [r_g, r_{g+1}) of every minibatch (the paper's per-image batch shard,
-//     P:511-516); CTA rank c owns input columns (pixels) [k_c, k_c + w_c) and
-//     keeps that slice of W1 resident in shared memory for all steps.
+//     [g B/G, (g+1) B/G) of every minibatch (the paper's per-image batch shard,
+//     P:511-516); CTA rank c owns input columns (pixels) [c ws, c ws + w) and keeps that
+//     slice of W1 resident in shared memory for all steps.
 //   * per step s:
-//       0  TMA 2-D tile load of the NEXT step's x slice (one cp.async.bulk.tensor
-//          per CTA, mbarrier completion) -- overlaps the whole step
-//       1  partial Z1 over the pixel slice (fp32 FFMA, smem operands)
-//       2  DSMEM push: each CTA bulk-copies the partial rows of every peer's owned
-//          rows into that peer's shared memory (mbarrier complete_tx, no cluster
-//          barrier); the owner sums the C partials in rank order, adds b1, applies
-//          sigma / sigma' (Eq. 2), then layer 2, delta_2 = (a2-y) sigma'(z2)
-//          and delta_1 = (W2^T delta_2) sigma'(z1) (backprop)
-//       3  DSMEM push of the owned delta_1 rows to every peer, and of the W2/b1/b2
-//          tendency partials to the rank that reduces them
-//       4  dW1 slice = sum_rows delta_1 (x) x (fp32 FFMA); cp.reduce.async.bulk adds
-//          it into an L2 accumulator: the paper's co_sum in-GPU
-//       5  grid barrier; every CTA applies W -= (eta/B) G to its resident
-//          parameters (reading R3) and zeroes the accumulator two steps ahead.
+//       P0  TMA 2-D tile load of the NEXT step's x slice (mbarrier completion) and
+//           cp.async of the next step's owned target rows -- overlaps the whole step
+//       P1  partial Z1 over the pixel slice: fp32 FFMA, 5-row x 4-neuron register tiles,
+//           K split in two halves across warps, halves summed in shared memory
+//       P2  DSMEM push of the partial rows each peer owns (bulk copy, mbarrier
+//           complete_tx on the receiver; no cluster barrier)
+//       P3  owner rows: sum the C partials in rank order, + b1, sigma/sigma' (Eq. 2,
+//           P:319-322), layer 2, delta_2 = (a2 - y) sigma'(z2), delta_1 = (W2^T delta_2)
+//           sigma'(z1); W2/b1/b2 tendency partials (one warp per row)
+//       P4  DSMEM push of the owned delta_1 rows to every peer and of the W2/b tendency
+//           partial slices to the rank that reduces them
+//       P5  dW1 slice = sum_rows delta_1 (x) x: 4x4 register tiles
+//       P6  co_sum: ONE cp.reduce.async.bulk .add.f32 of the [H][ws] slice into this
+//           rank's contiguous slice of the step's L2 accumulator (+ the W2/b slice)
+//       P7  grid barrier
+//       P8  ONE bulk copy of the reduced slice (+ the W2/b block) back into shared memory
+//       P9  W -= (eta/B) G on the resident parameters; zero this CTA's share of the
+//           accumulator used two steps ahead
 #include <algorithm>
 #include <cstdio>
 #include <cstdlib>
@@ -38,13 +44,17 @@ static thread_local char g_fs_err[256] = "";
 
 namespace {
 
-constexpr int kThreads = 256;
+constexpr int kThreads = 512;  // 16 warps: latency hiding for the short dependent phases
 constexpr int kWarps = kThreads / 32;
 constexpr int kMaxC = 8;       // cluster size
 constexpr int kMaxRows = 128;  // rows per cluster
+constexpr int kRG = 5;         // rows per P1 register tile
+constexpr int kKP = 4;         // P1: K (pixel) range split in kKP parts across threads
+constexpr int kRH = 2;         // P5: rows split in kRH parts across threads
 constexpr int kProf = 16;      // profiler slots per step
-constexpr int kRowsZ = 9;      // rows per warp per pass in the Z1 phase (72 rows per pass)
-constexpr int GP = 32 * 32 + 64;  // W2 [32][32] + b1 [32] + b2 [32] tendency partial (padded)
+constexpr int kSmall = 32 * 32 + 64;  // capacity of the W2/b1/b2 tendency block: O*H + H + O <= 1088
+constexpr int kSlots = 4;             // accumulator ring: step s uses slot s % 4; slot (s+2) % 4 is
+                                      // zeroed between this step's barrier arrive and wait
 
 struct FusedParams {
   int n0, H, O;          // dims
@@ -52,32 +62,31 @@ struct FusedParams {
   int B;                 // batch rows per step
   int G;                 // clusters
   int ws, wpad;          // pixel-slice stride and padded smem row length (floats)
-  int aligned;           // 1: n0 % 4 == 0 -> 16-B aligned slices, TMA / bulk paths
+  int aligned;           // 1: TMA x tiles and bulk reductions (n0 % 4 == 0, 16-B aligned X)
   int nSmax, nOwnMax;    // max rows per cluster / per CTA
   int64_t n_steps;
+  int64_t slot;          // accumulator slot stride (floats, multiple of 32)
+  int64_t small_off;     // offset of the W2/b1/b2 block inside a slot
+  int nsmp;              // W2/b1/b2 block length O*H + H + O, rounded up to a multiple of 4
   float scale;           // eta / B
   float inv_B;
   const float *X, *Y;
   const int64_t *starts; // device
   float *params;         // flat [W1 b1 W2 b2]
-  float *acc;            // 3 x nparams accumulators (zeroed by the host)
+  float *acc;            // kSlots accumulator slots (zeroed by the host)
   unsigned *bar;         // grid barrier counter (zeroed by the host)
   float *step_loss;      // nullable, zeroed by the host
-  unsigned long long *prof;  // nullable: per-CTA per-step phase timestamps (NF_FUSED_PROF=1)
+  long long *prof;       // nullable: per-CTA per-step clock64 stamps (NF_FUSED_PROF=1)
 };
 
-__device__ __forceinline__ unsigned long long globaltimer() {
-  unsigned long long t;
-  asm volatile("mov.u64 %0, %globaltimer;" : "=l"(t));
-  return t;
-}
 #define PROF(i) \
-  if (p.prof && threadIdx.x == 0 && s < 64) p.prof[((int64_t)blockIdx.x * 64 + s) * kProf + (i)] = globaltimer()
+  if (p.prof && threadIdx.x == 0 && s < 64) p.prof[((int64_t)blockIdx.x * 64 + s) * kProf + (i)] = clock64()
 
 __device__ __forceinline__ int row_begin(int g, int B, int G) { return (int)(((int64_t)g * B) / G); }
 __host__ __device__ __forceinline__ int own_begin(int c, int nS, int C) { return (c * nS) / C; }
-__host__ __device__ __forceinline__ int e_begin(int c, int C) { return 4 * (((GP / 4) * c) / C); }
-__host__ __device__ __forceinline__ int e_slot(int C) { return ((GP / C + 4) + 3) & ~3; }  // 16-B multiple
+// slice of the W2/b tendency block (nsmp floats) reduced by rank c: 16-B aligned chunks
+__host__ __device__ __forceinline__ int e_begin(int c, int C, int nsmp) { return 4 * (((nsmp / 4) * c) / C); }
+__host__ __device__ __forceinline__ int e_slot(int C) { return ((kSmall / C + 4) + 3) & ~3; }
 
 __device__ __forceinline__ void cp_async4(float *dst, const float *src) {
   asm volatile("cp.async.ca.shared.global [%0], [%1], 4;" ::"r"(ptx::smem_u32(dst)), "l"(src) : "memory");
@@ -85,30 +94,34 @@ __device__ __forceinline__ void cp_async4(float *dst, const float *src) {
 __device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;" ::: "memory"); }
 __device__ __forceinline__ void cp_async_wait0() { asm volatile("cp.async.wait_group 0;" ::: "memory"); }
 
-struct Smem {
-  // offsets in floats from the 128-B aligned base
-  int W1t, W2s, b1s, b2s, xs, ys, Pfull, Pown, D1, gpart, grecv, Gs, Gt, wred, lsum, total;
+struct Smem {  // offsets in floats from the 128-B aligned base
+  int W1t, W2s, b1s, b2s, xs, ys, Ppart, Pown, D1, A1own, D2own, gpart, grecv, Gs, Gs2, Gr, gsm, lsum, total;
 };
 
 __host__ __device__ inline int al32(int v) { return (v + 31) & ~31; }  // 128-B alignment in floats
 
+__host__ __device__ inline int xrows(int nSmax) { return (nSmax + kRG - 1) / kRG * kRG; }
+
 __host__ __device__ inline Smem smem_layout(int wpad, int nSmax, int nOwnMax, int C) {
   Smem L;
   int o = 32;  // mbarriers live in the first 128 B
-  L.W1t = o;   o = al32(o + wpad * 32);
-  L.W2s = o;   o = al32(o + 32 * 33);
+  L.W1t = o;   o = al32(o + wpad * 32);            // [wpad][32]: W1 slice, k-major
+  L.W2s = o;   o = al32(o + 32 * 33);              // [32][33]
   L.b1s = o;   o += 32;
   L.b2s = o;   o = al32(o + 32);
-  L.xs = o;    o = al32(o + 2 * al32(nSmax * wpad));  // TMA destinations: 128-B aligned
+  L.xs = o;    o = al32(o + 2 * al32(xrows(nSmax) * wpad));  // 2 TMA destinations
   L.ys = o;    o = al32(o + 2 * nOwnMax * 32);
-  L.Pfull = o; o = al32(o + nSmax * 32);
+  L.Ppart = o; o = al32(o + kKP * xrows(nSmax) * 32);  // P1 K-part partials; part 0 = Pfull
   L.Pown = o;  o = al32(o + C * nOwnMax * 32);
   L.D1 = o;    o = al32(o + nSmax * 32);
-  L.gpart = o; o = al32(o + GP);
+  L.A1own = o; o = al32(o + nOwnMax * 32);         // a1 of the owned rows
+  L.D2own = o; o = al32(o + nOwnMax * 32);         // delta_2 of the owned rows
+  L.gpart = o; o = al32(o + kSmall);
   L.grecv = o; o = al32(o + C * e_slot(C));
-  L.Gs = o;    o = al32(o + 32 * wpad);
-  L.Gt = o;    o = al32(o + wpad * 33);
-  L.wred = o;  o = al32(o + kWarps * GP);
+  L.Gs = o;    o = al32(o + wpad * 32);            // [wpad][32]: dW1 slice partial, k-major like W1t
+  L.Gs2 = o;   o = al32(o + wpad * 32);            // second row-half partial
+  L.Gr = o;    o = al32(o + wpad * 32);            // reduced slice read back
+  L.gsm = o;   o = al32(o + kSmall);               // reduced W2/b block read back
   L.lsum = o;  o = al32(o + kWarps);
   L.total = o;
   return L;
@@ -137,22 +150,26 @@ fused_small_kernel(const FusedParams p, const __grid_constant__ CUtensorMap tmX)
   // rows of this cluster and the rows each rank owns inside them
   const int r0 = row_begin(g, p.B, p.G), nS = row_begin(g + 1, p.B, p.G) - r0;
   const int o0 = own_begin(rank, nS, C), nOwn = own_begin(rank + 1, nS, C) - o0;
-  const int e0 = e_begin(rank, C), ne = e_begin(rank + 1, C) - e0;
+  const int nsmp = p.nsmp, nsm = O * H + H + O;
+  const int e0 = e_begin(rank, C, nsmp), ne = e_begin(rank + 1, C, nsmp) - e0;
   const int eslot = e_slot(C);
 
   const Smem L = smem_layout(wpad, p.nSmax, p.nOwnMax, C);
-  const int xstride = al32(p.nSmax * wpad);
+  const int xstride = al32(xrows(p.nSmax) * wpad);
   uint64_t *bar_x = reinterpret_cast<uint64_t *>(sm);  // [2]
   uint64_t *bar_P = bar_x + 2;
   uint64_t *bar_D = bar_x + 3;
+  uint64_t *bar_G = bar_x + 4;
   float *W1t = sm + L.W1t, *W2s = sm + L.W2s, *b1s = sm + L.b1s, *b2s = sm + L.b2s;
-  float *xs0 = sm + L.xs, *ys0 = sm + L.ys, *Pfull = sm + L.Pfull, *Pown = sm + L.Pown;
-  float *D1 = sm + L.D1, *gpart = sm + L.gpart, *grecv = sm + L.grecv, *Gs = sm + L.Gs, *Gt = sm + L.Gt;
-  float *wred = sm + L.wred, *lsum = sm + L.lsum;
+  float *xs0 = sm + L.xs, *ys0 = sm + L.ys, *Pfull = sm + L.Ppart, *Pown = sm + L.Pown;
+  const int pstride = xrows(p.nSmax) * 32;  // floats between P1 K-part buffers
+  float *D1 = sm + L.D1, *A1own = sm + L.A1own, *D2own = sm + L.D2own;
+  float *gpart = sm + L.gpart, *grecv = sm + L.grecv, *Gs = sm + L.Gs, *Gs2 = sm + L.Gs2, *Gr = sm + L.Gr;
+  float *gsm = sm + L.gsm, *lsum = sm + L.lsum;
 
   const int64_t oW1 = 0, ob1 = (int64_t)H * n0, oW2 = ob1 + H, ob2 = oW2 + (int64_t)O * H;
-  const int64_t np = ob2 + O;
-  const int64_t npad = (np + 3) & ~int64_t(3);  // accumulator stride (16-B aligned)
+  // accumulator slot layout: [C slices of ws x 32 (k-major)] [W2/b block of nsmp floats]
+  const int64_t slice_off = (int64_t)rank * p.ws * 32;
 
   // ---- one-time setup: zero smem, barriers, resident parameters
   for (int i = 32 + tid; i < L.total; i += kThreads) sm[i] = 0.0f;
@@ -161,6 +178,7 @@ fused_small_kernel(const FusedParams p, const __grid_constant__ CUtensorMap tmX)
     ptx::mbar_init(&bar_x[1], 1);
     ptx::mbar_init(bar_P, 1);
     ptx::mbar_init(bar_D, 1);
+    ptx::mbar_init(bar_G, 1);
     ptx::fence_mbar_init();
     if (p.aligned) ptx::prefetch_tensormap(&tmX);
   }
@@ -181,11 +199,16 @@ fused_small_kernel(const FusedParams p, const __grid_constant__ CUtensorMap tmX)
     bytesP += nOwn * 128;
     bytesD += (own_begin(c + 1, nS, C) - own_begin(c, nS, C)) * 128 + ne * 4;
   }
+  const uint32_t bytesG = (uint32_t)(p.ws * 32 * 4 + nsmp * 4);
 
   const uint32_t xbytes = (uint32_t)(p.nSmax * p.ws * 4);
+  // batch starts are read one step ahead of their use so their global-load latency overlaps
+  // a whole step (next_start holds starts[s + 1] while step s runs)
+  int64_t next_start = p.n_steps > 0 ? p.starts[0] : 0;
   auto prefetch = [&](int64_t s) {
     const int buf = (int)(s & 1);
-    const int64_t row0 = p.starts[s] + r0;
+    const int64_t row0 = next_start + r0;
+    next_start = s + 1 < p.n_steps ? p.starts[s + 1] : 0;
     float *xs = xs0 + buf * xstride;
     if (p.aligned) {
       if (tid == 0) {
@@ -208,14 +231,20 @@ fused_small_kernel(const FusedParams p, const __grid_constant__ CUtensorMap tmX)
 
   prefetch(0);
 
+  // P1 task geometry: kRG-row x 4-neuron tiles, K in kKP parts of 4-pixel chunks
+  const int RG = (nS + kRG - 1) / kRG;
+  const int nchunk = wpad / 4;
+  // P5 task geometry: 4-neuron x 4-pixel tiles, rows in kRH parts
+  const int nP5 = kRH * 8 * nchunk;
+
   for (int64_t s = 0; s < p.n_steps; ++s) {
     const int buf = (int)(s & 1);
     const uint32_t par = (uint32_t)(s & 1);
     const float *xs = xs0 + buf * xstride;
     const float *ys = ys0 + buf * p.nOwnMax * 32;
-    float *accS = p.acc + (s % 3) * npad;
+    float *accS = p.acc + (s % kSlots) * p.slot;
     PROF(0);
-    if (tid == 0) {  // arm this step's DSMEM receive barriers
+    if (tid == 0) {  // arm this step's receive barriers
       ptx::mbar_arrive_expect_tx(bar_P, bytesP);
       ptx::mbar_arrive_expect_tx(bar_D, bytesD);
     }
@@ -225,41 +254,57 @@ fused_small_kernel(const FusedParams p, const __grid_constant__ CUtensorMap tmX)
     if (s + 1 < p.n_steps) prefetch(s + 1);
     PROF(1);
 
-    // ---- 1. partial Z1: Pfull[i][j] = sum_{k<w} x[i][k] W1[j][k0+k]
-    //      warp: 8-row chunks (rows warp + 8u), lane: j; 8 independent FMA chains per lane
-    for (int rb = 0; rb * kWarps * kRowsZ < nS; ++rb) {
-      const float *xr[kRowsZ];
-      int rows[kRowsZ];
+    // ---- P1. partial Z1: P[i][j] = sum_{k<w} x[i][k] W1[j][k0+k]
+    for (int t = tid; t < kKP * RG * 8; t += kThreads) {
+      const int jg = t & 7, rg = (t >> 3) % RG, kp = (t >> 3) / RG;
+      const int cb = kp * nchunk / kKP, ce = (kp + 1) * nchunk / kKP;
+      const float *xr = xs + rg * kRG * wpad;
+      const float *wr = W1t + jg * 4;
+      float a[kRG][4];
 #pragma unroll
-      for (int u = 0; u < kRowsZ; ++u) {
-        rows[u] = warp + kWarps * (rb * kRowsZ + u);
-        xr[u] = xs + (rows[u] < nS ? rows[u] : 0) * wpad;
-      }
-      float a[kRowsZ];
+      for (int u = 0; u < kRG; ++u)
 #pragma unroll
-      for (int u = 0; u < kRowsZ; ++u) a[u] = 0.0f;
-      for (int k = 0; k < wpad; k += 4) {
-        const float w0 = W1t[(k + 0) * 32 + lane], w1 = W1t[(k + 1) * 32 + lane];
-        const float w2 = W1t[(k + 2) * 32 + lane], w3 = W1t[(k + 3) * 32 + lane];
-        float4 xv[kRowsZ];
+        for (int v = 0; v < 4; ++v) a[u][v] = 0.0f;
+#pragma unroll 2
+      for (int c = cb; c < ce; ++c) {
+        float4 xv[kRG], wv[4];
 #pragma unroll
-        for (int u = 0; u < kRowsZ; ++u) xv[u] = *reinterpret_cast<const float4 *>(xr[u] + k);
+        for (int u = 0; u < kRG; ++u) xv[u] = *reinterpret_cast<const float4 *>(xr + u * wpad + 4 * c);
 #pragma unroll
-        for (int u = 0; u < kRowsZ; ++u) {
-          a[u] = fmaf(xv[u].x, w0, a[u]);
-          a[u] = fmaf(xv[u].y, w1, a[u]);
-          a[u] = fmaf(xv[u].z, w2, a[u]);
-          a[u] = fmaf(xv[u].w, w3, a[u]);
+        for (int q = 0; q < 4; ++q) wv[q] = *reinterpret_cast<const float4 *>(wr + (4 * c + q) * 32);
+#pragma unroll
+        for (int u = 0; u < kRG; ++u) {
+          const float xq[4] = {xv[u].x, xv[u].y, xv[u].z, xv[u].w};
+#pragma unroll
+          for (int q = 0; q < 4; ++q) {
+            a[u][0] = fmaf(xq[q], wv[q].x, a[u][0]);
+            a[u][1] = fmaf(xq[q], wv[q].y, a[u][1]);
+            a[u][2] = fmaf(xq[q], wv[q].z, a[u][2]);
+            a[u][3] = fmaf(xq[q], wv[q].w, a[u][3]);
+          }
         }
       }
+      float *dst = Pfull + kp * pstride;
 #pragma unroll
-      for (int u = 0; u < kRowsZ; ++u)
-        if (rows[u] < nS) Pfull[rows[u] * 32 + lane] = a[u];
+      for (int u = 0; u < kRG; ++u)
+        *reinterpret_cast<float4 *>(dst + (rg * kRG + u) * 32 + jg * 4) = make_float4(a[u][0], a[u][1], a[u][2], a[u][3]);
+    }
+    __syncthreads();
+    for (int i = tid; i < nS * 8; i += kThreads) {  // parts summed in order 0 + 1 + 2 + 3
+      float4 *d = reinterpret_cast<float4 *>(Pfull) + i;
+      float4 v = *d;
+#pragma unroll
+      for (int kp = 1; kp < kKP; ++kp) {
+        const float4 h = reinterpret_cast<const float4 *>(Pfull + kp * pstride)[i];
+        v.x += h.x; v.y += h.y; v.z += h.z; v.w += h.w;
+      }
+      *d = v;
     }
     ptx::fence_proxy_async_smem();
     __syncthreads();
     PROF(2);
-    // push the partial rows each peer owns into its Pown[rank] slot
+
+    // ---- P2. push the partial rows each peer owns into its Pown[rank] slot
     if (warp == 0 && lane < C && lane != rank) {
       const int c = lane;
       const int a0 = own_begin(c, nS, C), na = own_begin(c + 1, nS, C) - a0;
@@ -269,69 +314,83 @@ fused_small_kernel(const FusedParams p, const __grid_constant__ CUtensorMap tmX)
     ptx::mbar_wait(bar_P, par);
     PROF(3);
 
-    // ---- 2. owned rows: reduce partials over the cluster, layer 1 epilogue, layer 2, deltas
-    float g2acc[32];  // per-lane accumulators: lane j holds G2[o][j] for all o
-#pragma unroll
-    for (int o = 0; o < 32; ++o) g2acc[o] = 0.0f;
-    float g1acc = 0.0f, gb2acc = 0.0f, lacc = 0.0f;
-    for (int q = warp; q < nOwn; q += kWarps) {
-      const int i = o0 + q;
-      float z = b1s[lane];
+    // ---- P3. owned rows, all rows at once in three CTA-wide passes:
+    //      (a) thread (q, j): z1 = b1 + sum of the C partials in rank order, a1, sigma'(z1)
+    //      (b) thread (q, o): z2 = b2 + W2 a1, a2, delta_2 = (a2 - y) sigma'(z2), cost
+    //      (c) thread (q, j): delta_1 = sigma'(z1) * W2^T delta_2
+    float lacc = 0.0f;
+    for (int t = tid; t < nOwn * 32; t += kThreads) {
+      const int q = t >> 5, j = t & 31, i = o0 + q;
+      float z = b1s[j];
 #pragma unroll
       for (int c = 0; c < kMaxC; ++c)
-        if (c < C) z += (c == rank) ? Pfull[i * 32 + lane] : Pown[(c * p.nOwnMax + q) * 32 + lane];
-      if (q == 0) PROF(12);
+        if (c < C) z += (c == rank) ? Pfull[i * 32 + j] : Pown[(c * p.nOwnMax + q) * 32 + j];
       float a1, s1;
       act_fwd(p.act_h, z, a1, s1);
-      if (lane >= H) { a1 = 0.0f; s1 = 0.0f; }
-      // z2[o] at lane o: four interleaved partial chains over j
-      const int orow = (lane < O ? lane : 0) * 33;
-      float zp[4] = {0.0f, 0.0f, 0.0f, 0.0f};
-#pragma unroll
-      for (int j = 0; j < 32; ++j)
-        if (j < H) zp[j & 3] = fmaf(W2s[orow + j], __shfl_sync(0xffffffffu, a1, j), zp[j & 3]);
-      const float z2 = b2s[lane] + ((zp[0] + zp[1]) + (zp[2] + zp[3]));
-      if (q == 0) PROF(13);
+      A1own[t] = j < H ? a1 : 0.0f;
+      D1[i * 32 + j] = j < H ? s1 : 0.0f;   // sigma'(z1) parked in the delta_1 row
+    }
+    __syncthreads();
+    PROF(11);
+    for (int t = tid; t < nOwn * O; t += kThreads) {
+      const int q = t / O, o = t - q * O;
+      const float *va = A1own + q * 32, *w2 = W2s + o * 33;
+      float c0 = 0.0f, c1 = 0.0f, c2 = 0.0f, c3 = 0.0f;
+      int j = 0;
+      for (; j + 4 <= H; j += 4) {
+        c0 = fmaf(w2[j], va[j], c0);
+        c1 = fmaf(w2[j + 1], va[j + 1], c1);
+        c2 = fmaf(w2[j + 2], va[j + 2], c2);
+        c3 = fmaf(w2[j + 3], va[j + 3], c3);
+      }
+      for (; j < H; ++j) c0 = fmaf(w2[j], va[j], c0);
+      const float z2 = b2s[o] + ((c0 + c1) + (c2 + c3));
       float a2, s2;
       act_fwd(p.act_o, z2, a2, s2);
-      const float yv = lane < O ? ys[q * 32 + lane] : 0.0f;
-      const float diff = lane < O ? a2 - yv : 0.0f;
-      const float d2 = diff * s2;
-      lacc += diff * diff;
-      // delta_1[j] = s1[j] * sum_o W2[o][j] d2[o];  G2[o][j] += d2[o] a1[j]
-      float t0 = 0.0f, t1 = 0.0f;
-#pragma unroll
-      for (int o = 0; o < 32; ++o) {
-        if (o < O) {
-          const float d2o = __shfl_sync(0xffffffffu, d2, o);
-          if (o & 1) t1 = fmaf(W2s[o * 33 + lane], d2o, t1);
-          else t0 = fmaf(W2s[o * 33 + lane], d2o, t0);
-          g2acc[o] = fmaf(d2o, a1, g2acc[o]);
-        }
-      }
-      const float d1 = lane < H ? (t0 + t1) * s1 : 0.0f;
-      D1[i * 32 + lane] = d1;
-      if (q == 0) PROF(14);
-      g1acc += d1;
-      gb2acc += lane < O ? d2 : 0.0f;
+      const float diff = a2 - ys[q * 32 + o];
+      lacc = fmaf(diff, diff, lacc);
+      D2own[q * 32 + o] = diff * s2;
     }
-    PROF(15);
-    // warp partials -> smem
+    __syncthreads();
+    PROF(12);
+    for (int t = tid; t < nOwn * 32; t += kThreads) {
+      const int q = t >> 5, j = t & 31, i = o0 + q;
+      const float *vd = D2own + q * 32;
+      float t0 = 0.0f, t1 = 0.0f;
+      int o = 0;
+      for (; o + 2 <= O; o += 2) {
+        t0 = fmaf(W2s[o * 33 + j], vd[o], t0);
+        t1 = fmaf(W2s[(o + 1) * 33 + j], vd[o + 1], t1);
+      }
+      if (o < O) t0 = fmaf(W2s[o * 33 + j], vd[o], t0);
+      D1[i * 32 + j] = j < H ? (t0 + t1) * D1[i * 32 + j] : 0.0f;
+    }
     {
-      float *wr = wred + warp * GP;
-#pragma unroll
-      for (int o = 0; o < 32; ++o) wr[o * 32 + lane] = g2acc[o];
-      wr[1024 + lane] = g1acc;
-      wr[1056 + lane] = gb2acc;
       const float l = warp_sum(lacc);
       if (lane == 0) lsum[warp] = l;
     }
+    ptx::fence_proxy_async_smem();
     __syncthreads();
-    for (int i = tid; i < GP; i += kThreads) {
+    PROF(4);
+
+    // ---- P4. push the owned delta_1 rows to every peer at once; then this CTA's W2/b1/b2
+    //      tendency partial over its owned rows (a 10x30x9 contraction) and its slices to
+    //      the ranks that reduce them
+    if (warp == 0 && lane < C && lane != rank && nOwn > 0)
+      ptx::bulk_s2peer(D1 + o0 * 32, D1 + o0 * 32, (uint32_t)(nOwn * 128), bar_D, lane);
+    for (int t = tid; t < nsmp; t += kThreads) {
       float v = 0.0f;
-#pragma unroll
-      for (int ww = 0; ww < kWarps; ++ww) v += wred[ww * GP + i];
-      gpart[i] = v;
+      if (t < O * H) {
+        const int o = t / H, j = t - o * H;
+        for (int q = 0; q < nOwn; ++q) v = fmaf(D2own[q * 32 + o], A1own[q * 32 + j], v);
+      } else if (t < O * H + H) {
+        const int j = t - O * H;
+        for (int q = 0; q < nOwn; ++q) v += D1[(o0 + q) * 32 + j];
+      } else if (t < nsm) {
+        const int o = t - O * H - H;
+        for (int q = 0; q < nOwn; ++q) v += D2own[q * 32 + o];
+      }
+      gpart[t] = v;
     }
     if (tid == 0 && p.step_loss) {
       float l = 0.0f;
@@ -340,138 +399,120 @@ fused_small_kernel(const FusedParams p, const __grid_constant__ CUtensorMap tmX)
     }
     ptx::fence_proxy_async_smem();
     __syncthreads();
-    PROF(4);
-
-    // ---- 3. push owned delta_1 rows to every peer; push tendency partial slices to their reducers
     if (warp == 0 && lane < C && lane != rank) {
       const int c = lane;
-      if (nOwn > 0) ptx::bulk_s2peer(D1 + o0 * 32, D1 + o0 * 32, (uint32_t)(nOwn * 128), bar_D, c);
-      const int ce0 = e_begin(c, C), cne = e_begin(c + 1, C) - ce0;
+      const int ce0 = e_begin(c, C, nsmp), cne = e_begin(c + 1, C, nsmp) - ce0;
       if (cne > 0) ptx::bulk_s2peer(grecv + rank * eslot, gpart + ce0, (uint32_t)(cne * 4), bar_D, c);
     }
     ptx::mbar_wait(bar_D, par);
     PROF(5);
+
+    // ---- P5. dW1 slice partial, k-major like W1t: Gs[k][j] = sum_{i<nS} D1[i][j] x[i][k]
+    for (int t = tid; t < nP5; t += kThreads) {
+      const int jg = t & 7, kc = (t >> 3) % nchunk, rh = (t >> 3) / nchunk;
+      const int ib = rh * nS / kRH, ie = (rh + 1) * nS / kRH;
+      const float *dcol = D1 + jg * 4;
+      const float *xcol = xs + kc * 4;
+      float a[4][4];
+#pragma unroll
+      for (int u = 0; u < 4; ++u)
+#pragma unroll
+        for (int v = 0; v < 4; ++v) a[u][v] = 0.0f;
+#pragma unroll 4
+      for (int i = ib; i < ie; ++i) {
+        const float4 d = *reinterpret_cast<const float4 *>(dcol + i * 32);
+        const float4 x = *reinterpret_cast<const float4 *>(xcol + i * wpad);
+        const float dv[4] = {d.x, d.y, d.z, d.w};
+#pragma unroll
+        for (int u = 0; u < 4; ++u) {
+          a[u][0] = fmaf(dv[u], x.x, a[u][0]);
+          a[u][1] = fmaf(dv[u], x.y, a[u][1]);
+          a[u][2] = fmaf(dv[u], x.z, a[u][2]);
+          a[u][3] = fmaf(dv[u], x.w, a[u][3]);
+        }
+      }
+      float *g = rh ? Gs2 : Gs;
+#pragma unroll
+      for (int v = 0; v < 4; ++v)
+        *reinterpret_cast<float4 *>(g + (kc * 4 + v) * 32 + jg * 4) = make_float4(a[0][v], a[1][v], a[2][v], a[3][v]);
+    }
+    __syncthreads();
+    for (int i = tid; i < wpad * 8; i += kThreads) {  // row halves summed in order
+      float4 *d = reinterpret_cast<float4 *>(Gs) + i;
+      const float4 h = reinterpret_cast<const float4 *>(Gs2)[i];
+      float4 v = *d;
+      v.x += h.x; v.y += h.y; v.z += h.z; v.w += h.w;
+      *d = v;
+    }
     // reduce my slice of the W2/b1/b2 tendencies over the cluster (rank order) -> L2
     for (int e = tid; e < ne; e += kThreads) {
       float v = 0.0f;
       for (int c = 0; c < C; ++c) v += (c == rank) ? gpart[e0 + e] : grecv[c * eslot + e];
-      const int ee = e0 + e;
-      int64_t dst = -1;
-      if (ee < 1024) {
-        const int o = ee >> 5, j = ee & 31;
-        if (o < O && j < H) dst = oW2 + (int64_t)o * H + j;
-      } else if (ee < 1056) {
-        if (ee - 1024 < H) dst = ob1 + (ee - 1024);
-      } else if (ee - 1056 < O) {
-        dst = ob2 + (ee - 1056);
-      }
-      if (dst >= 0) ptx::red_add_f32(accS + dst, v);
-    }
-    PROF(6);
-
-    // ---- 4. dW1 slice: Gs[j][k] = sum_{i<nS} D1[i][j] x[i][k]   (lane: j, warp: 16-column groups)
-    {
-      const int nchunk = wpad / 4;  // 4-column chunks
-      for (int cb = warp * 4; cb < nchunk; cb += kWarps * 4) {
-        int cc[4];
-#pragma unroll
-        for (int u = 0; u < 4; ++u) cc[u] = (cb + u < nchunk ? cb + u : cb) * 4;
-        float a[16];
-#pragma unroll
-        for (int u = 0; u < 16; ++u) a[u] = 0.0f;
-        for (int i = 0; i < nS; ++i) {
-          const float d = D1[i * 32 + lane];
-          const float *xr = xs + i * wpad;
-          float4 xv[4];
-#pragma unroll
-          for (int u = 0; u < 4; ++u) xv[u] = *reinterpret_cast<const float4 *>(xr + cc[u]);
-#pragma unroll
-          for (int u = 0; u < 4; ++u) {
-            a[4 * u + 0] = fmaf(d, xv[u].x, a[4 * u + 0]);
-            a[4 * u + 1] = fmaf(d, xv[u].y, a[4 * u + 1]);
-            a[4 * u + 2] = fmaf(d, xv[u].z, a[4 * u + 2]);
-            a[4 * u + 3] = fmaf(d, xv[u].w, a[4 * u + 3]);
-          }
-        }
-        if (lane < H) {
-#pragma unroll
-          for (int u = 0; u < 4; ++u)
-            if (cb + u < nchunk)
-              *reinterpret_cast<float4 *>(Gs + lane * wpad + cc[u]) =
-                  make_float4(a[4 * u + 0], a[4 * u + 1], a[4 * u + 2], a[4 * u + 3]);
-        }
-      }
+      ptx::red_add_f32(accS + p.small_off + e0 + e, v);
     }
     ptx::fence_proxy_async_smem();
     __syncthreads();
-    PROF(7);
-    // co_sum: add this CTA's dW1 slice into the L2 accumulator
+    PROF(6);
+
+    // ---- P6. co_sum: add this CTA's dW1 slice into the L2 accumulator (the paper's co_sum)
     if (p.aligned) {
-      if (warp == 0) {
-        if (lane < H) {
-          ptx::fence_proxy_async_global();
-          ptx::bulk_reduce_add_f32(accS + oW1 + (int64_t)lane * n0 + k0, Gs + lane * wpad, (uint32_t)(w * 4));
-          ptx::bulk_commit();
-          ptx::bulk_wait_all();
-          ptx::fence_proxy_async_global();
-        }
-        __syncwarp();
+      if (tid == 0) {
+        ptx::fence_proxy_async_global();
+        ptx::bulk_reduce_add_f32(accS + slice_off, Gs, (uint32_t)(p.ws * 32 * 4));
+        ptx::bulk_commit();
+        ptx::bulk_wait_all();
+        ptx::fence_proxy_async_global();
       }
     } else {
-      for (int j = warp; j < H; j += kWarps) {
-        float *dst = accS + oW1 + (int64_t)j * n0 + k0;
-        for (int k = lane; k < w; k += 32) ptx::red_add_f32(dst + k, Gs[j * wpad + k]);
-      }
+      for (int i = tid; i < w * 32; i += kThreads)
+        if ((i & 31) < H) ptx::red_add_f32(accS + slice_off + i, Gs[i]);
     }
+    PROF(7);
+
+    // ---- P7. grid barrier: the co_sum of this step is complete.  Between arrive and wait,
+    //      zero this CTA's share of the slot used two steps ahead (its last readers finished
+    //      before the previous barrier; its next writers start after the next one).
+    __syncthreads();
+    if (tid == 0) ptx::grid_arrive(p.bar);
+    {
+      float *z = p.acc + ((s + 2) % kSlots) * p.slot;
+      for (int64_t i = (int64_t)blockIdx.x * kThreads + tid; i < p.slot; i += (int64_t)nCTA * kThreads) z[i] = 0.0f;
+    }
+    if (tid == 0) ptx::grid_wait(p.bar, (unsigned)((s + 1) * nCTA));
+    __syncthreads();
     PROF(8);
 
-    // ---- 5. grid barrier (the co_sum is complete), then the SGD update of the resident parameters
-    ptx::grid_barrier(p.bar, (unsigned)((s + 1) * nCTA));
-    PROF(9);
-    // reduced dW1 slice rows (coalesced along k; 16 independent loads per lane) -> Gt[k][j]
-    for (int tb = 0; tb * 128 < w; ++tb) {
-      float v[4][4];
-#pragma unroll
-      for (int m = 0; m < 4; ++m)
-#pragma unroll
-        for (int t = 0; t < 4; ++t) {
-          const int j = warp + kWarps * m, k = tb * 128 + lane + 32 * t;
-          v[m][t] = (j < H && k < w) ? accS[oW1 + (int64_t)j * n0 + k0 + k] : 0.0f;  // L1 invalidated by the barrier
-        }
-#pragma unroll
-      for (int m = 0; m < 4; ++m)
-#pragma unroll
-        for (int t = 0; t < 4; ++t) {
-          const int j = warp + kWarps * m, k = tb * 128 + lane + 32 * t;
-          if (j < H && k < w) Gt[k * 33 + j] = v[m][t];
-        }
+    // ---- P8. read the reduced slice and the W2/b block back
+    if (p.aligned) {
+      if (tid == 0) {
+        ptx::fence_proxy_async_global();
+        ptx::mbar_arrive_expect_tx(bar_G, bytesG);
+        ptx::bulk_g2s(Gr, accS + slice_off, (uint32_t)(p.ws * 32 * 4), bar_G);
+        ptx::bulk_g2s(gsm, accS + p.small_off, (uint32_t)(nsmp * 4), bar_G);
+      }
+      ptx::mbar_wait(bar_G, par);
+    } else {
+      for (int i = tid; i < w * 32; i += kThreads) Gr[i] = accS[slice_off + i];
+      for (int i = tid; i < nsmp; i += kThreads) gsm[i] = accS[p.small_off + i];
+      __syncthreads();
     }
-    float gl[2];
-#pragma unroll
-    for (int u = 0; u < 2; ++u) {
-      const int e = tid + u * kThreads;
-      gl[u] = e < H + O * H + O ? accS[ob1 + e] : 0.0f;
+    PROF(9);
+
+    // ---- P9. SGD update of the resident parameters (all clusters apply the same sums)
+    for (int i = tid; i < w * 8; i += kThreads) {
+      float4 wv = reinterpret_cast<float4 *>(W1t)[i];
+      const float4 gv = reinterpret_cast<const float4 *>(Gr)[i];
+      wv.x -= p.scale * gv.x; wv.y -= p.scale * gv.y; wv.z -= p.scale * gv.z; wv.w -= p.scale * gv.w;
+      reinterpret_cast<float4 *>(W1t)[i] = wv;   // pad neurons j >= H: G = 0, W stays 0
+    }
+    for (int e = tid; e < nsm; e += kThreads) {
+      const float gv = p.scale * gsm[e];
+      if (e < O * H) { const int o = e / H; W2s[o * 33 + (e - o * H)] -= gv; }
+      else if (e < O * H + H) b1s[e - O * H] -= gv;
+      else b2s[e - O * H - H] -= gv;
     }
     __syncthreads();
     PROF(10);
-    for (int i = tid; i < w * 32; i += kThreads) {
-      const int k = i >> 5, j = i & 31;
-      if (j < H) W1t[i] -= p.scale * Gt[k * 33 + j];
-    }
-    for (int e = tid; e < H + O * H + O; e += kThreads) {
-      const float gsum = e < kThreads ? gl[0] : (e < 2 * kThreads ? gl[1] : accS[ob1 + e]);
-      if (e < H) b1s[e] -= p.scale * gsum;
-      else if (e < H + O * H) { const int f = e - H; W2s[(f / H) * 33 + f % H] -= p.scale * gsum; }
-      else b2s[e - H - O * H] -= p.scale * gsum;
-    }
-    // zero the accumulator used two steps ahead (its readers finished before this barrier)
-    {
-      float *z = p.acc + ((s + 2) % 3) * npad;
-      const int64_t bid = blockIdx.x;
-      for (int64_t i = bid * kThreads + tid; i < np; i += (int64_t)nCTA * kThreads) z[i] = 0.0f;
-    }
-    __syncthreads();
-    PROF(11);
   }
   cp_async_wait0();
 
@@ -575,9 +616,11 @@ int fused_small_train_steps(FusedSmall &fs, cudaStream_t st, const std::vector<i
     return -1;
   }
 
-  const int64_t np = (int64_t)H * n0 + H + (int64_t)O * H + O;
-  const int64_t npad = (np + 3) & ~int64_t(3);
-  const size_t need = 3 * npad * sizeof(float) + 256 + n_steps * sizeof(int64_t);
+  // accumulator slot: [C][ws][32] dW1 slices (k-major), then the W2/b1/b2 block (16-B aligned)
+  const int nsmp = (O * H + H + O + 3) & ~3;
+  const int64_t small_off = (int64_t)C * ws * 32;
+  const int64_t slot = (small_off + nsmp + 31) & ~int64_t(31);
+  const size_t need = kSlots * slot * sizeof(float) + 256 + n_steps * sizeof(int64_t);
   if (fs.ws_bytes < need) {
     if (fs.ws) cudaFree(fs.ws);
     fs.ws = nullptr;
@@ -594,23 +637,26 @@ int fused_small_train_steps(FusedSmall &fs, cudaStream_t st, const std::vector<i
   p.B = (int)batch; p.G = G; p.ws = ws; p.wpad = wpad; p.aligned = aligned ? 1 : 0;
   p.nSmax = nSmax; p.nOwnMax = nOwnMax;
   p.n_steps = n_steps;
+  p.slot = slot;
+  p.small_off = small_off;
+  p.nsmp = nsmp;
   p.scale = (float)((double)eta / (double)batch);
   p.inv_B = (float)(1.0 / (double)batch);
   p.X = X; p.Y = Y; p.params = params;
   p.acc = reinterpret_cast<float *>(base);
-  p.bar = reinterpret_cast<unsigned *>(base + 3 * npad * sizeof(float));
-  int64_t *dstarts = reinterpret_cast<int64_t *>(base + 3 * npad * sizeof(float) + 256);
+  p.bar = reinterpret_cast<unsigned *>(base + kSlots * slot * sizeof(float));
+  int64_t *dstarts = reinterpret_cast<int64_t *>(base + kSlots * slot * sizeof(float) + 256);
   p.starts = dstarts;
   p.step_loss = step_loss;
-  static unsigned long long *prof_buf = nullptr;
+  static long long *prof_buf = nullptr;
   const bool prof = env_int("NF_FUSED_PROF", 0) != 0;
   if (prof) {
-    if (!prof_buf) cudaMalloc(&prof_buf, sizeof(unsigned long long) * 148 * 64 * kProf);
-    cudaMemsetAsync(prof_buf, 0, sizeof(unsigned long long) * 148 * 64 * kProf, st);
+    if (!prof_buf) cudaMalloc(&prof_buf, sizeof(long long) * 148 * 64 * kProf);
+    cudaMemsetAsync(prof_buf, 0, sizeof(long long) * 148 * 64 * kProf, st);
     p.prof = prof_buf;
   }
 
-  cudaError_t e = cudaMemsetAsync(base, 0, 3 * npad * sizeof(float) + 256, st);
+  cudaError_t e = cudaMemsetAsync(base, 0, kSlots * slot * sizeof(float) + 256, st);
   if (e == cudaSuccess)
     e = cudaMemcpyAsync(dstarts, starts, n_steps * sizeof(int64_t), cudaMemcpyHostToDevice, st);
   if (e == cudaSuccess && step_loss) e = cudaMemsetAsync(step_loss, 0, n_steps * sizeof(float), st);
@@ -633,39 +679,53 @@ int fused_small_train_steps(FusedSmall &fs, cudaStream_t st, const std::vector<i
     return -1;
   }
   if (prof) {
-    std::vector<unsigned long long> h((size_t)G * C * 64 * kProf);
+    std::vector<long long> h((size_t)G * C * 64 * kProf);
     cudaStreamSynchronize(st);
-    cudaMemcpy(h.data(), prof_buf, h.size() * sizeof(unsigned long long), cudaMemcpyDeviceToHost);
+    cudaMemcpy(h.data(), prof_buf, h.size() * sizeof(long long), cudaMemcpyDeviceToHost);
+    int dev = 0, khz = 0;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&khz, cudaDevAttrClockRate, dev);
+    const double ns_per_clk = khz > 0 ? 1e6 / khz : 0.5;
     const int ns = (int)std::min<int64_t>(n_steps, 64);
-    // slot order in time; CTA-local deltas between consecutive recorded slots
-    const int order[16] = {0, 1, 2, 3, 12, 13, 14, 15, 4, 5, 6, 7, 8, 9, 10, 11};
-    const int nslot = 16;
+    const int nslot = 11;
     double ph[kProf] = {0}, phmax[kProf] = {0};
     int cnt = 0;
     for (int s = 2; s + 1 < ns; ++s, ++cnt) {
       for (int i = 0; i < nslot; ++i) {
         double mx = 0, sum = 0;
         for (int b = 0; b < G * C; ++b) {
-          const unsigned long long *t = &h[((size_t)b * 64 + s) * kProf];
-          const unsigned long long a = t[order[i]];
-          const unsigned long long nxt = i < nslot - 1 ? t[order[i + 1]] : h[((size_t)b * 64 + s + 1) * kProf];
+          const long long *t = &h[((size_t)b * 64 + s) * kProf];
+          const long long a = t[i];
+          const long long nxt = i < nslot - 1 ? t[i + 1] : h[((size_t)b * 64 + s + 1) * kProf];
           const double d = (a && nxt) ? (double)(nxt - a) : 0.0;
           sum += d; mx = std::max(mx, d);
         }
         ph[i] += sum / (G * C); phmax[i] += mx;
       }
     }
-    fprintf(stderr, "[fused prof] C=%d G=%d nS<=%d ws=%d aligned=%d smem=%zu  phase ns (mean over CTAs / max):\n",
-            C, G, nSmax, ws, (int)aligned, smem);
-    const char *names[16] = {"wait_x+issue", "z1_partial", "push_P+wait", "row:z_sum", "row:z2", "row:delta",
-                             "rows_rest", "owned_sums", "push_D+wait", "gpart_red", "dW1", "co_sum_red",
-                             "grid_bar", "acc_loads", "update", "tail"};
+    fprintf(stderr, "[fused prof] C=%d G=%d nS<=%d ws=%d aligned=%d smem=%zu  phase clk (mean over CTAs / max), "
+            "ns at %.0f MHz:\n", C, G, nSmax, ws, (int)aligned, smem, khz / 1e3);
+    const char *names[11] = {"P0 wait_x+issue", "P1 z1_partial", "P2 push_P+wait", "P3 owned_rows",
+                             "P4 push_D+gpart", "P5 dW1+small_red", "P6 co_sum_bulk", "P7 grid_bar",
+                             "P8 readback", "P9 update+zero", "tail"};
     double tot = 0;
     for (int i = 0; i < nslot; ++i) {
-      fprintf(stderr, "  %-14s %8.0f %8.0f\n", names[i], ph[i] / cnt, phmax[i] / cnt);
+      fprintf(stderr, "  %-18s %8.0f clk %8.0f max  %7.0f ns\n", names[i], ph[i] / cnt, phmax[i] / cnt,
+              ph[i] / cnt * ns_per_clk);
       tot += ph[i] / cnt;
     }
-    fprintf(stderr, "  %-14s %8.0f\n", "step", tot);
+    fprintf(stderr, "  %-18s %8.0f clk            %7.0f ns\n", "step", tot, tot * ns_per_clk);
+    {  // sub-phases of P3: slots 3 -> 11 -> 12 -> 4
+      double a = 0, b = 0, c = 0;
+      int n = 0;
+      for (int s = 2; s + 1 < ns; ++s)
+        for (int bl = 0; bl < G * C; ++bl, ++n) {
+          const long long *t = &h[((size_t)bl * 64 + s) * kProf];
+          a += (double)(t[11] - t[3]); b += (double)(t[12] - t[11]); c += (double)(t[4] - t[12]);
+        }
+      fprintf(stderr, "  P3 split: (a) z1/act %.0f clk, (b) layer 2 %.0f clk, (c) delta_1+loss %.0f clk\n", a / n, b / n,
+              c / n);
+    }
   }
   return 0;
 }

@@ -16,7 +16,7 @@ __device__ __forceinline__ void act_fwd(int kind, float z, float &a, float &s) {
   switch (kind) {
     case ACT_SIGMOID: {            // t = e^{-|z|}:  sigma = 1/(1+t) or t/(1+t);  sigma' = t/(1+t)^2
       const float t = expf(-fabsf(z));
-      const float r = 1.0f / (1.0f + t);
+      const float r = __frcp_rn(1.0f + t);  // == 1.0f / (1.0f + t), correctly rounded
       a = z >= 0.0f ? r : t * r;
       s = t * r * r;
       break;
@@ -24,7 +24,7 @@ __device__ __forceinline__ void act_fwd(int kind, float z, float &a, float &s) {
     case ACT_TANH: {               // sigma' = sech^2 z = 4t/(1+t)^2, t = e^{-2|z|}
       a = tanhf(z);
       const float t = expf(-2.0f * fabsf(z));
-      const float r = 1.0f / (1.0f + t);
+      const float r = __frcp_rn(1.0f + t);  // == 1.0f / (1.0f + t), correctly rounded
       s = 4.0f * t * r * r;
       break;
     }
@@ -59,7 +59,7 @@ __device__ __forceinline__ float act_only(int kind, float z) {
   switch (kind) {
     case ACT_SIGMOID: {
       const float t = expf(-fabsf(z));
-      const float r = 1.0f / (1.0f + t);
+      const float r = __frcp_rn(1.0f + t);  // == 1.0f / (1.0f + t), correctly rounded
       return z >= 0.0f ? r : t * r;
     }
     case ACT_TANH: return tanhf(z);

@@ -112,6 +112,17 @@ __device__ __forceinline__ uint32_t cluster_size() {
 __device__ __forceinline__ void red_add_f32(float *p, float v) {
   asm volatile("red.relaxed.gpu.global.add.f32 [%0], %1;" ::"l"(p), "f"(v) : "memory");
 }
+// split grid barrier (one thread per CTA): arrive publishes everything the CTA wrote before
+// (release, after a __syncthreads), wait spins until all CTAs of this generation arrived
+__device__ __forceinline__ void grid_arrive(unsigned *ctr) {
+  asm volatile("red.release.gpu.global.add.u32 [%0], 1;" ::"l"(ctr) : "memory");
+}
+__device__ __forceinline__ void grid_wait(unsigned *ctr, unsigned target) {
+  unsigned v;
+  do {
+    asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(ctr) : "memory");
+  } while (v < target);
+}
 // grid-wide barrier on a monotonically increasing counter (all CTAs co-resident)
 __device__ __forceinline__ void grid_barrier(unsigned *ctr, unsigned target) {
   __syncthreads();
