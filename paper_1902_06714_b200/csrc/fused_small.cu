@@ -34,6 +34,7 @@
 #include <cstring>
 
 #include "fused_small.cuh"
+#include "gemm_tc.cuh"
 #include "kernels.cuh"
 #include "nf_common.cuh"
 #include "sm100_ptx.cuh"
@@ -52,6 +53,17 @@ constexpr int kRG = 5;         // rows per P1 register tile
 constexpr int kKP = 4;         // P1: K (pixel) range split in kKP parts across threads
 constexpr int kRH = 2;         // P5: rows split in kRH parts across threads
 constexpr int kProf = 16;      // profiler slots per step
+// Tensor-core variant (TC): x tiles of kTcRows rows x 4 atoms of 32 pixels, staged twice per
+// step by TMA in the two smem layouts the tensor core needs (K-major SWIZZLE_128B for Z1,
+// MN-major SWIZZLE_128B_BASE32B for dW1), split in place into TF32 hi + fp32 lo.
+constexpr int kTcRows = 72;                     // x rows per tile (>= rows per cluster), 9 K-steps
+constexpr int kTcAS = kTcRows * 128;            // bytes per 32-pixel atom
+constexpr int kTcXLoK = 44032;                  // K-phase lo offset (hi reads 128 rows per atom)
+constexpr int kTcXLoM = 4 * kTcAS;              // M-phase lo offset
+constexpr int kTcXBytes = kTcXLoK + 3 * kTcAS + 128 * 128;  // 88064
+constexpr int kTcWBytes = 2 * 4 * 32 * 128;     // W1 slice hi | lo, K-major [32 j][128 px]
+constexpr int kTcDBytes = 2 * kTcAS;            // delta_1 hi | lo, MN-major [72 rows][32 j]
+constexpr int kTcBytes = kTcXBytes + kTcWBytes + kTcDBytes;
 constexpr int kSmall = 32 * 32 + 64;  // capacity of the W2/b1/b2 tendency block: O*H + H + O <= 1088
 constexpr int kSlots = 4;             // accumulator ring: step s uses slot s % 4; slot (s+2) % 4 is
                                       // zeroed between this step's barrier arrive and wait
@@ -95,23 +107,24 @@ __device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commi
 __device__ __forceinline__ void cp_async_wait0() { asm volatile("cp.async.wait_group 0;" ::: "memory"); }
 
 struct Smem {  // offsets in floats from the 128-B aligned base
-  int W1t, W2s, b1s, b2s, xs, ys, Ppart, Pown, D1, A1own, D2own, gpart, grecv, Gs, Gs2, Gr, gsm, lsum, total;
+  int tcr, W1t, W2s, b1s, b2s, xs, ys, Ppart, Pown, D1, A1own, D2own, gpart, grecv, Gs, Gs2, Gr, gsm, lsum, total;
 };
 
 __host__ __device__ inline int al32(int v) { return (v + 31) & ~31; }  // 128-B alignment in floats
 
 __host__ __device__ inline int xrows(int nSmax) { return (nSmax + kRG - 1) / kRG * kRG; }
 
-__host__ __device__ inline Smem smem_layout(int wpad, int nSmax, int nOwnMax, int C) {
+__host__ __device__ inline Smem smem_layout(int wpad, int nSmax, int nOwnMax, int C, bool tc) {
   Smem L;
-  int o = 32;  // mbarriers live in the first 128 B
-  L.W1t = o;   o = al32(o + wpad * 32);            // [wpad][32]: W1 slice, k-major
+  int o = 32;  // mbarriers (and the TMEM address) live in the first 128 B
+  L.tcr = o;   o = al32(o + (tc ? (kTcBytes + 1024) / 4 : 0));  // TC operand tiles (1024-B aligned inside)
+  L.W1t = o;   o = al32(o + (tc ? 0 : wpad * 32));  // [wpad][32]: W1 slice, k-major (SIMT variant)
   L.W2s = o;   o = al32(o + 32 * 33);              // [32][33]
   L.b1s = o;   o += 32;
   L.b2s = o;   o = al32(o + 32);
-  L.xs = o;    o = al32(o + 2 * al32(xrows(nSmax) * wpad));  // 2 TMA destinations
+  L.xs = o;    o = al32(o + (tc ? 0 : 2 * al32(xrows(nSmax) * wpad)));  // 2 TMA destinations (SIMT)
   L.ys = o;    o = al32(o + 2 * nOwnMax * 32);
-  L.Ppart = o; o = al32(o + kKP * xrows(nSmax) * 32);  // P1 K-part partials; part 0 = Pfull
+  L.Ppart = o; o = al32(o + (tc ? 1 : kKP) * xrows(nSmax) * 32);  // P1 K-part partials; part 0 = Pfull
   L.Pown = o;  o = al32(o + C * nOwnMax * 32);
   L.D1 = o;    o = al32(o + nSmax * 32);
   L.A1own = o; o = al32(o + nOwnMax * 32);         // a1 of the owned rows
@@ -119,7 +132,7 @@ __host__ __device__ inline Smem smem_layout(int wpad, int nSmax, int nOwnMax, in
   L.gpart = o; o = al32(o + kSmall);
   L.grecv = o; o = al32(o + C * e_slot(C));
   L.Gs = o;    o = al32(o + wpad * 32);            // [wpad][32]: dW1 slice partial, k-major like W1t
-  L.Gs2 = o;   o = al32(o + wpad * 32);            // second row-half partial
+  L.Gs2 = o;   o = al32(o + (tc ? 0 : wpad * 32)); // second row-half partial (SIMT)
   L.Gr = o;    o = al32(o + wpad * 32);            // reduced slice read back
   L.gsm = o;   o = al32(o + kSmall);               // reduced W2/b block read back
   L.lsum = o;  o = al32(o + kWarps);
@@ -127,8 +140,23 @@ __host__ __device__ inline Smem smem_layout(int wpad, int nSmax, int nOwnMax, in
   return L;
 }
 
+// byte offset of element (row r, column c < 32) inside a 32-column atom of 128-B rows
+__device__ __forceinline__ int sw128_k(int r, int c) { return r * 128 + ((((c >> 2) ^ (r & 7))) << 4) + ((c & 3) << 2); }
+__device__ __forceinline__ int sw128_32b(int r, int c) { return r * 128 + ((((c >> 3) ^ (r & 3))) << 5) + ((c & 7) << 2); }
+// in-place TF32 split of `bytes` of staged fp32 data: hi = rn_tf32(x) in place, lo = x - hi (exact)
+__device__ __forceinline__ void tc_split(uint8_t *hi, uint8_t *lo, int bytes, int tid) {
+  for (int i = tid; i < bytes / 16; i += kThreads) {
+    const float4 x = reinterpret_cast<const float4 *>(hi)[i];
+    const float4 h = make_float4(tc::tf32_hi(x.x), tc::tf32_hi(x.y), tc::tf32_hi(x.z), tc::tf32_hi(x.w));
+    reinterpret_cast<float4 *>(hi)[i] = h;
+    reinterpret_cast<float4 *>(lo)[i] = make_float4(x.x - h.x, x.y - h.y, x.z - h.z, x.w - h.w);
+  }
+}
+
+template <bool TC>
 __global__ void __launch_bounds__(kThreads, 1)
-fused_small_kernel(const FusedParams p, const __grid_constant__ CUtensorMap tmX) {
+fused_small_kernel(const FusedParams p, const __grid_constant__ CUtensorMap tmX,
+                   const __grid_constant__ CUtensorMap tmXK, const __grid_constant__ CUtensorMap tmXM) {
   extern __shared__ __align__(128) float sm[];
   const int C = (int)ptx::cluster_size();
   const int rank = (int)ptx::cluster_rank();
@@ -154,12 +182,18 @@ fused_small_kernel(const FusedParams p, const __grid_constant__ CUtensorMap tmX)
   const int e0 = e_begin(rank, C, nsmp), ne = e_begin(rank + 1, C, nsmp) - e0;
   const int eslot = e_slot(C);
 
-  const Smem L = smem_layout(wpad, p.nSmax, p.nOwnMax, C);
+  const Smem L = smem_layout(wpad, p.nSmax, p.nOwnMax, C, TC);
   const int xstride = al32(xrows(p.nSmax) * wpad);
   uint64_t *bar_x = reinterpret_cast<uint64_t *>(sm);  // [2]
   uint64_t *bar_P = bar_x + 2;
   uint64_t *bar_D = bar_x + 3;
   uint64_t *bar_G = bar_x + 4;
+  uint64_t *bar_mma = bar_x + 5;             // TC: tcgen05.commit arrivals (2 per step)
+  uint32_t *tmem_slot = reinterpret_cast<uint32_t *>(bar_x + 6);
+  // TC operand tiles (1024-B aligned): X (x tile, K- or MN-phase), Wt (W1 hi|lo), Dt (delta_1 hi|lo)
+  uint8_t *X = reinterpret_cast<uint8_t *>((reinterpret_cast<uintptr_t>(sm + L.tcr) + 1023) & ~uintptr_t(1023));
+  uint8_t *Wt = X + kTcXBytes, *Dt = Wt + kTcWBytes;
+  const uint32_t sX = ptx::smem_u32(X), sW = ptx::smem_u32(Wt), sD = ptx::smem_u32(Dt);
   float *W1t = sm + L.W1t, *W2s = sm + L.W2s, *b1s = sm + L.b1s, *b2s = sm + L.b2s;
   float *xs0 = sm + L.xs, *ys0 = sm + L.ys, *Pfull = sm + L.Ppart, *Pown = sm + L.Pown;
   const int pstride = xrows(p.nSmax) * 32;  // floats between P1 K-part buffers
@@ -179,13 +213,37 @@ fused_small_kernel(const FusedParams p, const __grid_constant__ CUtensorMap tmX)
     ptx::mbar_init(bar_P, 1);
     ptx::mbar_init(bar_D, 1);
     ptx::mbar_init(bar_G, 1);
+    ptx::mbar_init(bar_mma, 1);
     ptx::fence_mbar_init();
     if (p.aligned) ptx::prefetch_tensormap(&tmX);
+    if (TC) {
+      ptx::prefetch_tensormap(&tmXK);
+      ptx::prefetch_tensormap(&tmXM);
+    }
   }
+  if (TC && warp == 0) {  // 64 TMEM columns: Z1 partial accumulator | dW1 accumulator
+    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;"
+                 ::"r"(ptx::smem_u32(tmem_slot)), "r"(64u) : "memory");
+    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;" ::: "memory");
+  }
+  tc::tc_fence_before();
   __syncthreads();
-  for (int i = tid; i < w * 32; i += kThreads) {
-    const int k = i >> 5, j = i & 31;
-    if (j < H) W1t[i] = p.params[oW1 + (int64_t)j * n0 + k0 + k];
+  tc::tc_fence_after();
+  const uint32_t tmem = TC ? *tmem_slot : 0u;
+  if (TC) {  // W1 slice as TF32 hi + fp32 lo in the K-major SWIZZLE_128B B-operand layout
+    for (int i = tid; i < 32 * 128; i += kThreads) {
+      const int j = i >> 7, k = i & 127;
+      const float v = (j < H && k < w) ? p.params[oW1 + (int64_t)j * n0 + k0 + k] : 0.0f;
+      const float h = tc::tf32_hi(v);
+      const int off = (k >> 5) * 4096 + sw128_k(j, k & 31);
+      *reinterpret_cast<float *>(Wt + off) = h;
+      *reinterpret_cast<float *>(Wt + 16384 + off) = v - h;
+    }
+  } else {
+    for (int i = tid; i < w * 32; i += kThreads) {
+      const int k = i >> 5, j = i & 31;
+      if (j < H) W1t[i] = p.params[oW1 + (int64_t)j * n0 + k0 + k];
+    }
   }
   for (int i = tid; i < O * H; i += kThreads) W2s[(i / H) * 33 + i % H] = p.params[oW2 + i];
   for (int i = tid; i < H; i += kThreads) b1s[i] = p.params[ob1 + i];
@@ -210,7 +268,9 @@ fused_small_kernel(const FusedParams p, const __grid_constant__ CUtensorMap tmX)
     const int64_t row0 = next_start + r0;
     next_start = s + 1 < p.n_steps ? p.starts[s + 1] : 0;
     float *xs = xs0 + buf * xstride;
-    if (p.aligned) {
+    if (TC) {
+      // x tiles are staged by tc_issue (two layouts per step)
+    } else if (p.aligned) {
       if (tid == 0) {
         ptx::mbar_arrive_expect_tx(&bar_x[buf], xbytes);
         ptx::tma_load_2d(xs, &tmX, &bar_x[buf], k0, (int)row0);
@@ -229,7 +289,21 @@ fused_small_kernel(const FusedParams p, const __grid_constant__ CUtensorMap tmX)
     cp_async_commit();
   };
 
+  // TC: stage the x tile of a step in one layout: four {32 px, kTcRows rows} boxes
+  auto tc_issue = [&](const CUtensorMap *map, uint64_t *bar, int64_t row0) {
+    ptx::mbar_arrive_expect_tx(bar, 4u * kTcAS);
+#pragma unroll
+    for (int a = 0; a < 4; ++a) ptx::tma_load_2d(X + a * kTcAS, map, bar, k0 + 32 * a, (int)row0);
+  };
+  int64_t row_s = next_start + r0;  // first row of step s's batch slice for this cluster
   prefetch(0);
+  if (TC && p.n_steps > 0) {  // step 0's K-layout tile
+    if (tid == 0) tc_issue(&tmXK, &bar_x[0], row_s);
+    ptx::mbar_wait(&bar_x[0], 0);
+    tc_split(X, X + kTcXLoK, 4 * kTcAS, tid);
+    ptx::fence_proxy_async_smem();
+    __syncthreads();
+  }
 
   // P1 task geometry: kRG-row x 4-neuron tiles, K in kKP parts of 4-pixel chunks
   const int RG = (nS + kRG - 1) / kRG;
@@ -249,56 +323,88 @@ fused_small_kernel(const FusedParams p, const __grid_constant__ CUtensorMap tmX)
       ptx::mbar_arrive_expect_tx(bar_D, bytesD);
     }
     cp_async_wait0();
-    if (p.aligned) ptx::mbar_wait(&bar_x[buf], (uint32_t)((s >> 1) & 1));
+    if (!TC && p.aligned) ptx::mbar_wait(&bar_x[buf], (uint32_t)((s >> 1) & 1));
     __syncthreads();
+    const int64_t row_s1 = next_start + r0;  // step s+1's first row (valid if s+1 < n_steps)
     if (s + 1 < p.n_steps) prefetch(s + 1);
     PROF(1);
 
     // ---- P1. partial Z1: P[i][j] = sum_{k<w} x[i][k] W1[j][k0+k]
-    for (int t = tid; t < kKP * RG * 8; t += kThreads) {
-      const int jg = t & 7, rg = (t >> 3) % RG, kp = (t >> 3) / RG;
-      const int cb = kp * nchunk / kKP, ce = (kp + 1) * nchunk / kKP;
-      const float *xr = xs + rg * kRG * wpad;
-      const float *wr = W1t + jg * 4;
-      float a[kRG][4];
+    if constexpr (TC) {
+      // 3xTF32 on the tensor core: D[row][j] (TMEM cols 0..31), M = 128 rows, N = 32, K = pixels
+      if (tid == 0) {
+        tc::tc_fence_after();
+        constexpr uint32_t idK = tc::idesc_tf32(128, 32, false, false);
+        const int nks = (p.ws + 7) / 8;
+        for (int ks = 0; ks < nks; ++ks) {
+          const uint32_t ao = (ks >> 2) * kTcAS + (ks & 3) * 32, bo = (ks >> 2) * 4096 + (ks & 3) * 32;
+          const uint64_t ah = tc::smem_desc(sX + ao, 16, 1024, 2), al = tc::smem_desc(sX + kTcXLoK + ao, 16, 1024, 2);
+          const uint64_t bh = tc::smem_desc(sW + bo, 16, 1024, 2), bl = tc::smem_desc(sW + 16384 + bo, 16, 1024, 2);
+          tc::mma_tf32(tmem, ah, bh, idK, ks > 0 ? 1u : 0u);
+          tc::mma_tf32(tmem, ah, bl, idK, 1u);
+          tc::mma_tf32(tmem, al, bh, idK, 1u);
+        }
+        tc::mma_commit(bar_mma);
+      }
+      PROF(13);
+      ptx::mbar_wait(bar_mma, 0);
+      tc::tc_fence_after();
+      PROF(14);
+      if (tid == 0) tc_issue(&tmXM, &bar_x[1], row_s);  // the MMAs are done with the K-layout tile
+      if (warp < 4) {
+        float v[32];
+        tc::tmem_ld32(tmem + ((uint32_t)(32 * warp) << 16), v);
+        const int r = 32 * warp + lane;
+        if (r < nS) {
 #pragma unroll
-      for (int u = 0; u < kRG; ++u)
-#pragma unroll
-        for (int v = 0; v < 4; ++v) a[u][v] = 0.0f;
-#pragma unroll 2
-      for (int c = cb; c < ce; ++c) {
-        float4 xv[kRG], wv[4];
-#pragma unroll
-        for (int u = 0; u < kRG; ++u) xv[u] = *reinterpret_cast<const float4 *>(xr + u * wpad + 4 * c);
-#pragma unroll
-        for (int q = 0; q < 4; ++q) wv[q] = *reinterpret_cast<const float4 *>(wr + (4 * c + q) * 32);
-#pragma unroll
-        for (int u = 0; u < kRG; ++u) {
-          const float xq[4] = {xv[u].x, xv[u].y, xv[u].z, xv[u].w};
-#pragma unroll
-          for (int q = 0; q < 4; ++q) {
-            a[u][0] = fmaf(xq[q], wv[q].x, a[u][0]);
-            a[u][1] = fmaf(xq[q], wv[q].y, a[u][1]);
-            a[u][2] = fmaf(xq[q], wv[q].z, a[u][2]);
-            a[u][3] = fmaf(xq[q], wv[q].w, a[u][3]);
-          }
+          for (int j = 0; j < 32; j += 4)
+            *reinterpret_cast<float4 *>(Pfull + r * 32 + j) = make_float4(v[j], v[j + 1], v[j + 2], v[j + 3]);
         }
       }
-      float *dst = Pfull + kp * pstride;
+      tc::tc_fence_before();
+    } else {
+    // ---- P1. partial Z1: P[i][j] = sum_{k<w} x[i][k] W1[j][k0+k]
+      for (int t = tid; t < kKP * RG * 8; t += kThreads) {
+        const int jg = t & 7, rg = (t >> 3) % RG, kp = (t >> 3) / RG;
+        const int cb = kp * nchunk / kKP, ce = (kp + 1) * nchunk / kKP;
+        const float *xr = xs + rg * kRG * wpad;
+        const float *wr = W1t + jg * 4;
+        float2 a[kRG][2];  // neuron pairs (4jg, 4jg+1), (4jg+2, 4jg+3): packed FFMA2
 #pragma unroll
-      for (int u = 0; u < kRG; ++u)
-        *reinterpret_cast<float4 *>(dst + (rg * kRG + u) * 32 + jg * 4) = make_float4(a[u][0], a[u][1], a[u][2], a[u][3]);
-    }
-    __syncthreads();
-    for (int i = tid; i < nS * 8; i += kThreads) {  // parts summed in order 0 + 1 + 2 + 3
-      float4 *d = reinterpret_cast<float4 *>(Pfull) + i;
-      float4 v = *d;
+        for (int u = 0; u < kRG; ++u) a[u][0] = a[u][1] = make_float2(0.0f, 0.0f);
+#pragma unroll 2
+        for (int c = cb; c < ce; ++c) {
+          float4 xv[kRG], wv[4];
 #pragma unroll
-      for (int kp = 1; kp < kKP; ++kp) {
-        const float4 h = reinterpret_cast<const float4 *>(Pfull + kp * pstride)[i];
-        v.x += h.x; v.y += h.y; v.z += h.z; v.w += h.w;
+          for (int u = 0; u < kRG; ++u) xv[u] = *reinterpret_cast<const float4 *>(xr + u * wpad + 4 * c);
+#pragma unroll
+          for (int q = 0; q < 4; ++q) wv[q] = *reinterpret_cast<const float4 *>(wr + (4 * c + q) * 32);
+#pragma unroll
+          for (int u = 0; u < kRG; ++u) {
+            const float xq[4] = {xv[u].x, xv[u].y, xv[u].z, xv[u].w};
+#pragma unroll
+            for (int q = 0; q < 4; ++q) {
+              ffma2(a[u][0], xq[q], make_float2(wv[q].x, wv[q].y));
+              ffma2(a[u][1], xq[q], make_float2(wv[q].z, wv[q].w));
+            }
+          }
+        }
+        float *dst = Pfull + kp * pstride;
+#pragma unroll
+        for (int u = 0; u < kRG; ++u)
+          *reinterpret_cast<float4 *>(dst + (rg * kRG + u) * 32 + jg * 4) = make_float4(a[u][0].x, a[u][0].y, a[u][1].x, a[u][1].y);
       }
-      *d = v;
+      __syncthreads();
+      for (int i = tid; i < nS * 8; i += kThreads) {  // parts summed in order 0 + 1 + 2 + 3
+        float4 *d = reinterpret_cast<float4 *>(Pfull) + i;
+        float4 v = *d;
+#pragma unroll
+        for (int kp = 1; kp < kKP; ++kp) {
+          const float4 h = reinterpret_cast<const float4 *>(Pfull + kp * pstride)[i];
+          v.x += h.x; v.y += h.y; v.z += h.z; v.w += h.w;
+        }
+        *d = v;
+      }
     }
     ptx::fence_proxy_async_smem();
     __syncthreads();
@@ -407,17 +513,62 @@ fused_small_kernel(const FusedParams p, const __grid_constant__ CUtensorMap tmX)
     ptx::mbar_wait(bar_D, par);
     PROF(5);
 
+    if constexpr (TC) {
+      // ---- P5 (tensor core). dW1 slice: D[px][j] = sum_rows x[row][px] delta_1[row][j] with
+      //      M = 128 pixels (MN-major x tile), N = 32 neurons (MN-major delta_1), K = rows
+      ptx::mbar_wait(&bar_x[1], par);                       // M-layout x tile of this step
+      tc_split(X, X + kTcXLoM, 4 * kTcAS, tid);
+      for (int t = tid; t < kTcRows * 32; t += kThreads) {  // delta_1 hi | lo, rows >= nS zero
+        const int r = t >> 5, j = t & 31;
+        const float v = r < nS ? D1[r * 32 + j] : 0.0f;
+        const float h = tc::tf32_hi(v);
+        const int off = sw128_32b(r, j);
+        *reinterpret_cast<float *>(Dt + off) = h;
+        *reinterpret_cast<float *>(Dt + kTcAS + off) = v - h;
+      }
+      ptx::fence_proxy_async_smem();
+      __syncthreads();
+      PROF(15);
+      if (tid == 0) {
+        tc::tc_fence_after();
+        constexpr uint32_t idM = tc::idesc_tf32(128, 32, true, true);
+        const int nks = (nS + 7) / 8;
+        for (int ks = 0; ks < nks; ++ks) {
+          const uint64_t ah = tc::smem_desc(sX + 1024 * ks, kTcAS, 512, 1);
+          const uint64_t al = tc::smem_desc(sX + kTcXLoM + 1024 * ks, kTcAS, 512, 1);
+          const uint64_t bh = tc::smem_desc(sD + 1024 * ks, kTcAS, 512, 1);
+          const uint64_t bl = tc::smem_desc(sD + kTcAS + 1024 * ks, kTcAS, 512, 1);
+          tc::mma_tf32(tmem + 32, ah, bh, idM, ks > 0 ? 1u : 0u);
+          tc::mma_tf32(tmem + 32, ah, bl, idM, 1u);
+          tc::mma_tf32(tmem + 32, al, bh, idM, 1u);
+        }
+        tc::mma_commit(bar_mma);
+      }
+      ptx::mbar_wait(bar_mma, 1);
+      tc::tc_fence_after();
+      if (tid == 0 && s + 1 < p.n_steps) tc_issue(&tmXK, &bar_x[0], row_s1);  // next step's K-layout tile
+      if (warp < 4) {
+        float v[32];
+        tc::tmem_ld32(tmem + ((uint32_t)(32 * warp) << 16) + 32u, v);
+        const int px = 32 * warp + lane;
+        if (px < p.ws) {
+#pragma unroll
+          for (int j = 0; j < 32; j += 4)
+            *reinterpret_cast<float4 *>(Gs + px * 32 + j) = make_float4(v[j], v[j + 1], v[j + 2], v[j + 3]);
+        }
+      }
+      tc::tc_fence_before();
+    } else {
+
     // ---- P5. dW1 slice partial, k-major like W1t: Gs[k][j] = sum_{i<nS} D1[i][j] x[i][k]
     for (int t = tid; t < nP5; t += kThreads) {
       const int jg = t & 7, kc = (t >> 3) % nchunk, rh = (t >> 3) / nchunk;
       const int ib = rh * nS / kRH, ie = (rh + 1) * nS / kRH;
       const float *dcol = D1 + jg * 4;
       const float *xcol = xs + kc * 4;
-      float a[4][4];
+      float2 a[4][2];  // neuron u, pixel pairs (4kc, 4kc+1), (4kc+2, 4kc+3): packed FFMA2
 #pragma unroll
-      for (int u = 0; u < 4; ++u)
-#pragma unroll
-        for (int v = 0; v < 4; ++v) a[u][v] = 0.0f;
+      for (int u = 0; u < 4; ++u) a[u][0] = a[u][1] = make_float2(0.0f, 0.0f);
 #pragma unroll 4
       for (int i = ib; i < ie; ++i) {
         const float4 d = *reinterpret_cast<const float4 *>(dcol + i * 32);
@@ -425,16 +576,16 @@ fused_small_kernel(const FusedParams p, const __grid_constant__ CUtensorMap tmX)
         const float dv[4] = {d.x, d.y, d.z, d.w};
 #pragma unroll
         for (int u = 0; u < 4; ++u) {
-          a[u][0] = fmaf(dv[u], x.x, a[u][0]);
-          a[u][1] = fmaf(dv[u], x.y, a[u][1]);
-          a[u][2] = fmaf(dv[u], x.z, a[u][2]);
-          a[u][3] = fmaf(dv[u], x.w, a[u][3]);
+          ffma2(a[u][0], dv[u], make_float2(x.x, x.y));
+          ffma2(a[u][1], dv[u], make_float2(x.z, x.w));
         }
       }
       float *g = rh ? Gs2 : Gs;
 #pragma unroll
       for (int v = 0; v < 4; ++v)
-        *reinterpret_cast<float4 *>(g + (kc * 4 + v) * 32 + jg * 4) = make_float4(a[0][v], a[1][v], a[2][v], a[3][v]);
+        *reinterpret_cast<float4 *>(g + (kc * 4 + v) * 32 + jg * 4) =
+            make_float4(v & 1 ? a[0][v >> 1].y : a[0][v >> 1].x, v & 1 ? a[1][v >> 1].y : a[1][v >> 1].x,
+                        v & 1 ? a[2][v >> 1].y : a[2][v >> 1].x, v & 1 ? a[3][v >> 1].y : a[3][v >> 1].x);
     }
     __syncthreads();
     for (int i = tid; i < wpad * 8; i += kThreads) {  // row halves summed in order
@@ -444,6 +595,7 @@ fused_small_kernel(const FusedParams p, const __grid_constant__ CUtensorMap tmX)
       v.x += h.x; v.y += h.y; v.z += h.z; v.w += h.w;
       *d = v;
     }
+    }  // !TC
     // reduce my slice of the W2/b1/b2 tendencies over the cluster (rank order) -> L2
     for (int e = tid; e < ne; e += kThreads) {
       float v = 0.0f;
@@ -478,6 +630,11 @@ fused_small_kernel(const FusedParams p, const __grid_constant__ CUtensorMap tmX)
       float *z = p.acc + ((s + 2) % kSlots) * p.slot;
       for (int64_t i = (int64_t)blockIdx.x * kThreads + tid; i < p.slot; i += (int64_t)nCTA * kThreads) z[i] = 0.0f;
     }
+    if (TC && s + 1 < p.n_steps) {  // next step's K-layout tile: TF32 split while the barrier fills
+      ptx::mbar_wait(&bar_x[0], (uint32_t)((s + 1) & 1));
+      tc_split(X, X + kTcXLoK, 4 * kTcAS, tid);
+      ptx::fence_proxy_async_smem();
+    }
     if (tid == 0) ptx::grid_wait(p.bar, (unsigned)((s + 1) * nCTA));
     __syncthreads();
     PROF(8);
@@ -499,11 +656,26 @@ fused_small_kernel(const FusedParams p, const __grid_constant__ CUtensorMap tmX)
     PROF(9);
 
     // ---- P9. SGD update of the resident parameters (all clusters apply the same sums)
-    for (int i = tid; i < w * 8; i += kThreads) {
-      float4 wv = reinterpret_cast<float4 *>(W1t)[i];
-      const float4 gv = reinterpret_cast<const float4 *>(Gr)[i];
-      wv.x -= p.scale * gv.x; wv.y -= p.scale * gv.y; wv.z -= p.scale * gv.z; wv.w -= p.scale * gv.w;
-      reinterpret_cast<float4 *>(W1t)[i] = wv;   // pad neurons j >= H: G = 0, W stays 0
+    if constexpr (TC) {  // W = hi + lo exactly; re-split after the update
+      for (int i = tid; i < 32 * w; i += kThreads) {
+        const int k = i >> 5, j = i & 31;
+        if (j < H) {
+          const int off = (k >> 5) * 4096 + sw128_k(j, k & 31);
+          float *hp = reinterpret_cast<float *>(Wt + off), *lp = reinterpret_cast<float *>(Wt + 16384 + off);
+          const float wv = (*hp + *lp) - p.scale * Gr[i];
+          const float h = tc::tf32_hi(wv);
+          *hp = h;
+          *lp = wv - h;
+        }
+      }
+      ptx::fence_proxy_async_smem();
+    } else {
+      for (int i = tid; i < w * 8; i += kThreads) {
+        float4 wv = reinterpret_cast<float4 *>(W1t)[i];
+        const float4 gv = reinterpret_cast<const float4 *>(Gr)[i];
+        wv.x -= p.scale * gv.x; wv.y -= p.scale * gv.y; wv.z -= p.scale * gv.z; wv.w -= p.scale * gv.w;
+        reinterpret_cast<float4 *>(W1t)[i] = wv;   // pad neurons j >= H: G = 0, W stays 0
+      }
     }
     for (int e = tid; e < nsm; e += kThreads) {
       const float gv = p.scale * gsm[e];
@@ -513,6 +685,7 @@ fused_small_kernel(const FusedParams p, const __grid_constant__ CUtensorMap tmX)
     }
     __syncthreads();
     PROF(10);
+    row_s = row_s1;
   }
   cp_async_wait0();
 
@@ -520,7 +693,15 @@ fused_small_kernel(const FusedParams p, const __grid_constant__ CUtensorMap tmX)
   if (g == 0) {
     for (int i = tid; i < w * 32; i += kThreads) {
       const int k = i >> 5, j = i & 31;
-      if (j < H) p.params[oW1 + (int64_t)j * n0 + k0 + k] = W1t[i];
+      if (j >= H) continue;
+      float v;
+      if constexpr (TC) {
+        const int off = (k >> 5) * 4096 + sw128_k(j, k & 31);
+        v = *reinterpret_cast<const float *>(Wt + off) + *reinterpret_cast<const float *>(Wt + 16384 + off);
+      } else {
+        v = W1t[i];
+      }
+      p.params[oW1 + (int64_t)j * n0 + k0 + k] = v;
     }
     if (rank == 0) {
       for (int i = tid; i < O * H; i += kThreads) p.params[oW2 + i] = W2s[(i / H) * 33 + i % H];
@@ -529,6 +710,10 @@ fused_small_kernel(const FusedParams p, const __grid_constant__ CUtensorMap tmX)
     }
   }
   ptx::cluster_sync();  // no CTA exits while a peer may still push into it
+  if (TC && warp == 0) {
+    tc::tc_fence_after();
+    asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem), "r"(64u) : "memory");
+  }
 }
 
 int env_int(const char *name, int dflt) {
@@ -568,14 +753,21 @@ int fused_small_train_steps(FusedSmall &fs, cudaStream_t st, const std::vector<i
 
   static bool attr_done = false;
   if (!attr_done) {
-    cudaFuncSetAttribute(fused_small_kernel, cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
-    cudaFuncSetAttribute(fused_small_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024);
+    for (auto k : {fused_small_kernel<false>, fused_small_kernel<true>}) {
+      cudaFuncSetAttribute(k, cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
+      cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024);
+    }
     attr_done = true;
   }
+  // tensor-core variant: TMA-aligned x, pixel slices of <= 128 columns, <= kTcRows rows per cluster
+  // (opt-in, NF_FUSED_TC=1: at N = 32 the 3xTF32 MMAs are shared-memory-bandwidth bound and no
+  // faster than the FFMA2 path; profiles/r01_fused_tc_experiment.txt)
+  bool tc = aligned && ws <= 128 && env_int("NF_FUSED_TC", 0) != 0;
   auto smem_for = [&](int G) {
     const int nSmax = (int)((batch + G - 1) / G);
     const int nOwnMax = (nSmax + C - 1) / C;
-    return (size_t)smem_layout(wpad, nSmax, nOwnMax, C).total * sizeof(float);
+    return (size_t)smem_layout(wpad, nSmax, nOwnMax, C, tc && nSmax <= kTcRows).total * sizeof(float) +
+           (tc ? 1024 : 0);
   };
   // clusters: as many as co-reside at 1 CTA/SM, with <= kMaxRows rows per cluster
   int G = 0;
@@ -595,7 +787,9 @@ int fused_small_train_steps(FusedSmall &fs, cudaStream_t st, const std::vector<i
       cfg.dynamicSmemBytes = smem_for(cand);
       if (cfg.dynamicSmemBytes > 227 * 1024) continue;
       int ncl = 0;
-      if (cudaOccupancyMaxActiveClusters(&ncl, fused_small_kernel, &cfg) != cudaSuccess) {
+      const bool tcc = tc && (batch + cand - 1) / cand <= kTcRows;
+      if (cudaOccupancyMaxActiveClusters(&ncl, tcc ? fused_small_kernel<true> : fused_small_kernel<false>, &cfg) !=
+          cudaSuccess) {
         cudaGetLastError();
         continue;
       }
@@ -606,9 +800,19 @@ int fused_small_train_steps(FusedSmall &fs, cudaStream_t st, const std::vector<i
   const int nSmax = (int)((batch + G - 1) / G);
   const int nOwnMax = (nSmax + C - 1) / C;
   const size_t smem = smem_for(G);
+  tc = tc && nSmax <= kTcRows;
 
-  CUtensorMap tmX;
+  CUtensorMap tmX, tmXK, tmXM;
   memset(&tmX, 0, sizeof tmX);
+  memset(&tmXK, 0, sizeof tmXK);
+  memset(&tmXM, 0, sizeof tmXM);
+  if (tc && (!encode_tmap_2d_f32(&tmXK, X, (uint64_t)n0, (uint64_t)N, (uint64_t)n0 * 4, 32, kTcRows,
+                                 CU_TENSOR_MAP_SWIZZLE_128B) ||
+             !encode_tmap_2d_f32(&tmXM, X, (uint64_t)n0, (uint64_t)N, (uint64_t)n0 * 4, 32, kTcRows,
+                                 CU_TENSOR_MAP_SWIZZLE_128B_ATOM_32B))) {
+    snprintf(g_fs_err, sizeof g_fs_err, "cuTensorMapEncodeTiled (TC tiles) failed");
+    return -1;
+  }
   if (aligned && !encode_tmap_2d_f32(&tmX, X, (uint64_t)n0, (uint64_t)N, (uint64_t)n0 * 4, (uint32_t)ws,
                                      (uint32_t)nSmax, CU_TENSOR_MAP_SWIZZLE_NONE)) {
     snprintf(g_fs_err, sizeof g_fs_err, "cuTensorMapEncodeTiled failed (cols %d rows %lld box %dx%d)", n0,
@@ -671,7 +875,8 @@ int fused_small_train_steps(FusedSmall &fs, cudaStream_t st, const std::vector<i
     cfg.blockDim = dim3(kThreads);
     cfg.dynamicSmemBytes = smem;
     cfg.stream = st;
-    e = cudaLaunchKernelEx(&cfg, fused_small_kernel, p, tmX);
+    e = tc ? cudaLaunchKernelEx(&cfg, fused_small_kernel<true>, p, tmX, tmXK, tmXM)
+           : cudaLaunchKernelEx(&cfg, fused_small_kernel<false>, p, tmX, tmXK, tmXM);
     count_launch();
   }
   if (e != cudaSuccess) {
@@ -703,8 +908,8 @@ int fused_small_train_steps(FusedSmall &fs, cudaStream_t st, const std::vector<i
         ph[i] += sum / (G * C); phmax[i] += mx;
       }
     }
-    fprintf(stderr, "[fused prof] C=%d G=%d nS<=%d ws=%d aligned=%d smem=%zu  phase clk (mean over CTAs / max), "
-            "ns at %.0f MHz:\n", C, G, nSmax, ws, (int)aligned, smem, khz / 1e3);
+    fprintf(stderr, "[fused prof] %s C=%d G=%d nS<=%d ws=%d aligned=%d smem=%zu  phase clk (mean over CTAs / max), "
+            "ns at %.0f MHz:\n", tc ? "tcgen05" : "simt", C, G, nSmax, ws, (int)aligned, smem, khz / 1e3);
     const char *names[11] = {"P0 wait_x+issue", "P1 z1_partial", "P2 push_P+wait", "P3 owned_rows",
                              "P4 push_D+gpart", "P5 dW1+small_red", "P6 co_sum_bulk", "P7 grid_bar",
                              "P8 readback", "P9 update+zero", "tail"};
@@ -715,6 +920,19 @@ int fused_small_train_steps(FusedSmall &fs, cudaStream_t st, const std::vector<i
       tot += ph[i] / cnt;
     }
     fprintf(stderr, "  %-18s %8.0f clk            %7.0f ns\n", "step", tot, tot * ns_per_clk);
+    {  // TC sub-phases of P1 (1 -> 13 issue -> 14 mma wait -> 2) and P5 (5 -> 15 split -> 6)
+      double a = 0, b = 0, c = 0, d = 0;
+      int n = 0;
+      for (int s = 2; s + 1 < ns; ++s)
+        for (int bl = 0; bl < G * C; ++bl, ++n) {
+          const long long *t = &h[((size_t)bl * 64 + s) * kProf];
+          a += (double)(t[13] - t[1]); b += (double)(t[14] - t[13]); c += (double)(t[2] - t[14]);
+          d += (double)(t[15] - t[5]);
+        }
+      if (tc)
+        fprintf(stderr, "  P1 split: issue %.0f, mma wait %.0f, epilogue %.0f clk;  P5 split+D build %.0f clk\n",
+                a / n, b / n, c / n, d / n);
+    }
     {  // sub-phases of P3: slots 3 -> 11 -> 12 -> 4
       double a = 0, b = 0, c = 0;
       int n = 0;

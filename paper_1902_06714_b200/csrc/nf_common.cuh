@@ -69,6 +69,17 @@ __device__ __forceinline__ float act_only(int kind, float z) {
   }
 }
 
+// Blackwell packed fp32 FMA (FFMA2): d.{x,y} = a * b.{x,y} + d.{x,y}, a broadcast.  Two
+// correctly rounded fp32 FMAs per instruction (same arithmetic as two fmaf calls).
+__device__ __forceinline__ void ffma2(float2 &d, float a, float2 b) {
+  unsigned long long dd, bb, aa;
+  asm("mov.b64 %0, {%1, %2};" : "=l"(dd) : "f"(d.x), "f"(d.y));
+  asm("mov.b64 %0, {%1, %2};" : "=l"(bb) : "f"(b.x), "f"(b.y));
+  asm("mov.b64 %0, {%1, %1};" : "=l"(aa) : "f"(a));
+  asm("fma.rn.f32x2 %0, %1, %2, %0;" : "+l"(dd) : "l"(aa), "l"(bb));
+  asm("mov.b64 {%0, %1}, %2;" : "=f"(d.x), "=f"(d.y) : "l"(dd));
+}
+
 __device__ __forceinline__ float warp_sum(float v) {
 #pragma unroll
   for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
