@@ -122,28 +122,45 @@ def barrier(world):
 
 
 def max_over_ranks(v, world):
+    """Max of a per-rank time over all ranks (NCCL on the GPU box, gloo on CPU tests)."""
     if world == 1:
         return v
     import torch
     import torch.distributed as dist
-    t = torch.tensor([v], dtype=torch.float64, device="cuda")
+    dev = "cuda" if dist.get_backend() == "nccl" else "cpu"
+    t = torch.tensor([v], dtype=torch.float64, device=dev)
     dist.all_reduce(t, op=dist.ReduceOp.MAX)
     return float(t.item())
 
 
-def run_cpu_oracle(cid, steps, bits=32):
-    """The oracle as it stands (single-threaded C), `steps` SGD steps of config `cid`."""
+def job_throughput(world, steps, batch, t_max):
+    """Whole-job samples/s: every rank runs `steps` steps of `batch` rows (weak scaling,
+    replicas), timed as the slowest rank."""
+    return world * steps * batch / t_max
+
+
+# Bounded CPU-oracle samples (about 5-20 s of single-core work each): (steps, rows per step).
+# The oracle's per-sample cost does not depend on the batch size (one fwd/bwd per sample, one
+# update per step), so a reduced batch is a fair sample of samples/s for the wide configs.
+CPU_SAMPLE = {1: (20000, None), 2: (200, None), 3: (2, 256), 4: (4, 512), 5: (1, 32)}
+
+
+def run_cpu_oracle(cid, steps, batch=None, bits=32, X=None, Y=None):
+    """The oracle as it stands (single-threaded C): `steps` SGD steps of config `cid` with
+    `batch` rows per step (default: the config's).  Returns (samples/s, seconds, batch)."""
     import oracle
     cfg = synth.CONFIGS[cid]
-    X, Y = synth.dataset(cid)
-    starts = synth.batch_starts(cid, steps=steps, N=len(X))
+    batch = batch or cfg["batch"]
+    if X is None:
+        X, Y = synth.dataset(cid, N=max(batch * 4, min(cfg["N"], 65536)))
+    starts = synth.batch_starts(cid, steps=steps, N=len(X), batch=batch)
     o = oracle.Oracle(cfg["dims"], cfg["act"], bits=bits)
     p = synth.init_params(cid)
-    o.train_steps(p, X, Y, cfg["batch"], starts[:1], cfg["eta"])  # page in
+    o.train_steps(p, X, Y, batch, starts[:1], cfg["eta"])  # page in
     t0 = time.perf_counter()
-    o.train_steps(p, X, Y, cfg["batch"], starts, cfg["eta"])
+    o.train_steps(p, X, Y, batch, starts, cfg["eta"])
     dt = time.perf_counter() - t0
-    return steps * cfg["batch"] / dt, dt
+    return steps * batch / dt, dt, batch
 
 
 def reference_arm(args):
@@ -155,16 +172,20 @@ def reference_arm(args):
     cid = args.config
     cfg = synth.CONFIGS[cid]
     import oracle
-    X, Y = synth.dataset(cid)
-    starts = synth.batch_starts(cid, steps=args.warmup + args.steps, N=len(X))
+    # rows per step: the config's batch when a step costs well under a second on one core,
+    # else a bounded sample of it (per-sample cost is batch independent)
+    fl = flops_per_sample(cfg["dims"])
+    rows = max(1, min(cfg["batch"], int(2.0e8 / fl)))
+    X, Y = synth.dataset(cid, N=max(rows * 4, min(cfg["N"], 65536)))
+    starts = synth.batch_starts(cid, steps=args.warmup + args.steps, N=len(X), batch=rows)
     o = oracle.Oracle(cfg["dims"], cfg["act"], bits=32)
     p = synth.init_params(cid)
     if args.warmup:
-        p, _ = o.train_steps(p, X, Y, cfg["batch"], starts[:args.warmup], cfg["eta"])
+        p, _ = o.train_steps(p, X, Y, rows, starts[:args.warmup], cfg["eta"])
     t0 = time.perf_counter()
-    o.train_steps(p, X, Y, cfg["batch"], starts[args.warmup:], cfg["eta"])
+    o.train_steps(p, X, Y, rows, starts[args.warmup:], cfg["eta"])
     dt = time.perf_counter() - t0
-    v = args.steps * cfg["batch"] / dt
+    v = args.steps * rows / dt
     line = {
         "impl": "reference", "metric": "training samples/sec (fwd+bwd+SGD)", "value": v,
         "unit": "samples/s", "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
@@ -172,8 +193,8 @@ def reference_arm(args):
         "vs_baseline": None, "dtype": "f32", "data": "synthetic",
         "config": {"workload": cfg["name"], "dims": cfg["dims"], "batch": cfg["batch"]},
         "cpu_baseline": {"value": v, "unit": "samples/s", "cores": 1, "kind": "oracle",
-                         "sample": f"{args.steps} full SGD steps of B={cfg['batch']} (fp32 build of "
-                                   f"oracle/nf_oracle.c, single thread)"},
+                         "sample": f"{args.steps} SGD steps of {rows} rows (config batch {cfg['batch']}) of "
+                                   f"{cfg['name']}, fp32 build of oracle/nf_oracle.c, single thread"},
         "e2e": {"value": v, "unit": "samples/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
     }
     print(json.dumps(line), flush=True)
@@ -241,7 +262,7 @@ def main():
             times.append(timed_rep())
     t_med = statistics.median(times)
     t_max = max_over_ranks(t_med, world)
-    value = world * K * B / t_max
+    value = job_throughput(world, K, B, t_max)
 
     peaks, peak_src = measured_peaks()
     alg_bytes = K * B * BYTES_PER_SAMPLE[cid]
@@ -251,13 +272,34 @@ def main():
         # TF32 dense peak = measured bf16 x (1.1 / 2.25), the guide's nominal ratio
         tf32_peak = peaks["bf16_tflops"] * 1.1 / 2.25
         ach_tf = flops_per_sample(cfg["dims"]) * K * B / t_med / 1e12
+    # DRAM traffic of the dominant kernel from a committed `ncu --set full` capture
+    # (profiles/traffic_c<id>.json: dram bytes read + written per SGD step), scaled to this launch
     traffic = None
     prof = os.path.join(ROOT, "profiles", f"traffic_c{cid}.json")
     if os.path.exists(prof):
         try:
-            traffic = json.load(open(prof)).get("bytes_per_launch")
+            traffic = json.load(open(prof))["bytes_per_step"] * K
         except Exception:
             traffic = None
+
+    # ---- inference (the paper's `output`): nf_output over the whole resident dataset
+    out = torch.empty((N, cfg["dims"][-1]), device="cuda")
+    net.output(Xd, out)
+    torch.cuda.synchronize()
+    ti = []
+    for _ in range(5):
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record(stream)
+        net.output(Xd, out)
+        e1.record(stream)
+        torch.cuda.synchronize()
+        ti.append(e0.elapsed_time(e1) / 1e3)
+    t_inf = statistics.median(ti)
+    inf_bytes = N * 4 * (cfg["dims"][0] + cfg["dims"][-1])
+    inference = {"value": world * N / max_over_ranks(t_inf, world), "unit": "samples/s", "rows": N,
+                 "hbm_gbs": inf_bytes / t_inf / 1e9, "hbm_frac": inf_bytes / t_inf / 1e9 / peaks["hbm_gbs"],
+                 "tflops": sum(2 * cfg["dims"][l] * cfg["dims"][l - 1]
+                               for l in range(1, len(cfg["dims"]))) * N / t_inf / 1e12}
 
     # ---- e2e: same metric through the C-ABI with pinned HOST buffers; each step's batch
     # is copied host->device inside the call, the step losses are read back to the host.
@@ -287,10 +329,10 @@ def main():
 
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
-        cpu_steps = {1: 20000, 2: 200, 3: 1, 4: 3, 5: 1}[cid]
-        v, dt = run_cpu_oracle(cid, cpu_steps)
+        cpu_steps, cpu_rows = CPU_SAMPLE[cid]
+        v, dt, rows = run_cpu_oracle(cid, cpu_steps, cpu_rows, X=X, Y=Y)
         cpu = {"value": v, "unit": "samples/s", "cores": 1, "kind": "oracle",
-               "sample": f"{cpu_steps} SGD steps of B={B} on config {cid} ({dt:.1f} s), fp32 build of "
+               "sample": f"{cpu_steps} SGD steps of {rows} rows of {cfg['name']} ({dt:.1f} s), fp32 build of "
                          f"oracle/nf_oracle.c, single thread"}
 
     if rank == 0:
@@ -317,6 +359,7 @@ def main():
                           "kernel": "fused_small_kernel",
                           "algorithmic_bytes_per_launch": alg_bytes}),
             "flops": {"per_sample": fl, "achieved_tflops": fl * K * B / t_med / 1e12},
+            "inference": inference,
             "cpu_baseline": cpu,
             "e2e": e2e,
             "gpu_launches": launches,

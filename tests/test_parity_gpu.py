@@ -289,3 +289,21 @@ def test_c3_c4_full_width_one_step(cid, n):
     for (Wg, bg), (Wr, br) in zip(o.layers(gpu_params(net)), o.layers(ref)):
         assert rel_err(Wg, Wr) <= FP32_BAR
         assert rel_err(bg, br) <= FP32_BAR
+
+
+def test_c2_tensor_core_variant_of_fused_kernel(c2_trajectory, monkeypatch):
+    """The opt-in tcgen05 3xTF32 variant of the fused kernel (NF_FUSED_TC=1): same parity bar."""
+    monkeypatch.setenv("NF_FUSED_TC", "1")
+    t = c2_trajectory
+    cfg, X, Y = t["cfg"], t["X"], t["Y"]
+    starts = t["starts"][100:110]
+    p = t["ckpt"][100]
+    net = make_net(cfg["dims"], cfg["act"], p)
+    loss = torch.zeros(len(starts), device="cuda")
+    net.train_steps(dev(X), dev(Y), cfg["batch"], starts, cfg["eta"], step_loss=loss)
+    o = oracle.Oracle(cfg["dims"], cfg["act"])
+    ref, ref_loss = o.train_steps(p, X, Y, cfg["batch"], starts, cfg["eta"])
+    for (Wg, bg), (Wr, br) in zip(o.layers(gpu_params(net)), o.layers(ref)):
+        assert rel_err(Wg, Wr) <= FP32_BAR
+        assert rel_err(bg, br) <= FP32_BAR
+    assert rel_err(loss.cpu().numpy(), ref_loss) <= FP32_BAR
