@@ -137,7 +137,8 @@ int nf_accuracy(nf_net *net, const float *x, const float *y, int64_t n, float *a
 const char *nf_last_error(void);
 
 /* Number of this library's kernels launched since load (for the bench's
- * gpu_launches claim).  Counts launches, not graph replays. */
+ * gpu_launches claim), including the kernels of each replay of the CUDA graph
+ * nf_train_steps captures for generic nets. */
 int64_t nf_launch_count(void);
 
 #ifdef __cplusplus

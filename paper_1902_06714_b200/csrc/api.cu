@@ -110,6 +110,11 @@ struct nf_net {
   DevBuf stage_x, stage_y, stage_o, stage_g;  // host-pointer staging
   DevBuf d_starts;
   FusedSmall fused;                      // persistent small-net kernel state
+  // CUDA graph of the generic multi-step sequence (nf_train_steps): replayed when a call
+  // repeats the same arguments, rebuilt otherwise
+  cudaGraphExec_t graph = nullptr;
+  std::vector<int64_t> graph_key;
+  int64_t graph_kernels = 0;             // kernels in the graph (nf_launch_count on replay)
 
   float *W(int l) const { return params + offW[l]; }
   float *b(int l) const { return params + offB[l]; }
@@ -120,11 +125,18 @@ namespace {
 
 constexpr int64_t kEvalChunk = 32768;    // rows per forward chunk for eval calls
 
+void drop_graph(nf_net *net) {
+  if (net->graph) cudaGraphExecDestroy(net->graph);
+  net->graph = nullptr;
+  net->graph_key.clear();
+}
+
 int ensure_ws(nf_net *net, int64_t rows) {
   if (rows <= net->ws_rows) return NF_OK;
   int64_t per_row = 0;
   for (int l = 1; l <= net->L; ++l) per_row += 2 * (int64_t)net->dims[l];
   NF_CUDA(cudaStreamSynchronize(net->stream));
+  drop_graph(net);
   NF_CUDA(net->stash.ensure((size_t)(per_row * rows) * sizeof(float)));
   float *p = net->stash.as<float>();
   net->A.assign(net->L + 1, nullptr);
@@ -280,6 +292,7 @@ void nf_net_destroy(nf_net *net) {
   net->stage_g.release();
   net->d_starts.release();
   fused_small_release(net->fused);
+  drop_graph(net);
   delete net;
 }
 
@@ -411,11 +424,52 @@ int nf_train_steps(nf_net *net, const float *X, const float *Y, int64_t N, int64
   int rc = fused_small_train_steps(net->fused, net->stream, net->dims, net->act_h, net->act_o,
                                    net->params, dX, dY, dN, batch, st.data(), n_steps, eta, step_loss);
   if (rc == FUSED_NOT_APPLICABLE) {
+    // Generic nets: the per-step kernel sequence of all n_steps, captured once as a CUDA
+    // graph and replayed while the arguments repeat (removes the host launch gaps between the
+    // ~10-50 kernels of each step).  Workspaces are sized before capture.
+    if ((rc = ensure_ws(net, batch))) return rc;
+    NF_CUDA(net->red.ensure(sizeof(double2) * loss_acc_parts() + 64));
+    std::vector<int64_t> key = {(int64_t)(uintptr_t)dX, (int64_t)(uintptr_t)dY, N, batch, n_steps,
+                                (int64_t)(uintptr_t)step_loss, (int64_t)(uintptr_t)net->stream, net->math,
+                                (int64_t)(uintptr_t)net->stash.p};
+    int32_t eb;
+    memcpy(&eb, &eta, 4);
+    key.push_back(eb);
+    key.insert(key.end(), st.begin(), st.end());
+    const bool use_graph = !host_in && getenv("NF_NO_GRAPH") == nullptr;
+    if (use_graph && net->graph && key == net->graph_key) {
+      NF_CUDA(cudaGraphLaunch(net->graph, net->stream));
+      count_launch((int)net->graph_kernels);
+      return NF_OK;
+    }
+    const int64_t launches0 = nf_launch_count();
+    if (use_graph) {
+      drop_graph(net);
+      NF_CUDA(cudaStreamBeginCapture(net->stream, cudaStreamCaptureModeRelaxed));
+    }
     for (int64_t s = 0; s < n_steps; ++s) {
       rc = train_batch_dev(net, dX + st[s] * n0, dY + st[s] * nL, batch, eta,
                            step_loss ? step_loss + s : nullptr);
-      if (rc) return rc;
+      if (rc) break;
     }
+    if (use_graph) {
+      cudaGraph_t g = nullptr;
+      cudaError_t e = cudaStreamEndCapture(net->stream, &g);
+      if (rc) {
+        if (g) cudaGraphDestroy(g);
+        return rc;
+      }
+      if (e == cudaSuccess) e = cudaGraphInstantiate(&net->graph, g, 0);
+      if (g) cudaGraphDestroy(g);
+      if (e != cudaSuccess) {
+        net->graph = nullptr;
+        return fail(NF_ECUDA, "CUDA graph of the training steps: %s", cudaGetErrorString(e));
+      }
+      net->graph_key = key;
+      net->graph_kernels = nf_launch_count() - launches0;
+      NF_CUDA(cudaGraphLaunch(net->graph, net->stream));
+    }
+    if (rc) return rc;
   } else if (rc != 0) {
     return fail(NF_ECUDA, "fused small-net kernel: %s", fused_small_error());
   }

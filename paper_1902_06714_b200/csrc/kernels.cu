@@ -196,6 +196,119 @@ cudaError_t bias_grad(cudaStream_t st, const float *D, int64_t rows, int cols, c
   return cudaGetLastError();
 }
 
+// ---------------------------------------------------------------------------
+// Narrow output-layer contractions (the 10-wide last layer of configs 3 and 4): one
+// extent <= 32, memory-bound on the wide operand.  Dedicated kernels instead of tiles.
+
+// K1 with N <= 32: Z[m][o] = sum_k A[m][k] W[o][k] (+ bias/activation in epi).  One warp per
+// row; W [N][K] staged in shared memory; lane-strided K slices, butterfly reductions.
+template <int NMAX>
+__global__ void __launch_bounds__(256)
+fwd_smalln(const float *__restrict__ A, const float *__restrict__ W, int M, int N, int K, EpiFwd epi) {
+  extern __shared__ float ws_[];
+  for (int i = threadIdx.x; i < N * K; i += blockDim.x) ws_[i] = W[i];
+  __syncthreads();
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  for (int m = blockIdx.x * 8 + warp; m < M; m += gridDim.x * 8) {
+    const float *a = A + (int64_t)m * K;
+    float acc[NMAX];
+#pragma unroll
+    for (int o = 0; o < NMAX; ++o) acc[o] = 0.0f;
+    for (int k = lane * 4; k < K; k += 128) {
+      const float4 av = *reinterpret_cast<const float4 *>(a + k);
+#pragma unroll
+      for (int o = 0; o < NMAX; ++o) {
+        if (o < N) {
+          const float4 wv = *reinterpret_cast<const float4 *>(ws_ + o * K + k);
+          acc[o] = fmaf(av.x, wv.x, fmaf(av.y, wv.y, fmaf(av.z, wv.z, fmaf(av.w, wv.w, acc[o]))));
+        }
+      }
+    }
+#pragma unroll
+    for (int o = 0; o < NMAX; ++o)
+      if (o < N) acc[o] = warp_sum(acc[o]);
+    float z = 0.0f;
+#pragma unroll
+    for (int o = 0; o < NMAX; ++o)
+      if (o == lane) z = acc[o];
+    if (lane < N) epi(m, lane, z);
+  }
+}
+
+// K3 with K <= 32: SD[m][n] = sigma'[m][n] * sum_k D[m][k] W[k][n].  A thread owns 4 columns
+// (W column slice in registers) and walks TM rows; S read and written once, float4.
+template <int KMAX>
+__global__ void __launch_bounds__(128)
+bwd_smallk(const float *__restrict__ D, const float *__restrict__ W, int M, int N, int K, int TM, EpiBwd epi) {
+  const int n = (blockIdx.x * 128 + threadIdx.x) * 4;
+  if (n >= N) return;
+  float4 w[KMAX];
+#pragma unroll
+  for (int k = 0; k < KMAX; ++k)
+    w[k] = k < K ? *reinterpret_cast<const float4 *>(W + (int64_t)k * N + n) : make_float4(0.f, 0.f, 0.f, 0.f);
+  const int m0 = blockIdx.y * TM, m1 = min(M, m0 + TM);
+  for (int m = m0; m < m1; ++m) {
+    const float *d = D + (int64_t)m * K;
+    float4 acc = make_float4(0.f, 0.f, 0.f, 0.f);
+#pragma unroll
+    for (int k = 0; k < KMAX; ++k) {
+      if (k < K) {
+        const float dk = __ldg(d + k);
+        acc.x = fmaf(dk, w[k].x, acc.x);
+        acc.y = fmaf(dk, w[k].y, acc.y);
+        acc.z = fmaf(dk, w[k].z, acc.z);
+        acc.w = fmaf(dk, w[k].w, acc.w);
+      }
+    }
+    float4 *sp = reinterpret_cast<float4 *>(epi.SD + (int64_t)m * epi.ld + n);
+    const float4 s = *sp;
+    *sp = make_float4(acc.x * s.x, acc.y * s.y, acc.z * s.z, acc.w * s.w);
+  }
+}
+
+// K4 with M <= 32: G[i][n] = sum_b D[b][i] A[b][n] for n < N, and column n = N with A = 1
+// (the bias tendency).  Row chunks -> partials [R][M][N+1], summed in chunk order.
+template <int MMAX>
+__global__ void __launch_bounds__(128)
+grad_smallm_partial(const float *__restrict__ D, const float *__restrict__ A, int M, int N, int K, int chunk,
+                    float *__restrict__ part) {
+  __shared__ float dsm[128 * MMAX];
+  const int n = blockIdx.x * 128 + threadIdx.x;
+  const int b0 = blockIdx.y * chunk, b1 = min(K, b0 + chunk);
+  float acc[MMAX];
+#pragma unroll
+  for (int i = 0; i < MMAX; ++i) acc[i] = 0.0f;
+  for (int bb = b0; bb < b1; bb += 128) {
+    const int nb = min(128, b1 - bb);
+    __syncthreads();
+    for (int t = threadIdx.x; t < nb * M; t += 128) dsm[(t / M) * MMAX + t % M] = D[(int64_t)(bb + t / M) * M + t % M];
+    __syncthreads();
+    if (n <= N) {
+      for (int r = 0; r < nb; ++r) {
+        const float a = n < N ? __ldg(A + (int64_t)(bb + r) * N + n) : 1.0f;
+#pragma unroll
+        for (int i = 0; i < MMAX; ++i)
+          if (i < M) acc[i] = fmaf(dsm[r * MMAX + i], a, acc[i]);
+      }
+    }
+  }
+  if (n <= N) {
+#pragma unroll
+    for (int i = 0; i < MMAX; ++i)
+      if (i < M) part[((int64_t)blockIdx.y * M + i) * (N + 1) + n] = acc[i];
+  }
+}
+
+__global__ void __launch_bounds__(256)
+grad_smallm_final(const float *__restrict__ part, int R, int M, int N, EpiGrad epi) {
+  const int64_t MN = (int64_t)M * (N + 1);
+  for (int64_t t = blockIdx.x * 256 + threadIdx.x; t < MN; t += (int64_t)gridDim.x * 256) {
+    float s = 0.0f;
+    for (int r = 0; r < R; ++r) s += part[r * MN + t];
+    epi((int)(t / (N + 1)), (int)(t % (N + 1)), s);
+  }
+}
+
 }  // namespace
 
 cudaError_t gemm_fwd(cudaStream_t st, int M, int N, int K, const float *A, const float *W,
@@ -203,6 +316,17 @@ cudaError_t gemm_fwd(cudaStream_t st, int M, int N, int K, const float *A, const
   const TcOp a{A, K, false}, b{W, K, false};
   if (use_tc(M, N, K, a, b)) return run_tc<false, false>(st, M, N, K, a, b, epi, ws);
   g_last_engine = ENGINE_SIMT;
+  if (N <= 16 && K % 4 == 0 && (size_t)N * K * 4 <= 96 * 1024 && tc_ok(a) && tc_ok(b) && M >= 256) {
+    static bool attr = false;
+    if (!attr) {
+      cudaFuncSetAttribute(fwd_smalln<16>, cudaFuncAttributeMaxDynamicSharedMemorySize, 96 * 1024);
+      attr = true;
+    }
+    const int blocks = std::min((M + 7) / 8, 4 * kSMs);
+    fwd_smalln<16><<<blocks, 256, (size_t)N * K * 4, st>>>(A, W, M, N, K, epi);
+    count_launch();
+    return cudaGetLastError();
+  }
   GemmArgs g{M, N, K, A, K, W, K, N, 0, nullptr};
   return run_gemm<true, true>(st, g, epi, ws);
 }
@@ -212,6 +336,14 @@ cudaError_t gemm_bwd(cudaStream_t st, int M, int N, int K, const float *D, const
   const TcOp a{D, K, false}, b{W, N, true};
   if (use_tc(M, N, K, a, b)) return run_tc<false, true>(st, M, N, K, a, b, epi, ws);
   g_last_engine = ENGINE_SIMT;
+  if (K <= 16 && N % 4 == 0 && epi.ld % 4 == 0 && (reinterpret_cast<uintptr_t>(W) & 15) == 0 &&
+      (reinterpret_cast<uintptr_t>(epi.SD) & 15) == 0 && M >= 256) {
+    const int cb = (N / 4 + 127) / 128;
+    const int TM = std::max(1, (int)((int64_t)M * cb / (4 * kSMs)));
+    bwd_smallk<16><<<dim3(cb, (M + TM - 1) / TM), 128, 0, st>>>(D, W, M, N, K, TM, epi);
+    count_launch();
+    return cudaGetLastError();
+  }
   GemmArgs g{M, N, K, D, K, W, N, N, 0, nullptr};
   return run_gemm<true, false>(st, g, epi, ws);
 }
@@ -227,6 +359,18 @@ cudaError_t gemm_grad(cudaStream_t st, int M, int N, int K, const float *D, cons
     return run_tc<true, true>(st, M, N, K, a, b, epi, ws);
   }
   g_last_engine = ENGINE_SIMT;
+  if (M <= 16 && K >= 512) {
+    const int cb = (N + 1 + 127) / 128;
+    int R = std::max(1, std::min(K / 64, (4 * kSMs) / cb));
+    while (R > 1 && (size_t)R * M * (N + 1) > ws.partial_floats) --R;
+    const int chunk = (K + R - 1) / R;
+    R = (K + chunk - 1) / chunk;
+    grad_smallm_partial<16><<<dim3(cb, R), 128, 0, st>>>(D, Aprev, M, N, K, chunk, ws.partial);
+    const int64_t MN = (int64_t)M * (N + 1);
+    grad_smallm_final<<<(int)std::min<int64_t>((MN + 255) / 256, 2 * kSMs), 256, 0, st>>>(ws.partial, R, M, N, epi);
+    count_launch(2);
+    return cudaGetLastError();
+  }
   // C[M][N+1]: column N is the ones column -> bias gradient.
   GemmArgs g{M, N + 1, K, D, M, Aprev, N, N, 0, nullptr};
   return run_gemm<false, false>(st, g, epi, ws);

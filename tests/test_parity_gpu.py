@@ -44,6 +44,10 @@ SHAPES = [
     ([300, 260, 1], "tanh,relu", 300),
     ([1, 1], "sigmoid", 1),
     ([5, 1, 3], "step,sigmoid", 9),
+    # narrow output layers over >= 512 rows: the dedicated skinny kernels (fwd_smalln,
+    # bwd_smallk, grad_smallm in kernels.cu)
+    ([300, 200, 10], "tanh,sigmoid", 600),
+    ([516, 132, 7], "sigmoid", 1031),
 ]
 
 
