@@ -115,6 +115,8 @@ struct nf_net {
   cudaGraphExec_t graph = nullptr;
   std::vector<int64_t> graph_key;
   int64_t graph_kernels = 0;             // kernels in the graph (nf_launch_count on replay)
+  cudaStream_t cap_stream = nullptr;     // private stream the graph is captured on (the
+                                         // caller's stream may be the legacy default stream)
 
   float *W(int l) const { return params + offW[l]; }
   float *b(int l) const { return params + offB[l]; }
@@ -293,6 +295,7 @@ void nf_net_destroy(nf_net *net) {
   net->d_starts.release();
   fused_small_release(net->fused);
   drop_graph(net);
+  if (net->cap_stream) cudaStreamDestroy(net->cap_stream);
   delete net;
 }
 
@@ -443,18 +446,22 @@ int nf_train_steps(nf_net *net, const float *X, const float *Y, int64_t N, int64
       return NF_OK;
     }
     const int64_t launches0 = nf_launch_count();
+    cudaStream_t user = net->stream;
     if (use_graph) {
       drop_graph(net);
-      NF_CUDA(cudaStreamBeginCapture(net->stream, cudaStreamCaptureModeRelaxed));
+      if (!net->cap_stream) NF_CUDA(cudaStreamCreateWithFlags(&net->cap_stream, cudaStreamNonBlocking));
+      NF_CUDA(cudaStreamBeginCapture(net->cap_stream, cudaStreamCaptureModeRelaxed));
+      net->stream = net->cap_stream;  // the step kernels are recorded, not run
     }
     for (int64_t s = 0; s < n_steps; ++s) {
       rc = train_batch_dev(net, dX + st[s] * n0, dY + st[s] * nL, batch, eta,
                            step_loss ? step_loss + s : nullptr);
       if (rc) break;
     }
+    net->stream = user;
     if (use_graph) {
       cudaGraph_t g = nullptr;
-      cudaError_t e = cudaStreamEndCapture(net->stream, &g);
+      cudaError_t e = cudaStreamEndCapture(net->cap_stream, &g);
       if (rc) {
         if (g) cudaGraphDestroy(g);
         return rc;

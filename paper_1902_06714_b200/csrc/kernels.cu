@@ -117,7 +117,7 @@ cudaError_t launch_tc(cudaStream_t st, int M, int N, int K, const TcOp &a, const
   const int tiles = tm * tn;
   const int nkb = (K + tc::BK - 1) / tc::BK;
   int splits = 1;
-  if (2 * tiles < kSMs && nkb >= 8) {  // split-K only when under half a wave
+  if (2 * tiles < kSMs && nkb >= 16) {  // split-K only when under half a wave and K >= 512
     splits = std::min((kSMs + tiles - 1) / tiles, nkb / 4);
     while (splits > 1 && (size_t)splits * M * N > ws.partial_floats) --splits;
     splits = std::max(splits, 1);
@@ -214,6 +214,7 @@ fwd_smalln(const float *__restrict__ A, const float *__restrict__ W, int M, int 
     float acc[NMAX];
 #pragma unroll
     for (int o = 0; o < NMAX; ++o) acc[o] = 0.0f;
+#pragma unroll 4
     for (int k = lane * 4; k < K; k += 128) {
       const float4 av = *reinterpret_cast<const float4 *>(a + k);
 #pragma unroll
@@ -247,22 +248,30 @@ bwd_smallk(const float *__restrict__ D, const float *__restrict__ W, int M, int 
   for (int k = 0; k < KMAX; ++k)
     w[k] = k < K ? *reinterpret_cast<const float4 *>(W + (int64_t)k * N + n) : make_float4(0.f, 0.f, 0.f, 0.f);
   const int m0 = blockIdx.y * TM, m1 = min(M, m0 + TM);
-  for (int m = m0; m < m1; ++m) {
-    const float *d = D + (int64_t)m * K;
-    float4 acc = make_float4(0.f, 0.f, 0.f, 0.f);
+  for (int mb = m0; mb < m1; mb += 4) {  // 4 rows per pass: their sigma' loads issued together
+    float4 sv[4];
 #pragma unroll
-    for (int k = 0; k < KMAX; ++k) {
-      if (k < K) {
-        const float dk = __ldg(d + k);
-        acc.x = fmaf(dk, w[k].x, acc.x);
-        acc.y = fmaf(dk, w[k].y, acc.y);
-        acc.z = fmaf(dk, w[k].z, acc.z);
-        acc.w = fmaf(dk, w[k].w, acc.w);
+    for (int u = 0; u < 4; ++u)
+      if (mb + u < m1) sv[u] = *reinterpret_cast<const float4 *>(epi.SD + (int64_t)(mb + u) * epi.ld + n);
+#pragma unroll
+    for (int u = 0; u < 4; ++u) {
+      const int m = mb + u;
+      if (m >= m1) break;
+      const float *d = D + (int64_t)m * K;
+      float4 acc = make_float4(0.f, 0.f, 0.f, 0.f);
+#pragma unroll
+      for (int k = 0; k < KMAX; ++k) {
+        if (k < K) {
+          const float dk = __ldg(d + k);
+          acc.x = fmaf(dk, w[k].x, acc.x);
+          acc.y = fmaf(dk, w[k].y, acc.y);
+          acc.z = fmaf(dk, w[k].z, acc.z);
+          acc.w = fmaf(dk, w[k].w, acc.w);
+        }
       }
+      *reinterpret_cast<float4 *>(epi.SD + (int64_t)m * epi.ld + n) =
+          make_float4(acc.x * sv[u].x, acc.y * sv[u].y, acc.z * sv[u].z, acc.w * sv[u].w);
     }
-    float4 *sp = reinterpret_cast<float4 *>(epi.SD + (int64_t)m * epi.ld + n);
-    const float4 s = *sp;
-    *sp = make_float4(acc.x * s.x, acc.y * s.y, acc.z * s.z, acc.w * s.w);
   }
 }
 
@@ -284,7 +293,18 @@ grad_smallm_partial(const float *__restrict__ D, const float *__restrict__ A, in
     for (int t = threadIdx.x; t < nb * M; t += 128) dsm[(t / M) * MMAX + t % M] = D[(int64_t)(bb + t / M) * M + t % M];
     __syncthreads();
     if (n <= N) {
-      for (int r = 0; r < nb; ++r) {
+      int r = 0;
+      for (; r + 8 <= nb; r += 8) {  // 8 independent row loads in flight
+        float a[8];
+#pragma unroll
+        for (int u = 0; u < 8; ++u) a[u] = n < N ? __ldg(A + (int64_t)(bb + r + u) * N + n) : 1.0f;
+#pragma unroll
+        for (int u = 0; u < 8; ++u)
+#pragma unroll
+          for (int i = 0; i < MMAX; ++i)
+            if (i < M) acc[i] = fmaf(dsm[(r + u) * MMAX + i], a[u], acc[i]);
+      }
+      for (; r < nb; ++r) {
         const float a = n < N ? __ldg(A + (int64_t)(bb + r) * N + n) : 1.0f;
 #pragma unroll
         for (int i = 0; i < MMAX; ++i)
@@ -299,12 +319,20 @@ grad_smallm_partial(const float *__restrict__ D, const float *__restrict__ A, in
   }
 }
 
+// thread t sums the R partials of output t in order r = 0..R-1, four independent loads in
+// flight (deterministic)
 __global__ void __launch_bounds__(256)
 grad_smallm_final(const float *__restrict__ part, int R, int M, int N, EpiGrad epi) {
   const int64_t MN = (int64_t)M * (N + 1);
   for (int64_t t = blockIdx.x * 256 + threadIdx.x; t < MN; t += (int64_t)gridDim.x * 256) {
     float s = 0.0f;
-    for (int r = 0; r < R; ++r) s += part[r * MN + t];
+    int r = 0;
+    for (; r + 4 <= R; r += 4) {
+      const float v0 = part[r * MN + t], v1 = part[(r + 1) * MN + t];
+      const float v2 = part[(r + 2) * MN + t], v3 = part[(r + 3) * MN + t];
+      s += v0; s += v1; s += v2; s += v3;
+    }
+    for (; r < R; ++r) s += part[r * MN + t];
     epi((int)(t / (N + 1)), (int)(t % (N + 1)), s);
   }
 }
@@ -339,7 +367,7 @@ cudaError_t gemm_bwd(cudaStream_t st, int M, int N, int K, const float *D, const
   if (K <= 16 && N % 4 == 0 && epi.ld % 4 == 0 && (reinterpret_cast<uintptr_t>(W) & 15) == 0 &&
       (reinterpret_cast<uintptr_t>(epi.SD) & 15) == 0 && M >= 256) {
     const int cb = (N / 4 + 127) / 128;
-    const int TM = std::max(1, (int)((int64_t)M * cb / (4 * kSMs)));
+    const int TM = std::max(4, (int)((int64_t)M * cb / (8 * kSMs)));
     bwd_smallk<16><<<dim3(cb, (M + TM - 1) / TM), 128, 0, st>>>(D, W, M, N, K, TM, epi);
     count_launch();
     return cudaGetLastError();
@@ -361,7 +389,7 @@ cudaError_t gemm_grad(cudaStream_t st, int M, int N, int K, const float *D, cons
   g_last_engine = ENGINE_SIMT;
   if (M <= 16 && K >= 512) {
     const int cb = (N + 1 + 127) / 128;
-    int R = std::max(1, std::min(K / 64, (4 * kSMs) / cb));
+    int R = std::max(1, std::min(K / 32, (8 * kSMs) / cb));
     while (R > 1 && (size_t)R * M * (N + 1) > ws.partial_floats) --R;
     const int chunk = (K + R - 1) / R;
     R = (K + chunk - 1) / chunk;

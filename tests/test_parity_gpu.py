@@ -311,3 +311,43 @@ def test_c2_tensor_core_variant_of_fused_kernel(c2_trajectory, monkeypatch):
         assert rel_err(Wg, Wr) <= FP32_BAR
         assert rel_err(bg, br) <= FP32_BAR
     assert rel_err(loss.cpu().numpy(), ref_loss) <= FP32_BAR
+
+
+def test_generic_train_steps_graph_equals_train_batch_loop():
+    """nf_train_steps on a generic (non-fused) net runs as a captured CUDA graph, replayed on a
+    repeated call; it must equal the nf_train_batch loop, and its replay must equal a fresh run."""
+    dims, act, B = [200, 136, 72, 5], "tanh", 128
+    p = synth.random_params(31, dims, 0.1)
+    X, Y = synth.random_batch(32, 1024, dims[0], dims[-1], "uniform")
+    starts = [0, 300, 77, 896, 512]
+    a = make_net(dims, act, p)
+    b = make_net(dims, act, p)
+    a.train_steps(dev(X), dev(Y), B, starts, 0.5)            # capture + launch
+    for s in starts:
+        b.train_batch(dev(X[s:s + B]), dev(Y[s:s + B]), 0.5)
+    assert np.array_equal(gpu_params(a), gpu_params(b))
+    n0 = nf.nf_launch_count()
+    a.set_params(dev(p))
+    a.train_steps(dev(X), dev(Y), B, starts, 0.5)            # replay (same arguments)
+    assert nf.nf_launch_count() > n0                          # replays count their kernels
+    assert np.array_equal(gpu_params(a), gpu_params(b))
+    o = oracle.Oracle(dims, act)
+    ref, _ = o.train_steps(p, X, Y, B, starts, 0.5)
+    assert rel_err(gpu_params(a), ref) <= FP32_BAR
+
+
+def test_generic_train_steps_on_a_side_stream():
+    dims, act, B = [200, 136, 72, 5], "tanh", 128
+    p = synth.random_params(33, dims, 0.1)
+    X, Y = synth.random_batch(34, 512, dims[0], dims[-1], "uniform")
+    st = torch.cuda.Stream()
+    net = nf.Net(dims, act, stream=st)
+    net.set_params(dev(p))
+    with torch.cuda.stream(st):
+        net.train_steps(dev(X), dev(Y), B, [0, 128, 384], 0.5)
+    st.synchronize()
+    ref, _ = oracle.Oracle(dims, act).train_steps(p, X, Y, B, [0, 128, 384], 0.5)
+    out = torch.empty(net.n_params, dtype=torch.float32, device="cuda")
+    net.get_params(out)
+    st.synchronize()
+    assert rel_err(out.cpu().numpy(), ref) <= FP32_BAR
