@@ -3,6 +3,7 @@
 // sequences of one SGD step.  Every arithmetic step of the method runs in this
 // library's CUDA kernels; there is no CPU fallback (NF_ENODEV without a GPU).
 #include <cmath>
+#include <cstdlib>
 #include <cstdarg>
 #include <cstdio>
 #include <cstring>
@@ -11,6 +12,7 @@
 
 #include "../../include/nf.h"
 #include "fused_small.cuh"
+#include "infer_small.cuh"
 #include "kernels.cuh"
 
 using namespace nf;
@@ -354,13 +356,17 @@ int nf_output(nf_net *net, const float *x, int64_t n, float *out) {
     NF_CUDA(net->stage_o.ensure((size_t)n * nL * sizeof(float)));
     dout = net->stage_o.as<float>();
   }
-  const int64_t chunk = std::min<int64_t>(n, kEvalChunk);
-  if ((rc = ensure_ws(net, chunk))) return rc;
-  for (int64_t r = 0; r < n; r += chunk) {
-    const int64_t m = std::min(chunk, n - r);
-    if ((rc = forward(net, dx + r * n0, nullptr, m, 2))) return rc;
-    NF_CUDA(cudaMemcpyAsync(dout + r * nL, net->A[net->L], (size_t)m * nL * sizeof(float),
-                            cudaMemcpyDeviceToDevice, net->stream));
+  if (infer_small_applicable(net->dims, dx) && getenv("NF_DISABLE_FUSED") == nullptr) {
+    NF_CUDA(infer_small(net->stream, net->dims, net->act_h, net->act_o, net->params, dx, n, dout));
+  } else {
+    const int64_t chunk = std::min<int64_t>(n, kEvalChunk);
+    if ((rc = ensure_ws(net, chunk))) return rc;
+    for (int64_t r = 0; r < n; r += chunk) {
+      const int64_t m = std::min(chunk, n - r);
+      if ((rc = forward(net, dx + r * n0, nullptr, m, 2))) return rc;
+      NF_CUDA(cudaMemcpyAsync(dout + r * nL, net->A[net->L], (size_t)m * nL * sizeof(float),
+                              cudaMemcpyDeviceToDevice, net->stream));
+    }
   }
   if (host_out) {
     NF_CUDA(cudaMemcpyAsync(out, dout, (size_t)n * nL * sizeof(float), cudaMemcpyDeviceToHost, net->stream));
@@ -527,9 +533,12 @@ static int eval_loss_acc(nf_net *net, const float *x, const float *y, int64_t n,
   const int64_t nchunks = (n + chunk - 1) / chunk;
   NF_CUDA(net->red.ensure(sizeof(double2) * loss_acc_parts() + 64 + nchunks * 2 * sizeof(float)));
   float *res = reinterpret_cast<float *>(net->red.as<char>() + sizeof(double2) * loss_acc_parts() + 64);
+  const bool fused = infer_small_applicable(net->dims, dx) && getenv("NF_DISABLE_FUSED") == nullptr;
   for (int64_t c = 0; c < nchunks; ++c) {
     const int64_t r = c * chunk, m = std::min(chunk, n - r);
-    if ((rc = forward(net, dx + r * n0, nullptr, m, 2))) return rc;
+    if (fused) NF_CUDA(infer_small(net->stream, net->dims, net->act_h, net->act_o, net->params, dx + r * n0, m,
+                                   net->A[net->L]));
+    else if ((rc = forward(net, dx + r * n0, nullptr, m, 2))) return rc;
     NF_CUDA(loss_acc(net->stream, net->A[net->L], dy + r * nL, m, nL, net->red.as<double2>(), res + 2 * c, nullptr));
   }
   std::vector<float> h(2 * nchunks);

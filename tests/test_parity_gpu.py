@@ -48,6 +48,9 @@ SHAPES = [
     # bwd_smallk, grad_smallm in kernels.cu)
     ([300, 200, 10], "tanh,sigmoid", 600),
     ([516, 132, 7], "sigmoid", 1031),
+    # two-layer nets with narrow layers and n0 % 4 == 0: the fused inference kernel
+    # (infer_small.cu) with a ragged last 64-row tile and a ragged last pixel chunk
+    ([100, 17, 3], "tanh,sigmoid", 777),
 ]
 
 
@@ -351,3 +354,20 @@ def test_generic_train_steps_on_a_side_stream():
     net.get_params(out)
     st.synchronize()
     assert rel_err(out.cpu().numpy(), ref) <= FP32_BAR
+
+
+def test_fused_inference_equals_generic_path(monkeypatch):
+    """nf_output / nf_loss / nf_accuracy of a small two-layer net: the fused inference kernel
+    and the generic K1 chain agree (both against the oracle)."""
+    dims = [784, 30, 10]
+    p = synth.init_params(2)
+    X, Y = synth.dataset(2, N=5000)
+    net = make_net(dims, "sigmoid", p)
+    fused = net.output(dev(X)).cpu().numpy()
+    lf, af = net.loss(dev(X), dev(Y)), net.accuracy(dev(X), dev(Y))
+    monkeypatch.setenv("NF_DISABLE_FUSED", "1")
+    generic = net.output(dev(X)).cpu().numpy()
+    lg, ag = net.loss(dev(X), dev(Y)), net.accuracy(dev(X), dev(Y))
+    ref = oracle.Oracle(dims, "sigmoid").output(p, X)
+    assert rel_err(fused, ref) <= FP32_BAR and rel_err(generic, ref) <= FP32_BAR
+    assert abs(lf - lg) <= 1e-6 * abs(lg) + 1e-9 and af == ag
