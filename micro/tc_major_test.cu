@@ -128,6 +128,23 @@ void check(int M, int N, int K, int positive = 0, int reps = 0) {
 }
 
 template <class Epi>
+void perf_pers(const char *name, int M, int N, int K, Epi epi, float *A, float *B) {
+  CUtensorMap ta, tb;
+  map(&ta, A, M, K, false, tc::BM); map(&tb, B, N, K, false, 256);
+  using Cf = tc::Cfg<256, 1>;
+  auto kern = tc::gemm_tc_persistent<256, false, false, Epi>;
+  CK(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, Cf::SMEM));
+  kern<<<148, tc::kThreads, Cf::SMEM>>>(ta, tb, M, N, K, epi);
+  CK(cudaDeviceSynchronize());
+  cudaEvent_t e0, e1; cudaEventCreate(&e0); cudaEventCreate(&e1);
+  cudaEventRecord(e0);
+  for (int r = 0; r < 3; ++r) kern<<<148, tc::kThreads, Cf::SMEM>>>(ta, tb, M, N, K, epi);
+  cudaEventRecord(e1); CK(cudaEventSynchronize(e1));
+  float ms; cudaEventElapsedTime(&ms, e0, e1); ms /= 3;
+  printf("PERSISTENT %-10s M=%d N=%d K=%d: %.3f ms %.1f TFLOP/s\n", name, M, N, K, ms, 2.0 * M * N * K / ms / 1e9);
+}
+
+template <class Epi>
 void perf_epi(const char *name, int M, int N, int K, Epi epi, float *A, float *B) {
   CUtensorMap ta, tb;
   map(&ta, A, M, K, false, tc::BM); map(&tb, B, N, K, false, 256);
@@ -182,6 +199,33 @@ perf:
     perf_epi("fwd-sigm", M, N, K, nf::EpiFwd{bias, C, S, nullptr, N, nf::ACT_SIGMOID, 0}, A, B);
     perf_epi("fwd-infer", M, N, K, nf::EpiFwd{bias, C, S, nullptr, N, nf::ACT_RELU, 2}, A, B);
     perf_epi("bwd", M, N, K, nf::EpiBwd{S, N}, A, B);
+    perf_pers("store", M, N, K, EpiStore{C, N}, A, B);
+    perf_pers("fwd-relu", M, N, K, nf::EpiFwd{bias, C, S, nullptr, N, nf::ACT_RELU, 0}, A, B);
+    perf_pers("fwd-sigm", M, N, K, nf::EpiFwd{bias, C, S, nullptr, N, nf::ACT_SIGMOID, 0}, A, B);
+    perf_pers("bwd", M, N, K, nf::EpiBwd{S, N}, A, B);
+    // correctness of the persistent kernel against fp64 (and the per-tile kernel's error)
+    {
+      const int Mc = 1024;  // rows checked (fp64 reference cost)
+      float *C2; CK(cudaMalloc(&C2, (size_t)M * N * 4));
+      double *R; CK(cudaMalloc(&R, (size_t)Mc * N * 8));
+      perf_epi("store-ref", M, N, K, EpiStore{C2, N}, A, B);
+      perf_pers("store", M, N, K, EpiStore{C, N}, A, B);
+      ref_gemm<<<dim3((N + 15) / 16, (Mc + 15) / 16), dim3(16, 16)>>>(A, B, R, Mc, N, K, 0, 0);
+      CK(cudaDeviceSynchronize());
+      std::vector<float> h1((size_t)Mc * N), h2((size_t)Mc * N);
+      std::vector<double> r((size_t)Mc * N);
+      CK(cudaMemcpy(h1.data(), C, h1.size() * 4, cudaMemcpyDeviceToHost));
+      CK(cudaMemcpy(h2.data(), C2, h2.size() * 4, cudaMemcpyDeviceToHost));
+      CK(cudaMemcpy(r.data(), R, r.size() * 8, cudaMemcpyDeviceToHost));
+      double mx = 0, e1 = 0, e2 = 0;
+      for (size_t i = 0; i < r.size(); ++i) mx = std::max(mx, std::fabs(r[i]));
+      for (size_t i = 0; i < r.size(); ++i) {
+        const double sc = std::max(std::fabs(r[i]), 0.1 * mx);
+        e1 = std::max(e1, std::fabs(h1[i] - r[i]) / sc);
+        e2 = std::max(e2, std::fabs(h2[i] - r[i]) / sc);
+      }
+      printf("PERSISTENT max rel err (tau=0.1, first %d rows) %.3e; per-tile kernel %.3e\n", Mc, e1, e2);
+    }
   }
   printf("done\n");
 }

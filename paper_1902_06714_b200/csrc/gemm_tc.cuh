@@ -300,5 +300,139 @@ gemm_tc_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ 
   }
 }
 
+// ---- persistent variant (1xTF32) -------------------------------------------------------
+// One CTA per SM walks tiles tile = blockIdx.x + i * gridDim.x (n fastest, so a wave shares
+// A rows and all of B stays hot in L2).  Two TMEM accumulator stages of BN columns: the MMA
+// warp fills stage s for tile i+1 while the epilogue warps drain stage s^1 of tile i, so the
+// epilogue (bias + activation + stash / x sigma' / SGD RMW) overlaps the next main loop.
+template <int BN, bool A_MN, bool B_MN, class Epi>
+__global__ void __launch_bounds__(kThreads, 1)
+gemm_tc_persistent(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB, int M, int N,
+                   int K, Epi epi) {
+  using C = Cfg<BN, 1>;
+  static_assert(2 * BN <= 512, "two accumulator stages must fit in TMEM");
+  extern __shared__ uint8_t smem_raw[];
+  uint8_t *smem = reinterpret_cast<uint8_t *>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+  float *epibuf = reinterpret_cast<float *>(smem + C::STAGES * C::STAGE_BYTES);
+  uint64_t *full = reinterpret_cast<uint64_t *>(smem + C::STAGES * C::STAGE_BYTES + kEpiBytes);
+  uint64_t *empty = full + C::STAGES;
+  uint64_t *tfull = empty + C::STAGES;   // [2] accumulator stage ready (tcgen05.commit)
+  uint64_t *tempty = tfull + 2;          // [2] accumulator stage drained (4 epilogue warps)
+  uint32_t *tmem_slot = reinterpret_cast<uint32_t *>(tempty + 2);
+
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int tn = (N + BN - 1) / BN, ntiles = ((M + BM - 1) / BM) * tn;
+  const int nkb = (K + BK - 1) / BK;
+
+  if (threadIdx.x == 0) {
+    for (int s = 0; s < C::STAGES; ++s) {
+      ptx::mbar_init(&full[s], 1);
+      ptx::mbar_init(&empty[s], 1);
+    }
+    for (int s = 0; s < 2; ++s) {
+      ptx::mbar_init(&tfull[s], 1);
+      ptx::mbar_init(&tempty[s], 4);
+    }
+    ptx::fence_mbar_init();
+    ptx::prefetch_tensormap(&tmA);
+    ptx::prefetch_tensormap(&tmB);
+  }
+  if (warp == 1) {
+    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;"
+                 ::"r"(ptx::smem_u32(tmem_slot)), "r"((uint32_t)(2 * BN)) : "memory");
+    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;" ::: "memory");
+  }
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  const uint32_t tmem = *tmem_slot;
+
+  if (warp == 0) {
+    if (lane == 0) {  // ---- TMA producer, continuous over tiles
+      int it = 0;
+      for (int tile = blockIdx.x; tile < ntiles; tile += gridDim.x) {
+        const int m0 = (tile / tn) * BM, n0 = (tile % tn) * BN;
+        for (int kb = 0; kb < nkb; ++kb, ++it) {
+          const int s = it % C::STAGES;
+          if (it >= C::STAGES) ptx::mbar_wait(&empty[s], (uint32_t)(((it / C::STAGES) - 1) & 1));
+          uint8_t *sa = smem + s * C::STAGE_BYTES;
+          uint8_t *sb = sa + C::A_BYTES;
+          const int k = kb * BK;
+          ptx::mbar_arrive_expect_tx(&full[s], (uint32_t)C::RAW_BYTES);
+          if (A_MN) {
+#pragma unroll
+            for (int i = 0; i < BM / 32; ++i) ptx::tma_load_2d(sa + i * 4096, &tmA, &full[s], m0 + 32 * i, k);
+          } else {
+            ptx::tma_load_2d(sa, &tmA, &full[s], k, m0);
+          }
+          if (B_MN) {
+#pragma unroll
+            for (int i = 0; i < BN / 32; ++i) ptx::tma_load_2d(sb + i * 4096, &tmB, &full[s], n0 + 32 * i, k);
+          } else {
+            ptx::tma_load_2d(sb, &tmB, &full[s], k, n0);
+          }
+        }
+      }
+    }
+  } else if (warp == 1) {
+    if (lane == 0) {  // ---- MMA issuer
+      constexpr uint32_t idesc = idesc_tf32(BM, BN, A_MN, B_MN);
+      int it = 0, lt = 0;
+      for (int tile = blockIdx.x; tile < ntiles; tile += gridDim.x, ++lt) {
+        const int as = lt & 1;
+        if (lt >= 2) ptx::mbar_wait(&tempty[as], (uint32_t)(((lt >> 1) - 1) & 1));
+        tc_fence_after();
+        const uint32_t d = tmem + (uint32_t)(as * BN);
+        for (int kb = 0; kb < nkb; ++kb, ++it) {
+          const int s = it % C::STAGES;
+          ptx::mbar_wait(&full[s], (uint32_t)((it / C::STAGES) & 1));
+          tc_fence_after();
+          const uint32_t sa = ptx::smem_u32(smem + s * C::STAGE_BYTES);
+          const uint32_t sb = sa + C::A_BYTES;
+#pragma unroll
+          for (int ks = 0; ks < BK / 8; ++ks)
+            mma_tf32(d, op_desc<A_MN>(sa, ks), op_desc<B_MN>(sb, ks), idesc, (kb | ks) != 0 ? 1u : 0u);
+          mma_commit(&empty[s]);
+        }
+        mma_commit(&tfull[as]);
+      }
+    }
+  } else {  // ---- epilogue warps 2..5: TMEM lane quadrant = warp % 4
+    const int q = warp & 3;
+    float *buf = epibuf + q * 32 * 33;
+    int lt = 0;
+    for (int tile = blockIdx.x; tile < ntiles; tile += gridDim.x, ++lt) {
+      const int as = lt & 1;
+      const int m0 = (tile / tn) * BM, n0 = (tile % tn) * BN;
+      ptx::mbar_wait(&tfull[as], (uint32_t)((lt >> 1) & 1));
+      tc_fence_after();
+      const int mrow0 = m0 + q * 32;
+#pragma unroll 1
+      for (int c = 0; c < BN / 32; ++c) {
+        const int nc = n0 + c * 32;
+        if (nc >= N) break;  // warp-uniform
+        float v[32];
+        tmem_ld32(tmem + ((uint32_t)(q * 32) << 16) + (uint32_t)(as * BN + c * 32), v);
+#pragma unroll
+        for (int j = 0; j < 32; ++j) buf[lane * 33 + j] = v[j];
+        __syncwarp();
+        const int n = nc + lane;
+        if (n < N) epi.strip(mrow0, M, n, buf + lane);
+        __syncwarp();
+      }
+      tc_fence_before();
+      __syncwarp();
+      if (lane == 0) ptx::mbar_arrive(&tempty[as]);
+    }
+  }
+  tc_fence_before();
+  __syncthreads();
+  if (warp == 1) {
+    tc_fence_after();
+    asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem), "r"((uint32_t)(2 * BN))
+                 : "memory");
+  }
+}
+
 }  // namespace tc
 }  // namespace nf

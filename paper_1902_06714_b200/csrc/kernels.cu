@@ -136,6 +136,26 @@ cudaError_t launch_tc(cudaStream_t st, int M, int N, int K, const TcOp &a, const
   return cudaGetLastError();
 }
 
+// Persistent 1xTF32 kernel (double-buffered TMEM accumulators, epilogue overlapped with the
+// next tile's main loop): for GEMMs of more than one wave of 128x256 tiles.
+template <bool AMN, bool BMN, class Epi>
+cudaError_t launch_tc_persistent(cudaStream_t st, int M, int N, int K, const TcOp &a, const TcOp &b, const Epi &epi) {
+  using C = tc::Cfg<256, 1>;
+  auto kern = tc::gemm_tc_persistent<256, AMN, BMN, Epi>;
+  static bool attr = false;
+  if (!attr) {
+    cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, C::SMEM);
+    if (e != cudaSuccess) return e;
+    attr = true;
+  }
+  CUtensorMap ta, tb;
+  if (!make_map(&ta, a, M, K, tc::BM) || !make_map(&tb, b, N, K, 256)) return cudaErrorInvalidValue;
+  const int tiles = ((M + tc::BM - 1) / tc::BM) * ((N + 255) / 256);
+  kern<<<std::min(tiles, kSMs), tc::kThreads, C::SMEM, st>>>(ta, tb, M, N, K, epi);
+  count_launch();
+  return cudaGetLastError();
+}
+
 template <bool AMN, bool BMN, class Epi>
 cudaError_t run_tc(cudaStream_t st, int M, int N, int K, const TcOp &a, const TcOp &b, const Epi &epi,
                    const Workspace &ws) {
@@ -146,6 +166,8 @@ cudaError_t run_tc(cudaStream_t st, int M, int N, int K, const TcOp &a, const Tc
   const int fill = kSMs * 4 / 5;
   if (ws.math == 1) {
     g_last_engine = ENGINE_TC1;
+    if (N > 128 && tiles(256) > kSMs && getenv("NF_TC_NO_PERSISTENT") == nullptr)
+      return launch_tc_persistent<AMN, BMN>(st, M, N, K, a, b, epi);
     if (N > 128 && tiles(256) >= fill) return launch_tc<256, AMN, BMN, 1>(st, M, N, K, a, b, epi, ws);
     if (N > 64 && tiles(128) >= fill) return launch_tc<128, AMN, BMN, 1>(st, M, N, K, a, b, epi, ws);
     return launch_tc<64, AMN, BMN, 1>(st, M, N, K, a, b, epi, ws);
