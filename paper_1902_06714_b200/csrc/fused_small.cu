@@ -153,7 +153,15 @@ __device__ __forceinline__ void tc_split(uint8_t *hi, uint8_t *lo, int bytes, in
   }
 }
 
-template <bool TC>
+// AH / AO: compile-time hidden / output activations (-1 = read p.act_h / p.act_o at run time).
+// The sigmoid/sigmoid instantiation (configs 1 and 2) keeps the dependent owner-row chain
+// short: no activation switch.
+template <int AH, int AO>
+__device__ __forceinline__ void act_sel(int rt, float z, float &a, float &s) {
+  act_fwd(AH >= 0 ? AH : rt, z, a, s);
+}
+
+template <bool TC, int AH, int AO>
 __global__ void __launch_bounds__(kThreads, 1)
 fused_small_kernel(const FusedParams p, const __grid_constant__ CUtensorMap tmX,
                    const __grid_constant__ CUtensorMap tmXK, const __grid_constant__ CUtensorMap tmXM) {
@@ -271,7 +279,8 @@ fused_small_kernel(const FusedParams p, const __grid_constant__ CUtensorMap tmX,
     if (TC) {
       // x tiles are staged by tc_issue (two layouts per step)
     } else if (p.aligned) {
-      if (tid == 0) {
+      // issued by the last warp, which has no P1 task: the issue latency stays off the P1 path
+      if (tid == kThreads - 32) {
         ptx::mbar_arrive_expect_tx(&bar_x[buf], xbytes);
         ptx::tma_load_2d(xs, &tmX, &bar_x[buf], k0, (int)row0);
       }
@@ -282,7 +291,7 @@ fused_small_kernel(const FusedParams p, const __grid_constant__ CUtensorMap tmX,
       }
     }
     float *ys = ys0 + buf * p.nOwnMax * 32;
-    for (int i = tid; i < nOwn * O; i += kThreads) {
+    for (int i = tid - (kThreads - 64); i >= 0 && i < nOwn * O; i += 64) {  // the last two warps
       const int r = i / O, c = i % O;
       cp_async4(ys + r * 32 + c, p.Y + (row0 + o0 + r) * O + c);
     }
@@ -432,7 +441,7 @@ fused_small_kernel(const FusedParams p, const __grid_constant__ CUtensorMap tmX,
       for (int c = 0; c < kMaxC; ++c)
         if (c < C) z += (c == rank) ? Pfull[i * 32 + j] : Pown[(c * p.nOwnMax + q) * 32 + j];
       float a1, s1;
-      act_fwd(p.act_h, z, a1, s1);
+      act_sel<AH, AO>(p.act_h, z, a1, s1);
       A1own[t] = j < H ? a1 : 0.0f;
       D1[i * 32 + j] = j < H ? s1 : 0.0f;   // sigma'(z1) parked in the delta_1 row
     }
@@ -452,7 +461,7 @@ fused_small_kernel(const FusedParams p, const __grid_constant__ CUtensorMap tmX,
       for (; j < H; ++j) c0 = fmaf(w2[j], va[j], c0);
       const float z2 = b2s[o] + ((c0 + c1) + (c2 + c3));
       float a2, s2;
-      act_fwd(p.act_o, z2, a2, s2);
+      act_sel<AO, AO>(p.act_o, z2, a2, s2);
       const float diff = a2 - ys[q * 32 + o];
       lacc = fmaf(diff, diff, lacc);
       D2own[q * 32 + o] = diff * s2;
@@ -753,7 +762,8 @@ int fused_small_train_steps(FusedSmall &fs, cudaStream_t st, const std::vector<i
 
   static bool attr_done = false;
   if (!attr_done) {
-    for (auto k : {fused_small_kernel<false>, fused_small_kernel<true>}) {
+    for (auto k : {fused_small_kernel<false, -1, -1>, fused_small_kernel<true, -1, -1>,
+                   fused_small_kernel<false, ACT_SIGMOID, ACT_SIGMOID>}) {
       cudaFuncSetAttribute(k, cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
       cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024);
     }
@@ -788,7 +798,8 @@ int fused_small_train_steps(FusedSmall &fs, cudaStream_t st, const std::vector<i
       if (cfg.dynamicSmemBytes > 227 * 1024) continue;
       int ncl = 0;
       const bool tcc = tc && (batch + cand - 1) / cand <= kTcRows;
-      if (cudaOccupancyMaxActiveClusters(&ncl, tcc ? fused_small_kernel<true> : fused_small_kernel<false>, &cfg) !=
+      if (cudaOccupancyMaxActiveClusters(&ncl, tcc ? fused_small_kernel<true, -1, -1> : fused_small_kernel<false, -1, -1>,
+                                         &cfg) !=
           cudaSuccess) {
         cudaGetLastError();
         continue;
@@ -875,8 +886,10 @@ int fused_small_train_steps(FusedSmall &fs, cudaStream_t st, const std::vector<i
     cfg.blockDim = dim3(kThreads);
     cfg.dynamicSmemBytes = smem;
     cfg.stream = st;
-    e = tc ? cudaLaunchKernelEx(&cfg, fused_small_kernel<true>, p, tmX, tmXK, tmXM)
-           : cudaLaunchKernelEx(&cfg, fused_small_kernel<false>, p, tmX, tmXK, tmXM);
+    const bool sig = act_h == ACT_SIGMOID && act_o == ACT_SIGMOID;
+    e = tc    ? cudaLaunchKernelEx(&cfg, fused_small_kernel<true, -1, -1>, p, tmX, tmXK, tmXM)
+        : sig ? cudaLaunchKernelEx(&cfg, fused_small_kernel<false, ACT_SIGMOID, ACT_SIGMOID>, p, tmX, tmXK, tmXM)
+              : cudaLaunchKernelEx(&cfg, fused_small_kernel<false, -1, -1>, p, tmX, tmXK, tmXM);
     count_launch();
   }
   if (e != cudaSuccess) {
