@@ -45,7 +45,14 @@ static thread_local char g_fs_err[256] = "";
 
 namespace {
 
-constexpr int kThreads = 512;  // 16 warps: latency hiding for the short dependent phases
+#ifndef NF_FUSED_THREADS
+#define NF_FUSED_THREADS 512
+#endif
+#ifndef NF_FUSED_MINB
+#define NF_FUSED_MINB 1
+#endif
+constexpr int kThreads = NF_FUSED_THREADS;  // 16 warps: latency hiding for the short dependent phases
+constexpr int kMinBlocks = NF_FUSED_MINB;  // CTAs per SM the kernel is built for
 constexpr int kWarps = kThreads / 32;
 constexpr int kMaxC = 8;       // cluster size
 constexpr int kMaxRows = 128;  // rows per cluster
@@ -162,7 +169,7 @@ __device__ __forceinline__ void act_sel(int rt, float z, float &a, float &s) {
 }
 
 template <bool TC, int AH, int AO>
-__global__ void __launch_bounds__(kThreads, 1)
+__global__ void __launch_bounds__(kThreads, kMinBlocks)
 fused_small_kernel(const FusedParams p, const __grid_constant__ CUtensorMap tmX,
                    const __grid_constant__ CUtensorMap tmXK, const __grid_constant__ CUtensorMap tmXM) {
   extern __shared__ __align__(128) float sm[];
@@ -790,7 +797,7 @@ int fused_small_train_steps(FusedSmall &fs, cudaStream_t st, const std::vector<i
     cfg.numAttrs = 1;
     cfg.blockDim = dim3(kThreads);
     const int maxG = env_int("NF_FUSED_G", 0);
-    int want = maxG > 0 ? maxG : (int)std::max<int64_t>(1, std::min<int64_t>(batch / 16, 148 / C));
+    int want = maxG > 0 ? maxG : (int)std::max<int64_t>(1, std::min<int64_t>(batch / 16, kMinBlocks * 148 / C));
     for (int cand = want; cand >= 1; --cand) {
       if ((batch + cand - 1) / cand > kMaxRows) break;
       cfg.gridDim = dim3(cand * C);

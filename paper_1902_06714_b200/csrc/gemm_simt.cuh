@@ -14,6 +14,7 @@
 // kernel sums in a fixed order (deterministic) before the same epilogue.
 #pragma once
 #include "nf_common.cuh"
+#include "sm100_ptx.cuh"
 
 namespace nf {
 
@@ -130,6 +131,8 @@ struct EpiGrad {
 template <int BM, int BN, int BK, int TM, int TN, bool AK, bool BKM, class Epi>
 __global__ void __launch_bounds__((BM / TM) * (BN / TN))
 gemm_simt(GemmArgs g, Epi epi) {
+  ptx::pdl_trigger();
+  ptx::pdl_wait();
   constexpr int NT = (BM / TM) * (BN / TN);
   constexpr int APT = BM * BK / NT;
   constexpr int BPT = BN * BK / NT;
@@ -235,6 +238,8 @@ gemm_simt(GemmArgs g, Epi epi) {
 template <class Epi>
 __global__ void __launch_bounds__(256)
 splitk_epilogue(const float *__restrict__ partial, int splits, int M, int N, Epi epi) {
+  ptx::pdl_trigger();
+  ptx::pdl_wait();
   const int64_t MN = (int64_t)M * N;
   for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < MN;
        i += (int64_t)gridDim.x * blockDim.x) {

@@ -146,6 +146,7 @@ __global__ void __launch_bounds__(kThreads, 1)
 gemm_tc_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB, TileArgs g,
                Epi epi) {
   using C = Cfg<BN, SPLIT>;
+  ptx::pdl_trigger();
   extern __shared__ uint8_t smem_raw[];
   uint8_t *smem = reinterpret_cast<uint8_t *>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
   float *epibuf = reinterpret_cast<float *>(smem + C::STAGES * C::STAGE_BYTES);
@@ -181,6 +182,7 @@ gemm_tc_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ 
   __syncthreads();
   tc_fence_after();
   const uint32_t tmem = *tmem_slot;
+  ptx::pdl_wait();  // prologue above overlaps the previous kernel
 
   if (warp == 0) {
     if (lane == 0) {  // ---- TMA producer
@@ -311,6 +313,7 @@ gemm_tc_persistent(const __grid_constant__ CUtensorMap tmA, const __grid_constan
                    int K, Epi epi) {
   using C = Cfg<BN, 1>;
   static_assert(2 * BN <= 512, "two accumulator stages must fit in TMEM");
+  ptx::pdl_trigger();
   extern __shared__ uint8_t smem_raw[];
   uint8_t *smem = reinterpret_cast<uint8_t *>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
   float *epibuf = reinterpret_cast<float *>(smem + C::STAGES * C::STAGE_BYTES);
@@ -346,6 +349,7 @@ gemm_tc_persistent(const __grid_constant__ CUtensorMap tmA, const __grid_constan
   __syncthreads();
   tc_fence_after();
   const uint32_t tmem = *tmem_slot;
+  ptx::pdl_wait();  // prologue above overlaps the previous kernel
 
   if (warp == 0) {
     if (lane == 0) {  // ---- TMA producer, continuous over tiles

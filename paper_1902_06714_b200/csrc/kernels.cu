@@ -18,6 +18,32 @@ namespace {
 
 constexpr int kSMs = 148;
 
+// Every kernel of the generic path is launched with programmatic stream serialization (PDL):
+// the next kernel's CTAs are scheduled while the current one drains, run their prologue
+// (barrier init, TMEM allocation, tensor-map prefetch) and block in griddepcontrol.wait until
+// it has completed.  NF_NO_PDL=1 turns it off.
+bool pdl_enabled() {
+  static int v = -1;
+  if (v < 0) v = getenv("NF_NO_PDL") ? 0 : 1;
+  return v == 1;
+}
+
+template <class... KArgs, class... Args>
+cudaError_t launch_k(void (*kern)(KArgs...), dim3 grid, dim3 block, size_t smem, cudaStream_t st, Args... args) {
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = grid;
+  cfg.blockDim = block;
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = st;
+  cudaLaunchAttribute at[1];
+  at[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  at[0].val.programmaticStreamSerializationAllowed = 1;
+  cfg.attrs = at;
+  cfg.numAttrs = pdl_enabled() ? 1 : 0;
+  count_launch();
+  return cudaLaunchKernelEx(&cfg, kern, static_cast<KArgs>(args)...);
+}
+
 enum Cfg { CFG_L, CFG_M, CFG_S, CFG_T };
 
 Cfg choose_cfg(int M, int N) {
@@ -44,13 +70,13 @@ cudaError_t launch_cfg(cudaStream_t st, GemmArgs g, const Epi &epi, const Worksp
   g.kchunk = splits > 1 ? kchunk : std::max(g.K, 1);
   g.partial = splits > 1 ? ws.partial : nullptr;
   dim3 grid(tn, tm, splits);
-  gemm_simt<BM, BN, BK, TM, TN, AK, BKM, Epi><<<grid, (BM / TM) * (BN / TN), 0, st>>>(g, epi);
-  count_launch();
+  cudaError_t e = launch_k(gemm_simt<BM, BN, BK, TM, TN, AK, BKM, Epi>, grid, dim3((BM / TM) * (BN / TN)), 0, st, g, epi);
+  if (e != cudaSuccess) return e;
   if (splits > 1) {
     const int64_t MN = (int64_t)g.M * g.N;
     const int blocks = (int)std::min<int64_t>((MN + 255) / 256, 4 * kSMs);
-    splitk_epilogue<Epi><<<blocks, 256, 0, st>>>(ws.partial, splits, g.M, g.N, epi);
-    count_launch();
+    e = launch_k(splitk_epilogue<Epi>, dim3(blocks), dim3(256), 0, st, ws.partial, splits, g.M, g.N, epi);
+    if (e != cudaSuccess) return e;
   }
   return cudaGetLastError();
 }
@@ -125,13 +151,13 @@ cudaError_t launch_tc(cudaStream_t st, int M, int N, int K, const TcOp &a, const
   const int kbper = (nkb + splits - 1) / splits;
   splits = (nkb + kbper - 1) / kbper;  // no empty K-chunk
   tc::TileArgs g{M, N, K, kbper * tc::BK, splits > 1 ? ws.partial : nullptr};
-  kern<<<dim3(tn, tm, splits), tc::kThreads, C::SMEM, st>>>(ta, tb, g, epi);
-  count_launch();
+  cudaError_t e = launch_k(kern, dim3(tn, tm, splits), dim3(tc::kThreads), C::SMEM, st, ta, tb, g, epi);
+  if (e != cudaSuccess) return e;
   if (splits > 1) {
     const int64_t MN = (int64_t)M * N;
     const int blocks = (int)std::min<int64_t>((MN + 255) / 256, 4 * kSMs);
-    splitk_epilogue<Epi><<<blocks, 256, 0, st>>>(ws.partial, splits, M, N, epi);
-    count_launch();
+    e = launch_k(splitk_epilogue<Epi>, dim3(blocks), dim3(256), 0, st, ws.partial, splits, M, N, epi);
+    if (e != cudaSuccess) return e;
   }
   return cudaGetLastError();
 }
@@ -151,9 +177,7 @@ cudaError_t launch_tc_persistent(cudaStream_t st, int M, int N, int K, const TcO
   CUtensorMap ta, tb;
   if (!make_map(&ta, a, M, K, tc::BM) || !make_map(&tb, b, N, K, 256)) return cudaErrorInvalidValue;
   const int tiles = ((M + tc::BM - 1) / tc::BM) * ((N + 255) / 256);
-  kern<<<std::min(tiles, kSMs), tc::kThreads, C::SMEM, st>>>(ta, tb, M, N, K, epi);
-  count_launch();
-  return cudaGetLastError();
+  return launch_k(kern, dim3(std::min(tiles, kSMs)), dim3(tc::kThreads), C::SMEM, st, ta, tb, M, N, K, epi);
 }
 
 template <bool AMN, bool BMN, class Epi>
@@ -181,6 +205,8 @@ cudaError_t run_tc(cudaStream_t st, int M, int N, int K, const TcOp &a, const Tc
 // row chunks summed in a fixed order, then the same EpiGrad bias element update.
 __global__ void __launch_bounds__(256)
 colsum_partial(const float *__restrict__ D, int64_t rows, int cols, int chunk, float *__restrict__ part) {
+  ptx::pdl_trigger();
+  ptx::pdl_wait();
   const int c = blockIdx.x * 256 + threadIdx.x;
   if (c >= cols) return;
   const int64_t r0 = (int64_t)blockIdx.y * chunk, r1 = min(rows, r0 + chunk);
@@ -198,6 +224,8 @@ colsum_partial(const float *__restrict__ D, int64_t rows, int cols, int chunk, f
 
 __global__ void __launch_bounds__(256)
 colsum_final(const float *__restrict__ part, int nchunks, int cols, EpiGrad epi) {
+  ptx::pdl_trigger();
+  ptx::pdl_wait();
   const int c = blockIdx.x * 256 + threadIdx.x;
   if (c >= cols) return;
   float s = 0.f;
@@ -212,10 +240,9 @@ cudaError_t bias_grad(cudaStream_t st, const float *D, int64_t rows, int cols, c
   while (nchunks > 1 && (size_t)nchunks * cols > part_floats) --nchunks;
   const int chunk = (int)((rows + nchunks - 1) / nchunks);
   const dim3 grid((cols + 255) / 256, nchunks);
-  colsum_partial<<<grid, 256, 0, st>>>(D, rows, cols, chunk, part);
-  colsum_final<<<(cols + 255) / 256, 256, 0, st>>>(part, nchunks, cols, epi);
-  count_launch(2);
-  return cudaGetLastError();
+  cudaError_t e = launch_k(colsum_partial, grid, dim3(256), 0, st, D, rows, cols, chunk, part);
+  if (e != cudaSuccess) return e;
+  return launch_k(colsum_final, dim3((cols + 255) / 256), dim3(256), 0, st, (const float *)part, nchunks, cols, epi);
 }
 
 // ---------------------------------------------------------------------------
@@ -227,6 +254,8 @@ cudaError_t bias_grad(cudaStream_t st, const float *D, int64_t rows, int cols, c
 template <int NMAX>
 __global__ void __launch_bounds__(256)
 fwd_smalln(const float *__restrict__ A, const float *__restrict__ W, int M, int N, int K, EpiFwd epi) {
+  ptx::pdl_trigger();
+  ptx::pdl_wait();
   extern __shared__ float ws_[];
   for (int i = threadIdx.x; i < N * K; i += blockDim.x) ws_[i] = W[i];
   __syncthreads();
@@ -263,6 +292,8 @@ fwd_smalln(const float *__restrict__ A, const float *__restrict__ W, int M, int 
 template <int KMAX>
 __global__ void __launch_bounds__(128)
 bwd_smallk(const float *__restrict__ D, const float *__restrict__ W, int M, int N, int K, int TM, EpiBwd epi) {
+  ptx::pdl_trigger();
+  ptx::pdl_wait();
   const int n = (blockIdx.x * 128 + threadIdx.x) * 4;
   if (n >= N) return;
   float4 w[KMAX];
@@ -303,6 +334,8 @@ template <int MMAX>
 __global__ void __launch_bounds__(128)
 grad_smallm_partial(const float *__restrict__ D, const float *__restrict__ A, int M, int N, int K, int chunk,
                     float *__restrict__ part) {
+  ptx::pdl_trigger();
+  ptx::pdl_wait();
   __shared__ float dsm[128 * MMAX];
   const int n = blockIdx.x * 128 + threadIdx.x;
   const int b0 = blockIdx.y * chunk, b1 = min(K, b0 + chunk);
@@ -345,6 +378,8 @@ grad_smallm_partial(const float *__restrict__ D, const float *__restrict__ A, in
 // flight (deterministic)
 __global__ void __launch_bounds__(256)
 grad_smallm_final(const float *__restrict__ part, int R, int M, int N, EpiGrad epi) {
+  ptx::pdl_trigger();
+  ptx::pdl_wait();
   const int64_t MN = (int64_t)M * (N + 1);
   for (int64_t t = blockIdx.x * 256 + threadIdx.x; t < MN; t += (int64_t)gridDim.x * 256) {
     float s = 0.0f;
@@ -373,9 +408,7 @@ cudaError_t gemm_fwd(cudaStream_t st, int M, int N, int K, const float *A, const
       attr = true;
     }
     const int blocks = std::min((M + 7) / 8, 4 * kSMs);
-    fwd_smalln<16><<<blocks, 256, (size_t)N * K * 4, st>>>(A, W, M, N, K, epi);
-    count_launch();
-    return cudaGetLastError();
+    return launch_k(fwd_smalln<16>, dim3(blocks), dim3(256), (size_t)N * K * 4, st, A, W, M, N, K, epi);
   }
   GemmArgs g{M, N, K, A, K, W, K, N, 0, nullptr};
   return run_gemm<true, true>(st, g, epi, ws);
@@ -390,9 +423,7 @@ cudaError_t gemm_bwd(cudaStream_t st, int M, int N, int K, const float *D, const
       (reinterpret_cast<uintptr_t>(epi.SD) & 15) == 0 && M >= 256) {
     const int cb = (N / 4 + 127) / 128;
     const int TM = std::max(4, (int)((int64_t)M * cb / (8 * kSMs)));
-    bwd_smallk<16><<<dim3(cb, (M + TM - 1) / TM), 128, 0, st>>>(D, W, M, N, K, TM, epi);
-    count_launch();
-    return cudaGetLastError();
+    return launch_k(bwd_smallk<16>, dim3(cb, (M + TM - 1) / TM), dim3(128), 0, st, D, W, M, N, K, TM, epi);
   }
   GemmArgs g{M, N, K, D, K, W, N, N, 0, nullptr};
   return run_gemm<true, false>(st, g, epi, ws);
@@ -415,11 +446,12 @@ cudaError_t gemm_grad(cudaStream_t st, int M, int N, int K, const float *D, cons
     while (R > 1 && (size_t)R * M * (N + 1) > ws.partial_floats) --R;
     const int chunk = (K + R - 1) / R;
     R = (K + chunk - 1) / chunk;
-    grad_smallm_partial<16><<<dim3(cb, R), 128, 0, st>>>(D, Aprev, M, N, K, chunk, ws.partial);
+    cudaError_t e = launch_k(grad_smallm_partial<16>, dim3(cb, R), dim3(128), 0, st, D, Aprev, M, N, K, chunk,
+                             ws.partial);
+    if (e != cudaSuccess) return e;
     const int64_t MN = (int64_t)M * (N + 1);
-    grad_smallm_final<<<(int)std::min<int64_t>((MN + 255) / 256, 2 * kSMs), 256, 0, st>>>(ws.partial, R, M, N, epi);
-    count_launch(2);
-    return cudaGetLastError();
+    return launch_k(grad_smallm_final, dim3((int)std::min<int64_t>((MN + 255) / 256, 2 * kSMs)), dim3(256), 0, st,
+                    (const float *)ws.partial, R, M, N, epi);
   }
   // C[M][N+1]: column N is the ones column -> bias gradient.
   GemmArgs g{M, N + 1, K, D, M, Aprev, N, N, 0, nullptr};
@@ -440,6 +472,8 @@ __device__ __forceinline__ void argmax_merge(float &v, int &i, float v2, int i2)
 __global__ void __launch_bounds__(256)
 loss_acc_partial(const float *__restrict__ A, const float *__restrict__ Y, int64_t n, int w,
                  double2 *__restrict__ part) {
+  ptx::pdl_trigger();
+  ptx::pdl_wait();
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   const int64_t gw = (int64_t)blockIdx.x * 8 + warp, nw = (int64_t)gridDim.x * 8;
   double lsum = 0.0, csum = 0.0;
@@ -477,6 +511,8 @@ loss_acc_partial(const float *__restrict__ A, const float *__restrict__ Y, int64
 // (deterministic for a given nparts).
 __global__ void loss_acc_final(const double2 *__restrict__ part, int nparts, int64_t n,
                                float *out, float *step_loss) {
+  ptx::pdl_trigger();
+  ptx::pdl_wait();
   const int lane = threadIdx.x;
   double l = 0.0, c = 0.0;
   for (int i = lane; i < nparts; i += 32) { l += part[i].x; c += part[i].y; }
@@ -498,10 +534,9 @@ int loss_acc_parts() { return kLossBlocks; }
 cudaError_t loss_acc(cudaStream_t st, const float *A, const float *Y, int64_t n, int w,
                      double2 *part, float *out, float *step_loss) {
   const int blocks = (int)std::max<int64_t>(1, std::min<int64_t>(kLossBlocks, (n + 7) / 8));
-  loss_acc_partial<<<blocks, 256, 0, st>>>(A, Y, n, w, part);
-  loss_acc_final<<<1, 32, 0, st>>>(part, blocks, n, out, step_loss);
-  count_launch(2);
-  return cudaGetLastError();
+  cudaError_t e = launch_k(loss_acc_partial, dim3(blocks), dim3(256), 0, st, A, Y, n, w, part);
+  if (e != cudaSuccess) return e;
+  return launch_k(loss_acc_final, dim3(1), dim3(32), 0, st, (const double2 *)part, blocks, n, out, step_loss);
 }
 
 }  // namespace nf

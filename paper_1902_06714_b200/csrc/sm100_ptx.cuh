@@ -108,6 +108,13 @@ __device__ __forceinline__ uint32_t cluster_size() {
   return r;
 }
 
+// ---- programmatic dependent launch ---------------------------------------------------------
+// trigger: let the next kernel in the stream start launching (its CTAs run their prologue);
+// wait: block until every prerequisite grid has completed and its writes are visible.  Both
+// are no-ops for kernels launched without the programmatic-serialization attribute.
+__device__ __forceinline__ void pdl_trigger() { asm volatile("griddepcontrol.launch_dependents;" ::: "memory"); }
+__device__ __forceinline__ void pdl_wait() { asm volatile("griddepcontrol.wait;" ::: "memory"); }
+
 // ---- global atomics / barrier --------------------------------------------------------
 __device__ __forceinline__ void red_add_f32(float *p, float v) {
   asm volatile("red.relaxed.gpu.global.add.f32 [%0], %1;" ::"l"(p), "f"(v) : "memory");

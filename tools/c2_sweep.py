@@ -23,7 +23,10 @@ for _ in range(5):
     ts.append(e0.elapsed_time(e1) / len(st) * 1e3)
 print(sorted(ts)[2])
 '''
-for C, Gs in [(8, [15, 12, 10, 8]), (4, [33, 30, 24, 16]), (6, [22, 16])]:
+grid = [(8, [15, 12]), (4, [33, 30]), (6, [22])]
+if len(sys.argv) > 1 and sys.argv[1] == "2cta":
+    grid = [(8, [30, 36, 24]), (4, [60, 66, 50]), (2, [120])]
+for C, Gs in grid:
     for G in Gs:
         env = dict(os.environ, ROOT=ROOT, NF_FUSED_C=str(C), NF_FUSED_G=str(G))
         r = subprocess.run([sys.executable, "-c", code], env=env, capture_output=True, text=True, timeout=300)
