@@ -116,3 +116,38 @@ def test_tc_c5_full_width_grad():
     for (Wg, bg), (Wr, br) in zip(o.layers(g), o.layers(ref)):
         assert rel_err(Wg, Wr) <= FP32_BAR
         assert rel_err(bg, br) <= FP32_BAR
+
+
+# ------------------------------------------------------------------ full-size launches
+@pytest.mark.parametrize("cid,math", [(5, nf.NF_MATH_TF32), (5, nf.NF_MATH_FP32), (3, nf.NF_MATH_TF32)])
+def test_full_batch_forward_sampled_rows(cid, math):
+    """nf_output over a full training batch (c5: 16384 rows, the persistent 1xTF32 GEMM in TF32
+    mode; c3: 4096 rows) in the launch configuration bench.py times; 16 sampled rows against the
+    fp64 oracle (rows the oracle can afford one by one)."""
+    cfg = synth.CONFIGS[cid]
+    dims = cfg["dims"]
+    p = synth.init_params(cid)
+    X, _ = synth.dataset(cid, N=cfg["batch"])
+    net = make_net(dims, cfg["act"], p, math)
+    out = net.output(dev(X)).cpu().numpy()
+    rows = np.linspace(0, cfg["batch"] - 1, 16).astype(int)
+    ref = oracle.Oracle(dims, cfg["act"]).output(p, np.ascontiguousarray(X[rows]))
+    check(out[rows], ref, math)
+
+
+@pytest.mark.parametrize("cid,math", [(5, nf.NF_MATH_TF32), (3, nf.NF_MATH_TF32), (3, nf.NF_MATH_FP32)])
+def test_full_batch_grad_split_invariance(cid, math):
+    """The co_sum property at full batch size: the tendencies of the whole batch equal
+    the sum over its two halves, all on the GPU in the bench's launch configuration."""
+    cfg = synth.CONFIGS[cid]
+    dims, B = cfg["dims"], cfg["batch"]
+    p = synth.init_params(cid)
+    X, Y = synth.dataset(cid, N=B)
+    net = make_net(dims, cfg["act"], p, math)
+    g = net.grad(dev(X), dev(Y)).cpu().numpy().astype(np.float64)
+    g1 = net.grad(dev(X[:B // 2]), dev(Y[:B // 2])).cpu().numpy().astype(np.float64)
+    g2 = net.grad(dev(X[B // 2:]), dev(Y[B // 2:])).cpu().numpy().astype(np.float64)
+    o = oracle.Oracle(dims, cfg["act"])
+    for (Wa, ba), (Wb, bb) in zip(o.layers(g), o.layers(g1 + g2)):
+        check(Wa, Wb, math)
+        check(ba, bb, math)
