@@ -526,7 +526,7 @@ fused_small_kernel(const FusedParams p, const __grid_constant__ CUtensorMap tmX,
       const int ce0 = e_begin(c, C, nsmp), cne = e_begin(c + 1, C, nsmp) - ce0;
       if (cne > 0) ptx::bulk_s2peer(grecv + rank * eslot, gpart + ce0, (uint32_t)(cne * 4), bar_D, c);
     }
-    ptx::mbar_wait(bar_D, par);
+    if (TC) ptx::mbar_wait(bar_D, par);  // (the SIMT P5 starts on its own rows and waits inside)
     PROF(5);
 
     if constexpr (TC) {
@@ -577,6 +577,7 @@ fused_small_kernel(const FusedParams p, const __grid_constant__ CUtensorMap tmX,
     } else {
 
     // ---- P5. dW1 slice partial, k-major like W1t: Gs[k][j] = sum_{i<nS} D1[i][j] x[i][k]
+    // Rows of this CTA's own delta_1 first, while the peers' rows are still in flight.
     for (int t = tid; t < nP5; t += kThreads) {
       const int jg = t & 7, kc = (t >> 3) % nchunk, rh = (t >> 3) / nchunk;
       const int ib = rh * nS / kRH, ie = (rh + 1) * nS / kRH;
@@ -585,17 +586,24 @@ fused_small_kernel(const FusedParams p, const __grid_constant__ CUtensorMap tmX,
       float2 a[4][2];  // neuron u, pixel pairs (4kc, 4kc+1), (4kc+2, 4kc+3): packed FFMA2
 #pragma unroll
       for (int u = 0; u < 4; ++u) a[u][0] = a[u][1] = make_float2(0.0f, 0.0f);
+      auto rows = [&](int r0_, int r1_) {
 #pragma unroll 4
-      for (int i = ib; i < ie; ++i) {
-        const float4 d = *reinterpret_cast<const float4 *>(dcol + i * 32);
-        const float4 x = *reinterpret_cast<const float4 *>(xcol + i * wpad);
-        const float dv[4] = {d.x, d.y, d.z, d.w};
+        for (int i = r0_; i < r1_; ++i) {
+          const float4 d = *reinterpret_cast<const float4 *>(dcol + i * 32);
+          const float4 x = *reinterpret_cast<const float4 *>(xcol + i * wpad);
+          const float dv[4] = {d.x, d.y, d.z, d.w};
 #pragma unroll
-        for (int u = 0; u < 4; ++u) {
-          ffma2(a[u][0], dv[u], make_float2(x.x, x.y));
-          ffma2(a[u][1], dv[u], make_float2(x.z, x.w));
+          for (int u = 0; u < 4; ++u) {
+            ffma2(a[u][0], dv[u], make_float2(x.x, x.y));
+            ffma2(a[u][1], dv[u], make_float2(x.z, x.w));
+          }
         }
-      }
+      };
+      const int ob = max(ib, o0), oe = min(ie, o0 + nOwn);
+      rows(ob, oe);
+      ptx::mbar_wait(bar_D, par);  // the peers' delta_1 rows (and W2/b slices) have landed
+      rows(ib, min(ie, ob));
+      rows(max(ib, oe), ie);
       float *g = rh ? Gs2 : Gs;
 #pragma unroll
       for (int v = 0; v < 4; ++v)
@@ -611,6 +619,7 @@ fused_small_kernel(const FusedParams p, const __grid_constant__ CUtensorMap tmX,
       v.x += h.x; v.y += h.y; v.z += h.z; v.w += h.w;
       *d = v;
     }
+    ptx::mbar_wait(bar_D, par);  // threads without a P5 task
     }  // !TC
     // reduce my slice of the W2/b1/b2 tendencies over the cluster (rank order) -> L2
     for (int e = tid; e < ne; e += kThreads) {
