@@ -57,23 +57,30 @@ struct EpiFwd {
   template <int K>
   __device__ __forceinline__ void strip_t(int m0, int mlim, int n, const float *v) const {
     const float bn = bias[n];
-    float y[32];
-    if (mode == 1) {
+    // 8-row groups: the loads of a group are issued before its stores; the loop is not fully
+    // unrolled so the activation code stays small enough for the instruction cache
+    const int rows = min(32, mlim - m0);
+#pragma unroll 1
+    for (int r0 = 0; r0 < rows; r0 += 8) {
+      float y[8];
+      if (mode == 1) {
 #pragma unroll
-      for (int r = 0; r < 32; ++r) y[r] = m0 + r < mlim ? Y[(int64_t)(m0 + r) * ld + n] : 0.0f;
-    }
+        for (int u = 0; u < 8; ++u) y[u] = r0 + u < rows ? Y[(int64_t)(m0 + r0 + u) * ld + n] : 0.0f;
+      }
 #pragma unroll
-    for (int r = 0; r < 32; ++r) {
-      if (m0 + r >= mlim) break;
-      const int64_t i = (int64_t)(m0 + r) * ld + n;
-      const float z = v[33 * r] + bn;
-      if (mode == 2) {
-        A[i] = act_only_t<K>(z);
-      } else {
-        float a, s;
-        act_fwd_t<K>(z, a, s);
-        A[i] = a;
-        S[i] = mode == 0 ? s : (a - y[r]) * s;
+      for (int u = 0; u < 8; ++u) {
+        const int r = r0 + u;
+        if (r >= rows) break;
+        const int64_t i = (int64_t)(m0 + r) * ld + n;
+        const float z = v[33 * r] + bn;
+        if (mode == 2) {
+          A[i] = act_only_t<K>(z);
+        } else {
+          float a, s;
+          act_fwd_t<K>(z, a, s);
+          A[i] = a;
+          S[i] = mode == 0 ? s : (a - y[u]) * s;
+        }
       }
     }
   }

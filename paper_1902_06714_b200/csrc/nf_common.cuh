@@ -21,11 +21,12 @@ __device__ __forceinline__ void act_fwd(int kind, float z, float &a, float &s) {
       s = t * r * r;
       break;
     }
-    case ACT_TANH: {               // sigma' = sech^2 z = 4t/(1+t)^2, t = e^{-2|z|}
-      a = tanhf(z);
-      const float t = expf(-2.0f * fabsf(z));
-      const float r = __frcp_rn(1.0f + t);  // == 1.0f / (1.0f + t), correctly rounded
-      s = 4.0f * t * r * r;
+    case ACT_TANH: {               // t = e^{-2|z|}, e = expm1(-2|z|) = t - 1 (both accurate):
+      const float t = expf(-2.0f * fabsf(z));    // tanh|z| = (1 - t)/(1 + t) = -e / (2 + e),
+      const float e = expm1f(-2.0f * fabsf(z));  // sigma' = sech^2 z = 4t/(1+t)^2; 1 + t and
+      const float r = __frcp_rn(1.0f + t);       // 2 + e carry no cancellation, and t keeps its
+      a = copysignf(-e * __frcp_rn(2.0f + e), z);  // own precision when sigma' is tiny (reading
+      s = 4.0f * t * r * r;                      // R6; a compact replacement of tanhf)
       break;
     }
     case ACT_RELU:                 // relu'(0) = 0 (reading R8)
@@ -62,7 +63,10 @@ __device__ __forceinline__ float act_only(int kind, float z) {
       const float r = __frcp_rn(1.0f + t);  // == 1.0f / (1.0f + t), correctly rounded
       return z >= 0.0f ? r : t * r;
     }
-    case ACT_TANH: return tanhf(z);
+    case ACT_TANH: {
+      const float e = expm1f(-2.0f * fabsf(z));
+      return copysignf(-e * __frcp_rn(2.0f + e), z);
+    }
     case ACT_RELU: return z > 0.0f ? z : 0.0f;
     case ACT_GAUSSIAN: return expf(-z * z);
     default: return z > 0.0f ? 1.0f : 0.0f;

@@ -39,7 +39,12 @@ def main(rep, cubin, kname, top=40, src=None):
     ia, isamp = hdr.index("Address"), hdr.index("Warp Stall Sampling (All Samples)")
     reasons = [h for h in hdr if h.startswith("stall_") and "Not Issued" not in h]
     ir = [hdr.index(h) for h in reasons]
-    data = [r for r in rows[i0 + 1:] if len(r) == len(hdr)]
+    data = []
+    for r in rows[i0 + 1:]:
+        if r and r[0] == "Address":
+            break  # next kernel's section: only the first profiled kernel is attributed
+        if len(r) == len(hdr):
+            data.append(r)
     base = int(data[0][ia], 16)
     agg, tot = defaultdict(int), 0
     marks = phase_of(open(src).read().splitlines()) if src else []
