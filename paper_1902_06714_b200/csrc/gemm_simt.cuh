@@ -53,36 +53,43 @@ struct EpiFwd {
   __device__ __forceinline__ void operator()(int m, int n, float acc) const { store(m, n, acc, load(m, n)); }
 
   // Tensor-core epilogue strip: rows m0..m0+31 (valid while < mlim) of column n; value of
-  // row r at v[33 r].  One switch on the activation per strip, not per element.
-  template <int K>
-  __device__ __forceinline__ void strip_t(int m0, int mlim, int n, const float *v) const {
+  // row r at v[33 r].  The activation and the mode are compile-time inside the strip (one
+  // switch per strip), and each 8-row group evaluates its 8 activations unconditionally so the
+  // eight dependent exp/rcp chains interleave; only the stores are predicated.
+  template <int K, int MODE>
+  __device__ __forceinline__ void strip_km(int m0, int mlim, int n, const float *v) const {
     const float bn = bias[n];
-    // 8-row groups: the loads of a group are issued before its stores; the loop is not fully
-    // unrolled so the activation code stays small enough for the instruction cache
     const int rows = min(32, mlim - m0);
 #pragma unroll 1
     for (int r0 = 0; r0 < rows; r0 += 8) {
-      float y[8];
-      if (mode == 1) {
+      float z[8], a[8], s[8], y[8];
+#pragma unroll
+      for (int u = 0; u < 8; ++u) z[u] = v[33 * (r0 + u)] + bn;
+      if (MODE == 1) {
 #pragma unroll
         for (int u = 0; u < 8; ++u) y[u] = r0 + u < rows ? Y[(int64_t)(m0 + r0 + u) * ld + n] : 0.0f;
       }
 #pragma unroll
       for (int u = 0; u < 8; ++u) {
-        const int r = r0 + u;
-        if (r >= rows) break;
-        const int64_t i = (int64_t)(m0 + r) * ld + n;
-        const float z = v[33 * r] + bn;
-        if (mode == 2) {
-          A[i] = act_only_t<K>(z);
-        } else {
-          float a, s;
-          act_fwd_t<K>(z, a, s);
-          A[i] = a;
-          S[i] = mode == 0 ? s : (a - y[u]) * s;
+        if (MODE == 2) a[u] = act_only_t<K>(z[u]);
+        else act_fwd_t<K>(z[u], a[u], s[u]);
+      }
+#pragma unroll
+      for (int u = 0; u < 8; ++u) {
+        if (r0 + u < rows) {
+          const int64_t i = (int64_t)(m0 + r0 + u) * ld + n;
+          A[i] = a[u];
+          if (MODE == 0) S[i] = s[u];
+          if (MODE == 1) S[i] = (a[u] - y[u]) * s[u];
         }
       }
     }
+  }
+  template <int K>
+  __device__ __forceinline__ void strip_t(int m0, int mlim, int n, const float *v) const {
+    if (mode == 0) strip_km<K, 0>(m0, mlim, n, v);
+    else if (mode == 1) strip_km<K, 1>(m0, mlim, n, v);
+    else strip_km<K, 2>(m0, mlim, n, v);
   }
   __device__ __forceinline__ void strip(int m0, int mlim, int n, const float *v) const {
     switch (act) {

@@ -19,11 +19,11 @@
 // what SPLIT = 1 gets.
 //
 // One CTA computes one BM x BN tile (optionally one K-chunk of it: split-K writes raw
-// partials that splitk_epilogue sums in fixed order).  Warp roles (192 threads):
+// partials that splitk_epilogue sums in fixed order).  Warp roles (320 threads):
 //   warp 0      TMA producer: 2-D tensor-map loads (SWIZZLE_128B) into a STAGES-deep ring
 //   warp 1      TMEM allocator + single-thread tcgen05.mma issuer; tcgen05.commit frees
 //               ring slots and finally signals the accumulator
-//   warps 2..5  (SPLIT = 3) hi/lo splitters during the main loop; then the epilogue:
+//   warps 2..9  (SPLIT = 3) hi/lo splitters during the main loop; then the epilogue:
 //               tcgen05.ld 32x32b.x32 (thread = tile row), transpose through shared memory
 //               so that a warp touches 32 consecutive columns of one row per access
 //               (coalesced), then epi(m, n, value).
@@ -46,9 +46,10 @@ namespace tc {
 
 constexpr int BM = 128;
 constexpr int BK = 32;              // 32 fp32 = 128 B = one SWIZZLE_128B row
-constexpr int kThreads = 192;
+constexpr int kEpiWarps = 8;                 // epilogue warps: 2 per TMEM lane quadrant
+constexpr int kThreads = 64 + 32 * kEpiWarps;  // + TMA producer warp + MMA warp
 constexpr int kSmemBudget = 232448; // max dynamic shared memory per CTA on sm_100
-constexpr int kEpiBytes = 4 * 32 * 33 * 4;
+constexpr int kEpiBytes = kEpiWarps * 32 * 33 * 4;
 
 template <int BN, int SPLIT>
 struct Cfg {
@@ -166,7 +167,7 @@ gemm_tc_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ 
     for (int s = 0; s < C::STAGES; ++s) {
       ptx::mbar_init(&full[s], 1);
       ptx::mbar_init(&empty[s], 1);
-      ptx::mbar_init(&conv[s], 4);
+      ptx::mbar_init(&conv[s], kEpiWarps);
     }
     ptx::mbar_init(accum, 1);
     ptx::fence_mbar_init();
@@ -235,7 +236,7 @@ gemm_tc_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ 
       mma_commit(accum);
     }
   } else {
-    const int t = threadIdx.x - 64;  // 0..127
+    const int t = threadIdx.x - 64;  // 0 .. 32 kEpiWarps - 1
     if (SPLIT == 3) {  // ---- hi/lo splitters
       for (int it = 0; it < nkb; ++it) {
         const int s = it % C::STAGES;
@@ -243,7 +244,7 @@ gemm_tc_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ 
         float4 *raw = reinterpret_cast<float4 *>(smem + s * C::STAGE_BYTES);
         float4 *lo = reinterpret_cast<float4 *>(smem + s * C::STAGE_BYTES + C::RAW_BYTES);
 #pragma unroll 4
-        for (int i = t; i < C::RAW_BYTES / 16; i += 128) {
+        for (int i = t; i < C::RAW_BYTES / 16; i += 32 * kEpiWarps) {
           const float4 x = raw[i];
           const float4 h = make_float4(tf32_hi(x.x), tf32_hi(x.y), tf32_hi(x.z), tf32_hi(x.w));
           raw[i] = h;
@@ -254,15 +255,16 @@ gemm_tc_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ 
         if (lane == 0) ptx::mbar_arrive(&conv[s]);
       }
     }
-    // ---- epilogue: TMEM lane quadrant = warp % 4
-    const int q = warp & 3;
-    float *buf = epibuf + q * 32 * 33;
+    // ---- epilogue: TMEM lane quadrant = warp % 4; the two warps of a quadrant split the
+    //      32-column chunks (even / odd)
+    const int q = warp & 3, half = (warp - 2) >> 2;
+    float *buf = epibuf + (warp - 2) * 32 * 33;
     ptx::mbar_wait(accum, 0);
     tc_fence_after();
     const int mrow0 = m0 + q * 32;
     const int64_t MN = (int64_t)g.M * g.N;
 #pragma unroll 1
-    for (int c = 0; c < BN / 32; ++c) {
+    for (int c = half; c < BN / 32; c += 2) {
       const int nc = n0 + c * 32;
       if (nc >= g.N) break;  // warp-uniform
       float v[32];
@@ -320,7 +322,7 @@ gemm_tc_persistent(const __grid_constant__ CUtensorMap tmA, const __grid_constan
   uint64_t *full = reinterpret_cast<uint64_t *>(smem + C::STAGES * C::STAGE_BYTES + kEpiBytes);
   uint64_t *empty = full + C::STAGES;
   uint64_t *tfull = empty + C::STAGES;   // [2] accumulator stage ready (tcgen05.commit)
-  uint64_t *tempty = tfull + 2;          // [2] accumulator stage drained (4 epilogue warps)
+  uint64_t *tempty = tfull + 2;          // [2] accumulator stage drained (kEpiWarps arrivals)
   uint32_t *tmem_slot = reinterpret_cast<uint32_t *>(tempty + 2);
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
@@ -334,7 +336,7 @@ gemm_tc_persistent(const __grid_constant__ CUtensorMap tmA, const __grid_constan
     }
     for (int s = 0; s < 2; ++s) {
       ptx::mbar_init(&tfull[s], 1);
-      ptx::mbar_init(&tempty[s], 4);
+      ptx::mbar_init(&tempty[s], kEpiWarps);
     }
     ptx::fence_mbar_init();
     ptx::prefetch_tensormap(&tmA);
@@ -401,9 +403,9 @@ gemm_tc_persistent(const __grid_constant__ CUtensorMap tmA, const __grid_constan
         mma_commit(&tfull[as]);
       }
     }
-  } else {  // ---- epilogue warps 2..5: TMEM lane quadrant = warp % 4
-    const int q = warp & 3;
-    float *buf = epibuf + q * 32 * 33;
+  } else {  // ---- epilogue warps: TMEM lane quadrant = warp % 4, even / odd 32-column chunks
+    const int q = warp & 3, half = (warp - 2) >> 2;
+    float *buf = epibuf + (warp - 2) * 32 * 33;
     int lt = 0;
     for (int tile = blockIdx.x; tile < ntiles; tile += gridDim.x, ++lt) {
       const int as = lt & 1;
@@ -412,7 +414,7 @@ gemm_tc_persistent(const __grid_constant__ CUtensorMap tmA, const __grid_constan
       tc_fence_after();
       const int mrow0 = m0 + q * 32;
 #pragma unroll 1
-      for (int c = 0; c < BN / 32; ++c) {
+      for (int c = half; c < BN / 32; c += 2) {
         const int nc = n0 + c * 32;
         if (nc >= N) break;  // warp-uniform
         float v[32];

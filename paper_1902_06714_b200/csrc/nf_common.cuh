@@ -11,22 +11,39 @@ namespace nf {
 
 enum Act : int { ACT_SIGMOID = 0, ACT_TANH = 1, ACT_RELU = 2, ACT_GAUSSIAN = 3, ACT_STEP = 4 };
 
-// a = sigma(z), s = sigma'(z).  Accurate libdevice expf/tanhf (no fast-math).
+// e^x for x <= 0 through the SFU: ex2.approx(x log2 e).  Relative error <= 2^-21 + |x| 2^-24
+// (the rounding of x log2 e), i.e. < 1e-6 for |x| < 16 -- far inside the 1e-4 parity bar, and
+// ~20 dependent instructions shorter than libdevice expf (the epilogues are latency-bound).
+__device__ __forceinline__ float exp_neg(float x) { return __expf(x); }
+
+// tanh |z| for |z| < 0.5: odd Taylor series to z^15 (truncation < 5e-8 relative).
+__device__ __forceinline__ float tanh_small(float z) {
+  const float q = z * z;
+  float p = 929569.0f / 638512875.0f;
+  p = fmaf(p, q, -21844.0f / 6081075.0f);
+  p = fmaf(p, q, 1382.0f / 155925.0f);
+  p = fmaf(p, q, -62.0f / 2835.0f);
+  p = fmaf(p, q, 17.0f / 315.0f);
+  p = fmaf(p, q, -2.0f / 15.0f);
+  p = fmaf(p, q, 1.0f / 3.0f);
+  return fmaf(-z * q, p, z);  // z - z^3 (1/3 - 2 z^2/15 + ...)
+}
+
+// a = sigma(z), s = sigma'(z), branch-free stable forms (no fast-math elsewhere).
 __device__ __forceinline__ void act_fwd(int kind, float z, float &a, float &s) {
   switch (kind) {
     case ACT_SIGMOID: {            // t = e^{-|z|}:  sigma = 1/(1+t) or t/(1+t);  sigma' = t/(1+t)^2
-      const float t = expf(-fabsf(z));
+      const float t = exp_neg(-fabsf(z));
       const float r = __frcp_rn(1.0f + t);  // == 1.0f / (1.0f + t), correctly rounded
       a = z >= 0.0f ? r : t * r;
       s = t * r * r;
       break;
     }
-    case ACT_TANH: {               // t = e^{-2|z|}, e = expm1(-2|z|) = t - 1 (both accurate):
-      const float t = expf(-2.0f * fabsf(z));    // tanh|z| = (1 - t)/(1 + t) = -e / (2 + e),
-      const float e = expm1f(-2.0f * fabsf(z));  // sigma' = sech^2 z = 4t/(1+t)^2; 1 + t and
-      const float r = __frcp_rn(1.0f + t);       // 2 + e carry no cancellation, and t keeps its
-      a = copysignf(-e * __frcp_rn(2.0f + e), z);  // own precision when sigma' is tiny (reading
-      s = 4.0f * t * r * r;                      // R6; a compact replacement of tanhf)
+    case ACT_TANH: {               // t = e^{-2|z|}: tanh|z| = (1 - t)/(1 + t) for |z| >= 1/2 (no
+      const float t = exp_neg(-2.0f * fabsf(z));  // cancellation there), series below;
+      const float r = __frcp_rn(1.0f + t);        // sigma' = sech^2 z = 4t/(1+t)^2 from t itself
+      a = fabsf(z) < 0.5f ? tanh_small(z) : copysignf((1.0f - t) * r, z);  // (exact when tiny)
+      s = 4.0f * t * r * r;
       break;
     }
     case ACT_RELU:                 // relu'(0) = 0 (reading R8)
@@ -34,7 +51,7 @@ __device__ __forceinline__ void act_fwd(int kind, float z, float &a, float &s) {
       s = z > 0.0f ? 1.0f : 0.0f;
       break;
     case ACT_GAUSSIAN: {           // e^{-z^2}, -2z e^{-z^2}
-      const float e = expf(-z * z);
+      const float e = exp_neg(-z * z);
       a = e;
       s = -2.0f * z * e;
       break;
@@ -57,20 +74,9 @@ __device__ __forceinline__ float act_only_t(float z) {
 }
 
 __device__ __forceinline__ float act_only(int kind, float z) {
-  switch (kind) {
-    case ACT_SIGMOID: {
-      const float t = expf(-fabsf(z));
-      const float r = __frcp_rn(1.0f + t);  // == 1.0f / (1.0f + t), correctly rounded
-      return z >= 0.0f ? r : t * r;
-    }
-    case ACT_TANH: {
-      const float e = expm1f(-2.0f * fabsf(z));
-      return copysignf(-e * __frcp_rn(2.0f + e), z);
-    }
-    case ACT_RELU: return z > 0.0f ? z : 0.0f;
-    case ACT_GAUSSIAN: return expf(-z * z);
-    default: return z > 0.0f ? 1.0f : 0.0f;
-  }
+  float a, s;
+  act_fwd(kind, z, a, s);
+  return a;
 }
 
 // Blackwell packed fp32 FMA (FFMA2): d.{x,y} = a * b.{x,y} + d.{x,y}, a broadcast.  Two
