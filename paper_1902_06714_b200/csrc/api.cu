@@ -108,6 +108,12 @@ struct nf_net {
   DevBuf stash;
   Workspace ws;
   DevBuf partial;
+  // backward: the weight-gradient GEMMs (K4 + bias) of layer l run on a side stream,
+  // concurrently with the delta GEMM (K3) of layer l-1 on the main stream
+  cudaStream_t side = nullptr;
+  std::vector<cudaEvent_t> ev;           // fork, per-layer K3-done, join
+  Workspace ws2;                         // the side stream's own split-K / column-sum scratch
+  DevBuf partial2;
   DevBuf red;                            // loss/acc partials + results
   DevBuf stage_x, stage_y, stage_o, stage_g;  // host-pointer staging
   DevBuf d_starts;
@@ -169,18 +175,42 @@ int forward(nf_net *net, const float *x, const float *y, int64_t n, int mode) {
 // backprop + batch sum + update.  With
 // grad != nullptr the summed tendencies are stored there instead (nf_grad).
 // Order per layer: the delta of layer l-1 (reads W_l) BEFORE W_l is updated.
+int ensure_side(nf_net *net) {
+  if (net->side) return NF_OK;
+  NF_CUDA(cudaStreamCreateWithFlags(&net->side, cudaStreamNonBlocking));
+  net->ev.assign(net->L + 2, nullptr);
+  for (auto &e : net->ev) NF_CUDA(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
+  NF_CUDA(net->partial2.ensure(size_t(16) << 20 << 2));
+  net->ws2.partial = net->partial2.as<float>();
+  net->ws2.partial_floats = size_t(16) << 20;
+  return NF_OK;
+}
+
+// backprop + batch sum + update.  With grad != nullptr the
+// summed tendencies are stored there instead (nf_grad).  Per layer l (L..1): K3(l) computes
+// delta_{l-1} from delta_l and W_l on the main stream; K4(l) (tendencies of W_l, b_l and the
+// update) runs on the side stream once K3(l) has read W_l, overlapping K3(l-1).
 int backward(nf_net *net, const float *x, int64_t n, float eta, float *grad) {
+  if (int rc = ensure_side(net)) return rc;
+  net->ws2.math = net->ws.math;
+  cudaStream_t main_st = net->stream, side = net->side;
+  NF_CUDA(cudaEventRecord(net->ev[0], main_st));  // fork (delta_L and the stash are ready)
+  NF_CUDA(cudaStreamWaitEvent(side, net->ev[0], 0));
   for (int l = net->L; l >= 1; --l) {
     const int nl = net->dims[l], nk = net->dims[l - 1];
     if (l > 1) {
       EpiBwd eb{net->S[l - 1], nk};
-      NF_CUDA(gemm_bwd(net->stream, (int)n, nk, nl, net->S[l], net->W(l), eb, net->ws));
+      NF_CUDA(gemm_bwd(main_st, (int)n, nk, nl, net->S[l], net->W(l), eb, net->ws));
     }
+    NF_CUDA(cudaEventRecord(net->ev[l], main_st));  // K3(l) done with W_l and delta_l is final
+    NF_CUDA(cudaStreamWaitEvent(side, net->ev[l], 0));
     const float *aprev = l > 1 ? net->A[l - 1] : x;
     EpiGrad eg = grad ? EpiGrad{grad + net->offW[l], grad + net->offB[l], nk, nk, 0.0f, 1}
                       : EpiGrad{net->W(l), net->b(l), nk, nk, (float)((double)eta / (double)n), 0};
-    NF_CUDA(gemm_grad(net->stream, nl, nk, (int)n, net->S[l], aprev, eg, net->ws));
+    NF_CUDA(gemm_grad(side, nl, nk, (int)n, net->S[l], aprev, eg, net->ws2));
   }
+  NF_CUDA(cudaEventRecord(net->ev[net->L + 1], side));  // join
+  NF_CUDA(cudaStreamWaitEvent(main_st, net->ev[net->L + 1], 0));
   return NF_OK;
 }
 
@@ -298,6 +328,9 @@ void nf_net_destroy(nf_net *net) {
   fused_small_release(net->fused);
   drop_graph(net);
   if (net->cap_stream) cudaStreamDestroy(net->cap_stream);
+  for (auto e : net->ev) if (e) cudaEventDestroy(e);
+  if (net->side) cudaStreamDestroy(net->side);
+  net->partial2.release();
   delete net;
 }
 
@@ -437,6 +470,7 @@ int nf_train_steps(nf_net *net, const float *X, const float *Y, int64_t N, int64
     // graph and replayed while the arguments repeat (removes the host launch gaps between the
     // ~10-50 kernels of each step).  Workspaces are sized before capture.
     if ((rc = ensure_ws(net, batch))) return rc;
+    if ((rc = ensure_side(net))) return rc;
     NF_CUDA(net->red.ensure(sizeof(double2) * loss_acc_parts() + 64));
     std::vector<int64_t> key = {(int64_t)(uintptr_t)dX, (int64_t)(uintptr_t)dY, N, batch, n_steps,
                                 (int64_t)(uintptr_t)step_loss, (int64_t)(uintptr_t)net->stream, net->math,
