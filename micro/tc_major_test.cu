@@ -127,12 +127,12 @@ void check(int M, int N, int K, int positive = 0, int reps = 0) {
   cudaFree(A); cudaFree(B); cudaFree(C); cudaFree(R);
 }
 
-template <class Epi>
+template <class Epi, int BNP = 256>
 void perf_pers(const char *name, int M, int N, int K, Epi epi, float *A, float *B) {
   CUtensorMap ta, tb;
-  map(&ta, A, M, K, false, tc::BM); map(&tb, B, N, K, false, 256);
-  using Cf = tc::Cfg<256, 1>;
-  auto kern = tc::gemm_tc_persistent<256, false, false, Epi>;
+  map(&ta, A, M, K, false, tc::BM); map(&tb, B, N, K, false, BNP);
+  using Cf = tc::Cfg<BNP, 1>;
+  auto kern = tc::gemm_tc_persistent<BNP, false, false, Epi>;
   CK(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, Cf::SMEM));
   kern<<<148, tc::kThreads, Cf::SMEM>>>(ta, tb, M, N, K, epi);
   CK(cudaDeviceSynchronize());
@@ -141,18 +141,19 @@ void perf_pers(const char *name, int M, int N, int K, Epi epi, float *A, float *
   for (int r = 0; r < 3; ++r) kern<<<148, tc::kThreads, Cf::SMEM>>>(ta, tb, M, N, K, epi);
   cudaEventRecord(e1); CK(cudaEventSynchronize(e1));
   float ms; cudaEventElapsedTime(&ms, e0, e1); ms /= 3;
-  printf("PERSISTENT %-10s M=%d N=%d K=%d: %.3f ms %.1f TFLOP/s\n", name, M, N, K, ms, 2.0 * M * N * K / ms / 1e9);
+  printf("PERSISTENT BN=%d %-10s M=%d N=%d K=%d: %.3f ms %.1f TFLOP/s\n", BNP, name, M, N, K, ms,
+         2.0 * M * N * K / ms / 1e9);
 }
 
-template <class Epi>
+template <class Epi, int BNT = 256>
 void perf_epi(const char *name, int M, int N, int K, Epi epi, float *A, float *B) {
   CUtensorMap ta, tb;
-  map(&ta, A, M, K, false, tc::BM); map(&tb, B, N, K, false, 256);
-  using Cf = tc::Cfg<256, 1>;
-  auto kern = tc::gemm_tc_kernel<256, false, false, 1, Epi>;
+  map(&ta, A, M, K, false, tc::BM); map(&tb, B, N, K, false, BNT);
+  using Cf = tc::Cfg<BNT, 1>;
+  auto kern = tc::gemm_tc_kernel<BNT, false, false, 1, Epi>;
   CK(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, Cf::SMEM));
   tc::TileArgs g{M, N, K, ((K + 31) / 32) * 32, nullptr};
-  dim3 grid((N + 255) / 256, (M + 127) / 128, 1);
+  dim3 grid((N + BNT - 1) / BNT, (M + 127) / 128, 1);
   kern<<<grid, tc::kThreads, Cf::SMEM>>>(ta, tb, g, epi);
   CK(cudaDeviceSynchronize());
   cudaEvent_t e0, e1; cudaEventCreate(&e0); cudaEventCreate(&e1);
@@ -173,6 +174,15 @@ int main(int argc, char **argv) {
     fill<<<256, 256>>>(bias, N, 3, 0);
     perf_epi("c3-store", M, N, K, EpiStore{C, N}, A, B);
     perf_epi("c3-tanh", M, N, K, nf::EpiFwd{bias, C, S, nullptr, N, nf::ACT_TANH, 0}, A, B);
+    perf_pers<EpiStore, 64>("c3-store", M, N, K, EpiStore{C, N}, A, B);
+    perf_pers<nf::EpiFwd, 64>("c3-tanh", M, N, K, nf::EpiFwd{bias, C, S, nullptr, N, nf::ACT_TANH, 0}, A, B);
+    perf_pers<EpiStore, 128>("c3-store", M, N, K, EpiStore{C, N}, A, B);
+    perf_pers<nf::EpiFwd, 128>("c3-tanh", M, N, K, nf::EpiFwd{bias, C, S, nullptr, N, nf::ACT_TANH, 0}, A, B);
+    perf_pers<nf::EpiFwd, 256>("c3-tanh", M, N, K, nf::EpiFwd{bias, C, S, nullptr, N, nf::ACT_TANH, 0}, A, B);
+    // config-4 layer shape
+    const int M4 = 2048, N4 = 256, K4 = 256;
+    perf_pers<nf::EpiFwd, 64>("c4-relu", M4, N4, K4, nf::EpiFwd{bias, C, S, nullptr, N4, nf::ACT_RELU, 0}, A, B);
+    perf_pers<nf::EpiFwd, 32>("c4-relu", M4, N4, K4, nf::EpiFwd{bias, C, S, nullptr, N4, nf::ACT_RELU, 0}, A, B);
     return 0;
   }
   if (argc > 1) goto perf;

@@ -77,3 +77,48 @@ def test_product_package_never_imports_oracle():
                 txt = open(os.path.join(dp, f)).read()
                 assert "oracle" not in re.sub(r"(#|//).*", "", txt).lower() or f == "__init__.py" and \
                     "import oracle" not in txt, f
+
+
+def test_null_net_is_rejected_by_every_entry_point(nf):
+    """Every call validates its handle before touching the device (no GPU needed)."""
+    lib = nf.lib()
+    null = None
+    f = np.zeros(4, np.float32)
+    p = f.ctypes.data_as(ctypes.c_void_p)
+    assert lib.nf_set_stream(null, None) == nf.NF_EINVAL
+    assert lib.nf_set_math(null, 0) == nf.NF_EINVAL
+    assert lib.nf_param_count(null) == -1
+    assert lib.nf_get_params(null, p, 4) == nf.NF_EINVAL
+    assert lib.nf_set_params(null, p, 4) == nf.NF_EINVAL
+    assert lib.nf_output(null, p, 1, p) == nf.NF_EINVAL
+    assert lib.nf_train_batch(null, p, p, 1, 1.0) == nf.NF_EINVAL
+    assert lib.nf_grad(null, p, p, 1, p) == nf.NF_EINVAL
+    v = ctypes.c_float()
+    assert lib.nf_loss(null, p, p, 1, ctypes.byref(v)) == nf.NF_EINVAL
+    assert lib.nf_accuracy(null, p, p, 1, ctypes.byref(v)) == nf.NF_EINVAL
+    st = np.zeros(1, np.int64)
+    assert lib.nf_train_steps(null, p, p, 4, 1, st.ctypes.data_as(ctypes.c_void_p), 1, 1.0, None) == nf.NF_EINVAL
+    lib.nf_net_destroy(null)                     # no-op
+    assert lib.nf_launch_count() >= 0
+    assert "null net" in nf.nf_last_error()
+
+
+def test_create_rejects_bad_specs_before_the_device(nf):
+    for dims, act in [([3, 5, 2], "relu,softmax"), ([3, 5, 2], "tanh,"), ([2, -1], "sigmoid"), ([], "sigmoid")]:
+        with pytest.raises(nf.NFError) as e:
+            nf.nf_net_create(dims, act)
+        assert e.value.code == nf.NF_EINVAL, (dims, act)
+    out = ctypes.c_void_p()
+    d = np.array([3, 5, 2], np.int32)
+    assert nf.lib().nf_net_create(d.ctypes.data_as(ctypes.c_void_p), 3, b"sigmoid", 0, None) == nf.NF_EINVAL
+
+
+def test_header_documents_every_entry_point():
+    """Each declaration in include/nf.h is preceded by a comment block (argument meaning,
+    layout, ownership, errors) -- the boundary contract."""
+    src = open(os.path.join(ROOT, "include", "nf.h")).read()
+    for name in _declared():
+        m = re.search(r"^[A-Za-z_][\w \*]*\b" + name + r"\(", src, flags=re.M)   # the declaration line
+        assert m, name
+        before = src[:m.start()].rstrip()
+        assert before.endswith("*/"), name
