@@ -142,6 +142,9 @@ def job_throughput(world, steps, batch, t_max):
 # Bounded CPU-oracle samples (about 5-20 s of single-core work each): (steps, rows per step).
 # The oracle's per-sample cost does not depend on the batch size (one fwd/bwd per sample, one
 # update per step), so a reduced batch is a fair sample of samples/s for the wide configs.
+# NF_MATH_FP64 is bound by the FP64 FMA units (SIMT DFMA): peak measured by micro/fma_rate.cu
+FP64_DFMA_TFLOPS = 1.0  # placeholder, set from the measurement
+FP64_PEAK_SOURCE = "micro/fma_rate.cu DFMA rate, 148 SMs (profiles/r01_micro_fma_rate.txt)"
 CPU_SAMPLE = {1: (20000, None), 2: (200, None), 3: (2, 256), 4: (4, 512), 5: (1, 32)}
 
 
@@ -210,8 +213,9 @@ def main():
     ap.add_argument("--min-seconds", type=float, default=1.0)
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
-    ap.add_argument("--math", default="fp32", choices=["fp32", "tf32"],
-                    help="fp32: fp32 SIMT / 3xTF32 tensor cores (1e-4 parity); tf32: 1xTF32 tiles")
+    ap.add_argument("--math", default="fp32", choices=["fp32", "tf32", "fp64"],
+                    help="fp32: fp32 SIMT / 3xTF32 tensor cores (1e-4 parity); tf32: 1xTF32 tiles; "
+                         "fp64: the paper's real64 build on the FP64 units")
     args = ap.parse_args()
     if args.warmup < 3:
         ap.error("--warmup must be >= 3")
@@ -233,8 +237,8 @@ def main():
     Xd, Yd = torch.from_numpy(X).cuda(), torch.from_numpy(Y).cuda()
     stream = torch.cuda.current_stream()
     net = nf.Net(cfg["dims"], cfg["act"], stream=stream)
-    net.set_math(nf.NF_MATH_TF32 if args.math == "tf32" else nf.NF_MATH_FP32)
     net.set_params(torch.from_numpy(synth.init_params(cid)).cuda())
+    net.set_math({"fp32": nf.NF_MATH_FP32, "tf32": nf.NF_MATH_TF32, "fp64": nf.NF_MATH_FP64}[args.math])
     loss = torch.zeros(K, device="cuda")
 
     # warm-up (W untimed steps)
@@ -272,11 +276,12 @@ def main():
         # TF32 dense peak = measured bf16 x (1.1 / 2.25), the guide's nominal ratio
         tf32_peak = peaks["bf16_tflops"] * 1.1 / 2.25
         ach_tf = flops_per_sample(cfg["dims"]) * K * B / t_med / 1e12
+    ach_f64 = flops_per_sample(cfg["dims"]) * K * B / t_med / 1e12
     # DRAM traffic of the dominant kernel from a committed `ncu --set full` capture
     # (profiles/traffic_c<id>.json: dram bytes read + written per SGD step), scaled to this launch
     traffic = None
     prof = os.path.join(ROOT, "profiles", f"traffic_c{cid}.json")
-    if os.path.exists(prof):
+    if os.path.exists(prof) and args.math != "fp64":
         try:
             traffic = json.load(open(prof))["bytes_per_step"] * K
         except Exception:
@@ -341,13 +346,18 @@ def main():
             "metric": "training samples/sec (fwd+bwd+SGD)",
             "value": value, "unit": "samples/s", "n_gpus": world, "steps": K, "warmup": W,
             "ms_per_step": t_max * 1e3 / K, "higher_is_better": True, "scaling": "weak",
-            "vs_baseline": None, "dtype": "f32" if args.math == "fp32" else "tf32", "data": "synthetic",
+            "vs_baseline": None, "dtype": {"fp32": "f32", "tf32": "tf32", "fp64": "f64"}[args.math], "data": "synthetic",
             "config": {"workload": cfg["name"], "dims": cfg["dims"], "batch": B, "dataset_rows": N,
                        "math": args.math,
                        "eta": cfg["eta"], "steps_per_timed_call": K, "reps": reps, "stat": "median rep",
                        "l2": f"dataset {X.nbytes / 1e6:.0f} MB > 126 MB L2, not flushed",
                        "parallelism": f"replicas x{world}" if world > 1 else "1 GPU"},
-            "roofline": ({"bound": "tensor", "achieved": ach_tf, "peak": tf32_peak, "unit": "TFLOP/s",
+            "roofline": ({"bound": "alu", "achieved": ach_f64, "peak": FP64_DFMA_TFLOPS, "unit": "TFLOP/s",
+                          "frac": ach_f64 / FP64_DFMA_TFLOPS, "traffic": None,
+                          "peak_source": FP64_PEAK_SOURCE, "kernel": "whole step (gemm64_kernel + splitk64)",
+                          "algorithmic_flops_per_step": flops_per_sample(cfg["dims"]) * B}
+                         if args.math == "fp64" else
+                         {"bound": "tensor", "achieved": ach_tf, "peak": tf32_peak, "unit": "TFLOP/s",
                           "frac": ach_tf / tf32_peak, "traffic": traffic,
                           "peak_source": f"MEASURED_PEAKS.json bf16_tflops x 1.1/2.25 = TF32 dense ({peak_src})",
                           "kernel": "whole step (gemm_tc_kernel + epilogue kernels)",

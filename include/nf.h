@@ -52,8 +52,16 @@ enum {
  *   NF_MATH_FP32 : fp32 storage, fp32 FMA accumulation (default; the paper's
  *                  real32).  Parity bar 1e-4 (BASELINE.json).
  *   NF_MATH_TF32 : TF32 tensor-core tiles, fp32 accumulate, where a kernel
- *                  has them (configs 3 and 5).  Parity bar 5e-3.           */
-enum { NF_MATH_FP32 = 0, NF_MATH_TF32 = 1 };
+ *                  has them (configs 3 and 5).  Parity bar 5e-3.
+ *   NF_MATH_FP64 : the paper's real64 build: parameters,
+ *                  activations, deltas and every sum in double on the FP64
+ *                  units.  Inputs, targets and results still cross this ABI
+ *                  as fp32 (widened exactly on entry, rounded once on exit);
+ *                  the parameters are held in double while the mode is set
+ *                  (nf_get_params rounds them, nf_set_params widens them) and
+ *                  rounded back to the fp32 arena when the mode is left.
+ *                  Parity bar 1e-10 against the fp64 oracle.              */
+enum { NF_MATH_FP32 = 0, NF_MATH_TF32 = 1, NF_MATH_FP64 = 2 };
 
 /* Constructor (network_constructor_listing).
  *   dims[0..n_dims-1] : neurons per layer incl. input and output;
@@ -81,7 +89,8 @@ void nf_net_destroy(nf_net *net);
  * which every later call of this net is ordered. */
 int nf_set_stream(nf_net *net, void *cuda_stream);
 
-/* NF_MATH_FP32 or NF_MATH_TF32 (see above). */
+/* NF_MATH_FP32, NF_MATH_TF32 or NF_MATH_FP64 (see above); anything else ->
+ * NF_EINVAL.  Ordered on the net's stream. */
 int nf_set_math(nf_net *net, int mode);
 
 /* Number of parameters: sum_l n_l*n_{l-1} + n_l ([3,5,2] -> 32). */

@@ -44,6 +44,21 @@ __global__ void ffma2_k(float *out, float a, float b, int iters) {
   out[blockIdx.x * blockDim.x + threadIdx.x] = s;
 }
 
+__global__ void dfma_k(double *out, double a, double b, int iters) {
+  double r[16];
+#pragma unroll
+  for (int i = 0; i < 16; ++i) r[i] = threadIdx.x * 0.001 + i;
+  double bb = b + threadIdx.x * 1e-7;
+  for (int it = 0; it < iters; ++it) {
+#pragma unroll
+    for (int i = 0; i < 16; ++i) r[i] = fma(r[i], a, bb);
+  }
+  double s = 0;
+#pragma unroll
+  for (int i = 0; i < 16; ++i) s += r[i];
+  out[blockIdx.x * blockDim.x + threadIdx.x] = s;
+}
+
 int main() {
   float *out;
   cudaMalloc(&out, 148 * 1024 * sizeof(float));
@@ -67,6 +82,24 @@ int main() {
       printf("%s warps/SM=%2d: %.1f TFLOP/s  %.1f FMA/clk/SM (at %d MHz)\n", k ? "FFMA2" : "FFMA ", warps,
              2 * fmas / ms / 1e9, fmas / (ms * 1e-3) / 148 / (khz * 1e3), khz / 1000);
     }
+  }
+  // FP64 (DFMA): the NF_MATH_FP64 path's ALU roofline
+  double *dout;
+  cudaMalloc(&dout, 148 * 1024 * sizeof(double));
+  for (int warps : {4, 8, 16, 32}) {
+    const int di = 2000;
+    cudaEvent_t e0, e1;
+    cudaEventCreate(&e0); cudaEventCreate(&e1);
+    dfma_k<<<148, warps * 32>>>(dout, 0.999, 0.001, di);
+    cudaEventRecord(e0);
+    dfma_k<<<148, warps * 32>>>(dout, 0.999, 0.001, di);
+    cudaEventRecord(e1);
+    cudaEventSynchronize(e1);
+    float ms; cudaEventElapsedTime(&ms, e0, e1);
+    const double fmas = 148.0 * warps * 32 * di * 16;
+    int khz; cudaDeviceGetAttribute(&khz, cudaDevAttrClockRate, 0);
+    printf("DFMA  warps/SM=%2d: %.2f TFLOP/s  %.2f FMA/clk/SM (at %d MHz)\n", warps, 2 * fmas / ms / 1e9,
+           fmas / (ms * 1e-3) / 148 / (khz * 1e3), khz / 1000);
   }
   return 0;
 }

@@ -165,6 +165,19 @@ void perf_epi(const char *name, int M, int N, int K, Epi epi, float *A, float *B
 }
 
 int main(int argc, char **argv) {
+  if (argc > 1 && argv[1][0] == 't') {  // config-3 layer with the tanh epilogue only (ncu)
+    const int M = 4096, N = 1024, K = 1024;
+    float *A, *B, *C, *S, *bias;
+    CK(cudaMalloc(&A, (size_t)M * K * 4)); CK(cudaMalloc(&B, (size_t)N * K * 4));
+    CK(cudaMalloc(&C, (size_t)M * N * 4)); CK(cudaMalloc(&S, (size_t)M * N * 4)); CK(cudaMalloc(&bias, N * 4));
+    fill<<<256, 256>>>(A, (int64_t)M * K, 1, 0); fill<<<256, 256>>>(B, (int64_t)N * K, 2, 0);
+    fill<<<256, 256>>>(bias, N, 3, 0);
+    perf_epi("c3-store", M, N, K, EpiStore{C, N}, A, B);
+    perf_epi("c3-tanh", M, N, K, nf::EpiFwd{bias, C, S, nullptr, N, nf::ACT_TANH, 0}, A, B);
+    perf_epi("c3-relu", M, N, K, nf::EpiFwd{bias, C, S, nullptr, N, nf::ACT_RELU, 0}, A, B);
+    perf_epi("c3-tinf", M, N, K, nf::EpiFwd{bias, C, S, nullptr, N, nf::ACT_TANH, 2}, A, B);
+    return 0;
+  }
   if (argc > 1 && argv[1][0] == 'c') {  // config-3 shape only (profiling)
     const int M = 4096, N = 1024, K = 1024;
     float *A, *B, *C, *S, *bias;

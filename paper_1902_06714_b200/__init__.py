@@ -24,7 +24,7 @@ _PKG = os.path.dirname(os.path.abspath(__file__))
 LIB_PATH = os.path.join(_PKG, "libnf_b200.so")
 
 NF_OK, NF_EINVAL, NF_ECUDA, NF_ENOMEM, NF_ENODEV = 0, -1, -2, -3, -4
-NF_MATH_FP32, NF_MATH_TF32 = 0, 1
+NF_MATH_FP32, NF_MATH_TF32, NF_MATH_FP64 = 0, 1, 2
 
 
 class NFError(RuntimeError):

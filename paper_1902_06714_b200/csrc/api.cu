@@ -11,6 +11,7 @@
 #include <vector>
 
 #include "../../include/nf.h"
+#include "fp64.cuh"
 #include "fused_small.cuh"
 #include "infer_small.cuh"
 #include "kernels.cuh"
@@ -126,7 +127,15 @@ struct nf_net {
   cudaStream_t cap_stream = nullptr;     // private stream the graph is captured on (the
                                          // caller's stream may be the legacy default stream)
 
+  // NF_MATH_FP64: double parameters (authoritative while the mode is set), stash and scratch
+  double *params64 = nullptr;
+  int64_t ws64_rows = 0;
+  std::vector<double *> A64, S64;
+  DevBuf stash64, partial64, grad64;
+
   float *W(int l) const { return params + offW[l]; }
+  double *W64(int l) const { return params64 + offW[l]; }
+  double *b64(int l) const { return params64 + offB[l]; }
   float *b(int l) const { return params + offB[l]; }
   int act(int l) const { return l < L ? act_h : act_o; }
 };
@@ -214,13 +223,75 @@ int backward(nf_net *net, const float *x, int64_t n, float eta, float *grad) {
   return NF_OK;
 }
 
+// ---- NF_MATH_FP64: the same steps in double (fp64.cu), all on the net's stream -------------
+constexpr size_t kPartial64 = size_t(8) << 20;  // split-K partials (doubles)
+
+int ensure_ws64(nf_net *net, int64_t rows) {
+  if (rows <= net->ws64_rows) return NF_OK;
+  int64_t per_row = 0;
+  for (int l = 1; l <= net->L; ++l) per_row += 2 * (int64_t)net->dims[l];
+  NF_CUDA(cudaStreamSynchronize(net->stream));
+  drop_graph(net);
+  NF_CUDA(net->stash64.ensure((size_t)(per_row * rows) * sizeof(double)));
+  double *p = net->stash64.as<double>();
+  net->A64.assign(net->L + 1, nullptr);
+  net->S64.assign(net->L + 1, nullptr);
+  for (int l = 1; l <= net->L; ++l) {
+    net->A64[l] = p; p += rows * net->dims[l];
+    net->S64[l] = p; p += rows * net->dims[l];
+  }
+  net->ws64_rows = rows;
+  return NF_OK;
+}
+
+int forward64(nf_net *net, const float *x, const float *y, int64_t n, int mode) {
+  for (int l = 1; l <= net->L; ++l) {
+    const int lm = (mode == 2) ? 2 : (l < net->L ? 0 : 1);
+    Epi64Fwd epi{net->b64(l), net->A64[l], net->S64[l], y, net->dims[l], net->act(l), lm};
+    NF_CUDA(gemm64_fwd(net->stream, (int)n, net->dims[l], net->dims[l - 1], l == 1 ? x : nullptr,
+                       l == 1 ? nullptr : net->A64[l - 1], net->W64(l), epi, net->partial64.as<double>(),
+                       kPartial64));
+  }
+  return NF_OK;
+}
+
+int backward64(nf_net *net, const float *x, int64_t n, double eta, double *grad) {
+  for (int l = net->L; l >= 1; --l) {
+    const int nl = net->dims[l], nk = net->dims[l - 1];
+    if (l > 1) {
+      Epi64Bwd eb{net->S64[l - 1], nk};
+      NF_CUDA(gemm64_bwd(net->stream, (int)n, nk, nl, net->S64[l], net->W64(l), eb, net->partial64.as<double>(),
+                         kPartial64));
+    }
+    Epi64Grad eg = grad ? Epi64Grad{grad + net->offW[l], grad + net->offB[l], nk, nk, 0.0, 1}
+                        : Epi64Grad{net->W64(l), net->b64(l), nk, nk, eta / (double)n, 0};
+    NF_CUDA(gemm64_grad(net->stream, nl, nk, (int)n, net->S64[l], l == 1 ? x : nullptr,
+                        l == 1 ? nullptr : net->A64[l - 1], eg, net->partial64.as<double>(), kPartial64));
+  }
+  return NF_OK;
+}
+
+size_t red_bytes() {
+  return sizeof(double2) * std::max<size_t>(loss_acc_parts(), loss_acc64_parts()) + 64;
+}
+
 int train_batch_dev(nf_net *net, const float *x, const float *y, int64_t n, float eta,
                     float *step_loss) {
   int rc;
+  if (net->math == NF_MATH_FP64) {
+    if ((rc = ensure_ws64(net, n))) return rc;
+    if ((rc = forward64(net, x, y, n, 0))) return rc;
+    if (step_loss) {
+      NF_CUDA(net->red.ensure(red_bytes()));
+      NF_CUDA(loss_acc64(net->stream, net->A64[net->L], y, n, net->dims[net->L], net->red.as<double2>(), nullptr,
+                         step_loss));
+    }
+    return backward64(net, x, n, (double)eta, nullptr);
+  }
   if ((rc = ensure_ws(net, n))) return rc;
   if ((rc = forward(net, x, y, n, 0))) return rc;
   if (step_loss) {
-    NF_CUDA(net->red.ensure(sizeof(double2) * loss_acc_parts() + 64));
+    NF_CUDA(net->red.ensure(red_bytes()));
     NF_CUDA(loss_acc(net->stream, net->A[net->L], y, n, net->dims[net->L], net->red.as<double2>(),
                      nullptr, step_loss));
   }
@@ -317,6 +388,10 @@ void nf_net_destroy(nf_net *net) {
   if (!net) return;
   cudaStreamSynchronize(net->stream);
   if (net->params) cudaFree(net->params);
+  if (net->params64) cudaFree(net->params64);
+  net->stash64.release();
+  net->partial64.release();
+  net->grad64.release();
   net->stash.release();
   net->partial.release();
   net->red.release();
@@ -342,7 +417,18 @@ int nf_set_stream(nf_net *net, void *s) {
 
 int nf_set_math(nf_net *net, int mode) {
   if (int rc = check_net(net)) return rc;
-  if (mode != NF_MATH_FP32 && mode != NF_MATH_TF32) return fail(NF_EINVAL, "unknown math mode %d", mode);
+  if (mode != NF_MATH_FP32 && mode != NF_MATH_TF32 && mode != NF_MATH_FP64)
+    return fail(NF_EINVAL, "unknown math mode %d", mode);
+  if (mode == NF_MATH_FP64 && net->math != NF_MATH_FP64) {
+    // enter: the double parameters start as the exact widening of the fp32 arena
+    if (!net->params64) NF_CUDA(cudaMalloc(&net->params64, net->nparams * sizeof(double)));
+    NF_CUDA(net->partial64.ensure(kPartial64 * sizeof(double)));
+    NF_CUDA(f64_widen(net->stream, net->params, net->params64, net->nparams));
+  } else if (mode != NF_MATH_FP64 && net->math == NF_MATH_FP64) {
+    // leave: round the double parameters back into the fp32 arena
+    NF_CUDA(f64_round(net->stream, net->params64, net->params, net->nparams));
+    fused_small_invalidate(net->fused);
+  }
   net->math = mode;
   net->ws.math = mode;
   return NF_OK;
@@ -355,6 +441,19 @@ int nf_get_params(nf_net *net, float *dst, int64_t count) {
   if (int rc = check_ptr(dst, "dst")) return rc;
   if (count != net->nparams) return fail(NF_EINVAL, "count %lld != %lld", (long long)count, (long long)net->nparams);
   const bool dev = is_device_ptr(dst);
+  if (net->math == NF_MATH_FP64) {
+    float *d = dst;
+    if (!dev) {
+      NF_CUDA(net->stage_g.ensure((size_t)count * sizeof(float)));
+      d = net->stage_g.as<float>();
+    }
+    NF_CUDA(f64_round(net->stream, net->params64, d, count));
+    if (!dev) {
+      NF_CUDA(cudaMemcpyAsync(dst, d, count * sizeof(float), cudaMemcpyDeviceToHost, net->stream));
+      NF_CUDA(cudaStreamSynchronize(net->stream));
+    }
+    return NF_OK;
+  }
   NF_CUDA(cudaMemcpyAsync(dst, net->params, count * sizeof(float),
                           dev ? cudaMemcpyDeviceToDevice : cudaMemcpyDeviceToHost, net->stream));
   if (!dev) NF_CUDA(cudaStreamSynchronize(net->stream));
@@ -368,6 +467,7 @@ int nf_set_params(nf_net *net, const float *src, int64_t count) {
   const bool dev = is_device_ptr(src);
   NF_CUDA(cudaMemcpyAsync(net->params, src, count * sizeof(float),
                           dev ? cudaMemcpyDeviceToDevice : cudaMemcpyHostToDevice, net->stream));
+  if (net->math == NF_MATH_FP64) NF_CUDA(f64_widen(net->stream, net->params, net->params64, count));
   if (!dev) NF_CUDA(cudaStreamSynchronize(net->stream));
   fused_small_invalidate(net->fused);
   return NF_OK;
@@ -389,7 +489,15 @@ int nf_output(nf_net *net, const float *x, int64_t n, float *out) {
     NF_CUDA(net->stage_o.ensure((size_t)n * nL * sizeof(float)));
     dout = net->stage_o.as<float>();
   }
-  if (infer_small_applicable(net->dims, dx) && getenv("NF_DISABLE_FUSED") == nullptr) {
+  if (net->math == NF_MATH_FP64) {
+    const int64_t chunk = std::min<int64_t>(n, kEvalChunk);
+    if ((rc = ensure_ws64(net, chunk))) return rc;
+    for (int64_t r = 0; r < n; r += chunk) {
+      const int64_t m = std::min(chunk, n - r);
+      if ((rc = forward64(net, dx + r * n0, nullptr, m, 2))) return rc;
+      NF_CUDA(f64_round(net->stream, net->A64[net->L], dout + r * nL, m * nL));
+    }
+  } else if (infer_small_applicable(net->dims, dx) && getenv("NF_DISABLE_FUSED") == nullptr) {
     NF_CUDA(infer_small(net->stream, net->dims, net->act_h, net->act_o, net->params, dx, n, dout));
   } else {
     const int64_t chunk = std::min<int64_t>(n, kEvalChunk);
@@ -463,18 +571,18 @@ int nf_train_steps(nf_net *net, const float *X, const float *Y, int64_t N, int64
     dN = n_steps * batch;
   }
 
-  int rc = fused_small_train_steps(net->fused, net->stream, net->dims, net->act_h, net->act_o,
+  int rc = net->math == NF_MATH_FP64 ? FUSED_NOT_APPLICABLE : fused_small_train_steps(net->fused, net->stream, net->dims, net->act_h, net->act_o,
                                    net->params, dX, dY, dN, batch, st.data(), n_steps, eta, step_loss);
   if (rc == FUSED_NOT_APPLICABLE) {
     // Generic nets: the per-step kernel sequence of all n_steps, captured once as a CUDA
     // graph and replayed while the arguments repeat (removes the host launch gaps between the
     // ~10-50 kernels of each step).  Workspaces are sized before capture.
-    if ((rc = ensure_ws(net, batch))) return rc;
+    if ((rc = net->math == NF_MATH_FP64 ? ensure_ws64(net, batch) : ensure_ws(net, batch))) return rc;
     if ((rc = ensure_side(net))) return rc;
-    NF_CUDA(net->red.ensure(sizeof(double2) * loss_acc_parts() + 64));
+    NF_CUDA(net->red.ensure(red_bytes()));
     std::vector<int64_t> key = {(int64_t)(uintptr_t)dX, (int64_t)(uintptr_t)dY, N, batch, n_steps,
                                 (int64_t)(uintptr_t)step_loss, (int64_t)(uintptr_t)net->stream, net->math,
-                                (int64_t)(uintptr_t)net->stash.p};
+                                (int64_t)(uintptr_t)net->stash.p, (int64_t)(uintptr_t)net->stash64.p};
     int32_t eb;
     memcpy(&eb, &eta, 4);
     key.push_back(eb);
@@ -541,9 +649,17 @@ int nf_grad(nf_net *net, const float *x, const float *y, int64_t n, float *grad)
     NF_CUDA(net->stage_g.ensure((size_t)net->nparams * sizeof(float)));
     dg = net->stage_g.as<float>();
   }
-  if ((rc = ensure_ws(net, n))) return rc;
-  if ((rc = forward(net, dx, dy, n, 0))) return rc;
-  if ((rc = backward(net, dx, n, 0.0f, dg))) return rc;
+  if (net->math == NF_MATH_FP64) {
+    NF_CUDA(net->grad64.ensure((size_t)net->nparams * sizeof(double)));
+    if ((rc = ensure_ws64(net, n))) return rc;
+    if ((rc = forward64(net, dx, dy, n, 0))) return rc;
+    if ((rc = backward64(net, dx, n, 0.0, net->grad64.as<double>()))) return rc;
+    NF_CUDA(f64_round(net->stream, net->grad64.as<double>(), dg, net->nparams));
+  } else {
+    if ((rc = ensure_ws(net, n))) return rc;
+    if ((rc = forward(net, dx, dy, n, 0))) return rc;
+    if ((rc = backward(net, dx, n, 0.0f, dg))) return rc;
+  }
   if (host_out) {
     NF_CUDA(cudaMemcpyAsync(grad, dg, (size_t)net->nparams * sizeof(float), cudaMemcpyDeviceToHost, net->stream));
     NF_CUDA(cudaStreamSynchronize(net->stream));
@@ -563,13 +679,20 @@ static int eval_loss_acc(nf_net *net, const float *x, const float *y, int64_t n,
   const float *dy = stage_in(net, y, (size_t)n * nL, net->stage_y, &rc);
   if (rc) return rc;
   const int64_t chunk = std::min<int64_t>(n, kEvalChunk);
-  if ((rc = ensure_ws(net, chunk))) return rc;
+  const bool f64 = net->math == NF_MATH_FP64;
+  if ((rc = f64 ? ensure_ws64(net, chunk) : ensure_ws(net, chunk))) return rc;
   const int64_t nchunks = (n + chunk - 1) / chunk;
-  NF_CUDA(net->red.ensure(sizeof(double2) * loss_acc_parts() + 64 + nchunks * 2 * sizeof(float)));
-  float *res = reinterpret_cast<float *>(net->red.as<char>() + sizeof(double2) * loss_acc_parts() + 64);
-  const bool fused = infer_small_applicable(net->dims, dx) && getenv("NF_DISABLE_FUSED") == nullptr;
+  NF_CUDA(net->red.ensure(red_bytes() + nchunks * 2 * sizeof(float)));
+  float *res = reinterpret_cast<float *>(net->red.as<char>() + red_bytes());
+  const bool fused = !f64 && infer_small_applicable(net->dims, dx) && getenv("NF_DISABLE_FUSED") == nullptr;
   for (int64_t c = 0; c < nchunks; ++c) {
     const int64_t r = c * chunk, m = std::min(chunk, n - r);
+    if (f64) {
+      if ((rc = forward64(net, dx + r * n0, nullptr, m, 2))) return rc;
+      NF_CUDA(loss_acc64(net->stream, net->A64[net->L], dy + r * nL, m, nL, net->red.as<double2>(), res + 2 * c,
+                         nullptr));
+      continue;
+    }
     if (fused) NF_CUDA(infer_small(net->stream, net->dims, net->act_h, net->act_o, net->params, dx + r * n0, m,
                                    net->A[net->L]));
     else if ((rc = forward(net, dx + r * n0, nullptr, m, 2))) return rc;

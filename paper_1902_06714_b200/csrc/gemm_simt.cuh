@@ -258,7 +258,13 @@ splitk_epilogue(const float *__restrict__ partial, int splits, int M, int N, Epi
   for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < MN;
        i += (int64_t)gridDim.x * blockDim.x) {
     float s = 0.0f;
-    for (int z = 0; z < splits; ++z) s += partial[z * MN + i];
+    int z = 0;
+    for (; z + 4 <= splits; z += 4) {  // four loads in flight, summed in order z = 0, 1, ...
+      const float v0 = partial[z * MN + i], v1 = partial[(z + 1) * MN + i];
+      const float v2 = partial[(z + 2) * MN + i], v3 = partial[(z + 3) * MN + i];
+      s += v0; s += v1; s += v2; s += v3;
+    }
+    for (; z < splits; ++z) s += partial[z * MN + i];
     epi((int)(i / N), (int)(i % N), s);
   }
 }

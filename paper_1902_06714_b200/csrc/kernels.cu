@@ -144,7 +144,7 @@ cudaError_t launch_tc(cudaStream_t st, int M, int N, int K, const TcOp &a, const
   const int nkb = (K + tc::BK - 1) / tc::BK;
   int splits = 1;
   if (2 * tiles < kSMs && nkb >= 16) {  // split-K only when under half a wave and K >= 512
-    splits = std::min((kSMs + tiles - 1) / tiles, nkb / 4);
+    splits = std::min(kSMs / tiles, nkb / 4);  // one wave
     while (splits > 1 && (size_t)splits * M * N > ws.partial_floats) --splits;
     splits = std::max(splits, 1);
   }
@@ -193,6 +193,13 @@ cudaError_t run_tc(cudaStream_t st, int M, int N, int K, const TcOp &a, const Tc
     if (N > 128 && tiles(256) > kSMs && getenv("NF_TC_NO_PERSISTENT") == nullptr)
       return launch_tc_persistent<AMN, BMN>(st, M, N, K, a, b, epi);
     if (N > 128 && tiles(256) >= fill) return launch_tc<256, AMN, BMN, 1>(st, M, N, K, a, b, epi, ws);
+    // under one wave of 128x256 tiles but deep (the c3 weight gradients, 1024 x 1024 x 4096):
+    // keep the wide tile and split K so that tiles x splits fills the GPU in one wave
+    {
+      const int nkb = (K + tc::BK - 1) / tc::BK;
+      const int sp = std::min(kSMs / tiles(256), nkb / 8);
+      if (N > 128 && sp >= 2 && tiles(256) * sp >= fill) return launch_tc<256, AMN, BMN, 1>(st, M, N, K, a, b, epi, ws);
+    }
     if (N > 64 && tiles(128) >= fill) return launch_tc<128, AMN, BMN, 1>(st, M, N, K, a, b, epi, ws);
     return launch_tc<64, AMN, BMN, 1>(st, M, N, K, a, b, epi, ws);
   }
@@ -212,11 +219,12 @@ colsum_partial(const float *__restrict__ D, int64_t rows, int cols, int chunk, f
   const int64_t r0 = (int64_t)blockIdx.y * chunk, r1 = min(rows, r0 + chunk);
   float s0 = 0.f, s1 = 0.f, s2 = 0.f, s3 = 0.f;
   int64_t r = r0;
-  for (; r + 4 <= r1; r += 4) {
-    s0 += D[r * cols + c];
-    s1 += D[(r + 1) * cols + c];
-    s2 += D[(r + 2) * cols + c];
-    s3 += D[(r + 3) * cols + c];
+  for (; r + 16 <= r1; r += 16) {  // 16 independent loads in flight per thread
+    float v[16];
+#pragma unroll
+    for (int u = 0; u < 16; ++u) v[u] = D[(r + u) * cols + c];
+#pragma unroll
+    for (int u = 0; u < 16; u += 4) { s0 += v[u]; s1 += v[u + 1]; s2 += v[u + 2]; s3 += v[u + 3]; }
   }
   for (; r < r1; ++r) s0 += D[r * cols + c];
   part[(int64_t)blockIdx.y * cols + c] = (s0 + s1) + (s2 + s3);
@@ -226,11 +234,24 @@ __global__ void __launch_bounds__(256)
 colsum_final(const float *__restrict__ part, int nchunks, int cols, EpiGrad epi) {
   ptx::pdl_trigger();
   ptx::pdl_wait();
-  const int c = blockIdx.x * 256 + threadIdx.x;
-  if (c >= cols) return;
+  // 32 columns per block; warp w sums the chunks z = w (mod 8), then warp 0 adds the eight
+  // warp sums in order w = 0..7 (fixed order: deterministic)
+  __shared__ float red[8][33];
+  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+  const int c = blockIdx.x * 32 + lane;
   float s = 0.f;
-  for (int z = 0; z < nchunks; ++z) s += part[(int64_t)z * cols + c];
-  epi(c, epi.nreal, s);  // column nreal of the [M][N+1] gradient = the bias
+  if (c < cols) {
+#pragma unroll 4
+    for (int z = w; z < nchunks; z += 8) s += part[(int64_t)z * cols + c];
+  }
+  red[w][lane] = s;
+  __syncthreads();
+  if (w == 0 && c < cols) {
+    float t = red[0][lane];
+#pragma unroll
+    for (int i = 1; i < 8; ++i) t += red[i][lane];
+    epi(c, epi.nreal, t);  // column nreal of the [M][N+1] gradient = the bias
+  }
 }
 
 cudaError_t bias_grad(cudaStream_t st, const float *D, int64_t rows, int cols, const EpiGrad &epi,
@@ -242,7 +263,7 @@ cudaError_t bias_grad(cudaStream_t st, const float *D, int64_t rows, int cols, c
   const dim3 grid((cols + 255) / 256, nchunks);
   cudaError_t e = launch_k(colsum_partial, grid, dim3(256), 0, st, D, rows, cols, chunk, part);
   if (e != cudaSuccess) return e;
-  return launch_k(colsum_final, dim3((cols + 255) / 256), dim3(256), 0, st, (const float *)part, nchunks, cols, epi);
+  return launch_k(colsum_final, dim3((cols + 31) / 32), dim3(256), 0, st, (const float *)part, nchunks, cols, epi);
 }
 
 // ---------------------------------------------------------------------------
@@ -251,13 +272,23 @@ cudaError_t bias_grad(cudaStream_t st, const float *D, int64_t rows, int cols, c
 
 // K1 with N <= 32: Z[m][o] = sum_k A[m][k] W[o][k] (+ bias/activation in epi).  One warp per
 // row; W [N][K] staged in shared memory; lane-strided K slices, butterfly reductions.
-template <int NMAX>
+template <int NMAX, bool STAGE>
 __global__ void __launch_bounds__(256)
 fwd_smalln(const float *__restrict__ A, const float *__restrict__ W, int M, int N, int K, EpiFwd epi) {
   ptx::pdl_trigger();
   ptx::pdl_wait();
   extern __shared__ float ws_[];
-  for (int i = threadIdx.x; i < N * K; i += blockDim.x) ws_[i] = W[i];
+  const float *wsrc = STAGE ? ws_ : W;   // !STAGE: W read through L1 (16-B aligned W only)
+  if (!STAGE) {
+  } else if ((reinterpret_cast<uintptr_t>(W) & 15) == 0) {  // N*K % 4 == 0 (K % 4 == 0): float4 staging,
+    const int nk4 = N * K / 4;                       // several loads in flight per thread
+#pragma unroll 4
+    for (int i = threadIdx.x; i < nk4; i += blockDim.x)
+      reinterpret_cast<float4 *>(ws_)[i] = __ldg(reinterpret_cast<const float4 *>(W) + i);
+  } else {
+#pragma unroll 8
+    for (int i = threadIdx.x; i < N * K; i += blockDim.x) ws_[i] = __ldg(W + i);
+  }
   __syncthreads();
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   for (int m = blockIdx.x * 8 + warp; m < M; m += gridDim.x * 8) {
@@ -271,7 +302,8 @@ fwd_smalln(const float *__restrict__ A, const float *__restrict__ W, int M, int 
 #pragma unroll
       for (int o = 0; o < NMAX; ++o) {
         if (o < N) {
-          const float4 wv = *reinterpret_cast<const float4 *>(ws_ + o * K + k);
+          const float4 wv = STAGE ? *reinterpret_cast<const float4 *>(wsrc + o * K + k)
+                                  : __ldg(reinterpret_cast<const float4 *>(wsrc + o * K + k));
           acc[o] = fmaf(av.x, wv.x, fmaf(av.y, wv.y, fmaf(av.z, wv.z, fmaf(av.w, wv.w, acc[o]))));
         }
       }
@@ -336,7 +368,7 @@ grad_smallm_partial(const float *__restrict__ D, const float *__restrict__ A, in
                     float *__restrict__ part) {
   ptx::pdl_trigger();
   ptx::pdl_wait();
-  __shared__ float dsm[128 * MMAX];
+  __shared__ __align__(16) float dsm[128 * MMAX];
   const int n = blockIdx.x * 128 + threadIdx.x;
   const int b0 = blockIdx.y * chunk, b1 = min(K, b0 + chunk);
   float acc[MMAX];
@@ -356,8 +388,15 @@ grad_smallm_partial(const float *__restrict__ D, const float *__restrict__ A, in
 #pragma unroll
         for (int u = 0; u < 8; ++u)
 #pragma unroll
-          for (int i = 0; i < MMAX; ++i)
-            if (i < M) acc[i] = fmaf(dsm[(r + u) * MMAX + i], a[u], acc[i]);
+          for (int i4 = 0; i4 < MMAX; i4 += 4) {
+            if (i4 < M) {  // one 16-B shared load per 4 outputs (broadcast)
+              const float4 d4 = *reinterpret_cast<const float4 *>(dsm + (r + u) * MMAX + i4);
+              acc[i4] = fmaf(d4.x, a[u], acc[i4]);
+              if (i4 + 1 < M) acc[i4 + 1] = fmaf(d4.y, a[u], acc[i4 + 1]);
+              if (i4 + 2 < M) acc[i4 + 2] = fmaf(d4.z, a[u], acc[i4 + 2]);
+              if (i4 + 3 < M) acc[i4 + 3] = fmaf(d4.w, a[u], acc[i4 + 3]);
+            }
+          }
       }
       for (; r < nb; ++r) {
         const float a = n < N ? __ldg(A + (int64_t)(bb + r) * N + n) : 1.0f;
@@ -380,17 +419,24 @@ __global__ void __launch_bounds__(256)
 grad_smallm_final(const float *__restrict__ part, int R, int M, int N, EpiGrad epi) {
   ptx::pdl_trigger();
   ptx::pdl_wait();
+  // 32 outputs per block; warp w sums the partials r = w (mod 8), warp 0 adds the eight warp
+  // sums in order (deterministic)
+  __shared__ float red[8][33];
   const int64_t MN = (int64_t)M * (N + 1);
-  for (int64_t t = blockIdx.x * 256 + threadIdx.x; t < MN; t += (int64_t)gridDim.x * 256) {
-    float s = 0.0f;
-    int r = 0;
-    for (; r + 4 <= R; r += 4) {
-      const float v0 = part[r * MN + t], v1 = part[(r + 1) * MN + t];
-      const float v2 = part[(r + 2) * MN + t], v3 = part[(r + 3) * MN + t];
-      s += v0; s += v1; s += v2; s += v3;
-    }
-    for (; r < R; ++r) s += part[r * MN + t];
-    epi((int)(t / (N + 1)), (int)(t % (N + 1)), s);
+  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+  const int64_t t = (int64_t)blockIdx.x * 32 + lane;
+  float s = 0.0f;
+  if (t < MN) {
+#pragma unroll 4
+    for (int r = w; r < R; r += 8) s += part[r * MN + t];
+  }
+  red[w][lane] = s;
+  __syncthreads();
+  if (w == 0 && t < MN) {
+    float u = red[0][lane];
+#pragma unroll
+    for (int i = 1; i < 8; ++i) u += red[i][lane];
+    epi((int)(t / (N + 1)), (int)(t % (N + 1)), u);
   }
 }
 
@@ -404,11 +450,15 @@ cudaError_t gemm_fwd(cudaStream_t st, int M, int N, int K, const float *A, const
   if (N <= 16 && K % 4 == 0 && (size_t)N * K * 4 <= 96 * 1024 && tc_ok(a) && tc_ok(b) && M >= 256) {
     static bool attr = false;
     if (!attr) {
-      cudaFuncSetAttribute(fwd_smalln<16>, cudaFuncAttributeMaxDynamicSharedMemorySize, 96 * 1024);
+      cudaFuncSetAttribute(fwd_smalln<16, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, 96 * 1024);
       attr = true;
     }
-    const int blocks = std::min((M + 7) / 8, 4 * kSMs);
-    return launch_k(fwd_smalln<16>, dim3(blocks), dim3(256), (size_t)N * K * 4, st, A, W, M, N, K, epi);
+    static const int per_sm = getenv("NF_SMALLN_PER_SM") ? atoi(getenv("NF_SMALLN_PER_SM")) : 2;
+    static const bool nostage = getenv("NF_SMALLN_NOSTAGE") != nullptr;
+    const int blocks = std::min((M + 7) / 8, per_sm * kSMs);  // W is staged once per block
+    if (nostage && (reinterpret_cast<uintptr_t>(W) & 15) == 0)
+      return launch_k(fwd_smalln<16, false>, dim3(blocks), dim3(256), 0, st, A, W, M, N, K, epi);
+    return launch_k(fwd_smalln<16, true>, dim3(blocks), dim3(256), (size_t)N * K * 4, st, A, W, M, N, K, epi);
   }
   GemmArgs g{M, N, K, A, K, W, K, N, 0, nullptr};
   return run_gemm<true, true>(st, g, epi, ws);
@@ -450,7 +500,7 @@ cudaError_t gemm_grad(cudaStream_t st, int M, int N, int K, const float *D, cons
                              ws.partial);
     if (e != cudaSuccess) return e;
     const int64_t MN = (int64_t)M * (N + 1);
-    return launch_k(grad_smallm_final, dim3((int)std::min<int64_t>((MN + 255) / 256, 2 * kSMs)), dim3(256), 0, st,
+    return launch_k(grad_smallm_final, dim3((int)((MN + 31) / 32)), dim3(256), 0, st,
                     (const float *)ws.partial, R, M, N, epi);
   }
   // C[M][N+1]: column N is the ones column -> bias gradient.

@@ -35,6 +35,8 @@ def t(fn, reps=20):
 
 
 print(f"config {cid} math {'tf32' if math else 'fp32'} B={B}")
-print(f"  nf_output      {t(lambda: net.output(Xd, out)):9.1f} us")
-print(f"  nf_grad        {t(lambda: net.grad(Xd, Yd, g)):9.1f} us")
+only_train = len(sys.argv) > 3 and sys.argv[3] == "train"   # (for ncu launch lists of one step)
+if not only_train:
+    print(f"  nf_output      {t(lambda: net.output(Xd, out)):9.1f} us")
+    print(f"  nf_grad        {t(lambda: net.grad(Xd, Yd, g)):9.1f} us")
 print(f"  nf_train_batch {t(lambda: net.train_batch(Xd, Yd, 0.01)):9.1f} us")
