@@ -14,6 +14,7 @@ using namespace nf;
 #define CK(x) do { cudaError_t e = (x); if (e != cudaSuccess) { printf("CUDA %s at %s:%d\n", cudaGetErrorString(e), __FILE__, __LINE__); exit(1);} } while (0)
 
 struct EpiStore {
+  static constexpr bool kRed = false;
   float *C; int N;
   __device__ float load(int, int) const { return 0.0f; }
   __device__ void store(int m, int n, float v, float) const { C[(int64_t)m * N + n] = v; }

@@ -37,6 +37,7 @@ struct GemmArgs {
 // training (A = sigma(z), S = (sigma(z) - y) sigma'(z) = delta_L, S:150 /
 // quadratic cost P:111); mode 2 inference (A = sigma(z) only).
 struct EpiFwd {
+  static constexpr bool kRed = false;
   const float *bias; float *A; float *S; const float *Y; int ld; int act; int mode;
   __device__ __forceinline__ float load(int m, int n) const {
     return mode == 1 ? Y[(int64_t)m * ld + n] : 0.0f;
@@ -115,6 +116,7 @@ __device__ __forceinline__ void strip_generic(const E &e, int m0, int mlim, int 
 
 // Backward: SD holds sigma'(Z_l) on entry and delta_l on exit.
 struct EpiBwd {
+  static constexpr bool kRed = false;
   float *SD; int ld;
   __device__ __forceinline__ float load(int m, int n) const { return SD[(int64_t)m * ld + n]; }
   __device__ __forceinline__ void store(int m, int n, float acc, float s) const {
@@ -129,11 +131,19 @@ struct EpiBwd {
 // Gradient: store = 0 applies W -= scale*G, b -= scale*g (scale =
 // eta/B, reading R3); store = 1 writes G, g (nf_grad).  Column n == nreal is the bias.
 struct EpiGrad {
+  static constexpr bool kRed = true;   // the update is additive: split-K terms can go straight in
   float *W; float *b; int ldw; int nreal; float scale; int store_only;
   __device__ __forceinline__ float *at(int m, int n) const { return n < nreal ? W + (int64_t)m * ldw + n : b + m; }
   __device__ __forceinline__ float load(int m, int n) const { return store_only ? 0.0f : *at(m, n); }
   __device__ __forceinline__ void store(int m, int n, float acc, float w) const {
     *at(m, n) = store_only ? acc : w - scale * acc;
+  }
+  // one split-K term of the update: W[m][n] += -scale * acc as an L2 reduction (red, no return)
+  __device__ __forceinline__ void strip_red(int m0, int mlim, int n, const float *v) const {
+    const int rows = min(32, mlim - m0);
+#pragma unroll 8
+    for (int r = 0; r < rows; ++r)
+      asm volatile("red.global.add.f32 [%0], %1;" ::"l"(at(m0 + r, n)), "f"(-scale * v[33 * r]) : "memory");
   }
   __device__ __forceinline__ void operator()(int m, int n, float acc) const { store(m, n, acc, load(m, n)); }
   __device__ __forceinline__ void strip(int m0, int mlim, int n, const float *v) const {

@@ -139,6 +139,8 @@ struct TileArgs {
   int M, N, K;
   int kchunk;          // K range per blockIdx.z (multiple of BK)
   float *partial;      // non-null: write raw partials [z][M][N] (split-K) instead of epi
+  int red;             // split-K with an additive epilogue (EpiGrad update): each split adds
+                       // its own term straight into the output (red.global.add), no partials
 };
 
 // ---- the kernel ------------------------------------------------------------------------
@@ -283,6 +285,13 @@ gemm_tc_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ 
       __syncwarp();
       const int n = nc + lane;
       const bool nok = n < g.N;
+      if constexpr (Epi::kRed) {
+        if (g.red) {
+          if (nok) epi.strip_red(mrow0, g.M, n, buf + lane);
+          __syncwarp();
+          continue;
+        }
+      }
       if (g.partial) {
 #pragma unroll 4
         for (int r = 0; r < 32; ++r) {

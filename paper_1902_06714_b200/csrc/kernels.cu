@@ -142,18 +142,27 @@ cudaError_t launch_tc(cudaStream_t st, int M, int N, int K, const TcOp &a, const
   const int tm = (M + tc::BM - 1) / tc::BM, tn = (N + BN - 1) / BN;
   const int tiles = tm * tn;
   const int nkb = (K + tc::BK - 1) / tc::BK;
+  // An additive epilogue (the SGD update W -= scale G) takes its split-K terms straight into W
+  // as L2 reductions (no partial buffer, no second kernel; summation order = arrival order,
+  // reading R12); NF_SPLITK_DETERMINISTIC=1 keeps the fixed-order partial path.
+  bool red = false;
+  if constexpr (Epi::kRed) {
+    static const bool det = getenv("NF_SPLITK_DETERMINISTIC") != nullptr;
+    red = !epi.store_only && !det;
+  }
   int splits = 1;
   if (2 * tiles < kSMs && nkb >= 16) {  // split-K only when under half a wave and K >= 512
     splits = std::min(kSMs / tiles, nkb / 4);  // one wave
-    while (splits > 1 && (size_t)splits * M * N > ws.partial_floats) --splits;
+    while (!red && splits > 1 && (size_t)splits * M * N > ws.partial_floats) --splits;
     splits = std::max(splits, 1);
   }
   const int kbper = (nkb + splits - 1) / splits;
   splits = (nkb + kbper - 1) / kbper;  // no empty K-chunk
-  tc::TileArgs g{M, N, K, kbper * tc::BK, splits > 1 ? ws.partial : nullptr};
+  red = red && splits > 1;
+  tc::TileArgs g{M, N, K, kbper * tc::BK, (splits > 1 && !red) ? ws.partial : nullptr, red ? 1 : 0};
   cudaError_t e = launch_k(kern, dim3(tn, tm, splits), dim3(tc::kThreads), C::SMEM, st, ta, tb, g, epi);
   if (e != cudaSuccess) return e;
-  if (splits > 1) {
+  if (splits > 1 && !red) {
     const int64_t MN = (int64_t)M * N;
     const int blocks = (int)std::min<int64_t>((MN + 255) / 256, 4 * kSMs);
     e = launch_k(splitk_epilogue<Epi>, dim3(blocks), dim3(256), 0, st, ws.partial, splits, M, N, epi);
