@@ -213,6 +213,10 @@ def main():
     ap.add_argument("--min-seconds", type=float, default=1.0)
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--dp", action="store_true",
+                    help="true data parallelism (P:505-556): every step, each rank's tendencies over its "
+                         "B rows of a world*B global batch, NCCL all-reduce (co_sum), nf_update; default: "
+                         "independent replicas (no collective)")
     ap.add_argument("--math", default="fp32", choices=["fp32", "tf32", "fp64"],
                     help="fp32: fp32 SIMT / 3xTF32 tensor cores (1e-4 parity); tf32: 1xTF32 tiles; "
                          "fp64: the paper's real64 build on the FP64 units")
@@ -233,16 +237,31 @@ def main():
     B, K, W = cfg["batch"], args.steps, args.warmup
     X, Y = synth.dataset(cid)
     N = len(X)
-    starts = synth.batch_starts(cid, steps=W + K, N=N)
+    # --dp: the global batch of a step is world * B rows, rank r owns the r-th block of B
+    starts = synth.batch_starts(cid, steps=W + K, N=N - ((world - 1) * B if args.dp else 0))
     Xd, Yd = torch.from_numpy(X).cuda(), torch.from_numpy(Y).cuda()
     stream = torch.cuda.current_stream()
     net = nf.Net(cfg["dims"], cfg["act"], stream=stream)
     net.set_params(torch.from_numpy(synth.init_params(cid)).cuda())
     net.set_math({"fp32": nf.NF_MATH_FP32, "tf32": nf.NF_MATH_TF32, "fp64": nf.NF_MATH_FP64}[args.math])
     loss = torch.zeros(K, device="cuda")
+    if args.dp:
+        from paper_1902_06714_b200.dp import DataParallel
+        if world == 1:   # a one-rank NCCL group, so the all-reduce runs at N = 1 too
+            import torch.distributed as dist
+            os.environ.setdefault("MASTER_ADDR", "127.0.0.1")
+            os.environ.setdefault("MASTER_PORT", "29533")
+            dist.init_process_group("nccl", rank=0, world_size=1)
+        dp = DataParallel(net)
+
+        def run_steps(st, step_loss=None, Xs=Xd, Ys=Yd):
+            dp.train_steps(Xs, Ys, world * B, st, cfg["eta"])
+    else:
+        def run_steps(st, step_loss=None, Xs=Xd, Ys=Yd):
+            net.train_steps(Xs, Ys, B, st, cfg["eta"], step_loss=step_loss)
 
     # warm-up (W untimed steps)
-    net.train_steps(Xd, Yd, B, starts[:W], cfg["eta"])
+    run_steps(starts[:W])
     torch.cuda.synchronize()
 
     def timed_rep():
@@ -250,7 +269,7 @@ def main():
         torch.cuda.synchronize()
         e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
         e0.record(stream)
-        net.train_steps(Xd, Yd, B, starts[W:], cfg["eta"], step_loss=loss)
+        run_steps(starts[W:], step_loss=loss)
         e1.record(stream)
         torch.cuda.synchronize()
         barrier(world)
@@ -309,7 +328,7 @@ def main():
     # ---- e2e: same metric through the C-ABI with pinned HOST buffers; each step's batch
     # is copied host->device inside the call, the step losses are read back to the host.
     e2e = None
-    if not args.no_e2e:
+    if not args.no_e2e and not args.dp:
         Xh = torch.from_numpy(X).pin_memory()
         Yh = torch.from_numpy(Y).pin_memory()
         lh = torch.empty(K, dtype=torch.float32).pin_memory()
@@ -351,7 +370,9 @@ def main():
                        "math": args.math,
                        "eta": cfg["eta"], "steps_per_timed_call": K, "reps": reps, "stat": "median rep",
                        "l2": f"dataset {X.nbytes / 1e6:.0f} MB > 126 MB L2, not flushed",
-                       "parallelism": f"replicas x{world}" if world > 1 else "1 GPU"},
+                       "parallelism": (f"dp{world}: per step nf_grad on {B} rows per rank, NCCL all-reduce "
+                                       f"of the tendencies (co_sum), nf_update; global batch {world * B}"
+                                       if args.dp else f"replicas x{world}" if world > 1 else "1 GPU")},
             "roofline": ({"bound": "alu", "achieved": ach_f64, "peak": FP64_DFMA_TFLOPS, "unit": "TFLOP/s",
                           "frac": ach_f64 / FP64_DFMA_TFLOPS, "traffic": None,
                           "peak_source": FP64_PEAK_SOURCE, "kernel": "whole step (gemm64_kernel + splitk64)",
@@ -376,7 +397,7 @@ def main():
             "clocks": clk.summary(),
         }
         print(json.dumps(line), flush=True)
-    if world > 1:
+    if world > 1 or args.dp:
         import torch.distributed as dist
         dist.destroy_process_group()
 

@@ -133,6 +133,16 @@ int nf_train_steps(nf_net *net, const float *X, const float *Y, int64_t N, int64
  * Parameters are unchanged.  (Extension, for gradient parity.)             */
 int nf_grad(nf_net *net, const float *x, const float *y, int64_t n, float *grad);
 
+/* The paper's `update`, applied to externally summed tendencies:
+ *   params -= (eta / n) * grad
+ * grad: count = nf_param_count floats in the flat parameter layout (host or device), e.g. the
+ * nf_grad tendencies of each rank's piece of a batch after the paper's co_sum over ranks
+ * (paper_1902_06714_b200.dp.DataParallel does that with an NCCL all-reduce);
+ * n = the rows of the WHOLE batch (n >= 1; the eta/B scale of reading R3).  In NF_MATH_FP64
+ * the update is applied to the double parameters.  Extension of the north-star list (the
+ * data-parallel step of SURVEY 8(e)).  Host grad: synchronous. */
+int nf_update(nf_net *net, const float *grad, int64_t count, float eta, int64_t n);
+
 /* Mean quadratic cost (1/n) sum_s 1/2 ||a_L(x_s) - y_s||^2 (reading R9)
  * written to *loss (host).  n = 0 -> 0.  Synchronises. */
 int nf_loss(nf_net *net, const float *x, const float *y, int64_t n, float *loss);

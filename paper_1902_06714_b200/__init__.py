@@ -51,6 +51,7 @@ def _load() -> ctypes.CDLL:
         "nf_train_batch": (ctypes.c_int, [P, P, P, I64, F]),
         "nf_train_steps": (ctypes.c_int, [P, P, P, I64, I64, P, I64, F, P]),
         "nf_grad": (ctypes.c_int, [P, P, P, I64, P]),
+        "nf_update": (ctypes.c_int, [P, P, I64, F, I64]),
         "nf_loss": (ctypes.c_int, [P, P, P, I64, ctypes.POINTER(F)]),
         "nf_accuracy": (ctypes.c_int, [P, P, P, I64, ctypes.POINTER(F)]),
         "nf_last_error": (ctypes.c_char_p, []),
@@ -77,7 +78,7 @@ def lib() -> ctypes.CDLL:
 # Every symbol include/nf.h declares (checked by tests/test_abi.py).
 EXPORTS = ("nf_net_create", "nf_net_destroy", "nf_set_stream", "nf_set_math", "nf_param_count",
            "nf_get_params", "nf_set_params", "nf_output", "nf_train_batch", "nf_train_steps",
-           "nf_grad", "nf_loss", "nf_accuracy", "nf_last_error", "nf_launch_count")
+           "nf_grad", "nf_update", "nf_loss", "nf_accuracy", "nf_last_error", "nf_launch_count")
 
 
 def _check(rc: int):
@@ -150,6 +151,10 @@ def nf_train_steps(net, X, Y, N: int, batch: int, starts, n_steps: int, eta: flo
 
 def nf_grad(net, x, y, n: int, grad):
     _check(lib().nf_grad(net, _ptr(x), _ptr(y), n, _ptr(grad)))
+
+
+def nf_update(net, grad, count: int, eta: float, n: int):
+    _check(lib().nf_update(net, _ptr(grad), count, eta, n))
 
 
 def nf_loss(net, x, y, n: int) -> float:
@@ -236,6 +241,10 @@ class Net:
             out = _empty_like_rows(x, self.n_params, None)
         nf_grad(self.h, x, y, x.shape[0], out)
         return out
+
+    def update(self, grad, eta: float, n: int):
+        """params -= (eta / n) grad: the paper's update on co_summed tendencies (nf_update)."""
+        nf_update(self.h, grad, self.n_params, eta, n)
 
     def loss(self, x, y) -> float:
         return nf_loss(self.h, x, y, x.shape[0])

@@ -667,6 +667,23 @@ int nf_grad(nf_net *net, const float *x, const float *y, int64_t n, float *grad)
   return NF_OK;
 }
 
+int nf_update(nf_net *net, const float *grad, int64_t count, float eta, int64_t n) {
+  if (int rc = check_net(net)) return rc;
+  if (int rc = check_ptr(grad, "grad")) return rc;
+  if (count != net->nparams) return fail(NF_EINVAL, "count %lld != %lld", (long long)count, (long long)net->nparams);
+  if (n <= 0) return fail(NF_EINVAL, "n must be >= 1");
+  if (!std::isfinite(eta)) return fail(NF_EINVAL, "eta is not finite");
+  int rc;
+  const float *dg = stage_in(net, grad, (size_t)count, net->stage_g, &rc);
+  if (rc) return rc;
+  const double scale = (double)eta / (double)n;
+  if (net->math == NF_MATH_FP64) NF_CUDA(f64_update(net->stream, net->params64, dg, count, scale));
+  else NF_CUDA(sgd_update(net->stream, net->params, dg, count, (float)scale));
+  fused_small_invalidate(net->fused);
+  if (dg != grad) NF_CUDA(cudaStreamSynchronize(net->stream));
+  return NF_OK;
+}
+
 static int eval_loss_acc(nf_net *net, const float *x, const float *y, int64_t n, float *res2) {
   res2[0] = res2[1] = 0.0f;
   if (n == 0) return NF_OK;

@@ -194,6 +194,10 @@ __global__ void convert_kernel_df(const double *__restrict__ s, float *__restric
   for (int64_t i = blockIdx.x * 256 + threadIdx.x; i < n; i += (int64_t)gridDim.x * 256) d[i] = (float)s[i];
 }
 
+__global__ void update_kernel64(double *__restrict__ p, const float *__restrict__ g, int64_t n, double scale) {
+  for (int64_t i = blockIdx.x * 256 + threadIdx.x; i < n; i += (int64_t)gridDim.x * 256) p[i] -= scale * (double)g[i];
+}
+
 __device__ __forceinline__ void argmax_merge64(double &v, int &i, double v2, int i2) {
   if (v2 > v || (v2 == v && i2 < i)) { v = v2; i = i2; }
 }
@@ -296,6 +300,13 @@ cudaError_t f64_widen(cudaStream_t st, const float *s, double *d, int64_t n) {
 }
 cudaError_t f64_round(cudaStream_t st, const double *s, float *d, int64_t n) {
   convert_kernel_df<<<(int)std::min<int64_t>((n + 255) / 256, 8 * kSMs), 256, 0, st>>>(s, d, n);
+  count_launch();
+  return cudaGetLastError();
+}
+
+cudaError_t f64_update(cudaStream_t st, double *p, const float *g, int64_t n, double scale) {
+  if (n <= 0) return cudaSuccess;
+  update_kernel64<<<(int)std::min<int64_t>((n + 255) / 256, 8 * kSMs), 256, 0, st>>>(p, g, n, scale);
   count_launch();
   return cudaGetLastError();
 }

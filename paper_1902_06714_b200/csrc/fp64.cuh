@@ -43,6 +43,8 @@ cudaError_t gemm64_grad(cudaStream_t st, int M, int N, int K, const double *D, c
                         const Epi64Grad &epi, double *partial, size_t partial_doubles);
 
 cudaError_t f64_widen(cudaStream_t st, const float *src, double *dst, int64_t n);   // exact
+// nf_update in double: p[i] -= scale * g[i] (g fp32, widened exactly)
+cudaError_t f64_update(cudaStream_t st, double *p, const float *g, int64_t n, double scale);
 cudaError_t f64_round(cudaStream_t st, const double *src, float *dst, int64_t n);   // round to nearest
 // loss = 1/n sum 1/2 |a - y|^2, accuracy = share of rows with argmax a == argmax y, both in
 // double; out[2] = {loss, acc} (fp32) and/or *step_loss = loss.  part: >= loss_acc64_parts()

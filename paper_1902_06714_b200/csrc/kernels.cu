@@ -449,7 +449,20 @@ grad_smallm_final(const float *__restrict__ part, int R, int M, int N, EpiGrad e
   }
 }
 
+__global__ void __launch_bounds__(256) sgd_update_kernel(float *__restrict__ p, const float *__restrict__ g, int64_t n,
+                                                         float scale) {
+  ptx::pdl_trigger();
+  ptx::pdl_wait();
+  for (int64_t i = blockIdx.x * 256 + threadIdx.x; i < n; i += (int64_t)gridDim.x * 256) p[i] = p[i] - scale * g[i];
+}
+
 }  // namespace
+
+cudaError_t sgd_update(cudaStream_t st, float *p, const float *g, int64_t n, float scale) {
+  if (n <= 0) return cudaSuccess;
+  const int blocks = (int)std::min<int64_t>((n + 255) / 256, 8 * kSMs);
+  return launch_k(sgd_update_kernel, dim3(blocks), dim3(256), 0, st, p, g, n, scale);
+}
 
 cudaError_t gemm_fwd(cudaStream_t st, int M, int N, int K, const float *A, const float *W,
                      const EpiFwd &epi, const Workspace &ws) {

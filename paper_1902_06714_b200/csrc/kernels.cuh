@@ -39,6 +39,9 @@ cudaError_t gemm_grad(cudaStream_t st, int M, int N, int K, const float *D, cons
 // mean loss, out[1] = accuracy (device floats); step_loss (nullable) gets the
 // mean loss too.
 int loss_acc_parts();
+
+// The paper's `update` on externally summed tendencies (nf_update): p[i] -= scale * g[i].
+cudaError_t sgd_update(cudaStream_t st, float *p, const float *g, int64_t n, float scale);
 cudaError_t loss_acc(cudaStream_t st, const float *A, const float *Y, int64_t n, int w,
                      double2 *part, float *out, float *step_loss);
 

@@ -52,3 +52,97 @@ def test_single_rank_is_identity():
     import bench
     assert bench.max_over_ranks(0.3, 1) == 0.3
     assert bench.job_throughput(1, 10, 8, 0.5) == pytest.approx(160.0)
+
+
+# ------------------------------------------------------------ data parallelism
+class OracleNet:
+    """CPU stand-in for nf.Net in the host-logic test of paper_1902_06714_b200.dp: the same
+    method surface (grad / update / get_params / set_params), the arithmetic from the oracle,
+    fp32 at the boundary like the C ABI."""
+
+    def __init__(self, dims, act, params):
+        import numpy as np
+        import oracle
+        self.o = oracle.Oracle(dims, act)
+        self.p = np.asarray(params, dtype=np.float64)
+        self.n_params = self.o.n_params
+
+    def get_params(self, out):
+        import torch
+        out.copy_(torch.from_numpy(self.p.astype("float32")))
+
+    def set_params(self, p):
+        self.p = p.numpy().astype("float64")
+
+    def grad(self, x, y, out):
+        import torch
+        out.copy_(torch.from_numpy(self.o.grad(self.p, x.numpy(), y.numpy()).astype("float32")))
+
+    def update(self, g, eta, n):
+        import numpy as np
+        self.p = self.p - (float(np.float32(eta)) / n) * g.numpy().astype(np.float64)
+
+
+def _dp_worker(rank, world, port, q):
+    import sys
+    sys.path.insert(0, ROOT)
+    import numpy as np
+    import torch
+    import torch.distributed as dist
+    import synth
+    from paper_1902_06714_b200.dp import DataParallel
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    dims, act = [13, 9, 4], "tanh,sigmoid"
+    p0 = synth.random_params(7, dims, 0.5).astype(np.float32).astype(np.float64)
+    # only rank 0's initial parameters count: the co_broadcast must overwrite the others
+    net = OracleNet(dims, act, p0 if rank == 0 else p0 + 1.0)
+    dp = DataParallel(net, device="cpu")
+    X, Y = synth.random_batch(8, 40, dims[0], dims[-1], "uniform")
+    dp.train_steps(torch.from_numpy(X), torch.from_numpy(Y), 11, [0, 29, 5, 17], 0.8)
+    dp.train_batch(torch.from_numpy(X[:1]), torch.from_numpy(Y[:1]), 0.8)   # 1 row < 2 ranks
+    q.put((rank, net.p))
+    dist.destroy_process_group()
+
+
+def test_data_parallel_co_sum_equals_serial_gloo():
+    """World size 2 (gloo): co_broadcast, per-rank tendencies of each rank's rows, co_sum,
+    identical update on every rank == the serial oracle on the whole batch."""
+    import sys
+    sys.path.insert(0, ROOT)
+    import numpy as np
+    import oracle
+    import synth
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    procs = [ctx.Process(target=_dp_worker, args=(r, 2, port, q)) for r in range(2)]
+    for p in procs:
+        p.start()
+    res = dict(q.get(timeout=180) for _ in procs)
+    for p in procs:
+        p.join(timeout=60)
+        assert p.exitcode == 0
+    dims, act = [13, 9, 4], "tanh,sigmoid"
+    p0 = synth.random_params(7, dims, 0.5).astype(np.float32).astype(np.float64)
+    X, Y = synth.random_batch(8, 40, dims[0], dims[-1], "uniform")
+    o = oracle.Oracle(dims, act)
+    eta = float(np.float32(0.8))
+    ref, _ = o.train_steps(p0, X, Y, 11, [0, 29, 5, 17], eta)
+    ref, _ = o.train_batch(ref, X[:1], Y[:1], eta)
+    assert np.array_equal(res[0], res[1])                       # every rank holds the same net
+    scale = np.maximum(np.abs(ref), 0.1 * np.abs(ref).max())
+    assert np.max(np.abs(res[0] - ref) / scale) <= 1e-6         # fp32 tendencies at the boundary
+
+
+def test_shard_partitions_rows():
+    import sys
+    sys.path.insert(0, ROOT)
+    from paper_1902_06714_b200.dp import shard
+    for n in (1, 2, 7, 1000, 1001):
+        for world in (1, 2, 3, 8):
+            parts = [shard(n, world, r) for r in range(world)]
+            assert parts[0][0] == 0 and parts[-1][1] == n
+            assert all(parts[i][1] == parts[i + 1][0] for i in range(world - 1))
+            sizes = [hi - lo for lo, hi in parts]
+            assert max(sizes) - min(sizes) <= 1
