@@ -202,7 +202,15 @@ int ensure_side(nf_net *net) {
 int backward(nf_net *net, const float *x, int64_t n, float eta, float *grad) {
   if (int rc = ensure_side(net)) return rc;
   net->ws2.math = net->ws.math;
-  cudaStream_t main_st = net->stream, side = net->side;
+  // The overlap only pays while the GEMMs are under one wave of 128x256 tiles (c3, c4): a
+  // GEMM that fills the GPU (c5: 2048 tiles, the persistent kernel) would just contend for
+  // the SMs with the other stream's GEMM, so those nets keep both on the main stream.
+  int64_t max_tiles = 0;
+  for (int l = 1; l <= net->L; ++l)
+    max_tiles = std::max<int64_t>(max_tiles, ((n + 127) / 128) * ((net->dims[l - 1] + 255) / 256));
+  static const bool force_overlap = getenv("NF_BWD_OVERLAP") != nullptr;
+  const bool overlap = force_overlap || max_tiles <= 148;
+  cudaStream_t main_st = net->stream, side = overlap ? net->side : net->stream;
   NF_CUDA(cudaEventRecord(net->ev[0], main_st));  // fork (delta_L and the stash are ready)
   NF_CUDA(cudaStreamWaitEvent(side, net->ev[0], 0));
   for (int l = net->L; l >= 1; --l) {
