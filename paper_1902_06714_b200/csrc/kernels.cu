@@ -220,7 +220,8 @@ cudaError_t run_tc(cudaStream_t st, int M, int N, int K, const TcOp &a, const Tc
 // Bias tendency g[i] = sum_r D[r][i] over n rows (the ones-column of the SIMT path),
 // row chunks summed in a fixed order, then the same EpiGrad bias element update.
 __global__ void __launch_bounds__(256)
-colsum_partial(const float *__restrict__ D, int64_t rows, int cols, int chunk, float *__restrict__ part) {
+colsum_partial(const float *__restrict__ D, int64_t rows, int cols, int chunk, float *__restrict__ part,
+               float *__restrict__ bias, float scale) {
   ptx::pdl_trigger();
   ptx::pdl_wait();
   const int c = blockIdx.x * 256 + threadIdx.x;
@@ -236,7 +237,11 @@ colsum_partial(const float *__restrict__ D, int64_t rows, int cols, int chunk, f
     for (int u = 0; u < 16; u += 4) { s0 += v[u]; s1 += v[u + 1]; s2 += v[u + 2]; s3 += v[u + 3]; }
   }
   for (; r < r1; ++r) s0 += D[r * cols + c];
-  part[(int64_t)blockIdx.y * cols + c] = (s0 + s1) + (s2 + s3);
+  const float s = (s0 + s1) + (s2 + s3);
+  if (bias)  // the update is additive: this chunk's term goes straight into b (L2 reduction, R12)
+    asm volatile("red.global.add.f32 [%0], %1;" ::"l"(bias + c), "f"(-scale * s) : "memory");
+  else
+    part[(int64_t)blockIdx.y * cols + c] = s;
 }
 
 __global__ void __launch_bounds__(256)
@@ -270,7 +275,12 @@ cudaError_t bias_grad(cudaStream_t st, const float *D, int64_t rows, int cols, c
   while (nchunks > 1 && (size_t)nchunks * cols > part_floats) --nchunks;
   const int chunk = (int)((rows + nchunks - 1) / nchunks);
   const dim3 grid((cols + 255) / 256, nchunks);
-  cudaError_t e = launch_k(colsum_partial, grid, dim3(256), 0, st, D, rows, cols, chunk, part);
+  static const bool det = getenv("NF_SPLITK_DETERMINISTIC") != nullptr;
+  if (!epi.store_only && !det)  // SGD update: one kernel, chunk sums reduced into b in L2
+    return launch_k(colsum_partial, grid, dim3(256), 0, st, D, rows, cols, chunk, (float *)nullptr, epi.b,
+                    epi.scale);
+  cudaError_t e = launch_k(colsum_partial, grid, dim3(256), 0, st, D, rows, cols, chunk, part, (float *)nullptr,
+                           0.0f);
   if (e != cudaSuccess) return e;
   return launch_k(colsum_final, dim3((cols + 31) / 32), dim3(256), 0, st, (const float *)part, nchunks, cols, epi);
 }

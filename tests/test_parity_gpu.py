@@ -328,12 +328,14 @@ def test_generic_train_steps_graph_equals_train_batch_loop():
     a.train_steps(dev(X), dev(Y), B, starts, 0.5)            # capture + launch
     for s in starts:
         b.train_batch(dev(X[s:s + B]), dev(Y[s:s + B]), 0.5)
-    assert np.array_equal(gpu_params(a), gpu_params(b))
+    # same kernels; only the arrival order of the L2 reductions of the bias tendencies may
+    # differ between two runs (reading R12): equal to within fp32 rounding, 10x inside the bar
+    assert rel_err(gpu_params(a), gpu_params(b)) <= 1e-5
     n0 = nf.nf_launch_count()
     a.set_params(dev(p))
     a.train_steps(dev(X), dev(Y), B, starts, 0.5)            # replay (same arguments)
     assert nf.nf_launch_count() > n0                          # replays count their kernels
-    assert np.array_equal(gpu_params(a), gpu_params(b))
+    assert rel_err(gpu_params(a), gpu_params(b)) <= 1e-5
     o = oracle.Oracle(dims, act)
     ref, _ = o.train_steps(p, X, Y, B, starts, 0.5)
     assert rel_err(gpu_params(a), ref) <= FP32_BAR
