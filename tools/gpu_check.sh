@@ -19,5 +19,8 @@ done; done
 timeout 600 python bench.py --impl reference --steps 20 --warmup 3 > $out/bench_ref.json 2> $out/bench_ref.err; echo "ref rc=$?"
 timeout 900 ncu --metrics gpu__time_duration.sum --clock-control none -c 400 --csv --log-file $out/launches.csv \
   python bench.py --steps 500 --warmup 3 --no-cpu-baseline --no-e2e --min-seconds 0 > $out/ncu_launch.log 2>&1; echo "ncu launches rc=$?"
+# one ncu tool per gpurun call: the full capture runs separately (NCU_FULL=1 or tools/ncu_full.sh)
+if [ "${NCU_FULL:-0}" = 1 ]; then
 timeout 900 ncu --set full --clock-control none --import-source on -k regex:fused -s 1 -c 1 -o $out/prof_fused \
   python bench.py --steps 50 --warmup 3 --no-cpu-baseline --no-e2e --min-seconds 0 > $out/ncu_full.log 2>&1; echo "ncu full rc=$?"
+fi
