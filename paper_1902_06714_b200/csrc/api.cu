@@ -116,6 +116,8 @@ struct nf_net {
   Workspace ws2;                         // the side stream's own split-K / column-sum scratch
   DevBuf partial2;
   DevBuf red;                            // loss/acc partials + results
+  DevBuf part_out;                       // partial tendencies of the fused narrow output layer
+  bool out_fused = false;                // forward fused K1/K2(L) + K3(L-1): backward skips them
   DevBuf stage_x, stage_y, stage_o, stage_g;  // host-pointer staging
   DevBuf d_starts;
   FusedSmall fused;                      // persistent small-net kernel state
@@ -157,6 +159,9 @@ int ensure_ws(nf_net *net, int64_t rows) {
   NF_CUDA(cudaStreamSynchronize(net->stream));
   drop_graph(net);
   NF_CUDA(net->stash.ensure((size_t)(per_row * rows) * sizeof(float)));
+  if (net->L >= 2)
+    NF_CUDA(net->part_out.ensure((size_t)out_layer_blocks((int)rows) * net->dims[net->L] *
+                                 (net->dims[net->L - 1] + 1) * sizeof(float)));
   float *p = net->stash.as<float>();
   net->A.assign(net->L + 1, nullptr);
   net->S.assign(net->L + 1, nullptr);
@@ -172,7 +177,16 @@ int ensure_ws(nf_net *net, int64_t rows) {
 // S = delta_L), 2 inference (A only).  y only for mode 0.
 int forward(nf_net *net, const float *x, const float *y, int64_t n, int mode) {
   const float *in = x;
+  const int L = net->L;
+  net->out_fused = mode == 0 && L >= 2 &&
+                   out_layer_fusable((int)n, net->dims[L - 1], net->dims[L], net->A[L - 1], net->S[L - 1], net->W(L));
   for (int l = 1; l <= net->L; ++l) {
+    if (l == L && net->out_fused) {  // K1+K2 of the output layer, K3 of layer L-1, K4(L) partials
+      NF_CUDA(out_layer_train_fused(net->stream, (int)n, net->dims[L - 1], net->dims[L], net->A[L - 1],
+                                    net->S[L - 1], net->W(L), net->b(L), y, net->A[L], net->S[L], net->act_o,
+                                    net->part_out.as<float>()));
+      break;
+    }
     const int lm = (mode == 2) ? 2 : (l < net->L ? 0 : 1);
     EpiFwd epi{net->b(l), net->A[l], net->S[l], y, net->dims[l], net->act(l), lm};
     NF_CUDA(gemm_fwd(net->stream, (int)n, net->dims[l], net->dims[l - 1], in, net->W(l), epi, net->ws));
@@ -215,7 +229,8 @@ int backward(nf_net *net, const float *x, int64_t n, float eta, float *grad) {
   NF_CUDA(cudaStreamWaitEvent(side, net->ev[0], 0));
   for (int l = net->L; l >= 1; --l) {
     const int nl = net->dims[l], nk = net->dims[l - 1];
-    if (l > 1) {
+    const bool fused = l == net->L && net->out_fused;  // K3(L) ran inside the forward kernel
+    if (l > 1 && !fused) {
       EpiBwd eb{net->S[l - 1], nk};
       NF_CUDA(gemm_bwd(main_st, (int)n, nk, nl, net->S[l], net->W(l), eb, net->ws));
     }
@@ -224,7 +239,8 @@ int backward(nf_net *net, const float *x, int64_t n, float eta, float *grad) {
     const float *aprev = l > 1 ? net->A[l - 1] : x;
     EpiGrad eg = grad ? EpiGrad{grad + net->offW[l], grad + net->offB[l], nk, nk, 0.0f, 1}
                       : EpiGrad{net->W(l), net->b(l), nk, nk, (float)((double)eta / (double)n), 0};
-    NF_CUDA(gemm_grad(side, nl, nk, (int)n, net->S[l], aprev, eg, net->ws2));
+    if (fused) NF_CUDA(out_layer_grad_final(side, (int)n, nk, nl, net->part_out.as<float>(), eg));
+    else NF_CUDA(gemm_grad(side, nl, nk, (int)n, net->S[l], aprev, eg, net->ws2));
   }
   NF_CUDA(cudaEventRecord(net->ev[net->L + 1], side));  // join
   NF_CUDA(cudaStreamWaitEvent(main_st, net->ev[net->L + 1], 0));
@@ -403,6 +419,7 @@ void nf_net_destroy(nf_net *net) {
   net->stash.release();
   net->partial.release();
   net->red.release();
+  net->part_out.release();
   net->stage_x.release();
   net->stage_y.release();
   net->stage_o.release();

@@ -459,6 +459,121 @@ grad_smallm_final(const float *__restrict__ part, int R, int M, int N, EpiGrad e
   }
 }
 
+// The narrow output layer of a training step (n_L <= 16 after a wide hidden layer: the 10-wide
+// last layer of configs 3 and 4) in ONE pass over its wide operands, instead of fwd_smalln +
+// bwd_smallk + grad_smallm_partial:
+//   K1+K2 (layer L):  z = A_{L-1} W_L^T + b_L, a = sigma(z), delta_L = (a - y) sigma'(z)
+//                      (S:150), a and delta_L stashed for the loss and nf_grad;
+//   K3 (layer L-1):   delta_{L-1} = (delta_L W_L) .* sigma'(Z_{L-1}), in place of S_{L-1}
+//                      (P:409-411), reading W_L before it is updated;
+//   K4 partials:       G_L = delta_L^T [A_{L-1} | 1] over the block's rows -> part[blk][o][0..H]
+//                      (the layout grad_smallm_final sums in fixed order, then updates W_L, b_L).
+// Phase 1: one warp per row, the A row in registers (HMAX4 float4 slots per lane), W_L staged
+// in shared memory.  Phase 2: thread per 4 columns over the block's rows (A re-read from L2).
+template <int NMAX, int HMAX4>
+__global__ void __launch_bounds__(256)
+out_layer_train(const float *__restrict__ A, float *__restrict__ S, const float *__restrict__ W,
+                const float *__restrict__ bias, const float *__restrict__ Y, float *__restrict__ AL,
+                float *__restrict__ DL, int n, int H, int nL, int act, int rows_per_block, float *__restrict__ part) {
+  ptx::pdl_trigger();
+  ptx::pdl_wait();
+  extern __shared__ float4 sm4_[];
+  float *ws_ = reinterpret_cast<float *>(sm4_);          // [nL][H]
+  float *dsm = ws_ + nL * H;                             // [rows_per_block][NMAX] delta_L
+  {
+    const int nk4 = nL * H / 4;
+#pragma unroll 4
+    for (int i = threadIdx.x; i < nk4; i += blockDim.x) sm4_[i] = __ldg(reinterpret_cast<const float4 *>(W) + i);
+  }
+  __syncthreads();
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const int r0 = blockIdx.x * rows_per_block, r1 = min(n, r0 + rows_per_block);
+  const int H4 = H / 4;
+  for (int m = r0 + warp; m < r1; m += 8) {
+    float4 av[HMAX4];
+    const float4 *arow = reinterpret_cast<const float4 *>(A + (int64_t)m * H);
+#pragma unroll
+    for (int i = 0; i < HMAX4; ++i)
+      if (lane + 32 * i < H4) av[i] = __ldg(arow + lane + 32 * i);
+    float acc[NMAX];
+#pragma unroll
+    for (int o = 0; o < NMAX; ++o) {
+      acc[o] = 0.0f;
+      if (o < nL) {
+#pragma unroll
+        for (int i = 0; i < HMAX4; ++i) {
+          if (lane + 32 * i < H4) {
+            const float4 w = reinterpret_cast<const float4 *>(ws_ + o * H)[lane + 32 * i];
+            acc[o] = fmaf(av[i].x, w.x, fmaf(av[i].y, w.y, fmaf(av[i].z, w.z, fmaf(av[i].w, w.w, acc[o]))));
+          }
+        }
+        acc[o] = warp_sum(acc[o]);
+      }
+    }
+    float dl = 0.0f;  // lane o < nL: delta_L[m][o]
+#pragma unroll
+    for (int o = 0; o < NMAX; ++o)
+      if (o == lane && o < nL) {
+        float a, sg;
+        act_fwd(act, acc[o] + bias[o], a, sg);
+        dl = (a - Y[(int64_t)m * nL + o]) * sg;
+        AL[(int64_t)m * nL + o] = a;
+        DL[(int64_t)m * nL + o] = dl;
+      }
+    if (lane < NMAX) dsm[(m - r0) * NMAX + lane] = dl;
+    float d[NMAX];
+#pragma unroll
+    for (int o = 0; o < NMAX; ++o) d[o] = __shfl_sync(0xffffffffu, dl, o);
+    float4 *srow = reinterpret_cast<float4 *>(S + (int64_t)m * H);
+#pragma unroll
+    for (int i = 0; i < HMAX4; ++i) {
+      const int k4 = lane + 32 * i;
+      if (k4 < H4) {
+        const float4 sg = srow[k4];
+        float4 t = make_float4(0.f, 0.f, 0.f, 0.f);
+#pragma unroll
+        for (int o = 0; o < NMAX; ++o) {
+          if (o < nL) {
+            const float4 w = reinterpret_cast<const float4 *>(ws_ + o * H)[k4];
+            t.x = fmaf(d[o], w.x, t.x); t.y = fmaf(d[o], w.y, t.y);
+            t.z = fmaf(d[o], w.z, t.z); t.w = fmaf(d[o], w.w, t.w);
+          }
+        }
+        srow[k4] = make_float4(t.x * sg.x, t.y * sg.y, t.z * sg.z, t.w * sg.w);
+      }
+    }
+  }
+  __syncthreads();
+  // phase 2: partial tendencies of the block's rows, column group c (4 columns; c == H4: bias)
+  float *pb = part + (int64_t)blockIdx.x * nL * (H + 1);
+  for (int c = threadIdx.x; c <= H4; c += blockDim.x) {
+    float4 g[NMAX];
+#pragma unroll
+    for (int o = 0; o < NMAX; ++o) g[o] = make_float4(0.f, 0.f, 0.f, 0.f);
+    for (int m = r0; m < r1; ++m) {
+      const float4 a = c < H4 ? __ldg(reinterpret_cast<const float4 *>(A + (int64_t)m * H) + c)
+                              : make_float4(1.f, 0.f, 0.f, 0.f);
+      const float *dr = dsm + (m - r0) * NMAX;
+#pragma unroll
+      for (int o = 0; o < NMAX; ++o) {
+        if (o < nL) {
+          const float dv = dr[o];
+          g[o].x = fmaf(dv, a.x, g[o].x); g[o].y = fmaf(dv, a.y, g[o].y);
+          g[o].z = fmaf(dv, a.z, g[o].z); g[o].w = fmaf(dv, a.w, g[o].w);
+        }
+      }
+    }
+#pragma unroll
+    for (int o = 0; o < NMAX; ++o) {
+      if (o < nL) {
+        float *p = pb + (int64_t)o * (H + 1) + 4 * c;
+        if (c < H4) { p[0] = g[o].x; p[1] = g[o].y; p[2] = g[o].z; p[3] = g[o].w; }
+        else p[0] = g[o].x;  // bias column H
+      }
+    }
+  }
+}
+
 __global__ void __launch_bounds__(256) sgd_update_kernel(float *__restrict__ p, const float *__restrict__ g, int64_t n,
                                                          float scale) {
   ptx::pdl_trigger();
@@ -472,6 +587,52 @@ cudaError_t sgd_update(cudaStream_t st, float *p, const float *g, int64_t n, flo
   if (n <= 0) return cudaSuccess;
   const int blocks = (int)std::min<int64_t>((n + 255) / 256, 8 * kSMs);
   return launch_k(sgd_update_kernel, dim3(blocks), dim3(256), 0, st, p, g, n, scale);
+}
+
+int out_layer_blocks(int n) { return std::max(1, std::min(2 * kSMs, (n + 7) / 8)); }
+
+constexpr int kOutSmemMax = 200 * 1024;
+static size_t out_layer_smem(int n, int H, int nL) {
+  const int R = out_layer_blocks(n);
+  return (size_t)nL * H * 4 + (size_t)((n + R - 1) / R) * 16 * 4;
+}
+
+bool out_layer_fusable(int n, int H, int nL, const float *A, const float *S, const float *W) {
+  auto al16 = [](const void *p) { return (reinterpret_cast<uintptr_t>(p) & 15) == 0; };
+  static const bool off = getenv("NF_NO_OUT_FUSE") != nullptr;
+  return !off && nL >= 1 && nL <= 16 && H % 4 == 0 && H >= 128 && H <= 2048 && n >= 256 &&
+         out_layer_smem(n, H, nL) <= kOutSmemMax && al16(A) && al16(S) && al16(W);
+}
+
+cudaError_t out_layer_train_fused(cudaStream_t st, int n, int H, int nL, const float *A, float *S, const float *W,
+                                  const float *bias, const float *Y, float *AL, float *DL, int act, float *part) {
+  const int R = out_layer_blocks(n);
+  const int rpb = (n + R - 1) / R;
+  const int blocks = (n + rpb - 1) / rpb;
+  const size_t smem = out_layer_smem(n, H, nL);
+  static bool attr = false;
+  if (!attr) {
+    cudaFuncSetAttribute(out_layer_train<16, 4>, cudaFuncAttributeMaxDynamicSharedMemorySize, kOutSmemMax);
+    cudaFuncSetAttribute(out_layer_train<16, 8>, cudaFuncAttributeMaxDynamicSharedMemorySize, kOutSmemMax);
+    cudaFuncSetAttribute(out_layer_train<16, 16>, cudaFuncAttributeMaxDynamicSharedMemorySize, kOutSmemMax);
+    attr = true;
+  }
+  if (H <= 512)
+    return launch_k(out_layer_train<16, 4>, dim3(blocks), dim3(256), smem, st, A, S, W, bias, Y, AL, DL, n, H, nL,
+                    act, rpb, part);
+  if (H <= 1024)
+    return launch_k(out_layer_train<16, 8>, dim3(blocks), dim3(256), smem, st, A, S, W, bias, Y, AL, DL, n, H, nL,
+                    act, rpb, part);
+  return launch_k(out_layer_train<16, 16>, dim3(blocks), dim3(256), smem, st, A, S, W, bias, Y, AL, DL, n, H, nL,
+                  act, rpb, part);
+}
+
+cudaError_t out_layer_grad_final(cudaStream_t st, int n, int H, int nL, const float *part, const EpiGrad &epi) {
+  const int R = out_layer_blocks(n);
+  const int rpb = (n + R - 1) / R;
+  const int blocks = (n + rpb - 1) / rpb;
+  const int64_t MN = (int64_t)nL * (H + 1);
+  return launch_k(grad_smallm_final, dim3((int)((MN + 31) / 32)), dim3(256), 0, st, part, blocks, nL, H, epi);
 }
 
 cudaError_t gemm_fwd(cudaStream_t st, int M, int N, int K, const float *A, const float *W,

@@ -34,6 +34,16 @@ cudaError_t gemm_bwd(cudaStream_t st, int M, int N, int K, const float *D, const
 cudaError_t gemm_grad(cudaStream_t st, int M, int N, int K, const float *D, const float *Aprev,
                       const EpiGrad &epi, const Workspace &ws);
 
+// The narrow output layer of a training step fused into one pass (kernels.cu, out_layer_train):
+// K1+K2 of layer L, K3 of layer L-1 (in place of S_{L-1}) and the partial tendencies of layer L
+// into part[R][nL][H+1] (R = out_layer_blocks(n)); out_layer_grad_final then sums them in fixed
+// order and applies epi (update or store).
+bool out_layer_fusable(int n, int H, int nL, const float *A, const float *S, const float *W);
+int out_layer_blocks(int n);
+cudaError_t out_layer_train_fused(cudaStream_t st, int n, int H, int nL, const float *A, float *S, const float *W,
+                                  const float *bias, const float *Y, float *AL, float *DL, int act, float *part);
+cudaError_t out_layer_grad_final(cudaStream_t st, int n, int H, int nL, const float *part, const EpiGrad &epi);
+
 // K5: mean quadratic cost and argmax-accuracy of A_L against Y over n rows of
 // width w.  part: scratch of >= loss_acc_parts() double2.  Results: out[0] =
 // mean loss, out[1] = accuracy (device floats); step_loss (nullable) gets the

@@ -48,6 +48,12 @@ SHAPES = [
     # bwd_smallk, grad_smallm in kernels.cu)
     ([300, 200, 10], "tanh,sigmoid", 600),
     ([516, 132, 7], "sigmoid", 1031),
+    # narrow output layer (n_L <= 16) after a hidden layer of 128..2048 (multiple of 4) over
+    # >= 256 rows: the fused output-layer training kernel (out_layer_train: 4-, 8- and 16-slot
+    # variants; n_L = 1, 10, 12, 16)
+    ([40, 1100, 12], "tanh,sigmoid", 300),
+    ([64, 256, 16], "sigmoid", 513),
+    ([30, 640, 10], "gaussian,sigmoid", 257),
     # two-layer nets with narrow layers and n0 % 4 == 0: the fused inference kernel
     # (infer_small.cu) with a ragged last 64-row tile and a ragged last pixel chunk
     ([100, 17, 3], "tanh,sigmoid", 777),
