@@ -14,6 +14,7 @@
 #include "fp64.cuh"
 #include "fused_small.cuh"
 #include "infer_small.cuh"
+#include "single_cta.cuh"
 #include "kernels.cuh"
 
 using namespace nf;
@@ -596,6 +597,21 @@ int nf_train_steps(nf_net *net, const float *X, const float *Y, int64_t N, int64
     dN = n_steps * batch;
   }
 
+  // Latency regime (a few rows per step, parameters fit one SM): the single-CTA kernel
+  if (net->math != NF_MATH_FP64 && single_cta_applicable(net->dims, batch)) {
+    NF_CUDA(net->d_starts.ensure((size_t)n_steps * sizeof(int64_t)));
+    NF_CUDA(cudaMemcpyAsync(net->d_starts.p, st.data(), (size_t)n_steps * sizeof(int64_t), cudaMemcpyHostToDevice,
+                            net->stream));
+    const int src = single_cta_train_steps(net->stream, net->dims, net->act_h, net->act_o, net->params, dX, dY,
+                                           batch, net->d_starts.as<int64_t>(), n_steps, eta, step_loss);
+    if (src == 0) {
+      fused_small_invalidate(net->fused);
+      if (host_in) NF_CUDA(cudaStreamSynchronize(net->stream));
+      return NF_OK;
+    }
+    if (src != SINGLE_NOT_APPLICABLE)
+      return fail(NF_ECUDA, "single-CTA kernel: %s", cudaGetErrorString((cudaError_t)src));
+  }
   int rc = net->math == NF_MATH_FP64 ? FUSED_NOT_APPLICABLE : fused_small_train_steps(net->fused, net->stream, net->dims, net->act_h, net->act_o,
                                    net->params, dX, dY, dN, batch, st.data(), n_steps, eta, step_loss);
   if (rc == FUSED_NOT_APPLICABLE) {

@@ -396,3 +396,27 @@ def test_train_single_online_sgd(dims, act):
     net.train_steps(dev(X), dev(Y), 1, starts, 0.1)
     ref, _ = oracle.Oracle(dims, act).train_steps(p, X, Y, 1, starts, 0.1)
     assert rel_err(gpu_params(net), ref) <= FP32_BAR
+
+
+@pytest.mark.parametrize("dims,act,batch,steps", [
+    ([784, 30, 10], "sigmoid", 1, 40),          # train_single on the c2 net
+    ([200, 136, 72, 5], "tanh,sigmoid", 8, 10),  # no K6 for this net: one CTA up to ~1 M MAC/step
+    ([3, 5, 2], "sigmoid", 8, 100),             # c1's shape
+    ([100, 70, 40, 20, 3], "tanh,sigmoid", 5, 30),   # deeper net, thread-per-output layers
+    ([64, 130, 9], "gaussian,sigmoid", 3, 25),  # warp-per-element delta (n_l >= 64)
+])
+def test_small_batch_single_cta_path(dims, act, batch, steps):
+    """nf_train_steps in the latency regime (a few rows per step, parameters in one SM's shared
+    memory): the single-CTA kernel, parameters and per-step costs against the oracle."""
+    p = synth.random_params(61 + batch, dims, 0.4)
+    X, Y = synth.random_batch(62 + batch, 300, dims[0], dims[-1], "uniform")
+    rng = np.random.default_rng(batch)
+    starts = rng.integers(0, 300 - batch + 1, size=steps)
+    net = make_net(dims, act, p)
+    loss = torch.zeros(steps, device="cuda")
+    n0 = nf.nf_launch_count()
+    net.train_steps(dev(X), dev(Y), batch, starts, 0.5, step_loss=loss)
+    assert nf.nf_launch_count() - n0 == 1          # one kernel for all steps
+    ref, ref_loss = oracle.Oracle(dims, act).train_steps(p, X, Y, batch, starts, 0.5)
+    assert rel_err(gpu_params(net), ref) <= FP32_BAR
+    assert rel_err(loss.cpu().numpy(), ref_loss) <= FP32_BAR
