@@ -143,7 +143,7 @@ def job_throughput(world, steps, batch, t_max):
 # The oracle's per-sample cost does not depend on the batch size (one fwd/bwd per sample, one
 # update per step), so a reduced batch is a fair sample of samples/s for the wide configs.
 # NF_MATH_FP64 is bound by the FP64 FMA units (SIMT DFMA): peak measured by micro/fma_rate.cu
-FP64_DFMA_TFLOPS = 1.0  # placeholder, set from the measurement
+FP64_DFMA_TFLOPS = 34.82  # DFMA, 32 warps/SM, 148 SMs at 1965 MHz (59.9 FMA/clk/SM)
 FP64_PEAK_SOURCE = "micro/fma_rate.cu DFMA rate, 148 SMs (profiles/r01_micro_fma_rate.txt)"
 CPU_SAMPLE = {1: (20000, None), 2: (200, None), 3: (2, 256), 4: (4, 512), 5: (1, 32)}
 

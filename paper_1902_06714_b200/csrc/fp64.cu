@@ -59,10 +59,13 @@ struct Args64 {
   double *partial;  // split-K partials [z][M][N]
 };
 
-template <bool AK, bool BKM, class Epi>
+// 16 x 16 threads, each a TM x TN micro-tile of rows ty + 16 i, columns tx + 16 j (strided, so
+// the shared-memory reads of a warp are one broadcast / one 128-B wavefront each): BM = 16 TM.
+template <int TM, int TN, bool AK, bool BKM, class Epi>
 __global__ void __launch_bounds__(256)
 gemm64_kernel(Args64 g, Epi epi) {
-  constexpr int BM = 64, BN = 64, BK = 8, TM = 4, TN = 4;
+  constexpr int BM = 16 * TM, BN = 16 * TN, BK = 8;
+  constexpr int LA = BM * BK / 256, LB = BN * BK / 256;  // staged elements per thread
   __shared__ double As[2][BK][BM + 1];
   __shared__ double Bs[2][BK][BN + 1];
   ptx::pdl_trigger();
@@ -71,10 +74,10 @@ gemm64_kernel(Args64 g, Epi epi) {
   const int m0 = blockIdx.y * BM, n0 = blockIdx.x * BN;
   const int kbeg = blockIdx.z * g.kchunk, kend = min(g.K, kbeg + g.kchunk);
   const int nkt = (kend - kbeg + BK - 1) / BK;
-  double ra[2], rb[2];
+  double ra[LA], rb[LB];
   auto load = [&](int k0) {
 #pragma unroll
-    for (int i = 0; i < 2; ++i) {
+    for (int i = 0; i < LA; ++i) {
       const int idx = tid + i * 256;
       const int mm = AK ? idx / BK : idx % BM, kk = AK ? idx % BK : idx / BM;
       const int m = m0 + mm, k = k0 + kk;
@@ -84,6 +87,10 @@ gemm64_kernel(Args64 g, Epi epi) {
         v = g.Af ? (double)g.Af[off] : g.Ad[off];
       }
       ra[i] = v;
+    }
+#pragma unroll
+    for (int i = 0; i < LB; ++i) {
+      const int idx = tid + i * 256;
       const int nn = BKM ? idx / BK : idx % BN, kb = BKM ? idx % BK : idx / BN;
       const int n = n0 + nn, kq = k0 + kb;
       double w = 0.0;
@@ -99,10 +106,14 @@ gemm64_kernel(Args64 g, Epi epi) {
   };
   auto store = [&](int buf) {
 #pragma unroll
-    for (int i = 0; i < 2; ++i) {
+    for (int i = 0; i < LA; ++i) {
       const int idx = tid + i * 256;
       const int mm = AK ? idx / BK : idx % BM, kk = AK ? idx % BK : idx / BM;
       As[buf][kk][mm] = ra[i];
+    }
+#pragma unroll
+    for (int i = 0; i < LB; ++i) {
+      const int idx = tid + i * 256;
       const int nn = BKM ? idx / BK : idx % BN, kb = BKM ? idx % BK : idx / BN;
       Bs[buf][kb][nn] = rb[i];
     }
@@ -124,9 +135,9 @@ gemm64_kernel(Args64 g, Epi epi) {
     for (int kk = 0; kk < BK; ++kk) {
       double a[TM], b[TN];
 #pragma unroll
-      for (int i = 0; i < TM; ++i) a[i] = As[buf][kk][ty * TM + i];
+      for (int i = 0; i < TM; ++i) a[i] = As[buf][kk][ty + 16 * i];
 #pragma unroll
-      for (int j = 0; j < TN; ++j) b[j] = Bs[buf][kk][tx * TN + j];
+      for (int j = 0; j < TN; ++j) b[j] = Bs[buf][kk][tx + 16 * j];
 #pragma unroll
       for (int i = 0; i < TM; ++i)
 #pragma unroll
@@ -137,11 +148,11 @@ gemm64_kernel(Args64 g, Epi epi) {
   }
 #pragma unroll
   for (int i = 0; i < TM; ++i) {
-    const int m = m0 + ty * TM + i;
+    const int m = m0 + ty + 16 * i;
     if (m >= g.M) continue;
 #pragma unroll
     for (int j = 0; j < TN; ++j) {
-      const int n = n0 + tx * TN + j;
+      const int n = n0 + tx + 16 * j;
       if (n >= g.N) continue;
       if (g.partial) g.partial[((int64_t)blockIdx.z * g.M + m) * g.N + n] = acc[i][j];
       else epi(m, n, acc[i][j]);
@@ -164,6 +175,15 @@ __global__ void __launch_bounds__(256) splitk64(const double *__restrict__ part,
 template <bool AK, bool BKM, class Epi>
 cudaError_t run64(cudaStream_t st, Args64 g, const Epi &epi, double *partial, size_t partial_doubles) {
   if (g.M <= 0 || g.N <= 0) return cudaSuccess;
+  // 128 x 128 tiles (8 x 8 per thread: 64 DFMA per 16 shared loads) when they fill the GPU
+  const int64_t t128 = (int64_t)((g.M + 127) / 128) * ((g.N + 127) / 128);
+  if (t128 >= kSMs) {
+    g.kchunk = std::max(g.K, 1);
+    g.partial = nullptr;
+    gemm64_kernel<8, 8, AK, BKM, Epi><<<dim3((g.N + 127) / 128, (g.M + 127) / 128, 1), 256, 0, st>>>(g, epi);
+    count_launch();
+    return cudaGetLastError();
+  }
   const int tm = (g.M + 63) / 64, tn = (g.N + 63) / 64;
   const int tiles = tm * tn;
   int splits = 1;
@@ -176,7 +196,7 @@ cudaError_t run64(cudaStream_t st, Args64 g, const Epi &epi, double *partial, si
   splits = std::max(1, (g.K + kchunk - 1) / kchunk);
   g.kchunk = splits > 1 ? kchunk : std::max(g.K, 1);
   g.partial = splits > 1 ? partial : nullptr;
-  gemm64_kernel<AK, BKM, Epi><<<dim3(tn, tm, splits), 256, 0, st>>>(g, epi);
+  gemm64_kernel<4, 4, AK, BKM, Epi><<<dim3(tn, tm, splits), 256, 0, st>>>(g, epi);
   count_launch();
   if (splits > 1) {
     const int64_t MN = (int64_t)g.M * g.N;
