@@ -161,7 +161,7 @@ int ensure_ws(nf_net *net, int64_t rows) {
   drop_graph(net);
   NF_CUDA(net->stash.ensure((size_t)(per_row * rows) * sizeof(float)));
   if (net->L >= 2)
-    NF_CUDA(net->part_out.ensure((size_t)out_layer_blocks((int)rows) * net->dims[net->L] *
+    NF_CUDA(net->part_out.ensure((size_t)out_layer_blocks((int)rows, net->dims[net->L - 1]) * net->dims[net->L] *
                                  (net->dims[net->L - 1] + 1) * sizeof(float)));
   float *p = net->stash.as<float>();
   net->A.assign(net->L + 1, nullptr);

@@ -270,15 +270,22 @@ colsum_final(const float *__restrict__ part, int nchunks, int cols, EpiGrad epi)
 
 cudaError_t bias_grad(cudaStream_t st, const float *D, int64_t rows, int cols, const EpiGrad &epi,
                       float *part, size_t part_floats) {
+  static const bool det = getenv("NF_SPLITK_DETERMINISTIC") != nullptr;
+  const int cblocks = (cols + 255) / 256;
+  if (!epi.store_only && !det) {
+    // SGD update: one kernel, chunk sums reduced into b in L2.  Chunks of >= 64 rows: every
+    // b[c] receives one reduction per chunk, and more of them contend for the same L2 line
+    // (16-row chunks made the c4 step 164 -> 191 us)
+    const int nch = (int)std::min<int64_t>((rows + 63) / 64, 256);
+    const int ch = (int)((rows + nch - 1) / nch);
+    return launch_k(colsum_partial, dim3(cblocks, (int)((rows + ch - 1) / ch)), dim3(256), 0, st, D, rows, cols, ch,
+                    (float *)nullptr, epi.b, epi.scale);
+  }
   // ~4 column blocks x 64+ row chunks of <= 64 rows: enough CTAs to stream D at HBM rate
   int nchunks = (int)std::min<int64_t>((rows + 63) / 64, 256);
   while (nchunks > 1 && (size_t)nchunks * cols > part_floats) --nchunks;
   const int chunk = (int)((rows + nchunks - 1) / nchunks);
-  const dim3 grid((cols + 255) / 256, nchunks);
-  static const bool det = getenv("NF_SPLITK_DETERMINISTIC") != nullptr;
-  if (!epi.store_only && !det)  // SGD update: one kernel, chunk sums reduced into b in L2
-    return launch_k(colsum_partial, grid, dim3(256), 0, st, D, rows, cols, chunk, (float *)nullptr, epi.b,
-                    epi.scale);
+  const dim3 grid(cblocks, nchunks);
   cudaError_t e = launch_k(colsum_partial, grid, dim3(256), 0, st, D, rows, cols, chunk, part, (float *)nullptr,
                            0.0f);
   if (e != cudaSuccess) return e;
@@ -589,11 +596,17 @@ cudaError_t sgd_update(cudaStream_t st, float *p, const float *g, int64_t n, flo
   return launch_k(sgd_update_kernel, dim3(blocks), dim3(256), 0, st, p, g, n, scale);
 }
 
-int out_layer_blocks(int n) { return std::max(1, std::min(2 * kSMs, (n + 7) / 8)); }
+// blocks of the fused output-layer kernel: >= 8 rows each (>= 8192 / H for narrow hidden
+// layers, so that the fixed-order final sum has few partials), at most 2 per SM
+int out_layer_blocks(int n, int H) {
+  (void)H;  // (>= 8192 / H rows for narrow H cut the final sum's partials but made c4 slower)
+  const int rmin = 8;
+  return std::max(1, std::min(2 * kSMs, (n + rmin - 1) / rmin));
+}
 
 constexpr int kOutSmemMax = 200 * 1024;
 static size_t out_layer_smem(int n, int H, int nL) {
-  const int R = out_layer_blocks(n);
+  const int R = out_layer_blocks(n, H);
   return (size_t)nL * H * 4 + (size_t)((n + R - 1) / R) * 16 * 4;
 }
 
@@ -606,7 +619,7 @@ bool out_layer_fusable(int n, int H, int nL, const float *A, const float *S, con
 
 cudaError_t out_layer_train_fused(cudaStream_t st, int n, int H, int nL, const float *A, float *S, const float *W,
                                   const float *bias, const float *Y, float *AL, float *DL, int act, float *part) {
-  const int R = out_layer_blocks(n);
+  const int R = out_layer_blocks(n, H);
   const int rpb = (n + R - 1) / R;
   const int blocks = (n + rpb - 1) / rpb;
   const size_t smem = out_layer_smem(n, H, nL);
@@ -628,7 +641,7 @@ cudaError_t out_layer_train_fused(cudaStream_t st, int n, int H, int nL, const f
 }
 
 cudaError_t out_layer_grad_final(cudaStream_t st, int n, int H, int nL, const float *part, const EpiGrad &epi) {
-  const int R = out_layer_blocks(n);
+  const int R = out_layer_blocks(n, H);
   const int rpb = (n + R - 1) / R;
   const int blocks = (n + rpb - 1) / rpb;
   const int64_t MN = (int64_t)nL * (H + 1);

@@ -36,10 +36,10 @@ cudaError_t gemm_grad(cudaStream_t st, int M, int N, int K, const float *D, cons
 
 // The narrow output layer of a training step fused into one pass (kernels.cu, out_layer_train):
 // K1+K2 of layer L, K3 of layer L-1 (in place of S_{L-1}) and the partial tendencies of layer L
-// into part[R][nL][H+1] (R = out_layer_blocks(n)); out_layer_grad_final then sums them in fixed
+// into part[R][nL][H+1] (R = out_layer_blocks(n, H)); out_layer_grad_final then sums them in fixed
 // order and applies epi (update or store).
 bool out_layer_fusable(int n, int H, int nL, const float *A, const float *S, const float *W);
-int out_layer_blocks(int n);
+int out_layer_blocks(int n, int H);
 cudaError_t out_layer_train_fused(cudaStream_t st, int n, int H, int nL, const float *A, float *S, const float *W,
                                   const float *bias, const float *Y, float *AL, float *DL, int act, float *part);
 cudaError_t out_layer_grad_final(cudaStream_t st, int n, int H, int nL, const float *part, const EpiGrad &epi);
