@@ -29,15 +29,20 @@ _SRC = os.path.join(_HERE, "nf_oracle.c")
 ACT = {"sigmoid": 0, "tanh": 1, "relu": 2, "gaussian": 3, "step": 4}
 
 
-def parse_activation(spec: str) -> tuple[int, int]:
-    """'sigmoid' -> (hidden, output) = (sigmoid, sigmoid); 'relu,sigmoid' -> split
-    (reading R7).  Unknown names raise (never a silent default)."""
+def parse_activation(spec: str, L: int = 2) -> list[int]:
+    """Activation kind of each of the L layers: 'sigmoid' -> every layer; 'relu,sigmoid' ->
+    hidden layers / output layer (reading R7); L comma-separated names -> one per layer
+    (SURVEY 8(f)).  Unknown names or other counts raise (never a silent default)."""
     parts = [s.strip().lower() for s in spec.split(",")]
-    if len(parts) == 1:
-        parts = parts * 2
-    if len(parts) != 2 or any(p not in ACT for p in parts):
+    if any(p not in ACT for p in parts):
         raise ValueError(f"unknown activation spec {spec!r}")
-    return ACT[parts[0]], ACT[parts[1]]
+    if len(parts) == 1:
+        parts = parts * L
+    elif len(parts) == 2:
+        parts = [parts[0]] * (L - 1) + [parts[1]]
+    elif len(parts) != L:
+        raise ValueError(f"activation spec {spec!r}: need 1, 2 or {L} names")
+    return [ACT[p] for p in parts]
 
 
 def build(force: bool = False) -> None:
@@ -99,7 +104,9 @@ class Oracle:
         self.dims = [int(d) for d in dims]
         if len(self.dims) < 2 or min(self.dims) < 1:
             raise ValueError("dims needs >= 2 entries, each >= 1 (S:118-124)")
-        self.act_h, self.act_o = parse_activation(activation)
+        self.acts = parse_activation(activation, len(self.dims) - 1)
+        self.act_h, self.act_o = self.acts[0], self.acts[-1]
+        self._acts = np.ascontiguousarray(np.asarray(self.acts, dtype=np.int32))
         self.bits = bits
         self.lib = _lib(bits)
         self.real = _real(bits)
@@ -119,7 +126,7 @@ class Oracle:
     def _head(self):
         d, nd = _dims(self.dims)
         self._keep = d
-        return _ptr(d), nd, ctypes.c_int(self.act_h), ctypes.c_int(self.act_o)
+        return _ptr(d), nd, _ptr(self._acts)
 
     def layers(self, params):
         """Split a flat vector into [(W_l [n_l][n_{l-1}], b_l [n_l])] views."""
@@ -220,12 +227,10 @@ class Oracle:
         """Rows whose hidden pre-activations all keep |z| > margin, where a relu/step
         derivative is a discrete decision: the fp32 GPU sum and this fp64 sum may take it
         differently within rounding (reading R8 of DESIGN.md).  Parity compares these rows."""
-        acts = (self.act_h, self.act_o)
         _, _, Zs = self.stash(params, x, y, with_z=True)
         ok = np.ones(x.shape[0], dtype=bool)
         for l, z in enumerate(Zs, start=1):
-            kind = acts[0] if l < len(Zs) else acts[1]
-            if kind in (ACT["relu"], ACT["step"]):
+            if self.acts[l - 1] in (ACT["relu"], ACT["step"]):
                 ok &= np.all(np.abs(z) > margin, axis=1)
         return ok
 

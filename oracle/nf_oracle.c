@@ -67,10 +67,11 @@ REAL orc_act_prime(int kind, REAL x)
     return NAN;
 }
 
-/* the activation of layer l (1-based, l = 1..L): hidden kind for l < L,
- * output kind for l = L (reading R7: the paper has one activation per net,
- * P:158-161; configs 4/5 need relu hidden + sigmoid output). */
-static int act_of(int l, int L, int act_h, int act_o) { return l < L ? act_h : act_o; }
+/* the activation of layer l (1-based, l = 1..L) is acts[l-1] (reading R7: the paper has one
+ * activation per net; configs 4/5 need relu hidden + sigmoid output, and SURVEY
+ * 8(f) generalises to one activation per layer).  The Python wrapper expands "name" and
+ * "hidden,output" specs into this array. */
+static int act_of(const int *acts, int l) { return acts[l - 1]; }
 
 long orc_param_count(const int *dims, int nd)
 {
@@ -90,7 +91,8 @@ static void layer_offsets(const int *dims, int nd, long *offW, long *offB)
 }
 
 typedef struct {
-    int nd, L, act_h, act_o, maxw;
+    int nd, L, maxw;
+    const int *acts;             /* acts[l-1]: activation kind of layer l */
     const int *dims;
     long offW[ORC_MAX_LAYERS], offB[ORC_MAX_LAYERS];
     REAL *a[ORC_MAX_LAYERS];     /* a_l, l = 0..L (a_0 = x) */
@@ -98,11 +100,13 @@ typedef struct {
     REAL *delta[ORC_MAX_LAYERS]; /* delta_l, l = 1..L (backprop db(n)) */
 } net_t;
 
-static int net_open(net_t *t, const int *dims, int nd, int act_h, int act_o)
+static int net_open(net_t *t, const int *dims, int nd, const int *acts)
 {
     if (nd < 2 || nd > ORC_MAX_LAYERS) return -1;
     memset(t, 0, sizeof *t);
-    t->nd = nd; t->L = nd - 1; t->dims = dims; t->act_h = act_h; t->act_o = act_o;
+    t->nd = nd; t->L = nd - 1; t->dims = dims; t->acts = acts;
+    for (int l = 1; l < nd; ++l)
+        if (acts[l - 1] < ORC_SIGMOID || acts[l - 1] > ORC_STEP) return -1;
     for (int l = 0; l < nd; ++l) {
         if (dims[l] < 1) return -1;
         t->a[l] = (REAL *)calloc((size_t)dims[l], sizeof(REAL));
@@ -128,7 +132,7 @@ static void fwdprop(net_t *t, const REAL *p, const float *x)
     for (int l = 1; l <= t->L; ++l) {
         const int ni = t->dims[l], nk = t->dims[l - 1];
         const REAL *W = p + t->offW[l], *b = p + t->offB[l];
-        const int kind = act_of(l, t->L, t->act_h, t->act_o);
+        const int kind = act_of(t->acts, l);
         for (int i = 0; i < ni; ++i) {
             REAL s = 0;
             for (int k = 0; k < nk; ++k) s += W[(long)i * nk + k] * t->a[l - 1][k];
@@ -149,11 +153,11 @@ static void backprop_accumulate(net_t *t, const REAL *p, const float *y, REAL *G
     const int L = t->L;
     for (int i = 0; i < t->dims[L]; ++i)
         t->delta[L][i] = (t->a[L][i] - (REAL)y[i]) *
-                         orc_act_prime(act_of(L, L, t->act_h, t->act_o), t->z[L][i]);
+                         orc_act_prime(act_of(t->acts, L), t->z[L][i]);
     for (int l = L - 1; l >= 1; --l) {
         const int nk = t->dims[l], ni = t->dims[l + 1];
         const REAL *W = p + t->offW[l + 1];
-        const int kind = act_of(l, L, t->act_h, t->act_o);
+        const int kind = act_of(t->acts, l);
         for (int k = 0; k < nk; ++k) {
             REAL s = 0;
             for (int i = 0; i < ni; ++i) s += W[(long)i * nk + k] * t->delta[l + 1][i];
@@ -171,11 +175,11 @@ static void backprop_accumulate(net_t *t, const REAL *p, const float *y, REAL *G
 }
 
 /* output: the fwdprop recursion, returning a_L only. out[n][n_L]. */
-int orc_output(const int *dims, int nd, int act_h, int act_o, const REAL *p,
+int orc_output(const int *dims, int nd, const int *acts, const REAL *p,
                const float *x, long n, REAL *out)
 {
     net_t t;
-    if (net_open(&t, dims, nd, act_h, act_o)) { net_close(&t); return -1; }
+    if (net_open(&t, dims, nd, acts)) { net_close(&t); return -1; }
     for (long s = 0; s < n; ++s) {
         fwdprop(&t, p, x + s * dims[0]);
         for (int i = 0; i < dims[nd - 1]; ++i) out[s * dims[nd - 1] + i] = t.a[t.L][i];
@@ -186,11 +190,11 @@ int orc_output(const int *dims, int nd, int act_h, int act_o, const REAL *p,
 
 /* summed tendencies over a batch (the batch accumulation of train_batch,
  * P:460-476, and the co_sum total).  G is overwritten. */
-int orc_grad(const int *dims, int nd, int act_h, int act_o, const REAL *p,
+int orc_grad(const int *dims, int nd, const int *acts, const REAL *p,
              const float *x, const float *y, long n, REAL *G)
 {
     net_t t;
-    if (net_open(&t, dims, nd, act_h, act_o)) { net_close(&t); return -1; }
+    if (net_open(&t, dims, nd, acts)) { net_close(&t); return -1; }
     memset(G, 0, sizeof(REAL) * (size_t)orc_param_count(dims, nd));
     for (long s = 0; s < n; ++s) {
         fwdprop(&t, p, x + s * dims[0]);
@@ -222,14 +226,14 @@ static REAL sample_cost(const net_t *t, const float *y)
  * summed tendencies are applied once, scaled eta/n (reading R3).
  * If batch_loss != NULL it receives the mean cost of the batch under the
  * pre-update parameters (reading R9). */
-int orc_train_batch(const int *dims, int nd, int act_h, int act_o, REAL *p,
+int orc_train_batch(const int *dims, int nd, const int *acts, REAL *p,
                     const float *x, const float *y, long n, REAL eta, REAL *batch_loss)
 {
     if (n <= 0) return -1;
     const long cnt = orc_param_count(dims, nd);
     REAL *G = (REAL *)calloc((size_t)cnt, sizeof(REAL));
     net_t t;
-    if (!G || net_open(&t, dims, nd, act_h, act_o)) { free(G); return -1; }
+    if (!G || net_open(&t, dims, nd, acts)) { free(G); return -1; }
     REAL loss = 0;
     for (long s = 0; s < n; ++s) {
         fwdprop(&t, p, x + s * dims[0]);
@@ -246,13 +250,13 @@ int orc_train_batch(const int *dims, int nd, int act_h, int act_o, REAL *p,
 /* The MNIST driver's minibatch loop on a resident dataset:
  * step s trains on rows [starts[s], starts[s]+batch) of X/Y (reading R11:
  * 0-based starts uniform in [0, N-batch]).  step_loss may be NULL. */
-int orc_train_steps(const int *dims, int nd, int act_h, int act_o, REAL *p,
+int orc_train_steps(const int *dims, int nd, const int *acts, REAL *p,
                     const float *X, const float *Y, long N, long batch,
                     const long *starts, long n_steps, REAL eta, REAL *step_loss)
 {
     for (long s = 0; s < n_steps; ++s) {
         if (starts[s] < 0 || starts[s] + batch > N) return -2;
-        int rc = orc_train_batch(dims, nd, act_h, act_o, p, X + starts[s] * dims[0],
+        int rc = orc_train_batch(dims, nd, acts, p, X + starts[s] * dims[0],
                                  Y + starts[s] * dims[nd - 1], batch, eta,
                                  step_loss ? step_loss + s : NULL);
         if (rc) return rc;
@@ -261,11 +265,11 @@ int orc_train_steps(const int *dims, int nd, int act_h, int act_o, REAL *p,
 }
 
 /* mean quadratic cost over n samples (reading R9). */
-int orc_loss(const int *dims, int nd, int act_h, int act_o, const REAL *p,
+int orc_loss(const int *dims, int nd, const int *acts, const REAL *p,
              const float *x, const float *y, long n, REAL *loss)
 {
     net_t t;
-    if (net_open(&t, dims, nd, act_h, act_o)) { net_close(&t); return -1; }
+    if (net_open(&t, dims, nd, acts)) { net_close(&t); return -1; }
     REAL c = 0;
     for (long s = 0; s < n; ++s) {
         fwdprop(&t, p, x + s * dims[0]);
@@ -292,11 +296,11 @@ static int argmax_first_f(const float *v, int n)
 
 /* accuracy: fraction of samples whose
  * predicted class argmax(a_L) equals argmax(y).  n = 0 -> 0.0. */
-int orc_accuracy(const int *dims, int nd, int act_h, int act_o, const REAL *p,
+int orc_accuracy(const int *dims, int nd, const int *acts, const REAL *p,
                  const float *x, const float *y, long n, REAL *acc)
 {
     net_t t;
-    if (net_open(&t, dims, nd, act_h, act_o)) { net_close(&t); return -1; }
+    if (net_open(&t, dims, nd, acts)) { net_close(&t); return -1; }
     long good = 0;
     const int no = dims[nd - 1];
     for (long s = 0; s < n; ++s) {
@@ -311,12 +315,12 @@ int orc_accuracy(const int *dims, int nd, int act_h, int act_o, const REAL *p,
 /* per-layer stash of one forward pass over a batch, for kernel-level
  * parity (a_l, delta_l and z_l per sample).  A: for l=0..L, [n][n_l] blocks
  * concatenated; D and Z (Z may be NULL): for l=1..L, [n][n_l] blocks. */
-int orc_forward_backward_stash(const int *dims, int nd, int act_h, int act_o,
+int orc_forward_backward_stash(const int *dims, int nd, const int *acts,
                                const REAL *p, const float *x, const float *y,
                                long n, REAL *A, REAL *D, REAL *Z)
 {
     net_t t;
-    if (net_open(&t, dims, nd, act_h, act_o)) { net_close(&t); return -1; }
+    if (net_open(&t, dims, nd, acts)) { net_close(&t); return -1; }
     const long cnt = orc_param_count(dims, nd);
     REAL *G = (REAL *)calloc((size_t)cnt, sizeof(REAL));
     if (!G) { net_close(&t); return -1; }

@@ -210,6 +210,8 @@ cudaError_t run_tc(cudaStream_t st, int M, int N, int K, const TcOp &a, const Tc
       if (N > 128 && sp >= 2 && tiles(256) * sp >= fill) return launch_tc<256, AMN, BMN, 1>(st, M, N, K, a, b, epi, ws);
     }
     if (N > 64 && tiles(128) >= fill) return launch_tc<128, AMN, BMN, 1>(st, M, N, K, a, b, epi, ws);
+    static const bool bn32 = getenv("NF_TC_BN32") != nullptr;  // experiment: narrow tiles, more CTAs
+    if (bn32 && tiles(64) < fill && tiles(32) <= 2 * kSMs) return launch_tc<32, AMN, BMN, 1>(st, M, N, K, a, b, epi, ws);
     return launch_tc<64, AMN, BMN, 1>(st, M, N, K, a, b, epi, ws);
   }
   g_last_engine = ENGINE_TC3;

@@ -70,6 +70,51 @@ def test_unknown_activation_is_an_error():
         O64([2, 0, 1], "sigmoid")    # every dim >= 1
 
 
+def test_activation_spec_forms():
+    """One name -> every layer; "hidden,output" -> hidden / output (R7); L names -> one per
+    layer; any other count is an error."""
+    A = oracle.ACT
+    assert oracle.parse_activation("tanh", 3) == [A["tanh"]] * 3
+    assert oracle.parse_activation("relu,sigmoid", 4) == [A["relu"]] * 3 + [A["sigmoid"]]
+    assert oracle.parse_activation("relu,tanh,gaussian", 3) == [A["relu"], A["tanh"], A["gaussian"]]
+    assert oracle.parse_activation("relu,sigmoid", 1) == [A["sigmoid"]]
+    with pytest.raises(ValueError):
+        oracle.parse_activation("relu,tanh,sigmoid", 4)
+    with pytest.raises(ValueError):
+        O64([2, 3, 4, 2], "relu,tanh,sigmoid,step")
+
+
+def test_per_layer_activations_reduce_to_the_shared_forms():
+    """A per-layer list with the hidden name repeated is the "hidden,output" net, bit for bit;
+    a list of one name is the single-name net."""
+    dims = [5, 7, 6, 3]
+    p = synth.random_params(3, dims, 0.7).astype(np.float64)
+    x, y = synth.random_batch(4, 9, 5, 3, "normal")
+    assert np.array_equal(O64(dims, "tanh,tanh,sigmoid").grad(p, x, y), O64(dims, "tanh,sigmoid").grad(p, x, y))
+    assert np.array_equal(O64(dims, "gaussian,gaussian,gaussian").output(p, x), O64(dims, "gaussian").output(p, x))
+    # and the order matters: swapping two hidden activations changes the output
+    assert not np.array_equal(O64(dims, "tanh,gaussian,sigmoid").output(p, x),
+                              O64(dims, "gaussian,tanh,sigmoid").output(p, x))
+
+
+@pytest.mark.parametrize("acts", ["tanh,gaussian,sigmoid,tanh", "sigmoid,tanh,gaussian,sigmoid"])
+def test_per_layer_backprop_matches_centered_fd(acts):
+    """Backprop with a different activation in every layer: every dW, db entry equals the
+    centered FD (h = 1e-6) of the cost (fp64, rel 1e-5) -- the per-layer sigma' indexing."""
+    dims = [4, 6, 5, 3, 2]
+    o = O64(dims, acts)
+    p = synth.random_params(77, dims, 0.8).astype(np.float64)
+    x, y = synth.random_batch(78, 3, dims[0], dims[-1], "normal")
+    G = o.grad(p, x, y)
+    h = 1e-6
+    scale = max(np.abs(G).max(), 1e-8)
+    for i in range(p.size):
+        q = p.copy(); q[i] += h; cp = o.loss(q, x, y) * 3
+        q[i] -= 2 * h; cm = o.loss(q, x, y) * 3
+        fd = (cp - cm) / (2 * h)
+        assert abs(fd - G[i]) <= 1e-5 * max(abs(G[i]), 1e-3 * scale), (acts, i, fd, G[i])
+
+
 # --------------------------------------------------------------------------- shapes
 def test_param_counts(golden_dir):
     g = {k: float(v) for k, v in _read_golden(golden_dir, "paper_numbers.txt")}
@@ -348,3 +393,17 @@ def test_real32_build_tracks_real64():
     g64 = oracle.Oracle(dims, bits=64).grad(p, X, Y)
     g32 = oracle.Oracle(dims, bits=32).grad(p, X, Y)
     assert np.max(np.abs(g32 - g64)) <= 1e-4 * np.max(np.abs(g64))
+
+
+def test_per_layer_forward_matches_numpy_closed_forms():
+    """Per-layer activations against numpy's own closed forms (tanh, e^{-z^2}, 1/(1+e^{-z})):
+    layer l uses the l-th name."""
+    dims = [3, 4, 5, 2]
+    p = synth.random_params(5, dims, 0.9).astype(np.float64)
+    x, _ = synth.random_batch(6, 7, 3, 2, "normal")
+    o = O64(dims, "tanh,gaussian,sigmoid")
+    (W1, b1), (W2, b2), (W3, b3) = o.layers(p)
+    a = np.tanh(x.astype(np.float64) @ W1.T + b1)
+    a = np.exp(-(a @ W2.T + b2) ** 2)
+    a = 1.0 / (1.0 + np.exp(-(a @ W3.T + b3)))
+    np.testing.assert_allclose(o.output(p, x), a, rtol=1e-12, atol=1e-14)
