@@ -67,10 +67,12 @@ enum { NF_MATH_FP32 = 0, NF_MATH_TF32 = 1, NF_MATH_FP64 = 2 };
  *   dims[0..n_dims-1] : neurons per layer incl. input and output;
  *                       n_dims >= 2, every dim >= 1.
  *   activation        : "sigmoid" | "tanh" | "relu" | "gaussian" | "step"
- *                       (P:108-109), or "hidden,output" (e.g. "relu,sigmoid")
- *                       to give the output layer its own activation (an
- *                       extension, reading R7).  NULL means "sigmoid", the
- *                       paper's default.  Unknown -> NF_EINVAL.
+ *                        for every layer, or "hidden,output" (e.g.
+ *                       "relu,sigmoid": the output layer its own activation,
+ *                       reading R7), or n_dims-1 comma-separated names, one
+ *                       per layer.  NULL means "sigmoid", the
+ *                       paper's default.  An unknown name or
+ *                       another count of names -> NF_EINVAL.
  *   seed              : initial parameters are drawn on the host from a
  *                       documented splitmix64/Box-Muller stream:
  *                       W ~ N(0,1)/n_{l-1} ("normalized by the number of

@@ -98,7 +98,8 @@ struct HostRng {
 struct nf_net {
   std::vector<int> dims;
   int L = 0;
-  int act_h = 0, act_o = 0;
+  std::vector<int> acts;                 // activation kind of layer l = acts[l], l = 1..L
+  int act_h = 0, act_o = 0;              // acts[1] and acts[L]
   int math = NF_MATH_FP32;
   cudaStream_t stream = nullptr;
   int64_t nparams = 0;
@@ -140,7 +141,7 @@ struct nf_net {
   double *W64(int l) const { return params64 + offW[l]; }
   double *b64(int l) const { return params64 + offB[l]; }
   float *b(int l) const { return params + offB[l]; }
-  int act(int l) const { return l < L ? act_h : act_o; }
+  int act(int l) const { return acts[l]; }
 };
 
 namespace {
@@ -359,12 +360,28 @@ int nf_net_create(const int32_t *dims, int32_t n_dims, const char *activation, u
   if (!dims || n_dims < 2) return fail(NF_EINVAL, "need at least 2 dims (S:118-124)");
   for (int i = 0; i < n_dims; ++i)
     if (dims[i] < 1) return fail(NF_EINVAL, "dims[%d] = %d < 1", i, dims[i]);
-  std::string spec = activation ? activation : "sigmoid";
-  std::string h = spec, o = spec;
-  const size_t comma = spec.find(',');
-  if (comma != std::string::npos) { h = spec.substr(0, comma); o = spec.substr(comma + 1); }
-  const int ah = parse_act(h), ao = parse_act(o);
-  if (ah < 0 || ao < 0) return fail(NF_EINVAL, "unknown activation '%s' (S:32-33)", spec.c_str());
+  // activation spec: one name (every layer), "hidden,output" (R7), or one name per layer
+  const std::string spec = activation ? activation : "sigmoid";
+  std::vector<int> names;
+  for (size_t b = 0;;) {
+    const size_t e = spec.find(',', b);
+    const int k = parse_act(spec.substr(b, e == std::string::npos ? std::string::npos : e - b));
+    if (k < 0) return fail(NF_EINVAL, "unknown activation '%s' (S:32-33)", spec.c_str());
+    names.push_back(k);
+    if (e == std::string::npos) break;
+    b = e + 1;
+  }
+  const int L_ = n_dims - 1;
+  std::vector<int> acts(L_ + 1, 0);  // acts[l], l = 1..L
+  if (names.size() == 1) {
+    for (int l = 1; l <= L_; ++l) acts[l] = names[0];
+  } else if (names.size() == 2) {
+    for (int l = 1; l <= L_; ++l) acts[l] = l < L_ ? names[0] : names[1];
+  } else if ((int)names.size() == L_) {
+    for (int l = 1; l <= L_; ++l) acts[l] = names[l - 1];
+  } else {
+    return fail(NF_EINVAL, "activation spec '%s' needs 1, 2 or %d names", spec.c_str(), L_);
+  }
 
   int ndev = 0;
   if (cudaGetDeviceCount(&ndev) != cudaSuccess || ndev == 0) {
@@ -379,8 +396,9 @@ int nf_net_create(const int32_t *dims, int32_t n_dims, const char *activation, u
   nf_net *net = new nf_net();
   net->dims.assign(dims, dims + n_dims);
   net->L = n_dims - 1;
-  net->act_h = ah;
-  net->act_o = ao;
+  net->acts = acts;
+  net->act_h = acts[1];       // the two-layer kernels (K6, infer_small, single-CTA for L = 2)
+  net->act_o = acts[net->L];
   net->offW.assign(net->L + 1, 0);
   net->offB.assign(net->L + 1, 0);
   int64_t o_ = 0;
@@ -602,7 +620,7 @@ int nf_train_steps(nf_net *net, const float *X, const float *Y, int64_t N, int64
     NF_CUDA(net->d_starts.ensure((size_t)n_steps * sizeof(int64_t)));
     NF_CUDA(cudaMemcpyAsync(net->d_starts.p, st.data(), (size_t)n_steps * sizeof(int64_t), cudaMemcpyHostToDevice,
                             net->stream));
-    const int src = single_cta_train_steps(net->stream, net->dims, net->act_h, net->act_o, net->params, dX, dY,
+    const int src = single_cta_train_steps(net->stream, net->dims, net->acts, net->params, dX, dY,
                                            batch, net->d_starts.as<int64_t>(), n_steps, eta, step_loss);
     if (src == 0) {
       fused_small_invalidate(net->fused);

@@ -268,7 +268,7 @@ bool single_cta_applicable(const std::vector<int> &dims, int64_t batch) {
   return single_layout(dims, batch, p) != 0;
 }
 
-int single_cta_train_steps(cudaStream_t st, const std::vector<int> &dims, int act_h, int act_o, float *params,
+int single_cta_train_steps(cudaStream_t st, const std::vector<int> &dims, const std::vector<int> &acts, float *params,
                            const float *X, const float *Y, int64_t batch, const int64_t *d_starts, int64_t n_steps,
                            float eta, float *step_loss) {
   SingleParams p{};
@@ -278,7 +278,7 @@ int single_cta_train_steps(cudaStream_t st, const std::vector<int> &dims, int ac
   p.X = X; p.Y = Y; p.starts = d_starts; p.n_steps = n_steps; p.B = (int)batch; p.L = L;
   for (int l = 0; l <= L; ++l) {
     p.dims[l] = dims[l];
-    p.act[l] = l < L ? act_h : act_o;
+    p.act[l] = l >= 1 ? acts[l] : 0;
   }
   p.params = params;
   p.scale = (float)((double)eta / (double)batch);

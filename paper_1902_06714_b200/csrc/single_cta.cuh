@@ -16,7 +16,8 @@ constexpr int SINGLE_NOT_APPLICABLE = 1;
 // step.  Returns 0, SINGLE_NOT_APPLICABLE (shape / batch outside the latency regime: the caller
 // uses K6 or the generic kernels), or a cudaError_t value.
 bool single_cta_applicable(const std::vector<int> &dims, int64_t batch);
-int single_cta_train_steps(cudaStream_t st, const std::vector<int> &dims, int act_h, int act_o, float *params,
+// acts[l]: activation kind of layer l (l = 1..L)
+int single_cta_train_steps(cudaStream_t st, const std::vector<int> &dims, const std::vector<int> &acts, float *params,
                            const float *X, const float *Y, int64_t batch, const int64_t *d_starts, int64_t n_steps,
                            float eta, float *step_loss);
 

@@ -104,7 +104,8 @@ def test_null_net_is_rejected_by_every_entry_point(nf):
 
 
 def test_create_rejects_bad_specs_before_the_device(nf):
-    for dims, act in [([3, 5, 2], "relu,softmax"), ([3, 5, 2], "tanh,"), ([2, -1], "sigmoid"), ([], "sigmoid")]:
+    for dims, act in [([3, 5, 2], "relu,softmax"), ([3, 5, 2], "tanh,"), ([2, -1], "sigmoid"), ([], "sigmoid"),
+                      ([3, 5, 4, 2], "relu,tanh,sigmoid,step"), ([3, 5, 4, 2], "relu,,sigmoid")]:
         with pytest.raises(nf.NFError) as e:
             nf.nf_net_create(dims, act)
         assert e.value.code == nf.NF_EINVAL, (dims, act)

@@ -54,6 +54,9 @@ SHAPES = [
     ([40, 1100, 12], "tanh,sigmoid", 300),
     ([64, 256, 16], "sigmoid", 513),
     ([30, 640, 10], "gaussian,sigmoid", 257),
+    # one activation per layer: generic kernels, fused output layer
+    ([20, 50, 40, 30, 6], "tanh,gaussian,sigmoid,tanh", 150),
+    ([24, 130, 96, 10], "sigmoid,tanh,sigmoid", 300),
     # two-layer nets with narrow layers and n0 % 4 == 0: the fused inference kernel
     # (infer_small.cu) with a ragged last 64-row tile and a ragged last pixel chunk
     ([100, 17, 3], "tanh,sigmoid", 777),
@@ -404,6 +407,7 @@ def test_train_single_online_sgd(dims, act):
     ([3, 5, 2], "sigmoid", 8, 100),             # c1's shape
     ([100, 70, 40, 20, 3], "tanh,sigmoid", 5, 30),   # deeper net, thread-per-output layers
     ([64, 130, 9], "gaussian,sigmoid", 3, 25),  # warp-per-element delta (n_l >= 64)
+    ([30, 40, 20, 8], "tanh,gaussian,sigmoid", 4, 20),   # one activation per layer
 ])
 def test_small_batch_single_cta_path(dims, act, batch, steps):
     """nf_train_steps in the latency regime (a few rows per step, parameters in one SM's shared
