@@ -154,6 +154,18 @@ int nf_loss(nf_net *net, const float *x, const float *y, int64_t n, float *loss)
  * n = 0 -> 0.0.  Synchronises. */
 int nf_accuracy(nf_net *net, const float *x, const float *y, int64_t n, float *acc);
 
+/* Saving and loading networks to and from file (the paper gives no format, this
+ * library's is text: a header line "nf-b200-net 1", n_dims, the dims, the activation spec,
+ * then the nf_param_count parameters in the flat layout, one per line, 9 significant digits,
+ * exact for fp32).  nf_save synchronises; NF_EINVAL if the file cannot be written.
+ * Host file I/O; the parameters are read back from the device first. */
+int nf_save(nf_net *net, const char *path);
+
+/* Loads a file written by nf_save: parses the whole file first (NF_EINVAL on a missing file
+ * or a malformed one, before any device work), then nf_net_create + nf_set_params; *out is
+ * owned by the caller (nf_net_destroy).  The numerics mode starts as NF_MATH_FP32. */
+int nf_load(const char *path, nf_net **out);
+
 /* Thread-local text of the last error ("" if none). */
 const char *nf_last_error(void);
 

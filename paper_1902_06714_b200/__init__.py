@@ -52,6 +52,8 @@ def _load() -> ctypes.CDLL:
         "nf_train_steps": (ctypes.c_int, [P, P, P, I64, I64, P, I64, F, P]),
         "nf_grad": (ctypes.c_int, [P, P, P, I64, P]),
         "nf_update": (ctypes.c_int, [P, P, I64, F, I64]),
+        "nf_save": (ctypes.c_int, [P, ctypes.c_char_p]),
+        "nf_load": (ctypes.c_int, [ctypes.c_char_p, ctypes.POINTER(P)]),
         "nf_loss": (ctypes.c_int, [P, P, P, I64, ctypes.POINTER(F)]),
         "nf_accuracy": (ctypes.c_int, [P, P, P, I64, ctypes.POINTER(F)]),
         "nf_last_error": (ctypes.c_char_p, []),
@@ -78,7 +80,7 @@ def lib() -> ctypes.CDLL:
 # Every symbol include/nf.h declares (checked by tests/test_abi.py).
 EXPORTS = ("nf_net_create", "nf_net_destroy", "nf_set_stream", "nf_set_math", "nf_param_count",
            "nf_get_params", "nf_set_params", "nf_output", "nf_train_batch", "nf_train_steps",
-           "nf_grad", "nf_update", "nf_loss", "nf_accuracy", "nf_last_error", "nf_launch_count")
+           "nf_grad", "nf_update", "nf_save", "nf_load", "nf_loss", "nf_accuracy", "nf_last_error", "nf_launch_count")
 
 
 def _check(rc: int):
@@ -155,6 +157,16 @@ def nf_grad(net, x, y, n: int, grad):
 
 def nf_update(net, grad, count: int, eta: float, n: int):
     _check(lib().nf_update(net, _ptr(grad), count, eta, n))
+
+
+def nf_save(net, path: str):
+    _check(lib().nf_save(net, os.fsencode(path)))
+
+
+def nf_load(path: str):
+    h = ctypes.c_void_p()
+    _check(lib().nf_load(os.fsencode(path), ctypes.byref(h)))
+    return h
 
 
 def nf_loss(net, x, y, n: int) -> float:
@@ -245,6 +257,23 @@ class Net:
     def update(self, grad, eta: float, n: int):
         """params -= (eta / n) grad: the paper's update on co_summed tendencies (nf_update)."""
         nf_update(self.h, grad, self.n_params, eta, n)
+
+    def save(self, path: str):
+        """Write the net (dims, activation spec, parameters) to a file (nf_save)."""
+        nf_save(self.h, path)
+
+    @classmethod
+    def load(cls, path: str, stream=None):
+        """A Net from a file written by save() (nf_load)."""
+        net = cls.__new__(cls)
+        net.h = nf_load(path)
+        with open(path) as f:
+            f.readline(); f.readline()
+            net.dims = [int(v) for v in f.readline().split()]
+            net.activation = f.readline().strip()
+        if stream is not None:
+            nf_set_stream(net.h, stream)
+        return net
 
     def loss(self, x, y) -> float:
         return nf_loss(self.h, x, y, x.shape[0])

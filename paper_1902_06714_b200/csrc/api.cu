@@ -99,6 +99,7 @@ struct nf_net {
   std::vector<int> dims;
   int L = 0;
   std::vector<int> acts;                 // activation kind of layer l = acts[l], l = 1..L
+  std::string act_spec;                  // the spec it was created with (nf_save)
   int act_h = 0, act_o = 0;              // acts[1] and acts[L]
   int math = NF_MATH_FP32;
   cudaStream_t stream = nullptr;
@@ -397,6 +398,7 @@ int nf_net_create(const int32_t *dims, int32_t n_dims, const char *activation, u
   net->dims.assign(dims, dims + n_dims);
   net->L = n_dims - 1;
   net->acts = acts;
+  net->act_spec = spec;
   net->act_h = acts[1];       // the two-layer kernels (K6, infer_small, single-CTA for L = 2)
   net->act_o = acts[net->L];
   net->offW.assign(net->L + 1, 0);
@@ -423,6 +425,64 @@ int nf_net_create(const int32_t *dims, int32_t n_dims, const char *activation, u
   }
   net->ws.partial = net->partial.as<float>();
   net->ws.partial_floats = size_t(16) << 20;
+  *out = net;
+  return NF_OK;
+}
+
+// ---- saving and loading networks (the paper's feature list; file format of this
+// library, the paper does not give one): text, "nf-b200-net 1", n_dims, dims, activation
+// spec, then the flat parameters (include/nf.h layout) one per line with 9 significant
+// digits (exact for fp32).
+int nf_save(nf_net *net, const char *path) {
+  if (int rc = check_net(net)) return rc;
+  if (!path) return fail(NF_EINVAL, "path is NULL");
+  std::vector<float> p(net->nparams);
+  if (int rc = nf_get_params(net, p.data(), net->nparams)) return rc;
+  FILE *f = fopen(path, "w");
+  if (!f) return fail(NF_EINVAL, "cannot open '%s' for writing", path);
+  fprintf(f, "nf-b200-net 1\n%d\n", (int)net->dims.size());
+  for (size_t i = 0; i < net->dims.size(); ++i) fprintf(f, "%d%c", net->dims[i], i + 1 < net->dims.size() ? ' ' : '\n');
+  fprintf(f, "%s\n", net->act_spec.c_str());
+  for (float v : p) fprintf(f, "%.9g\n", v);
+  const bool ok = fclose(f) == 0;
+  return ok ? NF_OK : fail(NF_EINVAL, "writing '%s' failed", path);
+}
+
+int nf_load(const char *path, nf_net **out) {
+  if (!out) return fail(NF_EINVAL, "out is NULL");
+  *out = nullptr;
+  if (!path) return fail(NF_EINVAL, "path is NULL");
+  FILE *f = fopen(path, "r");
+  if (!f) return fail(NF_EINVAL, "cannot open '%s'", path);
+  char magic[32] = {0}, spec[256] = {0};
+  int ver = 0, nd = 0;
+  std::vector<int32_t> dims;
+  std::vector<float> p;
+  int rc = NF_OK;
+  if (fscanf(f, "%31s %d %d", magic, &ver, &nd) != 3 || strcmp(magic, "nf-b200-net") != 0 || ver != 1 || nd < 2 ||
+      nd > 1024) {
+    rc = fail(NF_EINVAL, "'%s' is not an nf-b200 network file", path);
+  } else {
+    dims.resize(nd);
+    int64_t np = 0;
+    for (int i = 0; i < nd && rc == NF_OK; ++i)
+      if (fscanf(f, "%d", &dims[i]) != 1 || dims[i] < 1) rc = fail(NF_EINVAL, "'%s': bad dims", path);
+    for (int l = 1; l < nd && rc == NF_OK; ++l) np += (int64_t)dims[l] * dims[l - 1] + dims[l];
+    if (rc == NF_OK && fscanf(f, "%255s", spec) != 1) rc = fail(NF_EINVAL, "'%s': no activation", path);
+    if (rc == NF_OK) {
+      p.resize(np);
+      for (int64_t i = 0; i < np && rc == NF_OK; ++i)
+        if (fscanf(f, "%f", &p[i]) != 1) rc = fail(NF_EINVAL, "'%s': %lld of %lld parameters", path, (long long)i, (long long)np);
+    }
+  }
+  fclose(f);
+  if (rc != NF_OK) return rc;
+  nf_net *net = nullptr;
+  if ((rc = nf_net_create(dims.data(), nd, spec, 0, &net))) return rc;
+  if ((rc = nf_set_params(net, p.data(), (int64_t)p.size()))) {
+    nf_net_destroy(net);
+    return rc;
+  }
   *out = net;
   return NF_OK;
 }

@@ -123,3 +123,22 @@ def test_header_documents_every_entry_point():
         assert m, name
         before = src[:m.start()].rstrip()
         assert before.endswith("*/"), name
+
+
+def test_load_rejects_missing_and_malformed_files_before_the_device(nf, tmp_path):
+    """nf_load parses the whole file before any device work: NF_EINVAL, not NF_ENODEV."""
+    with pytest.raises(nf.NFError) as e:
+        nf.nf_load(str(tmp_path / "missing.net"))
+    assert e.value.code == nf.NF_EINVAL
+    bad = [
+        "not a network\n",
+        "nf-b200-net 1\n3\n3 5 2\nsigmoid\n0.5\n",          # 1 of 32 parameters
+        "nf-b200-net 1\n3\n3 0 2\nsigmoid\n",               # a zero width
+        "nf-b200-net 2\n3\n3 5 2\nsigmoid\n",               # unknown version
+    ]
+    for i, text in enumerate(bad):
+        path = tmp_path / f"bad{i}.net"
+        path.write_text(text)
+        with pytest.raises(nf.NFError) as e:
+            nf.nf_load(str(path))
+        assert e.value.code == nf.NF_EINVAL, text

@@ -424,3 +424,19 @@ def test_small_batch_single_cta_path(dims, act, batch, steps):
     ref, ref_loss = oracle.Oracle(dims, act).train_steps(p, X, Y, batch, starts, 0.5)
     assert rel_err(gpu_params(net), ref) <= FP32_BAR
     assert rel_err(loss.cpu().numpy(), ref_loss) <= FP32_BAR
+
+
+def test_save_load_round_trip(tmp_path):
+    """nf_save / nf_load: the loaded net has the same dims, activations and
+    parameters bit for bit, and computes the same outputs."""
+    dims, act = [37, 45, 20, 13], "tanh,gaussian,sigmoid"
+    p = synth.random_params(81, dims, 0.5)
+    net = make_net(dims, act, p)
+    net.train_batch(dev(synth.random_batch(82, 64, 37, 13)[0]), dev(synth.random_batch(82, 64, 37, 13)[1]), 0.3)
+    path = str(tmp_path / "net.txt")
+    net.save(path)
+    back = nf.Net.load(path)
+    assert back.dims == dims and back.activation == act
+    assert np.array_equal(gpu_params(back), gpu_params(net))
+    x, _ = synth.random_batch(83, 50, 37, 13)
+    assert np.array_equal(back.output(dev(x)).cpu().numpy(), net.output(dev(x)).cpu().numpy())
