@@ -129,6 +129,8 @@ struct nf_net {
   cudaGraphExec_t graph = nullptr;
   std::vector<int64_t> graph_key;
   int64_t graph_kernels = 0;             // kernels in the graph (nf_launch_count on replay)
+  cudaStream_t h2d = nullptr, h2d_y = nullptr;  // copy streams of the host-dataset path
+  cudaEvent_t h2d_ev[6] = {};            // x slot 0/1 filled, slot 0/1 consumed, y slot 0/1 filled
   cudaStream_t cap_stream = nullptr;     // private stream the graph is captured on (the
                                          // caller's stream may be the legacy default stream)
 
@@ -507,6 +509,9 @@ void nf_net_destroy(nf_net *net) {
   fused_small_release(net->fused);
   drop_graph(net);
   if (net->cap_stream) cudaStreamDestroy(net->cap_stream);
+  for (auto e : net->h2d_ev) if (e) cudaEventDestroy(e);
+  if (net->h2d) cudaStreamDestroy(net->h2d);
+  if (net->h2d_y) cudaStreamDestroy(net->h2d_y);
   for (auto e : net->ev) if (e) cudaEventDestroy(e);
   if (net->side) cudaStreamDestroy(net->side);
   net->partial2.release();
@@ -637,44 +642,13 @@ int nf_train_batch(nf_net *net, const float *x, const float *y, int64_t n, float
   return rc;
 }
 
-int nf_train_steps(nf_net *net, const float *X, const float *Y, int64_t N, int64_t batch,
-                   const int64_t *starts, int64_t n_steps, float eta, float *step_loss) {
-  if (int rc = check_net(net)) return rc;
-  if (batch <= 0 || N < batch) return fail(NF_EINVAL, "need 1 <= batch <= N");
-  if (n_steps < 0) return fail(NF_EINVAL, "n_steps < 0");
-  if (n_steps == 0) return NF_OK;
-  if (!std::isfinite(eta)) return fail(NF_EINVAL, "eta is not finite");
-  if (int rc = check_ptr(X, "X")) return rc;
-  if (int rc = check_ptr(Y, "Y")) return rc;
-  if (!starts) return fail(NF_EINVAL, "starts is NULL");
-  if (is_device_ptr(starts)) return fail(NF_EINVAL, "starts must be a host array");
-  for (int64_t s = 0; s < n_steps; ++s)
-    if (starts[s] < 0 || starts[s] + batch > N)
-      return fail(NF_EINVAL, "starts[%lld] = %lld outside [0, N-batch]", (long long)s, (long long)starts[s]);
-  if (step_loss && !is_device_ptr(step_loss)) return fail(NF_EINVAL, "step_loss must be a device array");
+// The training steps on device-resident data: the single-CTA latency kernel, K6, or the
+// generic per-layer kernels (CUDA graph).  st: the steps' first rows in dX / dY (host array).
+static int train_steps_device(nf_net *net, const float *dX, const float *dY, int64_t N, int64_t batch,
+                              std::vector<int64_t> &st, int64_t n_steps, float eta, float *step_loss,
+                              bool allow_graph) {
   const int n0 = net->dims[0], nL = net->dims[net->L];
-
-  // Host dataset: gather each step's batch into device staging (one H2D copy
-  // per step, the e2e path) and renumber the starts.
-  const bool host_in = !is_device_ptr(X) || !is_device_ptr(Y);
-  std::vector<int64_t> st(starts, starts + n_steps);
-  const float *dX = X, *dY = Y;
-  int64_t dN = N;
-  if (host_in) {
-    NF_CUDA(net->stage_x.ensure((size_t)n_steps * batch * n0 * sizeof(float)));
-    NF_CUDA(net->stage_y.ensure((size_t)n_steps * batch * nL * sizeof(float)));
-    for (int64_t s = 0; s < n_steps; ++s) {
-      NF_CUDA(cudaMemcpyAsync(net->stage_x.as<float>() + s * batch * n0, X + starts[s] * n0,
-                              (size_t)batch * n0 * sizeof(float), cudaMemcpyHostToDevice, net->stream));
-      NF_CUDA(cudaMemcpyAsync(net->stage_y.as<float>() + s * batch * nL, Y + starts[s] * nL,
-                              (size_t)batch * nL * sizeof(float), cudaMemcpyHostToDevice, net->stream));
-      st[s] = s * batch;
-    }
-    dX = net->stage_x.as<float>();
-    dY = net->stage_y.as<float>();
-    dN = n_steps * batch;
-  }
-
+  const int64_t dN = N;
   // Latency regime (a few rows per step, parameters fit one SM): the single-CTA kernel
   if (net->math != NF_MATH_FP64 && single_cta_applicable(net->dims, batch)) {
     NF_CUDA(net->d_starts.ensure((size_t)n_steps * sizeof(int64_t)));
@@ -684,7 +658,6 @@ int nf_train_steps(nf_net *net, const float *X, const float *Y, int64_t N, int64
                                            batch, net->d_starts.as<int64_t>(), n_steps, eta, step_loss);
     if (src == 0) {
       fused_small_invalidate(net->fused);
-      if (host_in) NF_CUDA(cudaStreamSynchronize(net->stream));
       return NF_OK;
     }
     if (src != SINGLE_NOT_APPLICABLE)
@@ -706,7 +679,7 @@ int nf_train_steps(nf_net *net, const float *X, const float *Y, int64_t N, int64
     memcpy(&eb, &eta, 4);
     key.push_back(eb);
     key.insert(key.end(), st.begin(), st.end());
-    const bool use_graph = !host_in && getenv("NF_NO_GRAPH") == nullptr;
+    const bool use_graph = allow_graph && getenv("NF_NO_GRAPH") == nullptr;
     if (use_graph && net->graph && key == net->graph_key) {
       NF_CUDA(cudaGraphLaunch(net->graph, net->stream));
       count_launch((int)net->graph_kernels);
@@ -747,7 +720,74 @@ int nf_train_steps(nf_net *net, const float *X, const float *Y, int64_t N, int64
   } else if (rc != 0) {
     return fail(NF_ECUDA, "fused small-net kernel: %s", fused_small_error());
   }
-  if (host_in) NF_CUDA(cudaStreamSynchronize(net->stream));
+  return NF_OK;
+}
+
+
+int nf_train_steps(nf_net *net, const float *X, const float *Y, int64_t N, int64_t batch,
+                   const int64_t *starts, int64_t n_steps, float eta, float *step_loss) {
+  if (int rc = check_net(net)) return rc;
+  if (batch <= 0 || N < batch) return fail(NF_EINVAL, "need 1 <= batch <= N");
+  if (n_steps < 0) return fail(NF_EINVAL, "n_steps < 0");
+  if (n_steps == 0) return NF_OK;
+  if (!std::isfinite(eta)) return fail(NF_EINVAL, "eta is not finite");
+  if (int rc = check_ptr(X, "X")) return rc;
+  if (int rc = check_ptr(Y, "Y")) return rc;
+  if (!starts) return fail(NF_EINVAL, "starts is NULL");
+  if (is_device_ptr(starts)) return fail(NF_EINVAL, "starts must be a host array");
+  for (int64_t s = 0; s < n_steps; ++s)
+    if (starts[s] < 0 || starts[s] + batch > N)
+      return fail(NF_EINVAL, "starts[%lld] = %lld outside [0, N-batch]", (long long)s, (long long)starts[s]);
+  if (step_loss && !is_device_ptr(step_loss)) return fail(NF_EINVAL, "step_loss must be a device array");
+  const int n0 = net->dims[0], nL = net->dims[net->L];
+
+  // Device dataset: the steps run straight from it.
+  const bool host_in = !is_device_ptr(X) || !is_device_ptr(Y);
+  if (!host_in) {
+    std::vector<int64_t> st(starts, starts + n_steps);
+    return train_steps_device(net, X, Y, N, batch, st, n_steps, eta, step_loss, true);
+  }
+  // Host dataset (the e2e path): each step's batch is copied host -> device (one copy of its
+  // x rows and one of its y rows), in chunks of steps through two staging slots on a copy
+  // stream, so that the copies of chunk c+1 overlap the training of chunk c.
+  const int64_t row_f = n0 + nL;
+  static const int64_t chunk_mb = getenv("NF_H2D_CHUNK_MB") ? atoi(getenv("NF_H2D_CHUNK_MB")) : 16;
+  static const bool y_stream = getenv("NF_H2D_Y_STREAM") != nullptr;
+  const int64_t chunk = std::max<int64_t>(1, std::min<int64_t>(n_steps, (chunk_mb << 20) / (batch * row_f * 4)));
+  cudaStream_t ys = y_stream ? net->h2d_y : net->h2d;
+  const int64_t slot_f = chunk * batch * row_f;
+  NF_CUDA(net->stage_x.ensure((size_t)(2 * slot_f) * sizeof(float)));
+  if (!net->h2d) {
+    NF_CUDA(cudaStreamCreateWithFlags(&net->h2d, cudaStreamNonBlocking));
+    NF_CUDA(cudaStreamCreateWithFlags(&net->h2d_y, cudaStreamNonBlocking));
+    for (auto &e : net->h2d_ev) NF_CUDA(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
+  }
+  NF_CUDA(cudaEventRecord(net->h2d_ev[2], net->stream));  // the caller's prior work on the net
+  NF_CUDA(cudaEventRecord(net->h2d_ev[3], net->stream));
+  for (int64_t c0 = 0, ci = 0; c0 < n_steps; c0 += chunk, ++ci) {
+    const int slot = (int)(ci & 1);
+    const int64_t m = std::min(chunk, n_steps - c0);
+    float *sx = net->stage_x.as<float>() + slot * slot_f, *sy = sx + chunk * batch * n0;
+    NF_CUDA(cudaStreamWaitEvent(net->h2d, net->h2d_ev[2 + slot], 0));  // slot free again
+    NF_CUDA(cudaStreamWaitEvent(net->h2d_y, net->h2d_ev[2 + slot], 0));
+    std::vector<int64_t> st(m);
+    for (int64_t s = 0; s < m; ++s) {  // x rows and y rows on two copy streams (two engines)
+      NF_CUDA(cudaMemcpyAsync(sx + s * batch * n0, X + starts[c0 + s] * n0, (size_t)batch * n0 * sizeof(float),
+                              cudaMemcpyDefault, net->h2d));
+      NF_CUDA(cudaMemcpyAsync(sy + s * batch * nL, Y + starts[c0 + s] * nL, (size_t)batch * nL * sizeof(float),
+                              cudaMemcpyDefault, ys));
+      st[s] = s * batch;
+    }
+    NF_CUDA(cudaEventRecord(net->h2d_ev[slot], net->h2d));            // slot filled
+    NF_CUDA(cudaEventRecord(net->h2d_ev[4 + slot], ys));
+    NF_CUDA(cudaStreamWaitEvent(net->stream, net->h2d_ev[slot], 0));
+    NF_CUDA(cudaStreamWaitEvent(net->stream, net->h2d_ev[4 + slot], 0));
+    int rc = train_steps_device(net, sx, sy, m * batch, batch, st, m, eta, step_loss ? step_loss + c0 : nullptr,
+                                false);
+    if (rc) return rc;
+    NF_CUDA(cudaEventRecord(net->h2d_ev[2 + slot], net->stream));     // slot consumed
+  }
+  NF_CUDA(cudaStreamSynchronize(net->stream));
   return NF_OK;
 }
 

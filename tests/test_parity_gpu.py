@@ -440,3 +440,25 @@ def test_save_load_round_trip(tmp_path):
     assert np.array_equal(gpu_params(back), gpu_params(net))
     x, _ = synth.random_batch(83, 50, 37, 13)
     assert np.array_equal(back.output(dev(x)).cpu().numpy(), net.output(dev(x)).cpu().numpy())
+
+
+@pytest.mark.parametrize("dims,act,batch,steps", [
+    ([784, 30, 10], "sigmoid", 1000, 45),        # K6; 20-step chunks of the staging pipeline
+    ([200, 136, 72, 5], "tanh,sigmoid", 128, 7),  # generic kernels
+])
+def test_train_steps_from_host_dataset(dims, act, batch, steps):
+    """nf_train_steps with the dataset in (pinned) host memory: each step's rows are copied in
+    chunks overlapped with the training of the previous chunk; same result and per-step costs
+    as the device-resident dataset (within the L2-reduction ordering of R12)."""
+    p = synth.random_params(91, dims, 0.3)
+    X, Y = synth.random_batch(92, 3 * batch, dims[0], dims[-1], "uniform")
+    rng = np.random.default_rng(93)
+    starts = rng.integers(0, 2 * batch + 1, size=steps)
+    a, b = make_net(dims, act, p), make_net(dims, act, p)
+    la, lb = torch.zeros(steps, device="cuda"), torch.zeros(steps, device="cuda")
+    a.train_steps(torch.from_numpy(X).pin_memory(), torch.from_numpy(Y).pin_memory(), batch, starts, 0.5, step_loss=la)
+    b.train_steps(dev(X), dev(Y), batch, starts, 0.5, step_loss=lb)
+    assert rel_err(gpu_params(a), gpu_params(b)) <= 1e-5
+    assert rel_err(la.cpu().numpy(), lb.cpu().numpy()) <= 1e-5
+    ref, ref_loss = oracle.Oracle(dims, act).train_steps(p, X, Y, batch, starts, 0.5)
+    assert rel_err(gpu_params(a), ref) <= FP32_BAR
