@@ -160,10 +160,31 @@ def run_cpu_oracle(cid, steps, batch=None, bits=32, X=None, Y=None):
     o = oracle.Oracle(cfg["dims"], cfg["act"], bits=bits)
     p = synth.init_params(cid)
     o.train_steps(p, X, Y, batch, starts[:1], cfg["eta"])  # page in
-    t0 = time.perf_counter()
-    o.train_steps(p, X, Y, batch, starts, cfg["eta"])
-    dt = time.perf_counter() - t0
+    # one core (the calling thread pinned to the first CPU it may use), as SURVEY 8(d) plans
+    old = os.sched_getaffinity(0) if hasattr(os, "sched_getaffinity") else None
+    if old:
+        os.sched_setaffinity(0, {min(old)})
+    try:
+        t0 = time.perf_counter()
+        o.train_steps(p, X, Y, batch, starts, cfg["eta"])
+        dt = time.perf_counter() - t0
+    finally:
+        if old:
+            os.sched_setaffinity(0, old)
     return steps * batch / dt, dt, batch
+
+
+def host_cpu():
+    """Host CPU model and logical core count (the oracle baseline's hardware)."""
+    model = "unknown"
+    try:
+        for line in open("/proc/cpuinfo"):
+            if line.startswith("model name"):
+                model = line.split(":", 1)[1].strip()
+                break
+    except OSError:
+        pass
+    return {"model": model, "logical_cores": os.cpu_count()}
 
 
 def reference_arm(args):
@@ -195,7 +216,7 @@ def reference_arm(args):
         "ms_per_step": dt * 1e3 / args.steps, "higher_is_better": True, "scaling": "weak",
         "vs_baseline": None, "dtype": "f32", "data": "synthetic",
         "config": {"workload": cfg["name"], "dims": cfg["dims"], "batch": cfg["batch"]},
-        "cpu_baseline": {"value": v, "unit": "samples/s", "cores": 1, "kind": "oracle",
+        "cpu_baseline": {"value": v, "unit": "samples/s", "cores": 1, "kind": "oracle", "host": host_cpu(),
                          "sample": f"{args.steps} SGD steps of {rows} rows (config batch {cfg['batch']}) of "
                                    f"{cfg['name']}, fp32 build of oracle/nf_oracle.c, single thread"},
         "e2e": {"value": v, "unit": "samples/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
@@ -355,7 +376,7 @@ def main():
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
         cpu_steps, cpu_rows = CPU_SAMPLE[cid]
         v, dt, rows = run_cpu_oracle(cid, cpu_steps, cpu_rows, X=X, Y=Y)
-        cpu = {"value": v, "unit": "samples/s", "cores": 1, "kind": "oracle",
+        cpu = {"value": v, "unit": "samples/s", "cores": 1, "kind": "oracle", "host": host_cpu(),
                "sample": f"{cpu_steps} SGD steps of {rows} rows of {cfg['name']} ({dt:.1f} s), fp32 build of "
                          f"oracle/nf_oracle.c, single thread"}
 
