@@ -56,8 +56,14 @@ constexpr int kMinBlocks = NF_FUSED_MINB;  // CTAs per SM the kernel is built fo
 constexpr int kWarps = kThreads / 32;
 constexpr int kMaxC = 8;       // cluster size
 constexpr int kMaxRows = 128;  // rows per cluster
-constexpr int kRG = 5;         // rows per P1 register tile
-constexpr int kKP = 4;         // P1: K (pixel) range split in kKP parts across threads
+#ifndef NF_KRG
+#define NF_KRG 5
+#endif
+#ifndef NF_KKP
+#define NF_KKP 4
+#endif
+constexpr int kRG = NF_KRG;    // rows per P1 register tile
+constexpr int kKP = NF_KKP;    // P1: K (pixel) range split in kKP parts across threads
 constexpr int kRH = 2;         // P5: rows split in kRH parts across threads
 constexpr int kProf = 16;      // profiler slots per step
 // Tensor-core variant (TC): x tiles of kTcRows rows x 4 atoms of 32 pixels, staged twice per
