@@ -63,8 +63,11 @@ struct Cfg {
   // the epilogue sums them in fp32.  The tensor core's fp32 accumulation truncates
   // (measured error linear in K, micro/tc_major_test.cu); spreading the K-steps over
   // NACC accumulators divides that error by NACC.
-  static constexpr int NACC = 512 / BN;
-  static constexpr int TMEM_COLS = 512;
+  // 1xTF32 (SPLIT = 1): the operands' TF32 rounding dominates, one accumulator suffices, and
+  // allocating only BN columns lets the next kernel's CTA (programmatic dependent launch)
+  // take its TMEM while this one drains.
+  static constexpr int NACC = SPLIT == 3 ? 512 / BN : 1;
+  static constexpr int TMEM_COLS = SPLIT == 3 ? 512 : (BN < 32 ? 32 : BN);
   static constexpr int SMEM = STAGES * STAGE_BYTES + kEpiBytes + 1024 /*align*/ + 512 /*barriers*/;
   static_assert(STAGES >= 2, "ring too shallow");
 };
