@@ -15,11 +15,18 @@
 namespace nf {
 namespace {
 
-constexpr int kT = 256;
+#ifndef NF_INFER_T
+#define NF_INFER_T 256
+#endif
+#ifndef NF_INFER_S
+#define NF_INFER_S 4
+#endif
+constexpr int kT = NF_INFER_T;
+constexpr int kKH = kT / 128;  // pixel parts of a chunk (tasks: 8 neuron groups x 16 row groups x kKH)
 constexpr int kRows = 64;      // rows per tile
 constexpr int kKC = 64;        // pixels per staged chunk
 constexpr int kXs = kKC + 4;   // padded smem row (floats)
-constexpr int kS = 4;          // x chunk ring depth (prefetch distance 3 chunks, across tiles)
+constexpr int kS = NF_INFER_S;  // x chunk ring depth (prefetch distance kS - 1 chunks, across tiles)
 
 __device__ __forceinline__ void cp_async16(float *dst, const float *src) {
   asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"((uint32_t)__cvta_generic_to_shared(dst)), "l"(src)
@@ -40,13 +47,26 @@ infer_small_kernel(const float *__restrict__ X, int64_t n, int n0, int H, int O,
   float *b2s = b1s + 32;                  // [32]
   float *xs = b2s + 32;                   // kS x [kRows][kXs]
   float *a1s = xs + kS * kRows * kXs;     // [kRows][33]
+  float *a1p = a1s + kRows * 33;          // (kKH - 1) x [kRows][33] partial Z1 of pixel parts 1..
   const int tid = threadIdx.x;
   const float *W1 = params, *b1 = params + (int64_t)H * n0, *W2 = b1 + H, *b2 = W2 + O * H;
 
-  for (int i = tid; i < n0p * 32; i += kT) {
-    const int k = i >> 5, j = i & 31;
-    W1t[i] = (j < H && k < n0) ? W1[(int64_t)j * n0 + k] : 0.0f;
+  {  // W1 [H][n0] -> W1t [n0p][32]: a warp per 32-pixel block; coalesced row reads (lane =
+     // pixel) into a padded 32 x 33 tile (in the not yet used x ring), then coalesced
+     // transposed writes (lane = neuron), conflict-free on both sides
+    const int lane = tid & 31, warp = tid >> 5;
+    float *tile = xs + warp * 32 * 33;
+    for (int k0 = warp * 32; k0 < n0p; k0 += (kT / 32) * 32) {
+      const int k = k0 + lane;
+#pragma unroll 8
+      for (int j = 0; j < 32; ++j) tile[j * 33 + lane] = (j < H && k < n0) ? W1[(int64_t)j * n0 + k] : 0.0f;
+      __syncwarp();
+#pragma unroll 8
+      for (int kk = 0; kk < 32; ++kk) W1t[(k0 + kk) * 32 + lane] = tile[lane * 33 + kk];
+      __syncwarp();
+    }
   }
+  __syncthreads();  // the x ring is reused below
   for (int i = tid; i < 32 * 33; i += kT) {
     const int o = i / 33, j = i % 33;
     W2s[i] = (o < O && j < H) ? W2[o * H + j] : 0.0f;
@@ -56,7 +76,7 @@ infer_small_kernel(const float *__restrict__ X, int64_t n, int n0, int H, int O,
     b2s[tid] = tid < O ? b2[tid] : 0.0f;
   }
 
-  // Z1 task (256 = 8 neuron groups x 16 row groups x 2 pixel halves): neurons 4 jg .. 4 jg + 3,
+  // Z1 task (kT = 8 neuron groups x 16 row groups x kKH pixel parts): neurons 4 jg .. 4 jg + 3,
   // rows rgrp + 16 u (u < 4; interleaved so a warp's 4 row groups hit distinct banks)
   const int jg = tid & 7, rg = tid >> 3;
   const int rgrp = rg & 15, kh = rg >> 4;
@@ -65,40 +85,46 @@ infer_small_kernel(const float *__restrict__ X, int64_t n, int n0, int H, int O,
   // this CTA's stream of (tile, chunk) pairs: t -> tile blockIdx.x + (t / nchunk) * gridDim.x
   const int64_t my_tiles = ntiles > blockIdx.x ? (ntiles - 1 - blockIdx.x) / gridDim.x + 1 : 0;
   const int64_t T = my_tiles * nchunk;
-  auto stage = [&](int64_t t) {  // always commits a group (empty past the end) for uniform counting
-    if (t < T) {
-      const int64_t tile = blockIdx.x + (t / nchunk) * (int64_t)gridDim.x;
-      const int c = (int)(t % nchunk);
-      const int64_t r0 = tile * kRows;
-      float *dst = xs + (int)(t % kS) * kRows * kXs;
+  // staging cursor (chunk, tile row, ring slot) advanced incrementally: no 64-bit divisions
+  int s_c = 0, s_slot = 0;
+  int64_t s_r0 = (int64_t)blockIdx.x * kRows, s_t = 0;
+  auto stage = [&]() {  // stages the next (tile, chunk); always commits a group (uniform counting)
+    if (s_t < T) {
+      float *dst = xs + s_slot * kRows * kXs;
+#pragma unroll
       for (int i = tid; i < kRows * (kKC / 4); i += kT) {
-        const int r = i / (kKC / 4), q = i % (kKC / 4);
-        const int k = c * kKC + q * 4;
-        const int64_t row = r0 + r;
+        const int r = i >> 4, q = i & 15;  // kKC / 4 = 16 float4 per row
+        const int k = s_c * kKC + q * 4;
+        const int64_t row = s_r0 + r;
         float *d = dst + r * kXs + q * 4;
         if (row < n && k < n0) cp_async16(d, X + row * n0 + k);
         else *reinterpret_cast<float4 *>(d) = make_float4(0.f, 0.f, 0.f, 0.f);
       }
     }
     cp_commit();
+    ++s_t;
+    s_slot = s_slot + 1 == kS ? 0 : s_slot + 1;
+    if (++s_c == nchunk) { s_c = 0; s_r0 += (int64_t)gridDim.x * kRows; }
   };
+  static_assert(kKC / 4 == 16, "stage() indexes 16 float4 per row");
 
   __syncthreads();  // parameters staged
-  for (int64_t t = 0; t < kS - 1; ++t) stage(t);
+  for (int t = 0; t < kS - 1; ++t) stage();
   float2 acc[4][2];
+  int c = 0, slot = 0;
+  int64_t r0 = (int64_t)blockIdx.x * kRows;
   for (int64_t t = 0; t < T; ++t) {
-    const int c = (int)(t % nchunk);
     if (c == 0) {
 #pragma unroll
       for (int u = 0; u < 4; ++u) acc[u][0] = acc[u][1] = make_float2(0.f, 0.f);
     }
-    stage(t + kS - 1);
+    stage();
     cp_wait_ring();   // chunk t has landed (this thread's copies)
     __syncthreads();  // ... and everyone's
     {
-      const float *xb = xs + (int)(t % kS) * kRows * kXs + rgrp * kXs;
+      const float *xb = xs + slot * kRows * kXs + rgrp * kXs;
       const float *wb = W1t + (c * kKC) * 32 + jg * 4;
-      const int q0 = kh * (kKC / 8), q1 = q0 + kKC / 8;  // this thread's half of the chunk (float4 units)
+      const int q0 = kh * (kKC / 4 / kKH), q1 = q0 + kKC / 4 / kKH;  // this thread's part (float4 units)
 #pragma unroll 2
       for (int q = q0; q < q1; ++q) {
         float4 xv[4], wv[4];
@@ -107,23 +133,22 @@ infer_small_kernel(const float *__restrict__ X, int64_t n, int n0, int H, int O,
 #pragma unroll
         for (int v = 0; v < 4; ++v) wv[v] = *reinterpret_cast<const float4 *>(wb + (4 * q + v) * 32);
 #pragma unroll
-        for (int u = 0; u < 4; ++u) {
-          const float xq[4] = {xv[u].x, xv[u].y, xv[u].z, xv[u].w};
-#pragma unroll
-          for (int v = 0; v < 4; ++v) {
-            ffma2(acc[u][0], xq[v], make_float2(wv[v].x, wv[v].y));
-            ffma2(acc[u][1], xq[v], make_float2(wv[v].z, wv[v].w));
+        for (int v = 0; v < 4; ++v) {  // pixel outer: 8 independent accumulators between the
+#pragma unroll                          // dependent updates of each (FFMA2 latency hidden)
+          for (int u = 0; u < 4; ++u) {
+            const float xq = v == 0 ? xv[u].x : v == 1 ? xv[u].y : v == 2 ? xv[u].z : xv[u].w;
+            ffma2(acc[u][0], xq, make_float2(wv[v].x, wv[v].y));
+            ffma2(acc[u][1], xq, make_float2(wv[v].z, wv[v].w));
           }
         }
       }
     }
     if (c == nchunk - 1) {
-      const int64_t r0 = (blockIdx.x + (t / nchunk) * (int64_t)gridDim.x) * kRows;
-      // combine the two pixel halves through shared memory, then the layer-1 activation
-      if (kh == 1) {
+      // combine the pixel parts through shared memory (in part order), then the activation
+      if (kh >= 1) {
 #pragma unroll
         for (int u = 0; u < 4; ++u) {
-          float *d = a1s + (rgrp + 16 * u) * 33 + jg * 4;
+          float *d = a1p + (kh - 1) * kRows * 33 + (rgrp + 16 * u) * 33 + jg * 4;
           d[0] = acc[u][0].x; d[1] = acc[u][0].y; d[2] = acc[u][1].x; d[3] = acc[u][1].y;
         }
       }
@@ -132,7 +157,12 @@ infer_small_kernel(const float *__restrict__ X, int64_t n, int n0, int H, int O,
 #pragma unroll
         for (int u = 0; u < 4; ++u) {
           float *d = a1s + (rgrp + 16 * u) * 33 + jg * 4;
-          const float z[4] = {acc[u][0].x + d[0], acc[u][0].y + d[1], acc[u][1].x + d[2], acc[u][1].y + d[3]};
+          float z[4] = {acc[u][0].x, acc[u][0].y, acc[u][1].x, acc[u][1].y};
+#pragma unroll
+          for (int part = 0; part < kKH - 1; ++part) {
+            const float *e = a1p + part * kRows * 33 + (rgrp + 16 * u) * 33 + jg * 4;
+            z[0] += e[0]; z[1] += e[1]; z[2] += e[2]; z[3] += e[3];
+          }
 #pragma unroll
           for (int v = 0; v < 4; ++v) {
             const int j = jg * 4 + v;
@@ -157,6 +187,8 @@ infer_small_kernel(const float *__restrict__ X, int64_t n, int n0, int H, int O,
       }
     }
     __syncthreads();  // chunk t's buffer is refilled by stage(t + kS) next iteration
+    slot = slot + 1 == kS ? 0 : slot + 1;
+    if (++c == nchunk) { c = 0; r0 += (int64_t)gridDim.x * kRows; }
   }
   cp_wait_ring();
 }
@@ -170,7 +202,7 @@ bool infer_small_applicable(const std::vector<int> &dims, const float *X) {
 
 size_t infer_small_smem(int n0) {
   const int n0p = (n0 + kKC - 1) / kKC * kKC;
-  return sizeof(float) * ((size_t)n0p * 32 + 32 * 33 + 64 + kS * kRows * kXs + kRows * 33);
+  return sizeof(float) * ((size_t)n0p * 32 + 32 * 33 + 64 + kS * kRows * kXs + kKH * kRows * 33);
 }
 
 cudaError_t infer_small(cudaStream_t st, const std::vector<int> &dims, int act_h, int act_o, const float *params,
