@@ -24,7 +24,10 @@ namespace {
 constexpr int kT = NF_INFER_T;
 constexpr int kKH = kT / 128;  // pixel parts of a chunk (tasks: 8 neuron groups x 16 row groups x kKH)
 constexpr int kRows = 64;      // rows per tile
-constexpr int kKC = 64;        // pixels per staged chunk
+#ifndef NF_INFER_KC
+#define NF_INFER_KC 64
+#endif
+constexpr int kKC = NF_INFER_KC;        // pixels per staged chunk
 constexpr int kXs = kKC + 4;   // padded smem row (floats)
 constexpr int kS = NF_INFER_S;  // x chunk ring depth (prefetch distance kS - 1 chunks, across tiles)
 
@@ -93,7 +96,7 @@ infer_small_kernel(const float *__restrict__ X, int64_t n, int n0, int H, int O,
       float *dst = xs + s_slot * kRows * kXs;
 #pragma unroll
       for (int i = tid; i < kRows * (kKC / 4); i += kT) {
-        const int r = i >> 4, q = i & 15;  // kKC / 4 = 16 float4 per row
+        const int r = i / (kKC / 4), q = i % (kKC / 4);  // (powers of two: shifts)
         const int k = s_c * kKC + q * 4;
         const int64_t row = s_r0 + r;
         float *d = dst + r * kXs + q * 4;
@@ -106,7 +109,7 @@ infer_small_kernel(const float *__restrict__ X, int64_t n, int n0, int H, int O,
     s_slot = s_slot + 1 == kS ? 0 : s_slot + 1;
     if (++s_c == nchunk) { s_c = 0; s_r0 += (int64_t)gridDim.x * kRows; }
   };
-  static_assert(kKC / 4 == 16, "stage() indexes 16 float4 per row");
+  static_assert((kKC & (kKC - 1)) == 0, "kKC: a power of two");
 
   __syncthreads();  // parameters staged
   for (int t = 0; t < kS - 1; ++t) stage();
