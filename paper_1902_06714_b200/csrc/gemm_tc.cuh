@@ -51,14 +51,14 @@ constexpr int kThreads = 64 + 32 * kEpiWarps;  // + TMA producer warp + MMA warp
 constexpr int kSmemBudget = 232448; // max dynamic shared memory per CTA on sm_100
 constexpr int kEpiBytes = kEpiWarps * 32 * 33 * 4;
 
-template <int BN, int SPLIT>
+template <int BN, int SPLIT, int MAXST = 6>
 struct Cfg {
   static constexpr int A_BYTES = BM * BK * 4;
   static constexpr int B_BYTES = BN * BK * 4;
   static constexpr int RAW_BYTES = A_BYTES + B_BYTES;
   static constexpr int STAGE_BYTES = SPLIT == 3 ? 2 * RAW_BYTES : RAW_BYTES;  // raw(hi) | lo
   static constexpr int STAGES_FIT = (kSmemBudget - kEpiBytes - 1024 - 512) / STAGE_BYTES;
-  static constexpr int STAGES = STAGES_FIT > 6 ? 6 : STAGES_FIT;
+  static constexpr int STAGES = STAGES_FIT > MAXST ? MAXST : STAGES_FIT;
   // NACC accumulators (all 512 TMEM columns): K-step t accumulates into t % NACC, and
   // the epilogue sums them in fp32.  The tensor core's fp32 accumulation truncates
   // (measured error linear in K, micro/tc_major_test.cu); spreading the K-steps over
@@ -147,11 +147,13 @@ struct TileArgs {
 };
 
 // ---- the kernel ------------------------------------------------------------------------
-template <int BN, bool A_MN, bool B_MN, int SPLIT, class Epi>
+// MAXST < 6: a shallower ring (less shared memory) so that two CTAs co-reside on an SM and
+// one's epilogue overlaps the other's main loop
+template <int BN, bool A_MN, bool B_MN, int SPLIT, class Epi, int MAXST = 6>
 __global__ void __launch_bounds__(kThreads, 1)
 gemm_tc_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB, TileArgs g,
                Epi epi) {
-  using C = Cfg<BN, SPLIT>;
+  using C = Cfg<BN, SPLIT, MAXST>;
   ptx::pdl_trigger();
   extern __shared__ uint8_t smem_raw[];
   uint8_t *smem = reinterpret_cast<uint8_t *>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));

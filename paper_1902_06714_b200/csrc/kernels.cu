@@ -126,11 +126,11 @@ bool make_map(CUtensorMap *m, const TcOp &o, int rows, int K, int box_rows) {
                             CU_TENSOR_MAP_SWIZZLE_128B);
 }
 
-template <int BN, bool AMN, bool BMN, int SPLIT, class Epi>
+template <int BN, bool AMN, bool BMN, int SPLIT, class Epi, int MAXST = 6>
 cudaError_t launch_tc(cudaStream_t st, int M, int N, int K, const TcOp &a, const TcOp &b, const Epi &epi,
                       const Workspace &ws) {
-  using C = tc::Cfg<BN, SPLIT>;
-  auto kern = tc::gemm_tc_kernel<BN, AMN, BMN, SPLIT, Epi>;
+  using C = tc::Cfg<BN, SPLIT, MAXST>;
+  auto kern = tc::gemm_tc_kernel<BN, AMN, BMN, SPLIT, Epi, MAXST>;
   static bool attr = false;
   if (!attr) {
     cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, C::SMEM);
@@ -201,6 +201,9 @@ cudaError_t run_tc(cudaStream_t st, int M, int N, int K, const TcOp &a, const Tc
     g_last_engine = ENGINE_TC1;
     if (N > 128 && tiles(256) > kSMs && getenv("NF_TC_NO_PERSISTENT") == nullptr)
       return launch_tc_persistent<AMN, BMN>(st, M, N, K, a, b, epi);
+    static const bool dual = getenv("NF_TC_DUAL") != nullptr;  // experiment: 2 CTAs per SM
+    if (dual && N > 64 && tiles(128) >= fill && tiles(128) <= 2 * kSMs)
+      return launch_tc<128, AMN, BMN, 1, Epi, 2>(st, M, N, K, a, b, epi, ws);
     if (N > 128 && tiles(256) >= fill) return launch_tc<256, AMN, BMN, 1>(st, M, N, K, a, b, epi, ws);
     // under one wave of 128x256 tiles but deep (the c3 weight gradients, 1024 x 1024 x 4096):
     // keep the wide tile and split K so that tiles x splits fills the GPU in one wave
