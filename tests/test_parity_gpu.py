@@ -462,3 +462,24 @@ def test_train_steps_from_host_dataset(dims, act, batch, steps):
     assert rel_err(la.cpu().numpy(), lb.cpu().numpy()) <= 1e-5
     ref, ref_loss = oracle.Oracle(dims, act).train_steps(p, X, Y, batch, starts, 0.5)
     assert rel_err(gpu_params(a), ref) <= FP32_BAR
+
+
+@pytest.mark.parametrize("dims,act", [([20, 50, 5], "tanh,sigmoid"), ([784, 30, 10], "sigmoid")])
+def test_eval_over_several_chunks(dims, act):
+    """nf_output / nf_loss / nf_accuracy over 70,001 rows: more than two 32,768-row evaluation
+    chunks with a ragged last one (generic K1 chain and the fused inference kernel); sampled
+    outputs against the oracle, loss and accuracy against the oracle on all rows."""
+    n = 70001
+    p = synth.random_params(95, dims, 0.5)
+    X, Y = synth.random_batch(96, n, dims[0], dims[-1], "uniform")
+    net = make_net(dims, act, p)
+    o = oracle.Oracle(dims, act)
+    out = net.output(dev(X)).cpu().numpy()
+    rows = np.r_[0:5, 32766:32771, 65534:65538, n - 5:n]
+    assert rel_err(out[rows], o.output(p, np.ascontiguousarray(X[rows]))) <= FP32_BAR
+    ref_loss = o.loss(p, X, Y)
+    assert abs(net.loss(dev(X), dev(Y)) - ref_loss) <= FP32_BAR * ref_loss
+    ref_out = o.output(p, X)
+    mism, ties = argmax_agree(out, ref_out)
+    assert mism == 0
+    assert abs(net.accuracy(dev(X), dev(Y)) - o.accuracy(p, X, Y)) <= ties / n + 1e-6
