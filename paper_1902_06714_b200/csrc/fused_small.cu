@@ -627,11 +627,14 @@ fused_small_kernel(const FusedParams p, const __grid_constant__ CUtensorMap tmX,
     }
     ptx::mbar_wait(bar_D, par);  // threads without a P5 task
     }  // !TC
-    // reduce my slice of the W2/b1/b2 tendencies over the cluster (rank order) -> L2
+    // reduce my slice of the W2/b1/b2 tendencies over the cluster (rank order); the sum goes
+    // to L2 with the dW1 slice in P6 as one more bulk reduction (aligned path: the slice is
+    // 16-B aligned, e_begin), in place of gpart's own slice (never pushed to a peer)
     for (int e = tid; e < ne; e += kThreads) {
       float v = 0.0f;
       for (int c = 0; c < C; ++c) v += (c == rank) ? gpart[e0 + e] : grecv[c * eslot + e];
-      ptx::red_add_f32(accS + p.small_off + e0 + e, v);
+      if (p.aligned) gpart[e0 + e] = v;
+      else ptx::red_add_f32(accS + p.small_off + e0 + e, v);
     }
     ptx::fence_proxy_async_smem();
     __syncthreads();
@@ -642,6 +645,7 @@ fused_small_kernel(const FusedParams p, const __grid_constant__ CUtensorMap tmX,
       if (tid == 0) {
         ptx::fence_proxy_async_global();
         ptx::bulk_reduce_add_f32(accS + slice_off, Gs, (uint32_t)(p.ws * 32 * 4));
+        if (ne > 0) ptx::bulk_reduce_add_f32(accS + p.small_off + e0, gpart + e0, (uint32_t)(ne * 4));
         ptx::bulk_commit();
         ptx::bulk_wait_all();
         ptx::fence_proxy_async_global();
