@@ -150,8 +150,11 @@ cudaError_t launch_tc(cudaStream_t st, int M, int N, int K, const TcOp &a, const
     static const bool det = getenv("NF_SPLITK_DETERMINISTIC") != nullptr;
     red = !epi.store_only && !det;
   }
+  // Split-K when under half a wave and K >= 512; for an epilogue that is not additive (needs
+  // the partials + a second kernel) only under a quarter wave (c4's layer 1, 64 tiles of
+  // K = 784: the split + splitk_epilogue cost more than they saved, 158.9 -> 155.2 us/step)
   int splits = 1;
-  if (2 * tiles < kSMs && nkb >= 16) {  // split-K only when under half a wave and K >= 512
+  if ((red ? 2 : 4) * tiles < kSMs && nkb >= 16) {
     splits = std::min(kSMs / tiles, nkb / 4);  // one wave
     while (!red && splits > 1 && (size_t)splits * M * N > ws.partial_floats) --splits;
     splits = std::max(splits, 1);
