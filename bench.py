@@ -394,7 +394,12 @@ def main():
                        "parallelism": (f"dp{world}: per step nf_grad on {B} rows per rank, NCCL all-reduce "
                                        f"of the tendencies (co_sum), nf_update; global batch {world * B}"
                                        if args.dp else f"replicas x{world}" if world > 1 else "1 GPU")},
-            "roofline": ({"bound": "alu", "achieved": ach_f64, "peak": FP64_DFMA_TFLOPS, "unit": "TFLOP/s",
+            "roofline": ({"bound": "latency", "achieved": t_max * 1e6 / K, "peak": None, "unit": "us/step",
+                          "frac": None, "traffic": None, "kernel": "single_cta_kernel",
+                          "note": "config 1 (120 flop per sample): one CTA, a chain of CTA barriers per step "
+                                  "(SURVEY 8(d): latency-bound, report us/step)"}
+                         if cid == 1 and args.math != "fp64" else
+                         {"bound": "alu", "achieved": ach_f64, "peak": FP64_DFMA_TFLOPS, "unit": "TFLOP/s",
                           "frac": ach_f64 / FP64_DFMA_TFLOPS, "traffic": None,
                           "peak_source": FP64_PEAK_SOURCE, "kernel": "whole step (gemm64_kernel + splitk64)",
                           "algorithmic_flops_per_step": flops_per_sample(cfg["dims"]) * B}
