@@ -287,12 +287,17 @@ int single_cta_train_steps(cudaStream_t st, const std::vector<int> &dims, const 
   int64_t macs = 0;
   for (int l = 1; l <= L; ++l) macs += (int64_t)dims[l] * dims[l - 1];
   static const int force_t = getenv("NF_SINGLE_T") ? atoi(getenv("NF_SINGLE_T")) : 0;
-  const bool big = force_t ? force_t > 256 : batch * macs > 8192;
+  const int T = force_t ? force_t : batch * macs <= 8192 ? 256 : 1024;  // (32: slower, 4.9 vs 2.4 us on c1)
   auto launch = [&](void (*kern)(SingleParams), int threads) {
     cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024);
     kern<<<1, threads, smem, st>>>(p);
   };
-  switch ((big ? 10 : 0) + (L <= 4 ? L : 0)) {
+  switch ((T == 32 ? 20 : T == 256 ? 0 : 10) + (L <= 4 ? L : 0)) {
+    case 21: launch(single_cta_kernel<32, 1>, 32); break;
+    case 22: launch(single_cta_kernel<32, 2>, 32); break;
+    case 23: launch(single_cta_kernel<32, 3>, 32); break;
+    case 24: launch(single_cta_kernel<32, 4>, 32); break;
+    case 20: launch(single_cta_kernel<32, 0>, 32); break;
     case 1: launch(single_cta_kernel<256, 1>, 256); break;
     case 2: launch(single_cta_kernel<256, 2>, 256); break;
     case 3: launch(single_cta_kernel<256, 3>, 256); break;
