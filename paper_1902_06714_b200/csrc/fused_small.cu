@@ -463,15 +463,18 @@ fused_small_kernel(const FusedParams p, const __grid_constant__ CUtensorMap tmX,
     for (int t = tid; t < nOwn * O; t += kThreads) {
       const int q = t / O, o = t - q * O;
       const float *va = A1own + q * 32, *w2 = W2s + o * 33;
+      // fully unrolled over the 32-wide rows (W2s and A1own are zero past H): every load is
+      // issued up front instead of one iteration at a time
       float c0 = 0.0f, c1 = 0.0f, c2 = 0.0f, c3 = 0.0f;
-      int j = 0;
-      for (; j + 4 <= H; j += 4) {
-        c0 = fmaf(w2[j], va[j], c0);
-        c1 = fmaf(w2[j + 1], va[j + 1], c1);
-        c2 = fmaf(w2[j + 2], va[j + 2], c2);
-        c3 = fmaf(w2[j + 3], va[j + 3], c3);
+#pragma unroll
+      for (int j = 0; j < 32; j += 4) {
+        if (j < H) {  // uniform
+          c0 = fmaf(w2[j], va[j], c0);
+          c1 = fmaf(w2[j + 1], va[j + 1], c1);
+          c2 = fmaf(w2[j + 2], va[j + 2], c2);
+          c3 = fmaf(w2[j + 3], va[j + 3], c3);
+        }
       }
-      for (; j < H; ++j) c0 = fmaf(w2[j], va[j], c0);
       const float z2 = b2s[o] + ((c0 + c1) + (c2 + c3));
       float a2, s2;
       act_sel<AO, AO>(p.act_o, z2, a2, s2);
@@ -484,13 +487,14 @@ fused_small_kernel(const FusedParams p, const __grid_constant__ CUtensorMap tmX,
     for (int t = tid; t < nOwn * 32; t += kThreads) {
       const int q = t >> 5, j = t & 31, i = o0 + q;
       const float *vd = D2own + q * 32;
-      float t0 = 0.0f, t1 = 0.0f;
-      int o = 0;
-      for (; o + 2 <= O; o += 2) {
-        t0 = fmaf(W2s[o * 33 + j], vd[o], t0);
-        t1 = fmaf(W2s[(o + 1) * 33 + j], vd[o + 1], t1);
+      float t0 = 0.0f, t1 = 0.0f;  // unrolled over <= 32 outputs (D2own, W2s zero past O)
+#pragma unroll
+      for (int o = 0; o < 32; o += 2) {
+        if (o < O) {  // uniform
+          t0 = fmaf(W2s[o * 33 + j], vd[o], t0);
+          t1 = fmaf(W2s[(o + 1) * 33 + j], vd[o + 1], t1);
+        }
       }
-      if (o < O) t0 = fmaf(W2s[o * 33 + j], vd[o], t0);
       D1[i * 32 + j] = j < H ? (t0 + t1) * D1[i * 32 + j] : 0.0f;
     }
     {
