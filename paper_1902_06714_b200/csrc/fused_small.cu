@@ -514,20 +514,18 @@ fused_small_kernel(const FusedParams p, const __grid_constant__ CUtensorMap tmX,
       float v = 0.0f;
       if (t < O * H) {
         const int o = t / H, j = t - o * H;
+#pragma unroll 8
         for (int q = 0; q < nOwn; ++q) v = fmaf(D2own[q * 32 + o], A1own[q * 32 + j], v);
       } else if (t < O * H + H) {
         const int j = t - O * H;
+#pragma unroll 8
         for (int q = 0; q < nOwn; ++q) v += D1[(o0 + q) * 32 + j];
       } else if (t < nsm) {
         const int o = t - O * H - H;
+#pragma unroll 8
         for (int q = 0; q < nOwn; ++q) v += D2own[q * 32 + o];
       }
       gpart[t] = v;
-    }
-    if (tid == 0 && p.step_loss) {
-      float l = 0.0f;
-      for (int ww = 0; ww < kWarps; ++ww) l += lsum[ww];
-      ptx::red_add_f32(p.step_loss + s, 0.5f * l * p.inv_B);
     }
     ptx::fence_proxy_async_smem();
     __syncthreads();
@@ -665,6 +663,10 @@ fused_small_kernel(const FusedParams p, const __grid_constant__ CUtensorMap tmX,
     //      before the previous barrier; its next writers start after the next one).
     __syncthreads();
     if (tid == 0) ptx::grid_arrive(p.bar);
+    if (warp == 1 && p.step_loss) {  // this CTA's cost partial, off the critical path (the
+      const float l = warp_sum(lane < kWarps ? lsum[lane] : 0.0f);  // barrier wait); lsum is
+      if (lane == 0) ptx::red_add_f32(p.step_loss + s, 0.5f * l * p.inv_B);  // rewritten in P3
+    }
     {
       float *z = p.acc + ((s + 2) % kSlots) * p.slot;
       for (int64_t i = (int64_t)blockIdx.x * kThreads + tid; i < p.slot; i += (int64_t)nCTA * kThreads) z[i] = 0.0f;
