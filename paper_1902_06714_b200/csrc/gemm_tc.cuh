@@ -46,7 +46,10 @@ namespace tc {
 
 constexpr int BM = 128;
 constexpr int BK = 32;              // 32 fp32 = 128 B = one SWIZZLE_128B row
-constexpr int kEpiWarps = 8;                 // epilogue warps: 2 per TMEM lane quadrant
+#ifndef NF_EPI_WARPS
+#define NF_EPI_WARPS 8
+#endif
+constexpr int kEpiWarps = NF_EPI_WARPS;      // epilogue warps: kEpiWarps / 4 per TMEM lane quadrant
 constexpr int kThreads = 64 + 32 * kEpiWarps;  // + TMA producer warp + MMA warp
 constexpr int kSmemBudget = 232448; // max dynamic shared memory per CTA on sm_100
 constexpr int kEpiBytes = kEpiWarps * 32 * 33 * 4;
@@ -271,7 +274,7 @@ gemm_tc_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ 
     const int mrow0 = m0 + q * 32;
     const int64_t MN = (int64_t)g.M * g.N;
 #pragma unroll 1
-    for (int c = half; c < BN / 32; c += 2) {
+    for (int c = half; c < BN / 32; c += kEpiWarps / 4) {
       const int nc = n0 + c * 32;
       if (nc >= g.N) break;  // warp-uniform
       float v[32];
@@ -428,7 +431,7 @@ gemm_tc_persistent(const __grid_constant__ CUtensorMap tmA, const __grid_constan
       tc_fence_after();
       const int mrow0 = m0 + q * 32;
 #pragma unroll 1
-      for (int c = half; c < BN / 32; c += 2) {
+      for (int c = half; c < BN / 32; c += kEpiWarps / 4) {
         const int nc = n0 + c * 32;
         if (nc >= N) break;  // warp-uniform
         float v[32];
