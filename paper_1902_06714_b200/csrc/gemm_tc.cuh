@@ -54,13 +54,15 @@ constexpr int kThreads = 64 + 32 * kEpiWarps;  // + TMA producer warp + MMA warp
 constexpr int kSmemBudget = 232448; // max dynamic shared memory per CTA on sm_100
 constexpr int kEpiBytes = kEpiWarps * 32 * 33 * 4;
 
-template <int BN, int SPLIT, int MAXST = 6>
+template <int BN, int SPLIT, int MAXST = 6, int EW = kEpiWarps>
 struct Cfg {
+  static constexpr int EPI_BYTES = EW * 32 * 33 * 4;  // epilogue transpose buffers
+  static constexpr int THREADS = 64 + 32 * EW;
   static constexpr int A_BYTES = BM * BK * 4;
   static constexpr int B_BYTES = BN * BK * 4;
   static constexpr int RAW_BYTES = A_BYTES + B_BYTES;
   static constexpr int STAGE_BYTES = SPLIT == 3 ? 2 * RAW_BYTES : RAW_BYTES;  // raw(hi) | lo
-  static constexpr int STAGES_FIT = (kSmemBudget - kEpiBytes - 1024 - 512) / STAGE_BYTES;
+  static constexpr int STAGES_FIT = (kSmemBudget - EPI_BYTES - 1024 - 512) / STAGE_BYTES;
   static constexpr int STAGES = STAGES_FIT > MAXST ? MAXST : STAGES_FIT;
   // NACC accumulators (all 512 TMEM columns): K-step t accumulates into t % NACC, and
   // the epilogue sums them in fp32.  The tensor core's fp32 accumulation truncates
@@ -71,7 +73,7 @@ struct Cfg {
   // take its TMEM while this one drains.
   static constexpr int NACC = SPLIT == 3 ? 512 / BN : 1;
   static constexpr int TMEM_COLS = SPLIT == 3 ? 512 : (BN < 32 ? 32 : BN);
-  static constexpr int SMEM = STAGES * STAGE_BYTES + kEpiBytes + 1024 /*align*/ + 512 /*barriers*/;
+  static constexpr int SMEM = STAGES * STAGE_BYTES + EPI_BYTES + 1024 /*align*/ + 512 /*barriers*/;
   static_assert(STAGES >= 2, "ring too shallow");
 };
 
@@ -151,17 +153,17 @@ struct TileArgs {
 
 // ---- the kernel ------------------------------------------------------------------------
 // MAXST < 6: a shallower ring (less shared memory) so that two CTAs co-reside on an SM and
-// one's epilogue overlaps the other's main loop
-template <int BN, bool A_MN, bool B_MN, int SPLIT, class Epi, int MAXST = 6>
-__global__ void __launch_bounds__(kThreads, 1)
+// one's epilogue overlaps the other's main loop; EW: epilogue warps (a multiple of 4)
+template <int BN, bool A_MN, bool B_MN, int SPLIT, class Epi, int MAXST = 6, int EW = kEpiWarps>
+__global__ void __launch_bounds__(64 + 32 * EW, 1)
 gemm_tc_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB, TileArgs g,
                Epi epi) {
-  using C = Cfg<BN, SPLIT, MAXST>;
+  using C = Cfg<BN, SPLIT, MAXST, EW>;
   ptx::pdl_trigger();
   extern __shared__ uint8_t smem_raw[];
   uint8_t *smem = reinterpret_cast<uint8_t *>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
   float *epibuf = reinterpret_cast<float *>(smem + C::STAGES * C::STAGE_BYTES);
-  uint64_t *full = reinterpret_cast<uint64_t *>(smem + C::STAGES * C::STAGE_BYTES + kEpiBytes);
+  uint64_t *full = reinterpret_cast<uint64_t *>(smem + C::STAGES * C::STAGE_BYTES + C::EPI_BYTES);
   uint64_t *empty = full + C::STAGES;
   uint64_t *conv = empty + C::STAGES;
   uint64_t *accum = conv + C::STAGES;
@@ -177,7 +179,7 @@ gemm_tc_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ 
     for (int s = 0; s < C::STAGES; ++s) {
       ptx::mbar_init(&full[s], 1);
       ptx::mbar_init(&empty[s], 1);
-      ptx::mbar_init(&conv[s], kEpiWarps);
+      ptx::mbar_init(&conv[s], EW);
     }
     ptx::mbar_init(accum, 1);
     ptx::fence_mbar_init();
@@ -246,7 +248,7 @@ gemm_tc_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ 
       mma_commit(accum);
     }
   } else {
-    const int t = threadIdx.x - 64;  // 0 .. 32 kEpiWarps - 1
+    const int t = threadIdx.x - 64;  // 0 .. 32 EW - 1
     if (SPLIT == 3) {  // ---- hi/lo splitters
       for (int it = 0; it < nkb; ++it) {
         const int s = it % C::STAGES;
@@ -254,7 +256,7 @@ gemm_tc_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ 
         float4 *raw = reinterpret_cast<float4 *>(smem + s * C::STAGE_BYTES);
         float4 *lo = reinterpret_cast<float4 *>(smem + s * C::STAGE_BYTES + C::RAW_BYTES);
 #pragma unroll 4
-        for (int i = t; i < C::RAW_BYTES / 16; i += 32 * kEpiWarps) {
+        for (int i = t; i < C::RAW_BYTES / 16; i += 32 * EW) {
           const float4 x = raw[i];
           const float4 h = make_float4(tf32_hi(x.x), tf32_hi(x.y), tf32_hi(x.z), tf32_hi(x.w));
           raw[i] = h;
@@ -274,7 +276,7 @@ gemm_tc_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ 
     const int mrow0 = m0 + q * 32;
     const int64_t MN = (int64_t)g.M * g.N;
 #pragma unroll 1
-    for (int c = half; c < BN / 32; c += kEpiWarps / 4) {
+    for (int c = half; c < BN / 32; c += EW / 4) {
       const int nc = n0 + c * 32;
       if (nc >= g.N) break;  // warp-uniform
       float v[32];

@@ -126,11 +126,11 @@ bool make_map(CUtensorMap *m, const TcOp &o, int rows, int K, int box_rows) {
                             CU_TENSOR_MAP_SWIZZLE_128B);
 }
 
-template <int BN, bool AMN, bool BMN, int SPLIT, class Epi, int MAXST = 6>
+template <int BN, bool AMN, bool BMN, int SPLIT, class Epi, int MAXST = 6, int EW = tc::kEpiWarps>
 cudaError_t launch_tc(cudaStream_t st, int M, int N, int K, const TcOp &a, const TcOp &b, const Epi &epi,
                       const Workspace &ws) {
-  using C = tc::Cfg<BN, SPLIT, MAXST>;
-  auto kern = tc::gemm_tc_kernel<BN, AMN, BMN, SPLIT, Epi, MAXST>;
+  using C = tc::Cfg<BN, SPLIT, MAXST, EW>;
+  auto kern = tc::gemm_tc_kernel<BN, AMN, BMN, SPLIT, Epi, MAXST, EW>;
   static bool attr = false;
   if (!attr) {
     cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, C::SMEM);
@@ -163,7 +163,7 @@ cudaError_t launch_tc(cudaStream_t st, int M, int N, int K, const TcOp &a, const
   splits = (nkb + kbper - 1) / kbper;  // no empty K-chunk
   red = red && splits > 1;
   tc::TileArgs g{M, N, K, kbper * tc::BK, (splits > 1 && !red) ? ws.partial : nullptr, red ? 1 : 0};
-  cudaError_t e = launch_k(kern, dim3(tn, tm, splits), dim3(tc::kThreads), C::SMEM, st, ta, tb, g, epi);
+  cudaError_t e = launch_k(kern, dim3(tn, tm, splits), dim3(C::THREADS), C::SMEM, st, ta, tb, g, epi);
   if (e != cudaSuccess) return e;
   if (splits > 1 && !red) {
     const int64_t MN = (int64_t)M * N;
@@ -207,7 +207,12 @@ cudaError_t run_tc(cudaStream_t st, int M, int N, int K, const TcOp &a, const Tc
     static const bool dual = getenv("NF_TC_DUAL") != nullptr;  // experiment: 2 CTAs per SM
     if (dual && N > 64 && tiles(128) >= fill && tiles(128) <= 2 * kSMs)
       return launch_tc<128, AMN, BMN, 1, Epi, 2>(st, M, N, K, a, b, epi, ws);
-    if (N > 128 && tiles(256) >= fill) return launch_tc<256, AMN, BMN, 1>(st, M, N, K, a, b, epi, ws);
+    // one wave of wide tiles: the epilogue is exposed (no next tile to overlap), 16 epilogue
+    // warps (c3: 179 -> 171 us per step; the persistent and narrow-tile kernels keep 8)
+    static const int ew = getenv("NF_TC_EW8") ? 8 : 16;
+    if (N > 128 && tiles(256) >= fill)
+      return ew == 16 ? launch_tc<256, AMN, BMN, 1, Epi, 6, 16>(st, M, N, K, a, b, epi, ws)
+                      : launch_tc<256, AMN, BMN, 1>(st, M, N, K, a, b, epi, ws);
     // under one wave of 128x256 tiles but deep (the c3 weight gradients, 1024 x 1024 x 4096):
     // keep the wide tile and split K so that tiles x splits fills the GPU in one wave
     {
