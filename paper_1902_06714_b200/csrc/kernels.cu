@@ -570,7 +570,8 @@ out_layer_train(const float *__restrict__ A, float *__restrict__ S, const float 
     float4 g[NMAX];
 #pragma unroll
     for (int o = 0; o < NMAX; ++o) g[o] = make_float4(0.f, 0.f, 0.f, 0.f);
-    for (int m = r0; m < r1; ++m) {
+#pragma unroll 4
+    for (int m = r0; m < r1; ++m) {  // (unrolled: the rows' A loads overlap)
       const float4 a = c < H4 ? __ldg(reinterpret_cast<const float4 *>(A + (int64_t)m * H) + c)
                               : make_float4(1.f, 0.f, 0.f, 0.f);
       const float *dr = dsm + (m - r0) * NMAX;
