@@ -232,20 +232,29 @@ int backward(nf_net *net, const float *x, int64_t n, float eta, float *grad) {
   cudaStream_t main_st = net->stream, side = overlap ? net->side : net->stream;
   NF_CUDA(cudaEventRecord(net->ev[0], main_st));  // fork (delta_L and the stash are ready)
   NF_CUDA(cudaStreamWaitEvent(side, net->ev[0], 0));
+  const float scale = (float)((double)eta / (double)n);
+  std::vector<char> bias_done(net->L + 1, 0);  // layer's bias update applied by K3's epilogue
   for (int l = net->L; l >= 1; --l) {
     const int nl = net->dims[l], nk = net->dims[l - 1];
     const bool fused = l == net->L && net->out_fused;  // K3(L) ran inside the forward kernel
     if (l > 1 && !fused) {
       EpiBwd eb{net->S[l - 1], nk};
+      const float *aprev2 = l > 2 ? net->A[l - 2] : x;  // the operand of layer l-1's weight GEMM
+      if (!grad && gemm_bwd_fuses_bias((int)n, nk, nl, net->S[l], net->W(l)) &&
+          gemm_grad_tc(nk, net->dims[l - 2], (int)n, net->S[l - 1], aprev2)) {
+        eb.bias = net->b(l - 1);  // b_{l-1} -= scale * column sums of delta_{l-1}, in the epilogue
+        eb.bscale = scale;
+        bias_done[l - 1] = 1;
+      }
       NF_CUDA(gemm_bwd(main_st, (int)n, nk, nl, net->S[l], net->W(l), eb, net->ws));
     }
     NF_CUDA(cudaEventRecord(net->ev[l], main_st));  // K3(l) done with W_l and delta_l is final
     NF_CUDA(cudaStreamWaitEvent(side, net->ev[l], 0));
     const float *aprev = l > 1 ? net->A[l - 1] : x;
     EpiGrad eg = grad ? EpiGrad{grad + net->offW[l], grad + net->offB[l], nk, nk, 0.0f, 1}
-                      : EpiGrad{net->W(l), net->b(l), nk, nk, (float)((double)eta / (double)n), 0};
+                      : EpiGrad{net->W(l), net->b(l), nk, nk, scale, 0};
     if (fused) NF_CUDA(out_layer_grad_final(side, (int)n, nk, nl, net->part_out.as<float>(), eg));
-    else NF_CUDA(gemm_grad(side, nl, nk, (int)n, net->S[l], aprev, eg, net->ws2));
+    else NF_CUDA(gemm_grad(side, nl, nk, (int)n, net->S[l], aprev, eg, net->ws2, bias_done[l] != 0));
   }
   NF_CUDA(cudaEventRecord(net->ev[net->L + 1], side));  // join
   NF_CUDA(cudaStreamWaitEvent(main_st, net->ev[net->L + 1], 0));

@@ -115,16 +115,39 @@ __device__ __forceinline__ void strip_generic(const E &e, int m0, int mlim, int 
 }
 
 // Backward: SD holds sigma'(Z_l) on entry and delta_l on exit.
+// With bias != nullptr the epilogue also applies the SGD update of the layer's bias from the
+// deltas it produces: b[n] -= bscale * sum_m delta[m][n] (its rows' share, an L2 reduction,
+// reading R12) -- the bias column sum then needs no kernel of its own.
 struct EpiBwd {
   static constexpr bool kRed = false;
   float *SD; int ld;
+  float *bias = nullptr; float bscale = 0.0f;
   __device__ __forceinline__ float load(int m, int n) const { return SD[(int64_t)m * ld + n]; }
   __device__ __forceinline__ void store(int m, int n, float acc, float s) const {
     SD[(int64_t)m * ld + n] = acc * s;
   }
-  __device__ __forceinline__ void operator()(int m, int n, float acc) const { store(m, n, acc, load(m, n)); }
+  __device__ __forceinline__ void operator()(int m, int n, float acc) const {
+    const float d = acc * load(m, n);
+    SD[(int64_t)m * ld + n] = d;
+    if (bias) asm volatile("red.global.add.f32 [%0], %1;" ::"l"(bias + n), "f"(-bscale * d) : "memory");
+  }
   __device__ __forceinline__ void strip(int m0, int mlim, int n, const float *v) const {
-    strip_generic(*this, m0, mlim, n, v);
+    if (!bias) {
+      strip_generic(*this, m0, mlim, n, v);
+      return;
+    }
+    float aux[32];
+#pragma unroll
+    for (int r = 0; r < 32; ++r) aux[r] = m0 + r < mlim ? load(m0 + r, n) : 0.0f;
+    float sum = 0.0f;
+#pragma unroll
+    for (int r = 0; r < 32; ++r)
+      if (m0 + r < mlim) {
+        const float d = v[33 * r] * aux[r];
+        SD[(int64_t)(m0 + r) * ld + n] = d;
+        sum += d;
+      }
+    asm volatile("red.global.add.f32 [%0], %1;" ::"l"(bias + n), "f"(-bscale * sum) : "memory");
   }
 };
 

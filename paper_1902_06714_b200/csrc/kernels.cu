@@ -684,6 +684,19 @@ cudaError_t gemm_fwd(cudaStream_t st, int M, int N, int K, const float *A, const
   return run_gemm<true, true>(st, g, epi, ws);
 }
 
+bool gemm_bwd_fuses_bias(int M, int N, int K, const float *D, const float *W) {
+  // the tensor-core path only (its strip epilogue sums 32 rows per reduction); up to 4096
+  // rows (more would pile 128+ reductions onto each bias element)
+  static const bool off = getenv("NF_NO_BIAS_FUSE") != nullptr;
+  const TcOp a{D, K, false}, b{W, N, true};
+  return !off && M <= 4096 && use_tc(M, N, K, a, b);
+}
+
+bool gemm_grad_tc(int M, int N, int K, const float *D, const float *Aprev) {
+  const TcOp a{D, M, true}, b{Aprev, N, true};
+  return use_tc(M, N, K, a, b);
+}
+
 cudaError_t gemm_bwd(cudaStream_t st, int M, int N, int K, const float *D, const float *W,
                      const EpiBwd &epi, const Workspace &ws) {
   const TcOp a{D, K, false}, b{W, N, true};
@@ -700,13 +713,15 @@ cudaError_t gemm_bwd(cudaStream_t st, int M, int N, int K, const float *D, const
 }
 
 cudaError_t gemm_grad(cudaStream_t st, int M, int N, int K, const float *D, const float *Aprev,
-                      const EpiGrad &epi, const Workspace &ws) {
+                      const EpiGrad &epi, const Workspace &ws, bool bias_done) {
   const TcOp a{D, M, true}, b{Aprev, N, true};
   if (use_tc(M, N, K, a, b)) {
-    // bias tendencies first: they read D only, and the partial buffer is free again
-    // before the split-K GEMM uses it (same stream)
-    cudaError_t e = bias_grad(st, D, K, M, epi, ws.partial, ws.partial_floats);
-    if (e != cudaSuccess) return e;
+    // bias tendencies first (unless the delta GEMM's epilogue applied them): they read D only,
+    // and the partial buffer is free again before the split-K GEMM uses it (same stream)
+    if (!bias_done) {
+      cudaError_t e = bias_grad(st, D, K, M, epi, ws.partial, ws.partial_floats);
+      if (e != cudaSuccess) return e;
+    }
     return run_tc<true, true>(st, M, N, K, a, b, epi, ws);
   }
   g_last_engine = ENGINE_SIMT;

@@ -31,8 +31,14 @@ cudaError_t gemm_fwd(cudaStream_t st, int M, int N, int K, const float *A, const
 cudaError_t gemm_bwd(cudaStream_t st, int M, int N, int K, const float *D, const float *W,
                      const EpiBwd &epi, const Workspace &ws);
 // K4: C[M][N+1] = D^T (D is [K][M]) * [Aprev | 1] (Aprev is [K][N]), epilogue EpiGrad.
+// bias_done: the layer's bias update was already applied by the delta GEMM (EpiBwd::bias); only
+// meaningful on the tensor-core path (the SIMT path carries the bias as a ones column)
 cudaError_t gemm_grad(cudaStream_t st, int M, int N, int K, const float *D, const float *Aprev,
-                      const EpiGrad &epi, const Workspace &ws);
+                      const EpiGrad &epi, const Workspace &ws, bool bias_done = false);
+// whether gemm_bwd with these operands takes the path whose epilogue can apply the bias update
+bool gemm_bwd_fuses_bias(int M, int N, int K, const float *D, const float *W);
+// whether gemm_grad with these operands takes the tensor-core path (bias as a separate sum)
+bool gemm_grad_tc(int M, int N, int K, const float *D, const float *Aprev);
 
 // The narrow output layer of a training step fused into one pass (kernels.cu, out_layer_train):
 // K1+K2 of layer L, K3 of layer L-1 (in place of S_{L-1}) and the partial tendencies of layer L
