@@ -685,11 +685,12 @@ cudaError_t gemm_fwd(cudaStream_t st, int M, int N, int K, const float *A, const
 }
 
 bool gemm_bwd_fuses_bias(int M, int N, int K, const float *D, const float *W) {
-  // the tensor-core path only (its strip epilogue sums 32 rows per reduction); up to 4096
-  // rows (more would pile 128+ reductions onto each bias element)
+  // the tensor-core path only (its strip epilogue sums 32 rows per reduction); up to 16384
+  // rows = 512 reductions per bias element (c5: 9.17 -> 9.05 ms per step)
   static const bool off = getenv("NF_NO_BIAS_FUSE") != nullptr;
   const TcOp a{D, K, false}, b{W, N, true};
-  return !off && M <= 4096 && use_tc(M, N, K, a, b);
+  static const int maxm = getenv("NF_BIAS_FUSE_MAXM") ? atoi(getenv("NF_BIAS_FUSE_MAXM")) : 16384;
+  return !off && M <= maxm && use_tc(M, N, K, a, b);
 }
 
 bool gemm_grad_tc(int M, int N, int K, const float *D, const float *Aprev) {
