@@ -165,8 +165,8 @@ int ensure_ws(nf_net *net, int64_t rows) {
   drop_graph(net);
   NF_CUDA(net->stash.ensure((size_t)(per_row * rows) * sizeof(float)));
   if (net->L >= 2)
-    NF_CUDA(net->part_out.ensure((size_t)out_layer_blocks((int)rows, net->dims[net->L - 1]) * net->dims[net->L] *
-                                 (net->dims[net->L - 1] + 1) * sizeof(float)));
+    NF_CUDA(net->part_out.ensure((size_t)out_layer_blocks((int)rows, net->dims[net->L - 1]) *
+                                 (net->dims[net->L] * (net->dims[net->L - 1] + 1) + 1) * sizeof(float)));
   float *p = net->stash.as<float>();
   net->A.assign(net->L + 1, nullptr);
   net->S.assign(net->L + 1, nullptr);
@@ -218,7 +218,7 @@ int ensure_side(nf_net *net) {
 // summed tendencies are stored there instead (nf_grad).  Per layer l (L..1): K3(l) computes
 // delta_{l-1} from delta_l and W_l on the main stream; K4(l) (tendencies of W_l, b_l and the
 // update) runs on the side stream once K3(l) has read W_l, overlapping K3(l-1).
-int backward(nf_net *net, const float *x, int64_t n, float eta, float *grad) {
+int backward(nf_net *net, const float *x, int64_t n, float eta, float *grad, float *step_loss = nullptr) {
   if (int rc = ensure_side(net)) return rc;
   net->ws2.math = net->ws.math;
   // The overlap only pays while the GEMMs are under one wave of 128x256 tiles (c3, c4): a
@@ -253,7 +253,7 @@ int backward(nf_net *net, const float *x, int64_t n, float eta, float *grad) {
     const float *aprev = l > 1 ? net->A[l - 1] : x;
     EpiGrad eg = grad ? EpiGrad{grad + net->offW[l], grad + net->offB[l], nk, nk, 0.0f, 1}
                       : EpiGrad{net->W(l), net->b(l), nk, nk, scale, 0};
-    if (fused) NF_CUDA(out_layer_grad_final(side, (int)n, nk, nl, net->part_out.as<float>(), eg));
+    if (fused) NF_CUDA(out_layer_grad_final(side, (int)n, nk, nl, net->part_out.as<float>(), eg, step_loss));
     else NF_CUDA(gemm_grad(side, nl, nk, (int)n, net->S[l], aprev, eg, net->ws2, bias_done[l] != 0));
   }
   NF_CUDA(cudaEventRecord(net->ev[net->L + 1], side));  // join
@@ -328,12 +328,12 @@ int train_batch_dev(nf_net *net, const float *x, const float *y, int64_t n, floa
   }
   if ((rc = ensure_ws(net, n))) return rc;
   if ((rc = forward(net, x, y, n, 0))) return rc;
-  if (step_loss) {
+  if (step_loss && !net->out_fused) {  // (the fused output layer computes the cost itself)
     NF_CUDA(net->red.ensure(red_bytes()));
     NF_CUDA(loss_acc(net->stream, net->A[net->L], y, n, net->dims[net->L], net->red.as<double2>(),
                      nullptr, step_loss));
   }
-  return backward(net, x, n, eta, nullptr);
+  return backward(net, x, n, eta, nullptr, net->out_fused ? step_loss : nullptr);
 }
 
 const float *stage_in(nf_net *net, const float *p, size_t count, DevBuf &buf, int *rc) {

@@ -455,9 +455,16 @@ grad_smallm_partial(const float *__restrict__ D, const float *__restrict__ A, in
 // thread t sums the R partials of output t in order r = 0..R-1, four independent loads in
 // flight (deterministic)
 __global__ void __launch_bounds__(256)
-grad_smallm_final(const float *__restrict__ part, int R, int M, int N, EpiGrad epi) {
+grad_smallm_final(const float *__restrict__ part, int R, int M, int N, EpiGrad epi,
+                  const float *__restrict__ lpart = nullptr, float lscale = 0.0f, float *__restrict__ step_loss = nullptr) {
   ptx::pdl_trigger();
   ptx::pdl_wait();
+  if (step_loss && blockIdx.x == 0 && threadIdx.x < 32) {  // the step's mean cost from the fused
+    float l = 0.0f;                                        // output layer's per-block partials
+    for (int r = threadIdx.x; r < R; r += 32) l += lpart[r];  // (fixed order)
+    l = warp_sum(l);
+    if (threadIdx.x == 0) *step_loss = l * lscale;
+  }
   // 32 outputs per block; warp w sums the partials r = w (mod 8), warp 0 adds the eight warp
   // sums in order (deterministic)
   __shared__ float red[8][33];
@@ -494,9 +501,12 @@ template <int NMAX, int HMAX4>
 __global__ void __launch_bounds__(256)
 out_layer_train(const float *__restrict__ A, float *__restrict__ S, const float *__restrict__ W,
                 const float *__restrict__ bias, const float *__restrict__ Y, float *__restrict__ AL,
-                float *__restrict__ DL, int n, int H, int nL, int act, int rows_per_block, float *__restrict__ part) {
+                float *__restrict__ DL, int n, int H, int nL, int act, int rows_per_block, float *__restrict__ part,
+                float *__restrict__ lpart) {
   ptx::pdl_trigger();
   ptx::pdl_wait();
+  __shared__ float lred[8];
+  float lacc = 0.0f;  // sum of (a - y)^2 over this warp's rows: the block's cost partial
   extern __shared__ float4 sm4_[];
   float *ws_ = reinterpret_cast<float *>(sm4_);          // [nL][H]
   float *dsm = ws_ + nL * H;                             // [rows_per_block][NMAX] delta_L
@@ -536,7 +546,9 @@ out_layer_train(const float *__restrict__ A, float *__restrict__ S, const float 
       if (o == lane && o < nL) {
         float a, sg;
         act_fwd(act, acc[o] + bias[o], a, sg);
-        dl = (a - Y[(int64_t)m * nL + o]) * sg;
+        const float diff = a - Y[(int64_t)m * nL + o];
+        dl = diff * sg;
+        lacc = fmaf(diff, diff, lacc);
         AL[(int64_t)m * nL + o] = a;
         DL[(int64_t)m * nL + o] = dl;
       }
@@ -563,7 +575,14 @@ out_layer_train(const float *__restrict__ A, float *__restrict__ S, const float 
       }
     }
   }
+  lacc = warp_sum(lacc);
+  if (lane == 0) lred[warp] = lacc;
   __syncthreads();
+  if (threadIdx.x == 0) {
+    float l = 0.0f;
+    for (int i = 0; i < 8; ++i) l += lred[i];
+    lpart[blockIdx.x] = l;
+  }
   // phase 2: partial tendencies of the block's rows, column group c (4 columns; c == H4: bias)
   float *pb = part + (int64_t)blockIdx.x * nL * (H + 1);
   for (int c = threadIdx.x; c <= H4; c += blockDim.x) {
@@ -646,20 +665,22 @@ cudaError_t out_layer_train_fused(cudaStream_t st, int n, int H, int nL, const f
   }
   if (H <= 512)
     return launch_k(out_layer_train<16, 4>, dim3(blocks), dim3(256), smem, st, A, S, W, bias, Y, AL, DL, n, H, nL,
-                    act, rpb, part);
+                    act, rpb, part, part + (int64_t)blocks * nL * (H + 1));
   if (H <= 1024)
     return launch_k(out_layer_train<16, 8>, dim3(blocks), dim3(256), smem, st, A, S, W, bias, Y, AL, DL, n, H, nL,
-                    act, rpb, part);
+                    act, rpb, part, part + (int64_t)blocks * nL * (H + 1));
   return launch_k(out_layer_train<16, 16>, dim3(blocks), dim3(256), smem, st, A, S, W, bias, Y, AL, DL, n, H, nL,
-                  act, rpb, part);
+                  act, rpb, part, part + (int64_t)blocks * nL * (H + 1));
 }
 
-cudaError_t out_layer_grad_final(cudaStream_t st, int n, int H, int nL, const float *part, const EpiGrad &epi) {
+cudaError_t out_layer_grad_final(cudaStream_t st, int n, int H, int nL, const float *part, const EpiGrad &epi,
+                                 float *step_loss) {
   const int R = out_layer_blocks(n, H);
   const int rpb = (n + R - 1) / R;
   const int blocks = (n + rpb - 1) / rpb;
   const int64_t MN = (int64_t)nL * (H + 1);
-  return launch_k(grad_smallm_final, dim3((int)((MN + 31) / 32)), dim3(256), 0, st, part, blocks, nL, H, epi);
+  return launch_k(grad_smallm_final, dim3((int)((MN + 31) / 32)), dim3(256), 0, st, part, blocks, nL, H, epi,
+                  (const float *)(part + (int64_t)blocks * nL * (H + 1)), 0.5f / (float)n, step_loss);
 }
 
 cudaError_t gemm_fwd(cudaStream_t st, int M, int N, int K, const float *A, const float *W,
@@ -737,7 +758,7 @@ cudaError_t gemm_grad(cudaStream_t st, int M, int N, int K, const float *D, cons
     if (e != cudaSuccess) return e;
     const int64_t MN = (int64_t)M * (N + 1);
     return launch_k(grad_smallm_final, dim3((int)((MN + 31) / 32)), dim3(256), 0, st,
-                    (const float *)ws.partial, R, M, N, epi);
+                    (const float *)ws.partial, R, M, N, epi, (const float *)nullptr, 0.0f, (float *)nullptr);
   }
   // C[M][N+1]: column N is the ones column -> bias gradient.
   GemmArgs g{M, N + 1, K, D, M, Aprev, N, N, 0, nullptr};

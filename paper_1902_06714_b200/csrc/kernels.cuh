@@ -48,7 +48,9 @@ bool out_layer_fusable(int n, int H, int nL, const float *A, const float *S, con
 int out_layer_blocks(int n, int H);
 cudaError_t out_layer_train_fused(cudaStream_t st, int n, int H, int nL, const float *A, float *S, const float *W,
                                   const float *bias, const float *Y, float *AL, float *DL, int act, float *part);
-cudaError_t out_layer_grad_final(cudaStream_t st, int n, int H, int nL, const float *part, const EpiGrad &epi);
+// step_loss (nullable): also writes the step's mean cost from the kernel's per-block partials
+cudaError_t out_layer_grad_final(cudaStream_t st, int n, int H, int nL, const float *part, const EpiGrad &epi,
+                                 float *step_loss = nullptr);
 
 // K5: mean quadratic cost and argmax-accuracy of A_L against Y over n rows of
 // width w.  part: scratch of >= loss_acc_parts() double2.  Results: out[0] =

@@ -483,3 +483,18 @@ def test_eval_over_several_chunks(dims, act):
     mism, ties = argmax_agree(out, ref_out)
     assert mism == 0
     assert abs(net.accuracy(dev(X), dev(Y)) - o.accuracy(p, X, Y)) <= ties / n + 1e-6
+
+
+@pytest.mark.parametrize("dims,act,batch", [([64, 256, 10], "tanh,sigmoid", 300), ([48, 1024, 7], "sigmoid", 520)])
+def test_fused_output_layer_step_losses(dims, act, batch):
+    """The per-step costs of nf_train_steps when the fused output-layer kernel computes them
+    (per-block partials summed in fixed order by the tendency kernel) against the oracle."""
+    p = synth.random_params(97, dims, 0.3)
+    X, Y = synth.random_batch(98, 3 * batch, dims[0], dims[-1], "uniform")
+    starts = [0, batch, 2 * batch, batch // 2, 7]
+    net = make_net(dims, act, p)
+    loss = torch.full((len(starts),), -1.0, device="cuda")
+    net.train_steps(dev(X), dev(Y), batch, starts, 0.4, step_loss=loss)
+    ref, ref_loss = oracle.Oracle(dims, act).train_steps(p, X, Y, batch, starts, 0.4)
+    assert rel_err(loss.cpu().numpy(), ref_loss) <= FP32_BAR
+    assert rel_err(gpu_params(net), ref) <= FP32_BAR
