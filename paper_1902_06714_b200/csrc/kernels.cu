@@ -530,14 +530,16 @@ out_layer_train(const float *__restrict__ A, float *__restrict__ S, const float 
     for (int o = 0; o < NMAX; ++o) {
       acc[o] = 0.0f;
       if (o < nL) {
+        float2 p0 = make_float2(0.f, 0.f), p1 = make_float2(0.f, 0.f);  // packed FFMA2 over k pairs
 #pragma unroll
         for (int i = 0; i < HMAX4; ++i) {
           if (lane + 32 * i < H4) {
             const float4 w = reinterpret_cast<const float4 *>(ws_ + o * H)[lane + 32 * i];
-            acc[o] = fmaf(av[i].x, w.x, fmaf(av[i].y, w.y, fmaf(av[i].z, w.z, fmaf(av[i].w, w.w, acc[o]))));
+            ffma2v(p0, make_float2(av[i].x, av[i].y), make_float2(w.x, w.y));
+            ffma2v(p1, make_float2(av[i].z, av[i].w), make_float2(w.z, w.w));
           }
         }
-        acc[o] = warp_sum(acc[o]);
+        acc[o] = warp_sum((p0.x + p0.y) + (p1.x + p1.y));
       }
     }
     float dl = 0.0f;  // lane o < nL: delta_L[m][o]
@@ -562,16 +564,16 @@ out_layer_train(const float *__restrict__ A, float *__restrict__ S, const float 
       const int k4 = lane + 32 * i;
       if (k4 < H4) {
         const float4 sg = srow[k4];
-        float4 t = make_float4(0.f, 0.f, 0.f, 0.f);
+        float2 t0 = make_float2(0.f, 0.f), t1 = make_float2(0.f, 0.f);
 #pragma unroll
         for (int o = 0; o < NMAX; ++o) {
           if (o < nL) {
             const float4 w = reinterpret_cast<const float4 *>(ws_ + o * H)[k4];
-            t.x = fmaf(d[o], w.x, t.x); t.y = fmaf(d[o], w.y, t.y);
-            t.z = fmaf(d[o], w.z, t.z); t.w = fmaf(d[o], w.w, t.w);
+            ffma2(t0, d[o], make_float2(w.x, w.y));
+            ffma2(t1, d[o], make_float2(w.z, w.w));
           }
         }
-        srow[k4] = make_float4(t.x * sg.x, t.y * sg.y, t.z * sg.z, t.w * sg.w);
+        srow[k4] = make_float4(t0.x * sg.x, t0.y * sg.y, t1.x * sg.z, t1.y * sg.w);
       }
     }
   }
@@ -586,9 +588,9 @@ out_layer_train(const float *__restrict__ A, float *__restrict__ S, const float 
   // phase 2: partial tendencies of the block's rows, column group c (4 columns; c == H4: bias)
   float *pb = part + (int64_t)blockIdx.x * nL * (H + 1);
   for (int c = threadIdx.x; c <= H4; c += blockDim.x) {
-    float4 g[NMAX];
+    float2 g[NMAX][2];  // columns (4c, 4c+1), (4c+2, 4c+3) per output: packed FFMA2
 #pragma unroll
-    for (int o = 0; o < NMAX; ++o) g[o] = make_float4(0.f, 0.f, 0.f, 0.f);
+    for (int o = 0; o < NMAX; ++o) g[o][0] = g[o][1] = make_float2(0.f, 0.f);
 #pragma unroll 4
     for (int m = r0; m < r1; ++m) {  // (unrolled: the rows' A loads overlap)
       const float4 a = c < H4 ? __ldg(reinterpret_cast<const float4 *>(A + (int64_t)m * H) + c)
@@ -598,8 +600,8 @@ out_layer_train(const float *__restrict__ A, float *__restrict__ S, const float 
       for (int o = 0; o < NMAX; ++o) {
         if (o < nL) {
           const float dv = dr[o];
-          g[o].x = fmaf(dv, a.x, g[o].x); g[o].y = fmaf(dv, a.y, g[o].y);
-          g[o].z = fmaf(dv, a.z, g[o].z); g[o].w = fmaf(dv, a.w, g[o].w);
+          ffma2(g[o][0], dv, make_float2(a.x, a.y));
+          ffma2(g[o][1], dv, make_float2(a.z, a.w));
         }
       }
     }
@@ -607,8 +609,8 @@ out_layer_train(const float *__restrict__ A, float *__restrict__ S, const float 
     for (int o = 0; o < NMAX; ++o) {
       if (o < nL) {
         float *p = pb + (int64_t)o * (H + 1) + 4 * c;
-        if (c < H4) { p[0] = g[o].x; p[1] = g[o].y; p[2] = g[o].z; p[3] = g[o].w; }
-        else p[0] = g[o].x;  // bias column H
+        if (c < H4) { p[0] = g[o][0].x; p[1] = g[o][0].y; p[2] = g[o][1].x; p[3] = g[o][1].y; }
+        else p[0] = g[o][0].x;  // bias column H
       }
     }
   }
@@ -662,6 +664,24 @@ cudaError_t out_layer_train_fused(cudaStream_t st, int n, int H, int nL, const f
     cudaFuncSetAttribute(out_layer_train<16, 8>, cudaFuncAttributeMaxDynamicSharedMemorySize, kOutSmemMax);
     cudaFuncSetAttribute(out_layer_train<16, 16>, cudaFuncAttributeMaxDynamicSharedMemorySize, kOutSmemMax);
     attr = true;
+  }
+  float *lp = part + (int64_t)blocks * nL * (H + 1);
+  if (nL <= 10) {  // (MNIST-like 10-wide outputs: no idle unrolled output slots)
+    static bool attr10 = false;
+    if (!attr10) {
+      cudaFuncSetAttribute(out_layer_train<10, 4>, cudaFuncAttributeMaxDynamicSharedMemorySize, kOutSmemMax);
+      cudaFuncSetAttribute(out_layer_train<10, 8>, cudaFuncAttributeMaxDynamicSharedMemorySize, kOutSmemMax);
+      cudaFuncSetAttribute(out_layer_train<10, 16>, cudaFuncAttributeMaxDynamicSharedMemorySize, kOutSmemMax);
+      attr10 = true;
+    }
+    if (H <= 512)
+      return launch_k(out_layer_train<10, 4>, dim3(blocks), dim3(256), smem, st, A, S, W, bias, Y, AL, DL, n, H, nL,
+                      act, rpb, part, lp);
+    if (H <= 1024)
+      return launch_k(out_layer_train<10, 8>, dim3(blocks), dim3(256), smem, st, A, S, W, bias, Y, AL, DL, n, H, nL,
+                      act, rpb, part, lp);
+    return launch_k(out_layer_train<10, 16>, dim3(blocks), dim3(256), smem, st, A, S, W, bias, Y, AL, DL, n, H, nL,
+                    act, rpb, part, lp);
   }
   if (H <= 512)
     return launch_k(out_layer_train<16, 4>, dim3(blocks), dim3(256), smem, st, A, S, W, bias, Y, AL, DL, n, H, nL,
