@@ -254,6 +254,10 @@ int backward(nf_net *net, const float *x, int64_t n, float eta, float *grad, flo
     EpiGrad eg = grad ? EpiGrad{grad + net->offW[l], grad + net->offB[l], nk, nk, 0.0f, 1}
                       : EpiGrad{net->W(l), net->b(l), nk, nk, scale, 0};
     if (fused) NF_CUDA(out_layer_grad_final(side, (int)n, nk, nl, net->part_out.as<float>(), eg, step_loss));
+    else if (l == 1 && net->L > 1 && side != main_st && (net->math != NF_MATH_TF32 || n <= 2048))
+      // the main stream is idle after the last K3: K4(1) there, concurrent with K4(2) on the side
+      // stream (c4 134 -> 130 us, 3xTF32 c3 462 -> 445 us; c3's 1xTF32 pair contends: 154 -> 157)
+      NF_CUDA(gemm_grad(main_st, nl, nk, (int)n, net->S[l], aprev, eg, net->ws, bias_done[l] != 0));
     else NF_CUDA(gemm_grad(side, nl, nk, (int)n, net->S[l], aprev, eg, net->ws2, bias_done[l] != 0));
   }
   NF_CUDA(cudaEventRecord(net->ev[net->L + 1], side));  // join
