@@ -139,13 +139,13 @@ def job_throughput(world, steps, batch, t_max):
     return world * steps * batch / t_max
 
 
-# Bounded CPU-oracle samples (about 5-20 s of single-core work each): (steps, rows per step).
+# Bounded CPU-oracle samples (about 10-15 s of single-core work each): (steps, rows per step).
 # The oracle's per-sample cost does not depend on the batch size (one fwd/bwd per sample, one
 # update per step), so a reduced batch is a fair sample of samples/s for the wide configs.
 # NF_MATH_FP64 is bound by the FP64 FMA units (SIMT DFMA): peak measured by micro/fma_rate.cu
 FP64_DFMA_TFLOPS = 34.82  # DFMA, 32 warps/SM, 148 SMs at 1965 MHz (59.9 FMA/clk/SM)
 FP64_PEAK_SOURCE = "micro/fma_rate.cu DFMA rate, 148 SMs (profiles/r01_micro_fma_rate.txt)"
-CPU_SAMPLE = {1: (20000, None), 2: (200, None), 3: (2, 256), 4: (4, 512), 5: (1, 32)}
+CPU_SAMPLE = {1: (5000000, None), 2: (500, None), 3: (8, 256), 4: (20, 512), 5: (1, 32)}  # ~10-15 s each
 
 
 def run_cpu_oracle(cid, steps, batch=None, bits=32, X=None, Y=None):
