@@ -19,9 +19,14 @@ namespace {
 #define NF_INFER_T 256
 #endif
 #ifndef NF_INFER_S
-#define NF_INFER_S 4
+#define NF_INFER_S 2
 #endif
-constexpr int kT = NF_INFER_T;
+constexpr int kT = NF_INFER_T;                 // threads per tile group
+#ifndef NF_INFER_G
+#define NF_INFER_G 2
+#endif
+constexpr int kG = NF_INFER_G;  // independent tile groups per CTA (own ring, own named barrier):
+                                // one group's barrier / staging bubbles overlap the other's work
 constexpr int kKH = kT / 128;  // pixel parts of a chunk (tasks: 8 neuron groups x 16 row groups x kKH)
 constexpr int kRows = 64;      // rows per tile
 #ifndef NF_INFER_KC
@@ -38,7 +43,7 @@ __device__ __forceinline__ void cp_async16(float *dst, const float *src) {
 __device__ __forceinline__ void cp_commit() { asm volatile("cp.async.commit_group;" ::: "memory"); }
 __device__ __forceinline__ void cp_wait_ring() { asm volatile("cp.async.wait_group %0;" ::"n"(kS - 1) : "memory"); }
 
-__global__ void __launch_bounds__(kT, 1)
+__global__ void __launch_bounds__(kT * kG, 1)
 infer_small_kernel(const float *__restrict__ X, int64_t n, int n0, int H, int O, int act_h, int act_o,
                    const float *__restrict__ params, float *__restrict__ out) {
   extern __shared__ __align__(16) float sm[];
@@ -48,18 +53,25 @@ infer_small_kernel(const float *__restrict__ X, int64_t n, int n0, int H, int O,
   float *W2s = W1t + n0p * 32;            // [32][33]
   float *b1s = W2s + 32 * 33;             // [32]
   float *b2s = b1s + 32;                  // [32]
-  float *xs = b2s + 32;                   // kS x [kRows][kXs]
+  const int grp = threadIdx.x / kT;      // this thread's tile group
+  float *xs0 = b2s + 32;                  // kG x { kS x [kRows][kXs] ring, [kRows][33] a1s, parts }
+  const int gstride = kS * kRows * kXs + kKH * kRows * 33;
+  float *xs = xs0 + grp * gstride;        // kS x [kRows][kXs]
   float *a1s = xs + kS * kRows * kXs;     // [kRows][33]
   float *a1p = a1s + kRows * 33;          // (kKH - 1) x [kRows][33] partial Z1 of pixel parts 1..
-  const int tid = threadIdx.x;
+  const int tid = threadIdx.x % kT;
+  auto group_sync = [&]() {
+    if (kG == 1) __syncthreads();
+    else asm volatile("bar.sync %0, %1;" ::"r"(1 + grp), "r"(kT) : "memory");
+  };
   const float *W1 = params, *b1 = params + (int64_t)H * n0, *W2 = b1 + H, *b2 = W2 + O * H;
 
   {  // W1 [H][n0] -> W1t [n0p][32]: a warp per 32-pixel block; coalesced row reads (lane =
      // pixel) into a padded 32 x 33 tile (in the not yet used x ring), then coalesced
      // transposed writes (lane = neuron), conflict-free on both sides
-    const int lane = tid & 31, warp = tid >> 5;
-    float *tile = xs + warp * 32 * 33;
-    for (int k0 = warp * 32; k0 < n0p; k0 += (kT / 32) * 32) {
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;  // all groups' warps
+    float *tile = xs0 + warp * 32 * 33;
+    for (int k0 = warp * 32; k0 < n0p; k0 += (kT * kG / 32) * 32) {
       const int k = k0 + lane;
 #pragma unroll 8
       for (int j = 0; j < 32; ++j) tile[j * 33 + lane] = (j < H && k < n0) ? W1[(int64_t)j * n0 + k] : 0.0f;
@@ -70,13 +82,13 @@ infer_small_kernel(const float *__restrict__ X, int64_t n, int n0, int H, int O,
     }
   }
   __syncthreads();  // the x ring is reused below
-  for (int i = tid; i < 32 * 33; i += kT) {
+  for (int i = threadIdx.x; i < 32 * 33; i += kT * kG) {
     const int o = i / 33, j = i % 33;
     W2s[i] = (o < O && j < H) ? W2[o * H + j] : 0.0f;
   }
-  if (tid < 32) {
-    b1s[tid] = tid < H ? b1[tid] : 0.0f;
-    b2s[tid] = tid < O ? b2[tid] : 0.0f;
+  if (threadIdx.x < 32) {
+    b1s[threadIdx.x] = threadIdx.x < H ? b1[threadIdx.x] : 0.0f;
+    b2s[threadIdx.x] = threadIdx.x < O ? b2[threadIdx.x] : 0.0f;
   }
 
   // Z1 task (kT = 8 neuron groups x 16 row groups x kKH pixel parts): neurons 4 jg .. 4 jg + 3,
@@ -85,12 +97,13 @@ infer_small_kernel(const float *__restrict__ X, int64_t n, int n0, int H, int O,
   const int rgrp = rg & 15, kh = rg >> 4;
   const int64_t ntiles = (n + kRows - 1) / kRows;
 
-  // this CTA's stream of (tile, chunk) pairs: t -> tile blockIdx.x + (t / nchunk) * gridDim.x
-  const int64_t my_tiles = ntiles > blockIdx.x ? (ntiles - 1 - blockIdx.x) / gridDim.x + 1 : 0;
+  // this group's stream of (tile, chunk) pairs: tiles first + k * nstream, k = 0, 1, ...
+  const int64_t first = (int64_t)blockIdx.x * kG + grp, nstream = (int64_t)gridDim.x * kG;
+  const int64_t my_tiles = ntiles > first ? (ntiles - 1 - first) / nstream + 1 : 0;
   const int64_t T = my_tiles * nchunk;
   // staging cursor (chunk, tile row, ring slot) advanced incrementally: no 64-bit divisions
   int s_c = 0, s_slot = 0;
-  int64_t s_r0 = (int64_t)blockIdx.x * kRows, s_t = 0;
+  int64_t s_r0 = first * kRows, s_t = 0;
   auto stage = [&]() {  // stages the next (tile, chunk); always commits a group (uniform counting)
     if (s_t < T) {
       float *dst = xs + s_slot * kRows * kXs;
@@ -107,7 +120,7 @@ infer_small_kernel(const float *__restrict__ X, int64_t n, int n0, int H, int O,
     cp_commit();
     ++s_t;
     s_slot = s_slot + 1 == kS ? 0 : s_slot + 1;
-    if (++s_c == nchunk) { s_c = 0; s_r0 += (int64_t)gridDim.x * kRows; }
+    if (++s_c == nchunk) { s_c = 0; s_r0 += nstream * kRows; }
   };
   static_assert((kKC & (kKC - 1)) == 0, "kKC: a power of two");
 
@@ -115,7 +128,7 @@ infer_small_kernel(const float *__restrict__ X, int64_t n, int n0, int H, int O,
   for (int t = 0; t < kS - 1; ++t) stage();
   float2 acc[4][2];
   int c = 0, slot = 0;
-  int64_t r0 = (int64_t)blockIdx.x * kRows;
+  int64_t r0 = first * kRows;
   for (int64_t t = 0; t < T; ++t) {
     if (c == 0) {
 #pragma unroll
@@ -123,7 +136,7 @@ infer_small_kernel(const float *__restrict__ X, int64_t n, int n0, int H, int O,
     }
     stage();
     cp_wait_ring();   // chunk t has landed (this thread's copies)
-    __syncthreads();  // ... and everyone's
+    group_sync();  // ... and the group's
     {
       const float *xb = xs + slot * kRows * kXs + rgrp * kXs;
       const float *wb = W1t + (c * kKC) * 32 + jg * 4;
@@ -155,7 +168,7 @@ infer_small_kernel(const float *__restrict__ X, int64_t n, int n0, int H, int O,
           d[0] = acc[u][0].x; d[1] = acc[u][0].y; d[2] = acc[u][1].x; d[3] = acc[u][1].y;
         }
       }
-      __syncthreads();
+      group_sync();
       if (kh == 0) {
 #pragma unroll
         for (int u = 0; u < 4; ++u) {
@@ -173,7 +186,7 @@ infer_small_kernel(const float *__restrict__ X, int64_t n, int n0, int H, int O,
           }
         }
       }
-      __syncthreads();
+      group_sync();
       // layer 2: thread per (row, output)
       for (int i = tid; i < kRows * O; i += kT) {
         const int r = i / O, o = i - r * O;
@@ -189,9 +202,9 @@ infer_small_kernel(const float *__restrict__ X, int64_t n, int n0, int H, int O,
         out[(r0 + r) * O + o] = act_only(act_o, b2s[o] + (c0 + c1));
       }
     }
-    __syncthreads();  // chunk t's buffer is refilled by stage(t + kS) next iteration
+    group_sync();  // chunk t's buffer is refilled by stage(t + kS) next iteration
     slot = slot + 1 == kS ? 0 : slot + 1;
-    if (++c == nchunk) { c = 0; r0 += (int64_t)gridDim.x * kRows; }
+    if (++c == nchunk) { c = 0; r0 += nstream * kRows; }
   }
   cp_wait_ring();
 }
@@ -205,7 +218,7 @@ bool infer_small_applicable(const std::vector<int> &dims, const float *X) {
 
 size_t infer_small_smem(int n0) {
   const int n0p = (n0 + kKC - 1) / kKC * kKC;
-  return sizeof(float) * ((size_t)n0p * 32 + 32 * 33 + 64 + kS * kRows * kXs + kKH * kRows * 33);
+  return sizeof(float) * ((size_t)n0p * 32 + 32 * 33 + 64 + (size_t)kG * (kS * kRows * kXs + kKH * kRows * 33));
 }
 
 cudaError_t infer_small(cudaStream_t st, const std::vector<int> &dims, int act_h, int act_o, const float *params,
@@ -216,9 +229,9 @@ cudaError_t infer_small(cudaStream_t st, const std::vector<int> &dims, int act_h
     attr = true;
   }
   const int64_t ntiles = (n + kRows - 1) / kRows;
-  const int blocks = (int)std::min<int64_t>(ntiles, 148);
-  infer_small_kernel<<<blocks, kT, infer_small_smem(dims[0]), st>>>(X, n, dims[0], dims[1], dims[2], act_h, act_o,
-                                                                    params, out);
+  const int blocks = (int)std::max<int64_t>(1, std::min<int64_t>((ntiles + kG - 1) / kG, 148));
+  infer_small_kernel<<<blocks, kT * kG, infer_small_smem(dims[0]), st>>>(X, n, dims[0], dims[1], dims[2], act_h,
+                                                                         act_o, params, out);
   count_launch();
   return cudaGetLastError();
 }
