@@ -616,6 +616,22 @@ out_layer_train(const float *__restrict__ A, float *__restrict__ S, const float 
   }
 }
 
+// Host-dataset staging of the small per-step target rows (nf_train_steps e2e path): the rows
+// of up to kGatherMax steps read straight from mapped (pinned) host memory by the GPU, one
+// kernel per chunk instead of one small DMA per step (their per-copy cost was 8 % of the e2e
+// time on c2).  off[s]: first float of step s in src; len floats per step, contiguous.
+constexpr int kGatherMax = 64;
+struct GatherArgs {
+  int64_t off[kGatherMax];
+};
+__global__ void __launch_bounds__(256) gather_steps_kernel(const float *__restrict__ src, GatherArgs a, int64_t len,
+                                                           float *__restrict__ dst) {
+  const int s = blockIdx.y;
+  const float *p = src + a.off[s];
+  float *q = dst + (int64_t)s * len;
+  for (int64_t i = (int64_t)blockIdx.x * 256 + threadIdx.x; i < len; i += (int64_t)gridDim.x * 256) q[i] = p[i];
+}
+
 __global__ void __launch_bounds__(256) sgd_update_kernel(float *__restrict__ p, const float *__restrict__ g, int64_t n,
                                                          float scale) {
   ptx::pdl_trigger();
@@ -624,6 +640,17 @@ __global__ void __launch_bounds__(256) sgd_update_kernel(float *__restrict__ p, 
 }
 
 }  // namespace
+
+cudaError_t gather_steps(cudaStream_t st, const float *src, const int64_t *off, int m, int64_t len, float *dst) {
+  if (m <= 0) return cudaSuccess;
+  if (m > kGatherMax) return cudaErrorInvalidValue;
+  GatherArgs a;
+  for (int s = 0; s < m; ++s) a.off[s] = off[s];
+  const int bx = (int)std::min<int64_t>((len + 255) / 256, 16);
+  gather_steps_kernel<<<dim3(bx, m), 256, 0, st>>>(src, a, len, dst);
+  count_launch();
+  return cudaGetLastError();
+}
 
 cudaError_t sgd_update(cudaStream_t st, float *p, const float *g, int64_t n, float scale) {
   if (n <= 0) return cudaSuccess;

@@ -60,6 +60,9 @@ int loss_acc_parts();
 
 // The paper's `update` on externally summed tendencies (nf_update): p[i] -= scale * g[i].
 cudaError_t sgd_update(cudaStream_t st, float *p, const float *g, int64_t n, float scale);
+// copies m <= 64 contiguous runs of len floats, src + off[s] -> dst + s * len (src: device
+// memory or mapped pinned host memory; the e2e staging of the per-step target rows)
+cudaError_t gather_steps(cudaStream_t st, const float *src, const int64_t *off, int m, int64_t len, float *dst);
 cudaError_t loss_acc(cudaStream_t st, const float *A, const float *Y, int64_t n, int w,
                      double2 *part, float *out, float *step_loss);
 
