@@ -326,13 +326,15 @@ def main():
         tf32_burst = peaks["bf16_tflops"] * 1.1 / 2.25
         ach_tf = flops_per_sample(cfg["dims"]) * K * B / t_med / 1e12
     ach_f64 = flops_per_sample(cfg["dims"]) * K * B / t_med / 1e12
-    # DRAM traffic of the dominant kernel from a committed `ncu --set full` capture
+    # DRAM traffic of the roofline's kernel (c2: the fused kernel, `ncu --set full`; c3-c5: all
+    # kernels of one TF32 step, tools/step_traffic.py) from a committed capture
     # (profiles/traffic_c<id>.json: dram bytes read + written per SGD step), scaled to this launch
     traffic = None
     prof = os.path.join(ROOT, "profiles", f"traffic_c{cid}.json")
     if os.path.exists(prof) and args.math != "fp64":
         try:
-            traffic = json.load(open(prof))["bytes_per_step"] * K
+            tj = json.load(open(prof))
+            traffic = tj["bytes_per_step"] * K if tj.get("math", args.math) == args.math else None
         except Exception:
             traffic = None
 
