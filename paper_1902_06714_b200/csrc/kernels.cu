@@ -226,11 +226,14 @@ cudaError_t run_tc(cudaStream_t st, int M, int N, int K, const TcOp &a, const Tc
     return launch_tc<64, AMN, BMN, 1>(st, M, N, K, a, b, epi, ws);
   }
   g_last_engine = ENGINE_TC3;
-  // experiment: 128 x 256 tiles where they fill the GPU (c5 fp32 step 31.2 -> 27.2 ms) -- only
-  // NACC = 2 accumulators fit, and the truncating accumulation then breaks the 1e-4 bar (c5
-  // forward, K = 4096: 1.9e-4), so BN = 128 (4 accumulators) stays the default
+  // 128 x 256 tiles where they fill the GPU leave room for only NACC = 2 accumulators; the
+  // truncating accumulation then meets the 1e-4 bar for K <= 1024 (c3 forward / backward: fp32
+  // step 366 -> 327 us) but not at c5's K = 4096 (1.9e-4), which keeps BN = 128 unless
+  // NF_TC3_BN256=1 (experiment: c5 fp32 31.2 -> 27.2 ms); NF_TC3_NO_SHALLOW256=1 reverts
   static const bool bn256 = getenv("NF_TC3_BN256") != nullptr;
-  if (bn256 && N > 128 && tiles(256) >= fill) return launch_tc<256, AMN, BMN, 3>(st, M, N, K, a, b, epi, ws);
+  static const bool shallow256 = getenv("NF_TC3_NO_SHALLOW256") == nullptr;
+  if ((bn256 || (shallow256 && K <= 1024)) && N > 128 && tiles(256) >= fill)
+    return launch_tc<256, AMN, BMN, 3>(st, M, N, K, a, b, epi, ws);
   if (N > 64 && tiles(128) >= fill) return launch_tc<128, AMN, BMN, 3>(st, M, N, K, a, b, epi, ws);
   // under a wave but deep with an additive update (the c3 weight gradients, 1024 x 1024 x
   // 4096): 128 x 256 tiles split 4-way over K (L2 reductions into W) instead of 128 x 64 tiles
