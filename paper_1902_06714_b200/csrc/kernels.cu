@@ -128,7 +128,7 @@ bool make_map(CUtensorMap *m, const TcOp &o, int rows, int K, int box_rows) {
 
 template <int BN, bool AMN, bool BMN, int SPLIT, class Epi, int MAXST = 6, int EW = tc::kEpiWarps>
 cudaError_t launch_tc(cudaStream_t st, int M, int N, int K, const TcOp &a, const TcOp &b, const Epi &epi,
-                      const Workspace &ws) {
+                      const Workspace &ws, int force_splits = 0) {
   using C = tc::Cfg<BN, SPLIT, MAXST, EW>;
   auto kern = tc::gemm_tc_kernel<BN, AMN, BMN, SPLIT, Epi, MAXST, EW>;
   static bool attr = false;
@@ -159,6 +159,7 @@ cudaError_t launch_tc(cudaStream_t st, int M, int N, int K, const TcOp &a, const
     while (!red && splits > 1 && (size_t)splits * M * N > ws.partial_floats) --splits;
     splits = std::max(splits, 1);
   }
+  if (force_splits > 1 && red) splits = std::min(force_splits, nkb);
   const int kbper = (nkb + splits - 1) / splits;
   splits = (nkb + kbper - 1) / kbper;  // no empty K-chunk
   red = red && splits > 1;
@@ -234,6 +235,12 @@ cudaError_t run_tc(cudaStream_t st, int M, int N, int K, const TcOp &a, const Tc
   static const bool shallow256 = getenv("NF_TC3_NO_SHALLOW256") == nullptr;
   if ((bn256 || (shallow256 && K <= 1024)) && N > 128 && tiles(256) >= fill)
     return launch_tc<256, AMN, BMN, 3>(st, M, N, K, a, b, epi, ws);
+  if constexpr (Epi::kRed) {  // experiment: deep additive GEMMs in wide tiles, K split so each
+    // of the 2 accumulators sums no more than the 128-wide tiles' 4 do over the whole K
+    static const bool deep256 = getenv("NF_TC3_DEEP256") != nullptr;
+    if (deep256 && !epi.store_only && N > 128 && tiles(256) >= fill && K > 1024)
+      return launch_tc<256, AMN, BMN, 3>(st, M, N, K, a, b, epi, ws, 2);
+  }
   if (N > 64 && tiles(128) >= fill) return launch_tc<128, AMN, BMN, 3>(st, M, N, K, a, b, epi, ws);
   // under a wave but deep with an additive update (the c3 weight gradients, 1024 x 1024 x
   // 4096): 128 x 256 tiles split 4-way over K (L2 reductions into W) instead of 128 x 64 tiles
