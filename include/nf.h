@@ -45,7 +45,16 @@ enum {
     NF_EINVAL = -1,       /* bad argument: see nf_last_error()            */
     NF_ECUDA = -2,        /* CUDA runtime error (message has its string)  */
     NF_ENOMEM = -3,       /* device allocation failed                     */
-    NF_ENODEV = -4        /* no sm_100 device: there is NO CPU fallback   */
+    NF_ENODEV = -4,       /* no sm_100 device: there is NO CPU fallback   */
+    /* nf_load / nf_load_as format errors, one code per kind     */
+    NF_EFMT_MAGIC = -5,       /* not a file of this library                   */
+    NF_EFMT_VERSION = -6,     /* unsupported format version                   */
+    NF_EFMT_PRECISION = -7,   /* unknown precision tag, or a precision other
+                                 than the one requested (never narrowed)      */
+    NF_EFMT_TRUNCATED = -8,   /* fewer parameters than the dims imply         */
+    NF_EFMT_ACTIVATION = -9,  /* missing / unknown activation name            */
+    NF_EFMT_DIMS = -10,       /* bad dims header                              */
+    NF_EIO = -11              /* the file cannot be opened / written          */
 };
 
 /* Numerics mode of the contractions (nf_set_math).
@@ -155,16 +164,25 @@ int nf_loss(nf_net *net, const float *x, const float *y, int64_t n, float *loss)
 int nf_accuracy(nf_net *net, const float *x, const float *y, int64_t n, float *acc);
 
 /* Saving and loading networks to and from file (the paper gives no format, this
- * library's is text: a header line "nf-b200-net 1", n_dims, the dims, the activation spec,
- * then the nf_param_count parameters in the flat layout, one per line, 9 significant digits,
- * exact for fp32).  nf_save synchronises; NF_EINVAL if the file cannot be written.
- * Host file I/O; the parameters are read back from the device first. */
+ * library's is text): a header line "nf-b200-net 2", n_dims, the dims, the activation spec,
+ * the precision tag "fp32" or "fp64", then the nf_param_count parameters in the flat layout,
+ * one per line -- 9 significant digits for fp32, 17 for fp64 (both exact: a round trip is
+ * bitwise).  In NF_MATH_FP64 the double parameters are written, never narrowed.
+ * nf_save synchronises; NF_EIO if the file cannot be written.  Host file I/O. */
 int nf_save(nf_net *net, const char *path);
 
-/* Loads a file written by nf_save: parses the whole file first (NF_EINVAL on a missing file
- * or a malformed one, before any device work), then nf_net_create + nf_set_params; *out is
- * owned by the caller (nf_net_destroy).  The numerics mode starts as NF_MATH_FP32. */
+/* Loads a file written by nf_save (version 1 files, without a precision line, are fp32):
+ * parses and validates the header (magic, version, dims, activation, precision) before the
+ * payload, then the whole payload, before any device work; each kind of format error returns
+ * its own NF_EFMT_* code.  Then nf_net_create + the parameters; an fp64 file gives a net in
+ * NF_MATH_FP64 holding the exact doubles, an fp32 file one in NF_MATH_FP32.  *out is owned by
+ * the caller (nf_net_destroy). */
 int nf_load(const char *path, nf_net **out);
+
+/* nf_load that also states the numerics mode the caller wants: an fp64 file into
+ * NF_MATH_FP32 / NF_MATH_TF32, or an fp32 file into NF_MATH_FP64, is rejected with
+ * NF_EFMT_PRECISION (never silently narrowed or widened).  math = -1: as nf_load. */
+int nf_load_as(const char *path, int math, nf_net **out);
 
 /* Thread-local text of the last error ("" if none). */
 const char *nf_last_error(void);
@@ -173,6 +191,18 @@ const char *nf_last_error(void);
  * gpu_launches claim), including the kernels of each replay of the CUDA graph
  * nf_train_steps captures for generic nets. */
 int64_t nf_launch_count(void);
+
+/* Debug launch log (tests: which kernel instantiations a workload launches).
+ * nf_debug_log_enable(1) clears the log and records every later launch of this library as
+ * one line "<demangled kernel name> grid=(x,y,z) block=T smem=S [variant]" (variant: the
+ * epilogue mode, split-K "splitk-red" / "splitk-partial", the K6 cluster size); 0 stops
+ * recording.  NF_LOG_LAUNCHES=1 in the environment enables it at load.  A CUDA graph's
+ * kernels are logged once, when it is captured, not on replay.  Host-only, no errors. */
+void nf_debug_log_enable(int on);
+
+/* Copies the launch log (NUL-terminated, truncated to cap bytes) into buf (buf may be NULL,
+ * cap <= 0: nothing copied) and returns the bytes the whole log needs including the NUL. */
+int64_t nf_debug_log_read(char *buf, int64_t cap);
 
 #ifdef __cplusplus
 }

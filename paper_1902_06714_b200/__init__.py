@@ -24,6 +24,9 @@ _PKG = os.path.dirname(os.path.abspath(__file__))
 LIB_PATH = os.path.join(_PKG, "libnf_b200.so")
 
 NF_OK, NF_EINVAL, NF_ECUDA, NF_ENOMEM, NF_ENODEV = 0, -1, -2, -3, -4
+# nf_load format errors (one code per kind) and file I/O
+NF_EFMT_MAGIC, NF_EFMT_VERSION, NF_EFMT_PRECISION, NF_EFMT_TRUNCATED = -5, -6, -7, -8
+NF_EFMT_ACTIVATION, NF_EFMT_DIMS, NF_EIO = -9, -10, -11
 NF_MATH_FP32, NF_MATH_TF32, NF_MATH_FP64 = 0, 1, 2
 
 
@@ -54,6 +57,9 @@ def _load() -> ctypes.CDLL:
         "nf_update": (ctypes.c_int, [P, P, I64, F, I64]),
         "nf_save": (ctypes.c_int, [P, ctypes.c_char_p]),
         "nf_load": (ctypes.c_int, [ctypes.c_char_p, ctypes.POINTER(P)]),
+        "nf_load_as": (ctypes.c_int, [ctypes.c_char_p, ctypes.c_int, ctypes.POINTER(P)]),
+        "nf_debug_log_enable": (None, [ctypes.c_int]),
+        "nf_debug_log_read": (I64, [ctypes.c_char_p, I64]),
         "nf_loss": (ctypes.c_int, [P, P, P, I64, ctypes.POINTER(F)]),
         "nf_accuracy": (ctypes.c_int, [P, P, P, I64, ctypes.POINTER(F)]),
         "nf_last_error": (ctypes.c_char_p, []),
@@ -80,7 +86,8 @@ def lib() -> ctypes.CDLL:
 # Every symbol include/nf.h declares (checked by tests/test_abi.py).
 EXPORTS = ("nf_net_create", "nf_net_destroy", "nf_set_stream", "nf_set_math", "nf_param_count",
            "nf_get_params", "nf_set_params", "nf_output", "nf_train_batch", "nf_train_steps",
-           "nf_grad", "nf_update", "nf_save", "nf_load", "nf_loss", "nf_accuracy", "nf_last_error", "nf_launch_count")
+           "nf_grad", "nf_update", "nf_save", "nf_load", "nf_load_as", "nf_loss", "nf_accuracy", "nf_last_error",
+           "nf_launch_count", "nf_debug_log_enable", "nf_debug_log_read")
 
 
 def _check(rc: int):
@@ -167,6 +174,24 @@ def nf_load(path: str):
     h = ctypes.c_void_p()
     _check(lib().nf_load(os.fsencode(path), ctypes.byref(h)))
     return h
+
+
+def nf_load_as(path: str, math: int):
+    h = ctypes.c_void_p()
+    _check(lib().nf_load_as(os.fsencode(path), math, ctypes.byref(h)))
+    return h
+
+
+def nf_debug_log_enable(on: bool = True):
+    lib().nf_debug_log_enable(1 if on else 0)
+
+
+def nf_debug_log_read() -> list[str]:
+    """The launch log as a list of lines (see include/nf.h)."""
+    need = int(lib().nf_debug_log_read(None, 0))
+    buf = ctypes.create_string_buffer(need)
+    lib().nf_debug_log_read(buf, need)
+    return [l for l in buf.value.decode().split("\n") if l]
 
 
 def nf_loss(net, x, y, n: int) -> float:
@@ -263,10 +288,11 @@ class Net:
         nf_save(self.h, path)
 
     @classmethod
-    def load(cls, path: str, stream=None):
-        """A Net from a file written by save() (nf_load)."""
+    def load(cls, path: str, stream=None, math: int | None = None):
+        """A Net from a file written by save() (nf_load; with math: nf_load_as, which rejects a
+        file of another precision)."""
         net = cls.__new__(cls)
-        net.h = nf_load(path)
+        net.h = nf_load(path) if math is None else nf_load_as(path, math)
         with open(path) as f:
             f.readline(); f.readline()
             net.dims = [int(v) for v in f.readline().split()]

@@ -18,10 +18,11 @@ NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
 FLAGS = [
     "-gencode", "arch=compute_100a,code=sm_100a",
     "-O3", "-lineinfo", "-std=c++17",
-    "-Xcompiler", "-fPIC", "-shared",
+    "-Xcompiler", "-fPIC",
     "-Xptxas", "-O3",
     f"-I{os.path.join(ROOT, 'include')}",
 ]
+OBJ = os.path.join(PKG, "build_obj")
 
 
 def sources():
@@ -40,9 +41,22 @@ def up_to_date() -> bool:
 
 
 def build(force: bool = False, verbose: bool = False) -> str:
+    """Each .cu compiled to an object in parallel (nvcc -c), then one nvcc -shared link."""
     if not force and up_to_date():
         return LIB
-    cmd = [NVCC, *FLAGS, *sources(), "-o", LIB + ".tmp", "-lcuda"]
+    os.makedirs(OBJ, exist_ok=True)
+    objs, procs = [], []
+    for src in sources():
+        obj = os.path.join(OBJ, os.path.basename(src)[:-3] + ".o")
+        objs.append(obj)
+        cmd = [NVCC, *FLAGS, "-c", src, "-o", obj]
+        if verbose:
+            print(" ".join(cmd))
+        procs.append((src, subprocess.Popen(cmd)))
+    bad = [src for src, p in procs if p.wait() != 0]
+    if bad:
+        raise subprocess.CalledProcessError(1, f"nvcc {bad}")
+    cmd = [NVCC, "-gencode", "arch=compute_100a,code=sm_100a", "-shared", *objs, "-o", LIB + ".tmp", "-lcuda"]
     if verbose:
         print(" ".join(cmd))
     subprocess.check_call(cmd)

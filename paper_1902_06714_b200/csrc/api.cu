@@ -445,62 +445,126 @@ int nf_net_create(const int32_t *dims, int32_t n_dims, const char *activation, u
 }
 
 // ---- saving and loading networks (the paper's feature list; file format of this
-// library, the paper does not give one): text, "nf-b200-net 1", n_dims, dims, activation
-// spec, then the flat parameters (include/nf.h layout) one per line with 9 significant
-// digits (exact for fp32).
+// library, the paper does not give one).  Text:
+//   "nf-b200-net 2" / n_dims / dims / activation spec / precision "fp32" | "fp64" /
+//   the flat parameters (include/nf.h layout), one per line: %.9g for fp32 (exact), %.17g for
+//   fp64 (exact).  Version 1 files (no precision line) are fp32.  The header is parsed and
+//   validated before the payload; every kind of format error has its own code.
 int nf_save(nf_net *net, const char *path) {
   if (int rc = check_net(net)) return rc;
   if (!path) return fail(NF_EINVAL, "path is NULL");
-  std::vector<float> p(net->nparams);
-  if (int rc = nf_get_params(net, p.data(), net->nparams)) return rc;
+  const bool f64 = net->math == NF_MATH_FP64;
+  std::vector<float> p;
+  std::vector<double> p64;
+  if (f64) {  // the double parameters themselves: never narrowed
+    p64.resize(net->nparams);
+    NF_CUDA(cudaMemcpyAsync(p64.data(), net->params64, net->nparams * sizeof(double), cudaMemcpyDeviceToHost,
+                            net->stream));
+    NF_CUDA(cudaStreamSynchronize(net->stream));
+  } else {
+    p.resize(net->nparams);
+    if (int rc = nf_get_params(net, p.data(), net->nparams)) return rc;
+  }
   FILE *f = fopen(path, "w");
-  if (!f) return fail(NF_EINVAL, "cannot open '%s' for writing", path);
-  fprintf(f, "nf-b200-net 1\n%d\n", (int)net->dims.size());
+  if (!f) return fail(NF_EIO, "cannot open '%s' for writing", path);
+  fprintf(f, "nf-b200-net 2\n%d\n", (int)net->dims.size());
   for (size_t i = 0; i < net->dims.size(); ++i) fprintf(f, "%d%c", net->dims[i], i + 1 < net->dims.size() ? ' ' : '\n');
-  fprintf(f, "%s\n", net->act_spec.c_str());
-  for (float v : p) fprintf(f, "%.9g\n", v);
+  fprintf(f, "%s\n%s\n", net->act_spec.c_str(), f64 ? "fp64" : "fp32");
+  if (f64)
+    for (double v : p64) fprintf(f, "%.17g\n", v);
+  else
+    for (float v : p) fprintf(f, "%.9g\n", v);
   const bool ok = fclose(f) == 0;
-  return ok ? NF_OK : fail(NF_EINVAL, "writing '%s' failed", path);
+  return ok ? NF_OK : fail(NF_EIO, "writing '%s' failed", path);
 }
 
-int nf_load(const char *path, nf_net **out) {
+int nf_load_as(const char *path, int math, nf_net **out) {
   if (!out) return fail(NF_EINVAL, "out is NULL");
   *out = nullptr;
   if (!path) return fail(NF_EINVAL, "path is NULL");
+  if (math != -1 && math != NF_MATH_FP32 && math != NF_MATH_TF32 && math != NF_MATH_FP64)
+    return fail(NF_EINVAL, "unknown math mode %d", math);
   FILE *f = fopen(path, "r");
-  if (!f) return fail(NF_EINVAL, "cannot open '%s'", path);
-  char magic[32] = {0}, spec[256] = {0};
+  if (!f) return fail(NF_EIO, "cannot open '%s'", path);
+  char magic[32] = {0}, spec[256] = {0}, prec[16] = {0};
   int ver = 0, nd = 0;
   std::vector<int32_t> dims;
-  std::vector<float> p;
+  std::vector<double> p;
   int rc = NF_OK;
-  if (fscanf(f, "%31s %d %d", magic, &ver, &nd) != 3 || strcmp(magic, "nf-b200-net") != 0 || ver != 1 || nd < 2 ||
-      nd > 1024) {
-    rc = fail(NF_EINVAL, "'%s' is not an nf-b200 network file", path);
+  bool f64 = false;
+  if (fscanf(f, "%31s", magic) != 1 || strcmp(magic, "nf-b200-net") != 0) {
+    rc = fail(NF_EFMT_MAGIC, "'%s' is not an nf-b200 network file (magic)", path);
+  } else if (fscanf(f, "%d", &ver) != 1 || (ver != 1 && ver != 2)) {
+    rc = fail(NF_EFMT_VERSION, "'%s': unsupported format version", path);
+  } else if (fscanf(f, "%d", &nd) != 1 || nd < 2 || nd > 1024) {
+    rc = fail(NF_EFMT_DIMS, "'%s': bad number of dims", path);
   } else {
     dims.resize(nd);
-    int64_t np = 0;
     for (int i = 0; i < nd && rc == NF_OK; ++i)
-      if (fscanf(f, "%d", &dims[i]) != 1 || dims[i] < 1) rc = fail(NF_EINVAL, "'%s': bad dims", path);
-    for (int l = 1; l < nd && rc == NF_OK; ++l) np += (int64_t)dims[l] * dims[l - 1] + dims[l];
-    if (rc == NF_OK && fscanf(f, "%255s", spec) != 1) rc = fail(NF_EINVAL, "'%s': no activation", path);
+      if (fscanf(f, "%d", &dims[i]) != 1 || dims[i] < 1) rc = fail(NF_EFMT_DIMS, "'%s': bad dims", path);
+    if (rc == NF_OK && fscanf(f, "%255s", spec) != 1) rc = fail(NF_EFMT_ACTIVATION, "'%s': no activation", path);
+    if (rc == NF_OK) {  // the activation spec: validated before any payload is read
+      const std::string sp = spec;
+      int names = 0;
+      for (size_t b = 0;; ++names) {
+        const size_t e = sp.find(',', b);
+        if (parse_act(sp.substr(b, e == std::string::npos ? std::string::npos : e - b)) < 0) {
+          rc = fail(NF_EFMT_ACTIVATION, "'%s': unknown activation '%s'", path, spec);
+          break;
+        }
+        if (e == std::string::npos) { ++names; break; }
+        b = e + 1;
+      }
+      if (rc == NF_OK && names != 1 && names != 2 && names != nd - 1)
+        rc = fail(NF_EFMT_ACTIVATION, "'%s': activation spec '%s' has %d names", path, spec, names);
+    }
+    if (rc == NF_OK && ver == 2) {
+      if (fscanf(f, "%15s", prec) != 1 || (strcmp(prec, "fp32") != 0 && strcmp(prec, "fp64") != 0))
+        rc = fail(NF_EFMT_PRECISION, "'%s': unknown precision tag", path);
+      f64 = strcmp(prec, "fp64") == 0;
+    }
+    if (rc == NF_OK && math != -1 && f64 != (math == NF_MATH_FP64))
+      rc = fail(NF_EFMT_PRECISION, "'%s' holds %s parameters, %s requested (never narrowed or widened silently)",
+                path, f64 ? "fp64" : "fp32", math == NF_MATH_FP64 ? "fp64" : "fp32");
     if (rc == NF_OK) {
+      int64_t np = 0;
+      for (int l = 1; l < nd; ++l) np += (int64_t)dims[l] * dims[l - 1] + dims[l];
       p.resize(np);
       for (int64_t i = 0; i < np && rc == NF_OK; ++i)
-        if (fscanf(f, "%f", &p[i]) != 1) rc = fail(NF_EINVAL, "'%s': %lld of %lld parameters", path, (long long)i, (long long)np);
+        if (fscanf(f, "%lf", &p[i]) != 1)
+          rc = fail(NF_EFMT_TRUNCATED, "'%s': %lld of %lld parameters", path, (long long)i, (long long)np);
+      if (rc == NF_OK && !f64)
+        for (int64_t i = 0; i < np && rc == NF_OK; ++i)
+          if ((double)(float)p[i] != p[i]) rc = fail(NF_EFMT_PRECISION, "'%s': parameter %lld is not an fp32 value", path, (long long)i);
     }
   }
   fclose(f);
   if (rc != NF_OK) return rc;
   nf_net *net = nullptr;
   if ((rc = nf_net_create(dims.data(), nd, spec, 0, &net))) return rc;
-  if ((rc = nf_set_params(net, p.data(), (int64_t)p.size()))) {
+  std::vector<float> p32(p.begin(), p.end());
+  if ((rc = nf_set_params(net, p32.data(), (int64_t)p32.size()))) {
     nf_net_destroy(net);
     return rc;
+  }
+  if (f64 || math == NF_MATH_TF32) {
+    if ((rc = nf_set_math(net, f64 ? NF_MATH_FP64 : math))) {
+      nf_net_destroy(net);
+      return rc;
+    }
+  }
+  if (f64) {  // the exact doubles
+    cudaError_t e = cudaMemcpy(net->params64, p.data(), p.size() * sizeof(double), cudaMemcpyHostToDevice);
+    if (e != cudaSuccess) {
+      nf_net_destroy(net);
+      return fail(NF_ECUDA, "nf_load: %s", cudaGetErrorString(e));
+    }
   }
   *out = net;
   return NF_OK;
 }
+
+int nf_load(const char *path, nf_net **out) { return nf_load_as(path, -1, out); }
 
 void nf_net_destroy(nf_net *net) {
   if (!net) return;

@@ -182,6 +182,7 @@ cudaError_t run64(cudaStream_t st, Args64 g, const Epi &epi, double *partial, si
     g.partial = nullptr;
     gemm64_kernel<8, 8, AK, BKM, Epi><<<dim3((g.N + 127) / 128, (g.M + 127) / 128, 1), 256, 0, st>>>(g, epi);
     count_launch();
+    log_launch(reinterpret_cast<const void *>(gemm64_kernel<8, 8, AK, BKM, Epi>), dim3((g.N + 127) / 128, (g.M + 127) / 128, 1), dim3(256), 0);
     return cudaGetLastError();
   }
   const int tm = (g.M + 63) / 64, tn = (g.N + 63) / 64;
@@ -198,10 +199,12 @@ cudaError_t run64(cudaStream_t st, Args64 g, const Epi &epi, double *partial, si
   g.partial = splits > 1 ? partial : nullptr;
   gemm64_kernel<4, 4, AK, BKM, Epi><<<dim3(tn, tm, splits), 256, 0, st>>>(g, epi);
   count_launch();
+  log_launch(reinterpret_cast<const void *>(gemm64_kernel<4, 4, AK, BKM, Epi>), dim3(tn, tm, splits), dim3(256), 0);
   if (splits > 1) {
     const int64_t MN = (int64_t)g.M * g.N;
     splitk64<Epi><<<(int)std::min<int64_t>((MN + 255) / 256, 4 * kSMs), 256, 0, st>>>(partial, splits, g.M, g.N, epi);
     count_launch();
+    log_launch(reinterpret_cast<const void *>(splitk64<Epi>), dim3((int)std::min<int64_t>((MN + 255) / 256, 4 * kSMs)), dim3(256), 0);
   }
   return cudaGetLastError();
 }
@@ -316,11 +319,13 @@ cudaError_t gemm64_grad(cudaStream_t st, int M, int N, int K, const double *D, c
 cudaError_t f64_widen(cudaStream_t st, const float *s, double *d, int64_t n) {
   convert_kernel_fd<<<(int)std::min<int64_t>((n + 255) / 256, 8 * kSMs), 256, 0, st>>>(s, d, n);
   count_launch();
+  log_launch(reinterpret_cast<const void *>(convert_kernel_fd), dim3((int)std::min<int64_t>((n + 255) / 256, 8 * kSMs)), dim3(256), 0);
   return cudaGetLastError();
 }
 cudaError_t f64_round(cudaStream_t st, const double *s, float *d, int64_t n) {
   convert_kernel_df<<<(int)std::min<int64_t>((n + 255) / 256, 8 * kSMs), 256, 0, st>>>(s, d, n);
   count_launch();
+  log_launch(reinterpret_cast<const void *>(convert_kernel_df), dim3((int)std::min<int64_t>((n + 255) / 256, 8 * kSMs)), dim3(256), 0);
   return cudaGetLastError();
 }
 
@@ -328,6 +333,7 @@ cudaError_t f64_update(cudaStream_t st, double *p, const float *g, int64_t n, do
   if (n <= 0) return cudaSuccess;
   update_kernel64<<<(int)std::min<int64_t>((n + 255) / 256, 8 * kSMs), 256, 0, st>>>(p, g, n, scale);
   count_launch();
+  log_launch(reinterpret_cast<const void *>(update_kernel64), dim3((int)std::min<int64_t>((n + 255) / 256, 8 * kSMs)), dim3(256), 0);
   return cudaGetLastError();
 }
 
@@ -337,6 +343,8 @@ cudaError_t loss_acc64(cudaStream_t st, const double *A, const float *Y, int64_t
   loss_acc64_kernel<<<blocks, 256, 0, st>>>(A, Y, n, w, part);
   loss_acc64_final<<<1, 32, 0, st>>>(part, blocks, n, out, step_loss);
   count_launch(2);
+  log_launch(reinterpret_cast<const void *>(loss_acc64_kernel), dim3(blocks), dim3(256), 0);
+  log_launch(reinterpret_cast<const void *>(loss_acc64_final), dim3(1), dim3(32), 0);
   return cudaGetLastError();
 }
 

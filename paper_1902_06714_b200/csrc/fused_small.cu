@@ -32,6 +32,7 @@
 #include <cstdio>
 #include <cstdlib>
 #include <cstring>
+#include <mutex>
 
 #include "fused_small.cuh"
 #include "gemm_tc.cuh"
@@ -769,6 +770,9 @@ int fused_small_train_steps(FusedSmall &fs, cudaStream_t st, const std::vector<i
                             int64_t batch, const int64_t *starts, int64_t n_steps, float eta,
                             float *step_loss) {
   if (env_int("NF_DISABLE_FUSED", 0)) return FUSED_NOT_APPLICABLE;
+  // the co_sum here is an L2 bulk-add in arrival order: NF_SPLITK_DETERMINISTIC=1 (bitwise
+  // repeatable training, reading R12) takes the generic per-layer path, whose sums are fixed-order
+  if (getenv("NF_SPLITK_DETERMINISTIC")) return FUSED_NOT_APPLICABLE;
   if (dims.size() != 3) return FUSED_NOT_APPLICABLE;
   const int n0 = dims[0], H = dims[1], O = dims[2];
   if (H > 32 || O > 32 || batch > (int64_t)148 * kMaxRows) return FUSED_NOT_APPLICABLE;
@@ -792,14 +796,20 @@ int fused_small_train_steps(FusedSmall &fs, cudaStream_t st, const std::vector<i
   }
   if (wpad > 256) return FUSED_NOT_APPLICABLE;  // TMA box limit / smem budget
 
-  static bool attr_done = false;
-  if (!attr_done) {
-    for (auto k : {fused_small_kernel<false, -1, -1>, fused_small_kernel<true, -1, -1>,
-                   fused_small_kernel<false, ACT_SIGMOID, ACT_SIGMOID>}) {
-      cudaFuncSetAttribute(k, cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
-      cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024);
+  {  // (per device: the attributes belong to the device context)
+    static std::mutex mu;
+    static unsigned done = 0;
+    int dev = 0;
+    cudaGetDevice(&dev);
+    std::lock_guard<std::mutex> lk(mu);
+    if (!(done & (1u << (dev & 31)))) {
+      for (auto k : {fused_small_kernel<false, -1, -1>, fused_small_kernel<true, -1, -1>,
+                     fused_small_kernel<false, ACT_SIGMOID, ACT_SIGMOID>}) {
+        cudaFuncSetAttribute(k, cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
+        cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024);
+      }
+      done |= 1u << (dev & 31);
     }
-    attr_done = true;
   }
   // tensor-core variant: TMA-aligned x, pixel slices of <= 128 columns, <= kTcRows rows per cluster
   // (opt-in, NF_FUSED_TC=1: at N = 32 the 3xTF32 MMAs are shared-memory-bandwidth bound and no
@@ -919,10 +929,14 @@ int fused_small_train_steps(FusedSmall &fs, cudaStream_t st, const std::vector<i
     cfg.dynamicSmemBytes = smem;
     cfg.stream = st;
     const bool sig = act_h == ACT_SIGMOID && act_o == ACT_SIGMOID;
-    e = tc    ? cudaLaunchKernelEx(&cfg, fused_small_kernel<true, -1, -1>, p, tmX, tmXK, tmXM)
-        : sig ? cudaLaunchKernelEx(&cfg, fused_small_kernel<false, ACT_SIGMOID, ACT_SIGMOID>, p, tmX, tmXK, tmXM)
-              : cudaLaunchKernelEx(&cfg, fused_small_kernel<false, -1, -1>, p, tmX, tmXK, tmXM);
+    auto kern = tc    ? fused_small_kernel<true, -1, -1>
+                : sig ? fused_small_kernel<false, ACT_SIGMOID, ACT_SIGMOID>
+                      : fused_small_kernel<false, -1, -1>;
+    e = cudaLaunchKernelEx(&cfg, kern, p, tmX, tmXK, tmXM);
     count_launch();
+    char nt[64];
+    snprintf(nt, sizeof nt, "cluster=%d steps=%lld", C, (long long)n_steps);
+    log_launch(reinterpret_cast<const void *>(kern), cfg.gridDim, cfg.blockDim, smem, nt);
   }
   if (e != cudaSuccess) {
     snprintf(g_fs_err, sizeof g_fs_err, "launch (C=%d G=%d smem=%zu): %s", C, G, smem, cudaGetErrorString(e));

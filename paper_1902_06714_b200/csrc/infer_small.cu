@@ -223,16 +223,16 @@ size_t infer_small_smem(int n0) {
 
 cudaError_t infer_small(cudaStream_t st, const std::vector<int> &dims, int act_h, int act_o, const float *params,
                         const float *X, int64_t n, float *out) {
-  static bool attr = false;
-  if (!attr) {
-    cudaFuncSetAttribute(infer_small_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024);
-    attr = true;
+  {
+    cudaError_t e = set_max_smem(reinterpret_cast<const void *>(infer_small_kernel), 227 * 1024);
+    if (e != cudaSuccess) return e;
   }
   const int64_t ntiles = (n + kRows - 1) / kRows;
   const int blocks = (int)std::max<int64_t>(1, std::min<int64_t>((ntiles + kG - 1) / kG, 148));
   infer_small_kernel<<<blocks, kT * kG, infer_small_smem(dims[0]), st>>>(X, n, dims[0], dims[1], dims[2], act_h,
                                                                          act_o, params, out);
   count_launch();
+  log_launch(reinterpret_cast<const void *>(infer_small_kernel), dim3(blocks), dim3(kT * kG), infer_small_smem(dims[0]));
   return cudaGetLastError();
 }
 

@@ -3,6 +3,7 @@
 #include <algorithm>
 
 #include <cstdlib>
+#include <cstdio>
 #include <cstring>
 
 #include "gemm_tc.cuh"
@@ -22,6 +23,19 @@ constexpr int kSMs = 148;
 // the next kernel's CTAs are scheduled while the current one drains, run their prologue
 // (barrier init, TMEM allocation, tensor-map prefetch) and block in griddepcontrol.wait until
 // it has completed.  NF_NO_PDL=1 turns it off.
+thread_local const char *g_note = nullptr;  // runtime variant of the next launch (launch log)
+thread_local char g_note_buf[96];
+
+// runtime variant of an epilogue for the launch log: forward mode, fused bias update, SGD or store
+const char *epi_note(const EpiFwd &e) { return e.mode == 0 ? "fwd-hidden" : e.mode == 1 ? "fwd-output" : "fwd-infer"; }
+const char *epi_note(const EpiBwd &e) { return e.bias ? "bwd+bias-red" : "bwd"; }
+const char *epi_note(const EpiGrad &e) { return e.store_only ? "grad-store" : "grad-sgd"; }
+const char *note(const char *epi, const char *split) {
+  if (!launch_log_on()) return nullptr;
+  snprintf(g_note_buf, sizeof g_note_buf, "%s%s%s", epi, split ? " " : "", split ? split : "");
+  return g_note_buf;
+}
+
 bool pdl_enabled() {
   static int v = -1;
   if (v < 0) v = getenv("NF_NO_PDL") ? 0 : 1;
@@ -41,6 +55,8 @@ cudaError_t launch_k(void (*kern)(KArgs...), dim3 grid, dim3 block, size_t smem,
   cfg.attrs = at;
   cfg.numAttrs = pdl_enabled() ? 1 : 0;
   count_launch();
+  log_launch(reinterpret_cast<const void *>(kern), grid, block, smem, g_note);
+  g_note = nullptr;
   return cudaLaunchKernelEx(&cfg, kern, static_cast<KArgs>(args)...);
 }
 
@@ -70,6 +86,7 @@ cudaError_t launch_cfg(cudaStream_t st, GemmArgs g, const Epi &epi, const Worksp
   g.kchunk = splits > 1 ? kchunk : std::max(g.K, 1);
   g.partial = splits > 1 ? ws.partial : nullptr;
   dim3 grid(tn, tm, splits);
+  g_note = note(epi_note(epi), splits > 1 ? "splitk-partial" : nullptr);
   cudaError_t e = launch_k(gemm_simt<BM, BN, BK, TM, TN, AK, BKM, Epi>, grid, dim3((BM / TM) * (BN / TN)), 0, st, g, epi);
   if (e != cudaSuccess) return e;
   if (splits > 1) {
@@ -131,11 +148,9 @@ cudaError_t launch_tc(cudaStream_t st, int M, int N, int K, const TcOp &a, const
                       const Workspace &ws, int force_splits = 0) {
   using C = tc::Cfg<BN, SPLIT, MAXST, EW>;
   auto kern = tc::gemm_tc_kernel<BN, AMN, BMN, SPLIT, Epi, MAXST, EW>;
-  static bool attr = false;
-  if (!attr) {
-    cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, C::SMEM);
+  {
+    cudaError_t e = set_max_smem(reinterpret_cast<const void *>(kern), C::SMEM);
     if (e != cudaSuccess) return e;
-    attr = true;
   }
   CUtensorMap ta, tb;
   if (!make_map(&ta, a, M, K, tc::BM) || !make_map(&tb, b, N, K, BN)) return cudaErrorInvalidValue;
@@ -164,6 +179,7 @@ cudaError_t launch_tc(cudaStream_t st, int M, int N, int K, const TcOp &a, const
   splits = (nkb + kbper - 1) / kbper;  // no empty K-chunk
   red = red && splits > 1;
   tc::TileArgs g{M, N, K, kbper * tc::BK, (splits > 1 && !red) ? ws.partial : nullptr, red ? 1 : 0};
+  g_note = note(epi_note(epi), red ? "splitk-red" : (splits > 1 ? "splitk-partial" : nullptr));
   cudaError_t e = launch_k(kern, dim3(tn, tm, splits), dim3(C::THREADS), C::SMEM, st, ta, tb, g, epi);
   if (e != cudaSuccess) return e;
   if (splits > 1 && !red) {
@@ -181,15 +197,14 @@ template <bool AMN, bool BMN, class Epi>
 cudaError_t launch_tc_persistent(cudaStream_t st, int M, int N, int K, const TcOp &a, const TcOp &b, const Epi &epi) {
   using C = tc::Cfg<256, 1>;
   auto kern = tc::gemm_tc_persistent<256, AMN, BMN, Epi>;
-  static bool attr = false;
-  if (!attr) {
-    cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, C::SMEM);
+  {
+    cudaError_t e = set_max_smem(reinterpret_cast<const void *>(kern), C::SMEM);
     if (e != cudaSuccess) return e;
-    attr = true;
   }
   CUtensorMap ta, tb;
   if (!make_map(&ta, a, M, K, tc::BM) || !make_map(&tb, b, N, K, 256)) return cudaErrorInvalidValue;
   const int tiles = ((M + tc::BM - 1) / tc::BM) * ((N + 255) / 256);
+  g_note = note(epi_note(epi), nullptr);
   return launch_k(kern, dim3(std::min(tiles, kSMs)), dim3(tc::kThreads), C::SMEM, st, ta, tb, M, N, K, epi);
 }
 
@@ -237,7 +252,9 @@ cudaError_t run_tc(cudaStream_t st, int M, int N, int K, const TcOp &a, const Tc
     return launch_tc<256, AMN, BMN, 3>(st, M, N, K, a, b, epi, ws);
   if constexpr (Epi::kRed) {  // experiment: deep additive GEMMs in wide tiles, K split so each
     // of the 2 accumulators sums no more than the 128-wide tiles' 4 do over the whole K
-    static const bool deep256 = getenv("NF_TC3_DEEP256") != nullptr;
+    // (only with split-K terms reduced into W: without them -- NF_SPLITK_DETERMINISTIC -- the two
+    // accumulators would sum all of K = 16384, which misses the 1e-4 bar)
+    static const bool deep256 = getenv("NF_TC3_DEEP256") != nullptr && getenv("NF_SPLITK_DETERMINISTIC") == nullptr;
     if (deep256 && !epi.store_only && N > 128 && tiles(256) >= fill && K > 1024)
       return launch_tc<256, AMN, BMN, 3>(st, M, N, K, a, b, epi, ws, 2);
   }
@@ -673,6 +690,7 @@ cudaError_t gather_steps(cudaStream_t st, const float *src, const int64_t *off, 
   const int bx = (int)std::min<int64_t>((len + 255) / 256, 16);
   gather_steps_kernel<<<dim3(bx, m), 256, 0, st>>>(src, a, len, dst);
   count_launch();
+  log_launch(reinterpret_cast<const void *>(gather_steps_kernel), dim3(bx, m), dim3(256), 0);
   return cudaGetLastError();
 }
 
@@ -709,22 +727,14 @@ cudaError_t out_layer_train_fused(cudaStream_t st, int n, int H, int nL, const f
   const int rpb = (n + R - 1) / R;
   const int blocks = (n + rpb - 1) / rpb;
   const size_t smem = out_layer_smem(n, H, nL);
-  static bool attr = false;
-  if (!attr) {
-    cudaFuncSetAttribute(out_layer_train<16, 4>, cudaFuncAttributeMaxDynamicSharedMemorySize, kOutSmemMax);
-    cudaFuncSetAttribute(out_layer_train<16, 8>, cudaFuncAttributeMaxDynamicSharedMemorySize, kOutSmemMax);
-    cudaFuncSetAttribute(out_layer_train<16, 16>, cudaFuncAttributeMaxDynamicSharedMemorySize, kOutSmemMax);
-    attr = true;
+  for (const void *k : {reinterpret_cast<const void *>(out_layer_train<16, 4>), reinterpret_cast<const void *>(out_layer_train<16, 8>),
+                        reinterpret_cast<const void *>(out_layer_train<16, 16>), reinterpret_cast<const void *>(out_layer_train<10, 4>),
+                        reinterpret_cast<const void *>(out_layer_train<10, 8>), reinterpret_cast<const void *>(out_layer_train<10, 16>)}) {
+    cudaError_t e = set_max_smem(k, kOutSmemMax);
+    if (e != cudaSuccess) return e;
   }
   float *lp = part + (int64_t)blocks * nL * (H + 1);
   if (nL <= 10) {  // (MNIST-like 10-wide outputs: no idle unrolled output slots)
-    static bool attr10 = false;
-    if (!attr10) {
-      cudaFuncSetAttribute(out_layer_train<10, 4>, cudaFuncAttributeMaxDynamicSharedMemorySize, kOutSmemMax);
-      cudaFuncSetAttribute(out_layer_train<10, 8>, cudaFuncAttributeMaxDynamicSharedMemorySize, kOutSmemMax);
-      cudaFuncSetAttribute(out_layer_train<10, 16>, cudaFuncAttributeMaxDynamicSharedMemorySize, kOutSmemMax);
-      attr10 = true;
-    }
     if (H <= 512)
       return launch_k(out_layer_train<10, 4>, dim3(blocks), dim3(256), smem, st, A, S, W, bias, Y, AL, DL, n, H, nL,
                       act, rpb, part, lp);
@@ -760,10 +770,9 @@ cudaError_t gemm_fwd(cudaStream_t st, int M, int N, int K, const float *A, const
   if (use_tc(M, N, K, a, b)) return run_tc<false, false>(st, M, N, K, a, b, epi, ws);
   g_last_engine = ENGINE_SIMT;
   if (N <= 16 && K % 4 == 0 && (size_t)N * K * 4 <= 96 * 1024 && tc_ok(a) && tc_ok(b) && M >= 256) {
-    static bool attr = false;
-    if (!attr) {
-      cudaFuncSetAttribute(fwd_smalln<16, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, 96 * 1024);
-      attr = true;
+    {
+      cudaError_t e = set_max_smem(reinterpret_cast<const void *>(fwd_smalln<16, true>), 96 * 1024);
+      if (e != cudaSuccess) return e;
     }
     static const int per_sm = getenv("NF_SMALLN_PER_SM") ? atoi(getenv("NF_SMALLN_PER_SM")) : 2;
     static const bool nostage = getenv("NF_SMALLN_NOSTAGE") != nullptr;
@@ -779,7 +788,9 @@ cudaError_t gemm_fwd(cudaStream_t st, int M, int N, int K, const float *A, const
 bool gemm_bwd_fuses_bias(int M, int N, int K, const float *D, const float *W) {
   // the tensor-core path only (its strip epilogue sums 32 rows per reduction); up to 16384
   // rows = 512 reductions per bias element (c5: 9.17 -> 9.05 ms per step)
-  static const bool off = getenv("NF_NO_BIAS_FUSE") != nullptr;
+  // NF_SPLITK_DETERMINISTIC=1: off (its L2 reductions arrive in any order; the column-sum
+  // kernels then sum the chunks in a fixed order)
+  static const bool off = getenv("NF_NO_BIAS_FUSE") != nullptr || getenv("NF_SPLITK_DETERMINISTIC") != nullptr;
   const TcOp a{D, K, false}, b{W, N, true};
   static const int maxm = getenv("NF_BIAS_FUSE_MAXM") ? atoi(getenv("NF_BIAS_FUSE_MAXM")) : 16384;
   return !off && M <= maxm && use_tc(M, N, K, a, b);

@@ -10,6 +10,13 @@ namespace nf {
 
 extern int64_t g_launches;  // kernels launched by this library (nf_launch_count)
 inline void count_launch(int n = 1) { __atomic_add_fetch(&g_launches, n, __ATOMIC_RELAXED); }
+// launch log (launchlog.cu; NF_LOG_LAUNCHES=1 or nf_debug_log_enable): demangled kernel name,
+// grid, block, dynamic smem and a note naming the runtime variant (e.g. "red" split-K terms)
+bool launch_log_on();
+// cudaFuncSetAttribute(MaxDynamicSharedMemorySize) once per (kernel, device, bytes): the
+// attribute is per device context, so a process driving several GPUs sets it on each
+cudaError_t set_max_smem(const void *kern, int bytes);
+void log_launch(const void *func, dim3 grid, dim3 block, size_t smem, const char *note = nullptr);
 
 // Split-K partial workspace owned by the net (fixed capacity in floats) and the numerics
 // mode of the contractions (NF_MATH_FP32 = 0: fp32 SIMT or 3xTF32 tensor cores;

@@ -291,6 +291,7 @@ int single_cta_train_steps(cudaStream_t st, const std::vector<int> &dims, const 
   auto launch = [&](void (*kern)(SingleParams), int threads) {
     cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024);
     kern<<<1, threads, smem, st>>>(p);
+    log_launch(reinterpret_cast<const void *>(kern), dim3(1), dim3(threads), smem);
   };
   switch ((T == 32 ? 20 : T == 256 ? 0 : 10) + (L <= 4 ? L : 0)) {
     case 21: launch(single_cta_kernel<32, 1>, 32); break;

@@ -126,19 +126,40 @@ def test_header_documents_every_entry_point():
 
 
 def test_load_rejects_missing_and_malformed_files_before_the_device(nf, tmp_path):
-    """nf_load parses the whole file before any device work: NF_EINVAL, not NF_ENODEV."""
+    """nf_load validates the header, then the payload, before any device work; each kind of
+    format error has its own code, never NF_ENODEV on this GPU-less host."""
     with pytest.raises(nf.NFError) as e:
         nf.nf_load(str(tmp_path / "missing.net"))
-    assert e.value.code == nf.NF_EINVAL
+    assert e.value.code == nf.NF_EIO
     bad = [
-        "not a network\n",
-        "nf-b200-net 1\n3\n3 5 2\nsigmoid\n0.5\n",          # 1 of 32 parameters
-        "nf-b200-net 1\n3\n3 0 2\nsigmoid\n",               # a zero width
-        "nf-b200-net 2\n3\n3 5 2\nsigmoid\n",               # unknown version
+        ("not a network\n", nf.NF_EFMT_MAGIC),
+        ("nf-b200-net 7\n3\n3 5 2\nsigmoid\n", nf.NF_EFMT_VERSION),
+        ("nf-b200-net 1\n3\n3 5 2\nsigmoid\n0.5\n", nf.NF_EFMT_TRUNCATED),    # 1 of 32 parameters
+        ("nf-b200-net 1\n3\n3 0 2\nsigmoid\n", nf.NF_EFMT_DIMS),                # a zero width
+        ("nf-b200-net 2\n3\n3 5 2\nsoftmax\nfp32\n", nf.NF_EFMT_ACTIVATION),
+        ("nf-b200-net 2\n3\n3 5 2\nrelu,tanh,sigmoid\nfp32\n", nf.NF_EFMT_ACTIVATION),  # 3 names, 2 layers
+        ("nf-b200-net 2\n3\n3 5 2\nsigmoid\nfp16\n", nf.NF_EFMT_PRECISION),
+        ("nf-b200-net 2\n3\n3 5 2\nsigmoid\nfp32\n" + "0.1\n" * 32, nf.NF_EFMT_PRECISION),  # 0.1 is not fp32
+        ("nf-b200-net 2\n3\n3 5 2\nsigmoid\nfp64\n" + "0.5\n" * 31, nf.NF_EFMT_TRUNCATED),
     ]
-    for i, text in enumerate(bad):
+    for i, (text, code) in enumerate(bad):
         path = tmp_path / f"bad{i}.net"
         path.write_text(text)
         with pytest.raises(nf.NFError) as e:
             nf.nf_load(str(path))
-        assert e.value.code == nf.NF_EINVAL, text
+        assert e.value.code == code, text
+    # a precision other than the requested one is rejected before the device, never narrowed
+    path = tmp_path / "f64.net"
+    path.write_text("nf-b200-net 2\n3\n3 5 2\nsigmoid\nfp64\n" + "0.1\n" * 32)
+    with pytest.raises(nf.NFError) as e:
+        nf.nf_load_as(str(path), nf.NF_MATH_FP32)
+    assert e.value.code == nf.NF_EFMT_PRECISION
+    path.write_text("nf-b200-net 2\n3\n3 5 2\nsigmoid\nfp32\n" + "0.5\n" * 32)
+    with pytest.raises(nf.NFError) as e:
+        nf.nf_load_as(str(path), nf.NF_MATH_FP64)
+    assert e.value.code == nf.NF_EFMT_PRECISION
+    # well-formed files get as far as the device (no GPU here)
+    for math in (-1, nf.NF_MATH_FP32):
+        with pytest.raises(nf.NFError) as e:
+            nf.nf_load_as(str(path), math)
+        assert e.value.code == nf.NF_ENODEV

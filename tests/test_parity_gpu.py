@@ -498,3 +498,57 @@ def test_fused_output_layer_step_losses(dims, act, batch):
     ref, ref_loss = oracle.Oracle(dims, act).train_steps(p, X, Y, batch, starts, 0.4)
     assert rel_err(loss.cpu().numpy(), ref_loss) <= FP32_BAR
     assert rel_err(gpu_params(net), ref) <= FP32_BAR
+
+
+def test_save_load_fp64_keeps_the_doubles(tmp_path):
+    """NF_MATH_FP64 nets save their double parameters (17 digits, never narrowed):
+    save -> load -> save gives the identical file, the loaded net is in NF_MATH_FP64,
+    and asking for an fp32 net from that file is rejected (NF_EFMT_PRECISION)."""
+    dims, act = [37, 45, 13], "tanh,sigmoid"
+    p = synth.random_params(84, dims, 0.5)
+    net = make_net(dims, act, p)
+    net.set_math(nf.NF_MATH_FP64)
+    x, y = synth.random_batch(85, 64, 37, 13)
+    net.train_batch(dev(x), dev(y), 0.3)      # doubles that are not fp32 values
+    a, b = str(tmp_path / "a.net"), str(tmp_path / "b.net")
+    net.save(a)
+    text = open(a).read().split("\n")
+    assert text[4] == "fp64"
+    assert any(float(np.float32(float(v))) != float(v) for v in text[5:] if v)
+    back = nf.Net.load(a)
+    back.save(b)
+    assert open(a).read() == open(b).read()
+    assert np.array_equal(back.output(dev(x)).cpu().numpy(), net.output(dev(x)).cpu().numpy())
+    with pytest.raises(nf.NFError) as e:
+        nf.Net.load(a, math=nf.NF_MATH_FP32)
+    assert e.value.code == nf.NF_EFMT_PRECISION
+
+
+def test_deterministic_mode_is_bitwise_repeatable(tmp_path):
+    """NF_SPLITK_DETERMINISTIC=1 (reading R12): two trainings from the same seed give
+    bitwise-identical saved networks (SPEC acceptance 7) -- on the small-net path (the generic
+    kernels replace K6, whose co_sum is an arrival-order L2 reduction) and on a wide net whose
+    tensor-core steps use split-K and fused bias updates by default."""
+    import subprocess
+    import sys
+    script = r'''
+import sys, numpy as np, torch
+sys.path.insert(0, sys.argv[1])
+import synth, paper_1902_06714_b200 as nf
+out = sys.argv[2]
+for tag, dims, act, B, math in [("c2", [784, 30, 10], "sigmoid", 1000, nf.NF_MATH_FP32),
+                                ("wide", [784, 1024, 1024, 10], "tanh", 4096, nf.NF_MATH_TF32),
+                                ("wide3", [784, 1024, 1024, 10], "tanh", 4096, nf.NF_MATH_FP32)]:
+    X, Y = synth.random_batch(86, 3 * B, dims[0], dims[-1], "uniform")
+    p = synth.random_params(87, dims, 0.05)
+    for run in (0, 1):
+        net = nf.Net(dims, act); net.set_math(math); net.set_params(torch.from_numpy(p).cuda())
+        net.train_steps(torch.from_numpy(X).cuda(), torch.from_numpy(Y).cuda(), B, [0, B, 2 * B, 7], 0.5)
+        net.save(f"{out}/{tag}{run}.net")
+'''
+    import os
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    env = dict(os.environ, NF_SPLITK_DETERMINISTIC="1", NF_LOG_LAUNCHES="1")
+    subprocess.run([sys.executable, "-c", script, root, str(tmp_path)], check=True, env=env, timeout=600)
+    for tag in ("c2", "wide", "wide3"):
+        assert open(tmp_path / f"{tag}0.net").read() == open(tmp_path / f"{tag}1.net").read(), tag

@@ -119,7 +119,8 @@ def test_tc_c5_full_width_grad():
 
 
 # ------------------------------------------------------------------ full-size launches
-@pytest.mark.parametrize("cid,math", [(5, nf.NF_MATH_TF32), (5, nf.NF_MATH_FP32), (3, nf.NF_MATH_TF32)])
+@pytest.mark.parametrize("cid,math", [(5, nf.NF_MATH_TF32), (5, nf.NF_MATH_FP32), (3, nf.NF_MATH_TF32),
+                                      (3, nf.NF_MATH_FP32), (4, nf.NF_MATH_TF32), (4, nf.NF_MATH_FP32)])
 def test_full_batch_forward_sampled_rows(cid, math):
     """nf_output over a full training batch (c5: 16384 rows, the persistent 1xTF32 GEMM in TF32
     mode; c3: 4096 rows) in the launch configuration bench.py times; 16 sampled rows against the
