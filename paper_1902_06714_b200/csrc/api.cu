@@ -105,6 +105,11 @@ struct nf_net {
   cudaStream_t stream = nullptr;
   int64_t nparams = 0;
   float *params = nullptr;               // device, flat layout of nf.h
+  // NF_MATH_TF32: the TF32-rounded shadow of the parameters (same layout; only the W blocks are
+  // read), the tensor-core operand in place of W.  Kept current by the SGD epilogues of the
+  // TF32 step; re-rounded from params when shadow_ok is false (any other writer of params).
+  float *params_t = nullptr;
+  bool shadow_ok = false;
   std::vector<int64_t> offW, offB;       // index 1..L
   // stash: A_l (activations) and S_l (sigma'(Z_l), overwritten by delta_l), l = 1..L
   int64_t ws_rows = 0;
@@ -141,6 +146,8 @@ struct nf_net {
   DevBuf stash64, partial64, grad64;
 
   float *W(int l) const { return params + offW[l]; }
+  float *Wt(int l) const { return params_t + offW[l]; }
+  bool tf32() const { return math == NF_MATH_TF32; }
   double *W64(int l) const { return params64 + offW[l]; }
   double *b64(int l) const { return params64 + offB[l]; }
   float *b(int l) const { return params + offB[l]; }
@@ -178,23 +185,38 @@ int ensure_ws(nf_net *net, int64_t rows) {
   return NF_OK;
 }
 
+// NF_MATH_TF32: make the weight shadow current (one rounding pass after any write of params
+// other than a TF32 step's own epilogues)
+int ensure_shadow(nf_net *net) {
+  if (!net->tf32() || net->shadow_ok) return NF_OK;
+  if (!net->params_t) NF_CUDA(cudaMalloc(&net->params_t, net->nparams * sizeof(float)));
+  NF_CUDA(round_tf32(net->stream, net->params, net->params_t, net->nparams));
+  net->shadow_ok = true;
+  return NF_OK;
+}
+
 // fwdprop over a batch.  mode: 0 train (stash A, S; output layer
 // S = delta_L), 2 inference (A only).  y only for mode 0.
 int forward(nf_net *net, const float *x, const float *y, int64_t n, int mode) {
   const float *in = x;
   const int L = net->L;
+  if (int rc = ensure_shadow(net)) return rc;
+  const bool t = net->tf32();
   net->out_fused = mode == 0 && L >= 2 &&
                    out_layer_fusable((int)n, net->dims[L - 1], net->dims[L], net->A[L - 1], net->S[L - 1], net->W(L));
   for (int l = 1; l <= net->L; ++l) {
     if (l == L && net->out_fused) {  // K1+K2 of the output layer, K3 of layer L-1, K4(L) partials
       NF_CUDA(out_layer_train_fused(net->stream, (int)n, net->dims[L - 1], net->dims[L], net->A[L - 1],
                                     net->S[L - 1], net->W(L), net->b(L), y, net->A[L], net->S[L], net->act_o,
-                                    net->part_out.as<float>()));
+                                    net->part_out.as<float>(), t ? 1 : 0));
       break;
     }
     const int lm = (mode == 2) ? 2 : (l < net->L ? 0 : 1);
-    EpiFwd epi{net->b(l), net->A[l], net->S[l], y, net->dims[l], net->act(l), lm};
-    NF_CUDA(gemm_fwd(net->stream, (int)n, net->dims[l], net->dims[l - 1], in, net->W(l), epi, net->ws));
+    // TF32: a hidden layer's A and the output layer's delta_L are operands of later tensor-core
+    // contractions -> stored RN-rounded (the net's output A_L never is)
+    EpiFwd epi{net->b(l), net->A[l], net->S[l], y, net->dims[l], net->act(l), lm, (t && (lm == 1 || l < L)) ? 1 : 0};
+    NF_CUDA(gemm_fwd(net->stream, (int)n, net->dims[l], net->dims[l - 1], in, net->W(l), epi, net->ws,
+                     t ? net->Wt(l) : nullptr));
     in = net->A[l];
   }
   return NF_OK;
@@ -237,8 +259,10 @@ int backward(nf_net *net, const float *x, int64_t n, float eta, float *grad, flo
   for (int l = net->L; l >= 1; --l) {
     const int nl = net->dims[l], nk = net->dims[l - 1];
     const bool fused = l == net->L && net->out_fused;  // K3(L) ran inside the forward kernel
+    const bool t = net->tf32();
     if (l > 1 && !fused) {
       EpiBwd eb{net->S[l - 1], nk};
+      eb.rnd = t ? 1 : 0;
       const float *aprev2 = l > 2 ? net->A[l - 2] : x;  // the operand of layer l-1's weight GEMM
       if (!grad && gemm_bwd_fuses_bias((int)n, nk, nl, net->S[l], net->W(l)) &&
           gemm_grad_tc(nk, net->dims[l - 2], (int)n, net->S[l - 1], aprev2)) {
@@ -246,13 +270,14 @@ int backward(nf_net *net, const float *x, int64_t n, float eta, float *grad, flo
         eb.bscale = scale;
         bias_done[l - 1] = 1;
       }
-      NF_CUDA(gemm_bwd(main_st, (int)n, nk, nl, net->S[l], net->W(l), eb, net->ws));
+      NF_CUDA(gemm_bwd(main_st, (int)n, nk, nl, net->S[l], net->W(l), eb, net->ws, t ? net->Wt(l) : nullptr));
     }
     NF_CUDA(cudaEventRecord(net->ev[l], main_st));  // K3(l) done with W_l and delta_l is final
     NF_CUDA(cudaStreamWaitEvent(side, net->ev[l], 0));
     const float *aprev = l > 1 ? net->A[l - 1] : x;
     EpiGrad eg = grad ? EpiGrad{grad + net->offW[l], grad + net->offB[l], nk, nk, 0.0f, 1}
                       : EpiGrad{net->W(l), net->b(l), nk, nk, scale, 0};
+    if (!grad && t) eg.Wt = net->Wt(l);  // the update also refreshes the TF32 shadow of W_l
     if (fused) NF_CUDA(out_layer_grad_final(side, (int)n, nk, nl, net->part_out.as<float>(), eg, step_loss));
     else if (l == 1 && net->L > 1 && side != main_st && (net->math != NF_MATH_TF32 || n <= 2048))
       // the main stream is idle after the last K3: K4(1) there, concurrent with K4(2) on the side
@@ -530,12 +555,13 @@ int nf_load_as(const char *path, int math, nf_net **out) {
       int64_t np = 0;
       for (int l = 1; l < nd; ++l) np += (int64_t)dims[l] * dims[l - 1] + dims[l];
       p.resize(np);
-      for (int64_t i = 0; i < np && rc == NF_OK; ++i)
-        if (fscanf(f, "%lf", &p[i]) != 1)
+      for (int64_t i = 0; i < np && rc == NF_OK; ++i) {
+        float v32 = 0.0f;  // fp32 files: 9 digits parsed to the nearest float = the saved value
+        if (f64 ? fscanf(f, "%lf", &p[i]) != 1 : fscanf(f, "%f", &v32) != 1)
           rc = fail(NF_EFMT_TRUNCATED, "'%s': %lld of %lld parameters", path, (long long)i, (long long)np);
-      if (rc == NF_OK && !f64)
-        for (int64_t i = 0; i < np && rc == NF_OK; ++i)
-          if ((double)(float)p[i] != p[i]) rc = fail(NF_EFMT_PRECISION, "'%s': parameter %lld is not an fp32 value", path, (long long)i);
+        else if (!f64)
+          p[i] = v32;
+      }
     }
   }
   fclose(f);
@@ -571,6 +597,7 @@ void nf_net_destroy(nf_net *net) {
   cudaStreamSynchronize(net->stream);
   if (net->params) cudaFree(net->params);
   if (net->params64) cudaFree(net->params64);
+  if (net->params_t) cudaFree(net->params_t);
   net->stash64.release();
   net->partial64.release();
   net->grad64.release();
@@ -615,6 +642,7 @@ int nf_set_math(nf_net *net, int mode) {
     NF_CUDA(f64_round(net->stream, net->params64, net->params, net->nparams));
     fused_small_invalidate(net->fused);
   }
+  if (mode != net->math) net->shadow_ok = false;
   net->math = mode;
   net->ws.math = mode;
   return NF_OK;
@@ -653,6 +681,7 @@ int nf_set_params(nf_net *net, const float *src, int64_t count) {
   const bool dev = is_device_ptr(src);
   NF_CUDA(cudaMemcpyAsync(net->params, src, count * sizeof(float),
                           dev ? cudaMemcpyDeviceToDevice : cudaMemcpyHostToDevice, net->stream));
+  net->shadow_ok = false;
   if (net->math == NF_MATH_FP64) NF_CUDA(f64_widen(net->stream, net->params, net->params64, count));
   if (!dev) NF_CUDA(cudaStreamSynchronize(net->stream));
   fused_small_invalidate(net->fused);
@@ -735,6 +764,7 @@ static int train_steps_device(nf_net *net, const float *dX, const float *dY, int
                                            batch, net->d_starts.as<int64_t>(), n_steps, eta, step_loss);
     if (src == 0) {
       fused_small_invalidate(net->fused);
+      net->shadow_ok = false;
       return NF_OK;
     }
     if (src != SINGLE_NOT_APPLICABLE)
@@ -742,12 +772,14 @@ static int train_steps_device(nf_net *net, const float *dX, const float *dY, int
   }
   int rc = net->math == NF_MATH_FP64 ? FUSED_NOT_APPLICABLE : fused_small_train_steps(net->fused, net->stream, net->dims, net->act_h, net->act_o,
                                    net->params, dX, dY, dN, batch, st.data(), n_steps, eta, step_loss);
+  if (rc == 0) net->shadow_ok = false;  // K6 updated params
   if (rc == FUSED_NOT_APPLICABLE) {
     // Generic nets: the per-step kernel sequence of all n_steps, captured once as a CUDA
     // graph and replayed while the arguments repeat (removes the host launch gaps between the
     // ~10-50 kernels of each step).  Workspaces are sized before capture.
     if ((rc = net->math == NF_MATH_FP64 ? ensure_ws64(net, batch) : ensure_ws(net, batch))) return rc;
     if ((rc = ensure_side(net))) return rc;
+    if ((rc = ensure_shadow(net))) return rc;  // before capture: the graph keeps it current
     NF_CUDA(net->red.ensure(red_bytes()));
     std::vector<int64_t> key = {(int64_t)(uintptr_t)dX, (int64_t)(uintptr_t)dY, N, batch, n_steps,
                                 (int64_t)(uintptr_t)step_loss, (int64_t)(uintptr_t)net->stream, net->math,
@@ -931,6 +963,7 @@ int nf_update(nf_net *net, const float *grad, int64_t count, float eta, int64_t 
   const double scale = (double)eta / (double)n;
   if (net->math == NF_MATH_FP64) NF_CUDA(f64_update(net->stream, net->params64, dg, count, scale));
   else NF_CUDA(sgd_update(net->stream, net->params, dg, count, (float)scale));
+  net->shadow_ok = false;
   fused_small_invalidate(net->fused);
   if (dg != grad) NF_CUDA(cudaStreamSynchronize(net->stream));
   return NF_OK;

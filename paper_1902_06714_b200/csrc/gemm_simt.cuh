@@ -36,20 +36,23 @@ struct GemmArgs {
 // Forward: mode 0 hidden (A = sigma(z), S = sigma'(z)); mode 1 output layer in
 // training (A = sigma(z), S = (sigma(z) - y) sigma'(z) = delta_L, S:150 /
 // quadratic cost P:111); mode 2 inference (A = sigma(z) only).
+// rnd (NF_MATH_TF32): the values this epilogue stores as the operand of a later tensor-core
+// contraction -- a hidden layer's A, the output layer's delta_L in S -- are rounded to the
+// nearest TF32 value (tf32_rn; the output layer's A, the net's output, never is).
 struct EpiFwd {
   static constexpr bool kRed = false;
-  const float *bias; float *A; float *S; const float *Y; int ld; int act; int mode;
+  const float *bias; float *A; float *S; const float *Y; int ld; int act; int mode; int rnd = 0;
   __device__ __forceinline__ float load(int m, int n) const {
     return mode == 1 ? Y[(int64_t)m * ld + n] : 0.0f;
   }
   __device__ __forceinline__ void store(int m, int n, float acc, float y) const {
     const float z = acc + bias[n];
     const int64_t i = (int64_t)m * ld + n;
-    if (mode == 2) { A[i] = act_only(act, z); return; }
+    if (mode == 2) { const float a = act_only(act, z); A[i] = rnd ? tf32_rn(a) : a; return; }
     float a, s;
     act_fwd(act, z, a, s);
-    A[i] = a;
-    S[i] = mode == 0 ? s : (a - y) * s;
+    A[i] = (rnd && mode == 0) ? tf32_rn(a) : a;
+    S[i] = mode == 0 ? s : (rnd ? tf32_rn((a - y) * s) : (a - y) * s);
   }
   __device__ __forceinline__ void operator()(int m, int n, float acc) const { store(m, n, acc, load(m, n)); }
 
@@ -57,7 +60,7 @@ struct EpiFwd {
   // row r at v[33 r].  The activation and the mode are compile-time inside the strip (one
   // switch per strip), and each 8-row group evaluates its 8 activations unconditionally so the
   // eight dependent exp/rcp chains interleave; only the stores are predicated.
-  template <int K, int MODE>
+  template <int K, int MODE, bool RND>
   __device__ __forceinline__ void strip_km(int m0, int mlim, int n, const float *v) const {
     const float bn = bias[n];
     const int rows = min(32, mlim - m0);
@@ -79,18 +82,24 @@ struct EpiFwd {
       for (int u = 0; u < 8; ++u) {
         if (r0 + u < rows) {
           const int64_t i = (int64_t)(m0 + r0 + u) * ld + n;
-          A[i] = a[u];
+          A[i] = (RND && MODE != 1) ? tf32_rn(a[u]) : a[u];
           if (MODE == 0) S[i] = s[u];
-          if (MODE == 1) S[i] = (a[u] - y[u]) * s[u];
+          if (MODE == 1) S[i] = RND ? tf32_rn((a[u] - y[u]) * s[u]) : (a[u] - y[u]) * s[u];
         }
       }
     }
   }
   template <int K>
   __device__ __forceinline__ void strip_t(int m0, int mlim, int n, const float *v) const {
-    if (mode == 0) strip_km<K, 0>(m0, mlim, n, v);
-    else if (mode == 1) strip_km<K, 1>(m0, mlim, n, v);
-    else strip_km<K, 2>(m0, mlim, n, v);
+    if (rnd) {
+      if (mode == 0) strip_km<K, 0, true>(m0, mlim, n, v);
+      else if (mode == 1) strip_km<K, 1, true>(m0, mlim, n, v);
+      else strip_km<K, 2, true>(m0, mlim, n, v);
+    } else {
+      if (mode == 0) strip_km<K, 0, false>(m0, mlim, n, v);
+      else if (mode == 1) strip_km<K, 1, false>(m0, mlim, n, v);
+      else strip_km<K, 2, false>(m0, mlim, n, v);
+    }
   }
   __device__ __forceinline__ void strip(int m0, int mlim, int n, const float *v) const {
     switch (act) {
@@ -118,17 +127,20 @@ __device__ __forceinline__ void strip_generic(const E &e, int m0, int mlim, int 
 // With bias != nullptr the epilogue also applies the SGD update of the layer's bias from the
 // deltas it produces: b[n] -= bscale * sum_m delta[m][n] (its rows' share, an L2 reduction,
 // reading R12) -- the bias column sum then needs no kernel of its own.
+// rnd (NF_MATH_TF32): the stored delta (the next contractions' operand) is rounded to the
+// nearest TF32 value; the fused bias sum uses the unrounded deltas.
 struct EpiBwd {
   static constexpr bool kRed = false;
   float *SD; int ld;
   float *bias = nullptr; float bscale = 0.0f;
+  int rnd = 0;
   __device__ __forceinline__ float load(int m, int n) const { return SD[(int64_t)m * ld + n]; }
   __device__ __forceinline__ void store(int m, int n, float acc, float s) const {
-    SD[(int64_t)m * ld + n] = acc * s;
+    SD[(int64_t)m * ld + n] = rnd ? tf32_rn(acc * s) : acc * s;
   }
   __device__ __forceinline__ void operator()(int m, int n, float acc) const {
     const float d = acc * load(m, n);
-    SD[(int64_t)m * ld + n] = d;
+    SD[(int64_t)m * ld + n] = rnd ? tf32_rn(d) : d;
     if (bias) asm volatile("red.global.add.f32 [%0], %1;" ::"l"(bias + n), "f"(-bscale * d) : "memory");
   }
   __device__ __forceinline__ void strip(int m0, int mlim, int n, const float *v) const {
@@ -144,7 +156,7 @@ struct EpiBwd {
     for (int r = 0; r < 32; ++r)
       if (m0 + r < mlim) {
         const float d = v[33 * r] * aux[r];
-        SD[(int64_t)(m0 + r) * ld + n] = d;
+        SD[(int64_t)(m0 + r) * ld + n] = rnd ? tf32_rn(d) : d;
         sum += d;
       }
     asm volatile("red.global.add.f32 [%0], %1;" ::"l"(bias + n), "f"(-bscale * sum) : "memory");
@@ -153,20 +165,29 @@ struct EpiBwd {
 
 // Gradient: store = 0 applies W -= scale*G, b -= scale*g (scale =
 // eta/B, reading R3); store = 1 writes G, g (nf_grad).  Column n == nreal is the bias.
+// Wt (NF_MATH_TF32, SGD only): the TF32 shadow of W (same layout) the next step's tensor-core
+// contractions read; the update also stores tf32_rn(W') there.  (Split-K terms reduced into W
+// in L2 cannot: the launcher re-rounds the layer's shadow after such a launch.)
 struct EpiGrad {
   static constexpr bool kRed = true;   // the update is additive: split-K terms can go straight in
   float *W; float *b; int ldw; int nreal; float scale; int store_only;
+  float *Wt = nullptr;
   __device__ __forceinline__ float *at(int m, int n) const { return n < nreal ? W + (int64_t)m * ldw + n : b + m; }
   __device__ __forceinline__ float load(int m, int n) const { return store_only ? 0.0f : *at(m, n); }
   __device__ __forceinline__ void store(int m, int n, float acc, float w) const {
-    *at(m, n) = store_only ? acc : w - scale * acc;
+    if (store_only) { *at(m, n) = acc; return; }
+    const float w2 = w - scale * acc;
+    *at(m, n) = w2;
+    if (Wt && n < nreal) Wt[(int64_t)m * ldw + n] = tf32_rn(w2);
   }
   // one split-K term of the update: W[m][n] += -scale * acc as an L2 reduction (red, no return)
+  // (store_only: the term itself, into a zeroed tendency block)
   __device__ __forceinline__ void strip_red(int m0, int mlim, int n, const float *v) const {
     const int rows = min(32, mlim - m0);
+    const float f = store_only ? 1.0f : -scale;
 #pragma unroll 8
     for (int r = 0; r < rows; ++r)
-      asm volatile("red.global.add.f32 [%0], %1;" ::"l"(at(m0 + r, n)), "f"(-scale * v[33 * r]) : "memory");
+      asm volatile("red.global.add.f32 [%0], %1;" ::"l"(at(m0 + r, n)), "f"(f * v[33 * r]) : "memory");
   }
   __device__ __forceinline__ void operator()(int m, int n, float acc) const { store(m, n, acc, load(m, n)); }
   __device__ __forceinline__ void strip(int m0, int mlim, int n, const float *v) const {

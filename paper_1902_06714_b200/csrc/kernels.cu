@@ -163,7 +163,9 @@ cudaError_t launch_tc(cudaStream_t st, int M, int N, int K, const TcOp &a, const
   bool red = false;
   if constexpr (Epi::kRed) {
     static const bool det = getenv("NF_SPLITK_DETERMINISTIC") != nullptr;
-    red = !epi.store_only && !det;
+    // (nf_grad's store-only epilogue takes forced split-K terms the same way, into its zeroed
+    // output: the forced splits exist for accuracy, see run_tc)
+    red = !det && (!epi.store_only || force_splits > 1);
   }
   // Split-K when under half a wave and K >= 512; for an epilogue that is not additive (needs
   // the partials + a second kernel) only under a quarter wave (c4's layer 1, 64 tiles of
@@ -174,14 +176,23 @@ cudaError_t launch_tc(cudaStream_t st, int M, int N, int K, const TcOp &a, const
     while (!red && splits > 1 && (size_t)splits * M * N > ws.partial_floats) --splits;
     splits = std::max(splits, 1);
   }
-  if (force_splits > 1 && red) splits = std::min(force_splits, nkb);
+  if (force_splits > 1 && red) splits = std::max(splits, std::min(force_splits, nkb));
   const int kbper = (nkb + splits - 1) / splits;
   splits = (nkb + kbper - 1) / kbper;  // no empty K-chunk
   red = red && splits > 1;
+  if constexpr (Epi::kRed) {
+    if (red && epi.store_only) {  // the terms are added into the (zeroed) tendency block
+      cudaError_t e = cudaMemsetAsync(epi.W, 0, (size_t)M * epi.ldw * sizeof(float), st);
+      if (e != cudaSuccess) return e;
+    }
+  }
   tc::TileArgs g{M, N, K, kbper * tc::BK, (splits > 1 && !red) ? ws.partial : nullptr, red ? 1 : 0};
   g_note = note(epi_note(epi), red ? "splitk-red" : (splits > 1 ? "splitk-partial" : nullptr));
   cudaError_t e = launch_k(kern, dim3(tn, tm, splits), dim3(C::THREADS), C::SMEM, st, ta, tb, g, epi);
   if (e != cudaSuccess) return e;
+  if constexpr (Epi::kRed) {  // split-K terms went into W in L2: the TF32 shadow of W from the sum
+    if (red && epi.Wt) return round_tf32(st, epi.W, epi.Wt, (int64_t)M * epi.ldw);
+  }
   if (splits > 1 && !red) {
     const int64_t MN = (int64_t)M * N;
     const int blocks = (int)std::min<int64_t>((MN + 255) / 256, 4 * kSMs);
@@ -258,7 +269,16 @@ cudaError_t run_tc(cudaStream_t st, int M, int N, int K, const TcOp &a, const Tc
     if (deep256 && !epi.store_only && N > 128 && tiles(256) >= fill && K > 1024)
       return launch_tc<256, AMN, BMN, 3>(st, M, N, K, a, b, epi, ws, 2);
   }
-  if (N > 64 && tiles(128) >= fill) return launch_tc<128, AMN, BMN, 3>(st, M, N, K, a, b, epi, ws);
+  // Deep reductions (the c5 weight gradients, K = B = 16384): the tensor core's truncating fp32
+  // accumulation errs in proportion to the K-steps one accumulator sums (4 accumulators x 512
+  // K-steps: 1.1e-4 > the 1e-4 bar at c5, tests/test_fullsize_gpu.py), so an additive epilogue
+  // splits K into chunks of <= NF_TC3_KCHUNK (default 4096) whose terms are reduced into W in L2
+  int force = 1;
+  if constexpr (Epi::kRed) {
+    static const int kchunk = getenv("NF_TC3_KCHUNK") ? atoi(getenv("NF_TC3_KCHUNK")) : 4096;
+    if (kchunk > 0 && K > kchunk) force = (K + kchunk - 1) / kchunk;
+  }
+  if (N > 64 && tiles(128) >= fill) return launch_tc<128, AMN, BMN, 3>(st, M, N, K, a, b, epi, ws, force);
   // under a wave but deep with an additive update (the c3 weight gradients, 1024 x 1024 x
   // 4096): 128 x 256 tiles split 4-way over K (L2 reductions into W) instead of 128 x 64 tiles
   // over the whole K -- 2.5x fewer hi/lo conversions and operand bytes per flop (c3 fp32 step
@@ -434,8 +454,9 @@ bwd_smallk(const float *__restrict__ D, const float *__restrict__ W, int M, int 
           acc.w = fmaf(dk, w[k].w, acc.w);
         }
       }
-      *reinterpret_cast<float4 *>(epi.SD + (int64_t)m * epi.ld + n) =
-          make_float4(acc.x * sv[u].x, acc.y * sv[u].y, acc.z * sv[u].z, acc.w * sv[u].w);
+      float4 dv = make_float4(acc.x * sv[u].x, acc.y * sv[u].y, acc.z * sv[u].z, acc.w * sv[u].w);
+      if (epi.rnd) dv = make_float4(tf32_rn(dv.x), tf32_rn(dv.y), tf32_rn(dv.z), tf32_rn(dv.w));
+      *reinterpret_cast<float4 *>(epi.SD + (int64_t)m * epi.ld + n) = dv;
     }
   }
 }
@@ -543,7 +564,7 @@ __global__ void __launch_bounds__(256)
 out_layer_train(const float *__restrict__ A, float *__restrict__ S, const float *__restrict__ W,
                 const float *__restrict__ bias, const float *__restrict__ Y, float *__restrict__ AL,
                 float *__restrict__ DL, int n, int H, int nL, int act, int rows_per_block, float *__restrict__ part,
-                float *__restrict__ lpart) {
+                float *__restrict__ lpart, int rnd) {
   ptx::pdl_trigger();
   ptx::pdl_wait();
   __shared__ float lred[8];
@@ -614,7 +635,9 @@ out_layer_train(const float *__restrict__ A, float *__restrict__ S, const float 
             ffma2(t1, d[o], make_float2(w.z, w.w));
           }
         }
-        srow[k4] = make_float4(t0.x * sg.x, t0.y * sg.y, t1.x * sg.z, t1.y * sg.w);
+        float4 d = make_float4(t0.x * sg.x, t0.y * sg.y, t1.x * sg.z, t1.y * sg.w);
+        if (rnd) d = make_float4(tf32_rn(d.x), tf32_rn(d.y), tf32_rn(d.z), tf32_rn(d.w));  // a TC operand next
+        srow[k4] = d;
       }
     }
   }
@@ -673,6 +696,13 @@ __global__ void __launch_bounds__(256) gather_steps_kernel(const float *__restri
   for (int64_t i = (int64_t)blockIdx.x * 256 + threadIdx.x; i < len; i += (int64_t)gridDim.x * 256) q[i] = p[i];
 }
 
+__global__ void __launch_bounds__(256) round_tf32_kernel(const float *__restrict__ src, float *__restrict__ dst,
+                                                          int64_t n) {
+  ptx::pdl_trigger();
+  ptx::pdl_wait();
+  for (int64_t i = blockIdx.x * 256 + threadIdx.x; i < n; i += (int64_t)gridDim.x * 256) dst[i] = tf32_rn(src[i]);
+}
+
 __global__ void __launch_bounds__(256) sgd_update_kernel(float *__restrict__ p, const float *__restrict__ g, int64_t n,
                                                          float scale) {
   ptx::pdl_trigger();
@@ -692,6 +722,12 @@ cudaError_t gather_steps(cudaStream_t st, const float *src, const int64_t *off, 
   count_launch();
   log_launch(reinterpret_cast<const void *>(gather_steps_kernel), dim3(bx, m), dim3(256), 0);
   return cudaGetLastError();
+}
+
+cudaError_t round_tf32(cudaStream_t st, const float *src, float *dst, int64_t n) {
+  if (n <= 0) return cudaSuccess;
+  const int blocks = (int)std::min<int64_t>((n + 255) / 256, 8 * kSMs);
+  return launch_k(round_tf32_kernel, dim3(blocks), dim3(256), 0, st, src, dst, n);
 }
 
 cudaError_t sgd_update(cudaStream_t st, float *p, const float *g, int64_t n, float scale) {
@@ -722,7 +758,8 @@ bool out_layer_fusable(int n, int H, int nL, const float *A, const float *S, con
 }
 
 cudaError_t out_layer_train_fused(cudaStream_t st, int n, int H, int nL, const float *A, float *S, const float *W,
-                                  const float *bias, const float *Y, float *AL, float *DL, int act, float *part) {
+                                  const float *bias, const float *Y, float *AL, float *DL, int act, float *part,
+                                  int rnd) {
   const int R = out_layer_blocks(n, H);
   const int rpb = (n + R - 1) / R;
   const int blocks = (n + rpb - 1) / rpb;
@@ -737,21 +774,21 @@ cudaError_t out_layer_train_fused(cudaStream_t st, int n, int H, int nL, const f
   if (nL <= 10) {  // (MNIST-like 10-wide outputs: no idle unrolled output slots)
     if (H <= 512)
       return launch_k(out_layer_train<10, 4>, dim3(blocks), dim3(256), smem, st, A, S, W, bias, Y, AL, DL, n, H, nL,
-                      act, rpb, part, lp);
+                      act, rpb, part, lp, rnd);
     if (H <= 1024)
       return launch_k(out_layer_train<10, 8>, dim3(blocks), dim3(256), smem, st, A, S, W, bias, Y, AL, DL, n, H, nL,
-                      act, rpb, part, lp);
+                      act, rpb, part, lp, rnd);
     return launch_k(out_layer_train<10, 16>, dim3(blocks), dim3(256), smem, st, A, S, W, bias, Y, AL, DL, n, H, nL,
-                    act, rpb, part, lp);
+                    act, rpb, part, lp, rnd);
   }
   if (H <= 512)
     return launch_k(out_layer_train<16, 4>, dim3(blocks), dim3(256), smem, st, A, S, W, bias, Y, AL, DL, n, H, nL,
-                    act, rpb, part, part + (int64_t)blocks * nL * (H + 1));
+                    act, rpb, part, part + (int64_t)blocks * nL * (H + 1), rnd);
   if (H <= 1024)
     return launch_k(out_layer_train<16, 8>, dim3(blocks), dim3(256), smem, st, A, S, W, bias, Y, AL, DL, n, H, nL,
-                    act, rpb, part, part + (int64_t)blocks * nL * (H + 1));
+                    act, rpb, part, part + (int64_t)blocks * nL * (H + 1), rnd);
   return launch_k(out_layer_train<16, 16>, dim3(blocks), dim3(256), smem, st, A, S, W, bias, Y, AL, DL, n, H, nL,
-                  act, rpb, part, part + (int64_t)blocks * nL * (H + 1));
+                  act, rpb, part, part + (int64_t)blocks * nL * (H + 1), rnd);
 }
 
 cudaError_t out_layer_grad_final(cudaStream_t st, int n, int H, int nL, const float *part, const EpiGrad &epi,
@@ -765,8 +802,8 @@ cudaError_t out_layer_grad_final(cudaStream_t st, int n, int H, int nL, const fl
 }
 
 cudaError_t gemm_fwd(cudaStream_t st, int M, int N, int K, const float *A, const float *W,
-                     const EpiFwd &epi, const Workspace &ws) {
-  const TcOp a{A, K, false}, b{W, K, false};
+                     const EpiFwd &epi, const Workspace &ws, const float *Wtc) {
+  const TcOp a{A, K, false}, b{Wtc ? Wtc : W, K, false};
   if (use_tc(M, N, K, a, b)) return run_tc<false, false>(st, M, N, K, a, b, epi, ws);
   g_last_engine = ENGINE_SIMT;
   if (N <= 16 && K % 4 == 0 && (size_t)N * K * 4 <= 96 * 1024 && tc_ok(a) && tc_ok(b) && M >= 256) {
@@ -802,8 +839,8 @@ bool gemm_grad_tc(int M, int N, int K, const float *D, const float *Aprev) {
 }
 
 cudaError_t gemm_bwd(cudaStream_t st, int M, int N, int K, const float *D, const float *W,
-                     const EpiBwd &epi, const Workspace &ws) {
-  const TcOp a{D, K, false}, b{W, N, true};
+                     const EpiBwd &epi, const Workspace &ws, const float *Wtc) {
+  const TcOp a{D, K, false}, b{Wtc ? Wtc : W, N, true};
   if (use_tc(M, N, K, a, b)) return run_tc<false, true>(st, M, N, K, a, b, epi, ws);
   g_last_engine = ENGINE_SIMT;
   if (K <= 16 && N % 4 == 0 && epi.ld % 4 == 0 && (reinterpret_cast<uintptr_t>(W) & 15) == 0 &&

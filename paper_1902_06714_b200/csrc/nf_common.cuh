@@ -110,6 +110,17 @@ __device__ __forceinline__ void ffma2v(float2 &d, float2 a, float2 b) {
   asm("mov.b64 {%0, %1}, %2;" : "=f"(d.x), "=f"(d.y) : "l"(dd));
 }
 
+// x rounded to the nearest TF32 value (10-bit mantissa, ties away: cvt.rna), an fp32 bit
+// pattern whose low 13 mantissa bits are zero.  In NF_MATH_TF32 every tensor-core operand this
+// library produces (hidden activations, deltas, the weight shadow) is stored this way, so the
+// tensor core -- which reads fp32 bit patterns and truncates them to TF32 -- multiplies
+// round-to-nearest operands (reading R13).
+__device__ __forceinline__ float tf32_rn(float x) {
+  uint32_t r;
+  asm("cvt.rna.tf32.f32 %0, %1;" : "=r"(r) : "f"(x));
+  return __uint_as_float(r);
+}
+
 __device__ __forceinline__ float warp_sum(float v) {
 #pragma unroll
   for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);

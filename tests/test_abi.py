@@ -139,7 +139,6 @@ def test_load_rejects_missing_and_malformed_files_before_the_device(nf, tmp_path
         ("nf-b200-net 2\n3\n3 5 2\nsoftmax\nfp32\n", nf.NF_EFMT_ACTIVATION),
         ("nf-b200-net 2\n3\n3 5 2\nrelu,tanh,sigmoid\nfp32\n", nf.NF_EFMT_ACTIVATION),  # 3 names, 2 layers
         ("nf-b200-net 2\n3\n3 5 2\nsigmoid\nfp16\n", nf.NF_EFMT_PRECISION),
-        ("nf-b200-net 2\n3\n3 5 2\nsigmoid\nfp32\n" + "0.1\n" * 32, nf.NF_EFMT_PRECISION),  # 0.1 is not fp32
         ("nf-b200-net 2\n3\n3 5 2\nsigmoid\nfp64\n" + "0.5\n" * 31, nf.NF_EFMT_TRUNCATED),
     ]
     for i, (text, code) in enumerate(bad):
