@@ -43,7 +43,7 @@ import paper_1902_06714_b200 as nf  # noqa: E402
 MATH = {"fp32": nf.NF_MATH_FP32, "tf32": nf.NF_MATH_TF32}
 # relu kink band (fraction of the layer's rms pre-activation): >= ~50x the measured error of
 # the pre-activation sums in each mode (fp32: 3xTF32 / FFMA, TF32: RN-rounded operands)
-MARGIN = {"fp32": 3e-5, "tf32": 2e-3}
+MARGIN = {"fp32": 3e-5, "tf32": 1e-3}
 
 
 def dev(a):
@@ -60,7 +60,7 @@ def launch_keys(lines):
     return keys
 
 
-def select_rows(o, p, cid, act, B, margin, pool_factor=4):
+def select_rows(o, p, cid, act, B, margin, pool_factor=16):
     """B kink-free rows of config cid's seeded inputs (pool of up to pool_factor * B rows)."""
     cfg = synth.CONFIGS[cid]
     N = min(cfg["N"], pool_factor * B)
@@ -162,4 +162,4 @@ def test_full_size_step(name, cid, act, dims, math, B):
     missing = bench - tested
     assert not missing, f"bench launches not covered by {name}: {missing}"
     print(f"{name}: {len(tested)} kernel instantiations / variants covered: " +
-          " | ".join(sorted(f"{k[0].split('(')[0]} [{k[1]}]" for k in tested)))
+          " | ".join(sorted(f"{k[0].replace('(anonymous namespace)::', '').split('(')[0]} [{k[1]}]" for k in tested)))
