@@ -1,16 +1,25 @@
 #!/usr/bin/env python3
 """Benchmark of the hot path: minibatch SGD training of the paper's 784-30-10 MNIST net
-(BASELINE.json configs[1], "config 2"), synthetic digit-shaped data, on B200.
+(BASELINE.json configs[1], "config 2"), synthetic digit-shaped data, on B200 -- plus, in the
+same run, the wide configurations 3-5 in both numerics modes under "configs".
 
     python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference] [--config 2]
 
 A "step" is one SGD step (forward, backward, batch-summed tendencies, update) over one
-minibatch of B=1000 rows drawn at a random contiguous start from the resident 50000-row
-dataset.  K steps run as ONE nf_train_steps call (the fused persistent kernel
-for this config).  Timing: CUDA events on the launching stream around exactly K steps,
-barrier + synchronize on both sides, repeated R times (>= 1 s in total so nvidia-smi can
-sample clocks during the timed region); the median rep is reported, max over ranks.
-The dataset (157 MB) is larger than L2 (126 MB); L2 is not flushed between reps.
+minibatch of B rows drawn at a random contiguous start from the resident dataset.
+K steps run as ONE nf_train_steps call.  Timing: CUDA events on the launching stream around
+exactly K steps, barrier + synchronize on both sides, repeated R times (>= 1 s in total so
+nvidia-smi can sample clocks during the timed region); every rep draws FRESH batch starts
+from one long seeded schedule (no rep replays another's rows), over a dataset larger than
+the 126 MB L2; the median rep is reported, max over ranks.  That is the paper's protocol of
+timing the training portion only, repeated runs reported as a statistic (P:830-837,
+P:886-887).
+
+N > 1 (one process per GPU): launched by torchrun, or bench.py --gpus N spawns torchrun
+itself when WORLD_SIZE is unset.  The headline c2 runs as replicas (its 95 KB co_sum per
+step would cost more than the 11 us step); configs 3-5 run data-parallel
+(per-rank batch B of a global batch N*B, NCCL all-reduce of the tendencies per layer,
+overlapped with the backward; weak scaling).
 
 Prints ONE JSON line (rank 0).  --impl reference times the CPU oracle (oracle/, fp32
 build = the paper's real32) on the same config instead.
@@ -103,16 +112,39 @@ class ClockSampler:
                 "reasons": reasons, "samples": len(self.rows)}
 
 
-def dist_setup(n_gpus):
+def dist_setup():
     import torch
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
     local = int(os.environ.get("LOCAL_RANK", "0"))
     if world > 1:
         import torch.distributed as dist
+        os.environ.setdefault("NCCL_DEBUG", "INFO")     # rank count / transport visible in stderr
         torch.cuda.set_device(local)
         dist.init_process_group("nccl")
     return world, rank, local
+
+
+def ensure_group(world):
+    """A process group for the data-parallel path; at N = 1 a one-rank NCCL group, so the same
+    all-reduce runs."""
+    import torch.distributed as dist
+    if not dist.is_initialized():
+        os.environ.setdefault("MASTER_ADDR", "127.0.0.1")
+        os.environ.setdefault("MASTER_PORT", str(29533 + int(os.environ.get("LOCAL_RANK", "0"))))
+        dist.init_process_group("nccl", rank=0, world_size=1)
+
+
+def spawn_ranks(n):
+    """bench.py --gpus N without torchrun: re-launch this script under torch.distributed.run
+    with N processes on this node (127.0.0.1 rendezvous); returns its exit code."""
+    import socket
+    with socket.socket() as s:
+        s.bind(("127.0.0.1", 0))
+        port = s.getsockname()[1]
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={n}",
+           "--master-addr", "127.0.0.1", "--master-port", str(port), os.path.abspath(__file__), *sys.argv[1:]]
+    return subprocess.call(cmd)
 
 
 def barrier(world):
@@ -187,6 +219,14 @@ def host_cpu():
     return {"model": model, "logical_cores": os.cpu_count()}
 
 
+def workload_config(cid, math, N=None):
+    """The `config` object of the JSON line: names the workload only (identical in both arms)."""
+    cfg = synth.CONFIGS[cid]
+    return {"workload": cfg["name"], "dims": cfg["dims"], "batch": cfg["batch"],
+            "dataset_rows": N or cfg["N"], "math": math, "eta": cfg["eta"],
+            "activation": cfg["act"], "batch_starts": "synth.batch_starts (seeded, uniform in [0, N-B])"}
+
+
 def reference_arm(args):
     """--impl reference: the CPU oracle on this config (rank 0 only)."""
     world = int(os.environ.get("WORLD_SIZE", "1"))
@@ -215,13 +255,107 @@ def reference_arm(args):
         "unit": "samples/s", "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
         "ms_per_step": dt * 1e3 / args.steps, "higher_is_better": True, "scaling": "weak",
         "vs_baseline": None, "dtype": "f32", "data": "synthetic",
-        "config": {"workload": cfg["name"], "dims": cfg["dims"], "batch": cfg["batch"]},
+        "config": workload_config(cid, args.math),
+        "parallelism": "1 host core",
         "cpu_baseline": {"value": v, "unit": "samples/s", "cores": 1, "kind": "oracle", "host": host_cpu(),
                          "sample": f"{args.steps} SGD steps of {rows} rows (config batch {cfg['batch']}) of "
                                    f"{cfg['name']}, fp32 build of oracle/nf_oracle.c, single thread"},
         "e2e": {"value": v, "unit": "samples/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
     }
     print(json.dumps(line), flush=True)
+
+
+def tf32_peaks(peaks):
+    """TF32 dense peaks = measured bf16 x (1.1 / 2.25), the guide's nominal ratio: the burst
+    figure (a kernel / short step timed alone: the primary denominator) and the sustained one."""
+    return peaks["bf16_tflops"] * 1.1 / 2.25, peaks.get("bf16_tflops_sustained", peaks["bf16_tflops"]) * 1.1 / 2.25
+
+
+class Timer:
+    """Fresh-start reps of K steps each: CUDA events on `stream`, barrier + sync around each."""
+
+    def __init__(self, world, stream):
+        self.world, self.stream = world, stream
+
+    def rep(self, fn):
+        import torch
+        barrier(self.world)
+        torch.cuda.synchronize()
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record(self.stream)
+        fn()
+        e1.record(self.stream)
+        torch.cuda.synchronize()
+        barrier(self.world)
+        return e0.elapsed_time(e1) / 1e3
+
+
+def run_wide(nf, cid, math, world, rank, local, K, W, reps, dp, peaks, peak_src):
+    """One wide configuration (3-5) in one numerics mode: W warm-up steps, then `reps` timed
+    reps of K steps with fresh starts each; single GPU: nf_train_steps; N > 1 or dp:
+    DataParallel (per-rank B rows of an N*B global batch, per-layer all-reduce overlapped with
+    the backward).  Returns the sub-line dict."""
+    import torch
+    cfg = synth.CONFIGS[cid]
+    B = cfg["batch"]
+    gb = world * B if dp else B
+    N = max(cfg["N"], 2 * gb)
+    X, Y = synth.dataset(cid, N=N)
+    starts = synth.batch_starts(cid, steps=W + reps * K, N=N, batch=gb)
+    Xd, Yd = torch.from_numpy(X).cuda(), torch.from_numpy(Y).cuda()
+    del X, Y
+    stream = torch.cuda.current_stream()
+    net = nf.Net(cfg["dims"], cfg["act"], stream=stream)
+    net.set_params(torch.from_numpy(synth.init_params(cid)).cuda())
+    net.set_math({"fp32": nf.NF_MATH_FP32, "tf32": nf.NF_MATH_TF32}[math])
+    loss = torch.zeros(K, device="cuda")
+    if dp:
+        from paper_1902_06714_b200.dp import DataParallel
+        ensure_group(world)
+        dpar = DataParallel(net)
+
+        def steps(st):
+            dpar.train_steps(Xd, Yd, gb, st, cfg["eta"])
+    else:
+        def steps(st):
+            net.train_steps(Xd, Yd, B, st, cfg["eta"], step_loss=loss)
+    steps(starts[:W])
+    torch.cuda.synchronize()
+    tm = Timer(world, stream)
+    l0 = nf.nf_launch_count()
+    times = []
+    with ClockSampler(local) as clk:
+        for r in range(reps):
+            times.append(tm.rep(lambda: steps(starts[W + r * K:W + (r + 1) * K])))
+    launches = (nf.nf_launch_count() - l0) // reps
+    t = max_over_ranks(statistics.median(times), world)
+    fl = flops_per_sample(cfg["dims"]) * gb
+    burst, sust = tf32_peaks(peaks)
+    ach = fl * K / t / 1e12
+    traffic = None
+    prof = os.path.join(ROOT, "profiles", f"traffic_c{cid}.json")
+    if os.path.exists(prof):
+        tj = json.load(open(prof))
+        if tj.get("math") == math:
+            traffic = tj["bytes_per_step"] * K
+    del Xd, Yd, net
+    torch.cuda.empty_cache()
+    return {
+        "workload": cfg["name"], "math": math, "dims": cfg["dims"], "batch": B, "global_batch": gb,
+        "dataset_rows": N, "steps": K, "warmup": W, "reps": reps, "stat": "median rep, fresh starts per rep",
+        "ms_per_step": t * 1e3 / K, "value": gb * K / t, "unit": "samples/s",
+        "parallelism": (f"dp{world}: nf_grad_layers on {B} rows per rank, NCCL all-reduce per layer block "
+                        f"overlapped with the backward, nf_update" if dp else "1 GPU"),
+        "roofline": {"bound": "tensor", "achieved": ach, "peak": burst, "unit": "TFLOP/s", "frac": ach / burst,
+                     "frac_sustained": ach / sust, "traffic": traffic,
+                     "peak_source": f"MEASURED_PEAKS.json bf16_tflops x 1.1/2.25 = TF32 dense burst ({peak_src}); "
+                                    f"frac_sustained vs bf16_tflops_sustained x 1.1/2.25",
+                     "kernel": "whole step (every kernel of nf_train_steps)",
+                     "algorithmic_flops_per_step": fl,
+                     **({"mma_pipe_frac": 3 * ach / burst, "note": "3xTF32: 3 MMAs per useful product"}
+                        if math == "fp32" else {})},
+        "gpu_launches_per_rep": launches, "clocks": clk.summary(),
+    }
 
 
 def main():
@@ -234,96 +368,90 @@ def main():
     ap.add_argument("--min-seconds", type=float, default=1.0)
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--configs", default=None,
+                    help="wide configurations measured in the same run under 'configs', e.g. '5:tf32,5:fp32'; "
+                         "default with the c2 headline: c5, c3, c4 in tf32 and fp32 (+ c5 tf32 data-parallel at N=1); "
+                         "'none' to skip")
+    ap.add_argument("--sub-steps", type=int, default=0, help="steps per timed rep of each wide config (0: auto)")
     ap.add_argument("--dp", action="store_true",
-                    help="true data parallelism (P:505-556): every step, each rank's tendencies over its "
-                         "B rows of a world*B global batch, NCCL all-reduce (co_sum), nf_update; default: "
-                         "independent replicas (no collective)")
+                    help="the headline config data-parallel (P:505-556) instead of replicas")
     ap.add_argument("--math", default="fp32", choices=["fp32", "tf32", "fp64"],
-                    help="fp32: fp32 SIMT / 3xTF32 tensor cores (1e-4 parity); tf32: 1xTF32 tiles; "
-                         "fp64: the paper's real64 build on the FP64 units")
+                    help="fp32: fp32 SIMT / 3xTF32 tensor cores (1e-4 parity); tf32: 1xTF32 tiles on RN-rounded "
+                         "operands; fp64: the paper's real64 build on the FP64 units")
     args = ap.parse_args()
     if args.warmup < 3:
         ap.error("--warmup must be >= 3")
     if args.impl == "reference":
         return reference_arm(args)
+    if args.gpus > 1 and "WORLD_SIZE" not in os.environ:
+        sys.exit(spawn_ranks(args.gpus))
 
     import torch
     from paper_1902_06714_b200 import build as nfbuild
-    nfbuild.build()
+    if int(os.environ.get("LOCAL_RANK", "0")) == 0:
+        nfbuild.build()
     import paper_1902_06714_b200 as nf
 
-    world, rank, local = dist_setup(args.gpus)
+    world, rank, local = dist_setup()
+    barrier(world)
     cid = args.config
     cfg = synth.CONFIGS[cid]
     B, K, W = cfg["batch"], args.steps, args.warmup
-    X, Y = synth.dataset(cid)
+    dp = args.dp or (world > 1 and cid >= 3)
+    gb = world * B if dp else B
+    X, Y = synth.dataset(cid, N=max(cfg["N"], 2 * gb))
     N = len(X)
-    # --dp: the global batch of a step is world * B rows, rank r owns the r-th block of B
-    starts = synth.batch_starts(cid, steps=W + K, N=N - ((world - 1) * B if args.dp else 0))
+    # one long seeded schedule of starts; every rep takes the next K (replica r: its own stream)
+    max_reps = 2000
+    starts_all = synth.batch_starts(cid, steps=W + (max_reps + 1) * K, N=N, batch=gb)
+    if not dp and world > 1:
+        starts_all = np.roll(starts_all, -rank * 7919)
     Xd, Yd = torch.from_numpy(X).cuda(), torch.from_numpy(Y).cuda()
     stream = torch.cuda.current_stream()
     net = nf.Net(cfg["dims"], cfg["act"], stream=stream)
     net.set_params(torch.from_numpy(synth.init_params(cid)).cuda())
     net.set_math({"fp32": nf.NF_MATH_FP32, "tf32": nf.NF_MATH_TF32, "fp64": nf.NF_MATH_FP64}[args.math])
     loss = torch.zeros(K, device="cuda")
-    if args.dp:
+    if dp:
         from paper_1902_06714_b200.dp import DataParallel
-        if world == 1:   # a one-rank NCCL group, so the all-reduce runs at N = 1 too
-            import torch.distributed as dist
-            os.environ.setdefault("MASTER_ADDR", "127.0.0.1")
-            os.environ.setdefault("MASTER_PORT", "29533")
-            dist.init_process_group("nccl", rank=0, world_size=1)
-        dp = DataParallel(net)
+        ensure_group(world)
+        dpar = DataParallel(net)
 
         def run_steps(st, step_loss=None, Xs=Xd, Ys=Yd):
-            dp.train_steps(Xs, Ys, world * B, st, cfg["eta"])
+            dpar.train_steps(Xs, Ys, gb, st, cfg["eta"])
     else:
         def run_steps(st, step_loss=None, Xs=Xd, Ys=Yd):
             net.train_steps(Xs, Ys, B, st, cfg["eta"], step_loss=step_loss)
 
-    # warm-up (W untimed steps)
-    run_steps(starts[:W])
+    run_steps(starts_all[:W])
     torch.cuda.synchronize()
+    tm = Timer(world, stream)
+    rep_i = [0]
 
-    def timed_rep():
-        barrier(world)
-        torch.cuda.synchronize()
-        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-        e0.record(stream)
-        run_steps(starts[W:], step_loss=loss)
-        e1.record(stream)
-        torch.cuda.synchronize()
-        barrier(world)
-        return e0.elapsed_time(e1) / 1e3
+    def next_starts():
+        r = rep_i[0] % (max_reps + 1)
+        rep_i[0] += 1
+        return starts_all[W + r * K:W + (r + 1) * K]
 
     l0 = nf.nf_launch_count()
-    t_first = timed_rep()
+    t_first = tm.rep(lambda: run_steps(next_starts(), step_loss=loss))
     launches = nf.nf_launch_count() - l0
-    reps = max(5, min(2000, int(args.min_seconds / max(t_first, 1e-6)) + 1))
+    reps = max(5, min(max_reps, int(args.min_seconds / max(t_first, 1e-6)) + 1))
+    reps = int(max_over_ranks(reps, world))
     times = []
     with ClockSampler(local) as clk:
         for _ in range(reps):
-            times.append(timed_rep())
+            times.append(tm.rep(lambda: run_steps(next_starts(), step_loss=loss)))
     t_med = statistics.median(times)
     t_max = max_over_ranks(t_med, world)
-    value = job_throughput(world, K, B, t_max)
+    value = world * K * B / t_max
 
     peaks, peak_src = measured_peaks()
     alg_bytes = K * B * BYTES_PER_SAMPLE[cid]
     achieved = alg_bytes / t_med / 1e9
     tensor_bound = len(cfg["dims"]) > 3
     if tensor_bound:
-        # TF32 dense peak = measured bf16 x (1.1 / 2.25), the guide's nominal ratio.  The
-        # profiling recipe: the burst figure for a kernel timed alone, the sustained one for
-        # kernels under sustained load.  Which one applies is read off this run's clocks: the
-        # sustained figure when the SM clock under load sat below max (power cap: c5 runs at
-        # ~1.55 GHz), the burst one when it held the maximum clock (c3, c4).
-        ck = clk.summary()
-        sustained = ("bf16_tflops_sustained" in peaks and ck.get("sm_mhz") and ck.get("sm_max_mhz")
-                     and ck["sm_mhz"] < 0.95 * ck["sm_max_mhz"])
-        bf16 = peaks["bf16_tflops_sustained"] if sustained else peaks["bf16_tflops"]
-        tf32_peak = bf16 * 1.1 / 2.25
-        tf32_burst = peaks["bf16_tflops"] * 1.1 / 2.25
+        tf32_peak, tf32_sust = tf32_peaks(peaks)
         ach_tf = flops_per_sample(cfg["dims"]) * K * B / t_med / 1e12
     ach_f64 = flops_per_sample(cfg["dims"]) * K * B / t_med / 1e12
     # DRAM traffic of the roofline's kernel (c2: the fused kernel, `ncu --set full`; c3-c5: all
@@ -342,14 +470,7 @@ def main():
     out = torch.empty((N, cfg["dims"][-1]), device="cuda")
     net.output(Xd, out)
     torch.cuda.synchronize()
-    ti = []
-    for _ in range(5):
-        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-        e0.record(stream)
-        net.output(Xd, out)
-        e1.record(stream)
-        torch.cuda.synchronize()
-        ti.append(e0.elapsed_time(e1) / 1e3)
+    ti = [tm.rep(lambda: net.output(Xd, out)) for _ in range(5)]
     t_inf = statistics.median(ti)
     inf_bytes = N * 4 * (cfg["dims"][0] + cfg["dims"][-1])
     inference = {"value": world * N / max_over_ranks(t_inf, world), "unit": "samples/s", "rows": N,
@@ -360,28 +481,38 @@ def main():
     # ---- e2e: same metric through the C-ABI with pinned HOST buffers; each step's batch
     # is copied host->device inside the call, the step losses are read back to the host.
     e2e = None
-    if not args.no_e2e and not args.dp:
+    if not args.no_e2e and not dp:
         Xh = torch.from_numpy(X).pin_memory()
         Yh = torch.from_numpy(Y).pin_memory()
         lh = torch.empty(K, dtype=torch.float32).pin_memory()
 
-        def e2e_rep():
-            barrier(world)
-            torch.cuda.synchronize()
-            e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-            e0.record(stream)
-            net.train_steps(Xh, Yh, B, starts[W:], cfg["eta"], step_loss=loss)
+        def e2e_call():
+            net.train_steps(Xh, Yh, B, next_starts(), cfg["eta"], step_loss=loss)
             lh.copy_(loss, non_blocking=True)
-            e1.record(stream)
-            torch.cuda.synchronize()
-            barrier(world)
-            return e0.elapsed_time(e1) / 1e3
 
-        e2e_rep()
-        te = statistics.median([e2e_rep() for _ in range(3)])
+        tm.rep(e2e_call)
+        te = statistics.median([tm.rep(e2e_call) for _ in range(3)])
         te = max_over_ranks(te, world)
         e2e = {"value": world * K * B / te, "unit": "samples/s",
                "h2d_bytes_per_step": B * BYTES_PER_SAMPLE[cid], "d2h_bytes_per_step": 4}
+    del Xd, Yd
+    torch.cuda.empty_cache()
+
+    # ---- the wide configurations in the same run (configs 3-5, both numerics modes)
+    subs = {}
+    spec = args.configs
+    if spec is None:
+        spec = "none" if cid != 2 else "5:tf32,5:fp32,3:tf32,3:fp32,4:tf32,4:fp32"
+        if cid == 2 and world == 1:
+            spec += ",5:tf32:dp"
+    if spec != "none":
+        for item in spec.split(","):
+            parts = item.split(":")
+            c, m = int(parts[0]), parts[1]
+            sub_dp = world > 1 or (len(parts) > 2 and parts[2] == "dp")
+            Ks = args.sub_steps or {3: 20, 4: 20, 5: 5}[c]
+            subs[f"c{c}-{m}" + ("-dp" if sub_dp and world == 1 else "")] = run_wide(
+                nf, c, m, world, rank, local, Ks, 3, 3, sub_dp, peaks, peak_src)
 
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
@@ -398,13 +529,15 @@ def main():
             "value": value, "unit": "samples/s", "n_gpus": world, "steps": K, "warmup": W,
             "ms_per_step": t_max * 1e3 / K, "higher_is_better": True, "scaling": "weak",
             "vs_baseline": None, "dtype": {"fp32": "f32", "tf32": "tf32", "fp64": "f64"}[args.math], "data": "synthetic",
-            "config": {"workload": cfg["name"], "dims": cfg["dims"], "batch": B, "dataset_rows": N,
-                       "math": args.math,
-                       "eta": cfg["eta"], "steps_per_timed_call": K, "reps": reps, "stat": "median rep",
-                       "l2": f"dataset {X.nbytes / 1e6:.0f} MB > 126 MB L2, not flushed",
-                       "parallelism": (f"dp{world}: per step nf_grad on {B} rows per rank, NCCL all-reduce "
-                                       f"of the tendencies (co_sum), nf_update; global batch {world * B}"
-                                       if args.dp else f"replicas x{world}" if world > 1 else "1 GPU")},
+            "config": workload_config(cid, args.math, N),
+            "timing": {"steps_per_timed_call": K, "reps": reps,
+                       "stat": "median rep; every rep draws fresh batch starts from one seeded schedule",
+                       "l2": f"inputs larger than L2: dataset {X.nbytes / 1e6:.0f} MB > 126 MB L2, fresh random "
+                             f"batch starts every rep (not flushed)"},
+            "parallelism": (f"dp{world}: per step nf_grad_layers on {B} rows per rank, NCCL all-reduce "
+                            f"per layer block overlapped with the backward (co_sum), nf_update; "
+                            f"global batch {gb}"
+                            if dp else f"replicas x{world}" if world > 1 else "1 GPU"),
             "roofline": ({"bound": "latency", "achieved": t_max * 1e6 / K, "peak": None, "unit": "us/step",
                           "frac": None, "traffic": None, "kernel": "single_cta_kernel",
                           "note": "config 1 (120 flop per sample): one CTA, a chain of CTA barriers per step "
@@ -416,11 +549,8 @@ def main():
                           "algorithmic_flops_per_step": flops_per_sample(cfg["dims"]) * B}
                          if args.math == "fp64" else
                          {"bound": "tensor", "achieved": ach_tf, "peak": tf32_peak, "unit": "TFLOP/s",
-                          "frac": ach_tf / tf32_peak, "traffic": traffic,
-                          "peak_source": (f"MEASURED_PEAKS.json bf16_tflops{'_sustained' if sustained else ''}"
-                                          f" x 1.1/2.25 = TF32 dense, {'sustained: SM clock under load below max (power cap)' if sustained else 'burst: SM clock at max'}"
-                                          f" ({peak_src})"),
-                          "frac_vs_burst_peak": ach_tf / tf32_burst,
+                          "frac": ach_tf / tf32_peak, "frac_sustained": ach_tf / tf32_sust, "traffic": traffic,
+                          "peak_source": f"MEASURED_PEAKS.json bf16_tflops x 1.1/2.25 = TF32 dense burst ({peak_src})",
                           "kernel": "whole step (gemm_tc_kernel + epilogue kernels)",
                           "algorithmic_flops_per_step": flops_per_sample(cfg["dims"]) * B}
                          if tensor_bound else
@@ -431,14 +561,15 @@ def main():
                           "algorithmic_bytes_per_launch": alg_bytes}),
             "flops": {"per_sample": fl, "achieved_tflops": fl * K * B / t_med / 1e12},
             "inference": inference,
+            "configs": subs or None,
             "cpu_baseline": cpu,
             "e2e": e2e,
             "gpu_launches": launches,
             "clocks": clk.summary(),
         }
         print(json.dumps(line), flush=True)
-    if world > 1 or args.dp:
-        import torch.distributed as dist
+    import torch.distributed as dist
+    if dist.is_initialized():
         dist.destroy_process_group()
 
 

@@ -144,6 +144,19 @@ int nf_train_steps(nf_net *net, const float *X, const float *Y, int64_t N, int64
  * Parameters are unchanged.  (Extension, for gradient parity.)             */
 int nf_grad(nf_net *net, const float *x, const float *y, int64_t n, float *grad);
 
+/* nf_grad that announces each layer's tendencies as soon as they are final, so that the
+ * data-parallel co_sum of layer l can run while the backward pass still works on
+ * layers l-1..1 (bucketed all-reduce overlapped with the backward).
+ *   events   : n_events == L cudaEvent_t handles created by the caller (any flags);
+ *              events[l-1] is recorded on a stream of the library once the W_l and b_l blocks
+ *              of grad are written (layer L first, layer 1 last).  A NULL entry is skipped;
+ *              events == NULL is nf_grad.  Another count -> NF_EINVAL.
+ * With a HOST grad or in NF_MATH_FP64 every event is recorded at the end (no overlap).
+ * The caller makes its communication stream wait on events[l-1] before reading layer l's
+ * block and orders nf_update after its collectives (e.g. cudaStreamWaitEvent).           */
+int nf_grad_layers(nf_net *net, const float *x, const float *y, int64_t n, float *grad,
+                   void *const *events, int32_t n_events);
+
 /* The paper's `update`, applied to externally summed tendencies:
  *   params -= (eta / n) * grad
  * grad: count = nf_param_count floats in the flat parameter layout (host or device), e.g. the

@@ -54,6 +54,7 @@ def _load() -> ctypes.CDLL:
         "nf_train_batch": (ctypes.c_int, [P, P, P, I64, F]),
         "nf_train_steps": (ctypes.c_int, [P, P, P, I64, I64, P, I64, F, P]),
         "nf_grad": (ctypes.c_int, [P, P, P, I64, P]),
+        "nf_grad_layers": (ctypes.c_int, [P, P, P, I64, P, P, I32]),
         "nf_update": (ctypes.c_int, [P, P, I64, F, I64]),
         "nf_save": (ctypes.c_int, [P, ctypes.c_char_p]),
         "nf_load": (ctypes.c_int, [ctypes.c_char_p, ctypes.POINTER(P)]),
@@ -86,7 +87,7 @@ def lib() -> ctypes.CDLL:
 # Every symbol include/nf.h declares (checked by tests/test_abi.py).
 EXPORTS = ("nf_net_create", "nf_net_destroy", "nf_set_stream", "nf_set_math", "nf_param_count",
            "nf_get_params", "nf_set_params", "nf_output", "nf_train_batch", "nf_train_steps",
-           "nf_grad", "nf_update", "nf_save", "nf_load", "nf_load_as", "nf_loss", "nf_accuracy", "nf_last_error",
+           "nf_grad", "nf_grad_layers", "nf_update", "nf_save", "nf_load", "nf_load_as", "nf_loss", "nf_accuracy", "nf_last_error",
            "nf_launch_count", "nf_debug_log_enable", "nf_debug_log_read")
 
 
@@ -160,6 +161,14 @@ def nf_train_steps(net, X, Y, N: int, batch: int, starts, n_steps: int, eta: flo
 
 def nf_grad(net, x, y, n: int, grad):
     _check(lib().nf_grad(net, _ptr(x), _ptr(y), n, _ptr(grad)))
+
+
+def nf_grad_layers(net, x, y, n: int, grad, events):
+    """events: one torch.cuda.Event (or raw cudaEvent_t int) per layer; events[l-1] is recorded
+    when layer l's tendency block of grad is final (include/nf.h)."""
+    handles = [int(getattr(e, "cuda_event", e) or 0) for e in events]
+    arr = (ctypes.c_void_p * len(handles))(*handles)
+    _check(lib().nf_grad_layers(net, _ptr(x), _ptr(y), n, _ptr(grad), ctypes.cast(arr, ctypes.c_void_p), len(handles)))
 
 
 def nf_update(net, grad, count: int, eta: float, n: int):
@@ -277,6 +286,20 @@ class Net:
         if out is None:
             out = _empty_like_rows(x, self.n_params, None)
         nf_grad(self.h, x, y, x.shape[0], out)
+        return out
+
+    def grad_layers(self, x, y, out, events):
+        """nf_grad into `out`, recording events[l-1] when layer l's block is final."""
+        nf_grad_layers(self.h, x, y, x.shape[0], out, events)
+        return out
+
+    def layer_slices(self):
+        """(offset, count) of each layer's W_l, b_l block in the flat layout, l = 1..L."""
+        out, o = [], 0
+        for l in range(1, len(self.dims)):
+            c = self.dims[l] * self.dims[l - 1] + self.dims[l]
+            out.append((o, c))
+            o += c
         return out
 
     def update(self, grad, eta: float, n: int):

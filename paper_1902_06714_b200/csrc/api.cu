@@ -240,7 +240,8 @@ int ensure_side(nf_net *net) {
 // summed tendencies are stored there instead (nf_grad).  Per layer l (L..1): K3(l) computes
 // delta_{l-1} from delta_l and W_l on the main stream; K4(l) (tendencies of W_l, b_l and the
 // update) runs on the side stream once K3(l) has read W_l, overlapping K3(l-1).
-int backward(nf_net *net, const float *x, int64_t n, float eta, float *grad, float *step_loss = nullptr) {
+int backward(nf_net *net, const float *x, int64_t n, float eta, float *grad, float *step_loss = nullptr,
+             cudaEvent_t const *layer_done = nullptr) {
   if (int rc = ensure_side(net)) return rc;
   net->ws2.math = net->ws.math;
   // The overlap only pays while the GEMMs are under one wave of 128x256 tiles (c3, c4): a
@@ -278,12 +279,15 @@ int backward(nf_net *net, const float *x, int64_t n, float eta, float *grad, flo
     EpiGrad eg = grad ? EpiGrad{grad + net->offW[l], grad + net->offB[l], nk, nk, 0.0f, 1}
                       : EpiGrad{net->W(l), net->b(l), nk, nk, scale, 0};
     if (!grad && t) eg.Wt = net->Wt(l);  // the update also refreshes the TF32 shadow of W_l
+    cudaStream_t kst = side;  // the stream layer l's tendencies are produced on
     if (fused) NF_CUDA(out_layer_grad_final(side, (int)n, nk, nl, net->part_out.as<float>(), eg, step_loss));
-    else if (l == 1 && net->L > 1 && side != main_st && (net->math != NF_MATH_TF32 || n <= 2048))
+    else if (l == 1 && net->L > 1 && side != main_st && (net->math != NF_MATH_TF32 || n <= 2048)) {
       // the main stream is idle after the last K3: K4(1) there, concurrent with K4(2) on the side
       // stream (c4 134 -> 130 us, 3xTF32 c3 462 -> 445 us; c3's 1xTF32 pair contends: 154 -> 157)
       NF_CUDA(gemm_grad(main_st, nl, nk, (int)n, net->S[l], aprev, eg, net->ws, bias_done[l] != 0));
-    else NF_CUDA(gemm_grad(side, nl, nk, (int)n, net->S[l], aprev, eg, net->ws2, bias_done[l] != 0));
+      kst = main_st;
+    } else NF_CUDA(gemm_grad(side, nl, nk, (int)n, net->S[l], aprev, eg, net->ws2, bias_done[l] != 0));
+    if (layer_done && layer_done[l - 1]) NF_CUDA(cudaEventRecord(layer_done[l - 1], kst));  // nf_grad_layers
   }
   NF_CUDA(cudaEventRecord(net->ev[net->L + 1], side));  // join
   NF_CUDA(cudaStreamWaitEvent(main_st, net->ev[net->L + 1], 0));
@@ -916,8 +920,10 @@ int nf_train_steps(nf_net *net, const float *X, const float *Y, int64_t N, int64
   return NF_OK;
 }
 
-int nf_grad(nf_net *net, const float *x, const float *y, int64_t n, float *grad) {
+int nf_grad_layers(nf_net *net, const float *x, const float *y, int64_t n, float *grad, void *const *events,
+                   int32_t n_events) {
   if (int rc = check_net(net)) return rc;
+  if (events && n_events != net->L) return fail(NF_EINVAL, "n_events %d != the %d layers", n_events, net->L);
   if (n <= 0) return fail(NF_EINVAL, "n must be >= 1");
   if (int rc = check_ptr(x, "x")) return rc;
   if (int rc = check_ptr(y, "y")) return rc;
@@ -942,13 +948,22 @@ int nf_grad(nf_net *net, const float *x, const float *y, int64_t n, float *grad)
   } else {
     if ((rc = ensure_ws(net, n))) return rc;
     if ((rc = forward(net, dx, dy, n, 0))) return rc;
-    if ((rc = backward(net, dx, n, 0.0f, dg))) return rc;
+    if ((rc = backward(net, dx, n, 0.0f, dg, nullptr, events && !host_out ? reinterpret_cast<cudaEvent_t const *>(events)
+                                                                            : nullptr)))
+      return rc;
   }
+  if (events && (host_out || net->math == NF_MATH_FP64))  // no per-layer overlap there: all at the end
+    for (int l = 0; l < net->L; ++l)
+      if (events[l]) NF_CUDA(cudaEventRecord(static_cast<cudaEvent_t>(events[l]), net->stream));
   if (host_out) {
     NF_CUDA(cudaMemcpyAsync(grad, dg, (size_t)net->nparams * sizeof(float), cudaMemcpyDeviceToHost, net->stream));
     NF_CUDA(cudaStreamSynchronize(net->stream));
   }
   return NF_OK;
+}
+
+int nf_grad(nf_net *net, const float *x, const float *y, int64_t n, float *grad) {
+  return nf_grad_layers(net, x, y, n, grad, nullptr, 0);
 }
 
 int nf_update(nf_net *net, const float *grad, int64_t count, float eta, int64_t n) {

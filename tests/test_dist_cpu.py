@@ -78,6 +78,18 @@ class OracleNet:
         import torch
         out.copy_(torch.from_numpy(self.o.grad(self.p, x.numpy(), y.numpy()).astype("float32")))
 
+    def grad_layers(self, x, y, out, events):
+        assert len(events) == len(self.o.dims) - 1
+        self.grad(x, y, out)
+
+    def layer_slices(self):
+        out, o = [], 0
+        for l in range(1, len(self.o.dims)):
+            c = self.o.dims[l] * self.o.dims[l - 1] + self.o.dims[l]
+            out.append((o, c))
+            o += c
+        return out
+
     def update(self, g, eta, n):
         import numpy as np
         self.p = self.p - (float(np.float32(eta)) / n) * g.numpy().astype(np.float64)
@@ -93,7 +105,7 @@ def _dp_worker(rank, world, port, q):
     from paper_1902_06714_b200.dp import DataParallel
     os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
     dist.init_process_group("gloo", rank=rank, world_size=world)
-    dims, act = [13, 9, 4], "tanh,sigmoid"
+    dims, act = [13, 9, 7, 4], "tanh,sigmoid"
     p0 = synth.random_params(7, dims, 0.5).astype(np.float32).astype(np.float64)
     # only rank 0's initial parameters count: the co_broadcast must overwrite the others
     net = OracleNet(dims, act, p0 if rank == 0 else p0 + 1.0)
@@ -106,8 +118,10 @@ def _dp_worker(rank, world, port, q):
 
 
 def test_data_parallel_co_sum_equals_serial_gloo():
-    """World size 2 (gloo): co_broadcast, per-rank tendencies of each rank's rows, co_sum,
-    identical update on every rank == the serial oracle on the whole batch."""
+    """World size 2 (gloo): co_broadcast, per-rank tendencies of each rank's rows, co_sum as one
+    all-reduce per layer block (layer L first: the bucketing the GPU path overlaps with the
+    backward), identical update on every rank == the serial oracle on the whole batch
+    (P:536-556)."""
     import sys
     sys.path.insert(0, ROOT)
     import numpy as np
@@ -123,7 +137,7 @@ def test_data_parallel_co_sum_equals_serial_gloo():
     for p in procs:
         p.join(timeout=60)
         assert p.exitcode == 0
-    dims, act = [13, 9, 4], "tanh,sigmoid"
+    dims, act = [13, 9, 7, 4], "tanh,sigmoid"
     p0 = synth.random_params(7, dims, 0.5).astype(np.float32).astype(np.float64)
     X, Y = synth.random_batch(8, 40, dims[0], dims[-1], "uniform")
     o = oracle.Oracle(dims, act)

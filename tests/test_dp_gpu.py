@@ -66,6 +66,33 @@ def _free_port():
         return s.getsockname()[1]
 
 
+def test_grad_layers_events_and_blocks():
+    """nf_grad_layers writes the same tendencies as nf_grad and records one event per layer;
+    a comm stream that waits on event l sees layer l's final block (the overlap contract)."""
+    dims, act = [784, 1024, 1024, 10], "tanh"
+    p = synth.init_params(3)
+    X, Y = synth.dataset(3, N=4096)
+    net = nf.Net(dims, act, stream=torch.cuda.current_stream())
+    net.set_params(dev(p))
+    ref = net.grad(dev(X), dev(Y)).clone()
+    evs = [torch.cuda.Event() for _ in range(3)]
+    for e in evs:
+        e.record()
+    g = torch.full_like(ref, float("nan"))
+    comm = torch.cuda.Stream()
+    copies = torch.empty_like(ref)
+    net.grad_layers(dev(X), dev(Y), g, evs)
+    with torch.cuda.stream(comm):
+        for (off, cnt), e in zip(reversed(net.layer_slices()), reversed(evs)):
+            comm.wait_event(e)
+            copies[off:off + cnt].copy_(g[off:off + cnt])
+    torch.cuda.synchronize()
+    assert torch.isfinite(copies).all()
+    assert rel_err(copies.cpu().numpy(), ref.cpu().numpy()) <= FP32_BAR
+    with pytest.raises(nf.NFError):
+        nf.nf_grad_layers(net.h, dev(X), dev(Y), 4096, g, evs[:2])
+
+
 def test_data_parallel_one_rank_nccl():
     import torch.distributed as dist
     from paper_1902_06714_b200.dp import DataParallel
@@ -82,5 +109,9 @@ def test_data_parallel_one_rank_nccl():
         dp.train_steps(dev(X), dev(Y), 128, starts, 0.5)
         ref, _ = oracle.Oracle(dims, act).train_steps(p, X, Y, 128, starts, 0.5)
         assert rel_err(params_of(net), ref) <= FP32_BAR
+        net2 = nf.Net(dims, act)          # the same steps with the collectives not overlapped
+        net2.set_params(dev(p))
+        DataParallel(net2, overlap=False).train_steps(dev(X), dev(Y), 128, starts, 0.5)
+        assert rel_err(params_of(net2), params_of(net)) <= 1e-6
     finally:
         dist.destroy_process_group()
