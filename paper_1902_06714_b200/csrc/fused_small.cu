@@ -101,7 +101,9 @@ struct FusedParams {
   float *params;         // flat [W1 b1 W2 b2]
   float *acc;            // kSlots accumulator slots (zeroed by the host)
   unsigned *bar;         // grid barrier counter (zeroed by the host)
-  float *step_loss;      // nullable, zeroed by the host
+  float *step_loss;      // nullable; step s's entry zeroed in-kernel before barrier s
+  unsigned bar_base;     // barrier counter at launch (it runs on across calls)
+  int slot0;             // ring slot of step 0 (the ring runs on across calls)
   long long *prof;       // nullable: per-CTA per-step clock64 stamps (NF_FUSED_PROF=1)
 };
 
@@ -165,6 +167,15 @@ __device__ __forceinline__ void tc_split(uint8_t *hi, uint8_t *lo, int bytes, in
     reinterpret_cast<float4 *>(hi)[i] = h;
     reinterpret_cast<float4 *>(lo)[i] = make_float4(x.x - h.x, x.y - h.y, x.z - h.z, x.w - h.w);
   }
+}
+
+// wait until the monotonically running counter reaches `target` (wrap-safe: the counter runs
+// on across calls, bar_base + steps * CTAs may wrap around 2^32)
+__device__ __forceinline__ void grid_wait_from(unsigned *ctr, unsigned target) {
+  unsigned v;
+  do {
+    asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(ctr) : "memory");
+  } while ((int)(v - target) < 0);
 }
 
 // AH / AO: compile-time hidden / output activations (-1 = read p.act_h / p.act_o at run time).
@@ -339,7 +350,7 @@ fused_small_kernel(const FusedParams p, const __grid_constant__ CUtensorMap tmX,
     const uint32_t par = (uint32_t)(s & 1);
     const float *xs = xs0 + buf * xstride;
     const float *ys = ys0 + buf * p.nOwnMax * 32;
-    float *accS = p.acc + (s % kSlots) * p.slot;
+    float *accS = p.acc + ((p.slot0 + s) % kSlots) * p.slot;
     PROF(0);
     if (tid == 0) {  // arm this step's receive barriers
       ptx::mbar_arrive_expect_tx(bar_P, bytesP);
@@ -663,13 +674,14 @@ fused_small_kernel(const FusedParams p, const __grid_constant__ CUtensorMap tmX,
     //      zero this CTA's share of the slot used two steps ahead (its last readers finished
     //      before the previous barrier; its next writers start after the next one).
     __syncthreads();
-    if (tid == 0) ptx::grid_arrive(p.bar);
-    if (warp == 1 && p.step_loss) {  // this CTA's cost partial, off the critical path (the
-      const float l = warp_sum(lane < kWarps ? lsum[lane] : 0.0f);  // barrier wait); lsum is
-      if (lane == 0) ptx::red_add_f32(p.step_loss + s, 0.5f * l * p.inv_B);  // rewritten in P3
+    if (tid == 0) {
+      // step s's cost entry is zeroed by CTA 0 before its arrival; every CTA adds its partial
+      // after the barrier, i.e. after that zero (release / acquire through the counter)
+      if (blockIdx.x == 0 && p.step_loss) p.step_loss[s] = 0.0f;
+      ptx::grid_arrive(p.bar);
     }
     {
-      float *z = p.acc + ((s + 2) % kSlots) * p.slot;
+      float *z = p.acc + ((p.slot0 + s + 2) % kSlots) * p.slot;
       for (int64_t i = (int64_t)blockIdx.x * kThreads + tid; i < p.slot; i += (int64_t)nCTA * kThreads) z[i] = 0.0f;
     }
     if (TC && s + 1 < p.n_steps) {  // next step's K-layout tile: TF32 split while the barrier fills
@@ -677,8 +689,12 @@ fused_small_kernel(const FusedParams p, const __grid_constant__ CUtensorMap tmX,
       tc_split(X, X + kTcXLoK, 4 * kTcAS, tid);
       ptx::fence_proxy_async_smem();
     }
-    if (tid == 0) ptx::grid_wait(p.bar, (unsigned)((s + 1) * nCTA));
+    if (tid == 0) grid_wait_from(p.bar, p.bar_base + (unsigned)((s + 1) * nCTA));
     __syncthreads();
+    if (warp == 1 && p.step_loss) {  // this CTA's cost partial (lsum is rewritten in P3)
+      const float l = warp_sum(lane < kWarps ? lsum[lane] : 0.0f);
+      if (lane == 0) ptx::red_add_f32(p.step_loss + s, 0.5f * l * p.inv_B);
+    }
     PROF(8);
 
     // ---- P8. read the reduced slice and the W2/b block back
@@ -777,6 +793,13 @@ int fused_small_train_steps(FusedSmall &fs, cudaStream_t st, const std::vector<i
   const int n0 = dims[0], H = dims[1], O = dims[2];
   if (H > 32 || O > 32 || batch > (int64_t)148 * kMaxRows) return FUSED_NOT_APPLICABLE;
 
+  const bool aligned_now = (n0 % 4 == 0) && ((uintptr_t)X % 16 == 0) && env_int("NF_FUSED_NOTMA", 0) == 0;
+  // ---- launch configuration: decided once per (shape, batch, dataset, switches), then cached
+  // (the occupancy query and the tensor-map encodes cost host microseconds per call)
+  const std::vector<int64_t> key = {n0, H, O, batch, (int64_t)(uintptr_t)X, N, aligned_now,
+                                    env_int("NF_FUSED_C", 0), env_int("NF_FUSED_G", 0), env_int("NF_FUSED_TC", 0)};
+  if (key != fs.cfg_key) {
+    fs.cfg_key.clear();
   // cluster size: pixel slices of >= 32 columns, at most 8 CTAs
   int C = env_int("NF_FUSED_C", 0);
   if (C <= 0) {
@@ -784,7 +807,7 @@ int fused_small_train_steps(FusedSmall &fs, cudaStream_t st, const std::vector<i
     while (C > 1 && n0 / C < 32) C /= 2;
   }
   C = std::max(1, std::min(C, kMaxC));
-  const bool aligned = (n0 % 4 == 0) && ((uintptr_t)X % 16 == 0) && env_int("NF_FUSED_NOTMA", 0) == 0;
+  const bool aligned = aligned_now;
   int ws, wpad;
   if (aligned) {
     ws = ((n0 + C - 1) / C + 3) / 4 * 4;
@@ -872,21 +895,59 @@ int fused_small_train_steps(FusedSmall &fs, cudaStream_t st, const std::vector<i
              (long long)N, ws, nSmax);
     return -1;
   }
+    fs.C = C; fs.G = G; fs.ws_cols = ws; fs.wpad = wpad; fs.nSmax = nSmax; fs.nOwnMax = nOwnMax;
+    fs.smem = smem; fs.tc = tc; fs.aligned = aligned;
+    memcpy(fs.tmaps[0], &tmX, sizeof tmX);
+    memcpy(fs.tmaps[1], &tmXK, sizeof tmXK);
+    memcpy(fs.tmaps[2], &tmXM, sizeof tmXM);
+    fs.cfg_key = key;
+  }
+  const int C = fs.C, G = fs.G, ws = fs.ws_cols, wpad = fs.wpad, nSmax = fs.nSmax, nOwnMax = fs.nOwnMax;
+  const size_t smem = fs.smem;
+  const bool tc = fs.tc, aligned = fs.aligned;
+  CUtensorMap tmX, tmXK, tmXM;
+  memcpy(&tmX, fs.tmaps[0], sizeof tmX);
+  memcpy(&tmXK, fs.tmaps[1], sizeof tmXK);
+  memcpy(&tmXM, fs.tmaps[2], sizeof tmXM);
+  const int nCTA = G * C;
 
   // accumulator slot: [C][ws][32] dW1 slices (k-major), then the W2/b1/b2 block (16-B aligned)
   const int nsmp = (O * H + H + O + 3) & ~3;
   const int64_t small_off = (int64_t)C * ws * 32;
   const int64_t slot = (small_off + nsmp + 31) & ~int64_t(31);
-  const size_t need = kSlots * slot * sizeof(float) + 256 + n_steps * sizeof(int64_t);
+  const size_t need = kSlots * slot * sizeof(float) + 256;
   if (fs.ws_bytes < need) {
     if (fs.ws) cudaFree(fs.ws);
     fs.ws = nullptr;
     fs.ws_bytes = 0;
+    fs.ws_ready = false;
     if (cudaMalloc(&fs.ws, need) != cudaSuccess) {
       snprintf(g_fs_err, sizeof g_fs_err, "workspace allocation of %zu bytes failed", need);
       return -1;
     }
     fs.ws_bytes = need;
+  }
+  if (fs.ring_key[0] != slot || fs.ring_key[1] != nCTA) fs.ws_ready = false;
+  // batch starts: host array -> pinned staging buffer (double-buffered) -> device, asynchronous
+  if (fs.starts_cap < (size_t)n_steps) {
+    for (int i = 0; i < 2; ++i) {
+      if (fs.h_ev[i]) cudaEventSynchronize(fs.h_ev[i]);
+      if (fs.h_starts[i]) cudaFreeHost(fs.h_starts[i]);
+      fs.h_starts[i] = nullptr;
+    }
+    if (fs.d_starts) cudaFree(fs.d_starts);
+    fs.d_starts = nullptr;
+    fs.starts_cap = 0;
+    const size_t cap = std::max<size_t>(1024, (size_t)n_steps);
+    if (cudaMalloc(&fs.d_starts, cap * sizeof(int64_t)) != cudaSuccess ||
+        cudaMallocHost(&fs.h_starts[0], cap * sizeof(int64_t)) != cudaSuccess ||
+        cudaMallocHost(&fs.h_starts[1], cap * sizeof(int64_t)) != cudaSuccess) {
+      snprintf(g_fs_err, sizeof g_fs_err, "batch-start buffers: %s", cudaGetErrorString(cudaGetLastError()));
+      return -1;
+    }
+    for (int i = 0; i < 2; ++i)
+      if (!fs.h_ev[i]) cudaEventCreateWithFlags(&fs.h_ev[i], cudaEventDisableTiming);
+    fs.starts_cap = cap;
   }
   char *base = static_cast<char *>(fs.ws);
   FusedParams p{};
@@ -902,8 +963,7 @@ int fused_small_train_steps(FusedSmall &fs, cudaStream_t st, const std::vector<i
   p.X = X; p.Y = Y; p.params = params;
   p.acc = reinterpret_cast<float *>(base);
   p.bar = reinterpret_cast<unsigned *>(base + kSlots * slot * sizeof(float));
-  int64_t *dstarts = reinterpret_cast<int64_t *>(base + kSlots * slot * sizeof(float) + 256);
-  p.starts = dstarts;
+  p.starts = fs.d_starts;
   p.step_loss = step_loss;
   static long long *prof_buf = nullptr;
   const bool prof = env_int("NF_FUSED_PROF", 0) != 0;
@@ -913,17 +973,38 @@ int fused_small_train_steps(FusedSmall &fs, cudaStream_t st, const std::vector<i
     p.prof = prof_buf;
   }
 
-  cudaError_t e = cudaMemsetAsync(base, 0, kSlots * slot * sizeof(float) + 256, st);
-  if (e == cudaSuccess)
-    e = cudaMemcpyAsync(dstarts, starts, n_steps * sizeof(int64_t), cudaMemcpyHostToDevice, st);
-  if (e == cudaSuccess && step_loss) e = cudaMemsetAsync(step_loss, 0, n_steps * sizeof(float), st);
+  cudaError_t e = cudaSuccess;
+  if (!fs.ws_ready) {  // a fresh ring: all slots zero, counter 0
+    e = cudaMemsetAsync(base, 0, kSlots * slot * sizeof(float) + 256, st);
+    fs.steps_done = 0;
+    fs.bar_base = 0;
+    fs.ring_key[0] = slot;
+    fs.ring_key[1] = nCTA;
+  }
+  p.slot0 = (int)(fs.steps_done % kSlots);
+  p.bar_base = fs.bar_base;
+  {
+    const int hb = fs.h_i;
+    fs.h_i ^= 1;
+    if (e == cudaSuccess) e = cudaEventSynchronize(fs.h_ev[hb]);  // its previous copy has completed
+    if (e == cudaSuccess) {
+      memcpy(fs.h_starts[hb], starts, n_steps * sizeof(int64_t));
+      e = cudaMemcpyAsync(fs.d_starts, fs.h_starts[hb], n_steps * sizeof(int64_t), cudaMemcpyHostToDevice, st);
+    }
+    if (e == cudaSuccess) e = cudaEventRecord(fs.h_ev[hb], st);
+  }
   if (e == cudaSuccess) {
+    static const bool coop = env_int("NF_FUSED_NOCOOP", 0) == 0;
     cudaLaunchConfig_t cfg = {};
-    cudaLaunchAttribute at[1];
+    cudaLaunchAttribute at[2];
     at[0].id = cudaLaunchAttributeClusterDimension;
     at[0].val.clusterDim = {(unsigned)C, 1, 1};
+    // cooperative: the runtime guarantees every CTA is co-resident (the grid barriers need it)
+    // or fails the launch, instead of a hang when another stream holds SMs
+    at[1].id = cudaLaunchAttributeCooperative;
+    at[1].val.cooperative = 1;
     cfg.attrs = at;
-    cfg.numAttrs = 1;
+    cfg.numAttrs = coop ? 2 : 1;
     cfg.gridDim = dim3(G * C);
     cfg.blockDim = dim3(kThreads);
     cfg.dynamicSmemBytes = smem;
@@ -932,11 +1013,28 @@ int fused_small_train_steps(FusedSmall &fs, cudaStream_t st, const std::vector<i
     auto kern = tc    ? fused_small_kernel<true, -1, -1>
                 : sig ? fused_small_kernel<false, ACT_SIGMOID, ACT_SIGMOID>
                       : fused_small_kernel<false, -1, -1>;
+    static bool coop_ok = true;
+    if (!coop_ok) cfg.numAttrs = 1;
     e = cudaLaunchKernelEx(&cfg, kern, p, tmX, tmXK, tmXM);
+    if (e != cudaSuccess && cfg.numAttrs == 2 && e != cudaErrorCooperativeLaunchTooLarge) {
+      // cooperative + cluster launch unsupported by this driver: plain cluster launch (the grid
+      // was sized from cudaOccupancyMaxActiveClusters); a too-large grid is still an error
+      cudaGetLastError();
+      coop_ok = false;
+      cfg.numAttrs = 1;
+      e = cudaLaunchKernelEx(&cfg, kern, p, tmX, tmXK, tmXM);
+    }
     count_launch();
     char nt[64];
-    snprintf(nt, sizeof nt, "cluster=%d steps=%lld", C, (long long)n_steps);
+    snprintf(nt, sizeof nt, "cluster=%d steps=%lld%s", C, (long long)n_steps, cfg.numAttrs == 2 ? " cooperative" : "");
     log_launch(reinterpret_cast<const void *>(kern), cfg.gridDim, cfg.blockDim, smem, nt);
+  }
+  if (e == cudaSuccess) {
+    fs.ws_ready = true;
+    fs.steps_done += (uint64_t)n_steps;
+    fs.bar_base += (unsigned)(n_steps * nCTA);
+  } else {
+    fs.ws_ready = false;
   }
   if (e != cudaSuccess) {
     snprintf(g_fs_err, sizeof g_fs_err, "launch (C=%d G=%d smem=%zu): %s", C, G, smem, cudaGetErrorString(e));
@@ -1011,6 +1109,20 @@ void fused_small_release(FusedSmall &fs) {
   if (fs.ws) cudaFree(fs.ws);
   fs.ws = nullptr;
   fs.ws_bytes = 0;
+  fs.ws_ready = false;
+  for (int i = 0; i < 2; ++i) {
+    if (fs.h_ev[i]) {
+      cudaEventSynchronize(fs.h_ev[i]);
+      cudaEventDestroy(fs.h_ev[i]);
+    }
+    if (fs.h_starts[i]) cudaFreeHost(fs.h_starts[i]);
+    fs.h_ev[i] = nullptr;
+    fs.h_starts[i] = nullptr;
+  }
+  if (fs.d_starts) cudaFree(fs.d_starts);
+  fs.d_starts = nullptr;
+  fs.starts_cap = 0;
+  fs.cfg_key.clear();
 }
 
 void fused_small_invalidate(FusedSmall &fs) { fs.valid = false; }
