@@ -115,6 +115,14 @@ struct nf_net {
   int64_t ws_rows = 0;
   std::vector<float *> A, S;
   DevBuf stash;
+  // transposed copies for the weight-gradient contractions that read them K-major:
+  // tpose[l] -> DT[l] = delta_l^T [n_l][rows] and (l >= 2) AT[l-1] = A_{l-1}^T [n_{l-1}][rows]
+  std::vector<char> tpose;
+  std::vector<float *> AT, DT;
+  DevBuf tstash;
+  int64_t t_rows = 0;
+  std::vector<char> t_key;
+  bool red_round = false;                // a TF32 step reduced split-K terms into W: re-round shadow
   Workspace ws;
   DevBuf partial;
   // backward: the weight-gradient GEMMs (K4 + bias) of layer l run on a side stream,
@@ -185,6 +193,57 @@ int ensure_ws(nf_net *net, int64_t rows) {
   return NF_OK;
 }
 
+// Which weight-gradient contractions read transposed (K-major) copies of their operands, written
+// by the producing epilogues: the big tensor-core ones (more than one wave of 128 x 256 tiles: the
+// persistent kernels of config 5), whose MN-major smem operands cost ~16 % of the tensor rate.
+// NF_MATH_TF32 by default (NF_TPOSE=0 off, NF_TPOSE=2 also in the 3xTF32 fp32 mode).
+int ensure_tpose(nf_net *net, const float *x, int64_t n) {
+  static const int mode = getenv("NF_TPOSE") ? atoi(getenv("NF_TPOSE")) : 1;
+  const int L = net->L;
+  std::vector<char> tp(L + 1, 0);
+  const bool on = mode == 2 ? net->math != NF_MATH_FP64 : (mode == 1 && net->math == NF_MATH_TF32);
+  if (on && n >= 1024) {
+    for (int l = 1; l <= L; ++l) {
+      const int M = net->dims[l], N = net->dims[l - 1];
+      const int64_t tiles = (int64_t)((M + 127) / 128) * ((N + 255) / 256);
+      if (N <= 128 || tiles <= 148 || !gemm_grad_tc(M, N, (int)n, net->S[l], l > 1 ? net->A[l - 1] : x)) continue;
+      // the producers must be tensor-core epilogues (they write the copies)
+      const bool d_ok = l == L ? gemm_fwd_tc((int)n, M, N, l > 1 ? net->A[l - 1] : x, net->W(l))
+                               : gemm_bwd_tc((int)n, M, net->dims[l + 1], net->S[l + 1], net->W(l + 1));
+      const bool a_ok = l == 1 || gemm_fwd_tc((int)n, N, net->dims[l - 2], l > 2 ? net->A[l - 2] : x, net->W(l - 1));
+      tp[l] = d_ok && a_ok;
+    }
+  }
+  net->tpose = tp;
+  int64_t need = 0;
+  for (int l = 1; l <= L; ++l)
+    if (tp[l]) need += (int64_t)net->dims[l] + (l > 1 ? net->dims[l - 1] : 0);
+  if (need == 0) return NF_OK;
+  if (tp == net->t_key && n <= net->t_rows) return NF_OK;
+  cudaStreamCaptureStatus cs = cudaStreamCaptureStatusNone;
+  cudaStreamIsCapturing(net->stream, &cs);
+  if (cs != cudaStreamCaptureStatusNone) {  // no allocation inside a graph capture: MN-major operands
+    net->tpose.assign(L + 1, 0);
+    return NF_OK;
+  }
+  NF_CUDA(cudaStreamSynchronize(net->stream));
+  drop_graph(net);
+  NF_CUDA(net->tstash.ensure((size_t)(need * n) * sizeof(float)));
+  net->AT.assign(L + 1, nullptr);
+  net->DT.assign(L + 1, nullptr);
+  float *p = net->tstash.as<float>();
+  for (int l = 1; l <= L; ++l)
+    if (tp[l]) {
+      net->DT[l] = p; p += (int64_t)net->dims[l] * n;
+      if (l > 1) { net->AT[l - 1] = p; p += (int64_t)net->dims[l - 1] * n; }
+    }
+  net->t_key = tp;
+  net->t_rows = n;
+  return NF_OK;
+}
+
+bool tposed(const nf_net *net, int l) { return l >= 1 && l < (int)net->tpose.size() && net->tpose[l]; }
+
 // NF_MATH_TF32: make the weight shadow current (one rounding pass after any write of params
 // other than a TF32 step's own epilogues)
 int ensure_shadow(nf_net *net) {
@@ -215,6 +274,8 @@ int forward(nf_net *net, const float *x, const float *y, int64_t n, int mode) {
     // TF32: a hidden layer's A and the output layer's delta_L are operands of later tensor-core
     // contractions -> stored RN-rounded (the net's output A_L never is)
     EpiFwd epi{net->b(l), net->A[l], net->S[l], y, net->dims[l], net->act(l), lm, (t && (lm == 1 || l < L)) ? 1 : 0};
+    if (lm == 0 && tposed(net, l + 1)) { epi.T = net->AT[l]; epi.ldT = (int)n; }   // A_l^T for K4(l+1)
+    if (lm == 1 && tposed(net, l)) { epi.T = net->DT[l]; epi.ldT = (int)n; }       // delta_L^T for K4(L)
     NF_CUDA(gemm_fwd(net->stream, (int)n, net->dims[l], net->dims[l - 1], in, net->W(l), epi, net->ws,
                      t ? net->Wt(l) : nullptr));
     in = net->A[l];
@@ -257,6 +318,9 @@ int backward(nf_net *net, const float *x, int64_t n, float eta, float *grad, flo
   NF_CUDA(cudaStreamWaitEvent(side, net->ev[0], 0));
   const float scale = (float)((double)eta / (double)n);
   std::vector<char> bias_done(net->L + 1, 0);  // layer's bias update applied by K3's epilogue
+  // TF32 SGD: split-K terms reduced into W leave the shadow stale -> one rounding pass at the end
+  net->red_round = false;
+  net->ws.red_flag = net->ws2.red_flag = (!grad && net->tf32()) ? &net->red_round : nullptr;
   for (int l = net->L; l >= 1; --l) {
     const int nl = net->dims[l], nk = net->dims[l - 1];
     const bool fused = l == net->L && net->out_fused;  // K3(L) ran inside the forward kernel
@@ -264,6 +328,7 @@ int backward(nf_net *net, const float *x, int64_t n, float eta, float *grad, flo
     if (l > 1 && !fused) {
       EpiBwd eb{net->S[l - 1], nk};
       eb.rnd = t ? 1 : 0;
+      if (tposed(net, l - 1)) { eb.T = net->DT[l - 1]; eb.ldT = (int)n; }  // delta_{l-1}^T for K4(l-1)
       const float *aprev2 = l > 2 ? net->A[l - 2] : x;  // the operand of layer l-1's weight GEMM
       if (!grad && gemm_bwd_fuses_bias((int)n, nk, nl, net->S[l], net->W(l)) &&
           gemm_grad_tc(nk, net->dims[l - 2], (int)n, net->S[l - 1], aprev2)) {
@@ -284,13 +349,17 @@ int backward(nf_net *net, const float *x, int64_t n, float eta, float *grad, flo
     else if (l == 1 && net->L > 1 && side != main_st && (net->math != NF_MATH_TF32 || n <= 2048)) {
       // the main stream is idle after the last K3: K4(1) there, concurrent with K4(2) on the side
       // stream (c4 134 -> 130 us, 3xTF32 c3 462 -> 445 us; c3's 1xTF32 pair contends: 154 -> 157)
-      NF_CUDA(gemm_grad(main_st, nl, nk, (int)n, net->S[l], aprev, eg, net->ws, bias_done[l] != 0));
+      NF_CUDA(gemm_grad(main_st, nl, nk, (int)n, net->S[l], aprev, eg, net->ws, bias_done[l] != 0,
+                        tposed(net, l) ? net->DT[l] : nullptr, tposed(net, l) && l > 1 ? net->AT[l - 1] : nullptr));
       kst = main_st;
-    } else NF_CUDA(gemm_grad(side, nl, nk, (int)n, net->S[l], aprev, eg, net->ws2, bias_done[l] != 0));
+    } else NF_CUDA(gemm_grad(side, nl, nk, (int)n, net->S[l], aprev, eg, net->ws2, bias_done[l] != 0,
+                             tposed(net, l) ? net->DT[l] : nullptr, tposed(net, l) && l > 1 ? net->AT[l - 1] : nullptr));
     if (layer_done && layer_done[l - 1]) NF_CUDA(cudaEventRecord(layer_done[l - 1], kst));  // nf_grad_layers
   }
   NF_CUDA(cudaEventRecord(net->ev[net->L + 1], side));  // join
   NF_CUDA(cudaStreamWaitEvent(main_st, net->ev[net->L + 1], 0));
+  net->ws.red_flag = net->ws2.red_flag = nullptr;
+  if (net->red_round) NF_CUDA(round_tf32(main_st, net->params, net->params_t, net->nparams));
   return NF_OK;
 }
 
@@ -360,6 +429,7 @@ int train_batch_dev(nf_net *net, const float *x, const float *y, int64_t n, floa
     return backward64(net, x, n, (double)eta, nullptr);
   }
   if ((rc = ensure_ws(net, n))) return rc;
+  if ((rc = ensure_tpose(net, x, n))) return rc;
   if ((rc = forward(net, x, y, n, 0))) return rc;
   if (step_loss && !net->out_fused) {  // (the fused output layer computes the cost itself)
     NF_CUDA(net->red.ensure(red_bytes()));
@@ -784,6 +854,7 @@ static int train_steps_device(nf_net *net, const float *dX, const float *dY, int
     if ((rc = net->math == NF_MATH_FP64 ? ensure_ws64(net, batch) : ensure_ws(net, batch))) return rc;
     if ((rc = ensure_side(net))) return rc;
     if ((rc = ensure_shadow(net))) return rc;  // before capture: the graph keeps it current
+    if (net->math != NF_MATH_FP64 && (rc = ensure_tpose(net, dX + st[0] * n0, batch))) return rc;
     NF_CUDA(net->red.ensure(red_bytes()));
     std::vector<int64_t> key = {(int64_t)(uintptr_t)dX, (int64_t)(uintptr_t)dY, N, batch, n_steps,
                                 (int64_t)(uintptr_t)step_loss, (int64_t)(uintptr_t)net->stream, net->math,
@@ -947,6 +1018,7 @@ int nf_grad_layers(nf_net *net, const float *x, const float *y, int64_t n, float
     NF_CUDA(f64_round(net->stream, net->grad64.as<double>(), dg, net->nparams));
   } else {
     if ((rc = ensure_ws(net, n))) return rc;
+    if ((rc = ensure_tpose(net, dx, n))) return rc;
     if ((rc = forward(net, dx, dy, n, 0))) return rc;
     if ((rc = backward(net, dx, n, 0.0f, dg, nullptr, events && !host_out ? reinterpret_cast<cudaEvent_t const *>(events)
                                                                             : nullptr)))

@@ -39,9 +39,14 @@ struct GemmArgs {
 // rnd (NF_MATH_TF32): the values this epilogue stores as the operand of a later tensor-core
 // contraction -- a hidden layer's A, the output layer's delta_L in S -- are rounded to the
 // nearest TF32 value (tf32_rn; the output layer's A, the net's output, never is).
+// T (tensor-core path only, nullable): a transposed copy [n][ldT] of the value stored -- A for a
+// hidden layer, delta_L for the output layer -- so that the weight-gradient contraction reads it
+// K-major (the batch is that contraction's K).
 struct EpiFwd {
   static constexpr bool kRed = false;
+  static constexpr bool kHasT = true;
   const float *bias; float *A; float *S; const float *Y; int ld; int act; int mode; int rnd = 0;
+  float *T = nullptr; int ldT = 0;
   __device__ __forceinline__ float load(int m, int n) const {
     return mode == 1 ? Y[(int64_t)m * ld + n] : 0.0f;
   }
@@ -60,8 +65,10 @@ struct EpiFwd {
   // row r at v[33 r].  The activation and the mode are compile-time inside the strip (one
   // switch per strip), and each 8-row group evaluates its 8 activations unconditionally so the
   // eight dependent exp/rcp chains interleave; only the stores are predicated.
+  // (v: the strip's accumulators; each is replaced by the value stored -- the input of the
+  // transposed copy, see store_t)
   template <int K, int MODE, bool RND>
-  __device__ __forceinline__ void strip_km(int m0, int mlim, int n, const float *v) const {
+  __device__ __forceinline__ void strip_km(int m0, int mlim, int n, float *v) const {
     const float bn = bias[n];
     const int rows = min(32, mlim - m0);
 #pragma unroll 1
@@ -82,15 +89,22 @@ struct EpiFwd {
       for (int u = 0; u < 8; ++u) {
         if (r0 + u < rows) {
           const int64_t i = (int64_t)(m0 + r0 + u) * ld + n;
-          A[i] = (RND && MODE != 1) ? tf32_rn(a[u]) : a[u];
+          const float av = (RND && MODE != 1) ? tf32_rn(a[u]) : a[u];
+          A[i] = av;
           if (MODE == 0) S[i] = s[u];
-          if (MODE == 1) S[i] = RND ? tf32_rn((a[u] - y[u]) * s[u]) : (a[u] - y[u]) * s[u];
+          if (MODE == 1) {
+            const float d = RND ? tf32_rn((a[u] - y[u]) * s[u]) : (a[u] - y[u]) * s[u];
+            S[i] = d;
+            v[33 * (r0 + u)] = d;
+          } else {
+            v[33 * (r0 + u)] = av;
+          }
         }
       }
     }
   }
   template <int K>
-  __device__ __forceinline__ void strip_t(int m0, int mlim, int n, const float *v) const {
+  __device__ __forceinline__ void strip_t(int m0, int mlim, int n, float *v) const {
     if (rnd) {
       if (mode == 0) strip_km<K, 0, true>(m0, mlim, n, v);
       else if (mode == 1) strip_km<K, 1, true>(m0, mlim, n, v);
@@ -101,7 +115,7 @@ struct EpiFwd {
       else strip_km<K, 2, false>(m0, mlim, n, v);
     }
   }
-  __device__ __forceinline__ void strip(int m0, int mlim, int n, const float *v) const {
+  __device__ __forceinline__ void strip(int m0, int mlim, int n, float *v) const {
     switch (act) {
       case ACT_SIGMOID: strip_t<ACT_SIGMOID>(m0, mlim, n, v); break;
       case ACT_TANH: strip_t<ACT_TANH>(m0, mlim, n, v); break;
@@ -131,9 +145,11 @@ __device__ __forceinline__ void strip_generic(const E &e, int m0, int mlim, int 
 // nearest TF32 value; the fused bias sum uses the unrounded deltas.
 struct EpiBwd {
   static constexpr bool kRed = false;
+  static constexpr bool kHasT = true;
   float *SD; int ld;
   float *bias = nullptr; float bscale = 0.0f;
   int rnd = 0;
+  float *T = nullptr; int ldT = 0;  // transposed copy of delta (tensor-core path), see EpiFwd
   __device__ __forceinline__ float load(int m, int n) const { return SD[(int64_t)m * ld + n]; }
   __device__ __forceinline__ void store(int m, int n, float acc, float s) const {
     SD[(int64_t)m * ld + n] = rnd ? tf32_rn(acc * s) : acc * s;
@@ -143,11 +159,7 @@ struct EpiBwd {
     SD[(int64_t)m * ld + n] = rnd ? tf32_rn(d) : d;
     if (bias) asm volatile("red.global.add.f32 [%0], %1;" ::"l"(bias + n), "f"(-bscale * d) : "memory");
   }
-  __device__ __forceinline__ void strip(int m0, int mlim, int n, const float *v) const {
-    if (!bias) {
-      strip_generic(*this, m0, mlim, n, v);
-      return;
-    }
+  __device__ __forceinline__ void strip(int m0, int mlim, int n, float *v) const {
     float aux[32];
 #pragma unroll
     for (int r = 0; r < 32; ++r) aux[r] = m0 + r < mlim ? load(m0 + r, n) : 0.0f;
@@ -156,10 +168,12 @@ struct EpiBwd {
     for (int r = 0; r < 32; ++r)
       if (m0 + r < mlim) {
         const float d = v[33 * r] * aux[r];
-        SD[(int64_t)(m0 + r) * ld + n] = rnd ? tf32_rn(d) : d;
+        const float dr = rnd ? tf32_rn(d) : d;
+        SD[(int64_t)(m0 + r) * ld + n] = dr;
+        v[33 * r] = dr;
         sum += d;
       }
-    asm volatile("red.global.add.f32 [%0], %1;" ::"l"(bias + n), "f"(-bscale * sum) : "memory");
+    if (bias) asm volatile("red.global.add.f32 [%0], %1;" ::"l"(bias + n), "f"(-bscale * sum) : "memory");
   }
 };
 
@@ -170,8 +184,10 @@ struct EpiBwd {
 // in L2 cannot: the launcher re-rounds the layer's shadow after such a launch.)
 struct EpiGrad {
   static constexpr bool kRed = true;   // the update is additive: split-K terms can go straight in
+  static constexpr bool kHasT = false;
   float *W; float *b; int ldw; int nreal; float scale; int store_only;
   float *Wt = nullptr;
+  float *T = nullptr; int ldT = 0;     // (unused)
   __device__ __forceinline__ float *at(int m, int n) const { return n < nreal ? W + (int64_t)m * ldw + n : b + m; }
   __device__ __forceinline__ float load(int m, int n) const { return store_only ? 0.0f : *at(m, n); }
   __device__ __forceinline__ void store(int m, int n, float acc, float w) const {
@@ -190,7 +206,7 @@ struct EpiGrad {
       asm volatile("red.global.add.f32 [%0], %1;" ::"l"(at(m0 + r, n)), "f"(f * v[33 * r]) : "memory");
   }
   __device__ __forceinline__ void operator()(int m, int n, float acc) const { store(m, n, acc, load(m, n)); }
-  __device__ __forceinline__ void strip(int m0, int mlim, int n, const float *v) const {
+  __device__ __forceinline__ void strip(int m0, int mlim, int n, float *v) const {
     strip_generic(*this, m0, mlim, n, v);
   }
 };

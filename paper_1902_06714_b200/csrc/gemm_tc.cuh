@@ -308,8 +308,14 @@ gemm_tc_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ 
           const int m = mrow0 + r;
           if (m < g.M && nok) g.partial[blockIdx.z * MN + (int64_t)m * g.N + n] = buf[r * 33 + lane];
         }
-      } else if (nok) {
-        epi.strip(mrow0, g.M, n, buf + lane);  // 32 rows of column n, loads before stores
+      } else {
+        if (nok) epi.strip(mrow0, g.M, n, buf + lane);  // 32 rows of column n, loads before stores
+        if constexpr (Epi::kHasT) {
+          if (epi.T) {  // transposed copy from the block of stored values
+            __syncwarp();
+            store_t(epi.T, epi.ldT, mrow0, g.M, nc, g.N, buf, lane);
+          }
+        }
       }
       __syncwarp();
     }
@@ -443,6 +449,12 @@ gemm_tc_persistent(const __grid_constant__ CUtensorMap tmA, const __grid_constan
         __syncwarp();
         const int n = nc + lane;
         if (n < N) epi.strip(mrow0, M, n, buf + lane);
+        if constexpr (Epi::kHasT) {
+          if (epi.T) {
+            __syncwarp();
+            store_t(epi.T, epi.ldT, mrow0, M, nc, N, buf, lane);
+          }
+        }
         __syncwarp();
       }
       tc_fence_before();

@@ -177,6 +177,9 @@ cudaError_t launch_tc(cudaStream_t st, int M, int N, int K, const TcOp &a, const
     splits = std::max(splits, 1);
   }
   if (force_splits > 1 && red) splits = std::max(splits, std::min(force_splits, nkb));
+  if constexpr (Epi::kHasT) {
+    if (epi.T) splits = 1;  // the transposed copy is written by the tile epilogue (no split-K partials)
+  }
   const int kbper = (nkb + splits - 1) / splits;
   splits = (nkb + kbper - 1) / kbper;  // no empty K-chunk
   red = red && splits > 1;
@@ -190,8 +193,11 @@ cudaError_t launch_tc(cudaStream_t st, int M, int N, int K, const TcOp &a, const
   g_note = note(epi_note(epi), red ? "splitk-red" : (splits > 1 ? "splitk-partial" : nullptr));
   cudaError_t e = launch_k(kern, dim3(tn, tm, splits), dim3(C::THREADS), C::SMEM, st, ta, tb, g, epi);
   if (e != cudaSuccess) return e;
-  if constexpr (Epi::kRed) {  // split-K terms went into W in L2: the TF32 shadow of W from the sum
-    if (red && epi.Wt) return round_tf32(st, epi.W, epi.Wt, (int64_t)M * epi.ldw);
+  if constexpr (Epi::kRed) {  // split-K terms went into W in L2: the TF32 shadow of W from the sum --
+    if (red && epi.Wt) {      // by the caller in one pass after the step when it asked to (ws.red_flag)
+      if (ws.red_flag) *ws.red_flag = true;
+      else return round_tf32(st, epi.W, epi.Wt, (int64_t)M * epi.ldw);
+    }
   }
   if (splits > 1 && !red) {
     const int64_t MN = (int64_t)M * N;
@@ -838,6 +844,16 @@ bool gemm_grad_tc(int M, int N, int K, const float *D, const float *Aprev) {
   return use_tc(M, N, K, a, b);
 }
 
+bool gemm_fwd_tc(int M, int N, int K, const float *A, const float *W) {
+  const TcOp a{A, K, false}, b{W, K, false};
+  return use_tc(M, N, K, a, b);
+}
+
+bool gemm_bwd_tc(int M, int N, int K, const float *D, const float *W) {
+  const TcOp a{D, K, false}, b{W, N, true};
+  return use_tc(M, N, K, a, b);
+}
+
 cudaError_t gemm_bwd(cudaStream_t st, int M, int N, int K, const float *D, const float *W,
                      const EpiBwd &epi, const Workspace &ws, const float *Wtc) {
   const TcOp a{D, K, false}, b{Wtc ? Wtc : W, N, true};
@@ -854,7 +870,8 @@ cudaError_t gemm_bwd(cudaStream_t st, int M, int N, int K, const float *D, const
 }
 
 cudaError_t gemm_grad(cudaStream_t st, int M, int N, int K, const float *D, const float *Aprev,
-                      const EpiGrad &epi, const Workspace &ws, bool bias_done) {
+                      const EpiGrad &epi, const Workspace &ws, bool bias_done, const float *DT,
+                      const float *AprevT) {
   const TcOp a{D, M, true}, b{Aprev, N, true};
   if (use_tc(M, N, K, a, b)) {
     // bias tendencies first (unless the delta GEMM's epilogue applied them): they read D only,
@@ -862,6 +879,13 @@ cudaError_t gemm_grad(cudaStream_t st, int M, int N, int K, const float *D, cons
     if (!bias_done) {
       cudaError_t e = bias_grad(st, D, K, M, epi, ws.partial, ws.partial_floats);
       if (e != cudaSuccess) return e;
+    }
+    // transposed copies written by the producing epilogues make the operands K-major (the MN-major
+    // smem layouts run the tensor core at 552 vs 659 TF/s for K/K, profiles/r01_tc_majors_accuracy_perf.txt)
+    if (DT) {
+      const TcOp at{DT, K, false};
+      if (AprevT) return run_tc<false, false>(st, M, N, K, at, TcOp{AprevT, K, false}, epi, ws);
+      return run_tc<false, true>(st, M, N, K, at, b, epi, ws);
     }
     return run_tc<true, true>(st, M, N, K, a, b, epi, ws);
   }

@@ -25,6 +25,9 @@ struct Workspace {
   float *partial = nullptr;
   size_t partial_floats = 0;
   int math = 0;
+  // non-null: a split-K SGD launch that reduced terms into W in L2 sets *red_flag instead of
+  // re-rounding that layer's TF32 shadow itself (the caller rounds once after the step)
+  bool *red_flag = nullptr;
 };
 
 // Which engine ran the last gemm_* call (for tests / the bench's kernel attribution).
@@ -42,8 +45,15 @@ cudaError_t gemm_bwd(cudaStream_t st, int M, int N, int K, const float *D, const
 // K4: C[M][N+1] = D^T (D is [K][M]) * [Aprev | 1] (Aprev is [K][N]), epilogue EpiGrad.
 // bias_done: the layer's bias update was already applied by the delta GEMM (EpiBwd::bias); only
 // meaningful on the tensor-core path (the SIMT path carries the bias as a ones column)
+// DT [M][K] / AprevT [N][K] (nullable): transposed copies of D / Aprev (written by their producers'
+// epilogues, EpiBwd::T / EpiFwd::T) -- the tensor-core path then reads K-major operands
 cudaError_t gemm_grad(cudaStream_t st, int M, int N, int K, const float *D, const float *Aprev,
-                      const EpiGrad &epi, const Workspace &ws, bool bias_done = false);
+                      const EpiGrad &epi, const Workspace &ws, bool bias_done = false, const float *DT = nullptr,
+                      const float *AprevT = nullptr);
+// whether gemm_fwd / gemm_bwd with these operands take the tensor-core path (where EpiFwd::T /
+// EpiBwd::T are honoured)
+bool gemm_fwd_tc(int M, int N, int K, const float *A, const float *W);
+bool gemm_bwd_tc(int M, int N, int K, const float *D, const float *W);
 // whether gemm_bwd with these operands takes the path whose epilogue can apply the bias update
 bool gemm_bwd_fuses_bias(int M, int N, int K, const float *D, const float *W);
 // whether gemm_grad with these operands takes the tensor-core path (bias as a separate sum)

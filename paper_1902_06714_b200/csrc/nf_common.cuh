@@ -121,6 +121,17 @@ __device__ __forceinline__ float tf32_rn(float x) {
   return __uint_as_float(r);
 }
 
+// Transposed copy of a 32 x 32 epilogue block (rows m0.., columns nc..; buf[r * 33 + c] holds the
+// value stored at (m0 + r, nc + c)): thread `lane` writes row m0 + lane of T^T, i.e. one
+// coalesced 128-B run T[nc + c][m0 .. m0 + 31] per column c.
+__device__ __forceinline__ void store_t(float *T, int ldT, int m0, int mlim, int nc, int nlim, const float *buf,
+                                        int lane) {
+  if (m0 + lane >= mlim) return;
+  const int cols = min(32, nlim - nc);
+#pragma unroll 8
+  for (int c = 0; c < cols; ++c) T[(int64_t)(nc + c) * ldT + m0 + lane] = buf[lane * 33 + c];
+}
+
 __device__ __forceinline__ float warp_sum(float v) {
 #pragma unroll
   for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
