@@ -910,6 +910,7 @@ static int train_steps_device(nf_net *net, const float *dX, const float *dY, int
 
 int nf_train_steps(nf_net *net, const float *X, const float *Y, int64_t N, int64_t batch,
                    const int64_t *starts, int64_t n_steps, float eta, float *step_loss) {
+  host_trace("enter");
   if (int rc = check_net(net)) return rc;
   if (batch <= 0 || N < batch) return fail(NF_EINVAL, "need 1 <= batch <= N");
   if (n_steps < 0) return fail(NF_EINVAL, "n_steps < 0");
@@ -927,9 +928,12 @@ int nf_train_steps(nf_net *net, const float *X, const float *Y, int64_t N, int64
 
   // Device dataset: the steps run straight from it.
   const bool host_in = !is_device_ptr(X) || !is_device_ptr(Y);
+  host_trace("checks");
   if (!host_in) {
     std::vector<int64_t> st(starts, starts + n_steps);
-    return train_steps_device(net, X, Y, N, batch, st, n_steps, eta, step_loss, true);
+    const int rc = train_steps_device(net, X, Y, N, batch, st, n_steps, eta, step_loss, true);
+    host_trace("launched");
+    return rc;
   }
   // Host dataset (the e2e path): each step's batch is copied host -> device (one copy of its
   // x rows and one of its y rows), in chunks of steps through two staging slots on a copy

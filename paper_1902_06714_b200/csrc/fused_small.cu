@@ -902,6 +902,7 @@ int fused_small_train_steps(FusedSmall &fs, cudaStream_t st, const std::vector<i
     memcpy(fs.tmaps[2], &tmXM, sizeof tmXM);
     fs.cfg_key = key;
   }
+  host_trace("k6 config");
   const int C = fs.C, G = fs.G, ws = fs.ws_cols, wpad = fs.wpad, nSmax = fs.nSmax, nOwnMax = fs.nOwnMax;
   const size_t smem = fs.smem;
   const bool tc = fs.tc, aligned = fs.aligned;
@@ -993,6 +994,7 @@ int fused_small_train_steps(FusedSmall &fs, cudaStream_t st, const std::vector<i
     }
     if (e == cudaSuccess) e = cudaEventRecord(fs.h_ev[hb], st);
   }
+  host_trace("k6 starts");
   if (e == cudaSuccess) {
     static const bool coop = env_int("NF_FUSED_NOCOOP", 0) == 0;
     cudaLaunchConfig_t cfg = {};
@@ -1029,6 +1031,7 @@ int fused_small_train_steps(FusedSmall &fs, cudaStream_t st, const std::vector<i
     snprintf(nt, sizeof nt, "cluster=%d steps=%lld%s", C, (long long)n_steps, cfg.numAttrs == 2 ? " cooperative" : "");
     log_launch(reinterpret_cast<const void *>(kern), cfg.gridDim, cfg.blockDim, smem, nt);
   }
+  host_trace("k6 launch");
   if (e == cudaSuccess) {
     fs.ws_ready = true;
     fs.steps_done += (uint64_t)n_steps;

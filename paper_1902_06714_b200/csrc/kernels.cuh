@@ -13,6 +13,8 @@ inline void count_launch(int n = 1) { __atomic_add_fetch(&g_launches, n, __ATOMI
 // launch log (launchlog.cu; NF_LOG_LAUNCHES=1 or nf_debug_log_enable): demangled kernel name,
 // grid, block, dynamic smem and a note naming the runtime variant (e.g. "red" split-K terms)
 bool launch_log_on();
+// NF_TRACE_HOST=1: host-time stamps of one call's phases to stderr (us since the call's "enter")
+void host_trace(const char *what);
 // cudaFuncSetAttribute(MaxDynamicSharedMemorySize) once per (kernel, device, bytes): the
 // attribute is per device context, so a process driving several GPUs sets it on each
 cudaError_t set_max_smem(const void *kern, int bytes);

@@ -6,6 +6,7 @@
 #include <cxxabi.h>
 
 #include <atomic>
+#include <chrono>
 #include <cstdio>
 #include <cstdlib>
 #include <cstring>
@@ -34,6 +35,15 @@ bool launch_log_on() {
     v = g_log_on.load();
   }
   return v == 1;
+}
+
+void host_trace(const char *what) {
+  static const bool on = getenv("NF_TRACE_HOST") != nullptr;
+  if (!on) return;
+  static thread_local std::chrono::steady_clock::time_point t0;
+  const auto t = std::chrono::steady_clock::now();
+  if (!strcmp(what, "enter")) t0 = t;
+  fprintf(stderr, "[host] %-12s %8.2f us\n", what, std::chrono::duration<double, std::micro>(t - t0).count());
 }
 
 cudaError_t set_max_smem(const void *kern, int bytes) {

@@ -48,3 +48,21 @@ for k in (1, 2, 5, 20, 100, 500):
         host.append((t1 - t0) * 1e6)
     d, h = statistics.median(dev), statistics.median(host)
     print(f"steps {k:4d}: device {d:9.1f} us ({d / k:6.2f} us/step)   host call {h:7.1f} us", flush=True)
+
+# host-side breakdown of one call (NF_TRACE_HOST=1 stamps from the library) and the Python wrapper
+if os.environ.get("NF_TRACE_HOST"):
+    st = nxt(20)
+    torch.cuda.synchronize()
+    t0 = time.perf_counter()
+    net.train_steps(Xd, Yd, 1000, st, 3.0, step_loss=loss)
+    t1 = time.perf_counter()
+    print(f"python wrapper total {1e6 * (t1 - t0):.1f} us", flush=True)
+    lib = nf.lib()
+    import ctypes
+    args = (net.h, nf._ptr(Xd), nf._ptr(Yd), Xd.shape[0], 1000, nf._ptr(np.ascontiguousarray(st), np.int64), len(st),
+            ctypes.c_float(3.0), nf._ptr(loss))
+    torch.cuda.synchronize()
+    t0 = time.perf_counter()
+    lib.nf_train_steps(*args)
+    t1 = time.perf_counter()
+    print(f"raw ctypes call {1e6 * (t1 - t0):.1f} us", flush=True)
