@@ -96,19 +96,26 @@ def _check(rc: int):
         raise NFError(rc, lib().nf_last_error().decode())
 
 
+_TORCH_DT = {}
+
+
 def _ptr(a, dtype=np.float32):
     """Data pointer of a contiguous torch tensor or numpy array (no copies)."""
     if a is None:
         return None
+    if isinstance(a, np.ndarray):
+        if a.dtype != dtype or not a.flags.c_contiguous:
+            raise TypeError(f"expected a C-contiguous {np.dtype(dtype).name} array")
+        return a.ctypes.data
     if hasattr(a, "data_ptr"):          # torch.Tensor
-        import torch
-        want = {np.float32: torch.float32, np.int64: torch.int64}[dtype]
+        want = _TORCH_DT.get(dtype)
+        if want is None:
+            import torch
+            want = _TORCH_DT.setdefault(dtype, {np.float32: torch.float32, np.int64: torch.int64}[dtype])
         if a.dtype != want or not a.is_contiguous():
             raise TypeError(f"expected a contiguous {want} tensor")
-        return ctypes.c_void_p(a.data_ptr())
-    if not isinstance(a, np.ndarray) or a.dtype != dtype or not a.flags.c_contiguous:
-        raise TypeError(f"expected a C-contiguous {np.dtype(dtype).name} array")
-    return a.ctypes.data_as(ctypes.c_void_p)
+        return a.data_ptr()
+    raise TypeError(f"expected a C-contiguous {np.dtype(dtype).name} array or tensor")
 
 
 # ---------------------------------------------------------------- C-named functions
@@ -279,7 +286,8 @@ class Net:
         nf_train_batch(self.h, x, y, x.shape[0], eta)
 
     def train_steps(self, X, Y, batch: int, starts, eta: float, step_loss=None):
-        starts = np.ascontiguousarray(np.asarray(starts, dtype=np.int64))
+        if not (isinstance(starts, np.ndarray) and starts.dtype == np.int64 and starts.flags.c_contiguous):
+            starts = np.ascontiguousarray(np.asarray(starts, dtype=np.int64))
         nf_train_steps(self.h, X, Y, X.shape[0], batch, starts, len(starts), eta, step_loss)
 
     def grad(self, x, y, out=None):

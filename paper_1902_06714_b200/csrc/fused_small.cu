@@ -82,6 +82,13 @@ constexpr int kSmall = 32 * 32 + 64;  // capacity of the W2/b1/b2 tendency block
 constexpr int kSlots = 4;             // accumulator ring: step s uses slot s % 4; slot (s+2) % 4 is
                                       // zeroed between this step's barrier arrive and wait
 
+// Batch starts of calls with few steps travel in the launch's parameter buffer (no staging copy,
+// no event: ~8 us of host time per call), longer runs through a device array.
+constexpr int kInlineStarts = 1024;
+struct InlineStarts {
+  int64_t v[kInlineStarts];
+};
+
 struct FusedParams {
   int n0, H, O;          // dims
   int act_h, act_o;
@@ -97,7 +104,7 @@ struct FusedParams {
   float scale;           // eta / B
   float inv_B;
   const float *X, *Y;
-  const int64_t *starts; // device
+  const int64_t *starts; // device array, or null: the starts are in the kernel's InlineStarts
   float *params;         // flat [W1 b1 W2 b2]
   float *acc;            // kSlots accumulator slots (zeroed by the host)
   unsigned *bar;         // grid barrier counter (zeroed by the host)
@@ -189,7 +196,8 @@ __device__ __forceinline__ void act_sel(int rt, float z, float &a, float &s) {
 template <bool TC, int AH, int AO>
 __global__ void __launch_bounds__(kThreads, kMinBlocks)
 fused_small_kernel(const FusedParams p, const __grid_constant__ CUtensorMap tmX,
-                   const __grid_constant__ CUtensorMap tmXK, const __grid_constant__ CUtensorMap tmXM) {
+                   const __grid_constant__ CUtensorMap tmXK, const __grid_constant__ CUtensorMap tmXM,
+                   const __grid_constant__ InlineStarts ist) {
   extern __shared__ __align__(128) float sm[];
   const int C = (int)ptx::cluster_size();
   const int rank = (int)ptx::cluster_rank();
@@ -295,11 +303,12 @@ fused_small_kernel(const FusedParams p, const __grid_constant__ CUtensorMap tmX,
   const uint32_t xbytes = (uint32_t)(p.nSmax * p.ws * 4);
   // batch starts are read one step ahead of their use so their global-load latency overlaps
   // a whole step (next_start holds starts[s + 1] while step s runs)
-  int64_t next_start = p.n_steps > 0 ? p.starts[0] : 0;
+  auto start_of = [&](int64_t s) -> int64_t { return p.starts ? p.starts[s] : ist.v[s]; };
+  int64_t next_start = p.n_steps > 0 ? start_of(0) : 0;
   auto prefetch = [&](int64_t s) {
     const int buf = (int)(s & 1);
     const int64_t row0 = next_start + r0;
-    next_start = s + 1 < p.n_steps ? p.starts[s + 1] : 0;
+    next_start = s + 1 < p.n_steps ? start_of(s + 1) : 0;
     float *xs = xs0 + buf * xstride;
     if (TC) {
       // x tiles are staged by tc_issue (two layouts per step)
@@ -930,7 +939,7 @@ int fused_small_train_steps(FusedSmall &fs, cudaStream_t st, const std::vector<i
   }
   if (fs.ring_key[0] != slot || fs.ring_key[1] != nCTA) fs.ws_ready = false;
   // batch starts: host array -> pinned staging buffer (double-buffered) -> device, asynchronous
-  if (fs.starts_cap < (size_t)n_steps) {
+  if (n_steps > kInlineStarts && fs.starts_cap < (size_t)n_steps) {
     for (int i = 0; i < 2; ++i) {
       if (fs.h_ev[i]) cudaEventSynchronize(fs.h_ev[i]);
       if (fs.h_starts[i]) cudaFreeHost(fs.h_starts[i]);
@@ -984,7 +993,11 @@ int fused_small_train_steps(FusedSmall &fs, cudaStream_t st, const std::vector<i
   }
   p.slot0 = (int)(fs.steps_done % kSlots);
   p.bar_base = fs.bar_base;
-  {
+  static thread_local InlineStarts ist;  // host staging of the launch parameter buffer
+  if (n_steps <= kInlineStarts) {
+    memcpy(ist.v, starts, n_steps * sizeof(int64_t));
+    p.starts = nullptr;
+  } else {
     const int hb = fs.h_i;
     fs.h_i ^= 1;
     if (e == cudaSuccess) e = cudaEventSynchronize(fs.h_ev[hb]);  // its previous copy has completed
@@ -1017,14 +1030,14 @@ int fused_small_train_steps(FusedSmall &fs, cudaStream_t st, const std::vector<i
                       : fused_small_kernel<false, -1, -1>;
     static bool coop_ok = true;
     if (!coop_ok) cfg.numAttrs = 1;
-    e = cudaLaunchKernelEx(&cfg, kern, p, tmX, tmXK, tmXM);
+    e = cudaLaunchKernelEx(&cfg, kern, p, tmX, tmXK, tmXM, ist);
     if (e != cudaSuccess && cfg.numAttrs == 2 && e != cudaErrorCooperativeLaunchTooLarge) {
       // cooperative + cluster launch unsupported by this driver: plain cluster launch (the grid
       // was sized from cudaOccupancyMaxActiveClusters); a too-large grid is still an error
       cudaGetLastError();
       coop_ok = false;
       cfg.numAttrs = 1;
-      e = cudaLaunchKernelEx(&cfg, kern, p, tmX, tmXK, tmXM);
+      e = cudaLaunchKernelEx(&cfg, kern, p, tmX, tmXK, tmXM, ist);
     }
     count_launch();
     char nt[64];
