@@ -194,8 +194,8 @@ int ensure_ws(nf_net *net, int64_t rows) {
 }
 
 // Which weight-gradient contractions read transposed (K-major) copies of their operands, written
-// by the producing epilogues: the big tensor-core ones (more than one wave of 128 x 256 tiles: the
-// persistent kernels of config 5), whose MN-major smem operands cost ~16 % of the tensor rate.
+// by the producing epilogues: the big tensor-core ones (a wave of 128 x 256 tiles or more: config
+// 5's), whose MN-major smem operands cost ~16 % of the tensor rate.
 // NF_MATH_TF32 by default (NF_TPOSE=0 off, NF_TPOSE=2 also in the 3xTF32 fp32 mode).
 int ensure_tpose(nf_net *net, const float *x, int64_t n) {
   static const int mode = getenv("NF_TPOSE") ? atoi(getenv("NF_TPOSE")) : 1;
@@ -206,7 +206,8 @@ int ensure_tpose(nf_net *net, const float *x, int64_t n) {
     for (int l = 1; l <= L; ++l) {
       const int M = net->dims[l], N = net->dims[l - 1];
       const int64_t tiles = (int64_t)((M + 127) / 128) * ((N + 255) / 256);
-      if (N <= 128 || tiles <= 148 || !gemm_grad_tc(M, N, (int)n, net->S[l], l > 1 ? net->A[l - 1] : x)) continue;
+      // (one wave of 128 x 256 tiles or more: config 5's 4096-wide layers and its 1024-wide output layer)
+      if (N <= 128 || tiles < 148 * 4 / 5 || !gemm_grad_tc(M, N, (int)n, net->S[l], l > 1 ? net->A[l - 1] : x)) continue;
       // the producers must be tensor-core epilogues (they write the copies)
       const bool d_ok = l == L ? gemm_fwd_tc((int)n, M, N, l > 1 ? net->A[l - 1] : x, net->W(l))
                                : gemm_bwd_tc((int)n, M, net->dims[l + 1], net->S[l + 1], net->W(l + 1));
