@@ -78,7 +78,7 @@ constexpr int kTcXBytes = kTcXLoK + 3 * kTcAS + 128 * 128;  // 88064
 constexpr int kTcWBytes = 2 * 4 * 32 * 128;     // W1 slice hi | lo, K-major [32 j][128 px]
 constexpr int kTcDBytes = 2 * kTcAS;            // delta_1 hi | lo, MN-major [72 rows][32 j]
 constexpr int kTcBytes = kTcXBytes + kTcWBytes + kTcDBytes;
-constexpr int kSmall = 32 * 32 + 68;  // capacity of the W2/b1/b2 + cost block: O*H + H + O + 1 <= 1092
+constexpr int kSmall = 32 * 32 + 64;  // capacity of the W2/b1/b2 tendency block: O*H + H + O <= 1088
 constexpr int kSlots = 4;             // accumulator ring: step s uses slot s % 4; slot (s+2) % 4 is
                                       // zeroed between this step's barrier arrive and wait
 
@@ -100,7 +100,7 @@ struct FusedParams {
   int64_t n_steps;
   int64_t slot;          // accumulator slot stride (floats, multiple of 32)
   int64_t small_off;     // offset of the W2/b1/b2 block inside a slot
-  int nsmp;              // W2/b1/b2 block length O*H + H + O + 1 (the step's cost), rounded up to a multiple of 4
+  int nsmp;              // W2/b1/b2 block length O*H + H + O, rounded up to a multiple of 4
   float scale;           // eta / B
   float inv_B;
   const float *X, *Y;
@@ -119,10 +119,9 @@ struct FusedParams {
 
 __device__ __forceinline__ int row_begin(int g, int B, int G) { return (int)(((int64_t)g * B) / G); }
 __host__ __device__ __forceinline__ int own_begin(int c, int nS, int C) { return (c * nS) / C; }
-// Each rank c of a cluster reduces (co_sums) pixel slice c of dW1 with the rank-c CTAs of the
-// other clusters only, behind its own barrier counter (G arrivals per step, not G*C); rank 0 also
-// reduces the W2/b1/b2 tendency block (+ the step's cost) and hands the reduced block to its peers.
-constexpr int kBarStride = 32;  // uints between the per-rank barrier counters (128 B)
+// slice of the W2/b tendency block (nsmp floats) reduced by rank c: 16-B aligned chunks
+__host__ __device__ __forceinline__ int e_begin(int c, int C, int nsmp) { return 4 * (((nsmp / 4) * c) / C); }
+__host__ __device__ __forceinline__ int e_slot(int C) { return ((kSmall / C + 4) + 3) & ~3; }
 
 __device__ __forceinline__ void cp_async4(float *dst, const float *src) {
   asm volatile("cp.async.ca.shared.global [%0], [%1], 4;" ::"r"(ptx::smem_u32(dst)), "l"(src) : "memory");
@@ -138,7 +137,7 @@ __host__ __device__ inline int al32(int v) { return (v + 31) & ~31; }  // 128-B 
 
 __host__ __device__ inline int xrows(int nSmax) { return (nSmax + kRG - 1) / kRG * kRG; }
 
-__host__ __device__ inline Smem smem_layout(int wpad, int nSmax, int nOwnMax, int C, bool tc, int nsmp) {
+__host__ __device__ inline Smem smem_layout(int wpad, int nSmax, int nOwnMax, int C, bool tc) {
   Smem L;
   int o = 32;  // mbarriers (and the TMEM address) live in the first 128 B
   L.tcr = o;   o = al32(o + (tc ? (kTcBytes + 1024) / 4 : 0));  // TC operand tiles (1024-B aligned inside)
@@ -154,7 +153,7 @@ __host__ __device__ inline Smem smem_layout(int wpad, int nSmax, int nOwnMax, in
   L.A1own = o; o = al32(o + nOwnMax * 32);         // a1 of the owned rows
   L.D2own = o; o = al32(o + nOwnMax * 32);         // delta_2 of the owned rows
   L.gpart = o; o = al32(o + kSmall);
-  L.grecv = o; o = al32(o + C * nsmp);            // rank 0: the peers' W2/b block partials
+  L.grecv = o; o = al32(o + C * e_slot(C));
   L.Gs = o;    o = al32(o + wpad * 32);            // [wpad][32]: dW1 slice partial, k-major like W1t
   L.Gs2 = o;   o = al32(o + (tc ? 0 : wpad * 32)); // second row-half partial (SIMT)
   L.Gr = o;    o = al32(o + wpad * 32);            // reduced slice read back
@@ -205,6 +204,7 @@ fused_small_kernel(const FusedParams p, const __grid_constant__ CUtensorMap tmX,
   const int g = blockIdx.x / C;
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   const int n0 = p.n0, H = p.H, O = p.O;
+  const int nCTA = gridDim.x;
 
   // pixel slice of this rank
   int k0, w;
@@ -219,16 +219,16 @@ fused_small_kernel(const FusedParams p, const __grid_constant__ CUtensorMap tmX,
   // rows of this cluster and the rows each rank owns inside them
   const int r0 = row_begin(g, p.B, p.G), nS = row_begin(g + 1, p.B, p.G) - r0;
   const int o0 = own_begin(rank, nS, C), nOwn = own_begin(rank + 1, nS, C) - o0;
-  const int nsmp = p.nsmp, nsm = O * H + H + O + 1;   // [W2 | b1 | b2 | cost]
-  unsigned *bar_rank = p.bar + rank * kBarStride;      // this rank's group counter
+  const int nsmp = p.nsmp, nsm = O * H + H + O;
+  const int e0 = e_begin(rank, C, nsmp), ne = e_begin(rank + 1, C, nsmp) - e0;
+  const int eslot = e_slot(C);
 
-  const Smem L = smem_layout(wpad, p.nSmax, p.nOwnMax, C, TC, p.nsmp);
+  const Smem L = smem_layout(wpad, p.nSmax, p.nOwnMax, C, TC);
   const int xstride = al32(xrows(p.nSmax) * wpad);
   uint64_t *bar_x = reinterpret_cast<uint64_t *>(sm);  // [2]
   uint64_t *bar_P = bar_x + 2;
   uint64_t *bar_D = bar_x + 3;
   uint64_t *bar_G = bar_x + 4;
-  uint64_t *bar_S = bar_x + 7;               // ranks != 0: rank 0's reduced W2/b block has landed
   uint64_t *bar_mma = bar_x + 5;             // TC: tcgen05.commit arrivals (2 per step)
   uint32_t *tmem_slot = reinterpret_cast<uint32_t *>(bar_x + 6);
   // TC operand tiles (1024-B aligned): X (x tile, K- or MN-phase), Wt (W1 hi|lo), Dt (delta_1 hi|lo)
@@ -254,7 +254,6 @@ fused_small_kernel(const FusedParams p, const __grid_constant__ CUtensorMap tmX,
     ptx::mbar_init(bar_P, 1);
     ptx::mbar_init(bar_D, 1);
     ptx::mbar_init(bar_G, 1);
-    ptx::mbar_init(bar_S, 1);
     ptx::mbar_init(bar_mma, 1);
     ptx::fence_mbar_init();
     if (p.aligned) ptx::prefetch_tensormap(&tmX);
@@ -297,9 +296,9 @@ fused_small_kernel(const FusedParams p, const __grid_constant__ CUtensorMap tmX,
   for (int c = 0; c < C; ++c) {
     if (c == rank) continue;
     bytesP += nOwn * 128;
-    bytesD += (own_begin(c + 1, nS, C) - own_begin(c, nS, C)) * 128 + (rank == 0 ? nsmp * 4 : 0);
+    bytesD += (own_begin(c + 1, nS, C) - own_begin(c, nS, C)) * 128 + ne * 4;
   }
-  const uint32_t bytesG = (uint32_t)(p.ws * 32 * 4 + (rank == 0 ? nsmp * 4 : 0));
+  const uint32_t bytesG = (uint32_t)(p.ws * 32 * 4 + nsmp * 4);
 
   const uint32_t xbytes = (uint32_t)(p.nSmax * p.ws * 4);
   // batch starts are read one step ahead of their use so their global-load latency overlaps
@@ -349,17 +348,6 @@ fused_small_kernel(const FusedParams p, const __grid_constant__ CUtensorMap tmX,
     __syncthreads();
   }
 
-  // W -= (eta/B) G for the W2/b1/b2 block from the reduced tendencies in gsm (every rank: rank 0
-  // after its read-back, the others from rank 0's copy one step later, before they need them)
-  auto apply_small = [&]() {
-    for (int e = tid; e < nsm - 1; e += kThreads) {
-      const float gv = p.scale * gsm[e];
-      if (e < O * H) { const int o = e / H; W2s[o * 33 + (e - o * H)] -= gv; }
-      else if (e < O * H + H) b1s[e - O * H] -= gv;
-      else b2s[e - O * H - H] -= gv;
-    }
-  };
-
   // P1 task geometry: kRG-row x 4-neuron tiles, K in kKP parts of 4-pixel chunks
   const int RG = (nS + kRG - 1) / kRG;
   const int nchunk = wpad / 4;
@@ -376,7 +364,6 @@ fused_small_kernel(const FusedParams p, const __grid_constant__ CUtensorMap tmX,
     if (tid == 0) {  // arm this step's receive barriers
       ptx::mbar_arrive_expect_tx(bar_P, bytesP);
       ptx::mbar_arrive_expect_tx(bar_D, bytesD);
-      if (rank != 0 && s > 0) ptx::mbar_arrive_expect_tx(bar_S, (uint32_t)(nsmp * 4));
     }
     cp_async_wait0();
     if (!TC && p.aligned) ptx::mbar_wait(&bar_x[buf], (uint32_t)((s >> 1) & 1));
@@ -461,10 +448,6 @@ fused_small_kernel(const FusedParams p, const __grid_constant__ CUtensorMap tmX,
         }
         *d = v;
       }
-    }
-    if (rank != 0 && s > 0) {  // rank 0's reduced W2/b block of step s-1 (pushed at its P9)
-      ptx::mbar_wait(bar_S, (uint32_t)((s - 1) & 1));
-      apply_small();
     }
     ptx::fence_proxy_async_smem();
     __syncthreads();
@@ -558,19 +541,20 @@ fused_small_kernel(const FusedParams p, const __grid_constant__ CUtensorMap tmX,
         const int j = t - O * H;
 #pragma unroll 8
         for (int q = 0; q < nOwn; ++q) v += D1[(o0 + q) * 32 + j];
-      } else if (t < nsm - 1) {
+      } else if (t < nsm) {
         const int o = t - O * H - H;
 #pragma unroll 8
         for (int q = 0; q < nOwn; ++q) v += D2own[q * 32 + o];
-      } else if (t == nsm - 1) {  // this CTA's cost partial sum (a - y)^2 (P3's per-warp sums)
-        for (int w2 = 0; w2 < kWarps; ++w2) v += lsum[w2];
       }
       gpart[t] = v;
     }
     ptx::fence_proxy_async_smem();
     __syncthreads();
-    if (rank != 0 && tid == 0)  // the whole block to rank 0, which reduces it for the cluster
-      ptx::bulk_s2peer(grecv + rank * nsmp, gpart, (uint32_t)(nsmp * 4), bar_D, 0);
+    if (warp == 0 && lane < C && lane != rank) {
+      const int c = lane;
+      const int ce0 = e_begin(c, C, nsmp), cne = e_begin(c + 1, C, nsmp) - ce0;
+      if (cne > 0) ptx::bulk_s2peer(grecv + rank * eslot, gpart + ce0, (uint32_t)(cne * 4), bar_D, c);
+    }
     if (TC) ptx::mbar_wait(bar_D, par);  // (the SIMT P5 starts on its own rows and waits inside)
     PROF(5);
 
@@ -666,15 +650,14 @@ fused_small_kernel(const FusedParams p, const __grid_constant__ CUtensorMap tmX,
     }
     ptx::mbar_wait(bar_D, par);  // threads without a P5 task
     }  // !TC
-    // rank 0: the cluster's W2/b1/b2 tendencies + cost, its peers' blocks summed in rank order;
-    // the sum goes to L2 with the dW1 slice in P6 as one more bulk reduction
-    if (rank == 0) {
-      for (int e = tid; e < nsmp; e += kThreads) {
-        float v = gpart[e];
-        for (int c = 1; c < C; ++c) v += grecv[c * nsmp + e];
-        if (p.aligned) gpart[e] = v;
-        else if (e < nsm) ptx::red_add_f32(accS + p.small_off + e, v);
-      }
+    // reduce my slice of the W2/b1/b2 tendencies over the cluster (rank order); the sum goes
+    // to L2 with the dW1 slice in P6 as one more bulk reduction (aligned path: the slice is
+    // 16-B aligned, e_begin), in place of gpart's own slice (never pushed to a peer)
+    for (int e = tid; e < ne; e += kThreads) {
+      float v = 0.0f;
+      for (int c = 0; c < C; ++c) v += (c == rank) ? gpart[e0 + e] : grecv[c * eslot + e];
+      if (p.aligned) gpart[e0 + e] = v;
+      else ptx::red_add_f32(accS + p.small_off + e0 + e, v);
     }
     ptx::fence_proxy_async_smem();
     __syncthreads();
@@ -685,7 +668,7 @@ fused_small_kernel(const FusedParams p, const __grid_constant__ CUtensorMap tmX,
       if (tid == 0) {
         ptx::fence_proxy_async_global();
         ptx::bulk_reduce_add_f32(accS + slice_off, Gs, (uint32_t)(p.ws * 32 * 4));
-        if (rank == 0) ptx::bulk_reduce_add_f32(accS + p.small_off, gpart, (uint32_t)(nsmp * 4));
+        if (ne > 0) ptx::bulk_reduce_add_f32(accS + p.small_off + e0, gpart + e0, (uint32_t)(ne * 4));
         ptx::bulk_commit();
         ptx::bulk_wait_all();
         ptx::fence_proxy_async_global();
@@ -696,28 +679,31 @@ fused_small_kernel(const FusedParams p, const __grid_constant__ CUtensorMap tmX,
     }
     PROF(7);
 
-    // ---- P7. this rank's group barrier (the G CTAs co_summing pixel slice `rank`): its slice of
-    //      the step's co_sum is complete.  Between arrive and wait, zero this CTA's share of the
-    //      group's regions of the slot used two steps ahead (its last readers -- this group --
-    //      finished before the previous barrier; its next writers start after the next one).
+    // ---- P7. grid barrier: the co_sum of this step is complete.  Between arrive and wait,
+    //      zero this CTA's share of the slot used two steps ahead (its last readers finished
+    //      before the previous barrier; its next writers start after the next one).
     __syncthreads();
-    if (tid == 0) ptx::grid_arrive(bar_rank);
+    if (tid == 0) {
+      // step s's cost entry is zeroed by CTA 0 before its arrival; every CTA adds its partial
+      // after the barrier, i.e. after that zero (release / acquire through the counter)
+      if (blockIdx.x == 0 && p.step_loss) p.step_loss[s] = 0.0f;
+      ptx::grid_arrive(p.bar);
+    }
     {
       float *z = p.acc + ((p.slot0 + s + 2) % kSlots) * p.slot;
-      const int64_t len = (int64_t)p.ws * 32;
-      const int64_t z0 = len * g / p.G, z1 = len * (g + 1) / p.G;
-      for (int64_t i = z0 + tid; i < z1; i += kThreads) z[slice_off + i] = 0.0f;
-      if (rank == 0)
-        for (int i = tid; i < nsmp; i += kThreads)
-          if (i % p.G == g) z[p.small_off + i] = 0.0f;
+      for (int64_t i = (int64_t)blockIdx.x * kThreads + tid; i < p.slot; i += (int64_t)nCTA * kThreads) z[i] = 0.0f;
     }
     if (TC && s + 1 < p.n_steps) {  // next step's K-layout tile: TF32 split while the barrier fills
       ptx::mbar_wait(&bar_x[0], (uint32_t)((s + 1) & 1));
       tc_split(X, X + kTcXLoK, 4 * kTcAS, tid);
       ptx::fence_proxy_async_smem();
     }
-    if (tid == 0) grid_wait_from(bar_rank, p.bar_base + (unsigned)((s + 1) * p.G));
+    if (tid == 0) grid_wait_from(p.bar, p.bar_base + (unsigned)((s + 1) * nCTA));
     __syncthreads();
+    if (warp == 1 && p.step_loss) {  // this CTA's cost partial (lsum is rewritten in P3)
+      const float l = warp_sum(lane < kWarps ? lsum[lane] : 0.0f);
+      if (lane == 0) ptx::red_add_f32(p.step_loss + s, 0.5f * l * p.inv_B);
+    }
     PROF(8);
 
     // ---- P8. read the reduced slice and the W2/b block back
@@ -726,13 +712,12 @@ fused_small_kernel(const FusedParams p, const __grid_constant__ CUtensorMap tmX,
         ptx::fence_proxy_async_global();
         ptx::mbar_arrive_expect_tx(bar_G, bytesG);
         ptx::bulk_g2s(Gr, accS + slice_off, (uint32_t)(p.ws * 32 * 4), bar_G);
-        if (rank == 0) ptx::bulk_g2s(gsm, accS + p.small_off, (uint32_t)(nsmp * 4), bar_G);
+        ptx::bulk_g2s(gsm, accS + p.small_off, (uint32_t)(nsmp * 4), bar_G);
       }
       ptx::mbar_wait(bar_G, par);
     } else {
       for (int i = tid; i < w * 32; i += kThreads) Gr[i] = accS[slice_off + i];
-      if (rank == 0)
-        for (int i = tid; i < nsmp; i += kThreads) gsm[i] = accS[p.small_off + i];
+      for (int i = tid; i < nsmp; i += kThreads) gsm[i] = accS[p.small_off + i];
       __syncthreads();
     }
     PROF(9);
@@ -759,11 +744,11 @@ fused_small_kernel(const FusedParams p, const __grid_constant__ CUtensorMap tmX,
         reinterpret_cast<float4 *>(W1t)[i] = wv;   // pad neurons j >= H: G = 0, W stays 0
       }
     }
-    if (rank == 0) {
-      apply_small();
-      if (g == 0 && tid == 0 && p.step_loss) p.step_loss[s] = 0.5f * gsm[nsm - 1] * p.inv_B;
-      if (s + 1 < p.n_steps && warp == 0 && lane >= 1 && lane < C)  // the reduced block to the peers
-        ptx::bulk_s2peer(gsm, gsm, (uint32_t)(nsmp * 4), bar_S, lane);
+    for (int e = tid; e < nsm; e += kThreads) {
+      const float gv = p.scale * gsm[e];
+      if (e < O * H) { const int o = e / H; W2s[o * 33 + (e - o * H)] -= gv; }
+      else if (e < O * H + H) b1s[e - O * H] -= gv;
+      else b2s[e - O * H - H] -= gv;
     }
     __syncthreads();
     PROF(10);
@@ -865,7 +850,7 @@ int fused_small_train_steps(FusedSmall &fs, cudaStream_t st, const std::vector<i
   auto smem_for = [&](int G) {
     const int nSmax = (int)((batch + G - 1) / G);
     const int nOwnMax = (nSmax + C - 1) / C;
-    return (size_t)smem_layout(wpad, nSmax, nOwnMax, C, tc && nSmax <= kTcRows, (O * H + H + O + 1 + 3) & ~3).total * sizeof(float) +
+    return (size_t)smem_layout(wpad, nSmax, nOwnMax, C, tc && nSmax <= kTcRows).total * sizeof(float) +
            (tc ? 1024 : 0);
   };
   // clusters: as many as co-reside at 1 CTA/SM, with <= kMaxRows rows per cluster
@@ -937,10 +922,10 @@ int fused_small_train_steps(FusedSmall &fs, cudaStream_t st, const std::vector<i
   const int nCTA = G * C;
 
   // accumulator slot: [C][ws][32] dW1 slices (k-major), then the W2/b1/b2 block (16-B aligned)
-  const int nsmp = (O * H + H + O + 1 + 3) & ~3;  // + the step's cost
+  const int nsmp = (O * H + H + O + 3) & ~3;
   const int64_t small_off = (int64_t)C * ws * 32;
   const int64_t slot = (small_off + nsmp + 31) & ~int64_t(31);
-  const size_t need = kSlots * slot * sizeof(float) + kMaxC * kBarStride * sizeof(unsigned);
+  const size_t need = kSlots * slot * sizeof(float) + 256;
   if (fs.ws_bytes < need) {
     if (fs.ws) cudaFree(fs.ws);
     fs.ws = nullptr;
@@ -1000,7 +985,7 @@ int fused_small_train_steps(FusedSmall &fs, cudaStream_t st, const std::vector<i
 
   cudaError_t e = cudaSuccess;
   if (!fs.ws_ready) {  // a fresh ring: all slots zero, counter 0
-    e = cudaMemsetAsync(base, 0, need, st);
+    e = cudaMemsetAsync(base, 0, kSlots * slot * sizeof(float) + 256, st);
     fs.steps_done = 0;
     fs.bar_base = 0;
     fs.ring_key[0] = slot;
@@ -1063,7 +1048,7 @@ int fused_small_train_steps(FusedSmall &fs, cudaStream_t st, const std::vector<i
   if (e == cudaSuccess) {
     fs.ws_ready = true;
     fs.steps_done += (uint64_t)n_steps;
-    fs.bar_base += (unsigned)(n_steps * G);  // every rank's counter: G arrivals per step
+    fs.bar_base += (unsigned)(n_steps * nCTA);
   } else {
     fs.ws_ready = false;
   }
