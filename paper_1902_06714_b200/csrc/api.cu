@@ -11,6 +11,7 @@
 #include <vector>
 
 #include "../../include/nf.h"
+#include "deep_mk.cuh"
 #include "fp64.cuh"
 #include "fused_small.cuh"
 #include "infer_small.cuh"
@@ -137,6 +138,7 @@ struct nf_net {
   DevBuf stage_x, stage_y, stage_o, stage_g;  // host-pointer staging
   DevBuf d_starts;
   FusedSmall fused;                      // persistent small-net kernel state
+  DeepMK deep;                           // deep narrow-net task megakernel state (deep_mk.cu)
   // CUDA graph of the generic multi-step sequence (nf_train_steps): replayed when a call
   // repeats the same arguments, rebuilt otherwise
   cudaGraphExec_t graph = nullptr;
@@ -686,6 +688,7 @@ void nf_net_destroy(nf_net *net) {
   net->stage_g.release();
   net->d_starts.release();
   fused_small_release(net->fused);
+  deep_mk_release(net->deep);
   drop_graph(net);
   if (net->cap_stream) cudaStreamDestroy(net->cap_stream);
   for (auto e : net->h2d_ev) if (e) cudaEventDestroy(e);
@@ -844,6 +847,20 @@ static int train_steps_device(nf_net *net, const float *dX, const float *dY, int
     }
     if (src != SINGLE_NOT_APPLICABLE)
       return fail(NF_ECUDA, "single-CTA kernel: %s", cudaGetErrorString((cudaError_t)src));
+  }
+  // Deep nets of narrow hidden layers in TF32 (config 4): all steps in one task-megakernel launch
+  static const bool det = getenv("NF_SPLITK_DETERMINISTIC") != nullptr;
+  if (!det && deep_mk_applicable(net->dims, net->math, batch)) {
+    int rc2;
+    if ((rc2 = ensure_ws(net, batch))) return rc2;
+    if ((rc2 = ensure_shadow(net))) return rc2;
+    rc2 = deep_mk_train_steps(net->deep, net->stream, net->dims, net->acts, net->params, net->params_t, net->offW,
+                              net->offB, net->A, net->S, dX, dY, dN, batch, st.data(), n_steps, eta, step_loss);
+    if (rc2 == 0) {
+      fused_small_invalidate(net->fused);
+      return NF_OK;  // (the kernel leaves the TF32 shadow current)
+    }
+    if (rc2 != DEEP_NOT_APPLICABLE) return fail(NF_ECUDA, "deep-net megakernel: %s", deep_mk_error());
   }
   int rc = net->math == NF_MATH_FP64 ? FUSED_NOT_APPLICABLE : fused_small_train_steps(net->fused, net->stream, net->dims, net->act_h, net->act_o,
                                    net->params, dX, dY, dN, batch, st.data(), n_steps, eta, step_loss);
