@@ -850,6 +850,9 @@ static int train_steps_device(nf_net *net, const float *dX, const float *dY, int
   }
   // Deep nets of narrow hidden layers in TF32 (config 4): all steps in one task-megakernel launch
   static const bool det = getenv("NF_SPLITK_DETERMINISTIC") != nullptr;
+  if (getenv("NF_TRACE_HOST"))
+    fprintf(stderr, "[route] det=%d math=%d batch=%lld deep=%d\n", (int)det, net->math, (long long)batch,
+            (int)deep_mk_applicable(net->dims, net->math, batch));
   if (!det && deep_mk_applicable(net->dims, net->math, batch)) {
     int rc2;
     if ((rc2 = ensure_ws(net, batch))) return rc2;

@@ -46,6 +46,8 @@ constexpr int kThreads = 192;               // producer, MMA, 4 epilogue warps
 constexpr int kMaxL = 16;
 constexpr int A_BYTES = BM * BK * 4, B_BYTES = BN * BK * 4, STAGE_BYTES = A_BYTES + B_BYTES;
 constexpr int kNOut = 16;                   // max output width (OUT tasks)
+constexpr int BMO = 32;                     // rows per OUT task (4 per 128-row block)
+constexpr int kOutPer = BM / BMO;
 constexpr int kMaxH = 256;                  // max hidden width
 constexpr int kMapsPerLayer = 6;            // fwd A, fwd W, bwd D, bwd W (MN), grad D (MN), grad A (MN)
 enum : int { T_FWD = 0, T_OUT = 1, T_BWD = 2, T_GRAD = 3, T_GFIN = 4, T_ROUND = 5 };
@@ -68,7 +70,15 @@ struct Params {
   float *step_loss;
   float scale, inv_B;
   int64_t n_steps;
+  unsigned long long *prof;                 // NF_DMK_PROF=1: [grid][prof_cap][4] globaltimer stamps
+  int prof_cap;
 };
+
+__device__ __forceinline__ unsigned long long gtime() {
+  unsigned long long t;
+  asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+  return t;
+}
 
 // counter layout (uints): fwd[l][mb], dlt[l][mb], grad[l], bwdall[l], oall, step
 __device__ __forceinline__ unsigned *c_fwd(const Params &p, int l, int mb) { return p.ctr + l * p.nrb + mb; }
@@ -136,6 +146,7 @@ __global__ void __launch_bounds__(kThreads, 1) deep_mk_kernel(const __grid_const
   uint32_t it = 0;       // K-blocks issued by this CTA (ring position, across tasks)
   uint32_t ntc = 0;      // TC tasks run by this CTA (accumulator barrier parity)
   const int T = p.T;
+  int np = 0;  // profiled tasks of this CTA
   for (int64_t s = 0; s < p.n_steps; ++s) {
     const int64_t start = p.starts[s];
     const unsigned tgt = (unsigned)(s + 1);
@@ -143,26 +154,29 @@ __global__ void __launch_bounds__(kThreads, 1) deep_mk_kernel(const __grid_const
       const int4 tk = p.tasks[t];
       const int type = tk.x & 0xff, l = tk.x >> 8;
       // ---- dependencies (one thread spins, then the CTA goes)
+      unsigned long long t0 = 0, t1 = 0;
       if (tid == 0) {
+        if (p.prof) t0 = gtime();
         if (type == T_FWD) {
           if (l == 1) { if (s > 0) wait_ge(c_step(p), (unsigned)(s * T)); }
           else wait_ge(c_fwd(p, l - 1, tk.y), tgt * tn_of(p.dims[l - 1]));
-        } else if (type == T_OUT) {
-          wait_ge(c_fwd(p, L - 1, tk.y), tgt * tn_of(p.dims[L - 1]));
+        } else if (type == T_OUT) {  // rows [y*32, y*32+32) of A_{L-1}
+          wait_ge(c_fwd(p, L - 1, tk.y / kOutPer), tgt * tn_of(p.dims[L - 1]));
         } else if (type == T_BWD) {  // delta_l of row block y
-          wait_ge(c_dlt(p, l, tk.y), tgt * (l == L - 1 ? 1u : (unsigned)tn_of(p.dims[l])));
+          wait_ge(c_dlt(p, l, tk.y), tgt * (l == L - 1 ? (unsigned)kOutPer : (unsigned)tn_of(p.dims[l])));
         } else if (type == T_GRAD) {  // delta_l of every row block of chunk y
-          const unsigned per = l == L - 1 ? 1u : (unsigned)tn_of(p.dims[l]);
+          const unsigned per = l == L - 1 ? (unsigned)kOutPer : (unsigned)tn_of(p.dims[l]);
           const int rb0 = tk.y * p.kc / BM, rb1 = min(p.nrb, (tk.y + 1) * p.kc / BM);
           for (int mb = rb0; mb < rb1; ++mb) wait_ge(c_dlt(p, l, mb), tgt * per);
         } else if (type == T_GFIN) {
-          wait_ge(c_oall(p), tgt * (unsigned)p.nrb);
+          wait_ge(c_oall(p), tgt * (unsigned)(p.nrb * kOutPer));
         } else {  // ROUND(l): every GRAD(l) and BWD(l) of this step
           const int tm = cdiv(p.dims[l], BM), tnk = tn_of(p.dims[l - 1]);
           wait_ge(c_grad(p, l), tgt * (unsigned)(p.nchunk * tm * tnk));
           if (l >= 2) wait_ge(c_bwdall(p, l), tgt * (unsigned)(p.nrb * tn_of(p.dims[l - 1])));
         }
         ptx::fence_proxy_async_global();  // the producers' generic writes -> this CTA's TMA reads
+        if (p.prof) t1 = gtime();
       }
       __syncthreads();
 
@@ -190,6 +204,8 @@ __global__ void __launch_bounds__(kThreads, 1) deep_mk_kernel(const __grid_const
         const int krow0 = (type == T_GRAD && l == 1) ? (int)start : 0;  // x rows of the batch
         if (warp == 0) {
           if (lane == 0) {
+            ptx::prefetch_tensormap(mA);
+            ptx::prefetch_tensormap(mB);
             for (int kb = 0; kb < nkb; ++kb, ++it) {
               const int st = it % kStages;
               if (it >= kStages) ptx::mbar_wait(&empty[st], ((it / kStages) - 1) & 1);
@@ -254,6 +270,11 @@ __global__ void __launch_bounds__(kThreads, 1) deep_mk_kernel(const __grid_const
             float *Arow = p.A[l] + (int64_t)m * N, *Srow = p.S[l] + (int64_t)m * N;
             const int kind = p.act[l];
 #pragma unroll
+            for (int j = 0; j < 64; j += 4) {  // every bias load in flight before any store
+              const float4 b4 = __ldcg(reinterpret_cast<const float4 *>(bias + n0 + j));
+              v[j] += b4.x; v[j + 1] += b4.y; v[j + 2] += b4.z; v[j + 3] += b4.w;
+            }
+#pragma unroll
             for (int j = 0; j < 64; j += 4) {
               if (n0 + j < N) {  // N is a multiple of 64: whole float4s
                 float4 av, sv;
@@ -261,7 +282,7 @@ __global__ void __launch_bounds__(kThreads, 1) deep_mk_kernel(const __grid_const
 #pragma unroll
                 for (int u = 0; u < 4; ++u) {
                   float a_, s_;
-                  act_fwd(kind, v[j + u] + __ldcg(bias + n0 + j + u), a_, s_);
+                  act_fwd(kind, v[j + u], a_, s_);
                   pa[u] = tf32_rn(a_);
                   ps[u] = s_;
                 }
@@ -272,16 +293,28 @@ __global__ void __launch_bounds__(kThreads, 1) deep_mk_kernel(const __grid_const
           } else if (type == T_BWD) {  // delta_{l-1} = acc .* sigma'(Z_{l-1}), in place of S_{l-1}
             const int N = p.dims[l - 1], n0 = tk.z * BN, m = tk.y * BM + r;
             float *Srow = p.S[l - 1] + (int64_t)m * N;
+            float *cs = reinterpret_cast<float *>(smem);  // [BM][65] block of deltas (the idle ring)
+            float4 s4[16];  // every sigma' load in flight before any store (N is a multiple of 64)
+#pragma unroll
+            for (int j = 0; j < 16; ++j) s4[j] = __ldcg(reinterpret_cast<const float4 *>(Srow + n0) + j);
 #pragma unroll
             for (int j = 0; j < 64; j += 4) {
               if (n0 + j < N) {
-                float4 sv = __ldcg(reinterpret_cast<const float4 *>(Srow + n0 + j));
-                sv.x = tf32_rn(v[j] * sv.x);
-                sv.y = tf32_rn(v[j + 1] * sv.y);
-                sv.z = tf32_rn(v[j + 2] * sv.z);
-                sv.w = tf32_rn(v[j + 3] * sv.w);
-                *reinterpret_cast<float4 *>(Srow + n0 + j) = sv;
+                const float4 sv = s4[j / 4];
+                const float d0 = v[j] * sv.x, d1 = v[j + 1] * sv.y, d2 = v[j + 2] * sv.z, d3 = v[j + 3] * sv.w;
+                cs[r * 65 + j] = d0; cs[r * 65 + j + 1] = d1; cs[r * 65 + j + 2] = d2; cs[r * 65 + j + 3] = d3;
+                *reinterpret_cast<float4 *>(Srow + n0 + j) = make_float4(tf32_rn(d0), tf32_rn(d1), tf32_rn(d2), tf32_rn(d3));
               }
+            }
+            // the block's share of the bias update of layer l-1: b -= (eta/B) sum_rows delta
+            asm volatile("bar.sync 1, 128;" ::: "memory");
+            if (r < 64 && n0 + r < N) {
+              float s0 = 0.f, s1 = 0.f, s2 = 0.f, s3 = 0.f;
+#pragma unroll 8
+              for (int i = 0; i < BM; i += 4) {
+                s0 += cs[i * 65 + r]; s1 += cs[(i + 1) * 65 + r]; s2 += cs[(i + 2) * 65 + r]; s3 += cs[(i + 3) * 65 + r];
+              }
+              ptx::red_add_f32(p.params + p.offB[l - 1] + n0 + r, -p.scale * ((s0 + s1) + (s2 + s3)));
             }
           } else {  // GRAD: W_l[m][n] -= scale * acc (one term per chunk, L2 reductions)
             const int M = p.dims[l], N = p.dims[l - 1];
@@ -298,91 +331,115 @@ __global__ void __launch_bounds__(kThreads, 1) deep_mk_kernel(const __grid_const
                 for (int j = 0; j < 64; ++j)
                   if (n0 + j < N) ptx::red_add_f32(Wrow + n0 + j, sc * v[j]);
               }
-              if (tk.w == 0) {  // the chunk's bias tendency of neuron m: sum_b delta_l[b][m]
-                const float *D = p.S[l] + (int64_t)(tk.y * p.kc) * M + m;
-                const int rows = min(p.kc, p.B - tk.y * p.kc);
-                float s0 = 0.f, s1 = 0.f, s2 = 0.f, s3 = 0.f;
-                int b = 0;
-                for (; b + 4 <= rows; b += 4) {
-                  s0 += __ldcg(D + (int64_t)b * M); s1 += __ldcg(D + (int64_t)(b + 1) * M);
-                  s2 += __ldcg(D + (int64_t)(b + 2) * M); s3 += __ldcg(D + (int64_t)(b + 3) * M);
-                }
-                for (; b < rows; ++b) s0 += __ldcg(D + (int64_t)b * M);
-                ptx::red_add_f32(p.params + p.offB[l] + m, sc * ((s0 + s1) + (s2 + s3)));
-              }
             }
           }
         }
         ++ntc;
       } else if (type == T_OUT) {
-        // ---- the narrow output layer for rows [mb*128, mb*128 + 128) (SIMT, one warp per row)
-        const int mb = tk.y;
+        // ---- the narrow output layer for rows [y*32, y*32 + 32) (SIMT): warp w owns rows w, w+6,
+        //      ...; each warp loads all its rows' A_{L-1}, S_{L-1} and y values before computing
+        //      (every global access of the task is one round trip in flight, not one per row)
+        const int r0 = tk.y * BMO;
         const float *WL = p.params + p.offW[L], *bL = p.params + p.offB[L];
         for (int i = tid; i < nL * H; i += kThreads) sW[(i / H) * kMaxH + i % H] = __ldcg(WL + i);
-        __syncthreads();
         const float *AL1 = p.A[L - 1];
         float *SL1 = p.S[L - 1];
+        constexpr int kRW = (BMO + 5) / 6;  // rows per warp (6 warps)
+        constexpr int kC = kMaxH / 32;      // columns per lane
+        float av[kRW][kC], sv[kRW][kC], yv[kRW];
+#pragma unroll
+        for (int q = 0; q < kRW; ++q) {
+          const int rr = warp + 6 * q;
+          const int64_t m = r0 + rr;
+          yv[q] = (rr < BMO && lane < nL) ? __ldg(p.Y + (start + m) * nL + lane) : 0.0f;
+#pragma unroll
+          for (int i = 0; i < kC; ++i) {
+            const bool ok = rr < BMO && lane + 32 * i < H;
+            av[q][i] = ok ? __ldcg(AL1 + m * H + lane + 32 * i) : 0.0f;
+            sv[q][i] = ok ? __ldcg(SL1 + m * H + lane + 32 * i) : 0.0f;
+          }
+        }
+        const float bl = lane < nL ? __ldcg(bL + lane) : 0.0f;
+        __syncthreads();  // sW
         float lacc = 0.0f;
-        for (int rr = warp; rr < BM; rr += kThreads / 32) {
-          const int m = mb * BM + rr;
-          const float *arow = AL1 + (int64_t)m * H;
-          float av[kMaxH / 32];
+        float bsum[kC];   // this lane's columns: sum over the warp's rows of delta_{L-1}
 #pragma unroll
-          for (int i = 0; i < kMaxH / 32; ++i) av[i] = (lane + 32 * i < H) ? __ldcg(arow + lane + 32 * i) : 0.0f;
-          float dl = 0.0f;  // lane o < nL: delta_L[m][o]
+        for (int i = 0; i < kC; ++i) bsum[i] = 0.0f;
 #pragma unroll
-          for (int o = 0; o < kNOut; ++o) {
-            if (o < nL) {
-              float zpart = 0.0f;
+        for (int q = 0; q < kRW; ++q) {
+          const int rr = warp + 6 * q;
+          if (rr < BMO) {  // warp-uniform
+            const int64_t m = r0 + rr;
+            float dl = 0.0f;  // lane o < nL: delta_L[m][o]
 #pragma unroll
-              for (int i = 0; i < kMaxH / 32; ++i) zpart = fmaf(av[i], sW[o * kMaxH + lane + 32 * i], zpart);
-              const float z = warp_sum(zpart) + __ldcg(bL + o);
-              if (lane == o) {
-                float a_, s_;
-                act_fwd(p.act[L], z, a_, s_);
-                const float y = p.Y[(start + m) * nL + o];
-                const float diff = a_ - y;
-                lacc = fmaf(diff, diff, lacc);
-                dl = diff * s_;
-                p.A[L][(int64_t)m * nL + o] = a_;
-                p.S[L][(int64_t)m * nL + o] = dl;
+            for (int o = 0; o < kNOut; ++o) {
+              if (o < nL) {
+                float zpart = 0.0f;
+#pragma unroll
+                for (int i = 0; i < kC; ++i) zpart = fmaf(av[q][i], sW[o * kMaxH + lane + 32 * i], zpart);
+                const float z = warp_sum(zpart);
+                if (lane == o) {
+                  float a_, s_;
+                  act_fwd(p.act[L], z + bl, a_, s_);
+                  const float diff = a_ - yv[q];
+                  lacc = fmaf(diff, diff, lacc);
+                  dl = diff * s_;
+                  p.A[L][m * nL + o] = a_;
+                  p.S[L][m * nL + o] = dl;
+                }
               }
             }
-          }
-          if (lane < kNOut) sD[rr * kNOut + lane] = lane < nL ? dl : 0.0f;
-          float d[kNOut];
+            if (lane < kNOut) sD[rr * kNOut + lane] = lane < nL ? dl : 0.0f;
+            float d[kNOut];
 #pragma unroll
-          for (int o = 0; o < kNOut; ++o) d[o] = __shfl_sync(0xffffffffu, dl, o);
-          float *srow = SL1 + (int64_t)m * H;
+            for (int o = 0; o < kNOut; ++o) d[o] = __shfl_sync(0xffffffffu, dl, o);
 #pragma unroll
-          for (int i = 0; i < kMaxH / 32; ++i) {
-            const int j = lane + 32 * i;
-            if (j < H) {
-              float acc = 0.0f;
+            for (int i = 0; i < kC; ++i) {
+              const int j = lane + 32 * i;
+              if (j < H) {
+                float acc = 0.0f;
 #pragma unroll
-              for (int o = 0; o < kNOut; ++o)
-                if (o < nL) acc = fmaf(d[o], sW[o * kMaxH + j], acc);
-              srow[j] = tf32_rn(acc * __ldcg(srow + j));  // delta_{L-1}: operand of BWD(L-1) / GRAD(L-1)
+                for (int o = 0; o < kNOut; ++o)
+                  if (o < nL) acc = fmaf(d[o], sW[o * kMaxH + j], acc);
+                const float dv = acc * sv[q][i];
+                bsum[i] += dv;
+                SL1[m * H + j] = tf32_rn(dv);  // delta_{L-1}: operand of BWD(L-1) / GRAD(L-1)
+              }
             }
           }
         }
         sred[tid] = warp_sum(lacc);
+        float *sb = sD + BMO * kNOut;  // [6 warps][kMaxH] per-warp bias sums
+#pragma unroll
+        for (int i = 0; i < kC; ++i) sb[warp * kMaxH + lane + 32 * i] = bsum[i];
         __syncthreads();
         if (tid == 0) {
           float l2 = 0.0f;
           for (int w = 0; w < kThreads / 32; ++w) l2 += sred[w * 32];
-          p.lpart[mb] = l2;
+          p.lpart[tk.y] = l2;
         }
-        // partial tendency of W_L (columns j < H) and b_L (column H) over the block's rows
-        float *pb = p.part + (int64_t)mb * nL * (H + 1);
+        for (int j = tid; j < H; j += kThreads) {  // b_{L-1} -= (eta/B) sum over the task's rows
+          float bsv = 0.0f;
+#pragma unroll
+          for (int w = 0; w < kThreads / 32; ++w) bsv += sb[w * kMaxH + j];
+          ptx::red_add_f32(p.params + p.offB[L - 1] + j, -p.scale * bsv);
+        }
+        // partial tendency of W_L (columns j < H) and b_L (column H) over the task's rows (the
+        // A_{L-1} rows are re-read from L2: 16 loads in flight per thread)
+        float *pb = p.part + (int64_t)tk.y * nL * (H + 1);
         for (int j = tid; j <= H; j += kThreads) {
           float g[kNOut];
 #pragma unroll
           for (int o = 0; o < kNOut; ++o) g[o] = 0.0f;
-          for (int rr = 0; rr < BM; ++rr) {
-            const float a = j < H ? __ldcg(AL1 + (int64_t)(mb * BM + rr) * H + j) : 1.0f;
 #pragma unroll
-            for (int o = 0; o < kNOut; ++o) g[o] = fmaf(sD[rr * kNOut + o], a, g[o]);
+          for (int q0 = 0; q0 < BMO; q0 += 16) {
+            float a[16];
+#pragma unroll
+            for (int u = 0; u < 16; ++u) a[u] = j < H ? __ldcg(AL1 + (int64_t)(r0 + q0 + u) * H + j) : 1.0f;
+#pragma unroll
+            for (int u = 0; u < 16; ++u)
+#pragma unroll
+              for (int o = 0; o < kNOut; ++o) g[o] = fmaf(sD[(q0 + u) * kNOut + o], a[u], g[o]);
           }
 #pragma unroll
           for (int o = 0; o < kNOut; ++o)
@@ -390,16 +447,27 @@ __global__ void __launch_bounds__(kThreads, 1) deep_mk_kernel(const __grid_const
         }
       } else if (type == T_GFIN) {
         // ---- W_L, b_L -= scale * (partials summed in row-block order); the step's mean cost
+        const int npart = p.nrb * kOutPer;
+        const int64_t pstride = (int64_t)nL * (H + 1);
         for (int e = tid; e < nL * (H + 1); e += kThreads) {
-          float g = 0.0f;
-          for (int mb = 0; mb < p.nrb; ++mb) g += __ldcg(p.part + (int64_t)mb * nL * (H + 1) + e);
           const int o = e / (H + 1), j = e % (H + 1);
           float *dst = j < H ? p.params + p.offW[L] + o * H + j : p.params + p.offB[L] + o;
-          *dst = __ldcg(dst) - p.scale * g;
+          const float w0 = __ldcg(dst);
+          float g = 0.0f;
+          int mb = 0;
+          for (; mb + 8 <= npart; mb += 8) {  // 8 loads in flight, summed in partial order
+            float t[8];
+#pragma unroll
+            for (int u = 0; u < 8; ++u) t[u] = __ldcg(p.part + (mb + u) * pstride + e);
+#pragma unroll
+            for (int u = 0; u < 8; ++u) g += t[u];
+          }
+          for (; mb < npart; ++mb) g += __ldcg(p.part + mb * pstride + e);
+          *dst = w0 - p.scale * g;
         }
         if (tid == 0 && p.step_loss) {
           float l2 = 0.0f;
-          for (int mb = 0; mb < p.nrb; ++mb) l2 += __ldcg(p.lpart + mb);
+          for (int mb = 0; mb < npart; ++mb) l2 += __ldcg(p.lpart + mb);
           p.step_loss[s] = 0.5f * l2 * p.inv_B;
         }
       } else {  // ROUND(l, q): slice q of W~_l = rn(W_l)
@@ -407,7 +475,15 @@ __global__ void __launch_bounds__(kThreads, 1) deep_mk_kernel(const __grid_const
         const int64_t i0 = n * tk.y / p.nq, i1 = n * (tk.y + 1) / p.nq;
         const float *src = p.params + p.offW[l];
         float *dst = p.params_t + p.offW[l];
-        for (int64_t i = i0 + tid; i < i1; i += kThreads) dst[i] = tf32_rn(__ldcg(src + i));
+        int64_t i = i0 + tid;
+        for (; i + 3 * kThreads < i1; i += 4 * kThreads) {  // 4 loads in flight per thread
+          float t[4];
+#pragma unroll
+          for (int u = 0; u < 4; ++u) t[u] = __ldcg(src + i + u * kThreads);
+#pragma unroll
+          for (int u = 0; u < 4; ++u) dst[i + u * kThreads] = tf32_rn(t[u]);
+        }
+        for (; i < i1; i += kThreads) dst[i] = tf32_rn(__ldcg(src + i));
       }
 
       // ---- completion: publish this task's writes, then count it (the proxy fence orders this
@@ -419,10 +495,15 @@ __global__ void __launch_bounds__(kThreads, 1) deep_mk_kernel(const __grid_const
       if (tid == 0) {
         ptx::fence_proxy_async_global();
         if (type == T_FWD) signal(c_fwd(p, l, tk.y));
-        else if (type == T_OUT) { signal(c_dlt(p, L - 1, tk.y)); signal(c_oall(p)); }
+        else if (type == T_OUT) { signal(c_dlt(p, L - 1, tk.y / kOutPer)); signal(c_oall(p)); }
         else if (type == T_BWD) { signal(c_dlt(p, l - 1, tk.y)); signal(c_bwdall(p, l)); }
         else if (type == T_GRAD) signal(c_grad(p, l));
         signal(c_step(p));
+        if (p.prof && np < p.prof_cap) {
+          unsigned long long *q = p.prof + ((int64_t)blockIdx.x * p.prof_cap + np) * 4;
+          q[0] = t0; q[1] = t1; q[2] = gtime(); q[3] = (unsigned long long)tk.x | ((unsigned long long)s << 32);
+        }
+        ++np;
       }
     }
   }
@@ -463,13 +544,13 @@ int deep_mk_train_steps(DeepMK &st, cudaStream_t stream, const std::vector<int> 
   int nchunk = std::max(1, std::min(nrb, 8));
   const int kc = cdiv(nrb, nchunk) * BM;
   nchunk = cdiv(B, kc);
-  const int nq = 8;  // ROUND slices per layer
+  const int nq = 16;  // ROUND slices per layer
   if (key != st.key) {
     std::vector<int4> tasks;
     for (int l = 1; l < L; ++l)
       for (int mb = 0; mb < nrb; ++mb)
         for (int nb = 0; nb < tn_of(dims[l]); ++nb) tasks.push_back(make_int4(T_FWD | (l << 8), mb, nb, 0));
-    for (int mb = 0; mb < nrb; ++mb) tasks.push_back(make_int4(T_OUT | (L << 8), mb, 0, 0));
+    for (int mb = 0; mb < nrb * kOutPer; ++mb) tasks.push_back(make_int4(T_OUT | (L << 8), mb, 0, 0));
     for (int l = L - 1; l >= 1; --l) {
       if (l >= 2)
         for (int mb = 0; mb < nrb; ++mb)
@@ -514,8 +595,8 @@ int deep_mk_train_steps(DeepMK &st, cudaStream_t stream, const std::vector<int> 
     st.off_maps = take(maps.size() * sizeof(CUtensorMap));
     st.off_tasks = take(tasks.size() * sizeof(int4));
     st.off_ctr = take(ctr_uints * 4);
-    st.off_part = take((size_t)nrb * nL * (H + 1) * 4);
-    st.off_lpart = take((size_t)nrb * 4);
+    st.off_part = take((size_t)nrb * kOutPer * nL * (H + 1) * 4);
+    st.off_lpart = take((size_t)nrb * kOutPer * 4);
     st.off_starts = o;
     st.ctr_bytes = ctr_uints * 4;
     const size_t need = o + std::max<int64_t>(1024, n_steps) * 8;
@@ -598,6 +679,15 @@ int deep_mk_train_steps(DeepMK &st, cudaStream_t stream, const std::vector<int> 
   p.scale = (float)((double)eta / (double)batch);
   p.inv_B = (float)(1.0 / (double)batch);
   p.n_steps = n_steps;
+  static const bool prof = getenv("NF_DMK_PROF") != nullptr;
+  static unsigned long long *prof_buf = nullptr;
+  const int prof_cap = 64;
+  if (prof) {
+    if (!prof_buf) cudaMalloc(&prof_buf, (size_t)148 * prof_cap * 4 * 8);
+    cudaMemsetAsync(prof_buf, 0, (size_t)148 * prof_cap * 4 * 8, stream);
+    p.prof = prof_buf;
+    p.prof_cap = prof_cap;
+  }
   if (e == cudaSuccess) {
     cudaLaunchConfig_t cfg = {};
     cudaLaunchAttribute at[1];
@@ -618,6 +708,29 @@ int deep_mk_train_steps(DeepMK &st, cudaStream_t stream, const std::vector<int> 
   if (e != cudaSuccess) {
     snprintf(g_dmk_err, sizeof g_dmk_err, "launch: %s", cudaGetErrorString(e));
     return -1;
+  }
+  if (prof) {  // per task type: mean dependency wait and run time (the first 64 tasks of each CTA)
+    std::vector<unsigned long long> h((size_t)st.grid * prof_cap * 4);
+    cudaStreamSynchronize(stream);
+    cudaMemcpy(h.data(), prof_buf, h.size() * 8, cudaMemcpyDeviceToHost);
+    const char *names[6] = {"FWD", "OUT", "BWD", "GRAD", "GFIN", "ROUND"};
+    double wait[6] = {0}, run[6] = {0};
+    int cnt[6] = {0};
+    unsigned long long tmin = ~0ull, tmax = 0;
+    for (size_t i = 0; i < h.size(); i += 4) {
+      if (!h[i]) continue;
+      const int ty = (int)(h[i + 3] & 0xff);
+      wait[ty] += (double)(h[i + 1] - h[i]);
+      run[ty] += (double)(h[i + 2] - h[i + 1]);
+      cnt[ty]++;
+      tmin = std::min(tmin, h[i]);
+      tmax = std::max(tmax, h[i + 2]);
+    }
+    fprintf(stderr, "[deep_mk prof] %d CTAs, span of the profiled tasks %.1f us\n", st.grid, (tmax - tmin) / 1e3);
+    for (int t = 0; t < 6; ++t)
+      if (cnt[t])
+        fprintf(stderr, "  %-6s %5d tasks  wait %7.2f us  run %7.2f us (mean)\n", names[t], cnt[t], wait[t] / cnt[t] / 1e3,
+                run[t] / cnt[t] / 1e3);
   }
   return 0;
 }
