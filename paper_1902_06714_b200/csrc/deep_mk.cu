@@ -255,6 +255,7 @@ __global__ void __launch_bounds__(kThreads, 1) deep_mk_kernel(const __grid_const
           const int q = warp & 3, r = 32 * q + lane;
           ptx::mbar_wait(accum, ntc & 1);
           tc::tc_fence_after();
+          if (p.prof && r == 0) sred[0] = __int_as_float((int)(gtime() & 0x7fffffff));
           float v[64];
           {
             float a[32], b[32];
@@ -416,7 +417,7 @@ __global__ void __launch_bounds__(kThreads, 1) deep_mk_kernel(const __grid_const
         if (tid == 0) {
           float l2 = 0.0f;
           for (int w = 0; w < kThreads / 32; ++w) l2 += sred[w * 32];
-          p.lpart[tk.y] = l2;
+          ptx::red_add_f32(p.lpart, l2);  // the step's cost sum (GFIN reads and re-zeroes it)
         }
         for (int j = tid; j < H; j += kThreads) {  // b_{L-1} -= (eta/B) sum over the task's rows
           float bsv = 0.0f;
@@ -424,9 +425,10 @@ __global__ void __launch_bounds__(kThreads, 1) deep_mk_kernel(const __grid_const
           for (int w = 0; w < kThreads / 32; ++w) bsv += sb[w * kMaxH + j];
           ptx::red_add_f32(p.params + p.offB[L - 1] + j, -p.scale * bsv);
         }
-        // partial tendency of W_L (columns j < H) and b_L (column H) over the task's rows (the
-        // A_{L-1} rows are re-read from L2: 16 loads in flight per thread)
-        float *pb = p.part + (int64_t)tk.y * nL * (H + 1);
+        // tendency of W_L (columns j < H) and b_L (column H) over the task's rows, added into the
+        // step's accumulator (applied by GFIN after every OUT task, so that all of them read the
+        // pre-step W_L); the A_{L-1} rows are re-read from L2, 16 loads in flight per thread
+        float *pb = p.part;
         for (int j = tid; j <= H; j += kThreads) {
           float g[kNOut];
 #pragma unroll
@@ -443,32 +445,24 @@ __global__ void __launch_bounds__(kThreads, 1) deep_mk_kernel(const __grid_const
           }
 #pragma unroll
           for (int o = 0; o < kNOut; ++o)
-            if (o < nL) pb[o * (H + 1) + j] = g[o];
+            if (o < nL) ptx::red_add_f32(pb + o * (H + 1) + j, g[o]);
         }
       } else if (type == T_GFIN) {
         // ---- W_L, b_L -= scale * (partials summed in row-block order); the step's mean cost
-        const int npart = p.nrb * kOutPer;
-        const int64_t pstride = (int64_t)nL * (H + 1);
-        for (int e = tid; e < nL * (H + 1); e += kThreads) {
+        // slice y of nq: W_L, b_L -= scale * accumulated tendency, accumulator re-zeroed; slice 0
+        // also writes the step's mean cost
+        const int ne = nL * (H + 1);
+        const int e0 = ne * tk.y / p.nq, e1 = ne * (tk.y + 1) / p.nq;
+        for (int e = e0 + tid; e < e1; e += kThreads) {
           const int o = e / (H + 1), j = e % (H + 1);
           float *dst = j < H ? p.params + p.offW[L] + o * H + j : p.params + p.offB[L] + o;
-          const float w0 = __ldcg(dst);
-          float g = 0.0f;
-          int mb = 0;
-          for (; mb + 8 <= npart; mb += 8) {  // 8 loads in flight, summed in partial order
-            float t[8];
-#pragma unroll
-            for (int u = 0; u < 8; ++u) t[u] = __ldcg(p.part + (mb + u) * pstride + e);
-#pragma unroll
-            for (int u = 0; u < 8; ++u) g += t[u];
-          }
-          for (; mb < npart; ++mb) g += __ldcg(p.part + mb * pstride + e);
+          const float g = __ldcg(p.part + e), w0 = __ldcg(dst);
           *dst = w0 - p.scale * g;
+          p.part[e] = 0.0f;
         }
-        if (tid == 0 && p.step_loss) {
-          float l2 = 0.0f;
-          for (int mb = 0; mb < npart; ++mb) l2 += __ldcg(p.lpart + mb);
-          p.step_loss[s] = 0.5f * l2 * p.inv_B;
+        if (tk.y == 0 && tid == 0) {
+          if (p.step_loss) p.step_loss[s] = 0.5f * __ldcg(p.lpart) * p.inv_B;
+          p.lpart[0] = 0.0f;
         }
       } else {  // ROUND(l, q): slice q of W~_l = rn(W_l)
         const int64_t n = (int64_t)p.dims[l] * p.dims[l - 1];
@@ -501,7 +495,11 @@ __global__ void __launch_bounds__(kThreads, 1) deep_mk_kernel(const __grid_const
         signal(c_step(p));
         if (p.prof && np < p.prof_cap) {
           unsigned long long *q = p.prof + ((int64_t)blockIdx.x * p.prof_cap + np) * 4;
-          q[0] = t0; q[1] = t1; q[2] = gtime(); q[3] = (unsigned long long)tk.x | ((unsigned long long)s << 32);
+          const unsigned long long te = gtime();
+          // word 3: task word | accumulator-ready time (low 31 bits of globaltimer) << 32 (TC tasks)
+          const unsigned long long ta = (type == T_FWD || type == T_BWD || type == T_GRAD)
+                                            ? (unsigned long long)(unsigned)__float_as_int(sred[0]) : 0ull;
+          q[0] = t0; q[1] = t1; q[2] = te; q[3] = (unsigned long long)(tk.x & 0xffff) | (ta << 32);
         }
         ++np;
       }
@@ -559,7 +557,7 @@ int deep_mk_train_steps(DeepMK &st, cudaStream_t stream, const std::vector<int> 
         for (int mt = 0; mt < cdiv(dims[l], BM); ++mt)
           for (int nt = 0; nt < tn_of(dims[l - 1]); ++nt) tasks.push_back(make_int4(T_GRAD | (l << 8), c, mt, nt));
     }
-    tasks.push_back(make_int4(T_GFIN | (L << 8), 0, 0, 0));
+    for (int q = 0; q < nq; ++q) tasks.push_back(make_int4(T_GFIN | (L << 8), q, 0, 0));
     for (int l = 1; l < L; ++l)
       for (int q = 0; q < nq; ++q) tasks.push_back(make_int4(T_ROUND | (l << 8), q, 0, 0));
     const int T = (int)tasks.size();
@@ -595,8 +593,8 @@ int deep_mk_train_steps(DeepMK &st, cudaStream_t stream, const std::vector<int> 
     st.off_maps = take(maps.size() * sizeof(CUtensorMap));
     st.off_tasks = take(tasks.size() * sizeof(int4));
     st.off_ctr = take(ctr_uints * 4);
-    st.off_part = take((size_t)nrb * kOutPer * nL * (H + 1) * 4);
-    st.off_lpart = take((size_t)nrb * kOutPer * 4);
+    st.off_part = take((size_t)nL * (H + 1) * 4);
+    st.off_lpart = take(64);
     st.off_starts = o;
     st.ctr_bytes = ctr_uints * 4;
     const size_t need = o + std::max<int64_t>(1024, n_steps) * 8;
@@ -656,7 +654,8 @@ int deep_mk_train_steps(DeepMK &st, cudaStream_t stream, const std::vector<int> 
     e = cudaMemcpyAsync(d + st.off_starts, st.h_starts, (size_t)n_steps * 8, cudaMemcpyHostToDevice, stream);
   }
   if (e == cudaSuccess) e = cudaEventRecord(st.h_ev, stream);
-  if (e == cudaSuccess) e = cudaMemsetAsync(d + st.off_ctr, 0, st.ctr_bytes, stream);
+  if (e == cudaSuccess) e = cudaMemsetAsync(d + st.off_ctr, 0, st.off_starts - st.off_ctr, stream);  // counters,
+                                                                    // output-layer accumulators
   Params p{};
   p.L = L; p.B = B; p.nrb = nrb; p.kc = kc; p.nchunk = nchunk; p.nq = nq; p.T = st.tasks_per_step;
   for (int l = 0; l <= L; ++l) {
@@ -714,7 +713,7 @@ int deep_mk_train_steps(DeepMK &st, cudaStream_t stream, const std::vector<int> 
     cudaStreamSynchronize(stream);
     cudaMemcpy(h.data(), prof_buf, h.size() * 8, cudaMemcpyDeviceToHost);
     const char *names[6] = {"FWD", "OUT", "BWD", "GRAD", "GFIN", "ROUND"};
-    double wait[6] = {0}, run[6] = {0};
+    double wait[6] = {0}, run[6] = {0}, mma[6] = {0};
     int cnt[6] = {0};
     unsigned long long tmin = ~0ull, tmax = 0;
     for (size_t i = 0; i < h.size(); i += 4) {
@@ -722,6 +721,11 @@ int deep_mk_train_steps(DeepMK &st, cudaStream_t stream, const std::vector<int> 
       const int ty = (int)(h[i + 3] & 0xff);
       wait[ty] += (double)(h[i + 1] - h[i]);
       run[ty] += (double)(h[i + 2] - h[i + 1]);
+      const unsigned long long ta = h[i + 3] >> 32;
+      if (ta) {  // accumulator ready (reconstruct the high bits from t1)
+        const unsigned long long full = (h[i + 1] & ~0x7fffffffull) | ta;
+        mma[ty] += (double)((full >= h[i + 1] ? full : full + 0x80000000ull) - h[i + 1]);
+      }
       cnt[ty]++;
       tmin = std::min(tmin, h[i]);
       tmax = std::max(tmax, h[i + 2]);
@@ -729,8 +733,8 @@ int deep_mk_train_steps(DeepMK &st, cudaStream_t stream, const std::vector<int> 
     fprintf(stderr, "[deep_mk prof] %d CTAs, span of the profiled tasks %.1f us\n", st.grid, (tmax - tmin) / 1e3);
     for (int t = 0; t < 6; ++t)
       if (cnt[t])
-        fprintf(stderr, "  %-6s %5d tasks  wait %7.2f us  run %7.2f us (mean)\n", names[t], cnt[t], wait[t] / cnt[t] / 1e3,
-                run[t] / cnt[t] / 1e3);
+        fprintf(stderr, "  %-6s %5d tasks  wait %7.2f us  run %7.2f us (of which to accumulator ready %6.2f us) (mean)\n",
+                names[t], cnt[t], wait[t] / cnt[t] / 1e3, run[t] / cnt[t] / 1e3, mma[t] / cnt[t] / 1e3);
   }
   return 0;
 }
