@@ -110,17 +110,34 @@ __host__ __device__ inline int cdiv(int a, int b) { return (a + b - 1) / b; }
 // per-step counts
 __host__ __device__ inline int tn_of(int n) { return cdiv(n, BN); }       // 64-col tiles of width n
 
+// forward epilogue of 32 columns of one row: z = acc + b, A = rn(sigma(z)), S = sigma'(z)
+template <int K>
+__device__ __forceinline__ void fwd_chunk(float (&v)[32], const float *bias, float *Arow, float *Srow) {
+  float4 b4[8];  // every bias load in flight before any store
+#pragma unroll
+  for (int j = 0; j < 8; ++j) b4[j] = __ldcg(reinterpret_cast<const float4 *>(bias) + j);
+#pragma unroll
+  for (int j = 0; j < 8; ++j) {
+    const float bb[4] = {b4[j].x, b4[j].y, b4[j].z, b4[j].w};
+    float a[4], sg[4];
+#pragma unroll
+    for (int u = 0; u < 4; ++u) {
+      act_fwd_t<K>(v[4 * j + u] + bb[u], a[u], sg[u]);
+      a[u] = tf32_rn(a[u]);
+    }
+    reinterpret_cast<float4 *>(Arow)[j] = make_float4(a[0], a[1], a[2], a[3]);
+    reinterpret_cast<float4 *>(Srow)[j] = make_float4(sg[0], sg[1], sg[2], sg[3]);
+  }
+}
+
 __global__ void __launch_bounds__(kThreads, 1) deep_mk_kernel(const __grid_constant__ Params p) {
   extern __shared__ __align__(1024) uint8_t smem_raw[];
   uint8_t *smem = reinterpret_cast<uint8_t *>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
   uint64_t *full = reinterpret_cast<uint64_t *>(smem + kStages * STAGE_BYTES);
   uint64_t *empty = full + kStages;
-  uint64_t *accum = empty + kStages;
-  uint32_t *tmem_slot = reinterpret_cast<uint32_t *>(accum + 1);
+  uint64_t *accum = empty + kStages;          // [0] accumulator ready, [2] OUT staging
+  uint32_t *tmem_slot = reinterpret_cast<uint32_t *>(accum + 4);
   float *sred = reinterpret_cast<float *>(tmem_slot + 4);  // [kThreads] reduction scratch
-  // OUT-task buffers alias the (idle) stage ring
-  float *sW = reinterpret_cast<float *>(smem);              // [kNOut][kMaxH] W_L
-  float *sD = sW + kNOut * kMaxH;                           // [BM][kNOut] delta_L of the block
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31, tid = threadIdx.x;
   const int L = p.L, nL = p.dims[L], H = p.dims[L - 1];
@@ -131,6 +148,7 @@ __global__ void __launch_bounds__(kThreads, 1) deep_mk_kernel(const __grid_const
       ptx::mbar_init(&empty[s], 1);
     }
     ptx::mbar_init(accum, 1);
+    ptx::mbar_init(accum + 2, 1);
     ptx::fence_mbar_init();
   }
   if (warp == 1) {
@@ -145,6 +163,7 @@ __global__ void __launch_bounds__(kThreads, 1) deep_mk_kernel(const __grid_const
 
   uint32_t it = 0;       // K-blocks issued by this CTA (ring position, across tasks)
   uint32_t ntc = 0;      // TC tasks run by this CTA (accumulator barrier parity)
+  uint32_t nout = 0;     // OUT tasks run by this CTA (staging barrier parity)
   const int T = p.T;
   int np = 0;  // profiled tasks of this CTA
   for (int64_t s = 0; s < p.n_steps; ++s) {
@@ -256,57 +275,44 @@ __global__ void __launch_bounds__(kThreads, 1) deep_mk_kernel(const __grid_const
           ptx::mbar_wait(accum, ntc & 1);
           tc::tc_fence_after();
           if (p.prof && r == 0) sred[0] = __int_as_float((int)(gtime() & 0x7fffffff));
-          float v[64];
-          {
-            float a[32], b[32];
-            tc::tmem_ld32(tmem + ((uint32_t)(32 * q) << 16), a);
-            tc::tmem_ld32(tmem + ((uint32_t)(32 * q) << 16) + 32u, b);
-#pragma unroll
-            for (int j = 0; j < 32; ++j) { v[j] = a[j]; v[32 + j] = b[j]; }
-          }
-          tc::tc_fence_before();
           if (type == T_FWD) {
             const int N = p.dims[l], n0 = tk.z * BN, m = tk.y * BM + r;
-            const float *bias = p.params + p.offB[l];
-            float *Arow = p.A[l] + (int64_t)m * N, *Srow = p.S[l] + (int64_t)m * N;
-            const int kind = p.act[l];
-#pragma unroll
-            for (int j = 0; j < 64; j += 4) {  // every bias load in flight before any store
-              const float4 b4 = __ldcg(reinterpret_cast<const float4 *>(bias + n0 + j));
-              v[j] += b4.x; v[j + 1] += b4.y; v[j + 2] += b4.z; v[j + 3] += b4.w;
-            }
-#pragma unroll
-            for (int j = 0; j < 64; j += 4) {
-              if (n0 + j < N) {  // N is a multiple of 64: whole float4s
-                float4 av, sv;
-                float *pa = &av.x, *ps = &sv.x;
-#pragma unroll
-                for (int u = 0; u < 4; ++u) {
-                  float a_, s_;
-                  act_fwd(kind, v[j + u], a_, s_);
-                  pa[u] = tf32_rn(a_);
-                  ps[u] = s_;
-                }
-                *reinterpret_cast<float4 *>(Arow + n0 + j) = av;
-                *reinterpret_cast<float4 *>(Srow + n0 + j) = sv;
+            const float *bias = p.params + p.offB[l] + n0;
+            float *Arow = p.A[l] + (int64_t)m * N + n0, *Srow = p.S[l] + (int64_t)m * N + n0;
+#pragma unroll 1
+            for (int c = 0; c < BN / 32; ++c) {  // 32-column chunks (keeps the code small: it runs once per task)
+              float v[32];
+              tc::tmem_ld32(tmem + ((uint32_t)(32 * q) << 16) + 32u * c, v);
+              switch (p.act[l]) {
+                case ACT_SIGMOID: fwd_chunk<ACT_SIGMOID>(v, bias + 32 * c, Arow + 32 * c, Srow + 32 * c); break;
+                case ACT_TANH: fwd_chunk<ACT_TANH>(v, bias + 32 * c, Arow + 32 * c, Srow + 32 * c); break;
+                case ACT_RELU: fwd_chunk<ACT_RELU>(v, bias + 32 * c, Arow + 32 * c, Srow + 32 * c); break;
+                case ACT_GAUSSIAN: fwd_chunk<ACT_GAUSSIAN>(v, bias + 32 * c, Arow + 32 * c, Srow + 32 * c); break;
+                default: fwd_chunk<ACT_STEP>(v, bias + 32 * c, Arow + 32 * c, Srow + 32 * c); break;
               }
             }
+            tc::tc_fence_before();
           } else if (type == T_BWD) {  // delta_{l-1} = acc .* sigma'(Z_{l-1}), in place of S_{l-1}
             const int N = p.dims[l - 1], n0 = tk.z * BN, m = tk.y * BM + r;
-            float *Srow = p.S[l - 1] + (int64_t)m * N;
+            float *Srow = p.S[l - 1] + (int64_t)m * N + n0;
             float *cs = reinterpret_cast<float *>(smem);  // [BM][65] block of deltas (the idle ring)
-            float4 s4[16];  // every sigma' load in flight before any store (N is a multiple of 64)
+#pragma unroll 1
+            for (int c = 0; c < BN / 32; ++c) {
+              float v[32];
+              tc::tmem_ld32(tmem + ((uint32_t)(32 * q) << 16) + 32u * c, v);
+              float4 s4[8];  // every sigma' load in flight before any store (N is a multiple of 64)
 #pragma unroll
-            for (int j = 0; j < 16; ++j) s4[j] = __ldcg(reinterpret_cast<const float4 *>(Srow + n0) + j);
+              for (int j = 0; j < 8; ++j) s4[j] = __ldcg(reinterpret_cast<const float4 *>(Srow + 32 * c) + j);
 #pragma unroll
-            for (int j = 0; j < 64; j += 4) {
-              if (n0 + j < N) {
-                const float4 sv = s4[j / 4];
-                const float d0 = v[j] * sv.x, d1 = v[j + 1] * sv.y, d2 = v[j + 2] * sv.z, d3 = v[j + 3] * sv.w;
-                cs[r * 65 + j] = d0; cs[r * 65 + j + 1] = d1; cs[r * 65 + j + 2] = d2; cs[r * 65 + j + 3] = d3;
-                *reinterpret_cast<float4 *>(Srow + n0 + j) = make_float4(tf32_rn(d0), tf32_rn(d1), tf32_rn(d2), tf32_rn(d3));
+              for (int j = 0; j < 8; ++j) {
+                const float d0 = v[4 * j] * s4[j].x, d1 = v[4 * j + 1] * s4[j].y, d2 = v[4 * j + 2] * s4[j].z,
+                            d3 = v[4 * j + 3] * s4[j].w;
+                float *cr = cs + r * 65 + 32 * c + 4 * j;
+                cr[0] = d0; cr[1] = d1; cr[2] = d2; cr[3] = d3;
+                reinterpret_cast<float4 *>(Srow + 32 * c)[j] = make_float4(tf32_rn(d0), tf32_rn(d1), tf32_rn(d2), tf32_rn(d3));
               }
             }
+            tc::tc_fence_before();
             // the block's share of the bias update of layer l-1: b -= (eta/B) sum_rows delta
             asm volatile("bar.sync 1, 128;" ::: "memory");
             if (r < 64 && n0 + r < N) {
@@ -320,99 +326,101 @@ __global__ void __launch_bounds__(kThreads, 1) deep_mk_kernel(const __grid_const
           } else {  // GRAD: W_l[m][n] -= scale * acc (one term per chunk, L2 reductions)
             const int M = p.dims[l], N = p.dims[l - 1];
             const int m = tk.z * BM + r, n0 = tk.w * BN;
-            if (m < M) {
-              float *Wrow = p.params + p.offW[l] + (int64_t)m * N;
-              const float sc = -p.scale;
-              if ((N & 3) == 0) {
+            float *Wrow = p.params + p.offW[l] + (int64_t)m * N + n0;
+            const float sc = -p.scale;
+#pragma unroll 1
+            for (int c = 0; c < BN / 32; ++c) {
+              float v[32];
+              tc::tmem_ld32(tmem + ((uint32_t)(32 * q) << 16) + 32u * c, v);
+              if (m < M) {
+                if ((N & 3) == 0) {
 #pragma unroll
-                for (int j = 0; j < 64; j += 4)
-                  if (n0 + j < N) red_v4(Wrow + n0 + j, sc * v[j], sc * v[j + 1], sc * v[j + 2], sc * v[j + 3]);
-              } else {
+                  for (int j = 0; j < 32; j += 4)
+                    if (n0 + 32 * c + j < N)
+                      red_v4(Wrow + 32 * c + j, sc * v[j], sc * v[j + 1], sc * v[j + 2], sc * v[j + 3]);
+                } else {
 #pragma unroll
-                for (int j = 0; j < 64; ++j)
-                  if (n0 + j < N) ptx::red_add_f32(Wrow + n0 + j, sc * v[j]);
+                  for (int j = 0; j < 32; ++j)
+                    if (n0 + 32 * c + j < N) ptx::red_add_f32(Wrow + 32 * c + j, sc * v[j]);
+                }
               }
             }
+            tc::tc_fence_before();
           }
         }
         ++ntc;
       } else if (type == T_OUT) {
-        // ---- the narrow output layer for rows [y*32, y*32 + 32) (SIMT): warp w owns rows w, w+6,
-        //      ...; each warp loads all its rows' A_{L-1}, S_{L-1} and y values before computing
-        //      (every global access of the task is one round trip in flight, not one per row)
+        // ---- the narrow output layer for rows [y*32, y*32 + 32) (SIMT).  The task's rows of A_{L-1}
+        //      and S_{L-1} and all of W_L are staged into shared memory by bulk copies (one
+        //      round trip), then warp w works on rows w, w+6, ... from shared memory.
         const int r0 = tk.y * BMO;
-        const float *WL = p.params + p.offW[L], *bL = p.params + p.offB[L];
-        for (int i = tid; i < nL * H; i += kThreads) sW[(i / H) * kMaxH + i % H] = __ldcg(WL + i);
+        float *sA = reinterpret_cast<float *>(smem);   // [BMO][H]
+        float *sS = sA + BMO * kMaxH;                   // [BMO][H]
+        float *sWo = sS + BMO * kMaxH;                  // [nL][H]
+        float *sDo = sWo + kNOut * kMaxH;               // [BMO][kNOut] delta_L
+        float *sb = sDo + BMO * kNOut;                  // [6][H] per-warp bias sums
+        uint64_t *bar = accum + 2;                      // (a spare mbarrier slot, see below)
         const float *AL1 = p.A[L - 1];
         float *SL1 = p.S[L - 1];
-        constexpr int kRW = (BMO + 5) / 6;  // rows per warp (6 warps)
-        constexpr int kC = kMaxH / 32;      // columns per lane
-        float av[kRW][kC], sv[kRW][kC], yv[kRW];
-#pragma unroll
-        for (int q = 0; q < kRW; ++q) {
-          const int rr = warp + 6 * q;
-          const int64_t m = r0 + rr;
-          yv[q] = (rr < BMO && lane < nL) ? __ldg(p.Y + (start + m) * nL + lane) : 0.0f;
-#pragma unroll
-          for (int i = 0; i < kC; ++i) {
-            const bool ok = rr < BMO && lane + 32 * i < H;
-            av[q][i] = ok ? __ldcg(AL1 + m * H + lane + 32 * i) : 0.0f;
-            sv[q][i] = ok ? __ldcg(SL1 + m * H + lane + 32 * i) : 0.0f;
-          }
+        if (tid == 0) {
+          const uint32_t rb = (uint32_t)(BMO * H * 4), wb = (uint32_t)(nL * H * 4);
+          ptx::mbar_arrive_expect_tx(bar, 2 * rb + wb);
+          ptx::bulk_g2s(sA, AL1 + (int64_t)r0 * H, rb, bar);
+          ptx::bulk_g2s(sS, SL1 + (int64_t)r0 * H, rb, bar);
+          ptx::bulk_g2s(sWo, p.params + p.offW[L], wb, bar);
         }
-        const float bl = lane < nL ? __ldcg(bL + lane) : 0.0f;
-        __syncthreads();  // sW
+        const float bl = lane < nL ? __ldcg(p.params + p.offB[L] + lane) : 0.0f;
         float lacc = 0.0f;
-        float bsum[kC];   // this lane's columns: sum over the warp's rows of delta_{L-1}
+        constexpr int kC = kMaxH / 32;  // columns per lane
+        float bsum[kC];
 #pragma unroll
         for (int i = 0; i < kC; ++i) bsum[i] = 0.0f;
+        ptx::mbar_wait(bar, nout & 1);
+        ++nout;
+#pragma unroll 1
+        for (int rr = warp; rr < BMO; rr += kThreads / 32) {
+          const int64_t m = r0 + rr;
+          const float y = lane < nL ? __ldg(p.Y + (start + m) * nL + lane) : 0.0f;
+          const float *ar = sA + rr * H;
+          float dl = 0.0f;  // lane o < nL: delta_L[m][o]
+#pragma unroll 1
+          for (int o = 0; o < nL; ++o) {
+            float zpart = 0.0f;
 #pragma unroll
-        for (int q = 0; q < kRW; ++q) {
-          const int rr = warp + 6 * q;
-          if (rr < BMO) {  // warp-uniform
-            const int64_t m = r0 + rr;
-            float dl = 0.0f;  // lane o < nL: delta_L[m][o]
-#pragma unroll
-            for (int o = 0; o < kNOut; ++o) {
-              if (o < nL) {
-                float zpart = 0.0f;
-#pragma unroll
-                for (int i = 0; i < kC; ++i) zpart = fmaf(av[q][i], sW[o * kMaxH + lane + 32 * i], zpart);
-                const float z = warp_sum(zpart);
-                if (lane == o) {
-                  float a_, s_;
-                  act_fwd(p.act[L], z + bl, a_, s_);
-                  const float diff = a_ - yv[q];
-                  lacc = fmaf(diff, diff, lacc);
-                  dl = diff * s_;
-                  p.A[L][m * nL + o] = a_;
-                  p.S[L][m * nL + o] = dl;
-                }
-              }
+            for (int i = 0; i < kC; ++i)
+              if (lane + 32 * i < H) zpart = fmaf(ar[lane + 32 * i], sWo[o * H + lane + 32 * i], zpart);
+            const float z = warp_sum(zpart);
+            if (lane == o) {
+              float a_, s_;
+              act_fwd(p.act[L], z + bl, a_, s_);
+              const float diff = a_ - y;
+              lacc = fmaf(diff, diff, lacc);
+              dl = diff * s_;
+              p.A[L][m * nL + o] = a_;
+              p.S[L][m * nL + o] = dl;
             }
-            if (lane < kNOut) sD[rr * kNOut + lane] = lane < nL ? dl : 0.0f;
-            float d[kNOut];
+          }
+          if (lane < kNOut) sDo[rr * kNOut + lane] = lane < nL ? dl : 0.0f;
 #pragma unroll
-            for (int o = 0; o < kNOut; ++o) d[o] = __shfl_sync(0xffffffffu, dl, o);
-#pragma unroll
-            for (int i = 0; i < kC; ++i) {
-              const int j = lane + 32 * i;
-              if (j < H) {
-                float acc = 0.0f;
-#pragma unroll
-                for (int o = 0; o < kNOut; ++o)
-                  if (o < nL) acc = fmaf(d[o], sW[o * kMaxH + j], acc);
-                const float dv = acc * sv[q][i];
-                bsum[i] += dv;
-                SL1[m * H + j] = tf32_rn(dv);  // delta_{L-1}: operand of BWD(L-1) / GRAD(L-1)
-              }
+          for (int i = 0; i < kC; ++i) {
+            const int j = lane + 32 * i;
+            if (j < H) {
+              float acc = 0.0f;
+#pragma unroll 1
+              for (int o = 0; o < nL; ++o) acc = fmaf(__shfl_sync(0xffffffffu, dl, o), sWo[o * H + j], acc);
+              const float dv = acc * sS[rr * H + j];
+              bsum[i] += dv;
+              SL1[m * H + j] = tf32_rn(dv);  // delta_{L-1}: operand of BWD(L-1) / GRAD(L-1)
+            } else {
+#pragma unroll 1
+              for (int o = 0; o < nL; ++o) (void)__shfl_sync(0xffffffffu, dl, o);
             }
           }
         }
         sred[tid] = warp_sum(lacc);
-        float *sb = sD + BMO * kNOut;  // [6 warps][kMaxH] per-warp bias sums
 #pragma unroll
-        for (int i = 0; i < kC; ++i) sb[warp * kMaxH + lane + 32 * i] = bsum[i];
+        for (int i = 0; i < kC; ++i)
+          if (lane + 32 * i < H) sb[warp * H + lane + 32 * i] = bsum[i];
         __syncthreads();
         if (tid == 0) {
           float l2 = 0.0f;
@@ -422,30 +430,25 @@ __global__ void __launch_bounds__(kThreads, 1) deep_mk_kernel(const __grid_const
         for (int j = tid; j < H; j += kThreads) {  // b_{L-1} -= (eta/B) sum over the task's rows
           float bsv = 0.0f;
 #pragma unroll
-          for (int w = 0; w < kThreads / 32; ++w) bsv += sb[w * kMaxH + j];
+          for (int w = 0; w < kThreads / 32; ++w) bsv += sb[w * H + j];
           ptx::red_add_f32(p.params + p.offB[L - 1] + j, -p.scale * bsv);
         }
         // tendency of W_L (columns j < H) and b_L (column H) over the task's rows, added into the
         // step's accumulator (applied by GFIN after every OUT task, so that all of them read the
-        // pre-step W_L); the A_{L-1} rows are re-read from L2, 16 loads in flight per thread
-        float *pb = p.part;
+        // pre-step W_L)
         for (int j = tid; j <= H; j += kThreads) {
           float g[kNOut];
 #pragma unroll
           for (int o = 0; o < kNOut; ++o) g[o] = 0.0f;
+#pragma unroll 4
+          for (int q0 = 0; q0 < BMO; ++q0) {
+            const float a = j < H ? sA[q0 * H + j] : 1.0f;
 #pragma unroll
-          for (int q0 = 0; q0 < BMO; q0 += 16) {
-            float a[16];
-#pragma unroll
-            for (int u = 0; u < 16; ++u) a[u] = j < H ? __ldcg(AL1 + (int64_t)(r0 + q0 + u) * H + j) : 1.0f;
-#pragma unroll
-            for (int u = 0; u < 16; ++u)
-#pragma unroll
-              for (int o = 0; o < kNOut; ++o) g[o] = fmaf(sD[(q0 + u) * kNOut + o], a[u], g[o]);
+            for (int o = 0; o < kNOut; ++o) g[o] = fmaf(sDo[q0 * kNOut + o], a, g[o]);
           }
 #pragma unroll
           for (int o = 0; o < kNOut; ++o)
-            if (o < nL) ptx::red_add_f32(pb + o * (H + 1) + j, g[o]);
+            if (o < nL) ptx::red_add_f32(p.part + o * (H + 1) + j, g[o]);
         }
       } else if (type == T_GFIN) {
         // ---- W_L, b_L -= scale * (partials summed in row-block order); the step's mean cost
