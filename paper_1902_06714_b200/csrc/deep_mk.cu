@@ -137,7 +137,7 @@ __global__ void __launch_bounds__(kThreads, 1) deep_mk_kernel(const __grid_const
   uint64_t *empty = full + kStages;
   uint64_t *accum = empty + kStages;          // [0] accumulator ready, [2] OUT staging
   uint32_t *tmem_slot = reinterpret_cast<uint32_t *>(accum + 4);
-  float *sred = reinterpret_cast<float *>(tmem_slot + 4);  // [kThreads] reduction scratch
+  float *sred = reinterpret_cast<float *>(tmem_slot + 4);  // [kThreads + 8] reduction scratch / stamps
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31, tid = threadIdx.x;
   const int L = p.L, nL = p.dims[L], H = p.dims[L - 1];
@@ -377,6 +377,7 @@ __global__ void __launch_bounds__(kThreads, 1) deep_mk_kernel(const __grid_const
         for (int i = 0; i < kC; ++i) bsum[i] = 0.0f;
         ptx::mbar_wait(bar, nout & 1);
         ++nout;
+        if (p.prof && tid == 0) sred[kThreads + 1] = __int_as_float((int)(gtime() & 0x7fffffff));
 #pragma unroll 1
         for (int rr = warp; rr < BMO; rr += kThreads / 32) {
           const int64_t m = r0 + rr;
@@ -422,6 +423,7 @@ __global__ void __launch_bounds__(kThreads, 1) deep_mk_kernel(const __grid_const
         for (int i = 0; i < kC; ++i)
           if (lane + 32 * i < H) sb[warp * H + lane + 32 * i] = bsum[i];
         __syncthreads();
+        if (p.prof && tid == 0) sred[kThreads + 2] = __int_as_float((int)(gtime() & 0x7fffffff));
         if (tid == 0) {
           float l2 = 0.0f;
           for (int w = 0; w < kThreads / 32; ++w) l2 += sred[w * 32];
@@ -433,6 +435,7 @@ __global__ void __launch_bounds__(kThreads, 1) deep_mk_kernel(const __grid_const
           for (int w = 0; w < kThreads / 32; ++w) bsv += sb[w * H + j];
           ptx::red_add_f32(p.params + p.offB[L - 1] + j, -p.scale * bsv);
         }
+        if (p.prof) { __syncthreads(); if (tid == 0) sred[kThreads + 3] = __int_as_float((int)(gtime() & 0x7fffffff)); }
         // tendency of W_L (columns j < H) and b_L (column H) over the task's rows, added into the
         // step's accumulator (applied by GFIN after every OUT task, so that all of them read the
         // pre-step W_L)
@@ -490,6 +493,7 @@ __global__ void __launch_bounds__(kThreads, 1) deep_mk_kernel(const __grid_const
       __syncthreads();
       tc::tc_fence_after();
       if (tid == 0) {
+        if (p.prof && type == T_OUT) sred[kThreads + 4] = __int_as_float((int)(gtime() & 0x7fffffff));
         ptx::fence_proxy_async_global();
         if (type == T_FWD) signal(c_fwd(p, l, tk.y));
         else if (type == T_OUT) { signal(c_dlt(p, L - 1, tk.y / kOutPer)); signal(c_oall(p)); }
@@ -497,7 +501,8 @@ __global__ void __launch_bounds__(kThreads, 1) deep_mk_kernel(const __grid_const
         else if (type == T_GRAD) signal(c_grad(p, l));
         signal(c_step(p));
         if (p.prof && np < p.prof_cap) {
-          unsigned long long *q = p.prof + ((int64_t)blockIdx.x * p.prof_cap + np) * 4;
+          unsigned long long *q = p.prof + ((int64_t)blockIdx.x * p.prof_cap + np) * 8;
+          for (int k = 1; k <= 4; ++k) q[3 + k] = type == T_OUT ? (unsigned)__float_as_int(sred[kThreads + k]) : 0u;
           const unsigned long long te = gtime();
           // word 3: task word | accumulator-ready time (low 31 bits of globaltimer) << 32 (TC tasks)
           const unsigned long long ta = (type == T_FWD || type == T_BWD || type == T_GRAD)
@@ -519,8 +524,11 @@ __global__ void __launch_bounds__(kThreads, 1) deep_mk_kernel(const __grid_const
 }  // namespace
 
 bool deep_mk_applicable(const std::vector<int> &dims, int math, int64_t batch) {
-  static const bool off = getenv("NF_NO_DEEP_MK") != nullptr;
-  if (off || math != 1) return false;
+  // opt-in (NF_DEEP_MK=1, read per call): measured slower than the per-layer kernels on config 4
+  // (196 vs 140 us per step, profiles/r02_deep_mk_experiment.txt) -- each task's fixed latencies
+  // (TMA fill, epilogue, release / acquire) are not overlapped across tasks yet
+  const char *on = getenv("NF_DEEP_MK");
+  if (!on || atoi(on) == 0 || math != 1) return false;
   const int L = (int)dims.size() - 1;
   if (L < 2 || L > kMaxL - 1) return false;
   if (dims[0] % 4 != 0 || dims[0] < 32) return false;
@@ -685,8 +693,8 @@ int deep_mk_train_steps(DeepMK &st, cudaStream_t stream, const std::vector<int> 
   static unsigned long long *prof_buf = nullptr;
   const int prof_cap = 64;
   if (prof) {
-    if (!prof_buf) cudaMalloc(&prof_buf, (size_t)148 * prof_cap * 4 * 8);
-    cudaMemsetAsync(prof_buf, 0, (size_t)148 * prof_cap * 4 * 8, stream);
+    if (!prof_buf) cudaMalloc(&prof_buf, (size_t)148 * prof_cap * 8 * 8);
+    cudaMemsetAsync(prof_buf, 0, (size_t)148 * prof_cap * 8 * 8, stream);
     p.prof = prof_buf;
     p.prof_cap = prof_cap;
   }
@@ -712,15 +720,26 @@ int deep_mk_train_steps(DeepMK &st, cudaStream_t stream, const std::vector<int> 
     return -1;
   }
   if (prof) {  // per task type: mean dependency wait and run time (the first 64 tasks of each CTA)
-    std::vector<unsigned long long> h((size_t)st.grid * prof_cap * 4);
+    std::vector<unsigned long long> h((size_t)st.grid * prof_cap * 8);
     cudaStreamSynchronize(stream);
     cudaMemcpy(h.data(), prof_buf, h.size() * 8, cudaMemcpyDeviceToHost);
     const char *names[6] = {"FWD", "OUT", "BWD", "GRAD", "GFIN", "ROUND"};
     double wait[6] = {0}, run[6] = {0}, mma[6] = {0};
     int cnt[6] = {0};
     unsigned long long tmin = ~0ull, tmax = 0;
-    for (size_t i = 0; i < h.size(); i += 4) {
+    double osub[5] = {0};
+    int ocnt = 0;
+    for (size_t i = 0; i < h.size(); i += 8) {
       if (!h[i]) continue;
+      if ((int)(h[i + 3] & 0xff) == T_OUT) {  // sub-phase ends relative to t1 (low 31 bits)
+        unsigned long long prev = h[i + 1] & 0x7fffffffull;
+        for (int k = 1; k <= 4; ++k) {
+          const unsigned long long tk2 = h[i + 3 + k];
+          osub[k] += (double)((tk2 - prev) & 0x7fffffffull);
+          prev = tk2;
+        }
+        ++ocnt;
+      }
       const int ty = (int)(h[i + 3] & 0xff);
       wait[ty] += (double)(h[i + 1] - h[i]);
       run[ty] += (double)(h[i + 2] - h[i + 1]);
@@ -734,6 +753,9 @@ int deep_mk_train_steps(DeepMK &st, cudaStream_t stream, const std::vector<int> 
       tmax = std::max(tmax, h[i + 2]);
     }
     fprintf(stderr, "[deep_mk prof] %d CTAs, span of the profiled tasks %.1f us\n", st.grid, (tmax - tmin) / 1e3);
+    if (ocnt)
+      fprintf(stderr, "  OUT phases: staging %.2f, rows %.2f, bias %.2f, W_L tendency %.2f us\n", osub[1] / ocnt / 1e3,
+              osub[2] / ocnt / 1e3, osub[3] / ocnt / 1e3, osub[4] / ocnt / 1e3);
     for (int t = 0; t < 6; ++t)
       if (cnt[t])
         fprintf(stderr, "  %-6s %5d tasks  wait %7.2f us  run %7.2f us (of which to accumulator ready %6.2f us) (mean)\n",

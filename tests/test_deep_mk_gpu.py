@@ -1,4 +1,5 @@
-"""The deep-net task megakernel (csrc/deep_mk.cu: config 4's path in NF_MATH_TF32) against the
+"""The deep-net task megakernel (csrc/deep_mk.cu, opt-in NF_DEEP_MK=1, TF32 nets of narrow hidden
+layers such as config 4) against the
 fp64 oracle (-m gpu): several SGD steps in ONE launch of nf_train_steps, per-step costs and the
 applied updates at the TF32 bar (5e-3 normwise, reading R14b), on nets with ragged input widths,
 hidden widths 64..256, one activation per layer and narrow output layers; plus its launch
@@ -25,7 +26,8 @@ CASES = [
 
 
 @pytest.mark.parametrize("dims,act,batch,steps", CASES)
-def test_deep_megakernel_steps(dims, act, batch, steps):
+def test_deep_megakernel_steps(dims, act, batch, steps, monkeypatch):
+    monkeypatch.setenv("NF_DEEP_MK", "1")   # opt-in path (read per call)
     p = synth.random_params(601 + len(dims), dims, 0.08)
     X, Y = synth.random_batch(602, 3 * batch, dims[0], dims[-1], "uniform")
     starts = np.random.default_rng(603).integers(0, 2 * batch + 1, size=steps)
