@@ -111,6 +111,14 @@ struct nf_net {
   // TF32 step; re-rounded from params when shadow_ok is false (any other writer of params).
   float *params_t = nullptr;
   bool shadow_ok = false;
+  // NF_MATH_FP32 with pre-split 3xTF32 (NF_PRESPLIT, default on): tf32_lo of every tensor-core
+  // operand, written by its producer -- the weights' lo shadow (kept by the SGD epilogue like
+  // params_t), the hidden activations' and deltas' lo arrays (stash_lo), the input rows' (xlo)
+  float *params_lo = nullptr;
+  bool lo_ok = false;
+  DevBuf stash_lo, xlo;
+  std::vector<float *> Alo, Dlo;
+  int64_t lo_rows = 0;
   std::vector<int64_t> offW, offB;       // index 1..L
   // stash: A_l (activations) and S_l (sigma'(Z_l), overwritten by delta_l), l = 1..L
   int64_t ws_rows = 0;
@@ -157,7 +165,12 @@ struct nf_net {
 
   float *W(int l) const { return params + offW[l]; }
   float *Wt(int l) const { return params_t + offW[l]; }
+  float *Wlo(int l) const { return params_lo + offW[l]; }
   bool tf32() const { return math == NF_MATH_TF32; }
+  bool presplit() const {
+    static const bool on = getenv("NF_PRESPLIT") == nullptr || atoi(getenv("NF_PRESPLIT")) != 0;
+    return on && math == NF_MATH_FP32;
+  }
   double *W64(int l) const { return params64 + offW[l]; }
   double *b64(int l) const { return params64 + offB[l]; }
   float *b(int l) const { return params + offB[l]; }
@@ -257,6 +270,36 @@ int ensure_shadow(nf_net *net) {
   return NF_OK;
 }
 
+// fp32 mode: the lo shadow of the weights and the lo arrays of a training batch of `rows` rows
+int ensure_lo(nf_net *net, int64_t rows) {
+  if (!net->presplit()) return NF_OK;
+  if (!net->params_lo) NF_CUDA(cudaMalloc(&net->params_lo, net->nparams * sizeof(float)));
+  if (!net->lo_ok) {
+    NF_CUDA(split_lo(net->stream, net->params, net->params_lo, net->nparams));
+    net->lo_ok = true;
+  }
+  if (rows > net->lo_rows) {
+    cudaStreamCaptureStatus cs = cudaStreamCaptureStatusNone;
+    cudaStreamIsCapturing(net->stream, &cs);
+    if (cs != cudaStreamCaptureStatusNone) return fail(NF_ECUDA, "lo arrays must be sized before a graph capture");
+    int64_t per_row = net->dims[0];
+    for (int l = 1; l <= net->L; ++l) per_row += 2 * (int64_t)net->dims[l];
+    NF_CUDA(cudaStreamSynchronize(net->stream));
+    drop_graph(net);
+    NF_CUDA(net->stash_lo.ensure((size_t)(per_row * rows) * sizeof(float)));
+    float *p = net->stash_lo.as<float>();
+    net->Alo.assign(net->L + 1, nullptr);
+    net->Dlo.assign(net->L + 1, nullptr);
+    net->Alo[0] = p; p += rows * net->dims[0];  // the input rows' lo (xlo)
+    for (int l = 1; l <= net->L; ++l) {
+      net->Alo[l] = p; p += rows * net->dims[l];
+      net->Dlo[l] = p; p += rows * net->dims[l];
+    }
+    net->lo_rows = rows;
+  }
+  return NF_OK;
+}
+
 // fwdprop over a batch.  mode: 0 train (stash A, S; output layer
 // S = delta_L), 2 inference (A only).  y only for mode 0.
 int forward(nf_net *net, const float *x, const float *y, int64_t n, int mode) {
@@ -264,13 +307,19 @@ int forward(nf_net *net, const float *x, const float *y, int64_t n, int mode) {
   const int L = net->L;
   if (int rc = ensure_shadow(net)) return rc;
   const bool t = net->tf32();
+  // fp32 training / tendencies: pre-split operands (the input rows' lo first)
+  const bool lo = mode == 0 && net->presplit();
+  if (lo) {
+    if (int rc = ensure_lo(net, n)) return rc;
+    NF_CUDA(split_lo(net->stream, x, net->Alo[0], n * net->dims[0]));
+  }
   net->out_fused = mode == 0 && L >= 2 &&
                    out_layer_fusable((int)n, net->dims[L - 1], net->dims[L], net->A[L - 1], net->S[L - 1], net->W(L));
   for (int l = 1; l <= net->L; ++l) {
     if (l == L && net->out_fused) {  // K1+K2 of the output layer, K3 of layer L-1, K4(L) partials
       NF_CUDA(out_layer_train_fused(net->stream, (int)n, net->dims[L - 1], net->dims[L], net->A[L - 1],
                                     net->S[L - 1], net->W(L), net->b(L), y, net->A[L], net->S[L], net->act_o,
-                                    net->part_out.as<float>(), t ? 1 : 0));
+                                    net->part_out.as<float>(), t ? 1 : 0, lo ? net->Dlo[L - 1] : nullptr));
       break;
     }
     const int lm = (mode == 2) ? 2 : (l < net->L ? 0 : 1);
@@ -279,8 +328,9 @@ int forward(nf_net *net, const float *x, const float *y, int64_t n, int mode) {
     EpiFwd epi{net->b(l), net->A[l], net->S[l], y, net->dims[l], net->act(l), lm, (t && (lm == 1 || l < L)) ? 1 : 0};
     if (lm == 0 && tposed(net, l + 1)) { epi.T = net->AT[l]; epi.ldT = (int)n; }   // A_l^T for K4(l+1)
     if (lm == 1 && tposed(net, l)) { epi.T = net->DT[l]; epi.ldT = (int)n; }       // delta_L^T for K4(L)
+    if (lo) epi.lo = lm == 0 ? net->Alo[l] : net->Dlo[l];
     NF_CUDA(gemm_fwd(net->stream, (int)n, net->dims[l], net->dims[l - 1], in, net->W(l), epi, net->ws,
-                     t ? net->Wt(l) : nullptr));
+                     t ? net->Wt(l) : nullptr, lo ? net->Alo[l - 1] : nullptr, lo ? net->Wlo(l) : nullptr));
     in = net->A[l];
   }
   return NF_OK;
@@ -322,8 +372,10 @@ int backward(nf_net *net, const float *x, int64_t n, float eta, float *grad, flo
   const float scale = (float)((double)eta / (double)n);
   std::vector<char> bias_done(net->L + 1, 0);  // layer's bias update applied by K3's epilogue
   // TF32 SGD: split-K terms reduced into W leave the shadow stale -> one rounding pass at the end
+  // (fp32 with pre-split: the lo shadow, one split pass)
+  const bool lo = net->presplit() && net->lo_rows >= n && !net->Alo.empty();
   net->red_round = false;
-  net->ws.red_flag = net->ws2.red_flag = (!grad && net->tf32()) ? &net->red_round : nullptr;
+  net->ws.red_flag = net->ws2.red_flag = (!grad && (net->tf32() || lo)) ? &net->red_round : nullptr;
   for (int l = net->L; l >= 1; --l) {
     const int nl = net->dims[l], nk = net->dims[l - 1];
     const bool fused = l == net->L && net->out_fused;  // K3(L) ran inside the forward kernel
@@ -332,6 +384,7 @@ int backward(nf_net *net, const float *x, int64_t n, float eta, float *grad, flo
       EpiBwd eb{net->S[l - 1], nk};
       eb.rnd = t ? 1 : 0;
       if (tposed(net, l - 1)) { eb.T = net->DT[l - 1]; eb.ldT = (int)n; }  // delta_{l-1}^T for K4(l-1)
+      if (lo) eb.lo = net->Dlo[l - 1];
       const float *aprev2 = l > 2 ? net->A[l - 2] : x;  // the operand of layer l-1's weight GEMM
       if (!grad && gemm_bwd_fuses_bias((int)n, nk, nl, net->S[l], net->W(l)) &&
           gemm_grad_tc(nk, net->dims[l - 2], (int)n, net->S[l - 1], aprev2)) {
@@ -339,7 +392,8 @@ int backward(nf_net *net, const float *x, int64_t n, float eta, float *grad, flo
         eb.bscale = scale;
         bias_done[l - 1] = 1;
       }
-      NF_CUDA(gemm_bwd(main_st, (int)n, nk, nl, net->S[l], net->W(l), eb, net->ws, t ? net->Wt(l) : nullptr));
+      NF_CUDA(gemm_bwd(main_st, (int)n, nk, nl, net->S[l], net->W(l), eb, net->ws, t ? net->Wt(l) : nullptr,
+                       lo ? net->Dlo[l] : nullptr, lo ? net->Wlo(l) : nullptr));
     }
     NF_CUDA(cudaEventRecord(net->ev[l], main_st));  // K3(l) done with W_l and delta_l is final
     NF_CUDA(cudaStreamWaitEvent(side, net->ev[l], 0));
@@ -347,22 +401,28 @@ int backward(nf_net *net, const float *x, int64_t n, float eta, float *grad, flo
     EpiGrad eg = grad ? EpiGrad{grad + net->offW[l], grad + net->offB[l], nk, nk, 0.0f, 1}
                       : EpiGrad{net->W(l), net->b(l), nk, nk, scale, 0};
     if (!grad && t) eg.Wt = net->Wt(l);  // the update also refreshes the TF32 shadow of W_l
+    if (!grad && lo) eg.Wlo = net->Wlo(l);  // ... or the lo shadow (fp32 mode)
     cudaStream_t kst = side;  // the stream layer l's tendencies are produced on
     if (fused) NF_CUDA(out_layer_grad_final(side, (int)n, nk, nl, net->part_out.as<float>(), eg, step_loss));
     else if (l == 1 && net->L > 1 && side != main_st && (net->math != NF_MATH_TF32 || n <= 2048)) {
       // the main stream is idle after the last K3: K4(1) there, concurrent with K4(2) on the side
       // stream (c4 134 -> 130 us, 3xTF32 c3 462 -> 445 us; c3's 1xTF32 pair contends: 154 -> 157)
       NF_CUDA(gemm_grad(main_st, nl, nk, (int)n, net->S[l], aprev, eg, net->ws, bias_done[l] != 0,
-                        tposed(net, l) ? net->DT[l] : nullptr, tposed(net, l) && l > 1 ? net->AT[l - 1] : nullptr));
+                        tposed(net, l) ? net->DT[l] : nullptr, tposed(net, l) && l > 1 ? net->AT[l - 1] : nullptr,
+                        lo ? net->Dlo[l] : nullptr, lo ? net->Alo[l - 1] : nullptr));
       kst = main_st;
     } else NF_CUDA(gemm_grad(side, nl, nk, (int)n, net->S[l], aprev, eg, net->ws2, bias_done[l] != 0,
-                             tposed(net, l) ? net->DT[l] : nullptr, tposed(net, l) && l > 1 ? net->AT[l - 1] : nullptr));
+                             tposed(net, l) ? net->DT[l] : nullptr, tposed(net, l) && l > 1 ? net->AT[l - 1] : nullptr,
+                             lo ? net->Dlo[l] : nullptr, lo ? net->Alo[l - 1] : nullptr));
     if (layer_done && layer_done[l - 1]) NF_CUDA(cudaEventRecord(layer_done[l - 1], kst));  // nf_grad_layers
   }
   NF_CUDA(cudaEventRecord(net->ev[net->L + 1], side));  // join
   NF_CUDA(cudaStreamWaitEvent(main_st, net->ev[net->L + 1], 0));
   net->ws.red_flag = net->ws2.red_flag = nullptr;
-  if (net->red_round) NF_CUDA(round_tf32(main_st, net->params, net->params_t, net->nparams));
+  if (net->red_round) {
+    if (net->tf32()) NF_CUDA(round_tf32(main_st, net->params, net->params_t, net->nparams));
+    else NF_CUDA(split_lo(main_st, net->params, net->params_lo, net->nparams));
+  }
   return NF_OK;
 }
 
@@ -675,6 +735,9 @@ void nf_net_destroy(nf_net *net) {
   if (net->params) cudaFree(net->params);
   if (net->params64) cudaFree(net->params64);
   if (net->params_t) cudaFree(net->params_t);
+  if (net->params_lo) cudaFree(net->params_lo);
+  net->stash_lo.release();
+  net->xlo.release();
   net->stash64.release();
   net->partial64.release();
   net->grad64.release();
@@ -720,7 +783,10 @@ int nf_set_math(nf_net *net, int mode) {
     NF_CUDA(f64_round(net->stream, net->params64, net->params, net->nparams));
     fused_small_invalidate(net->fused);
   }
-  if (mode != net->math) net->shadow_ok = false;
+  if (mode != net->math) {
+    net->shadow_ok = false;
+    net->lo_ok = false;
+  }
   net->math = mode;
   net->ws.math = mode;
   return NF_OK;
@@ -760,6 +826,7 @@ int nf_set_params(nf_net *net, const float *src, int64_t count) {
   NF_CUDA(cudaMemcpyAsync(net->params, src, count * sizeof(float),
                           dev ? cudaMemcpyDeviceToDevice : cudaMemcpyHostToDevice, net->stream));
   net->shadow_ok = false;
+  net->lo_ok = false;
   if (net->math == NF_MATH_FP64) NF_CUDA(f64_widen(net->stream, net->params, net->params64, count));
   if (!dev) NF_CUDA(cudaStreamSynchronize(net->stream));
   fused_small_invalidate(net->fused);
@@ -843,6 +910,7 @@ static int train_steps_device(nf_net *net, const float *dX, const float *dY, int
     if (src == 0) {
       fused_small_invalidate(net->fused);
       net->shadow_ok = false;
+  net->lo_ok = false;
       return NF_OK;
     }
     if (src != SINGLE_NOT_APPLICABLE)
@@ -867,7 +935,8 @@ static int train_steps_device(nf_net *net, const float *dX, const float *dY, int
   }
   int rc = net->math == NF_MATH_FP64 ? FUSED_NOT_APPLICABLE : fused_small_train_steps(net->fused, net->stream, net->dims, net->act_h, net->act_o,
                                    net->params, dX, dY, dN, batch, st.data(), n_steps, eta, step_loss);
-  if (rc == 0) net->shadow_ok = false;  // K6 updated params
+  if (rc == 0) net->shadow_ok = false;
+  net->lo_ok = false;  // K6 updated params
   if (rc == FUSED_NOT_APPLICABLE) {
     // Generic nets: the per-step kernel sequence of all n_steps, captured once as a CUDA
     // graph and replayed while the arguments repeat (removes the host launch gaps between the
@@ -876,6 +945,7 @@ static int train_steps_device(nf_net *net, const float *dX, const float *dY, int
     if ((rc = ensure_side(net))) return rc;
     if ((rc = ensure_shadow(net))) return rc;  // before capture: the graph keeps it current
     if (net->math != NF_MATH_FP64 && (rc = ensure_tpose(net, dX + st[0] * n0, batch))) return rc;
+    if ((rc = ensure_lo(net, batch))) return rc;  // (sized before the capture)
     NF_CUDA(net->red.ensure(red_bytes()));
     std::vector<int64_t> key = {(int64_t)(uintptr_t)dX, (int64_t)(uintptr_t)dY, N, batch, n_steps,
                                 (int64_t)(uintptr_t)step_loss, (int64_t)(uintptr_t)net->stream, net->math,
@@ -1076,6 +1146,7 @@ int nf_update(nf_net *net, const float *grad, int64_t count, float eta, int64_t 
   if (net->math == NF_MATH_FP64) NF_CUDA(f64_update(net->stream, net->params64, dg, count, scale));
   else NF_CUDA(sgd_update(net->stream, net->params, dg, count, (float)scale));
   net->shadow_ok = false;
+  net->lo_ok = false;
   fused_small_invalidate(net->fused);
   if (dg != grad) NF_CUDA(cudaStreamSynchronize(net->stream));
   return NF_OK;

@@ -47,6 +47,9 @@ struct EpiFwd {
   static constexpr bool kHasT = true;
   const float *bias; float *A; float *S; const float *Y; int ld; int act; int mode; int rnd = 0;
   float *T = nullptr; int ldT = 0;
+  // lo (fp32 mode, pre-split 3xTF32 consumers): tf32_lo of the stored operand value -- A for a
+  // hidden layer, delta_L for the output layer -- [rows][ld] like A
+  float *lo = nullptr;
   __device__ __forceinline__ float load(int m, int n) const {
     return mode == 1 ? Y[(int64_t)m * ld + n] : 0.0f;
   }
@@ -57,7 +60,9 @@ struct EpiFwd {
     float a, s;
     act_fwd(act, z, a, s);
     A[i] = (rnd && mode == 0) ? tf32_rn(a) : a;
-    S[i] = mode == 0 ? s : (rnd ? tf32_rn((a - y) * s) : (a - y) * s);
+    const float sv = mode == 0 ? s : (rnd ? tf32_rn((a - y) * s) : (a - y) * s);
+    S[i] = sv;
+    if (lo) lo[i] = tf32_lo(mode == 0 ? a : sv);
   }
   __device__ __forceinline__ void operator()(int m, int n, float acc) const { store(m, n, acc, load(m, n)); }
 
@@ -96,8 +101,10 @@ struct EpiFwd {
             const float d = RND ? tf32_rn((a[u] - y[u]) * s[u]) : (a[u] - y[u]) * s[u];
             S[i] = d;
             v[33 * (r0 + u)] = d;
+            if (lo) lo[i] = tf32_lo(d);
           } else {
             v[33 * (r0 + u)] = av;
+            if (MODE == 0 && lo) lo[i] = tf32_lo(av);
           }
         }
       }
@@ -150,13 +157,17 @@ struct EpiBwd {
   float *bias = nullptr; float bscale = 0.0f;
   int rnd = 0;
   float *T = nullptr; int ldT = 0;  // transposed copy of delta (tensor-core path), see EpiFwd
+  float *lo = nullptr;              // tf32_lo of delta (pre-split 3xTF32 consumers), see EpiFwd
   __device__ __forceinline__ float load(int m, int n) const { return SD[(int64_t)m * ld + n]; }
   __device__ __forceinline__ void store(int m, int n, float acc, float s) const {
-    SD[(int64_t)m * ld + n] = rnd ? tf32_rn(acc * s) : acc * s;
+    const float d = rnd ? tf32_rn(acc * s) : acc * s;
+    SD[(int64_t)m * ld + n] = d;
+    if (lo) lo[(int64_t)m * ld + n] = tf32_lo(d);
   }
   __device__ __forceinline__ void operator()(int m, int n, float acc) const {
     const float d = acc * load(m, n);
     SD[(int64_t)m * ld + n] = rnd ? tf32_rn(d) : d;
+    if (lo) lo[(int64_t)m * ld + n] = tf32_lo(d);
     if (bias) asm volatile("red.global.add.f32 [%0], %1;" ::"l"(bias + n), "f"(-bscale * d) : "memory");
   }
   __device__ __forceinline__ void strip(int m0, int mlim, int n, float *v) const {
@@ -170,6 +181,7 @@ struct EpiBwd {
         const float d = v[33 * r] * aux[r];
         const float dr = rnd ? tf32_rn(d) : d;
         SD[(int64_t)(m0 + r) * ld + n] = dr;
+        if (lo) lo[(int64_t)(m0 + r) * ld + n] = tf32_lo(dr);
         v[33 * r] = dr;
         sum += d;
       }
@@ -188,6 +200,7 @@ struct EpiGrad {
   float *W; float *b; int ldw; int nreal; float scale; int store_only;
   float *Wt = nullptr;
   float *T = nullptr; int ldT = 0;     // (unused)
+  float *Wlo = nullptr;                // fp32 mode: tf32_lo shadow of W (pre-split 3xTF32), see EpiFwd
   __device__ __forceinline__ float *at(int m, int n) const { return n < nreal ? W + (int64_t)m * ldw + n : b + m; }
   __device__ __forceinline__ float load(int m, int n) const { return store_only ? 0.0f : *at(m, n); }
   __device__ __forceinline__ void store(int m, int n, float acc, float w) const {
@@ -195,6 +208,7 @@ struct EpiGrad {
     const float w2 = w - scale * acc;
     *at(m, n) = w2;
     if (Wt && n < nreal) Wt[(int64_t)m * ldw + n] = tf32_rn(w2);
+    if (Wlo && n < nreal) Wlo[(int64_t)m * ldw + n] = tf32_lo(w2);
   }
   // one split-K term of the update: W[m][n] += -scale * acc as an L2 reduction (red, no return)
   // (store_only: the term itself, into a zeroed tendency block)

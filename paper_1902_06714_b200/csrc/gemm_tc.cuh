@@ -149,6 +149,8 @@ struct TileArgs {
   float *partial;      // non-null: write raw partials [z][M][N] (split-K) instead of epi
   int red;             // split-K with an additive epilogue (EpiGrad update): each split adds
                        // its own term straight into the output (red.global.add), no partials
+  int pre = 0;         // SPLIT = 3 with pre-split operands: the lo parts come from their own
+                       // tensor maps (written by the producers' epilogues), no in-smem splitting
 };
 
 // ---- the kernel ------------------------------------------------------------------------
@@ -157,7 +159,7 @@ struct TileArgs {
 template <int BN, bool A_MN, bool B_MN, int SPLIT, class Epi, int MAXST = 6, int EW = kEpiWarps>
 __global__ void __launch_bounds__(64 + 32 * EW, 1)
 gemm_tc_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB, TileArgs g,
-               Epi epi) {
+               Epi epi, const __grid_constant__ CUtensorMap tmAlo, const __grid_constant__ CUtensorMap tmBlo) {
   using C = Cfg<BN, SPLIT, MAXST, EW>;
   ptx::pdl_trigger();
   extern __shared__ uint8_t smem_raw[];
@@ -185,6 +187,10 @@ gemm_tc_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ 
     ptx::fence_mbar_init();
     ptx::prefetch_tensormap(&tmA);
     ptx::prefetch_tensormap(&tmB);
+    if (SPLIT == 3 && g.pre) {
+      ptx::prefetch_tensormap(&tmAlo);
+      ptx::prefetch_tensormap(&tmBlo);
+    }
   }
   if (warp == 1) {  // TMEM allocation (whole warp)
     asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;"
@@ -205,18 +211,24 @@ gemm_tc_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ 
         uint8_t *sa = smem + s * C::STAGE_BYTES;
         uint8_t *sb = sa + C::A_BYTES;
         const int k = kbeg + it * BK;
-        ptx::mbar_arrive_expect_tx(&full[s], (uint32_t)C::RAW_BYTES);
-        if (A_MN) {
+        const bool pre = SPLIT == 3 && g.pre;
+        ptx::mbar_arrive_expect_tx(&full[s], (uint32_t)(pre ? 2 * C::RAW_BYTES : C::RAW_BYTES));
+        // (pre: a second pass with the lo maps into the lo half of the stage)
+        for (int half = 0; half < (pre ? 2 : 1); ++half) {
+          const CUtensorMap *ma = half ? &tmAlo : &tmA, *mb = half ? &tmBlo : &tmB;
+          uint8_t *da = sa + half * C::RAW_BYTES, *db = sb + half * C::RAW_BYTES;
+          if (A_MN) {
 #pragma unroll
-          for (int i = 0; i < BM / 32; ++i) ptx::tma_load_2d(sa + i * 4096, &tmA, &full[s], m0 + 32 * i, k);
-        } else {
-          ptx::tma_load_2d(sa, &tmA, &full[s], k, m0);
-        }
-        if (B_MN) {
+            for (int i = 0; i < BM / 32; ++i) ptx::tma_load_2d(da + i * 4096, ma, &full[s], m0 + 32 * i, k);
+          } else {
+            ptx::tma_load_2d(da, ma, &full[s], k, m0);
+          }
+          if (B_MN) {
 #pragma unroll
-          for (int i = 0; i < BN / 32; ++i) ptx::tma_load_2d(sb + i * 4096, &tmB, &full[s], n0 + 32 * i, k);
-        } else {
-          ptx::tma_load_2d(sb, &tmB, &full[s], k, n0);
+            for (int i = 0; i < BN / 32; ++i) ptx::tma_load_2d(db + i * 4096, mb, &full[s], n0 + 32 * i, k);
+          } else {
+            ptx::tma_load_2d(db, mb, &full[s], k, n0);
+          }
         }
       }
     }
@@ -226,7 +238,7 @@ gemm_tc_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ 
       for (int it = 0; it < nkb; ++it) {
         const int s = it % C::STAGES;
         const uint32_t par = (uint32_t)((it / C::STAGES) & 1);
-        ptx::mbar_wait(SPLIT == 3 ? &conv[s] : &full[s], par);
+        ptx::mbar_wait((SPLIT == 3 && !g.pre) ? &conv[s] : &full[s], par);
         tc_fence_after();
         const uint32_t sa = ptx::smem_u32(smem + s * C::STAGE_BYTES);
         const uint32_t sb = sa + C::A_BYTES;
@@ -249,7 +261,7 @@ gemm_tc_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ 
     }
   } else {
     const int t = threadIdx.x - 64;  // 0 .. 32 EW - 1
-    if (SPLIT == 3) {  // ---- hi/lo splitters
+    if (SPLIT == 3 && !g.pre) {  // ---- hi/lo splitters
       for (int it = 0; it < nkb; ++it) {
         const int s = it % C::STAGES;
         ptx::mbar_wait(&full[s], (uint32_t)((it / C::STAGES) & 1));

@@ -116,6 +116,7 @@ struct TcOp {
   const float *p;
   int64_t ld;
   bool mn;
+  const float *lo = nullptr;  // fp32 mode: tf32_lo of the operand, same layout (pre-split 3xTF32)
 };
 
 bool tc_enabled() {
@@ -152,8 +153,19 @@ cudaError_t launch_tc(cudaStream_t st, int M, int N, int K, const TcOp &a, const
     cudaError_t e = set_max_smem(reinterpret_cast<const void *>(kern), C::SMEM);
     if (e != cudaSuccess) return e;
   }
-  CUtensorMap ta, tb;
+  CUtensorMap ta, tb, tal, tbl;
   if (!make_map(&ta, a, M, K, tc::BM) || !make_map(&tb, b, N, K, BN)) return cudaErrorInvalidValue;
+  // pre-split 3xTF32: both operands' lo parts written by their producers -> no in-smem splitting
+  static const bool presplit = getenv("NF_PRESPLIT") == nullptr || atoi(getenv("NF_PRESPLIT")) != 0;
+  const bool pre = SPLIT == 3 && presplit && a.lo && b.lo;
+  memset(&tal, 0, sizeof tal);
+  memset(&tbl, 0, sizeof tbl);
+  if (pre) {
+    TcOp al = a, bl = b;
+    al.p = a.lo;
+    bl.p = b.lo;
+    if (!make_map(&tal, al, M, K, tc::BM) || !make_map(&tbl, bl, N, K, BN)) return cudaErrorInvalidValue;
+  }
   const int tm = (M + tc::BM - 1) / tc::BM, tn = (N + BN - 1) / BN;
   const int tiles = tm * tn;
   const int nkb = (K + tc::BK - 1) / tc::BK;
@@ -189,14 +201,17 @@ cudaError_t launch_tc(cudaStream_t st, int M, int N, int K, const TcOp &a, const
       if (e != cudaSuccess) return e;
     }
   }
-  tc::TileArgs g{M, N, K, kbper * tc::BK, (splits > 1 && !red) ? ws.partial : nullptr, red ? 1 : 0};
-  g_note = note(epi_note(epi), red ? "splitk-red" : (splits > 1 ? "splitk-partial" : nullptr));
-  cudaError_t e = launch_k(kern, dim3(tn, tm, splits), dim3(C::THREADS), C::SMEM, st, ta, tb, g, epi);
+  tc::TileArgs g{M, N, K, kbper * tc::BK, (splits > 1 && !red) ? ws.partial : nullptr, red ? 1 : 0, pre ? 1 : 0};
+  g_note = note(epi_note(epi), red ? (pre ? "splitk-red presplit" : "splitk-red")
+                                    : (splits > 1 ? (pre ? "splitk-partial presplit" : "splitk-partial")
+                                                  : (pre ? "presplit" : nullptr)));
+  cudaError_t e = launch_k(kern, dim3(tn, tm, splits), dim3(C::THREADS), C::SMEM, st, ta, tb, g, epi, tal, tbl);
   if (e != cudaSuccess) return e;
-  if constexpr (Epi::kRed) {  // split-K terms went into W in L2: the TF32 shadow of W from the sum --
-    if (red && epi.Wt) {      // by the caller in one pass after the step when it asked to (ws.red_flag)
+  if constexpr (Epi::kRed) {  // split-K terms went into W in L2: the TF32 / lo shadow of W from the sum --
+    if (red && (epi.Wt || epi.Wlo)) {  // by the caller in one pass after the step when it asked to (ws.red_flag)
       if (ws.red_flag) *ws.red_flag = true;
-      else return round_tf32(st, epi.W, epi.Wt, (int64_t)M * epi.ldw);
+      else if (epi.Wt) return round_tf32(st, epi.W, epi.Wt, (int64_t)M * epi.ldw);
+      else return split_lo(st, epi.W, epi.Wlo, (int64_t)M * epi.ldw);
     }
   }
   if (splits > 1 && !red) {
@@ -463,6 +478,9 @@ bwd_smallk(const float *__restrict__ D, const float *__restrict__ W, int M, int 
       float4 dv = make_float4(acc.x * sv[u].x, acc.y * sv[u].y, acc.z * sv[u].z, acc.w * sv[u].w);
       if (epi.rnd) dv = make_float4(tf32_rn(dv.x), tf32_rn(dv.y), tf32_rn(dv.z), tf32_rn(dv.w));
       *reinterpret_cast<float4 *>(epi.SD + (int64_t)m * epi.ld + n) = dv;
+      if (epi.lo)
+        *reinterpret_cast<float4 *>(epi.lo + (int64_t)m * epi.ld + n) =
+            make_float4(tf32_lo(dv.x), tf32_lo(dv.y), tf32_lo(dv.z), tf32_lo(dv.w));
     }
   }
 }
@@ -570,7 +588,7 @@ __global__ void __launch_bounds__(256)
 out_layer_train(const float *__restrict__ A, float *__restrict__ S, const float *__restrict__ W,
                 const float *__restrict__ bias, const float *__restrict__ Y, float *__restrict__ AL,
                 float *__restrict__ DL, int n, int H, int nL, int act, int rows_per_block, float *__restrict__ part,
-                float *__restrict__ lpart, int rnd) {
+                float *__restrict__ lpart, int rnd, float *__restrict__ Dlo) {
   ptx::pdl_trigger();
   ptx::pdl_wait();
   __shared__ float lred[8];
@@ -644,6 +662,8 @@ out_layer_train(const float *__restrict__ A, float *__restrict__ S, const float 
         float4 d = make_float4(t0.x * sg.x, t0.y * sg.y, t1.x * sg.z, t1.y * sg.w);
         if (rnd) d = make_float4(tf32_rn(d.x), tf32_rn(d.y), tf32_rn(d.z), tf32_rn(d.w));  // a TC operand next
         srow[k4] = d;
+        if (Dlo)  // fp32 mode: its lo part for pre-split 3xTF32 consumers
+          reinterpret_cast<float4 *>(Dlo + (int64_t)m * H)[k4] = make_float4(tf32_lo(d.x), tf32_lo(d.y), tf32_lo(d.z), tf32_lo(d.w));
       }
     }
   }
@@ -709,6 +729,13 @@ __global__ void __launch_bounds__(256) round_tf32_kernel(const float *__restrict
   for (int64_t i = blockIdx.x * 256 + threadIdx.x; i < n; i += (int64_t)gridDim.x * 256) dst[i] = tf32_rn(src[i]);
 }
 
+__global__ void __launch_bounds__(256) split_lo_kernel(const float *__restrict__ src, float *__restrict__ dst,
+                                                        int64_t n) {
+  ptx::pdl_trigger();
+  ptx::pdl_wait();
+  for (int64_t i = blockIdx.x * 256 + threadIdx.x; i < n; i += (int64_t)gridDim.x * 256) dst[i] = tf32_lo(src[i]);
+}
+
 __global__ void __launch_bounds__(256) sgd_update_kernel(float *__restrict__ p, const float *__restrict__ g, int64_t n,
                                                          float scale) {
   ptx::pdl_trigger();
@@ -734,6 +761,12 @@ cudaError_t round_tf32(cudaStream_t st, const float *src, float *dst, int64_t n)
   if (n <= 0) return cudaSuccess;
   const int blocks = (int)std::min<int64_t>((n + 255) / 256, 8 * kSMs);
   return launch_k(round_tf32_kernel, dim3(blocks), dim3(256), 0, st, src, dst, n);
+}
+
+cudaError_t split_lo(cudaStream_t st, const float *src, float *dst, int64_t n) {
+  if (n <= 0) return cudaSuccess;
+  const int blocks = (int)std::min<int64_t>((n + 255) / 256, 8 * kSMs);
+  return launch_k(split_lo_kernel, dim3(blocks), dim3(256), 0, st, src, dst, n);
 }
 
 cudaError_t sgd_update(cudaStream_t st, float *p, const float *g, int64_t n, float scale) {
@@ -765,7 +798,7 @@ bool out_layer_fusable(int n, int H, int nL, const float *A, const float *S, con
 
 cudaError_t out_layer_train_fused(cudaStream_t st, int n, int H, int nL, const float *A, float *S, const float *W,
                                   const float *bias, const float *Y, float *AL, float *DL, int act, float *part,
-                                  int rnd) {
+                                  int rnd, float *Dlo) {
   const int R = out_layer_blocks(n, H);
   const int rpb = (n + R - 1) / R;
   const int blocks = (n + rpb - 1) / rpb;
@@ -780,21 +813,21 @@ cudaError_t out_layer_train_fused(cudaStream_t st, int n, int H, int nL, const f
   if (nL <= 10) {  // (MNIST-like 10-wide outputs: no idle unrolled output slots)
     if (H <= 512)
       return launch_k(out_layer_train<10, 4>, dim3(blocks), dim3(256), smem, st, A, S, W, bias, Y, AL, DL, n, H, nL,
-                      act, rpb, part, lp, rnd);
+                      act, rpb, part, lp, rnd, Dlo);
     if (H <= 1024)
       return launch_k(out_layer_train<10, 8>, dim3(blocks), dim3(256), smem, st, A, S, W, bias, Y, AL, DL, n, H, nL,
-                      act, rpb, part, lp, rnd);
+                      act, rpb, part, lp, rnd, Dlo);
     return launch_k(out_layer_train<10, 16>, dim3(blocks), dim3(256), smem, st, A, S, W, bias, Y, AL, DL, n, H, nL,
-                    act, rpb, part, lp, rnd);
+                    act, rpb, part, lp, rnd, Dlo);
   }
   if (H <= 512)
     return launch_k(out_layer_train<16, 4>, dim3(blocks), dim3(256), smem, st, A, S, W, bias, Y, AL, DL, n, H, nL,
-                    act, rpb, part, part + (int64_t)blocks * nL * (H + 1), rnd);
+                    act, rpb, part, part + (int64_t)blocks * nL * (H + 1), rnd, Dlo);
   if (H <= 1024)
     return launch_k(out_layer_train<16, 8>, dim3(blocks), dim3(256), smem, st, A, S, W, bias, Y, AL, DL, n, H, nL,
-                    act, rpb, part, part + (int64_t)blocks * nL * (H + 1), rnd);
+                    act, rpb, part, part + (int64_t)blocks * nL * (H + 1), rnd, Dlo);
   return launch_k(out_layer_train<16, 16>, dim3(blocks), dim3(256), smem, st, A, S, W, bias, Y, AL, DL, n, H, nL,
-                  act, rpb, part, part + (int64_t)blocks * nL * (H + 1), rnd);
+                  act, rpb, part, part + (int64_t)blocks * nL * (H + 1), rnd, Dlo);
 }
 
 cudaError_t out_layer_grad_final(cudaStream_t st, int n, int H, int nL, const float *part, const EpiGrad &epi,
@@ -808,8 +841,8 @@ cudaError_t out_layer_grad_final(cudaStream_t st, int n, int H, int nL, const fl
 }
 
 cudaError_t gemm_fwd(cudaStream_t st, int M, int N, int K, const float *A, const float *W,
-                     const EpiFwd &epi, const Workspace &ws, const float *Wtc) {
-  const TcOp a{A, K, false}, b{Wtc ? Wtc : W, K, false};
+                     const EpiFwd &epi, const Workspace &ws, const float *Wtc, const float *Alo, const float *Wlo) {
+  const TcOp a{A, K, false, Alo}, b{Wtc ? Wtc : W, K, false, Wlo};
   if (use_tc(M, N, K, a, b)) return run_tc<false, false>(st, M, N, K, a, b, epi, ws);
   g_last_engine = ENGINE_SIMT;
   if (N <= 16 && K % 4 == 0 && (size_t)N * K * 4 <= 96 * 1024 && tc_ok(a) && tc_ok(b) && M >= 256) {
@@ -855,8 +888,8 @@ bool gemm_bwd_tc(int M, int N, int K, const float *D, const float *W) {
 }
 
 cudaError_t gemm_bwd(cudaStream_t st, int M, int N, int K, const float *D, const float *W,
-                     const EpiBwd &epi, const Workspace &ws, const float *Wtc) {
-  const TcOp a{D, K, false}, b{Wtc ? Wtc : W, N, true};
+                     const EpiBwd &epi, const Workspace &ws, const float *Wtc, const float *Dlo, const float *Wlo) {
+  const TcOp a{D, K, false, Dlo}, b{Wtc ? Wtc : W, N, true, Wlo};
   if (use_tc(M, N, K, a, b)) return run_tc<false, true>(st, M, N, K, a, b, epi, ws);
   g_last_engine = ENGINE_SIMT;
   if (K <= 16 && N % 4 == 0 && epi.ld % 4 == 0 && (reinterpret_cast<uintptr_t>(W) & 15) == 0 &&
@@ -871,8 +904,8 @@ cudaError_t gemm_bwd(cudaStream_t st, int M, int N, int K, const float *D, const
 
 cudaError_t gemm_grad(cudaStream_t st, int M, int N, int K, const float *D, const float *Aprev,
                       const EpiGrad &epi, const Workspace &ws, bool bias_done, const float *DT,
-                      const float *AprevT) {
-  const TcOp a{D, M, true}, b{Aprev, N, true};
+                      const float *AprevT, const float *Dlo, const float *Aprevlo) {
+  const TcOp a{D, M, true, Dlo}, b{Aprev, N, true, Aprevlo};
   if (use_tc(M, N, K, a, b)) {
     // bias tendencies first (unless the delta GEMM's epilogue applied them): they read D only,
     // and the partial buffer is free again before the split-K GEMM uses it (same stream)

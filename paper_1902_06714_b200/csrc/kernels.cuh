@@ -39,11 +39,14 @@ Engine last_engine();
 // K1: Z = A[M][K] * W[N][K]^T, epilogue EpiFwd.
 // Wtc (NF_MATH_TF32, may be null): the TF32-rounded shadow of W, read by the tensor-core path
 // instead of W (the SIMT paths read W itself)
+// Alo / Wlo (fp32 mode, nullable): tf32_lo parts of the operands (pre-split 3xTF32 when both are given)
 cudaError_t gemm_fwd(cudaStream_t st, int M, int N, int K, const float *A, const float *W,
-                     const EpiFwd &epi, const Workspace &ws, const float *Wtc = nullptr);
+                     const EpiFwd &epi, const Workspace &ws, const float *Wtc = nullptr, const float *Alo = nullptr,
+                     const float *Wlo = nullptr);
 // K3: C[M][N] = D[M][K] * W[K][N], epilogue EpiBwd.
 cudaError_t gemm_bwd(cudaStream_t st, int M, int N, int K, const float *D, const float *W,
-                     const EpiBwd &epi, const Workspace &ws, const float *Wtc = nullptr);
+                     const EpiBwd &epi, const Workspace &ws, const float *Wtc = nullptr, const float *Dlo = nullptr,
+                     const float *Wlo = nullptr);
 // K4: C[M][N+1] = D^T (D is [K][M]) * [Aprev | 1] (Aprev is [K][N]), epilogue EpiGrad.
 // bias_done: the layer's bias update was already applied by the delta GEMM (EpiBwd::bias); only
 // meaningful on the tensor-core path (the SIMT path carries the bias as a ones column)
@@ -51,7 +54,7 @@ cudaError_t gemm_bwd(cudaStream_t st, int M, int N, int K, const float *D, const
 // epilogues, EpiBwd::T / EpiFwd::T) -- the tensor-core path then reads K-major operands
 cudaError_t gemm_grad(cudaStream_t st, int M, int N, int K, const float *D, const float *Aprev,
                       const EpiGrad &epi, const Workspace &ws, bool bias_done = false, const float *DT = nullptr,
-                      const float *AprevT = nullptr);
+                      const float *AprevT = nullptr, const float *Dlo = nullptr, const float *Aprevlo = nullptr);
 // whether gemm_fwd / gemm_bwd with these operands take the tensor-core path (where EpiFwd::T /
 // EpiBwd::T are honoured)
 bool gemm_fwd_tc(int M, int N, int K, const float *A, const float *W);
@@ -69,7 +72,8 @@ bool out_layer_fusable(int n, int H, int nL, const float *A, const float *S, con
 int out_layer_blocks(int n, int H);
 cudaError_t out_layer_train_fused(cudaStream_t st, int n, int H, int nL, const float *A, float *S, const float *W,
                                   const float *bias, const float *Y, float *AL, float *DL, int act, float *part,
-                                  int rnd = 0);  // rnd: delta_{L-1} stored TF32-rounded (NF_MATH_TF32)
+                                  int rnd = 0,   // rnd: delta_{L-1} stored TF32-rounded (NF_MATH_TF32)
+                                  float *Dlo = nullptr);  // fp32 mode: tf32_lo of delta_{L-1}
 // step_loss (nullable): also writes the step's mean cost from the kernel's per-block partials
 cudaError_t out_layer_grad_final(cudaStream_t st, int n, int H, int nL, const float *part, const EpiGrad &epi,
                                  float *step_loss = nullptr);
@@ -84,6 +88,8 @@ int loss_acc_parts();
 cudaError_t sgd_update(cudaStream_t st, float *p, const float *g, int64_t n, float scale);
 // dst[i] = tf32_rn(src[i]): the TF32 weight shadow of NF_MATH_TF32
 cudaError_t round_tf32(cudaStream_t st, const float *src, float *dst, int64_t n);
+// dst[i] = tf32_lo(src[i]): the lo shadow of the fp32 mode's pre-split 3xTF32
+cudaError_t split_lo(cudaStream_t st, const float *src, float *dst, int64_t n);
 // copies m <= 64 contiguous runs of len floats, src + off[s] -> dst + s * len (src: device
 // memory or mapped pinned host memory; the e2e staging of the per-step target rows)
 cudaError_t gather_steps(cudaStream_t st, const float *src, const int64_t *off, int m, int64_t len, float *dst);

@@ -132,6 +132,14 @@ __device__ __forceinline__ void store_t(float *T, int ldT, int m0, int mlim, int
   for (int c = 0; c < cols; ++c) T[(int64_t)(nc + c) * ldT + m0 + lane] = buf[lane * 33 + c];
 }
 
+// The lo part of x for pre-split 3xTF32 (reading R13): the tensor core reads x itself as the hi
+// operand (it keeps the TF32 bits, i.e. truncates), so lo = rn_tf32(x - trunc_tf32(x)) (the
+// difference is exact in fp32, |lo| <= 2^-10 |x|).  hi*hi + hi*lo + lo*hi then errs by the dropped
+// lo*lo (<= 2^-20 relative) and lo's rounding (<= 2^-22).
+__device__ __forceinline__ float tf32_lo(float x) {
+  return tf32_rn(x - __uint_as_float(__float_as_uint(x) & 0xffffe000u));
+}
+
 __device__ __forceinline__ float warp_sum(float v) {
 #pragma unroll
   for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
