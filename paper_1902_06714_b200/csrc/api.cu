@@ -114,10 +114,10 @@ struct nf_net {
   // NF_MATH_FP32 with pre-split 3xTF32 (NF_PRESPLIT, default on): tf32_lo of every tensor-core
   // operand, written by its producer -- the weights' lo shadow (kept by the SGD epilogue like
   // params_t), the hidden activations' and deltas' lo arrays (stash_lo), the input rows' (xlo)
-  float *params_lo = nullptr;
+  float *params_lo = nullptr;             // (with params_t = tf32_rn(W) as the weights' hi)
   bool lo_ok = false;
   DevBuf stash_lo, xlo;
-  std::vector<float *> Alo, Dlo;
+  std::vector<float *> Ahi, Alo, Dlo;     // index 0: the input rows
   int64_t lo_rows = 0;
   std::vector<int64_t> offW, offB;       // index 1..L
   // stash: A_l (activations) and S_l (sigma'(Z_l), overwritten by delta_l), l = 1..L
@@ -274,26 +274,31 @@ int ensure_shadow(nf_net *net) {
 int ensure_lo(nf_net *net, int64_t rows) {
   if (!net->presplit()) return NF_OK;
   if (!net->params_lo) NF_CUDA(cudaMalloc(&net->params_lo, net->nparams * sizeof(float)));
-  if (!net->lo_ok) {
-    NF_CUDA(split_lo(net->stream, net->params, net->params_lo, net->nparams));
+  if (!net->params_t) NF_CUDA(cudaMalloc(&net->params_t, net->nparams * sizeof(float)));
+  if (!net->lo_ok) {  // the weights' RN split: hi in params_t, lo in params_lo
+    NF_CUDA(split_rn(net->stream, net->params, net->params_t, net->params_lo, net->nparams));
     net->lo_ok = true;
   }
   if (rows > net->lo_rows) {
     cudaStreamCaptureStatus cs = cudaStreamCaptureStatusNone;
     cudaStreamIsCapturing(net->stream, &cs);
     if (cs != cudaStreamCaptureStatusNone) return fail(NF_ECUDA, "lo arrays must be sized before a graph capture");
-    int64_t per_row = net->dims[0];
-    for (int l = 1; l <= net->L; ++l) per_row += 2 * (int64_t)net->dims[l];
+    auto blk = [&](int w) { return (rows * w + 31) / 32 * 32; };  // 128-B aligned arrays (TMA, float4)
+    int64_t total = 2 * blk(net->dims[0]);
+    for (int l = 1; l <= net->L; ++l) total += 3 * blk(net->dims[l]);
     NF_CUDA(cudaStreamSynchronize(net->stream));
     drop_graph(net);
-    NF_CUDA(net->stash_lo.ensure((size_t)(per_row * rows) * sizeof(float)));
+    NF_CUDA(net->stash_lo.ensure((size_t)total * sizeof(float)));
     float *p = net->stash_lo.as<float>();
+    net->Ahi.assign(net->L + 1, nullptr);
     net->Alo.assign(net->L + 1, nullptr);
     net->Dlo.assign(net->L + 1, nullptr);
-    net->Alo[0] = p; p += rows * net->dims[0];  // the input rows' lo (xlo)
+    net->Ahi[0] = p; p += blk(net->dims[0]);  // the input rows' RN split
+    net->Alo[0] = p; p += blk(net->dims[0]);
     for (int l = 1; l <= net->L; ++l) {
-      net->Alo[l] = p; p += rows * net->dims[l];
-      net->Dlo[l] = p; p += rows * net->dims[l];
+      net->Ahi[l] = p; p += blk(net->dims[l]);
+      net->Alo[l] = p; p += blk(net->dims[l]);
+      net->Dlo[l] = p; p += blk(net->dims[l]);
     }
     net->lo_rows = rows;
   }
@@ -311,7 +316,7 @@ int forward(nf_net *net, const float *x, const float *y, int64_t n, int mode) {
   const bool lo = mode == 0 && net->presplit();
   if (lo) {
     if (int rc = ensure_lo(net, n)) return rc;
-    NF_CUDA(split_lo(net->stream, x, net->Alo[0], n * net->dims[0]));
+    NF_CUDA(split_rn(net->stream, x, net->Ahi[0], net->Alo[0], n * net->dims[0]));
   }
   net->out_fused = mode == 0 && L >= 2 &&
                    out_layer_fusable((int)n, net->dims[L - 1], net->dims[L], net->A[L - 1], net->S[L - 1], net->W(L));
@@ -328,9 +333,13 @@ int forward(nf_net *net, const float *x, const float *y, int64_t n, int mode) {
     EpiFwd epi{net->b(l), net->A[l], net->S[l], y, net->dims[l], net->act(l), lm, (t && (lm == 1 || l < L)) ? 1 : 0};
     if (lm == 0 && tposed(net, l + 1)) { epi.T = net->AT[l]; epi.ldT = (int)n; }   // A_l^T for K4(l+1)
     if (lm == 1 && tposed(net, l)) { epi.T = net->DT[l]; epi.ldT = (int)n; }       // delta_L^T for K4(L)
-    if (lo) epi.lo = lm == 0 ? net->Alo[l] : net->Dlo[l];
+    if (lo) {
+      epi.lo = lm == 0 ? net->Alo[l] : net->Dlo[l];
+      epi.hi = lm == 0 ? net->Ahi[l] : nullptr;
+    }
     NF_CUDA(gemm_fwd(net->stream, (int)n, net->dims[l], net->dims[l - 1], in, net->W(l), epi, net->ws,
-                     t ? net->Wt(l) : nullptr, lo ? net->Alo[l - 1] : nullptr, lo ? net->Wlo(l) : nullptr));
+                     (t || lo) ? net->Wt(l) : nullptr, lo ? net->Alo[l - 1] : nullptr, lo ? net->Wlo(l) : nullptr,
+                     lo ? net->Ahi[l - 1] : nullptr));
     in = net->A[l];
   }
   return NF_OK;
@@ -392,7 +401,7 @@ int backward(nf_net *net, const float *x, int64_t n, float eta, float *grad, flo
         eb.bscale = scale;
         bias_done[l - 1] = 1;
       }
-      NF_CUDA(gemm_bwd(main_st, (int)n, nk, nl, net->S[l], net->W(l), eb, net->ws, t ? net->Wt(l) : nullptr,
+      NF_CUDA(gemm_bwd(main_st, (int)n, nk, nl, net->S[l], net->W(l), eb, net->ws, (t || lo) ? net->Wt(l) : nullptr,
                        lo ? net->Dlo[l] : nullptr, lo ? net->Wlo(l) : nullptr));
     }
     NF_CUDA(cudaEventRecord(net->ev[l], main_st));  // K3(l) done with W_l and delta_l is final
@@ -401,7 +410,10 @@ int backward(nf_net *net, const float *x, int64_t n, float eta, float *grad, flo
     EpiGrad eg = grad ? EpiGrad{grad + net->offW[l], grad + net->offB[l], nk, nk, 0.0f, 1}
                       : EpiGrad{net->W(l), net->b(l), nk, nk, scale, 0};
     if (!grad && t) eg.Wt = net->Wt(l);  // the update also refreshes the TF32 shadow of W_l
-    if (!grad && lo) eg.Wlo = net->Wlo(l);  // ... or the lo shadow (fp32 mode)
+    if (!grad && lo) {  // ... or the RN split of W_l (fp32 mode)
+      eg.Wt = net->Wt(l);
+      eg.Wlo = net->Wlo(l);
+    }
     cudaStream_t kst = side;  // the stream layer l's tendencies are produced on
     if (fused) NF_CUDA(out_layer_grad_final(side, (int)n, nk, nl, net->part_out.as<float>(), eg, step_loss));
     else if (l == 1 && net->L > 1 && side != main_st && (net->math != NF_MATH_TF32 || n <= 2048)) {
@@ -409,11 +421,11 @@ int backward(nf_net *net, const float *x, int64_t n, float eta, float *grad, flo
       // stream (c4 134 -> 130 us, 3xTF32 c3 462 -> 445 us; c3's 1xTF32 pair contends: 154 -> 157)
       NF_CUDA(gemm_grad(main_st, nl, nk, (int)n, net->S[l], aprev, eg, net->ws, bias_done[l] != 0,
                         tposed(net, l) ? net->DT[l] : nullptr, tposed(net, l) && l > 1 ? net->AT[l - 1] : nullptr,
-                        lo ? net->Dlo[l] : nullptr, lo ? net->Alo[l - 1] : nullptr));
+                        lo ? net->Dlo[l] : nullptr, lo ? net->Alo[l - 1] : nullptr, lo ? net->Ahi[l - 1] : nullptr));
       kst = main_st;
     } else NF_CUDA(gemm_grad(side, nl, nk, (int)n, net->S[l], aprev, eg, net->ws2, bias_done[l] != 0,
                              tposed(net, l) ? net->DT[l] : nullptr, tposed(net, l) && l > 1 ? net->AT[l - 1] : nullptr,
-                             lo ? net->Dlo[l] : nullptr, lo ? net->Alo[l - 1] : nullptr));
+                             lo ? net->Dlo[l] : nullptr, lo ? net->Alo[l - 1] : nullptr, lo ? net->Ahi[l - 1] : nullptr));
     if (layer_done && layer_done[l - 1]) NF_CUDA(cudaEventRecord(layer_done[l - 1], kst));  // nf_grad_layers
   }
   NF_CUDA(cudaEventRecord(net->ev[net->L + 1], side));  // join
@@ -421,7 +433,7 @@ int backward(nf_net *net, const float *x, int64_t n, float eta, float *grad, flo
   net->ws.red_flag = net->ws2.red_flag = nullptr;
   if (net->red_round) {
     if (net->tf32()) NF_CUDA(round_tf32(main_st, net->params, net->params_t, net->nparams));
-    else NF_CUDA(split_lo(main_st, net->params, net->params_lo, net->nparams));
+    else NF_CUDA(split_rn(main_st, net->params, net->params_t, net->params_lo, net->nparams));
   }
   return NF_OK;
 }
@@ -935,8 +947,10 @@ static int train_steps_device(nf_net *net, const float *dX, const float *dY, int
   }
   int rc = net->math == NF_MATH_FP64 ? FUSED_NOT_APPLICABLE : fused_small_train_steps(net->fused, net->stream, net->dims, net->act_h, net->act_o,
                                    net->params, dX, dY, dN, batch, st.data(), n_steps, eta, step_loss);
-  if (rc == 0) net->shadow_ok = false;
-  net->lo_ok = false;  // K6 updated params
+  if (rc == 0) {  // K6 updated params
+    net->shadow_ok = false;
+    net->lo_ok = false;
+  }
   if (rc == FUSED_NOT_APPLICABLE) {
     // Generic nets: the per-step kernel sequence of all n_steps, captured once as a CUDA
     // graph and replayed while the arguments repeat (removes the host launch gaps between the

@@ -47,9 +47,11 @@ struct EpiFwd {
   static constexpr bool kHasT = true;
   const float *bias; float *A; float *S; const float *Y; int ld; int act; int mode; int rnd = 0;
   float *T = nullptr; int ldT = 0;
-  // lo (fp32 mode, pre-split 3xTF32 consumers): tf32_lo of the stored operand value -- A for a
-  // hidden layer, delta_L for the output layer -- [rows][ld] like A
+  // lo / hi (fp32 mode, pre-split 3xTF32 consumers, [rows][ld] like A): a hidden layer's A as the
+  // RN split (hi = tf32_rn(A), lo = tf32_lo_rn(A)); the output layer's delta_L as the truncation
+  // split (lo only: tf32_lo(delta_L))
   float *lo = nullptr;
+  float *hi = nullptr;
   __device__ __forceinline__ float load(int m, int n) const {
     return mode == 1 ? Y[(int64_t)m * ld + n] : 0.0f;
   }
@@ -62,7 +64,10 @@ struct EpiFwd {
     A[i] = (rnd && mode == 0) ? tf32_rn(a) : a;
     const float sv = mode == 0 ? s : (rnd ? tf32_rn((a - y) * s) : (a - y) * s);
     S[i] = sv;
-    if (lo) lo[i] = tf32_lo(mode == 0 ? a : sv);
+    if (lo) {
+      if (mode == 0) { hi[i] = tf32_rn(a); lo[i] = tf32_lo_rn(a); }
+      else lo[i] = tf32_lo(sv);
+    }
   }
   __device__ __forceinline__ void operator()(int m, int n, float acc) const { store(m, n, acc, load(m, n)); }
 
@@ -104,7 +109,7 @@ struct EpiFwd {
             if (lo) lo[i] = tf32_lo(d);
           } else {
             v[33 * (r0 + u)] = av;
-            if (MODE == 0 && lo) lo[i] = tf32_lo(av);
+            if (MODE == 0 && lo) { hi[i] = tf32_rn(av); lo[i] = tf32_lo_rn(av); }
           }
         }
       }
@@ -200,7 +205,7 @@ struct EpiGrad {
   float *W; float *b; int ldw; int nreal; float scale; int store_only;
   float *Wt = nullptr;
   float *T = nullptr; int ldT = 0;     // (unused)
-  float *Wlo = nullptr;                // fp32 mode: tf32_lo shadow of W (pre-split 3xTF32), see EpiFwd
+  float *Wlo = nullptr;                // fp32 mode: tf32_lo_rn shadow of W (with Wt = its hi), see EpiFwd
   __device__ __forceinline__ float *at(int m, int n) const { return n < nreal ? W + (int64_t)m * ldw + n : b + m; }
   __device__ __forceinline__ float load(int m, int n) const { return store_only ? 0.0f : *at(m, n); }
   __device__ __forceinline__ void store(int m, int n, float acc, float w) const {
@@ -208,7 +213,7 @@ struct EpiGrad {
     const float w2 = w - scale * acc;
     *at(m, n) = w2;
     if (Wt && n < nreal) Wt[(int64_t)m * ldw + n] = tf32_rn(w2);
-    if (Wlo && n < nreal) Wlo[(int64_t)m * ldw + n] = tf32_lo(w2);
+    if (Wlo && n < nreal) Wlo[(int64_t)m * ldw + n] = tf32_lo_rn(w2);
   }
   // one split-K term of the update: W[m][n] += -scale * acc as an L2 reduction (red, no return)
   // (store_only: the term itself, into a zeroed tendency block)

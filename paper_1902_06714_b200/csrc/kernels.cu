@@ -210,8 +210,8 @@ cudaError_t launch_tc(cudaStream_t st, int M, int N, int K, const TcOp &a, const
   if constexpr (Epi::kRed) {  // split-K terms went into W in L2: the TF32 / lo shadow of W from the sum --
     if (red && (epi.Wt || epi.Wlo)) {  // by the caller in one pass after the step when it asked to (ws.red_flag)
       if (ws.red_flag) *ws.red_flag = true;
-      else if (epi.Wt) return round_tf32(st, epi.W, epi.Wt, (int64_t)M * epi.ldw);
-      else return split_lo(st, epi.W, epi.Wlo, (int64_t)M * epi.ldw);
+      else if (epi.Wlo) return split_rn(st, epi.W, epi.Wt, epi.Wlo, (int64_t)M * epi.ldw);
+      else return round_tf32(st, epi.W, epi.Wt, (int64_t)M * epi.ldw);
     }
   }
   if (splits > 1 && !red) {
@@ -736,6 +736,17 @@ __global__ void __launch_bounds__(256) split_lo_kernel(const float *__restrict__
   for (int64_t i = blockIdx.x * 256 + threadIdx.x; i < n; i += (int64_t)gridDim.x * 256) dst[i] = tf32_lo(src[i]);
 }
 
+__global__ void __launch_bounds__(256) split_rn_kernel(const float *__restrict__ src, float *__restrict__ hi,
+                                                        float *__restrict__ lo, int64_t n) {
+  ptx::pdl_trigger();
+  ptx::pdl_wait();
+  for (int64_t i = blockIdx.x * 256 + threadIdx.x; i < n; i += (int64_t)gridDim.x * 256) {
+    const float x = src[i];
+    hi[i] = tf32_rn(x);
+    lo[i] = tf32_lo_rn(x);
+  }
+}
+
 __global__ void __launch_bounds__(256) sgd_update_kernel(float *__restrict__ p, const float *__restrict__ g, int64_t n,
                                                          float scale) {
   ptx::pdl_trigger();
@@ -767,6 +778,12 @@ cudaError_t split_lo(cudaStream_t st, const float *src, float *dst, int64_t n) {
   if (n <= 0) return cudaSuccess;
   const int blocks = (int)std::min<int64_t>((n + 255) / 256, 8 * kSMs);
   return launch_k(split_lo_kernel, dim3(blocks), dim3(256), 0, st, src, dst, n);
+}
+
+cudaError_t split_rn(cudaStream_t st, const float *src, float *hi, float *lo, int64_t n) {
+  if (n <= 0) return cudaSuccess;
+  const int blocks = (int)std::min<int64_t>((n + 255) / 256, 8 * kSMs);
+  return launch_k(split_rn_kernel, dim3(blocks), dim3(256), 0, st, src, hi, lo, n);
 }
 
 cudaError_t sgd_update(cudaStream_t st, float *p, const float *g, int64_t n, float scale) {
@@ -841,8 +858,9 @@ cudaError_t out_layer_grad_final(cudaStream_t st, int n, int H, int nL, const fl
 }
 
 cudaError_t gemm_fwd(cudaStream_t st, int M, int N, int K, const float *A, const float *W,
-                     const EpiFwd &epi, const Workspace &ws, const float *Wtc, const float *Alo, const float *Wlo) {
-  const TcOp a{A, K, false, Alo}, b{Wtc ? Wtc : W, K, false, Wlo};
+                     const EpiFwd &epi, const Workspace &ws, const float *Wtc, const float *Alo, const float *Wlo,
+                     const float *Ahi) {
+  const TcOp a{Ahi ? Ahi : A, K, false, Alo}, b{Wtc ? Wtc : W, K, false, Wlo};
   if (use_tc(M, N, K, a, b)) return run_tc<false, false>(st, M, N, K, a, b, epi, ws);
   g_last_engine = ENGINE_SIMT;
   if (N <= 16 && K % 4 == 0 && (size_t)N * K * 4 <= 96 * 1024 && tc_ok(a) && tc_ok(b) && M >= 256) {
@@ -904,8 +922,8 @@ cudaError_t gemm_bwd(cudaStream_t st, int M, int N, int K, const float *D, const
 
 cudaError_t gemm_grad(cudaStream_t st, int M, int N, int K, const float *D, const float *Aprev,
                       const EpiGrad &epi, const Workspace &ws, bool bias_done, const float *DT,
-                      const float *AprevT, const float *Dlo, const float *Aprevlo) {
-  const TcOp a{D, M, true, Dlo}, b{Aprev, N, true, Aprevlo};
+                      const float *AprevT, const float *Dlo, const float *Aprevlo, const float *Aprevhi) {
+  const TcOp a{D, M, true, Dlo}, b{Aprevhi ? Aprevhi : Aprev, N, true, Aprevlo};
   if (use_tc(M, N, K, a, b)) {
     // bias tendencies first (unless the delta GEMM's epilogue applied them): they read D only,
     // and the partial buffer is free again before the split-K GEMM uses it (same stream)

@@ -42,7 +42,7 @@ Engine last_engine();
 // Alo / Wlo (fp32 mode, nullable): tf32_lo parts of the operands (pre-split 3xTF32 when both are given)
 cudaError_t gemm_fwd(cudaStream_t st, int M, int N, int K, const float *A, const float *W,
                      const EpiFwd &epi, const Workspace &ws, const float *Wtc = nullptr, const float *Alo = nullptr,
-                     const float *Wlo = nullptr);
+                     const float *Wlo = nullptr, const float *Ahi = nullptr);
 // K3: C[M][N] = D[M][K] * W[K][N], epilogue EpiBwd.
 cudaError_t gemm_bwd(cudaStream_t st, int M, int N, int K, const float *D, const float *W,
                      const EpiBwd &epi, const Workspace &ws, const float *Wtc = nullptr, const float *Dlo = nullptr,
@@ -54,7 +54,8 @@ cudaError_t gemm_bwd(cudaStream_t st, int M, int N, int K, const float *D, const
 // epilogues, EpiBwd::T / EpiFwd::T) -- the tensor-core path then reads K-major operands
 cudaError_t gemm_grad(cudaStream_t st, int M, int N, int K, const float *D, const float *Aprev,
                       const EpiGrad &epi, const Workspace &ws, bool bias_done = false, const float *DT = nullptr,
-                      const float *AprevT = nullptr, const float *Dlo = nullptr, const float *Aprevlo = nullptr);
+                      const float *AprevT = nullptr, const float *Dlo = nullptr, const float *Aprevlo = nullptr,
+                      const float *Aprevhi = nullptr);
 // whether gemm_fwd / gemm_bwd with these operands take the tensor-core path (where EpiFwd::T /
 // EpiBwd::T are honoured)
 bool gemm_fwd_tc(int M, int N, int K, const float *A, const float *W);
@@ -88,8 +89,10 @@ int loss_acc_parts();
 cudaError_t sgd_update(cudaStream_t st, float *p, const float *g, int64_t n, float scale);
 // dst[i] = tf32_rn(src[i]): the TF32 weight shadow of NF_MATH_TF32
 cudaError_t round_tf32(cudaStream_t st, const float *src, float *dst, int64_t n);
-// dst[i] = tf32_lo(src[i]): the lo shadow of the fp32 mode's pre-split 3xTF32
+// dst[i] = tf32_lo(src[i]): the truncation split of the fp32 mode's pre-split 3xTF32
 cudaError_t split_lo(cudaStream_t st, const float *src, float *dst, int64_t n);
+// hi[i] = tf32_rn(src[i]), lo[i] = tf32_lo_rn(src[i]): the RN split (weights, input rows)
+cudaError_t split_rn(cudaStream_t st, const float *src, float *hi, float *lo, int64_t n);
 // copies m <= 64 contiguous runs of len floats, src + off[s] -> dst + s * len (src: device
 // memory or mapped pinned host memory; the e2e staging of the per-step target rows)
 cudaError_t gather_steps(cudaStream_t st, const float *src, const int64_t *off, int m, int64_t len, float *dst);

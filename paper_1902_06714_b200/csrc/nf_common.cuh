@@ -132,13 +132,18 @@ __device__ __forceinline__ void store_t(float *T, int ldT, int m0, int mlim, int
   for (int c = 0; c < cols; ++c) T[(int64_t)(nc + c) * ldT + m0 + lane] = buf[lane * 33 + c];
 }
 
-// The lo part of x for pre-split 3xTF32 (reading R13): the tensor core reads x itself as the hi
-// operand (it keeps the TF32 bits, i.e. truncates), so lo = rn_tf32(x - trunc_tf32(x)) (the
-// difference is exact in fp32, |lo| <= 2^-10 |x|).  hi*hi + hi*lo + lo*hi then errs by the dropped
-// lo*lo (<= 2^-20 relative) and lo's rounding (<= 2^-22).
-__device__ __forceinline__ float tf32_lo(float x) {
+// Pre-split 3xTF32 (reading R13): every tensor-core operand x reaches the MMA as hi + lo.
+//  * RN split (activations, weights): hi = tf32_rn(x) is stored as its own array, lo = tf32_rn(x - hi)
+//    (x - hi exact in fp32, |lo| <= 2^-11 |x|): the dropped lo*lo is <= 2^-22 relative and of either
+//    sign.
+//  * truncation split (deltas): the tensor core reads x itself as hi, i.e. its truncated TF32 bits,
+//    and lo = tf32_rn(x - trunc(x)) (|lo| < 2^-10 |x|, the sign of x).  Its lo*lo term alone would
+//    be biased (same sign as the product), so every contraction pairs a truncation-split operand
+//    with an RN-split one: the dropped lo_a*lo_b then has zero mean.
+__device__ __forceinline__ float tf32_lo(float x) {  // truncation split
   return tf32_rn(x - __uint_as_float(__float_as_uint(x) & 0xffffe000u));
 }
+__device__ __forceinline__ float tf32_lo_rn(float x) { return tf32_rn(x - tf32_rn(x)); }  // RN split
 
 __device__ __forceinline__ float warp_sum(float v) {
 #pragma unroll
