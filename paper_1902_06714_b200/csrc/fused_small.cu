@@ -28,6 +28,13 @@
 //       P8  ONE bulk copy of the reduced slice (+ the W2/b block) back into shared memory
 //       P9  W -= (eta/B) G on the resident parameters; zero this CTA's share of the
 //           accumulator used two steps ahead
+//
+// Contraction engines of P1 / P5 (template MM, chosen per launch): packed FFMA2 SIMT (default), or
+// the warp-level tensor-core MMA (mma.sync m16n8k8 TF32, 3xTF32 = hi*hi + hi*lo + lo*hi, fp32
+// accumulate; NF_FUSED_MM=1).  HMMA runs 511 MAC/clk/SM at ~21 cycles latency with register
+// operands, while tcgen05's issue -> commit -> mbarrier round trip alone is 1.3-3 K cycles at these
+// 128 x 32 shapes (profiles/r02_micro_small_mma_launch.txt); but 3xTF32 needs three HMMAs per
+// product and the m16 / k8 tiles pad config 2's 67 rows x 100 pixels, so MM measured no faster.
 #include <algorithm>
 #include <cstdio>
 #include <cstdlib>
@@ -84,10 +91,20 @@ constexpr int kSlots = 4;             // accumulator ring: step s uses slot s % 
 
 // Batch starts of calls with few steps travel in the launch's parameter buffer (no staging copy,
 // no event: ~8 us of host time per call), longer runs through a device array.
+// The parameter buffer's size costs host time per launch (32 B: 3.0 us, 8 KB: 6.0 us;
+// profiles/r02_micro_small_mma_launch.txt): calls of <= 32 steps use the small variant.
+constexpr int kInlineSmall = 32;
 constexpr int kInlineStarts = 1024;
+template <int NI>
 struct InlineStarts {
-  int64_t v[kInlineStarts];
+  int64_t v[NI];
 };
+// MM variant geometry: P1 m-tiles of 16 rows (<= kMT1), P5 m-tiles / W fragment blocks of 16 pixels
+constexpr int kMT1 = 8;        // rows per cluster <= 128 (m-tiles mg, mg + 4 per warp)
+constexpr int kMJ = 8;         // pixel slice <= 128
+constexpr int kDS = 36;        // delta_1 row stride (floats) in the MM variant: conflict-free B fragments
+__host__ __device__ inline int mm_rows(int nSmax) { return (nSmax + 15) / 16 * 16; }
+__host__ __device__ inline int mm_nj(int wpad) { return (wpad + 15) / 16; }
 
 struct FusedParams {
   int n0, H, O;          // dims
@@ -101,6 +118,7 @@ struct FusedParams {
   int64_t slot;          // accumulator slot stride (floats, multiple of 32)
   int64_t small_off;     // offset of the W2/b1/b2 block inside a slot
   int nsmp;              // W2/b1/b2 block length O*H + H + O, rounded up to a multiple of 4
+  int gsl;               // floats of one rank's dW1 slice in an accumulator slot
   float scale;           // eta / B
   float inv_B;
   const float *X, *Y;
@@ -116,6 +134,10 @@ struct FusedParams {
 
 #define PROF(i) \
   if (p.prof && threadIdx.x == 0 && s < 64) p.prof[((int64_t)blockIdx.x * 64 + s) * kProf + (i)] = clock64()
+// latest arrival over the CTA's warps (lane 0 of each)
+#define PROF_MAX(i) \
+  if (p.prof && (threadIdx.x & 31) == 0 && s < 64) \
+    atomicMax(reinterpret_cast<unsigned long long *>(&p.prof[((int64_t)blockIdx.x * 64 + s) * kProf + (i)]), (unsigned long long)clock64())
 
 __device__ __forceinline__ int row_begin(int g, int B, int G) { return (int)(((int64_t)g * B) / G); }
 __host__ __device__ __forceinline__ int own_begin(int c, int nS, int C) { return (c * nS) / C; }
@@ -137,26 +159,31 @@ __host__ __device__ inline int al32(int v) { return (v + 31) & ~31; }  // 128-B 
 
 __host__ __device__ inline int xrows(int nSmax) { return (nSmax + kRG - 1) / kRG * kRG; }
 
-__host__ __device__ inline Smem smem_layout(int wpad, int nSmax, int nOwnMax, int C, bool tc) {
+__host__ __device__ inline Smem smem_layout(int wpad, int nSmax, int nOwnMax, int C, bool tc, bool mm) {
   Smem L;
+  const int nj = mm_nj(wpad);
+  const int xr = mm ? mm_rows(nSmax) : xrows(nSmax);  // x rows staged (MM: whole 16-row m-tiles)
   int o = 32;  // mbarriers (and the TMEM address) live in the first 128 B
   L.tcr = o;   o = al32(o + (tc ? (kTcBytes + 1024) / 4 : 0));  // TC operand tiles (1024-B aligned inside)
-  L.W1t = o;   o = al32(o + (tc ? 0 : wpad * 32));  // [wpad][32]: W1 slice, k-major (SIMT variant)
+  // W1 slice: SIMT [wpad][32] k-major; MM fragment order hi | lo ([j][nb][lane][4] each)
+  L.W1t = o;   o = al32(o + (tc ? 0 : mm ? 2 * nj * 512 : wpad * 32));
   L.W2s = o;   o = al32(o + 32 * 33);              // [32][33]
   L.b1s = o;   o += 32;
   L.b2s = o;   o = al32(o + 32);
-  L.xs = o;    o = al32(o + (tc ? 0 : 2 * al32(xrows(nSmax) * wpad)));  // 2 TMA destinations (SIMT)
+  // 2 TMA destinations (SIMT / MM); MM reads up to 28 floats past a buffer's last row
+  L.xs = o;    o = al32(o + (tc ? 0 : 2 * al32(xr * wpad + (mm ? 32 : 0))));
   L.ys = o;    o = al32(o + 2 * nOwnMax * 32);
-  L.Ppart = o; o = al32(o + (tc ? 1 : kKP) * xrows(nSmax) * 32);  // P1 K-part partials; part 0 = Pfull
+  // P1 K-part partials (SIMT: part 0 = Pfull; MM: Pfull [rows][32] only)
+  L.Ppart = o; o = al32(o + (tc ? xrows(nSmax) * 32 : mm ? xr * 32 : kKP * xrows(nSmax) * 32));
   L.Pown = o;  o = al32(o + C * nOwnMax * 32);
-  L.D1 = o;    o = al32(o + nSmax * 32);
+  L.D1 = o;    o = al32(o + (mm ? ((nSmax + 7) / 8 * 8) * kDS : nSmax * 32));
   L.A1own = o; o = al32(o + nOwnMax * 32);         // a1 of the owned rows
   L.D2own = o; o = al32(o + nOwnMax * 32);         // delta_2 of the owned rows
   L.gpart = o; o = al32(o + kSmall);
   L.grecv = o; o = al32(o + C * e_slot(C));
-  L.Gs = o;    o = al32(o + wpad * 32);            // [wpad][32]: dW1 slice partial, k-major like W1t
-  L.Gs2 = o;   o = al32(o + (tc ? 0 : wpad * 32)); // second row-half partial (SIMT)
-  L.Gr = o;    o = al32(o + wpad * 32);            // reduced slice read back
+  L.Gs = o;    o = al32(o + (mm ? nj * 512 : wpad * 32));  // dW1 slice partial (SIMT k-major; MM fragment order)
+  L.Gs2 = o;   o = al32(o + (tc || mm ? 0 : wpad * 32)); // second row-half partial (SIMT)
+  L.Gr = o;    o = al32(o + (mm ? nj * 512 : wpad * 32));  // reduced slice read back
   L.gsm = o;   o = al32(o + kSmall);               // reduced W2/b block read back
   L.lsum = o;  o = al32(o + kWarps);
   L.total = o;
@@ -185,6 +212,93 @@ __device__ __forceinline__ void grid_wait_from(unsigned *ctr, unsigned target) {
   } while ((int)(v - target) < 0);
 }
 
+// ---- warp-level TF32 MMA (MM variant): D[16x8] += A[16x8] B[8x8], fp32 accumulate.  Fragments
+// (g = lane / 4, t = lane % 4): a0 = A[g][t], a1 = A[g+8][t], a2 = A[g][t+4], a3 = A[g+8][t+4];
+// b0 = B[t][g], b1 = B[t+4][g]; c0 = C[g][2t], c1 = C[g][2t+1], c2 = C[g+8][2t], c3 = C[g+8][2t+1].
+// Row and k indices may be permuted freely (the same way in A and B / in A and C): the loads
+// below use that to read 16 or 8 contiguous bytes per lane without shared-memory bank conflicts.
+__device__ __forceinline__ void hmma_tf32(float (&d)[4], const uint32_t (&a)[4], const uint32_t (&b)[2]) {
+  asm volatile(
+      "mma.sync.aligned.m16n8k8.row.col.f32.tf32.tf32.f32 {%0,%1,%2,%3}, {%4,%5,%6,%7}, {%8,%9}, {%0,%1,%2,%3};"
+      : "+f"(d[0]), "+f"(d[1]), "+f"(d[2]), "+f"(d[3])
+      : "r"(a[0]), "r"(a[1]), "r"(a[2]), "r"(a[3]), "r"(b[0]), "r"(b[1]));
+}
+// 3xTF32 operand split: hi = rn_tf32(x) (an exact TF32 value), lo = x - hi (exact in fp32; the
+// tensor core reads its TF32 part)
+__device__ __forceinline__ void split_tf32(float x, uint32_t &hi, uint32_t &lo) {
+  const float h = tc::tf32_hi(x);
+  hi = __float_as_uint(h);
+  lo = __float_as_uint(x - h);
+}
+// truncation split: hi = x itself (the tensor core reads its TF32 part, i.e. x with the low 13
+// mantissa bits cleared), lo = x - that part (exact); pairs with an RN-split partner operand so
+// the dropped lo*lo term has zero mean (R13)
+__device__ __forceinline__ void split_trunc(float x, uint32_t &hi, uint32_t &lo) {
+  hi = __float_as_uint(x);
+  lo = __float_as_uint(x - __uint_as_float(hi & 0xffffe000u));
+}
+// D += A B in 3xTF32: small terms first
+__device__ __forceinline__ void hmma3(float (&d)[4], const uint32_t (&ah)[4], const uint32_t (&al)[4],
+                                      const uint32_t (&bh)[2], const uint32_t (&bl)[2]) {
+  hmma_tf32(d, al, bh);
+  hmma_tf32(d, ah, bl);
+  hmma_tf32(d, ah, bh);
+}
+
+// P1 of the MM variant for one warp: Z1 partial rows of the NM m-tiles m0, m0 + MSTEP, ... (16 rows
+// each) x one n-block (8 neurons) over the 16-pixel blocks [jb, je) of the slice.  Logical row g of
+// an m-tile is physical row pr (the caller picks the permutation that makes the LDS.128
+// conflict-free for the slice's row stride); k-step 2j / 2j+1 takes pixels 16 j + 4 t + {0, 1} /
+// {2, 3}, matching the W fragment order [j][nb][lane][4].  Output: rows of Pz [rows][32], or (pf
+// non-null) fragments pf[(m * 4 + nb) * 32 + lane].
+template <int NM, int MSTEP>
+__device__ __forceinline__ void p1_mma(const float *xs, int wpad, const float4 *Wh4, const float4 *Wl4, int jb,
+                                       int je, int m0, int nb, int lane, int pr, float *Pz, float4 *pf) {
+  const int tt = lane & 3;
+  float acc[NM][4];
+#pragma unroll
+  for (int m = 0; m < NM; ++m) acc[m][0] = acc[m][1] = acc[m][2] = acc[m][3] = 0.0f;
+  const float *xr = xs + (16 * m0 + pr) * wpad + 4 * tt;
+  for (int j = jb; j < je; ++j) {
+    const float4 wh = Wh4[(j * 4 + nb) * 32 + lane], wl = Wl4[(j * 4 + nb) * 32 + lane];
+    float4 xa[NM], xb[NM];
+#pragma unroll
+    for (int m = 0; m < NM; ++m) {
+      xa[m] = *reinterpret_cast<const float4 *>(xr + 16 * MSTEP * m * wpad + 16 * j);
+      xb[m] = *reinterpret_cast<const float4 *>(xr + (16 * MSTEP * m + 8) * wpad + 16 * j);
+    }
+#pragma unroll
+    for (int h = 0; h < 2; ++h) {  // k-steps 2j, 2j+1
+      const uint32_t bh[2] = {__float_as_uint(h ? wh.z : wh.x), __float_as_uint(h ? wh.w : wh.y)};
+      const uint32_t bl[2] = {__float_as_uint(h ? wl.z : wl.x), __float_as_uint(h ? wl.w : wl.y)};
+      uint32_t ah[NM][4], al[NM][4];
+#pragma unroll
+      for (int m = 0; m < NM; ++m) {
+        split_trunc(h ? xa[m].z : xa[m].x, ah[m][0], al[m][0]);
+        split_trunc(h ? xb[m].z : xb[m].x, ah[m][1], al[m][1]);
+        split_trunc(h ? xa[m].w : xa[m].y, ah[m][2], al[m][2]);
+        split_trunc(h ? xb[m].w : xb[m].y, ah[m][3], al[m][3]);
+      }
+#pragma unroll
+      for (int m = 0; m < NM; ++m) hmma_tf32(acc[m], al[m], bh);
+#pragma unroll
+      for (int m = 0; m < NM; ++m) hmma_tf32(acc[m], ah[m], bl);
+#pragma unroll
+      for (int m = 0; m < NM; ++m) hmma_tf32(acc[m], ah[m], bh);
+    }
+  }
+#pragma unroll
+  for (int m = 0; m < NM; ++m) {
+    if (pf) {
+      pf[(MSTEP * m * 4 + nb) * 32 + lane] = make_float4(acc[m][0], acc[m][1], acc[m][2], acc[m][3]);
+    } else {  // c0, c1 = row g (physical pr), neurons 8 nb + 2t, +1; c2, c3 = row g + 8
+      float *d = Pz + (16 * (m0 + MSTEP * m) + pr) * 32 + 8 * nb + 2 * tt;
+      *reinterpret_cast<float2 *>(d) = make_float2(acc[m][0], acc[m][1]);
+      *reinterpret_cast<float2 *>(d + 8 * 32) = make_float2(acc[m][2], acc[m][3]);
+    }
+  }
+}
+
 // AH / AO: compile-time hidden / output activations (-1 = read p.act_h / p.act_o at run time).
 // The sigmoid/sigmoid instantiation (configs 1 and 2) keeps the dependent owner-row chain
 // short: no activation switch.
@@ -193,11 +307,13 @@ __device__ __forceinline__ void act_sel(int rt, float z, float &a, float &s) {
   act_fwd(AH >= 0 ? AH : rt, z, a, s);
 }
 
-template <bool TC, int AH, int AO>
+template <bool TC, bool MM, int AH, int AO, int NI>
 __global__ void __launch_bounds__(kThreads, kMinBlocks)
 fused_small_kernel(const FusedParams p, const __grid_constant__ CUtensorMap tmX,
                    const __grid_constant__ CUtensorMap tmXK, const __grid_constant__ CUtensorMap tmXM,
-                   const __grid_constant__ InlineStarts ist) {
+                   const __grid_constant__ InlineStarts<NI> ist) {
+  static_assert(!MM || kThreads == 512, "the MM variant maps 16 warps onto 4 n-blocks x 4 parts");
+  constexpr int ds = MM ? kDS : 32;  // delta_1 row stride
   extern __shared__ __align__(128) float sm[];
   const int C = (int)ptx::cluster_size();
   const int rank = (int)ptx::cluster_rank();
@@ -223,8 +339,9 @@ fused_small_kernel(const FusedParams p, const __grid_constant__ CUtensorMap tmX,
   const int e0 = e_begin(rank, C, nsmp), ne = e_begin(rank + 1, C, nsmp) - e0;
   const int eslot = e_slot(C);
 
-  const Smem L = smem_layout(wpad, p.nSmax, p.nOwnMax, C, TC);
-  const int xstride = al32(xrows(p.nSmax) * wpad);
+  const Smem L = smem_layout(wpad, p.nSmax, p.nOwnMax, C, TC, MM);
+  const int xstride = MM ? al32(mm_rows(p.nSmax) * wpad + 32) : al32(xrows(p.nSmax) * wpad);
+  const int nj = mm_nj(wpad);  // MM: 16-pixel blocks of the slice
   uint64_t *bar_x = reinterpret_cast<uint64_t *>(sm);  // [2]
   uint64_t *bar_P = bar_x + 2;
   uint64_t *bar_D = bar_x + 3;
@@ -236,7 +353,9 @@ fused_small_kernel(const FusedParams p, const __grid_constant__ CUtensorMap tmX,
   uint8_t *Wt = X + kTcXBytes, *Dt = Wt + kTcWBytes;
   const uint32_t sX = ptx::smem_u32(X), sW = ptx::smem_u32(Wt), sD = ptx::smem_u32(Dt);
   float *W1t = sm + L.W1t, *W2s = sm + L.W2s, *b1s = sm + L.b1s, *b2s = sm + L.b2s;
-  float *xs0 = sm + L.xs, *ys0 = sm + L.ys, *Pfull = sm + L.Ppart, *Pown = sm + L.Pown;
+  float *xs0 = sm + L.xs, *ys0 = sm + L.ys, *Ppart = sm + L.Ppart, *Pown = sm + L.Pown;
+  // row-major Z1 partial rows [rows][32] (SIMT / TC: K part 0 itself; MM: after the 4 fragment-order parts)
+  float *Pfull = Ppart;
   const int pstride = xrows(p.nSmax) * 32;  // floats between P1 K-part buffers
   float *D1 = sm + L.D1, *A1own = sm + L.A1own, *D2own = sm + L.D2own;
   float *gpart = sm + L.gpart, *grecv = sm + L.grecv, *Gs = sm + L.Gs, *Gs2 = sm + L.Gs2, *Gr = sm + L.Gr;
@@ -244,7 +363,7 @@ fused_small_kernel(const FusedParams p, const __grid_constant__ CUtensorMap tmX,
 
   const int64_t oW1 = 0, ob1 = (int64_t)H * n0, oW2 = ob1 + H, ob2 = oW2 + (int64_t)O * H;
   // accumulator slot layout: [C slices of ws x 32 (k-major)] [W2/b block of nsmp floats]
-  const int64_t slice_off = (int64_t)rank * p.ws * 32;
+  const int64_t slice_off = (int64_t)rank * p.gsl;
 
   // ---- one-time setup: zero smem, barriers, resident parameters
   for (int i = 32 + tid; i < L.total; i += kThreads) sm[i] = 0.0f;
@@ -280,6 +399,15 @@ fused_small_kernel(const FusedParams p, const __grid_constant__ CUtensorMap tmX,
       *reinterpret_cast<float *>(Wt + off) = h;
       *reinterpret_cast<float *>(Wt + 16384 + off) = v - h;
     }
+  } else if (MM) {  // fragment order: [j][nb][lane][4] = W1[8 nb + lane / 4][k0 + 16 j + 4 (lane % 4) + e]
+    for (int i = tid; i < nj * 512; i += kThreads) {
+      const int ln = (i >> 2) & 31, nbj = i >> 7;
+      const int n = 8 * (nbj & 3) + (ln >> 2), k = 16 * (nbj >> 2) + 4 * (ln & 3) + (i & 3);
+      const float v = (n < H && k < w) ? p.params[oW1 + (int64_t)n * n0 + k0 + k] : 0.0f;
+      const float h = tc::tf32_hi(v);
+      W1t[i] = h;
+      W1t[nj * 512 + i] = v - h;
+    }
   } else {
     for (int i = tid; i < w * 32; i += kThreads) {
       const int k = i >> 5, j = i & 31;
@@ -296,9 +424,9 @@ fused_small_kernel(const FusedParams p, const __grid_constant__ CUtensorMap tmX,
   for (int c = 0; c < C; ++c) {
     if (c == rank) continue;
     bytesP += nOwn * 128;
-    bytesD += (own_begin(c + 1, nS, C) - own_begin(c, nS, C)) * 128 + ne * 4;
+    bytesD += (own_begin(c + 1, nS, C) - own_begin(c, nS, C)) * ds * 4 + ne * 4;
   }
-  const uint32_t bytesG = (uint32_t)(p.ws * 32 * 4 + nsmp * 4);
+  const uint32_t bytesG = (uint32_t)(p.gsl * 4 + nsmp * 4);
 
   const uint32_t xbytes = (uint32_t)(p.nSmax * p.ws * 4);
   // batch starts are read one step ahead of their use so their global-load latency overlaps
@@ -405,6 +533,20 @@ fused_small_kernel(const FusedParams p, const __grid_constant__ CUtensorMap tmX,
         }
       }
       tc::tc_fence_before();
+    } else if constexpr (MM) {
+      // warp = (n-block nb of 8 neurons = the SMSP, mg): m-tiles mg and mg + 4 of 16 rows over all
+      // pixels of the slice (p1_mma; no K split, no partial sums).  Measured faster than splitting
+      // the fifth m-tile by K quarters for balance (shorter dependent HMMA chains per warp, more
+      // fragment re-reads).  Row permutation: rows 4 apart (row stride = 1 mod 8 16-B groups, e.g.
+      // config 2's 100-pixel slices) or adjacent (stride = 4 mod 8, 112-pixel slices) share an
+      // 8-lane LDS.128 phase, which then covers all 32 banks.
+      const int nb = warp & 3, mg = warp >> 2, gg = lane >> 2;
+      const int nmt = (nS + 15) >> 4;
+      const int pr = (wpad & 31) == 16 ? gg : (gg >> 1) + 4 * (gg & 1);
+      const float4 *Wh4 = reinterpret_cast<const float4 *>(W1t), *Wl4 = Wh4 + nj * 128;
+      if (mg + 4 < nmt) p1_mma<2, 4>(xs, wpad, Wh4, Wl4, 0, nj, mg, nb, lane, pr, Pfull, nullptr);
+      else if (mg < nmt) p1_mma<1, 4>(xs, wpad, Wh4, Wl4, 0, nj, mg, nb, lane, pr, Pfull, nullptr);
+      PROF_MAX(13);
     } else {
     // ---- P1. partial Z1: P[i][j] = sum_{k<w} x[i][k] W1[j][k0+k]
       for (int t = tid; t < kKP * RG * 8; t += kThreads) {
@@ -477,7 +619,7 @@ fused_small_kernel(const FusedParams p, const __grid_constant__ CUtensorMap tmX,
       float a1, s1;
       act_sel<AH, AO>(p.act_h, z, a1, s1);
       A1own[t] = j < H ? a1 : 0.0f;
-      D1[i * 32 + j] = j < H ? s1 : 0.0f;   // sigma'(z1) parked in the delta_1 row
+      D1[i * ds + j] = j < H ? s1 : 0.0f;   // sigma'(z1) parked in the delta_1 row
     }
     __syncthreads();
     PROF(11);
@@ -516,7 +658,7 @@ fused_small_kernel(const FusedParams p, const __grid_constant__ CUtensorMap tmX,
           t1 = fmaf(W2s[(o + 1) * 33 + j], vd[o + 1], t1);
         }
       }
-      D1[i * 32 + j] = j < H ? (t0 + t1) * D1[i * 32 + j] : 0.0f;
+      D1[i * ds + j] = j < H ? (t0 + t1) * D1[i * ds + j] : 0.0f;
     }
     {
       const float l = warp_sum(lacc);
@@ -530,7 +672,7 @@ fused_small_kernel(const FusedParams p, const __grid_constant__ CUtensorMap tmX,
     //      tendency partial over its owned rows (a 10x30x9 contraction) and its slices to
     //      the ranks that reduce them
     if (warp == 0 && lane < C && lane != rank && nOwn > 0)
-      ptx::bulk_s2peer(D1 + o0 * 32, D1 + o0 * 32, (uint32_t)(nOwn * 128), bar_D, lane);
+      ptx::bulk_s2peer(D1 + o0 * ds, D1 + o0 * ds, (uint32_t)(nOwn * ds * 4), bar_D, lane);
     for (int t = tid; t < nsmp; t += kThreads) {
       float v = 0.0f;
       if (t < O * H) {
@@ -540,7 +682,7 @@ fused_small_kernel(const FusedParams p, const __grid_constant__ CUtensorMap tmX,
       } else if (t < O * H + H) {
         const int j = t - O * H;
 #pragma unroll 8
-        for (int q = 0; q < nOwn; ++q) v += D1[(o0 + q) * 32 + j];
+        for (int q = 0; q < nOwn; ++q) v += D1[(o0 + q) * ds + j];
       } else if (t < nsm) {
         const int o = t - O * H - H;
 #pragma unroll 8
@@ -565,7 +707,7 @@ fused_small_kernel(const FusedParams p, const __grid_constant__ CUtensorMap tmX,
       tc_split(X, X + kTcXLoM, 4 * kTcAS, tid);
       for (int t = tid; t < kTcRows * 32; t += kThreads) {  // delta_1 hi | lo, rows >= nS zero
         const int r = t >> 5, j = t & 31;
-        const float v = r < nS ? D1[r * 32 + j] : 0.0f;
+        const float v = r < nS ? D1[r * ds + j] : 0.0f;
         const float h = tc::tf32_hi(v);
         const int off = sw128_32b(r, j);
         *reinterpret_cast<float *>(Dt + off) = h;
@@ -603,6 +745,50 @@ fused_small_kernel(const FusedParams p, const __grid_constant__ CUtensorMap tmX,
         }
       }
       tc::tc_fence_before();
+    } else if constexpr (MM) {
+      // ---- P5 (MM). dW1 slice, transposed: C(j, px) = sum_rows delta_1[row][j] x[row][px] with
+      //      M = neurons (m-tile mt: 16 neurons), N = pixels, K = rows.  warp = (mt, 16-pixel
+      //      block j = two n-blocks): n index g of n-block 2j / 2j+1 is pixel 16 j + 2g / +1 (one
+      //      8-B load per lane and row), k = t / t + 4 of k-step ks are rows 8 ks + 2t / +1.  Then
+      //      lane (g, t) holds exactly the elements it holds of W's fragments [j][nb][lane][4]
+      //      (neurons 16 mt + g (nb = 2 mt) and 16 mt + 8 + g (nb = 2 mt + 1), pixels 16 j + 4t + e):
+      //      Gs is written in that order and P9 is elementwise.  delta_1 RN-split (A), x
+      //      truncation-split (B); delta_1 rows >= nS are zero.
+      ptx::mbar_wait(bar_D, par);  // the peers' delta_1 rows (and W2/b slices) have landed
+      PROF_MAX(15);
+      // warp = (m-tile mt of 16 neurons, 16-pixel block j) over all rows (14 of the 16 warps for
+      // config 2's 7 blocks; splitting the rows in halves for balance measured slower)
+      const int mt = warp & 1, j = warp >> 1, gg = lane >> 2, tt = lane & 3;
+      if (j < nj) {
+        const int nks = (nS + 7) >> 3;
+        float acc[2][4];
+#pragma unroll
+        for (int h = 0; h < 2; ++h) acc[h][0] = acc[h][1] = acc[h][2] = acc[h][3] = 0.0f;
+        const float *dcol = D1 + 16 * mt + gg;
+        const float *xc = xs + 16 * j + 2 * gg;
+        for (int ks = 0; ks < nks; ++ks) {
+          const int r0 = 8 * ks + 2 * tt;
+          uint32_t ah[4], al[4];
+          split_tf32(dcol[r0 * kDS], ah[0], al[0]);
+          split_tf32(dcol[r0 * kDS + 8], ah[1], al[1]);
+          split_tf32(dcol[(r0 + 1) * kDS], ah[2], al[2]);
+          split_tf32(dcol[(r0 + 1) * kDS + 8], ah[3], al[3]);
+          const float2 u = *reinterpret_cast<const float2 *>(xc + r0 * wpad);        // b0 of n-blocks 2j, 2j+1
+          const float2 v = *reinterpret_cast<const float2 *>(xc + (r0 + 1) * wpad);  // b1
+          uint32_t bh0[2], bl0[2], bh1[2], bl1[2];
+          split_trunc(u.x, bh0[0], bl0[0]); split_trunc(v.x, bh0[1], bl0[1]);
+          split_trunc(u.y, bh1[0], bl1[0]); split_trunc(v.y, bh1[1], bl1[1]);
+          hmma_tf32(acc[0], al, bh0); hmma_tf32(acc[1], al, bh1);
+          hmma_tf32(acc[0], ah, bl0); hmma_tf32(acc[1], ah, bl1);
+          hmma_tf32(acc[0], ah, bh0); hmma_tf32(acc[1], ah, bh1);
+        }
+        // acc[h] = C over n-block 2j + h: c0 / c1 = neuron 16 mt + g, pixels 16 j + 4t + h / + 2 + h;
+        // c2 / c3 the same for neuron 16 mt + 8 + g
+        float4 *gs4 = reinterpret_cast<float4 *>(Gs);
+        gs4[(j * 4 + 2 * mt) * 32 + lane] = make_float4(acc[0][0], acc[1][0], acc[0][1], acc[1][1]);
+        gs4[(j * 4 + 2 * mt + 1) * 32 + lane] = make_float4(acc[0][2], acc[1][2], acc[0][3], acc[1][3]);
+      }
+      PROF_MAX(14);
     } else {
 
     // ---- P5. dW1 slice partial, k-major like W1t: Gs[k][j] = sum_{i<nS} D1[i][j] x[i][k]
@@ -667,7 +853,7 @@ fused_small_kernel(const FusedParams p, const __grid_constant__ CUtensorMap tmX,
     if (p.aligned) {
       if (tid == 0) {
         ptx::fence_proxy_async_global();
-        ptx::bulk_reduce_add_f32(accS + slice_off, Gs, (uint32_t)(p.ws * 32 * 4));
+        ptx::bulk_reduce_add_f32(accS + slice_off, Gs, (uint32_t)(p.gsl * 4));
         if (ne > 0) ptx::bulk_reduce_add_f32(accS + p.small_off + e0, gpart + e0, (uint32_t)(ne * 4));
         ptx::bulk_commit();
         ptx::bulk_wait_all();
@@ -711,7 +897,7 @@ fused_small_kernel(const FusedParams p, const __grid_constant__ CUtensorMap tmX,
       if (tid == 0) {
         ptx::fence_proxy_async_global();
         ptx::mbar_arrive_expect_tx(bar_G, bytesG);
-        ptx::bulk_g2s(Gr, accS + slice_off, (uint32_t)(p.ws * 32 * 4), bar_G);
+        ptx::bulk_g2s(Gr, accS + slice_off, (uint32_t)(p.gsl * 4), bar_G);
         ptx::bulk_g2s(gsm, accS + p.small_off, (uint32_t)(nsmp * 4), bar_G);
       }
       ptx::mbar_wait(bar_G, par);
@@ -736,6 +922,25 @@ fused_small_kernel(const FusedParams p, const __grid_constant__ CUtensorMap tmX,
         }
       }
       ptx::fence_proxy_async_smem();
+    } else if constexpr (MM) {  // W = hi + lo exactly; re-split after the update.  Gr has W's fragment order.
+      float4 *Wh4 = reinterpret_cast<float4 *>(W1t), *Wl4 = Wh4 + nj * 128;
+      const float4 *Gr4 = reinterpret_cast<const float4 *>(Gr);
+      for (int i = tid; i < nj * 128; i += kThreads) {
+        const int k = 16 * (i >> 7) + 4 * (i & 3);  // first pixel of the 4 (neurons >= H: W = G = 0)
+        if (k >= w) continue;
+        const float4 h = Wh4[i], l = Wl4[i], gv = Gr4[i];
+        float wv[4] = {h.x + l.x, h.y + l.y, h.z + l.z, h.w + l.w};
+        const float gq[4] = {gv.x, gv.y, gv.z, gv.w};
+        float hh[4], ll[4];
+#pragma unroll
+        for (int e = 0; e < 4; ++e) {
+          if (k + e < w) wv[e] -= p.scale * gq[e];
+          hh[e] = tc::tf32_hi(wv[e]);
+          ll[e] = wv[e] - hh[e];
+        }
+        Wh4[i] = make_float4(hh[0], hh[1], hh[2], hh[3]);
+        Wl4[i] = make_float4(ll[0], ll[1], ll[2], ll[3]);
+      }
     } else {
       for (int i = tid; i < w * 8; i += kThreads) {
         float4 wv = reinterpret_cast<float4 *>(W1t)[i];
@@ -758,7 +963,14 @@ fused_small_kernel(const FusedParams p, const __grid_constant__ CUtensorMap tmX,
 
   // ---- write the resident parameters back (W1 slice by every CTA of cluster 0; the rest by CTA 0)
   if (g == 0) {
-    for (int i = tid; i < w * 32; i += kThreads) {
+    if constexpr (MM) {
+      for (int i = tid; i < nj * 512; i += kThreads) {
+        const int ln = (i >> 2) & 31, nbj = i >> 7;
+        const int n = 8 * (nbj & 3) + (ln >> 2), k = 16 * (nbj >> 2) + 4 * (ln & 3) + (i & 3);
+        if (n < H && k < w) p.params[oW1 + (int64_t)n * n0 + k0 + k] = W1t[i] + W1t[nj * 512 + i];
+      }
+    }
+    for (int i = tid; i < (MM ? 0 : w * 32); i += kThreads) {
       const int k = i >> 5, j = i & 31;
       if (j >= H) continue;
       float v;
@@ -806,7 +1018,8 @@ int fused_small_train_steps(FusedSmall &fs, cudaStream_t st, const std::vector<i
   // ---- launch configuration: decided once per (shape, batch, dataset, switches), then cached
   // (the occupancy query and the tensor-map encodes cost host microseconds per call)
   const std::vector<int64_t> key = {n0, H, O, batch, (int64_t)(uintptr_t)X, N, aligned_now,
-                                    env_int("NF_FUSED_C", 0), env_int("NF_FUSED_G", 0), env_int("NF_FUSED_TC", 0)};
+                                    env_int("NF_FUSED_C", 0), env_int("NF_FUSED_G", 0), env_int("NF_FUSED_TC", 0),
+                                    env_int("NF_FUSED_MM", 0)};
   if (key != fs.cfg_key) {
     fs.cfg_key.clear();
   // cluster size: pixel slices of >= 32 columns, at most 8 CTAs
@@ -835,8 +1048,17 @@ int fused_small_train_steps(FusedSmall &fs, cudaStream_t st, const std::vector<i
     cudaGetDevice(&dev);
     std::lock_guard<std::mutex> lk(mu);
     if (!(done & (1u << (dev & 31)))) {
-      for (auto k : {fused_small_kernel<false, -1, -1>, fused_small_kernel<true, -1, -1>,
-                     fused_small_kernel<false, ACT_SIGMOID, ACT_SIGMOID>}) {
+      const void *ks[] = {
+          (const void *)fused_small_kernel<false, false, -1, -1, kInlineStarts>,
+          (const void *)fused_small_kernel<true, false, -1, -1, kInlineStarts>,
+          (const void *)fused_small_kernel<false, false, ACT_SIGMOID, ACT_SIGMOID, kInlineStarts>,
+          (const void *)fused_small_kernel<false, true, -1, -1, kInlineStarts>,
+          (const void *)fused_small_kernel<false, true, ACT_SIGMOID, ACT_SIGMOID, kInlineStarts>,
+          (const void *)fused_small_kernel<false, false, -1, -1, kInlineSmall>,
+          (const void *)fused_small_kernel<false, false, ACT_SIGMOID, ACT_SIGMOID, kInlineSmall>,
+          (const void *)fused_small_kernel<false, true, -1, -1, kInlineSmall>,
+          (const void *)fused_small_kernel<false, true, ACT_SIGMOID, ACT_SIGMOID, kInlineSmall>};
+      for (const void *k : ks) {
         cudaFuncSetAttribute(k, cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
         cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024);
       }
@@ -847,10 +1069,15 @@ int fused_small_train_steps(FusedSmall &fs, cudaStream_t st, const std::vector<i
   // (opt-in, NF_FUSED_TC=1: at N = 32 the 3xTF32 MMAs are shared-memory-bandwidth bound and no
   // faster than the FFMA2 path; profiles/r01_fused_tc_experiment.txt)
   bool tc = aligned && ws <= 128 && env_int("NF_FUSED_TC", 0) != 0;
+  // warp-level MMA contractions (opt-in NF_FUSED_MM=1; TMA-aligned x, <= 128 rows per cluster,
+  // pixel slices <= 128): parity-green, but 11.25 vs 11.05 us per config-2 step against the FFMA2
+  // SIMT default (profiles/r02_k6_mma_experiment.txt)
+  const bool mm_ok = aligned && !tc && mm_nj(wpad) <= kMJ && env_int("NF_FUSED_MM", 0) != 0;
+  auto mm_for = [&](int nSmax) { return mm_ok && mm_rows(nSmax) <= 16 * kMT1; };
   auto smem_for = [&](int G) {
     const int nSmax = (int)((batch + G - 1) / G);
     const int nOwnMax = (nSmax + C - 1) / C;
-    return (size_t)smem_layout(wpad, nSmax, nOwnMax, C, tc && nSmax <= kTcRows).total * sizeof(float) +
+    return (size_t)smem_layout(wpad, nSmax, nOwnMax, C, tc && nSmax <= kTcRows, mm_for(nSmax)).total * sizeof(float) +
            (tc ? 1024 : 0);
   };
   // clusters: as many as co-reside at 1 CTA/SM, with <= kMaxRows rows per cluster
@@ -872,7 +1099,10 @@ int fused_small_train_steps(FusedSmall &fs, cudaStream_t st, const std::vector<i
       if (cfg.dynamicSmemBytes > 227 * 1024) continue;
       int ncl = 0;
       const bool tcc = tc && (batch + cand - 1) / cand <= kTcRows;
-      if (cudaOccupancyMaxActiveClusters(&ncl, tcc ? fused_small_kernel<true, -1, -1> : fused_small_kernel<false, -1, -1>,
+      const bool mmc = mm_for((int)((batch + cand - 1) / cand));
+      if (cudaOccupancyMaxActiveClusters(&ncl, tcc ? fused_small_kernel<true, false, -1, -1, kInlineStarts>
+                                               : mmc ? fused_small_kernel<false, true, -1, -1, kInlineStarts>
+                                                     : fused_small_kernel<false, false, -1, -1, kInlineStarts>,
                                          &cfg) !=
           cudaSuccess) {
         cudaGetLastError();
@@ -886,6 +1116,7 @@ int fused_small_train_steps(FusedSmall &fs, cudaStream_t st, const std::vector<i
   const int nOwnMax = (nSmax + C - 1) / C;
   const size_t smem = smem_for(G);
   tc = tc && nSmax <= kTcRows;
+  const bool mm = mm_for(nSmax);
 
   CUtensorMap tmX, tmXK, tmXM;
   memset(&tmX, 0, sizeof tmX);
@@ -905,7 +1136,7 @@ int fused_small_train_steps(FusedSmall &fs, cudaStream_t st, const std::vector<i
     return -1;
   }
     fs.C = C; fs.G = G; fs.ws_cols = ws; fs.wpad = wpad; fs.nSmax = nSmax; fs.nOwnMax = nOwnMax;
-    fs.smem = smem; fs.tc = tc; fs.aligned = aligned;
+    fs.smem = smem; fs.tc = tc; fs.mm = mm; fs.aligned = aligned;
     memcpy(fs.tmaps[0], &tmX, sizeof tmX);
     memcpy(fs.tmaps[1], &tmXK, sizeof tmXK);
     memcpy(fs.tmaps[2], &tmXM, sizeof tmXM);
@@ -914,7 +1145,7 @@ int fused_small_train_steps(FusedSmall &fs, cudaStream_t st, const std::vector<i
   host_trace("k6 config");
   const int C = fs.C, G = fs.G, ws = fs.ws_cols, wpad = fs.wpad, nSmax = fs.nSmax, nOwnMax = fs.nOwnMax;
   const size_t smem = fs.smem;
-  const bool tc = fs.tc, aligned = fs.aligned;
+  const bool tc = fs.tc, mm = fs.mm, aligned = fs.aligned;
   CUtensorMap tmX, tmXK, tmXM;
   memcpy(&tmX, fs.tmaps[0], sizeof tmX);
   memcpy(&tmXK, fs.tmaps[1], sizeof tmXK);
@@ -923,7 +1154,8 @@ int fused_small_train_steps(FusedSmall &fs, cudaStream_t st, const std::vector<i
 
   // accumulator slot: [C][ws][32] dW1 slices (k-major), then the W2/b1/b2 block (16-B aligned)
   const int nsmp = (O * H + H + O + 3) & ~3;
-  const int64_t small_off = (int64_t)C * ws * 32;
+  const int gsl = mm ? mm_nj(wpad) * 512 : ws * 32;  // floats of a rank's dW1 slice
+  const int64_t small_off = (int64_t)C * gsl;
   const int64_t slot = (small_off + nsmp + 31) & ~int64_t(31);
   const size_t need = kSlots * slot * sizeof(float) + 256;
   if (fs.ws_bytes < need) {
@@ -968,6 +1200,7 @@ int fused_small_train_steps(FusedSmall &fs, cudaStream_t st, const std::vector<i
   p.slot = slot;
   p.small_off = small_off;
   p.nsmp = nsmp;
+  p.gsl = gsl;
   p.scale = (float)((double)eta / (double)batch);
   p.inv_B = (float)(1.0 / (double)batch);
   p.X = X; p.Y = Y; p.params = params;
@@ -993,8 +1226,13 @@ int fused_small_train_steps(FusedSmall &fs, cudaStream_t st, const std::vector<i
   }
   p.slot0 = (int)(fs.steps_done % kSlots);
   p.bar_base = fs.bar_base;
-  static thread_local InlineStarts ist;  // host staging of the launch parameter buffer
-  if (n_steps <= kInlineStarts) {
+  static thread_local InlineStarts<kInlineStarts> ist;  // host staging of the launch parameter buffer
+  static thread_local InlineStarts<kInlineSmall> ist_s;
+  const bool small_ist = n_steps <= kInlineSmall;
+  if (small_ist) {
+    memcpy(ist_s.v, starts, n_steps * sizeof(int64_t));
+    p.starts = nullptr;
+  } else if (n_steps <= kInlineStarts) {
     memcpy(ist.v, starts, n_steps * sizeof(int64_t));
     p.starts = nullptr;
   } else {
@@ -1025,24 +1263,44 @@ int fused_small_train_steps(FusedSmall &fs, cudaStream_t st, const std::vector<i
     cfg.dynamicSmemBytes = smem;
     cfg.stream = st;
     const bool sig = act_h == ACT_SIGMOID && act_o == ACT_SIGMOID;
-    auto kern = tc    ? fused_small_kernel<true, -1, -1>
-                : sig ? fused_small_kernel<false, ACT_SIGMOID, ACT_SIGMOID>
-                      : fused_small_kernel<false, -1, -1>;
     static bool coop_ok = true;
     if (!coop_ok) cfg.numAttrs = 1;
-    e = cudaLaunchKernelEx(&cfg, kern, p, tmX, tmXK, tmXM, ist);
+    const void *kern = nullptr;
+    auto launch = [&]() {
+      if (small_ist) {
+        auto k = mm ? (sig ? fused_small_kernel<false, true, ACT_SIGMOID, ACT_SIGMOID, kInlineSmall>
+                           : fused_small_kernel<false, true, -1, -1, kInlineSmall>)
+                    : tc ? nullptr
+                    : sig ? fused_small_kernel<false, false, ACT_SIGMOID, ACT_SIGMOID, kInlineSmall>
+                          : fused_small_kernel<false, false, -1, -1, kInlineSmall>;
+        if (k) {
+          kern = reinterpret_cast<const void *>(k);
+          return cudaLaunchKernelEx(&cfg, k, p, tmX, tmXK, tmXM, ist_s);
+        }
+        memcpy(ist.v, ist_s.v, n_steps * sizeof(int64_t));  // (TC: large-buffer variant only)
+      }
+      auto k = tc   ? fused_small_kernel<true, false, -1, -1, kInlineStarts>
+               : mm ? (sig ? fused_small_kernel<false, true, ACT_SIGMOID, ACT_SIGMOID, kInlineStarts>
+                           : fused_small_kernel<false, true, -1, -1, kInlineStarts>)
+               : sig ? fused_small_kernel<false, false, ACT_SIGMOID, ACT_SIGMOID, kInlineStarts>
+                     : fused_small_kernel<false, false, -1, -1, kInlineStarts>;
+      kern = reinterpret_cast<const void *>(k);
+      return cudaLaunchKernelEx(&cfg, k, p, tmX, tmXK, tmXM, ist);
+    };
+    e = launch();
     if (e != cudaSuccess && cfg.numAttrs == 2 && e != cudaErrorCooperativeLaunchTooLarge) {
       // cooperative + cluster launch unsupported by this driver: plain cluster launch (the grid
       // was sized from cudaOccupancyMaxActiveClusters); a too-large grid is still an error
       cudaGetLastError();
       coop_ok = false;
       cfg.numAttrs = 1;
-      e = cudaLaunchKernelEx(&cfg, kern, p, tmX, tmXK, tmXM, ist);
+      e = launch();
     }
     count_launch();
     char nt[64];
-    snprintf(nt, sizeof nt, "cluster=%d steps=%lld%s", C, (long long)n_steps, cfg.numAttrs == 2 ? " cooperative" : "");
-    log_launch(reinterpret_cast<const void *>(kern), cfg.gridDim, cfg.blockDim, smem, nt);
+    snprintf(nt, sizeof nt, "cluster=%d steps=%lld%s%s", C, (long long)n_steps, cfg.numAttrs == 2 ? " cooperative" : "",
+             mm ? " mma" : tc ? " tcgen05" : " simt");
+    log_launch(kern, cfg.gridDim, cfg.blockDim, smem, nt);
   }
   host_trace("k6 launch");
   if (e == cudaSuccess) {
@@ -1082,7 +1340,7 @@ int fused_small_train_steps(FusedSmall &fs, cudaStream_t st, const std::vector<i
       }
     }
     fprintf(stderr, "[fused prof] %s C=%d G=%d nS<=%d ws=%d aligned=%d smem=%zu  phase clk (mean over CTAs / max), "
-            "ns at %.0f MHz:\n", tc ? "tcgen05" : "simt", C, G, nSmax, ws, (int)aligned, smem, khz / 1e3);
+            "ns at %.0f MHz:\n", tc ? "tcgen05" : mm ? "mma" : "simt", C, G, nSmax, ws, (int)aligned, smem, khz / 1e3);
     const char *names[11] = {"P0 wait_x+issue", "P1 z1_partial", "P2 push_P+wait", "P3 owned_rows",
                              "P4 push_D+gpart", "P5 dW1+small_red", "P6 co_sum_bulk", "P7 grid_bar",
                              "P8 readback", "P9 update+zero", "tail"};
@@ -1105,6 +1363,18 @@ int fused_small_train_steps(FusedSmall &fs, cudaStream_t st, const std::vector<i
       if (tc)
         fprintf(stderr, "  P1 split: issue %.0f, mma wait %.0f, epilogue %.0f clk;  P5 split+D build %.0f clk\n",
                 a / n, b / n, c / n, d / n);
+      if (mm) {  // slots 13 / 15 / 14: last warp done with P1's MMAs / through P5's wait / done with P5's MMAs
+        double e1 = 0, e2 = 0, e3 = 0, e4 = 0, e5 = 0;
+        int m = 0;
+        for (int s = 2; s + 1 < ns; ++s)
+          for (int bl = 0; bl < G * C; ++bl, ++m) {
+            const long long *t = &h[((size_t)bl * 64 + s) * kProf];
+            e1 += (double)(t[13] - t[1]); e2 += (double)(t[2] - t[13]); e3 += (double)(t[15] - t[5]);
+            e4 += (double)(t[14] - t[15]); e5 += (double)(t[6] - t[14]);
+          }
+        fprintf(stderr, "  MM split: P1 mma (last warp) %.0f, P1 K-part sum %.0f;  P5 wait %.0f, P5 mma (last warp) %.0f, "
+                "P5 rest %.0f clk\n", e1 / m, e2 / m, e3 / m, e4 / m, e5 / m);
+      }
     }
     {  // sub-phases of P3: slots 3 -> 11 -> 12 -> 4
       double a = 0, b = 0, c = 0;

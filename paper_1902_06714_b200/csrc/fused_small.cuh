@@ -28,7 +28,7 @@ struct FusedSmall {
   std::vector<int64_t> cfg_key;
   int C = 0, G = 0, ws_cols = 0, wpad = 0, nSmax = 0, nOwnMax = 0;
   size_t smem = 0;
-  bool tc = false, aligned = false;
+  bool tc = false, mm = false, aligned = false;
   alignas(64) unsigned char tmaps[3][128];
 };
 

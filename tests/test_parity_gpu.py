@@ -325,6 +325,35 @@ def test_c2_tensor_core_variant_of_fused_kernel(c2_trajectory, monkeypatch):
     assert rel_err(loss.cpu().numpy(), ref_loss) <= FP32_BAR
 
 
+@pytest.mark.parametrize("geom,batch", [({}, 1000), ({"NF_FUSED_C": "7"}, 1000), ({}, 900), ({}, 333)])
+def test_c2_warp_mma_variant_of_fused_kernel(c2_trajectory, monkeypatch, geom, batch):
+    """The opt-in warp-level MMA (mma.sync 3xTF32) variant of the fused kernel (NF_FUSED_MM=1),
+    in the default decomposition (5 row m-tiles, 100-pixel slices), 112-pixel slices (the other row
+    permutation of its conflict-free loads), 60-row clusters (4 m-tiles) and ragged 23-row clusters:
+    same parity bar."""
+    monkeypatch.setenv("NF_FUSED_MM", "1")
+    for k, v in geom.items():
+        monkeypatch.setenv(k, v)
+    nf.nf_debug_log_enable(True)
+    t = c2_trajectory
+    cfg, X, Y = t["cfg"], t["X"], t["Y"]
+    starts = t["starts"][100:110]
+    p = t["ckpt"][100]
+    net = make_net(cfg["dims"], cfg["act"], p)
+    loss = torch.zeros(len(starts), device="cuda")
+    net.train_steps(dev(X), dev(Y), batch, starts, cfg["eta"], step_loss=loss)
+    torch.cuda.synchronize()
+    log = nf.nf_debug_log_read()
+    nf.nf_debug_log_enable(False)
+    assert any("fused_small_kernel" in l and " mma" in l for l in log), log
+    o = oracle.Oracle(cfg["dims"], cfg["act"])
+    ref, ref_loss = o.train_steps(p, X, Y, batch, starts, cfg["eta"])
+    for (Wg, bg), (Wr, br) in zip(o.layers(gpu_params(net)), o.layers(ref)):
+        assert rel_err(Wg, Wr) <= FP32_BAR
+        assert rel_err(bg, br) <= FP32_BAR
+    assert rel_err(loss.cpu().numpy(), ref_loss) <= FP32_BAR
+
+
 def test_generic_train_steps_graph_equals_train_batch_loop():
     """nf_train_steps on a generic (non-fused) net runs as a captured CUDA graph, replayed on a
     repeated call; it must equal the nf_train_batch loop, and its replay must equal a fresh run."""
