@@ -70,12 +70,32 @@ int parse_act(const std::string &s) {
 }
 
 bool is_device_ptr(const void *p) {
+  // Small per-thread cache of the last answers (a call passes the same X, Y and step_loss every
+  // step; cudaPointerGetAttributes costs ~1 us).  Sound under unified addressing: an address the
+  // driver reports as device memory stays in its reserved device VA range, and host addresses never
+  // enter it, so a cached answer for an address cannot flip.
+  constexpr int kCache = 8;
+  static thread_local const void *ck[kCache] = {};
+  static thread_local bool cv[kCache] = {};
+  static thread_local int cn = 0;
+  if (!p) return false;
+  for (int i = 0; i < kCache; ++i)
+    if (ck[i] == p) return cv[i];
   cudaPointerAttributes at;
+  bool dev;
   if (cudaPointerGetAttributes(&at, p) != cudaSuccess) {
     cudaGetLastError();
-    return false;
+    dev = false;
+  } else {
+    dev = at.type == cudaMemoryTypeDevice || at.type == cudaMemoryTypeManaged;
   }
-  return at.type == cudaMemoryTypeDevice || at.type == cudaMemoryTypeManaged;
+  // only device answers are cached: a host address can later become registered / mapped memory
+  if (dev) {
+    ck[cn] = p;
+    cv[cn] = dev;
+    cn = (cn + 1) % kCache;
+  }
+  return dev;
 }
 
 // splitmix64 + Box-Muller: the documented host stream of nf_net_create.

@@ -408,10 +408,21 @@ fused_small_kernel(const FusedParams p, const __grid_constant__ CUtensorMap tmX,
       W1t[i] = h;
       W1t[nj * 512 + i] = v - h;
     }
-  } else {
-    for (int i = tid; i < w * 32; i += kThreads) {
-      const int k = i >> 5, j = i & 31;
-      if (j < H) W1t[i] = p.params[oW1 + (int64_t)j * n0 + k0 + k];
+  } else {  // coalesced row reads (consecutive threads: consecutive pixels of one neuron's row), all
+             // loads of a thread issued before its transposed shared-memory stores
+    constexpr int kPer = 8;
+    for (int i0 = tid; i0 < H * w; i0 += kThreads * kPer) {
+      float v[kPer];
+#pragma unroll
+      for (int u = 0; u < kPer; ++u) {
+        const int i = i0 + u * kThreads;
+        v[u] = i < H * w ? p.params[oW1 + (int64_t)(i / w) * n0 + k0 + i % w] : 0.0f;
+      }
+#pragma unroll
+      for (int u = 0; u < kPer; ++u) {
+        const int i = i0 + u * kThreads;
+        if (i < H * w) W1t[(i % w) * 32 + i / w] = v[u];
+      }
     }
   }
   for (int i = tid; i < O * H; i += kThreads) W2s[(i / H) * 33 + i % H] = p.params[oW2 + i];
