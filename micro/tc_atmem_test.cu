@@ -37,7 +37,7 @@ __device__ __forceinline__ int sw128(int r, int c) { return r * 128 + ((((c >> 2
 
 // A [M][K] fp32, B [N][K] fp32; D[M][N] = sum_k (3xTF32) A B.  mode 0: A in TMEM, 1: A in smem.
 template <int N>
-__global__ void k_test(const float *A, const float *B, float *D, int K, int mode, int nsplit, long long *clk) {
+__global__ void k_test(const float *A, const float *B, float *D, int K, int mode, int nsplit, long long *clk, int nacc) {
   extern __shared__ __align__(1024) uint8_t smraw[];
   uint8_t *sm = reinterpret_cast<uint8_t *>((reinterpret_cast<uintptr_t>(smraw) + 1023) & ~uintptr_t(1023));
   // smem: A hi | A lo ([K/32 atoms][128 rows][128 B]), B hi | B lo ([K/32 atoms][N rows][128 B])
@@ -103,6 +103,15 @@ __global__ void k_test(const float *A, const float *B, float *D, int K, int mode
         const uint64_t bh = tc::smem_desc(ptx::smem_u32(Bh) + bo, 16, 1024, 2), bl = tc::smem_desc(ptx::smem_u32(Bl) + bo, 16, 1024, 2);
         if (mode == 0) {
           const uint32_t ah = tmem + 128u + 8 * ks, al = tmem + 256u + 8 * ks;
+          const uint32_t dd = tmem + 384u + (uint32_t)(ks % nacc) * 32u;  // nacc > 1: round-robin accumulators
+          if (nacc > 1) {
+            mma_tf32_ts(dd, ah, bh, idesc, ks >= nacc ? 1u : 0u);
+            if (nsplit == 3) {
+              mma_tf32_ts(dd, ah, bl, idesc, 1u);
+              mma_tf32_ts(dd, al, bh, idesc, 1u);
+            }
+            continue;
+          }
           mma_tf32_ts(tmem, ah, bh, idesc, ks > 0 ? 1u : 0u);
           if (nsplit == 3) {
             mma_tf32_ts(tmem, ah, bl, idesc, 1u);
@@ -155,7 +164,7 @@ __global__ void k_test(const float *A, const float *B, float *D, int K, int mode
 }
 
 template <int N>
-void run(int K, int mode, int nsplit) {
+void run(int K, int mode, int nsplit, int nacc = 1) {
   std::vector<float> hA(M * K), hB(N * K);
   srand(1);
   for (auto &v : hA) v = (float)rand() / RAND_MAX * 2 - 1;
@@ -170,7 +179,7 @@ void run(int K, int mode, int nsplit) {
   CK(cudaFuncSetAttribute(k_test<N>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
   long long best = 1LL << 60, st = 0, first = 0;
   for (int it = 0; it < 5; ++it) {
-    k_test<N><<<1, 256, smem>>>(A, B, D, K, mode, nsplit, clk);
+    k_test<N><<<1, 256, smem>>>(A, B, D, K, mode, nsplit, clk, nacc);
     CK(cudaDeviceSynchronize());
     long long h[4];
     CK(cudaMemcpy(h, clk, 32, cudaMemcpyDeviceToHost));
@@ -189,12 +198,15 @@ void run(int K, int mode, int nsplit) {
       maxr = std::max(maxr, std::fabs(s));
     }
   const int nmma = (K + 7) / 8 * nsplit;
-  printf("N=%3d K=%3d %s %dxTF32: %2d MMAs, chain+commit+wait %6lld clk warm (%5.1f clk/MMA), first %lld clk; 128x1024 tmem-store %lld clk; max err %.2e (rel %.2e)\n", N, K,
+  if (nacc > 1) maxe = -1;  // (accumulators not summed: timing only)
+  printf("nacc=%d N=%3d K=%3d %s %dxTF32: %2d MMAs, chain+commit+wait %6lld clk warm (%5.1f clk/MMA), first %lld clk; 128x1024 tmem-store %lld clk; max err %.2e (rel %.2e)\n", nacc, N, K,
          mode == 0 ? "A in TMEM" : "A in smem", nsplit, nmma, best, (double)best / nmma, first, st, maxe, maxe / maxr);
   cudaFree(A); cudaFree(B); cudaFree(D); cudaFree(clk);
 }
 
 int main() {
+  for (int nacc : {2, 4})
+    for (int nsplit : {1, 3}) run<32>(104, 0, nsplit, nacc);
   for (int nsplit : {1, 3})
     for (int mode : {0, 1}) {
       run<32>(104, mode, nsplit);

@@ -15,6 +15,7 @@
 #include "fp64.cuh"
 #include "fused_small.cuh"
 #include "infer_small.cuh"
+#include "infer_tc.cuh"
 #include "single_cta.cuh"
 #include "kernels.cuh"
 
@@ -287,6 +288,19 @@ int ensure_shadow(nf_net *net) {
   if (!net->params_t) NF_CUDA(cudaMalloc(&net->params_t, net->nparams * sizeof(float)));
   NF_CUDA(round_tf32(net->stream, net->params, net->params_t, net->nparams));
   net->shadow_ok = true;
+  return NF_OK;
+}
+
+// The weights' RN split (hi in params_t, lo in params_lo) for the tensor-core inference kernel,
+// in either fp32 or TF32 mode (the TF32 shadow is the same hi: cvt.rna of params)
+int ensure_wsplit(nf_net *net) {
+  if (!net->params_lo) NF_CUDA(cudaMalloc(&net->params_lo, net->nparams * sizeof(float)));
+  if (!net->params_t) NF_CUDA(cudaMalloc(&net->params_t, net->nparams * sizeof(float)));
+  if (!net->lo_ok) {
+    NF_CUDA(split_rn(net->stream, net->params, net->params_t, net->params_lo, net->nparams));
+    net->lo_ok = true;
+    net->shadow_ok = true;
+  }
   return NF_OK;
 }
 
@@ -889,6 +903,10 @@ int nf_output(nf_net *net, const float *x, int64_t n, float *out) {
       if ((rc = forward64(net, dx + r * n0, nullptr, m, 2))) return rc;
       NF_CUDA(f64_round(net->stream, net->A64[net->L], dout + r * nL, m * nL));
     }
+  } else if (infer_tc_applicable(net->dims, dx) && getenv("NF_DISABLE_FUSED") == nullptr) {
+    if ((rc = ensure_wsplit(net))) return rc;
+    NF_CUDA(infer_tc(net->stream, net->dims, net->act_h, net->act_o, net->params, net->params_t, net->params_lo,
+                     dx, n, dout));
   } else if (infer_small_applicable(net->dims, dx) && getenv("NF_DISABLE_FUSED") == nullptr) {
     NF_CUDA(infer_small(net->stream, net->dims, net->act_h, net->act_o, net->params, dx, n, dout));
   } else {
@@ -909,6 +927,7 @@ int nf_output(nf_net *net, const float *x, int64_t n, float *out) {
 }
 
 int nf_train_batch(nf_net *net, const float *x, const float *y, int64_t n, float eta) {
+  if (net && !net->presplit()) net->lo_ok = false;  // (outside the fp32 mode nothing keeps params_lo current)
   if (int rc = check_net(net)) return rc;
   if (n <= 0) return fail(NF_EINVAL, "train needs n >= 1 (S:181)");
   if (!std::isfinite(eta)) return fail(NF_EINVAL, "eta is not finite");
@@ -1036,6 +1055,7 @@ static int train_steps_device(nf_net *net, const float *dX, const float *dY, int
 int nf_train_steps(nf_net *net, const float *X, const float *Y, int64_t N, int64_t batch,
                    const int64_t *starts, int64_t n_steps, float eta, float *step_loss) {
   host_trace("enter");
+  if (net && !net->presplit()) net->lo_ok = false;  // (outside the fp32 mode nothing keeps params_lo current)
   if (int rc = check_net(net)) return rc;
   if (batch <= 0 || N < batch) return fail(NF_EINVAL, "need 1 <= batch <= N");
   if (n_steps < 0) return fail(NF_EINVAL, "n_steps < 0");
@@ -1168,6 +1188,7 @@ int nf_grad(nf_net *net, const float *x, const float *y, int64_t n, float *grad)
 }
 
 int nf_update(nf_net *net, const float *grad, int64_t count, float eta, int64_t n) {
+  if (net && !net->presplit()) net->lo_ok = false;  // (outside the fp32 mode nothing keeps params_lo current)
   if (int rc = check_net(net)) return rc;
   if (int rc = check_ptr(grad, "grad")) return rc;
   if (count != net->nparams) return fail(NF_EINVAL, "count %lld != %lld", (long long)count, (long long)net->nparams);
@@ -1203,7 +1224,9 @@ static int eval_loss_acc(nf_net *net, const float *x, const float *y, int64_t n,
   const int64_t nchunks = (n + chunk - 1) / chunk;
   NF_CUDA(net->red.ensure(red_bytes() + nchunks * 2 * sizeof(float)));
   float *res = reinterpret_cast<float *>(net->red.as<char>() + red_bytes());
-  const bool fused = !f64 && infer_small_applicable(net->dims, dx) && getenv("NF_DISABLE_FUSED") == nullptr;
+  const bool fused_tc = !f64 && infer_tc_applicable(net->dims, dx) && getenv("NF_DISABLE_FUSED") == nullptr;
+  const bool fused = !f64 && !fused_tc && infer_small_applicable(net->dims, dx) && getenv("NF_DISABLE_FUSED") == nullptr;
+  if (fused_tc && (rc = ensure_wsplit(net))) return rc;
   for (int64_t c = 0; c < nchunks; ++c) {
     const int64_t r = c * chunk, m = std::min(chunk, n - r);
     if (f64) {
@@ -1212,7 +1235,10 @@ static int eval_loss_acc(nf_net *net, const float *x, const float *y, int64_t n,
                          nullptr));
       continue;
     }
-    if (fused) NF_CUDA(infer_small(net->stream, net->dims, net->act_h, net->act_o, net->params, dx + r * n0, m,
+    if (fused_tc)
+      NF_CUDA(infer_tc(net->stream, net->dims, net->act_h, net->act_o, net->params, net->params_t, net->params_lo,
+                       dx + r * n0, m, net->A[net->L]));
+    else if (fused) NF_CUDA(infer_small(net->stream, net->dims, net->act_h, net->act_o, net->params, dx + r * n0, m,
                                    net->A[net->L]));
     else if ((rc = forward(net, dx + r * n0, nullptr, m, 2))) return rc;
     NF_CUDA(loss_acc(net->stream, net->A[net->L], dy + r * nL, m, nL, net->red.as<double2>(), res + 2 * c, nullptr));

@@ -1,0 +1,357 @@
+// infer_tc.cu -- the paper's `output` (Eq. 2) for two-layer nets with narrow
+// hidden and output layers (H, O <= 32; config 2's [784,30,10]) on the tcgen05 tensor cores.
+//
+// Why tensor cores: streaming x at the HBM rate (6.5 TB/s = 2.06 G rows/s of 784 pixels) needs
+// 2 * 784 * 30 flops per row = 97 TF/s of fp32 FMA, above the 72 TF/s FFMA peak; the FFMA2 kernel
+// (infer_small.cu) is shared-memory / issue bound at 19 % of HBM.  Z1 = X W1^T is a dense
+// contraction (M = rows, N = 32 neurons, K = pixels), run here in 3xTF32 (hi*hi + hi*lo + lo*hi,
+// fp32 accumulate; the fp32 parity bar of 1e-4 rules out 1xTF32).
+//
+// Design (one persistent CTA per SM, 480 threads, rows split into equal runs of 32-row blocks):
+//   warp 0      TMA producer of x: per K-block of 32 pixels, the x tile (4 boxes of 32 rows x 128 B,
+//               SWIZZLE_128B) into an 8-deep ring freed by the converters (16 KB per stage)
+//   warp 14     TMA producer of the W1 hi / lo K-blocks (RN split kept by the library next to the
+//               parameters, L2-resident) into a 4-deep ring freed by the MMA commits: the slow
+//               commit round trip never holds an x stage
+//   warps 2-9   converters (two groups alternating K-blocks), thread = row: read the row's 32 pixels from the swizzled tile, split
+//               them (truncation split: hi = x with the low 13 mantissa bits cleared, lo =
+//               rn_tf32(x - hi)) and store hi | lo into a 7-deep TMEM ring with tcgen05.st -- so
+//               the MMA reads its A operand from tensor memory (A in TMEM: no shared-memory read
+//               of the 128-row operand per MMA; micro/tc_atmem_test.cu: ~14 cycles per M=128 x
+//               N=32 x K=8 MMA marginal, vs ~61 with A in shared memory)
+//   warp 1      MMA issuer: 4 k-steps x 3 MMAs per K-block into one of two 32-column TMEM
+//               accumulators (double-buffered per 128-row tile); tcgen05.commit frees the ring
+//               slots and hands the finished accumulator to the epilogue
+//   warps 10-13 epilogue, thread = row: tcgen05.ld Z1 row, + b1, sigma_h, layer 2 (W2, b2 in
+//               shared memory, broadcast reads), sigma_o, store the O outputs
+// The x tile is read from HBM once; W1 (94 KB) is re-read from L2 per tile.
+#include <algorithm>
+#include <cstring>
+#include <mutex>
+
+#include "gemm_tc.cuh"
+#include "infer_tc.cuh"
+#include "kernels.cuh"
+#include "nf_common.cuh"
+#include "sm100_ptx.cuh"
+
+namespace nf {
+namespace {
+
+constexpr int kTileRows = 128;                      // M of the MMA, rows per tile
+constexpr int kBoxRows = 32;                        // rows per TMA box (tile tails in 32-row steps)
+constexpr int kKB = 32;                             // pixels per K-block (one 128-B swizzle row)
+constexpr int kStages = 8;                          // x ring depth (freed by the converters)
+constexpr int kWStages = 4;                         // W1 hi | lo ring depth (freed by the MMA commits)
+constexpr int kTStages = 7;                         // TMEM x-operand ring depth (64 columns: hi | lo)
+constexpr int kCG = 2;                              // converter warp groups (alternating K-blocks)
+constexpr int kXBytes = kTileRows * kKB * 4;        // 16 KB
+constexpr int kWBytes = 32 * kKB * 4;               // 4 KB (hi or lo)
+constexpr int kWStageBytes = 2 * kWBytes;           // 8 KB
+constexpr int kAccCol = kTStages * 64;              // accumulators after the x ring: 2 x 32 columns
+constexpr int kThreads = 32 * (2 + 4 * kCG + 4 + 1);  // + the W producer warp
+constexpr int kSmem = 1024 + kStages * kXBytes + kWStages * kWStageBytes + (32 * 33 + 64) * 4 + 512;
+
+struct InferTcParams {
+  int64_t n;      // rows
+  int64_t nblk;   // 32-row blocks
+  int n0, H, O, act_h, act_o;
+  int nkb;        // K-blocks of 32 pixels
+  int exp;        // experiment bits (NF_ITC_EXP, timing only): 1 no W reload, 2 no MMAs, 4 no conversion
+  const float *b1, *W2, *b2;  // in the parameter arena
+  float *out;
+};
+
+__device__ __forceinline__ void tmem_st32(uint32_t taddr, const float (&v)[32]) {
+  asm volatile(
+      "tcgen05.st.sync.aligned.32x32b.x32.b32 [%0], {%1, %2, %3, %4, %5, %6, %7, %8, %9, %10, %11, %12, %13, %14, "
+      "%15, %16, %17, %18, %19, %20, %21, %22, %23, %24, %25, %26, %27, %28, %29, %30, %31, %32};"
+      ::"r"(taddr), "f"(v[0]), "f"(v[1]), "f"(v[2]), "f"(v[3]), "f"(v[4]), "f"(v[5]), "f"(v[6]), "f"(v[7]),
+        "f"(v[8]), "f"(v[9]), "f"(v[10]), "f"(v[11]), "f"(v[12]), "f"(v[13]), "f"(v[14]), "f"(v[15]),
+        "f"(v[16]), "f"(v[17]), "f"(v[18]), "f"(v[19]), "f"(v[20]), "f"(v[21]), "f"(v[22]), "f"(v[23]),
+        "f"(v[24]), "f"(v[25]), "f"(v[26]), "f"(v[27]), "f"(v[28]), "f"(v[29]), "f"(v[30]), "f"(v[31])
+      : "memory");
+}
+// D (TMEM) += A (TMEM, M = 128 lanes x 8 columns) * B (shared-memory descriptor)
+__device__ __forceinline__ void mma_tf32_ts(uint32_t tmem_d, uint32_t tmem_a, uint64_t db, uint32_t idesc,
+                                            uint32_t acc) {
+  asm volatile(
+      "{\n\t.reg .pred p;\n\t"
+      "setp.ne.b32 p, %4, 0;\n\t"
+      "tcgen05.mma.cta_group::1.kind::tf32 [%0], [%1], %2, %3, p;\n\t}"
+      ::"r"(tmem_d), "r"(tmem_a), "l"(db), "r"(idesc), "r"(acc));
+}
+
+__global__ void __launch_bounds__(kThreads, 1)
+infer_tc_kernel(const InferTcParams p, const __grid_constant__ CUtensorMap tmX,
+                const __grid_constant__ CUtensorMap tmWh, const __grid_constant__ CUtensorMap tmWl) {
+  extern __shared__ __align__(1024) uint8_t smraw[];
+  uint8_t *ring = reinterpret_cast<uint8_t *>((reinterpret_cast<uintptr_t>(smraw) + 1023) & ~uintptr_t(1023));
+  uint8_t *wring = ring + kStages * kXBytes;
+  float *W2s = reinterpret_cast<float *>(wring + kWStages * kWStageBytes);  // [32][33]
+  float *b1s = W2s + 32 * 33, *b2s = b1s + 32;
+  uint64_t *full = reinterpret_cast<uint64_t *>(b2s + 32);
+  uint64_t *empty = full + kStages, *tfull = empty + kStages, *tempty = tfull + kTStages;
+  uint64_t *afull = tempty + kTStages, *aempty = afull + 2;
+  uint64_t *wfull = aempty + 2, *wempty = wfull + kWStages;
+  uint32_t *tslot = reinterpret_cast<uint32_t *>(wempty + kWStages);
+  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+
+  // this CTA's rows: an equal share of whole 32-row blocks
+  const int64_t bb = (int64_t)blockIdx.x * p.nblk / gridDim.x, be = (int64_t)(blockIdx.x + 1) * p.nblk / gridDim.x;
+  const int64_t r0 = bb * kBoxRows, r1 = min(p.n, be * kBoxRows);
+  const int ntiles = r1 > r0 ? (int)((r1 - r0 + kTileRows - 1) / kTileRows) : 0;
+
+  if (tid == 0) {
+    for (int i = 0; i < kStages; ++i) {
+      ptx::mbar_init(&full[i], 1);
+      ptx::mbar_init(&empty[i], 4);  // one converter group's four warps have read the x tile
+    }
+    for (int i = 0; i < kWStages; ++i) {
+      ptx::mbar_init(&wfull[i], 1);
+      ptx::mbar_init(&wempty[i], 1);  // the MMA commit
+    }
+    for (int i = 0; i < kTStages; ++i) {
+      ptx::mbar_init(&tfull[i], 4);
+      ptx::mbar_init(&tempty[i], 1);
+    }
+    for (int i = 0; i < 2; ++i) {
+      ptx::mbar_init(&afull[i], 1);
+      ptx::mbar_init(&aempty[i], 4);
+    }
+    ptx::fence_mbar_init();
+    ptx::prefetch_tensormap(&tmX);
+    ptx::prefetch_tensormap(&tmWh);
+    ptx::prefetch_tensormap(&tmWl);
+  }
+  if (warp == 1) {
+    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(ptx::smem_u32(tslot)),
+                 "r"(512u) : "memory");
+    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;" ::: "memory");
+  }
+  for (int i = tid; i < 32 * 32; i += kThreads) {
+    const int o = i >> 5, j = i & 31;
+    W2s[o * 33 + j] = (o < p.O && j < p.H) ? p.W2[o * p.H + j] : 0.0f;
+  }
+  if (tid < 32) {
+    b1s[tid] = tid < p.H ? p.b1[tid] : 0.0f;
+    b2s[tid] = tid < p.O ? p.b2[tid] : 0.0f;
+  }
+  tc::tc_fence_before();
+  __syncthreads();
+  tc::tc_fence_after();
+  const uint32_t tmem = *tslot;
+
+  if (warp == 0) {
+    // ---- TMA producer of the x tiles
+    if (lane == 0) {
+      int g = 0;
+      for (int i = 0; i < ntiles; ++i) {
+        const int64_t row = r0 + (int64_t)i * kTileRows;
+        const int64_t rows_here = r1 - row < kTileRows ? r1 - row : kTileRows;
+        const int nbox = (int)((rows_here + kBoxRows - 1) / kBoxRows);
+        for (int kb = 0; kb < p.nkb; ++kb, ++g) {
+          const int s = g % kStages;
+          ptx::mbar_wait(&empty[s], ((g / kStages) & 1) ^ 1);
+          uint8_t *st = ring + s * kXBytes;
+          ptx::mbar_arrive_expect_tx(&full[s], (uint32_t)(nbox * kBoxRows * kKB * 4));
+          for (int b = 0; b < nbox; ++b)
+            ptx::tma_load_2d(st + b * (kBoxRows * 128), &tmX, &full[s], kb * kKB, (int)(row + b * kBoxRows));
+        }
+      }
+    }
+  } else if (warp == kThreads / 32 - 1) {
+    // ---- TMA producer of the W1 hi | lo K-blocks (L2-resident)
+    if (lane == 0 && !(p.exp & 8)) {
+      int g = 0;
+      for (int i = 0; i < ntiles; ++i) {
+        for (int kb = 0; kb < p.nkb; ++kb, ++g) {
+          const int w = g % kWStages;
+          ptx::mbar_wait(&wempty[w], ((g / kWStages) & 1) ^ 1);
+          uint8_t *st = wring + w * kWStageBytes;
+          if ((p.exp & 1) && g >= kWStages) {  // (timing experiment: no reload)
+            ptx::mbar_arrive(&wfull[w]);
+            continue;
+          }
+          ptx::mbar_arrive_expect_tx(&wfull[w], (uint32_t)kWStageBytes);
+          ptx::tma_load_2d(st, &tmWh, &wfull[w], kb * kKB, 0);
+          ptx::tma_load_2d(st + kWBytes, &tmWl, &wfull[w], kb * kKB, 0);
+        }
+      }
+    }
+  } else if (warp == 1) {
+    // ---- MMA issuer
+    if (lane == 0 && !(p.exp & 8)) {
+      constexpr uint32_t idesc = tc::idesc_tf32(kTileRows, 32, false, false);
+      int g = 0;
+      for (int i = 0; i < ntiles; ++i) {
+        const int a = i & 1;
+        ptx::mbar_wait(&aempty[a], ((i >> 1) & 1) ^ 1);
+        tc::tc_fence_after();
+        const uint32_t d = tmem + kAccCol + 32u * a;
+        for (int kb = 0; kb < p.nkb; ++kb, ++g) {
+          const int w = g % kWStages, t = g % kTStages;
+          ptx::mbar_wait(&wfull[w], (g / kWStages) & 1);    // W K-block landed
+          ptx::mbar_wait(&tfull[t], (g / kTStages) & 1);    // x K-block split into TMEM
+          tc::tc_fence_after();
+          const uint32_t sw = ptx::smem_u32(wring + w * kWStageBytes);
+#pragma unroll
+          for (int ks = 0; ks < kKB / 8; ++ks) {
+            if (p.exp & 2) break;
+            const uint64_t bh = tc::smem_desc(sw + 32u * ks, 16, 1024, 2);
+            const uint64_t bl = tc::smem_desc(sw + kWBytes + 32u * ks, 16, 1024, 2);
+            const uint32_t ah = tmem + 64u * t + 8u * ks, al = ah + 32u;
+            mma_tf32_ts(d, al, bh, idesc, (kb | ks) ? 1u : 0u);  // small terms first
+            mma_tf32_ts(d, ah, bl, idesc, 1u);
+            mma_tf32_ts(d, ah, bh, idesc, 1u);
+          }
+          tc::mma_commit(&wempty[w]);
+          tc::mma_commit(&tempty[t]);
+          if (kb == p.nkb - 1) tc::mma_commit(&afull[a]);
+        }
+      }
+    }
+  } else if (warp < 2 + 4 * kCG) {
+    // ---- converters: thread = row 32 q + lane of the tile (TMEM lane quadrant q = warp % 4); group
+    //      cg takes the K-blocks g = cg mod kCG
+    const int q = warp & 3, cg = (warp - 2) >> 2;
+    int g = 0;
+    for (int i = 0; i < ntiles; ++i) {
+      for (int kb = 0; kb < p.nkb; ++kb, ++g) {
+        if (g % kCG != cg) continue;
+        const int s = g % kStages, t = g % kTStages;
+        ptx::mbar_wait(&full[s], (g / kStages) & 1);
+        if (p.exp & 8) {  // (timing experiment: x streaming alone)
+          __syncwarp();
+          if (lane == 0) ptx::mbar_arrive(&empty[s]);
+          continue;
+        }
+        ptx::mbar_wait(&tempty[t], ((g / kTStages) & 1) ^ 1);
+        // this row's 128 B in the swizzled box q: 16-B chunk c at physical chunk c ^ (row % 8)
+        const uint8_t *xr = ring + s * kXBytes + q * (kBoxRows * 128) + lane * 128;
+        float hi[32], lo[32];
+        if (!(p.exp & 4)) {
+#pragma unroll
+        for (int c = 0; c < 8; ++c) {
+          const float4 v = *reinterpret_cast<const float4 *>(xr + ((c ^ (lane & 7)) << 4));
+          const float xv[4] = {v.x, v.y, v.z, v.w};
+#pragma unroll
+          for (int e = 0; e < 4; ++e) {
+            hi[4 * c + e] = __uint_as_float(__float_as_uint(xv[e]) & 0xffffe000u);
+            lo[4 * c + e] = tf32_lo(xv[e]);
+          }
+        }
+        const uint32_t ta = tmem + ((uint32_t)(32 * q) << 16) + 64u * t;
+        tmem_st32(ta, hi);
+        tmem_st32(ta + 32u, lo);
+        asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory");
+        }
+        tc::tc_fence_before();
+        __syncwarp();
+        if (lane == 0) {
+          ptx::mbar_arrive(&empty[s]);
+          ptx::mbar_arrive(&tfull[t]);
+        }
+      }
+    }
+  } else if (warp < 2 + 4 * kCG + 4 && !(p.exp & 8)) {
+    // ---- epilogue: thread = row 32 q + lane of the tile
+    const int q = warp & 3;
+    const int H = p.H, O = p.O;
+    for (int i = 0; i < ntiles; ++i) {
+      const int a = i & 1;
+      ptx::mbar_wait(&afull[a], (i >> 1) & 1);
+      tc::tc_fence_after();
+      float z[32];
+      tc::tmem_ld32(tmem + ((uint32_t)(32 * q) << 16) + kAccCol + 32u * a, z);
+      tc::tc_fence_before();
+      __syncwarp();
+      if (lane == 0) ptx::mbar_arrive(&aempty[a]);
+      const int64_t row = r0 + (int64_t)i * kTileRows + 32 * q + lane;
+      if (row < r1) {
+        float a1[32];
+#pragma unroll
+        for (int j = 0; j < 32; ++j) a1[j] = j < H ? act_only(p.act_h, z[j] + b1s[j]) : 0.0f;
+        float *orow = p.out + row * O;
+        for (int o = 0; o < O; ++o) {
+          const float *w2 = W2s + o * 33;
+          float c0 = b2s[o], c1 = 0.0f, c2 = 0.0f, c3 = 0.0f;
+#pragma unroll
+          for (int j = 0; j < 32; j += 4) {
+            c0 = fmaf(w2[j], a1[j], c0);
+            c1 = fmaf(w2[j + 1], a1[j + 1], c1);
+            c2 = fmaf(w2[j + 2], a1[j + 2], c2);
+            c3 = fmaf(w2[j + 3], a1[j + 3], c3);
+          }
+          orow[o] = act_only(p.act_o, (c0 + c1) + (c2 + c3));
+        }
+      }
+    }
+  }
+  tc::tc_fence_before();
+  __syncthreads();
+  if (warp == 1) {
+    tc::tc_fence_after();
+    asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem), "r"(512u) : "memory");
+  }
+}
+
+}  // namespace
+
+bool infer_tc_applicable(const std::vector<int> &dims, const float *X) {
+  return dims.size() == 3 && dims[1] <= 32 && dims[2] <= 32 && dims[0] % 4 == 0 && dims[0] >= kKB &&
+         (reinterpret_cast<uintptr_t>(X) & 15) == 0 && getenv("NF_INFER_SIMT") == nullptr;
+}
+
+cudaError_t infer_tc(cudaStream_t st, const std::vector<int> &dims, int act_h, int act_o, const float *params,
+                     const float *W1hi, const float *W1lo, const float *X, int64_t n, float *out) {
+  const int n0 = dims[0], H = dims[1], O = dims[2];
+  {
+    cudaError_t e = set_max_smem(reinterpret_cast<const void *>(infer_tc_kernel), kSmem);
+    if (e != cudaSuccess) return e;
+  }
+  // tensor maps, cached per (pointer, shape): encoding costs host microseconds per call
+  static std::mutex mu;
+  static struct {
+    const void *x = nullptr, *wh = nullptr, *wl = nullptr;
+    int64_t n = 0;
+    int n0 = 0, H = 0;
+    CUtensorMap mX, mWh, mWl;
+  } c;
+  CUtensorMap mX, mWh, mWl;
+  {
+    std::lock_guard<std::mutex> lk(mu);
+    if (c.x != X || c.n != n || c.n0 != n0) {
+      if (!encode_tmap_2d_f32(&c.mX, X, (uint64_t)n0, (uint64_t)n, (uint64_t)n0 * 4, kKB, kBoxRows,
+                              CU_TENSOR_MAP_SWIZZLE_128B))
+        return cudaErrorInvalidValue;
+      c.x = X; c.n = n; c.n0 = n0;
+    }
+    if (c.wh != W1hi || c.wl != W1lo || c.H != H || c.n0 != n0) {
+      if (!encode_tmap_2d_f32(&c.mWh, W1hi, (uint64_t)n0, (uint64_t)H, (uint64_t)n0 * 4, kKB, 32,
+                              CU_TENSOR_MAP_SWIZZLE_128B) ||
+          !encode_tmap_2d_f32(&c.mWl, W1lo, (uint64_t)n0, (uint64_t)H, (uint64_t)n0 * 4, kKB, 32,
+                              CU_TENSOR_MAP_SWIZZLE_128B))
+        return cudaErrorInvalidValue;
+      c.wh = W1hi; c.wl = W1lo; c.H = H;
+    }
+    mX = c.mX; mWh = c.mWh; mWl = c.mWl;
+  }
+  InferTcParams p{};
+  p.n = n;
+  p.nblk = (n + kBoxRows - 1) / kBoxRows;
+  p.n0 = n0; p.H = H; p.O = O; p.act_h = act_h; p.act_o = act_o;
+  p.nkb = (n0 + kKB - 1) / kKB;
+  p.b1 = params + (int64_t)H * n0;
+  p.W2 = p.b1 + H;
+  p.b2 = p.W2 + (int64_t)O * H;
+  p.out = out;
+  p.exp = getenv("NF_ITC_EXP") ? atoi(getenv("NF_ITC_EXP")) : 0;
+  const int blocks = (int)std::max<int64_t>(1, std::min<int64_t>(p.nblk, 148));
+  infer_tc_kernel<<<blocks, kThreads, kSmem, st>>>(p, mX, mWh, mWl);
+  count_launch();
+  log_launch(reinterpret_cast<const void *>(infer_tc_kernel), dim3(blocks), dim3(kThreads), kSmem);
+  return cudaGetLastError();
+}
+
+}  // namespace nf
