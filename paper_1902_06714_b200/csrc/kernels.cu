@@ -7,6 +7,7 @@
 #include <cstring>
 
 #include "gemm_tc.cuh"
+#include "gemm_hmma.cuh"
 #include "kernels.cuh"
 
 namespace nf {
@@ -98,9 +99,64 @@ cudaError_t launch_cfg(cudaStream_t st, GemmArgs g, const Epi &epi, const Worksp
   return cudaGetLastError();
 }
 
+// Warp-level tensor-core engine (gemm_hmma.cuh) for small contractions (<= 2 GFLOP: config 4's
+// layers), opt-in NF_HMMA=1: parity-green, but config 4 ran 433 vs 149 us per TF32 step against
+// the tcgen05 kernels (profiles/r02_hmma_gemm_experiment.txt)
+bool tc_enabled();
+bool hmma_engine(int M, int N, int K) {
+  const char *e = getenv("NF_HMMA");
+  if (!tc_enabled() || !e || atoi(e) == 0) return false;
+  return M >= 16 && N >= 16 && K >= 64 && 2.0 * M * N * K <= 2.0e9;
+}
+
+template <bool AK, bool BKM, class Epi>
+cudaError_t launch_hmma(cudaStream_t st, GemmArgs g, const Epi &epi, const Workspace &ws) {
+  constexpr int BM = 64, BN = 64, BK = 32;
+  const int tm = (g.M + BM - 1) / BM, tn = (g.N + BN - 1) / BN;
+  const int64_t tiles = (int64_t)tm * tn;
+  // split-K (fixed-order partials + splitk_epilogue) only under half a wave: the forward / delta
+  // GEMMs of config 4 (128 tiles) run unsplit, its weight gradients (20 tiles, K = 2048) split
+  int splits = 1;
+  if (tiles < kSMs / 2 && g.K >= 256) {
+    splits = (int)std::min<int64_t>(kSMs / tiles, g.K / 128);
+    while (splits > 1 && (size_t)splits * g.M * g.N > ws.partial_floats) --splits;
+    splits = std::max(splits, 1);
+  }
+  int kchunk = (g.K + splits - 1) / splits;
+  kchunk = (kchunk + BK - 1) / BK * BK;
+  splits = std::max(1, (g.K + kchunk - 1) / kchunk);
+  g.kchunk = splits > 1 ? kchunk : std::max(g.K, 1);
+  g.partial = splits > 1 ? ws.partial : nullptr;
+  dim3 grid(tn, tm, splits);
+  g_note = note(epi_note(epi), splits > 1 ? (ws.math == 1 ? "hmma1 splitk-partial" : "hmma3 splitk-partial")
+                                          : (ws.math == 1 ? "hmma1" : "hmma3"));
+  g_last_engine = ws.math == 1 ? ENGINE_HMMA1 : ENGINE_HMMA3;
+  auto k1 = gemm_hmma<AK, BKM, 1, Epi>;
+  auto k3 = gemm_hmma<AK, BKM, 3, Epi>;
+  {
+    cudaError_t e = set_max_smem(reinterpret_cast<const void *>(ws.math == 1 ? k1 : k3), hm::SMEM);
+    if (e != cudaSuccess) return e;
+  }
+  // 16-B cp.async copies when every operand row starts 16-B aligned
+  const int vec = (g.lda % 4 == 0 && g.ldb % 4 == 0 && (reinterpret_cast<uintptr_t>(g.A) & 15) == 0 &&
+                   (reinterpret_cast<uintptr_t>(g.B) & 15) == 0) ? 1 : 0;
+  cudaError_t e = ws.math == 1 ? launch_k(k1, grid, dim3(256), hm::SMEM, st, g, epi, vec)
+                               : launch_k(k3, grid, dim3(256), hm::SMEM, st, g, epi, vec);
+  if (e != cudaSuccess) return e;
+  if (splits > 1) {
+    const int64_t MN = (int64_t)g.M * g.N;
+    const int blocks = (int)std::min<int64_t>((MN + 255) / 256, 4 * kSMs);
+    e = launch_k(splitk_epilogue<Epi>, dim3(blocks), dim3(256), 0, st, ws.partial, splits, g.M, g.N, epi);
+    if (e != cudaSuccess) return e;
+  }
+  return cudaGetLastError();
+}
+
 template <bool AK, bool BKM, class Epi>
 cudaError_t run_gemm(cudaStream_t st, GemmArgs g, const Epi &epi, const Workspace &ws) {
   if (g.M <= 0 || g.N <= 0) return cudaSuccess;
+  if (ws.math != 2 && hmma_engine(g.M, g.N, g.K)) return launch_hmma<AK, BKM>(st, g, epi, ws);
+  g_last_engine = ENGINE_SIMT;
   switch (choose_cfg(g.M, g.N)) {
     case CFG_L: return launch_cfg<128, 128, 8, 8, 8, AK, BKM>(st, g, epi, ws);
     case CFG_S: return launch_cfg<128, 32, 16, 8, 2, AK, BKM>(st, g, epi, ws);
@@ -133,7 +189,7 @@ bool tc_ok(const TcOp &o) { return (reinterpret_cast<uintptr_t>(o.p) & 15) == 0 
 // The tensor-core path is used for contractions whose three extents are all >= 64
 // (the output layer's 10-wide GEMMs stay on the SIMT kernels).
 bool use_tc(int M, int N, int K, const TcOp &a, const TcOp &b) {
-  return tc_enabled() && M >= 64 && N >= 64 && K >= 64 && tc_ok(a) && tc_ok(b);
+  return tc_enabled() && M >= 64 && N >= 64 && K >= 64 && tc_ok(a) && tc_ok(b) && !hmma_engine(M, N, K);
 }
 
 bool make_map(CUtensorMap *m, const TcOp &o, int rows, int K, int box_rows) {

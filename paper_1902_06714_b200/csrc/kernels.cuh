@@ -33,7 +33,7 @@ struct Workspace {
 };
 
 // Which engine ran the last gemm_* call (for tests / the bench's kernel attribution).
-enum Engine { ENGINE_SIMT = 0, ENGINE_TC1 = 1, ENGINE_TC3 = 3 };
+enum Engine { ENGINE_SIMT = 0, ENGINE_TC1 = 1, ENGINE_TC3 = 3, ENGINE_HMMA1 = 11, ENGINE_HMMA3 = 13 };
 Engine last_engine();
 
 // K1: Z = A[M][K] * W[N][K]^T, epilogue EpiFwd.

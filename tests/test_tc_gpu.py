@@ -26,6 +26,17 @@ TC_SHAPES = [
 ]
 
 
+@pytest.fixture(autouse=True, params=["tcgen05", "hmma"])
+def engine(request, monkeypatch):
+    """Every test runs on both tensor-core engines: tcgen05 (the default) and the opt-in warp-level
+    MMA GEMM (gemm_hmma.cuh, NF_HMMA=1: the contractions of <= 2 GFLOP)."""
+    if request.param == "hmma":
+        monkeypatch.setenv("NF_HMMA", "1")
+    else:
+        monkeypatch.delenv("NF_HMMA", raising=False)
+    return request.param
+
+
 def dev(a):
     return torch.from_numpy(np.ascontiguousarray(a)).cuda()
 
