@@ -296,6 +296,206 @@ infer_tc_kernel(const InferTcParams p, const __grid_constant__ CUtensorMap tmX,
   }
 }
 
+// ---- transposed formulation (infer_tcT_kernel, the default): Z1^T = W1 X^T, one MMA per
+// (M = 128 neuron lanes, N = 128 rows, K = 8 pixels): a quarter of the M=128 x N=32 instructions
+// per row (the instruction cost, not the MMA width, bounds the N = 32 form).  W1 (30 rows of the
+// A operand) is read through a K-major descriptor whose rows 32..127 fall on neighbouring shared
+// memory: those accumulator lanes are garbage and never read.  x is the B operand straight from
+// its TMA tile (the tensor core truncates it: the hi part), the converters write x_lo =
+// rn_tf32(x - trunc(x)) into a second tile of the same swizzled layout (elementwise, conflict-free).
+// One warp reads the accumulator (lanes = neurons 0..31, columns = rows) and transposes it through
+// shared memory; the epilogue warps (thread = row) finish layers 1 and 2.
+namespace tt {
+#ifndef NF_ITT_ROWS
+#define NF_ITT_ROWS 128
+#endif
+constexpr int kRows = NF_ITT_ROWS;                // rows per tile = N of the MMA (128 or 256)
+constexpr int kStages = kRows == 256 ? 2 : 4;
+constexpr int kXBytes = kRows * kKB * 4;          // 16 KB
+constexpr int kWBytes = 32 * kKB * 4;             // 4 KB: the 32 rows TMA writes of a W K-block
+constexpr int kStageBytes = 2 * kXBytes + 2 * kWBytes;   // x | x_lo | W hi | W lo = 40 KB
+constexpr int kOverread = 128 * 128 - kWBytes;    // A descriptor rows 32..127 past the last W block
+constexpr int kThreads = 32 * (1 + 1 + 4 + 4);    // TMA, MMA, 4 converter warps, 4 epilogue warps
+constexpr int kSmem = 1024 + kStages * kStageBytes + kOverread + (kRows * 33 + 32 * 33 + 64) * 4 + 256;
+}  // namespace tt
+
+__global__ void __launch_bounds__(tt::kThreads, 1)
+infer_tcT_kernel(const InferTcParams p, const __grid_constant__ CUtensorMap tmX,
+                 const __grid_constant__ CUtensorMap tmWh, const __grid_constant__ CUtensorMap tmWl) {
+  extern __shared__ __align__(1024) uint8_t smraw[];
+  uint8_t *ring = reinterpret_cast<uint8_t *>((reinterpret_cast<uintptr_t>(smraw) + 1023) & ~uintptr_t(1023));
+  float *zt = reinterpret_cast<float *>(ring + tt::kStages * tt::kStageBytes + tt::kOverread);  // [rows][33]
+  float *W2s = zt + tt::kRows * 33;                 // [32][33]
+  float *b1s = W2s + 32 * 33, *b2s = b1s + 32;
+  uint64_t *full = reinterpret_cast<uint64_t *>(b2s + 32);
+  uint64_t *cvt = full + tt::kStages, *empty = cvt + tt::kStages, *afull = empty + tt::kStages, *aempty = afull + 2;
+  uint32_t *tslot = reinterpret_cast<uint32_t *>(aempty + 2);
+  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+
+  const int64_t bb = (int64_t)blockIdx.x * p.nblk / gridDim.x, be = (int64_t)(blockIdx.x + 1) * p.nblk / gridDim.x;
+  const int64_t r0 = bb * kBoxRows, r1 = min(p.n, be * kBoxRows);
+  const int ntiles = r1 > r0 ? (int)((r1 - r0 + tt::kRows - 1) / tt::kRows) : 0;
+
+  if (tid == 0) {
+    for (int i = 0; i < tt::kStages; ++i) {
+      ptx::mbar_init(&full[i], 1);
+      ptx::mbar_init(&cvt[i], 4);
+      ptx::mbar_init(&empty[i], 1);
+    }
+    for (int i = 0; i < 2; ++i) {
+      ptx::mbar_init(&afull[i], 1);
+      ptx::mbar_init(&aempty[i], 1);
+    }
+    ptx::fence_mbar_init();
+    ptx::prefetch_tensormap(&tmX);
+    ptx::prefetch_tensormap(&tmWh);
+    ptx::prefetch_tensormap(&tmWl);
+  }
+  if (warp == 1) {
+    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(ptx::smem_u32(tslot)),
+                 "r"((uint32_t)(2 * tt::kRows)) : "memory");
+    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;" ::: "memory");
+  }
+  for (int i = tid; i < 32 * 32; i += tt::kThreads) {
+    const int o = i >> 5, j = i & 31;
+    W2s[o * 33 + j] = (o < p.O && j < p.H) ? p.W2[o * p.H + j] : 0.0f;
+  }
+  if (tid < 32) {
+    b1s[tid] = tid < p.H ? p.b1[tid] : 0.0f;
+    b2s[tid] = tid < p.O ? p.b2[tid] : 0.0f;
+  }
+  tc::tc_fence_before();
+  __syncthreads();
+  tc::tc_fence_after();
+  const uint32_t tmem = *tslot;
+  auto sx = [&](int s) { return ring + s * tt::kStageBytes; };           // x tile (B hi)
+  auto sxl = [&](int s) { return ring + s * tt::kStageBytes + tt::kXBytes; };  // x_lo tile (B lo)
+  auto swh = [&](int s) { return ring + s * tt::kStageBytes + 2 * tt::kXBytes; };
+  auto swl = [&](int s) { return ring + s * tt::kStageBytes + 2 * tt::kXBytes + tt::kWBytes; };
+
+  if (warp == 0) {
+    if (lane == 0) {  // ---- TMA: x tile (4 boxes of 32 rows) + W1 hi / lo K-blocks
+      int g = 0;
+      for (int i = 0; i < ntiles; ++i) {
+        const int64_t row = r0 + (int64_t)i * tt::kRows;
+        const int64_t rows_here = r1 - row < tt::kRows ? r1 - row : tt::kRows;
+        const int nbox = (int)((rows_here + kBoxRows - 1) / kBoxRows);
+        for (int kb = 0; kb < p.nkb; ++kb, ++g) {
+          const int s = g % tt::kStages;
+          ptx::mbar_wait(&empty[s], ((g / tt::kStages) & 1) ^ 1);
+          ptx::mbar_arrive_expect_tx(&full[s], (uint32_t)(nbox * kBoxRows * 128 + 2 * tt::kWBytes));
+          for (int b = 0; b < nbox; ++b)
+            ptx::tma_load_2d(sx(s) + b * (kBoxRows * 128), &tmX, &full[s], kb * kKB, (int)(row + b * kBoxRows));
+          ptx::tma_load_2d(swh(s), &tmWh, &full[s], kb * kKB, 0);
+          ptx::tma_load_2d(swl(s), &tmWl, &full[s], kb * kKB, 0);
+        }
+      }
+    }
+  } else if (warp == 1) {
+    if (lane == 0) {  // ---- MMA issuer
+      constexpr uint32_t idesc = tc::idesc_tf32(128, tt::kRows, false, false);
+      int g = 0;
+      for (int i = 0; i < ntiles; ++i) {
+        const int a = i & 1;
+        ptx::mbar_wait(&aempty[a], ((i >> 1) & 1) ^ 1);
+        tc::tc_fence_after();
+        const uint32_t d = tmem + (uint32_t)(tt::kRows * a);
+        for (int kb = 0; kb < p.nkb; ++kb, ++g) {
+          const int s = g % tt::kStages;
+          ptx::mbar_wait(&cvt[s], (g / tt::kStages) & 1);  // (x landed and its lo part written)
+          tc::tc_fence_after();
+          const uint32_t xh = ptx::smem_u32(sx(s)), xl = ptx::smem_u32(sxl(s));
+          const uint32_t wh = ptx::smem_u32(swh(s)), wl = ptx::smem_u32(swl(s));
+#pragma unroll
+          for (int ks = 0; ks < kKB / 8; ++ks) {
+            if (p.exp & 2) break;
+            const uint64_t dwh = tc::smem_desc(wh + 32u * ks, 16, 1024, 2), dwl = tc::smem_desc(wl + 32u * ks, 16, 1024, 2);
+            const uint64_t dxh = tc::smem_desc(xh + 32u * ks, 16, 1024, 2), dxl = tc::smem_desc(xl + 32u * ks, 16, 1024, 2);
+            tc::mma_tf32(d, dwh, dxl, idesc, (kb | ks) ? 1u : 0u);  // small terms first
+            tc::mma_tf32(d, dwl, dxh, idesc, 1u);
+            tc::mma_tf32(d, dwh, dxh, idesc, 1u);
+          }
+          tc::mma_commit(&empty[s]);
+          if (kb == p.nkb - 1) tc::mma_commit(&afull[a]);
+        }
+      }
+    }
+  } else if (warp < 6) {
+    // ---- converters: x_lo = rn_tf32(x - trunc(x)), elementwise over the swizzled tile (the
+    //      layouts match: same byte offset), 128 B per thread per K-block
+    const int ct = tid - 64;
+    int g = 0;
+    for (int i = 0; i < ntiles; ++i) {
+      for (int kb = 0; kb < p.nkb; ++kb, ++g) {
+        const int s = g % tt::kStages;
+        ptx::mbar_wait(&full[s], (g / tt::kStages) & 1);
+        const float4 *src = reinterpret_cast<const float4 *>(sx(s));
+        float4 *dst = reinterpret_cast<float4 *>(sxl(s));
+#pragma unroll
+        for (int c = 0; c < tt::kXBytes / 16 / 128; ++c) {
+          if (p.exp & 4) break;
+          const float4 v = src[ct + 128 * c];
+          dst[ct + 128 * c] = make_float4(tf32_lo(v.x), tf32_lo(v.y), tf32_lo(v.z), tf32_lo(v.w));
+        }
+        ptx::fence_proxy_async_smem();  // generic-proxy writes -> visible to the tensor core
+        __syncwarp();
+        if (lane == 0) ptx::mbar_arrive(&cvt[s]);
+      }
+    }
+  } else {
+    // ---- epilogue: warp 6 + (the warp of TMEM lane quadrant 0) reads Z1^T rows 0..31 (neurons)
+    //      x 128 columns (rows) and transposes them into zt; then thread = row finishes
+    const int q = warp & 3, et = tid - 192;  // q == 0: warp 8
+    const int H = p.H, O = p.O;
+    for (int i = 0; i < ntiles; ++i) {
+      const int a = i & 1;
+      if (q == 0) {
+        ptx::mbar_wait(&afull[a], (i >> 1) & 1);
+        tc::tc_fence_after();
+#pragma unroll
+        for (int c0 = 0; c0 < tt::kRows; c0 += 32) {
+          float z[32];
+          tc::tmem_ld32(tmem + (uint32_t)(tt::kRows * a + c0), z);  // lane = neuron, z[c] = row c0 + c
+#pragma unroll
+          for (int c = 0; c < 32; ++c) zt[(c0 + c) * 33 + lane] = z[c];
+        }
+        tc::tc_fence_before();
+        __syncwarp();
+        if (lane == 0) ptx::mbar_arrive(&aempty[a]);
+      }
+      asm volatile("bar.sync 1, 128;" ::: "memory");  // zt filled
+      for (int rr = et; rr < tt::kRows; rr += 128) {
+      const int64_t row = r0 + (int64_t)i * tt::kRows + rr;
+      if (row < r1) {
+        float a1[32];
+#pragma unroll
+        for (int j = 0; j < 32; ++j) a1[j] = j < H ? act_only(p.act_h, zt[rr * 33 + j] + b1s[j]) : 0.0f;
+        float *orow = p.out + row * O;
+        for (int o = 0; o < O; ++o) {
+          const float *w2 = W2s + o * 33;
+          float c0 = b2s[o], c1 = 0.0f, c2 = 0.0f, c3 = 0.0f;
+#pragma unroll
+          for (int j = 0; j < 32; j += 4) {
+            c0 = fmaf(w2[j], a1[j], c0);
+            c1 = fmaf(w2[j + 1], a1[j + 1], c1);
+            c2 = fmaf(w2[j + 2], a1[j + 2], c2);
+            c3 = fmaf(w2[j + 3], a1[j + 3], c3);
+          }
+          orow[o] = act_only(p.act_o, (c0 + c1) + (c2 + c3));
+        }
+      }
+      }
+      asm volatile("bar.sync 1, 128;" ::: "memory");  // zt free for the next tile
+    }
+  }
+  tc::tc_fence_before();
+  __syncthreads();
+  if (warp == 1) {
+    tc::tc_fence_after();
+    asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem), "r"((uint32_t)(2 * tt::kRows)) : "memory");
+  }
+}
+
 }  // namespace
 
 bool infer_tc_applicable(const std::vector<int> &dims, const float *X) {
@@ -308,6 +508,7 @@ cudaError_t infer_tc(cudaStream_t st, const std::vector<int> &dims, int act_h, i
   const int n0 = dims[0], H = dims[1], O = dims[2];
   {
     cudaError_t e = set_max_smem(reinterpret_cast<const void *>(infer_tc_kernel), kSmem);
+    if (e == cudaSuccess) e = set_max_smem(reinterpret_cast<const void *>(infer_tcT_kernel), tt::kSmem);
     if (e != cudaSuccess) return e;
   }
   // tensor maps, cached per (pointer, shape): encoding costs host microseconds per call
@@ -348,6 +549,13 @@ cudaError_t infer_tc(cudaStream_t st, const std::vector<int> &dims, int act_h, i
   p.out = out;
   p.exp = getenv("NF_ITC_EXP") ? atoi(getenv("NF_ITC_EXP")) : 0;
   const int blocks = (int)std::max<int64_t>(1, std::min<int64_t>(p.nblk, 148));
+  static const int form = getenv("NF_INFER_TC_FORM") ? atoi(getenv("NF_INFER_TC_FORM")) : 1;
+  if (form == 1) {  // transposed: Z1^T = W1 X^T, N = 128 rows per MMA (default)
+    infer_tcT_kernel<<<blocks, tt::kThreads, tt::kSmem, st>>>(p, mX, mWh, mWl);
+    count_launch();
+    log_launch(reinterpret_cast<const void *>(infer_tcT_kernel), dim3(blocks), dim3(tt::kThreads), tt::kSmem);
+    return cudaGetLastError();
+  }
   infer_tc_kernel<<<blocks, kThreads, kSmem, st>>>(p, mX, mWh, mWl);
   count_launch();
   log_launch(reinterpret_cast<const void *>(infer_tc_kernel), dim3(blocks), dim3(kThreads), kSmem);

@@ -429,7 +429,7 @@ def test_tensor_core_inference(dims, act, n, monkeypatch):
     out = net.output(dev(x)).cpu().numpy()
     log = nf.nf_debug_log_read()
     nf.nf_debug_log_enable(False)
-    assert any("infer_tc_kernel" in l for l in log), log
+    assert any("infer_tc" in l for l in log), log
     rows = np.arange(n) if n <= 5000 else np.random.default_rng(0).choice(n, 4000, replace=False)
     ref = oracle.Oracle(dims, act).output(p, np.ascontiguousarray(x[rows]))
     assert rel_err(out[rows], ref) <= FP32_BAR
