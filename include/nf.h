@@ -58,10 +58,14 @@ enum {
 };
 
 /* Numerics mode of the contractions (nf_set_math).
- *   NF_MATH_FP32 : fp32 storage, fp32 FMA accumulation (default; the paper's
- *                  real32).  Parity bar 1e-4 (BASELINE.json).
- *   NF_MATH_TF32 : TF32 tensor-core tiles, fp32 accumulate, where a kernel
- *                  has them (configs 3 and 5).  Parity bar 5e-3.
+ *   NF_MATH_FP32 : fp32 storage; fp32 FMA accumulation or 3xTF32 tensor-core
+ *                  tiles (hi*hi + hi*lo + lo*hi, fp32 accumulate) (default; the
+ *                  paper's real32).  Parity bar 1e-4 at tau = 0.1
+ *                  (BASELINE.json; R14).
+ *   NF_MATH_TF32 : 1xTF32 tensor-core tiles on round-to-nearest TF32 operands,
+ *                  fp32 accumulate, wherever a contraction has all extents >= 64
+ *                  (configs 3, 4 and 5; narrower ones stay fp32).  Parity bar
+ *                  5e-3 normwise (tau = 1; R14b).
  *   NF_MATH_FP64 : the paper's real64 build: parameters,
  *                  activations, deltas and every sum in double on the FP64
  *                  units.  Inputs, targets and results still cross this ABI
@@ -69,7 +73,8 @@ enum {
  *                  the parameters are held in double while the mode is set
  *                  (nf_get_params rounds them, nf_set_params widens them) and
  *                  rounded back to the fp32 arena when the mode is left.
- *                  Parity bar 1e-10 against the fp64 oracle.              */
+ *                  Parity bar 2.5e-7 at tau = 0.1 against the fp64 oracle
+ *                  (4 fp32 ulps: the rounding at the ABI; R19).   */
 enum { NF_MATH_FP32 = 0, NF_MATH_TF32 = 1, NF_MATH_FP64 = 2 };
 
 /* Constructor (network_constructor_listing).

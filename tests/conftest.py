@@ -14,9 +14,9 @@ def pytest_configure(config):
 
 
 def pytest_collection_modifyitems(config, items):
-    # A GPU test on a box without CUDA is a failure, not a skip, when -m gpu was
-    # asked for explicitly (the product path has no CPU fallback).
-    pass
+    # No GPU test is ever skipped: on a host without an sm_100 device the library raises
+    # NF_ENODEV (an NFError) and the test fails -- the product path has no CPU fallback.
+    return
 
 
 @pytest.fixture(scope="session")
