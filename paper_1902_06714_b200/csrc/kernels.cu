@@ -762,6 +762,209 @@ out_layer_train(const float *__restrict__ A, float *__restrict__ S, const float 
   }
 }
 
+// Butterfly reduce-scatter of N per-lane values over the lanes OFF, OFF/2, .., 1: after it lane
+// l holds, in v[0], the warp sum of value index (l mod N) (N = 2 * OFF).  N - 1 shuffles instead of
+// N * 5 for N separate warp_sums.
+template <int N>
+__device__ __forceinline__ void warp_reduce_scatter(float (&v)[32], int lane) {
+  if constexpr (N >= 2) {
+    constexpr int H = N / 2;
+    const bool up = (lane & H) != 0;
+#pragma unroll
+    for (int i = 0; i < H; ++i) {
+      const float send = up ? v[i] : v[i + H];
+      const float keep = up ? v[i + H] : v[i];
+      v[i] = keep + __shfl_xor_sync(0xffffffffu, send, H);
+    }
+    warp_reduce_scatter<H>(v, lane);
+  }
+}
+
+// The narrow output layer of a training step, register-resident form (hidden width H <= 1024,
+// H % 128 == 0; the same three results as out_layer_train above, same part / lpart layout):
+// thread = one float4 column group of the hidden layer, W_L's columns and the K4 partial sums
+// of those columns held in registers for the whole kernel, so the 40 KB of W_L are never
+// re-read per row (the shared-memory bandwidth that bound out_layer_train).  Threads form
+// RG = 256 / (H/4) row groups; each iteration a group takes RC = 2 rows:
+//   z partials over the thread's 4 columns for 2 rows x 16 outputs -> one 32-value butterfly
+//   reduce-scatter per warp (31 shuffles) -> per-warp sums in shared memory -> the group's
+//   first warp finishes z, sigma, delta_L, the cost (lane = (row, output)) -> delta_L in shared
+//   memory -> every thread: delta_{L-1} of its columns (S read once, written once) and the
+//   K4 partials (the A values still in registers).  The next rows' A and S are loaded while
+//   the current ones are processed.
+constexpr int kOutStages = 8;  // ring stages of out_layer_train_rg (16 KB each: 2 x 2048 floats)
+template <int NMAX>
+__global__ void __launch_bounds__(256, 1)
+out_layer_train_rg(const float *__restrict__ A, float *__restrict__ S, const float *__restrict__ W,
+                   const float *__restrict__ bias, const float *__restrict__ Y, float *__restrict__ AL,
+                   float *__restrict__ DL, int n, int H, int nL, int act, int rows_per_block, float *__restrict__ part,
+                   float *__restrict__ lpart, int rnd, float *__restrict__ Dlo) {
+  constexpr int RC = 2;  // rows per group per iteration (RC x 16 = 32 butterfly values)
+  ptx::pdl_trigger();
+  ptx::pdl_wait();
+  __shared__ float red[8][32];      // per-warp butterfly results
+  __shared__ float dsm[8][RC][16];  // delta_L of the iteration's rows, per group
+  __shared__ float bsm[8][32];      // per-group bias / cost partials
+  __shared__ __align__(8) uint64_t full[kOutStages];
+  extern __shared__ float4 sm4_[];  // ring: kOutStages x (A rows | S rows), then the groups' K4 partials
+  const int H4 = H >> 2;
+  const int GS = H4, GW = GS >> 5, RG = 256 / GS;
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const int grp = tid / GS, gt = tid - grp * GS, gw = gt >> 5;
+  const bool act_t = grp < RG;
+  const int r0 = blockIdx.x * rows_per_block, r1 = min(n, r0 + rows_per_block);
+  const int per_it = RG * RC;             // rows per iteration, contiguous in A and S
+  const int stage_f = 2 * per_it * H;     // floats per ring stage
+  const int niter = r1 > r0 ? (r1 - r0 + per_it - 1) / per_it : 0;
+  float *ring = reinterpret_cast<float *>(sm4_);
+  // a stage holds the rows [m0, m0 + nr) of A and of S, copied by two bulk copies
+  auto issue = [&](int it) {
+    if (it >= niter) return;
+    const int st = it % kOutStages, m0 = r0 + it * per_it, nr = min(per_it, r1 - m0);
+    const uint32_t bytes = (uint32_t)nr * H * 4;
+    ptx::mbar_arrive_expect_tx(&full[st], 2 * bytes);
+    ptx::bulk_g2s(ring + (int64_t)st * stage_f, A + (int64_t)m0 * H, bytes, &full[st]);
+    ptx::bulk_g2s(ring + (int64_t)st * stage_f + per_it * H, S + (int64_t)m0 * H, bytes, &full[st]);
+  };
+  if (tid == 0) {
+    for (int i = 0; i < kOutStages; ++i) ptx::mbar_init(&full[i], 1);
+    ptx::fence_mbar_init();
+    for (int i = 0; i < kOutStages; ++i) issue(i);
+  }
+  float4 w[NMAX], g[NMAX];
+#pragma unroll
+  for (int o = 0; o < NMAX; ++o) {
+    w[o] = (act_t && o < nL) ? __ldg(reinterpret_cast<const float4 *>(W + (int64_t)o * H) + gt) : make_float4(0.f, 0.f, 0.f, 0.f);
+    g[o] = make_float4(0.f, 0.f, 0.f, 0.f);
+  }
+  // the block's target rows and the output bias, off the per-iteration critical path
+  float *ysm = ring + (int64_t)kOutStages * stage_f + (RG > 1 ? nL * H : 0);
+  for (int i = tid; i < (r1 - r0) * nL; i += 256) ysm[i] = Y[(int64_t)r0 * nL + i];
+  const float bo = (lane & 15) < nL ? bias[lane & 15] : 0.0f;
+  __syncthreads();  // barriers initialised, ysm filled
+  float gb = 0.0f, lacc = 0.0f;  // first warp of a group: bias tendency / cost of lane (row slot, output)
+  auto row_of = [&](int it, int rr) { return r0 + it * per_it + grp * RC + rr; };
+  for (int it = 0; it < niter; ++it) {
+    const int st = it % kOutStages;
+    ptx::mbar_wait(&full[st], (it / kOutStages) & 1);
+    const float4 *sa = reinterpret_cast<const float4 *>(ring + (int64_t)st * stage_f);
+    const float4 *ss = sa + per_it * H4;
+    float4 a[RC];
+#pragma unroll
+    for (int rr = 0; rr < RC; ++rr)
+      a[rr] = (act_t && row_of(it, rr) < r1) ? sa[(grp * RC + rr) * H4 + gt] : make_float4(0.f, 0.f, 0.f, 0.f);
+    float v[32];
+#pragma unroll
+    for (int rr = 0; rr < RC; ++rr)
+#pragma unroll
+      for (int o = 0; o < 16; ++o) {
+        float z = 0.0f;
+        if (o < NMAX) {
+          z = a[rr].x * w[o].x;
+          z = fmaf(a[rr].y, w[o].y, z);
+          z = fmaf(a[rr].z, w[o].z, z);
+          z = fmaf(a[rr].w, w[o].w, z);
+        }
+        v[rr * 16 + o] = z;
+      }
+    warp_reduce_scatter<32>(v, lane);  // lane l: value (row slot l >> 4, output l & 15)
+    red[warp][lane] = v[0];
+    __syncthreads();
+    // every thread is past iteration it - 1: its stage is refilled with iteration it - 1 + stages
+    if (tid == 0 && it >= 1) issue(it - 1 + kOutStages);
+    if (act_t && gw == 0) {
+      const int rr = lane >> 4, o = lane & 15, m = row_of(it, rr);
+      float z = 0.0f;
+      for (int q = 0; q < GW; ++q) z += red[grp * GW + q][lane];
+      float dl = 0.0f;
+      if (o < nL && m < r1) {
+        float av, sg;
+        act_fwd(act, z + bo, av, sg);
+        const float diff = av - ysm[(m - r0) * nL + o];
+        dl = diff * sg;
+        lacc = fmaf(diff, diff, lacc);
+        gb += dl;
+        AL[(int64_t)m * nL + o] = av;
+        DL[(int64_t)m * nL + o] = dl;
+      }
+      dsm[grp][rr][o] = dl;
+    }
+    __syncthreads();
+    if (act_t) {
+#pragma unroll
+      for (int rr = 0; rr < RC; ++rr) {
+        const int m = row_of(it, rr);
+        float d[NMAX];
+#pragma unroll
+        for (int o = 0; o < NMAX; ++o) d[o] = dsm[grp][rr][o];
+        float4 t = make_float4(0.f, 0.f, 0.f, 0.f);
+#pragma unroll
+        for (int o = 0; o < NMAX; ++o) {
+          t.x = fmaf(d[o], w[o].x, t.x);
+          t.y = fmaf(d[o], w[o].y, t.y);
+          t.z = fmaf(d[o], w[o].z, t.z);
+          t.w = fmaf(d[o], w[o].w, t.w);
+          g[o].x = fmaf(d[o], a[rr].x, g[o].x);
+          g[o].y = fmaf(d[o], a[rr].y, g[o].y);
+          g[o].z = fmaf(d[o], a[rr].z, g[o].z);
+          g[o].w = fmaf(d[o], a[rr].w, g[o].w);
+        }
+        if (m < r1) {
+          const float4 sv = ss[(grp * RC + rr) * H4 + gt];
+          float4 dd = make_float4(t.x * sv.x, t.y * sv.y, t.z * sv.z, t.w * sv.w);
+          if (rnd) dd = make_float4(tf32_rn(dd.x), tf32_rn(dd.y), tf32_rn(dd.z), tf32_rn(dd.w));  // a TC operand next
+          reinterpret_cast<float4 *>(S + (int64_t)m * H)[gt] = dd;
+          if (Dlo)
+            reinterpret_cast<float4 *>(Dlo + (int64_t)m * H)[gt] =
+                make_float4(tf32_lo(dd.x), tf32_lo(dd.y), tf32_lo(dd.z), tf32_lo(dd.w));
+        }
+      }
+    }
+  }
+  // the groups' K4 partials summed in group order (deterministic), written by group 0
+  float *gs = ring + (int64_t)kOutStages * stage_f;
+  for (int q = 1; q < RG; ++q) {
+    __syncthreads();
+    if (grp == q)
+#pragma unroll
+      for (int o = 0; o < NMAX; ++o)
+        if (o < nL) reinterpret_cast<float4 *>(gs + (int64_t)o * H)[gt] = g[o];
+    __syncthreads();
+    if (grp == 0)
+#pragma unroll
+      for (int o = 0; o < NMAX; ++o)
+        if (o < nL) {
+          const float4 u = reinterpret_cast<const float4 *>(gs + (int64_t)o * H)[gt];
+          g[o].x += u.x; g[o].y += u.y; g[o].z += u.z; g[o].w += u.w;
+        }
+  }
+  float *pb = part + (int64_t)blockIdx.x * nL * (H + 1);
+  if (grp == 0)
+#pragma unroll
+    for (int o = 0; o < NMAX; ++o)
+      if (o < nL) {
+        float *p = pb + (int64_t)o * (H + 1) + 4 * gt;
+        p[0] = g[o].x; p[1] = g[o].y; p[2] = g[o].z; p[3] = g[o].w;
+      }
+  // bias column H and the block's cost: lanes (row slot, output) of each group's first warp
+  if (act_t && gw == 0) {  // (warp-uniform: GS is a multiple of 32)
+    gb += __shfl_xor_sync(0xffffffffu, gb, 16);  // both row slots
+    const float lw = warp_sum(lacc);
+    bsm[grp][lane] = lane < 16 ? gb : lw;
+  }
+  __syncthreads();
+  if (tid < 16 && tid < nL) {
+    float u = 0.0f;
+    for (int q = 0; q < RG; ++q) u += bsm[q][tid];
+    pb[(int64_t)tid * (H + 1) + H] = u;
+  }
+  if (tid == 0) {
+    float l = 0.0f;
+    for (int q = 0; q < RG; ++q) l += bsm[q][16];
+    lpart[blockIdx.x] = l;
+  }
+}
+
 // Host-dataset staging of the small per-step target rows (nf_train_steps e2e path): the rows
 // of up to kGatherMax steps read straight from mapped (pinned) host memory by the GPU, one
 // kernel per chunk instead of one small DMA per step (their per-copy cost was 8 % of the e2e
@@ -850,10 +1053,17 @@ cudaError_t sgd_update(cudaStream_t st, float *p, const float *g, int64_t n, flo
 
 // blocks of the fused output-layer kernel: >= 8 rows each (>= 8192 / H for narrow hidden
 // layers, so that the fixed-order final sum has few partials), at most 2 per SM
+// the register-resident form (out_layer_train_rg) for hidden widths 128..1024 in steps of 128;
+// NF_OUT_V1=1 keeps out_layer_train
+bool out_layer_rg(int H) {
+  static const bool v1 = getenv("NF_OUT_V1") != nullptr;
+  return !v1 && H % 128 == 0 && H >= 128 && H <= 1024;
+}
+
 int out_layer_blocks(int n, int H) {
-  (void)H;  // (>= 8192 / H rows for narrow H cut the final sum's partials but made c4 slower)
+  // (>= 8192 / H rows for narrow H cut the final sum's partials but made c4 slower)
   const int rmin = 8;
-  return std::max(1, std::min(2 * kSMs, (n + rmin - 1) / rmin));
+  return std::max(1, std::min((out_layer_rg(H) ? 1 : 2) * kSMs, (n + rmin - 1) / rmin));
 }
 
 constexpr int kOutSmemMax = 200 * 1024;
@@ -882,7 +1092,21 @@ cudaError_t out_layer_train_fused(cudaStream_t st, int n, int H, int nL, const f
     cudaError_t e = set_max_smem(k, kOutSmemMax);
     if (e != cudaSuccess) return e;
   }
+  for (const void *k : {reinterpret_cast<const void *>(out_layer_train_rg<10>), reinterpret_cast<const void *>(out_layer_train_rg<16>)}) {
+    cudaError_t e = set_max_smem(k, 200 * 1024);
+    if (e != cudaSuccess) return e;
+  }
   float *lp = part + (int64_t)blocks * nL * (H + 1);
+  if (out_layer_rg(H)) {
+    const size_t gsm = (size_t)kOutStages * 2 * 2 * (256 / (H / 4)) * H * 4 + (256 / (H / 4) > 1 ? (size_t)nL * H * 4 : 0) +
+                       (size_t)rpb * nL * 4;
+    if (gsm > 200 * 1024) return cudaErrorInvalidValue;
+    if (nL <= 10)
+      return launch_k(out_layer_train_rg<10>, dim3(blocks), dim3(256), gsm, st, A, S, W, bias, Y, AL, DL, n, H, nL,
+                      act, rpb, part, lp, rnd, Dlo);
+    return launch_k(out_layer_train_rg<16>, dim3(blocks), dim3(256), gsm, st, A, S, W, bias, Y, AL, DL, n, H, nL,
+                    act, rpb, part, lp, rnd, Dlo);
+  }
   if (nL <= 10) {  // (MNIST-like 10-wide outputs: no idle unrolled output slots)
     if (H <= 512)
       return launch_k(out_layer_train<10, 4>, dim3(blocks), dim3(256), smem, st, A, S, W, bias, Y, AL, DL, n, H, nL,

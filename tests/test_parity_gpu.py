@@ -54,6 +54,10 @@ SHAPES = [
     ([40, 1100, 12], "tanh,sigmoid", 300),
     ([64, 256, 16], "sigmoid", 513),
     ([30, 640, 10], "gaussian,sigmoid", 257),
+    # register-resident form (out_layer_train_rg: H % 128 == 0, H <= 1024): 8 row groups of one
+    # warp (H = 128), 2 groups with idle threads (H = 384), ragged last iteration
+    ([50, 128, 1], "tanh,sigmoid", 389),
+    ([70, 384, 16], "relu,sigmoid", 1001),
     # one activation per layer: generic kernels, fused output layer
     ([20, 50, 40, 30, 6], "tanh,gaussian,sigmoid,tanh", 150),
     ([24, 130, 96, 10], "sigmoid,tanh,sigmoid", 300),
