@@ -15,19 +15,24 @@
 //               commit round trip never holds an x stage
 //   warps 2-9   converters (two groups alternating K-blocks), thread = row: read the row's 32 pixels from the swizzled tile, split
 //               them (truncation split: hi = x with the low 13 mantissa bits cleared, lo =
-//               rn_tf32(x - hi)) and store hi | lo into a 7-deep TMEM ring with tcgen05.st -- so
+//               rn_tf32(x - hi)) and store hi | lo into a 6-deep TMEM ring with tcgen05.st -- so
 //               the MMA reads its A operand from tensor memory (A in TMEM: no shared-memory read
 //               of the 128-row operand per MMA; micro/tc_atmem_test.cu: ~14 cycles per M=128 x
 //               N=32 x K=8 MMA marginal, vs ~61 with A in shared memory)
-//   warp 1      MMA issuer: 4 k-steps x 3 MMAs per K-block into one of two 32-column TMEM
-//               accumulators (double-buffered per 128-row tile); tcgen05.commit frees the ring
-//               slots and hands the finished accumulator to the epilogue
-//   warps 10-13 epilogue, thread = row: tcgen05.ld Z1 row, + b1, sigma_h, layer 2 (W2, b2 in
+//   warp 1      MMA issuer: 4 k-steps x 2 MMAs (x_lo, x_hi) per K-block against B = the W stage's 64
+//               rows, W1 hi | W1 lo STACKED along N: accumulator columns 0..31 get x W_hi, columns
+//               32..63 x W_lo (all four partial products for two instructions per k-step instead of
+//               the three of hi*hi + hi*lo + lo*hi; the epilogue adds the two halves), into one of
+//               two 64-column TMEM accumulators (double-buffered per 128-row tile); tcgen05.commit
+//               frees the ring slots and hands the finished accumulator to the epilogue
+//   warps 10-13 epilogue, thread = row: tcgen05.ld both halves of the Z1 row, + b1, sigma_h, layer 2 (W2, b2 in
 //               shared memory, broadcast reads), sigma_o, store the O outputs
 // The x tile is read from HBM once; W1 (94 KB) is re-read from L2 per tile.
 #include <algorithm>
 #include <cstring>
+#include <cstdio>
 #include <mutex>
+#include <vector>
 
 #include "gemm_tc.cuh"
 #include "infer_tc.cuh"
@@ -43,12 +48,12 @@ constexpr int kBoxRows = 32;                        // rows per TMA box (tile ta
 constexpr int kKB = 32;                             // pixels per K-block (one 128-B swizzle row)
 constexpr int kStages = 8;                          // x ring depth (freed by the converters)
 constexpr int kWStages = 4;                         // W1 hi | lo ring depth (freed by the MMA commits)
-constexpr int kTStages = 7;                         // TMEM x-operand ring depth (64 columns: hi | lo)
+constexpr int kTStages = 6;                         // TMEM x-operand ring depth (64 columns: hi | lo)
 constexpr int kCG = 2;                              // converter warp groups (alternating K-blocks)
 constexpr int kXBytes = kTileRows * kKB * 4;        // 16 KB
 constexpr int kWBytes = 32 * kKB * 4;               // 4 KB (hi or lo)
 constexpr int kWStageBytes = 2 * kWBytes;           // 8 KB
-constexpr int kAccCol = kTStages * 64;              // accumulators after the x ring: 2 x 32 columns
+constexpr int kAccCol = kTStages * 64;              // accumulators after the x ring: 2 x 64 columns (W hi | lo stacked along N)
 constexpr int kThreads = 32 * (2 + 4 * kCG + 4 + 1);  // + the W producer warp
 constexpr int kSmem = 1024 + kStages * kXBytes + kWStages * kWStageBytes + (32 * 33 + 64) * 4 + 512;
 
@@ -57,10 +62,14 @@ struct InferTcParams {
   int64_t nblk;   // 32-row blocks
   int n0, H, O, act_h, act_o;
   int nkb;        // K-blocks of 32 pixels
-  int exp;        // experiment bits (NF_ITC_EXP, timing only): 1 no W reload, 2 no MMAs, 4 no conversion
+  int exp;        // experiment bits (NF_ITC_EXP, timing only): 1 no W reload, 2 no MMAs, 4 no conversion, 16 no x_lo MMA
   const float *b1, *W2, *b2;  // in the parameter arena
   float *out;
+  long long *prof;  // NF_ITC_PROF: per-CTA wait-time counters of the stacked kernel (16 per CTA)
 };
+
+#define ITC_T0() const long long t0_ = p.prof ? clock64() : 0
+#define ITC_ACC(v) do { if (p.prof) v += clock64() - t0_; } while (0)
 
 __device__ __forceinline__ void tmem_st32(uint32_t taddr, const float (&v)[32]) {
   asm volatile(
@@ -95,7 +104,7 @@ infer_tc_kernel(const InferTcParams p, const __grid_constant__ CUtensorMap tmX,
   uint64_t *afull = tempty + kTStages, *aempty = afull + 2;
   uint64_t *wfull = aempty + 2, *wempty = wfull + kWStages;
   uint32_t *tslot = reinterpret_cast<uint32_t *>(wempty + kWStages);
-  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+  const int tid = threadIdx.x, warp = ptx::warp_uniform(tid >> 5), lane = tid & 31;
 
   // this CTA's rows: an equal share of whole 32-row blocks
   const int64_t bb = (int64_t)blockIdx.x * p.nblk / gridDim.x, be = (int64_t)(blockIdx.x + 1) * p.nblk / gridDim.x;
@@ -141,6 +150,9 @@ infer_tc_kernel(const InferTcParams p, const __grid_constant__ CUtensorMap tmX,
   __syncthreads();
   tc::tc_fence_after();
   const uint32_t tmem = *tslot;
+  const long long tstart = p.prof ? clock64() : 0;
+  long long w0 = 0, w1 = 0, w2 = 0;
+  long long *prof = p.prof ? p.prof + 16 * blockIdx.x : nullptr;
 
   if (warp == 0) {
     // ---- TMA producer of the x tiles
@@ -152,13 +164,14 @@ infer_tc_kernel(const InferTcParams p, const __grid_constant__ CUtensorMap tmX,
         const int nbox = (int)((rows_here + kBoxRows - 1) / kBoxRows);
         for (int kb = 0; kb < p.nkb; ++kb, ++g) {
           const int s = g % kStages;
-          ptx::mbar_wait(&empty[s], ((g / kStages) & 1) ^ 1);
+          { ITC_T0(); ptx::mbar_wait(&empty[s], ((g / kStages) & 1) ^ 1); ITC_ACC(w0); }
           uint8_t *st = ring + s * kXBytes;
           ptx::mbar_arrive_expect_tx(&full[s], (uint32_t)(nbox * kBoxRows * kKB * 4));
           for (int b = 0; b < nbox; ++b)
             ptx::tma_load_2d(st + b * (kBoxRows * 128), &tmX, &full[s], kb * kKB, (int)(row + b * kBoxRows));
         }
       }
+      if (prof) prof[0] = w0;
     }
   } else if (warp == kThreads / 32 - 1) {
     // ---- TMA producer of the W1 hi | lo K-blocks (L2-resident)
@@ -167,7 +180,7 @@ infer_tc_kernel(const InferTcParams p, const __grid_constant__ CUtensorMap tmX,
       for (int i = 0; i < ntiles; ++i) {
         for (int kb = 0; kb < p.nkb; ++kb, ++g) {
           const int w = g % kWStages;
-          ptx::mbar_wait(&wempty[w], ((g / kWStages) & 1) ^ 1);
+          { ITC_T0(); ptx::mbar_wait(&wempty[w], ((g / kWStages) & 1) ^ 1); ITC_ACC(w0); }
           uint8_t *st = wring + w * kWStageBytes;
           if ((p.exp & 1) && g >= kWStages) {  // (timing experiment: no reload)
             ptx::mbar_arrive(&wfull[w]);
@@ -178,38 +191,49 @@ infer_tc_kernel(const InferTcParams p, const __grid_constant__ CUtensorMap tmX,
           ptx::tma_load_2d(st + kWBytes, &tmWl, &wfull[w], kb * kKB, 0);
         }
       }
+      if (prof) prof[1] = w0;
     }
   } else if (warp == 1) {
-    // ---- MMA issuer
-    if (lane == 0 && !(p.exp & 8)) {
-      constexpr uint32_t idesc = tc::idesc_tf32(kTileRows, 32, false, false);
-      int g = 0;
+    // ---- MMA issuer: the whole warp runs the loop and the barrier waits (warp-uniform control flow
+    //      and operands: descriptors / tensor-memory addresses stay in uniform registers), one
+    //      elected lane issues the tcgen05 instructions
+    if (!(p.exp & 8)) {
+      constexpr uint32_t idesc = tc::idesc_tf32(kTileRows, 64, false, false);  // N = 64: W1 hi rows | W1 lo rows
+      const uint32_t tmem_u = (uint32_t)ptx::warp_uniform((int)tmem);
+      const uint32_t wring_u = ptx::smem_u32(wring);
+      int g = 0, w = 0, t = 0;
+      uint32_t wpar = 0, tpar = 0;
       for (int i = 0; i < ntiles; ++i) {
         const int a = i & 1;
-        ptx::mbar_wait(&aempty[a], ((i >> 1) & 1) ^ 1);
+        { ITC_T0(); ptx::mbar_wait(&aempty[a], ((i >> 1) & 1) ^ 1); ITC_ACC(w2); }
         tc::tc_fence_after();
-        const uint32_t d = tmem + kAccCol + 32u * a;
+        const uint32_t d = tmem_u + kAccCol + 64u * a;
         for (int kb = 0; kb < p.nkb; ++kb, ++g) {
-          const int w = g % kWStages, t = g % kTStages;
-          ptx::mbar_wait(&wfull[w], (g / kWStages) & 1);    // W K-block landed
-          ptx::mbar_wait(&tfull[t], (g / kTStages) & 1);    // x K-block split into TMEM
+          { ITC_T0(); ptx::mbar_wait(&wfull[w], wpar); ITC_ACC(w0); }    // W K-block landed
+          { ITC_T0(); ptx::mbar_wait(&tfull[t], tpar); ITC_ACC(w1); }    // x K-block split into TMEM
           tc::tc_fence_after();
-          const uint32_t sw = ptx::smem_u32(wring + w * kWStageBytes);
+          const uint32_t sw = wring_u + (uint32_t)w * kWStageBytes;
+          // B = the stage's 64 rows: W1 hi (rows 0..31) | W1 lo (rows 32..63), so one MMA per x part
+          // gives x W_hi in accumulator columns 0..31 and x W_lo in 32..63 (all four partial products)
+          const uint64_t bw = tc::smem_desc(sw, 16, 1024, 2);
+          const uint32_t ah = tmem_u + 64u * (uint32_t)t;
+          if (ptx::elect_one()) {
 #pragma unroll
-          for (int ks = 0; ks < kKB / 8; ++ks) {
-            if (p.exp & 2) break;
-            const uint64_t bh = tc::smem_desc(sw + 32u * ks, 16, 1024, 2);
-            const uint64_t bl = tc::smem_desc(sw + kWBytes + 32u * ks, 16, 1024, 2);
-            const uint32_t ah = tmem + 64u * t + 8u * ks, al = ah + 32u;
-            mma_tf32_ts(d, al, bh, idesc, (kb | ks) ? 1u : 0u);  // small terms first
-            mma_tf32_ts(d, ah, bl, idesc, 1u);
-            mma_tf32_ts(d, ah, bh, idesc, 1u);
+            for (int ks = 0; ks < kKB / 8; ++ks) {
+              if (p.exp & 2) break;
+              if (!(p.exp & 16)) mma_tf32_ts(d, ah + 8u * ks + 32u, bw + 2u * ks, idesc, (kb | ks) ? 1u : 0u);  // small terms first
+              mma_tf32_ts(d, ah + 8u * ks, bw + 2u * ks, idesc, (p.exp & 16) ? ((kb | ks) ? 1u : 0u) : 1u);
+            }
+            tc::mma_commit(&wempty[w]);
+            tc::mma_commit(&tempty[t]);
+            if (kb == p.nkb - 1) tc::mma_commit(&afull[a]);
           }
-          tc::mma_commit(&wempty[w]);
-          tc::mma_commit(&tempty[t]);
-          if (kb == p.nkb - 1) tc::mma_commit(&afull[a]);
+          __syncwarp();
+          if (++w == kWStages) { w = 0; wpar ^= 1; }
+          if (++t == kTStages) { t = 0; tpar ^= 1; }
         }
       }
+      if (prof && lane == 0) { prof[2] = w0; prof[3] = w1; prof[4] = w2; }
     }
   } else if (warp < 2 + 4 * kCG) {
     // ---- converters: thread = row 32 q + lane of the tile (TMEM lane quadrant q = warp % 4); group
@@ -220,13 +244,13 @@ infer_tc_kernel(const InferTcParams p, const __grid_constant__ CUtensorMap tmX,
       for (int kb = 0; kb < p.nkb; ++kb, ++g) {
         if (g % kCG != cg) continue;
         const int s = g % kStages, t = g % kTStages;
-        ptx::mbar_wait(&full[s], (g / kStages) & 1);
+        { ITC_T0(); ptx::mbar_wait(&full[s], (g / kStages) & 1); ITC_ACC(w0); }
         if (p.exp & 8) {  // (timing experiment: x streaming alone)
           __syncwarp();
           if (lane == 0) ptx::mbar_arrive(&empty[s]);
           continue;
         }
-        ptx::mbar_wait(&tempty[t], ((g / kTStages) & 1) ^ 1);
+        { ITC_T0(); ptx::mbar_wait(&tempty[t], ((g / kTStages) & 1) ^ 1); ITC_ACC(w1); }
         // this row's 128 B in the swizzled box q: 16-B chunk c at physical chunk c ^ (row % 8)
         const uint8_t *xr = ring + s * kXBytes + q * (kBoxRows * 128) + lane * 128;
         float hi[32], lo[32];
@@ -254,16 +278,20 @@ infer_tc_kernel(const InferTcParams p, const __grid_constant__ CUtensorMap tmX,
         }
       }
     }
+    if (prof && tid == 64) { prof[5] = w0; prof[6] = w1; }
   } else if (warp < 2 + 4 * kCG + 4 && !(p.exp & 8)) {
     // ---- epilogue: thread = row 32 q + lane of the tile
     const int q = warp & 3;
     const int H = p.H, O = p.O;
     for (int i = 0; i < ntiles; ++i) {
       const int a = i & 1;
-      ptx::mbar_wait(&afull[a], (i >> 1) & 1);
+      { ITC_T0(); ptx::mbar_wait(&afull[a], (i >> 1) & 1); ITC_ACC(w0); }
       tc::tc_fence_after();
-      float z[32];
-      tc::tmem_ld32(tmem + ((uint32_t)(32 * q) << 16) + kAccCol + 32u * a, z);
+      float z[32], zl[32];
+      tc::tmem_ld32(tmem + ((uint32_t)(32 * q) << 16) + kAccCol + 64u * a, z);
+      tc::tmem_ld32(tmem + ((uint32_t)(32 * q) << 16) + kAccCol + 64u * a + 32u, zl);
+#pragma unroll
+      for (int j = 0; j < 32; ++j) z[j] += zl[j];
       tc::tc_fence_before();
       __syncwarp();
       if (lane == 0) ptx::mbar_arrive(&aempty[a]);
@@ -288,8 +316,10 @@ infer_tc_kernel(const InferTcParams p, const __grid_constant__ CUtensorMap tmX,
       }
     }
   }
+  if (prof && warp == 2 + 4 * kCG && lane == 0) { prof[7] = w0; prof[9] = clock64() - tstart; }
   tc::tc_fence_before();
   __syncthreads();
+  if (prof && tid == 0) { prof[8] = clock64() - tstart; prof[10] = ntiles * p.nkb; }
   if (warp == 1) {
     tc::tc_fence_after();
     asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem), "r"(512u) : "memory");
@@ -496,6 +526,443 @@ infer_tcT_kernel(const InferTcParams p, const __grid_constant__ CUtensorMap tmX,
   }
 }
 
+// ---- stacked formulation (infer_tcS_kernel, the default): the transposed contraction with the
+// W1 hi and lo parts STACKED along M.  The A descriptor's 128 rows read W1_hi (rows 0..31) and,
+// right behind it in shared memory, W1_lo (rows 32..63), so ONE MMA against an x operand gives
+// W_hi x in accumulator lanes 0..31 and W_lo x in lanes 32..63 -- the M = 128 instruction costs the
+// same as before (the tensor core's floor is max(M,128) N / 256 cycles) but the separate W_lo MMA is
+// gone: 2 MMAs per k-step (x_hi, x_lo) instead of 3, and the lo*lo term comes for free (all four
+// partial products; lanes 64..127 read neighbouring shared memory and are never looked at).  The
+// epilogue adds the two lane groups.  Rings by lifetime: the x tiles (HBM latency) in a 6-deep ring,
+// the x_lo tiles the converters write and the W1 K-blocks (L2-resident) in 3-deep rings, all freed
+// by the MMA commits; the W1 producer is its own warp so its short ring never delays an x load.
+// The last tile of a CTA issues MMAs only as wide (N) as its rows.
+namespace ts {
+constexpr int kRows = 128;
+constexpr int kXS = 6, kLS = 3;                      // x ring / (x_lo, W) ring depths
+constexpr int kXBytes = kRows * kKB * 4;             // 16 KB
+constexpr int kWStage = 2 * 32 * kKB * 4;            // 8 KB: W hi rows 0..31 | W lo rows 32..63
+constexpr int kCvtWarps = 8;
+constexpr int kThreads = 32 * (2 + kCvtWarps + 4 + 1);   // x TMA, MMA, converters, epilogue, W TMA
+constexpr int kZt = kRows * 33;                      // floats per transposed accumulator half
+// the A descriptor of the last W stage reads 8 KB past it: into zt (any bit pattern will do)
+constexpr int kSmem = 1024 + kXS * kXBytes + kLS * kXBytes + kLS * kWStage + (2 * kZt + 32 * 33 + 64) * 4 + 256;
+static_assert(2 * kZt * 4 >= 128 * 128 - kWStage, "A over-read must stay inside the CTA's shared memory");
+static_assert(kSmem <= 232448, "shared memory");
+}  // namespace ts
+
+__global__ void __launch_bounds__(ts::kThreads, 1)
+infer_tcS_kernel(const InferTcParams p, const __grid_constant__ CUtensorMap tmX,
+                 const __grid_constant__ CUtensorMap tmWh, const __grid_constant__ CUtensorMap tmWl) {
+  extern __shared__ __align__(1024) uint8_t smraw[];
+  uint8_t *xring = reinterpret_cast<uint8_t *>((reinterpret_cast<uintptr_t>(smraw) + 1023) & ~uintptr_t(1023));
+  uint8_t *lring = xring + ts::kXS * ts::kXBytes;
+  uint8_t *wring = lring + ts::kLS * ts::kXBytes;
+  float *zt = reinterpret_cast<float *>(wring + ts::kLS * ts::kWStage);   // [2][rows][33]
+  float *W2s = zt + 2 * ts::kZt;                    // [32][33]
+  float *b1s = W2s + 32 * 33, *b2s = b1s + 32;
+  uint64_t *xfull = reinterpret_cast<uint64_t *>(b2s + 32);
+  uint64_t *xempty = xfull + ts::kXS, *lfull = xempty + ts::kXS, *wfull = lfull + ts::kLS, *mdone = wfull + ts::kLS;
+  uint64_t *afull = mdone + ts::kLS, *aempty = afull + 2;
+  uint32_t *tslot = reinterpret_cast<uint32_t *>(aempty + 2);
+  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+
+  const int64_t bb = (int64_t)blockIdx.x * p.nblk / gridDim.x, be = (int64_t)(blockIdx.x + 1) * p.nblk / gridDim.x;
+  const int64_t r0 = bb * kBoxRows, r1 = min(p.n, be * kBoxRows);
+  const int ntiles = r1 > r0 ? (int)((r1 - r0 + ts::kRows - 1) / ts::kRows) : 0;
+
+  if (tid == 0) {
+    for (int i = 0; i < ts::kXS; ++i) {
+      ptx::mbar_init(&xfull[i], 1);
+      ptx::mbar_init(&xempty[i], 1);
+    }
+    for (int i = 0; i < ts::kLS; ++i) {
+      ptx::mbar_init(&lfull[i], ts::kCvtWarps);
+      ptx::mbar_init(&wfull[i], 1);
+      ptx::mbar_init(&mdone[i], 1);   // the MMAs of this x_lo / W slot have completed
+    }
+    for (int i = 0; i < 2; ++i) {
+      ptx::mbar_init(&afull[i], 1);
+      ptx::mbar_init(&aempty[i], 2);
+    }
+    ptx::fence_mbar_init();
+    ptx::prefetch_tensormap(&tmX);
+    ptx::prefetch_tensormap(&tmWh);
+    ptx::prefetch_tensormap(&tmWl);
+  }
+  if (warp == 1) {
+    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(ptx::smem_u32(tslot)),
+                 "r"((uint32_t)(2 * ts::kRows)) : "memory");
+    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;" ::: "memory");
+  }
+  for (int i = tid; i < 32 * 32; i += ts::kThreads) {
+    const int o = i >> 5, j = i & 31;
+    W2s[o * 33 + j] = (o < p.O && j < p.H) ? p.W2[o * p.H + j] : 0.0f;
+  }
+  for (int i = tid; i < 2 * ts::kZt; i += ts::kThreads) zt[i] = 0.0f;
+  if (tid < 32) {
+    b1s[tid] = tid < p.H ? p.b1[tid] : 0.0f;
+    b2s[tid] = tid < p.O ? p.b2[tid] : 0.0f;
+  }
+  tc::tc_fence_before();
+  __syncthreads();
+  tc::tc_fence_after();
+  const uint32_t tmem = *tslot;
+  const long long tstart = p.prof ? clock64() : 0;
+  long long w0 = 0, w1 = 0, w2 = 0;
+  long long *prof = p.prof ? p.prof + 16 * blockIdx.x : nullptr;
+
+  if (warp == 0) {
+    if (lane == 0) {  // ---- TMA: x tiles (boxes of 32 rows)
+      int g = 0;
+      for (int i = 0; i < ntiles; ++i) {
+        const int64_t row = r0 + (int64_t)i * ts::kRows;
+        const int64_t rows_here = r1 - row < ts::kRows ? r1 - row : ts::kRows;
+        const int nbox = (int)((rows_here + kBoxRows - 1) / kBoxRows);
+        for (int kb = 0; kb < p.nkb; ++kb, ++g) {
+          const int s = g % ts::kXS;
+          { ITC_T0(); ptx::mbar_wait(&xempty[s], ((g / ts::kXS) & 1) ^ 1); ITC_ACC(w0); }
+          uint8_t *st = xring + s * ts::kXBytes;
+          ptx::mbar_arrive_expect_tx(&xfull[s], (uint32_t)(nbox * kBoxRows * 128));
+          for (int b = 0; b < nbox; ++b)
+            ptx::tma_load_2d(st + b * (kBoxRows * 128), &tmX, &xfull[s], kb * kKB, (int)(row + b * kBoxRows));
+        }
+      }
+      if (prof) prof[0] = w0;
+    }
+  } else if (warp == ts::kThreads / 32 - 1) {
+    if (lane == 0) {  // ---- TMA: W1 hi | lo K-blocks
+      const int total = ntiles * p.nkb;
+      for (int g = 0; g < total; ++g) {
+        const int w = g % ts::kLS, kb = g % p.nkb;
+        { ITC_T0(); ptx::mbar_wait(&mdone[w], ((g / ts::kLS) & 1) ^ 1); ITC_ACC(w0); }
+        uint8_t *st = wring + w * ts::kWStage;
+        ptx::mbar_arrive_expect_tx(&wfull[w], (uint32_t)ts::kWStage);
+        ptx::tma_load_2d(st, &tmWh, &wfull[w], kb * kKB, 0);
+        ptx::tma_load_2d(st + ts::kWStage / 2, &tmWl, &wfull[w], kb * kKB, 0);
+      }
+      if (prof) prof[1] = w0;
+    }
+  } else if (warp == 1) {
+    if (lane == 0) {  // ---- MMA issuer
+      int g = 0;
+      for (int i = 0; i < ntiles; ++i) {
+        const int a = i & 1;
+        const int64_t left = r1 - (r0 + (int64_t)i * ts::kRows);
+        const int nn = left >= ts::kRows ? ts::kRows : (int)((left + 15) & ~int64_t(15));   // N: multiple of 16
+        const uint32_t idesc = tc::idesc_tf32(128, nn, false, false);
+        { ITC_T0(); ptx::mbar_wait(&aempty[a], ((i >> 1) & 1) ^ 1); ITC_ACC(w2); }
+        tc::tc_fence_after();
+        const uint32_t d = tmem + (uint32_t)(ts::kRows * a);
+        for (int kb = 0; kb < p.nkb; ++kb, ++g) {
+          const int s = g % ts::kXS, w = g % ts::kLS;
+          { ITC_T0(); ptx::mbar_wait(&wfull[w], (g / ts::kLS) & 1); ITC_ACC(w0); }
+          { ITC_T0(); ptx::mbar_wait(&lfull[w], (g / ts::kLS) & 1); ITC_ACC(w1); }  // x landed and its lo part written
+          tc::tc_fence_after();
+          const uint32_t xh = ptx::smem_u32(xring + s * ts::kXBytes), xl = ptx::smem_u32(lring + w * ts::kXBytes);
+          const uint32_t ws = ptx::smem_u32(wring + w * ts::kWStage);
+#pragma unroll
+          for (int ks = 0; ks < kKB / 8; ++ks) {
+            if (p.exp & 2) break;
+            const uint64_t dw = tc::smem_desc(ws + 32u * ks, 16, 1024, 2);
+            const uint64_t dxh = tc::smem_desc(xh + 32u * ks, 16, 1024, 2), dxl = tc::smem_desc(xl + 32u * ks, 16, 1024, 2);
+            tc::mma_tf32(d, dw, dxl, idesc, (kb | ks) ? 1u : 0u);  // small terms first
+            tc::mma_tf32(d, dw, dxh, idesc, 1u);
+          }
+          tc::mma_commit(&xempty[s]);
+          tc::mma_commit(&mdone[w]);
+          if (kb == p.nkb - 1) tc::mma_commit(&afull[a]);
+        }
+      }
+      if (prof) { prof[2] = w0; prof[3] = w1; prof[4] = w2; }
+    }
+  } else if (warp < 2 + ts::kCvtWarps) {
+    // ---- converters: x_lo = rn_tf32(x - trunc(x)), elementwise over the swizzled tile (the
+    //      layouts match: same byte offset), 64 B per thread per K-block
+    const int ct = tid - 64;
+    const int total = ntiles * p.nkb;
+    for (int g = 0; g < total; ++g) {
+      const int s = g % ts::kXS, w = g % ts::kLS;
+      { ITC_T0(); ptx::mbar_wait(&xfull[s], (g / ts::kXS) & 1); ITC_ACC(w0); }
+      { ITC_T0(); ptx::mbar_wait(&mdone[w], ((g / ts::kLS) & 1) ^ 1); ITC_ACC(w1); }
+      const float4 *src = reinterpret_cast<const float4 *>(xring + s * ts::kXBytes);
+      float4 *dst = reinterpret_cast<float4 *>(lring + w * ts::kXBytes);
+      float4 v[ts::kXBytes / 16 / (32 * ts::kCvtWarps)];
+#pragma unroll
+      for (int c = 0; c < ts::kXBytes / 16 / (32 * ts::kCvtWarps); ++c) v[c] = src[ct + 32 * ts::kCvtWarps * c];
+#pragma unroll
+      for (int c = 0; c < ts::kXBytes / 16 / (32 * ts::kCvtWarps); ++c) {
+        if (p.exp & 4) break;
+        dst[ct + 32 * ts::kCvtWarps * c] = make_float4(tf32_lo(v[c].x), tf32_lo(v[c].y), tf32_lo(v[c].z), tf32_lo(v[c].w));
+      }
+      ptx::fence_proxy_async_smem();  // generic-proxy writes -> visible to the tensor core
+      __syncwarp();
+      if (lane == 0) ptx::mbar_arrive(&lfull[w]);
+    }
+    if (prof && tid == 64) { prof[5] = w0; prof[6] = w1; }
+  } else {
+    // ---- epilogue: the warps of TMEM lane quadrants 0 and 1 read Z1^T lanes 0..31 (W_hi x) and
+    //      32..63 (W_lo x) and transpose them into zt[0] / zt[1]; then thread = row finishes
+    const int q = warp & 3, et = tid - 32 * (2 + ts::kCvtWarps);
+    const int H = p.H, O = p.O;
+    for (int i = 0; i < ntiles; ++i) {
+      const int a = i & 1;
+      const int64_t left = r1 - (r0 + (int64_t)i * ts::kRows);
+      const int nn = left >= ts::kRows ? ts::kRows : (int)((left + 15) & ~int64_t(15));
+      if (q < 2) {
+        { ITC_T0(); ptx::mbar_wait(&afull[a], (i >> 1) & 1); ITC_ACC(w0); }
+        tc::tc_fence_after();
+        float *zq = zt + q * ts::kZt;
+        for (int c0 = 0; c0 < nn; c0 += 32) {
+          float z[32];
+          tc::tmem_ld32(tmem + ((uint32_t)(32 * q) << 16) + (uint32_t)(ts::kRows * a + c0), z);  // lane = neuron, z[c] = row c0 + c
+#pragma unroll
+          for (int c = 0; c < 32; ++c) zq[(c0 + c) * 33 + lane] = z[c];
+        }
+        tc::tc_fence_before();
+        __syncwarp();
+        if (lane == 0) ptx::mbar_arrive(&aempty[a]);
+      }
+      asm volatile("bar.sync 1, 128;" ::: "memory");  // zt filled
+      const int64_t row = r0 + (int64_t)i * ts::kRows + et;
+      if (row < r1) {
+        float a1[32];
+#pragma unroll
+        for (int j = 0; j < 32; ++j)
+          a1[j] = j < H ? act_only(p.act_h, (zt[et * 33 + j] + zt[ts::kZt + et * 33 + j]) + b1s[j]) : 0.0f;
+        float *orow = p.out + row * O;
+        for (int o = 0; o < O; ++o) {
+          const float *w2 = W2s + o * 33;
+          float c0 = b2s[o], c1 = 0.0f, c2 = 0.0f, c3 = 0.0f;
+#pragma unroll
+          for (int j = 0; j < 32; j += 4) {
+            c0 = fmaf(w2[j], a1[j], c0);
+            c1 = fmaf(w2[j + 1], a1[j + 1], c1);
+            c2 = fmaf(w2[j + 2], a1[j + 2], c2);
+            c3 = fmaf(w2[j + 3], a1[j + 3], c3);
+          }
+          orow[o] = act_only(p.act_o, (c0 + c1) + (c2 + c3));
+        }
+      }
+      asm volatile("bar.sync 1, 128;" ::: "memory");  // zt free for the next tile
+    }
+    if (prof && q == 0 && lane == 0) { prof[7] = w0; prof[9] = clock64() - tstart; }
+  }
+  tc::tc_fence_before();
+  __syncthreads();
+  if (prof && tid == 0) { prof[8] = clock64() - tstart; prof[10] = ntiles * p.nkb; }
+  if (warp == 1) {
+    tc::tc_fence_after();
+    asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem), "r"((uint32_t)(2 * ts::kRows)) : "memory");
+  }
+}
+
+// ---- x as the shared-memory A operand (infer_tcX_kernel): Z1 = X [W1_hi ; W1_lo]^T with A = the x
+// tile exactly as TMA wrote it (M = 128 rows, K-major SWIZZLE_128B; the tensor core truncates it to
+// its TF32 part) and, second MMA of the k-step, A = the x_lo tile the converters write beside it; B =
+// the W stage's 64 rows (W1 hi | W1 lo stacked along N), D = 128 lanes (rows) x 64 columns.  No
+// tensor-memory staging of x (tcgen05.st) and no transposition in the epilogue (thread = row).
+namespace tx {
+constexpr int kRows = 128;
+constexpr int kXS = 7, kLS = 4;                      // x ring / (x_lo, W) ring depths
+constexpr int kXBytes = kRows * kKB * 4;             // 16 KB
+constexpr int kWStage = 2 * 32 * kKB * 4;            // 8 KB: W hi rows 0..31 | W lo rows 32..63
+constexpr int kCvtWarps = 8;
+constexpr int kThreads = 32 * (2 + kCvtWarps + 4 + 1);   // x TMA, MMA, converters, epilogue, W TMA
+constexpr int kSmem = 1024 + kXS * kXBytes + kLS * kXBytes + kLS * kWStage + (32 * 33 + 64) * 4 + 256;
+static_assert(kSmem <= 232448, "shared memory");
+}  // namespace ts
+
+__global__ void __launch_bounds__(tx::kThreads, 1)
+infer_tcX_kernel(const InferTcParams p, const __grid_constant__ CUtensorMap tmX,
+                 const __grid_constant__ CUtensorMap tmWh, const __grid_constant__ CUtensorMap tmWl) {
+  extern __shared__ __align__(1024) uint8_t smraw[];
+  uint8_t *xring = reinterpret_cast<uint8_t *>((reinterpret_cast<uintptr_t>(smraw) + 1023) & ~uintptr_t(1023));
+  uint8_t *lring = xring + tx::kXS * tx::kXBytes;
+  uint8_t *wring = lring + tx::kLS * tx::kXBytes;
+  float *W2s = reinterpret_cast<float *>(wring + tx::kLS * tx::kWStage);   // [32][33]
+  float *b1s = W2s + 32 * 33, *b2s = b1s + 32;
+  uint64_t *xfull = reinterpret_cast<uint64_t *>(b2s + 32);
+  uint64_t *xempty = xfull + tx::kXS, *lfull = xempty + tx::kXS, *wfull = lfull + tx::kLS, *mdone = wfull + tx::kLS;
+  uint64_t *afull = mdone + tx::kLS, *aempty = afull + 2;
+  uint32_t *tslot = reinterpret_cast<uint32_t *>(aempty + 2);
+  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+
+  const int64_t bb = (int64_t)blockIdx.x * p.nblk / gridDim.x, be = (int64_t)(blockIdx.x + 1) * p.nblk / gridDim.x;
+  const int64_t r0 = bb * kBoxRows, r1 = min(p.n, be * kBoxRows);
+  const int ntiles = r1 > r0 ? (int)((r1 - r0 + tx::kRows - 1) / tx::kRows) : 0;
+
+  if (tid == 0) {
+    for (int i = 0; i < tx::kXS; ++i) {
+      ptx::mbar_init(&xfull[i], 1);
+      ptx::mbar_init(&xempty[i], 1);
+    }
+    for (int i = 0; i < tx::kLS; ++i) {
+      ptx::mbar_init(&lfull[i], tx::kCvtWarps);
+      ptx::mbar_init(&wfull[i], 1);
+      ptx::mbar_init(&mdone[i], 1);   // the MMAs of this x_lo / W slot have completed
+    }
+    for (int i = 0; i < 2; ++i) {
+      ptx::mbar_init(&afull[i], 1);
+      ptx::mbar_init(&aempty[i], 4);
+    }
+    ptx::fence_mbar_init();
+    ptx::prefetch_tensormap(&tmX);
+    ptx::prefetch_tensormap(&tmWh);
+    ptx::prefetch_tensormap(&tmWl);
+  }
+  if (warp == 1) {
+    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(ptx::smem_u32(tslot)),
+                 "r"(128u) : "memory");
+    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;" ::: "memory");
+  }
+  for (int i = tid; i < 32 * 32; i += tx::kThreads) {
+    const int o = i >> 5, j = i & 31;
+    W2s[o * 33 + j] = (o < p.O && j < p.H) ? p.W2[o * p.H + j] : 0.0f;
+  }
+  if (tid < 32) {
+    b1s[tid] = tid < p.H ? p.b1[tid] : 0.0f;
+    b2s[tid] = tid < p.O ? p.b2[tid] : 0.0f;
+  }
+  tc::tc_fence_before();
+  __syncthreads();
+  tc::tc_fence_after();
+  const uint32_t tmem = *tslot;
+  const long long tstart = p.prof ? clock64() : 0;
+  long long w0 = 0, w1 = 0, w2 = 0;
+  long long *prof = p.prof ? p.prof + 16 * blockIdx.x : nullptr;
+
+  if (warp == 0) {
+    if (lane == 0) {  // ---- TMA: x tiles (boxes of 32 rows)
+      int g = 0;
+      for (int i = 0; i < ntiles; ++i) {
+        const int64_t row = r0 + (int64_t)i * tx::kRows;
+        const int64_t rows_here = r1 - row < tx::kRows ? r1 - row : tx::kRows;
+        const int nbox = (int)((rows_here + kBoxRows - 1) / kBoxRows);
+        for (int kb = 0; kb < p.nkb; ++kb, ++g) {
+          const int s = g % tx::kXS;
+          { ITC_T0(); ptx::mbar_wait(&xempty[s], ((g / tx::kXS) & 1) ^ 1); ITC_ACC(w0); }
+          uint8_t *st = xring + s * tx::kXBytes;
+          ptx::mbar_arrive_expect_tx(&xfull[s], (uint32_t)(nbox * kBoxRows * 128));
+          for (int b = 0; b < nbox; ++b)
+            ptx::tma_load_2d(st + b * (kBoxRows * 128), &tmX, &xfull[s], kb * kKB, (int)(row + b * kBoxRows));
+        }
+      }
+      if (prof) prof[0] = w0;
+    }
+  } else if (warp == tx::kThreads / 32 - 1) {
+    if (lane == 0) {  // ---- TMA: W1 hi | lo K-blocks
+      const int total = ntiles * p.nkb;
+      for (int g = 0; g < total; ++g) {
+        const int w = g % tx::kLS, kb = g % p.nkb;
+        { ITC_T0(); ptx::mbar_wait(&mdone[w], ((g / tx::kLS) & 1) ^ 1); ITC_ACC(w0); }
+        uint8_t *st = wring + w * tx::kWStage;
+        ptx::mbar_arrive_expect_tx(&wfull[w], (uint32_t)tx::kWStage);
+        ptx::tma_load_2d(st, &tmWh, &wfull[w], kb * kKB, 0);
+        ptx::tma_load_2d(st + tx::kWStage / 2, &tmWl, &wfull[w], kb * kKB, 0);
+      }
+      if (prof) prof[1] = w0;
+    }
+  } else if (warp == 1) {
+    if (lane == 0) {  // ---- MMA issuer
+      constexpr uint32_t idesc = tc::idesc_tf32(128, 64, false, false);   // N = 64: W1 hi rows | W1 lo rows
+      int g = 0;
+      for (int i = 0; i < ntiles; ++i) {
+        const int a = i & 1;
+        { ITC_T0(); ptx::mbar_wait(&aempty[a], ((i >> 1) & 1) ^ 1); ITC_ACC(w2); }
+        tc::tc_fence_after();
+        const uint32_t d = tmem + 64u * a;
+        for (int kb = 0; kb < p.nkb; ++kb, ++g) {
+          const int s = g % tx::kXS, w = g % tx::kLS;
+          { ITC_T0(); ptx::mbar_wait(&wfull[w], (g / tx::kLS) & 1); ITC_ACC(w0); }
+          { ITC_T0(); ptx::mbar_wait(&lfull[w], (g / tx::kLS) & 1); ITC_ACC(w1); }  // x landed and its lo part written
+          tc::tc_fence_after();
+          const uint32_t xh = ptx::smem_u32(xring + s * tx::kXBytes), xl = ptx::smem_u32(lring + w * tx::kXBytes);
+          const uint32_t ws = ptx::smem_u32(wring + w * tx::kWStage);
+#pragma unroll
+          for (int ks = 0; ks < kKB / 8; ++ks) {
+            if (p.exp & 2) break;
+            const uint64_t dw = tc::smem_desc(ws + 32u * ks, 16, 1024, 2);
+            const uint64_t dxh = tc::smem_desc(xh + 32u * ks, 16, 1024, 2), dxl = tc::smem_desc(xl + 32u * ks, 16, 1024, 2);
+            if (!(p.exp & 16)) tc::mma_tf32(d, dxl, dw, idesc, (kb | ks) ? 1u : 0u);  // small terms first
+            tc::mma_tf32(d, dxh, dw, idesc, (p.exp & 16) ? ((kb | ks) ? 1u : 0u) : 1u);
+          }
+          tc::mma_commit(&xempty[s]);
+          tc::mma_commit(&mdone[w]);
+          if (kb == p.nkb - 1) tc::mma_commit(&afull[a]);
+        }
+      }
+      if (prof) { prof[2] = w0; prof[3] = w1; prof[4] = w2; }
+    }
+  } else if (warp < 2 + tx::kCvtWarps) {
+    // ---- converters: x_lo = rn_tf32(x - trunc(x)), elementwise over the swizzled tile (the
+    //      layouts match: same byte offset), 64 B per thread per K-block
+    const int ct = tid - 64;
+    const int total = ntiles * p.nkb;
+    for (int g = 0; g < total; ++g) {
+      const int s = g % tx::kXS, w = g % tx::kLS;
+      { ITC_T0(); ptx::mbar_wait(&xfull[s], (g / tx::kXS) & 1); ITC_ACC(w0); }
+      { ITC_T0(); ptx::mbar_wait(&mdone[w], ((g / tx::kLS) & 1) ^ 1); ITC_ACC(w1); }
+      const float4 *src = reinterpret_cast<const float4 *>(xring + s * tx::kXBytes);
+      float4 *dst = reinterpret_cast<float4 *>(lring + w * tx::kXBytes);
+      float4 v[tx::kXBytes / 16 / (32 * tx::kCvtWarps)];
+#pragma unroll
+      for (int c = 0; c < tx::kXBytes / 16 / (32 * tx::kCvtWarps); ++c) v[c] = src[ct + 32 * tx::kCvtWarps * c];
+#pragma unroll
+      for (int c = 0; c < tx::kXBytes / 16 / (32 * tx::kCvtWarps); ++c) {
+        if (p.exp & 4) break;
+        dst[ct + 32 * tx::kCvtWarps * c] = make_float4(tf32_lo(v[c].x), tf32_lo(v[c].y), tf32_lo(v[c].z), tf32_lo(v[c].w));
+      }
+      ptx::fence_proxy_async_smem();  // generic-proxy writes -> visible to the tensor core
+      __syncwarp();
+      if (lane == 0) ptx::mbar_arrive(&lfull[w]);
+    }
+    if (prof && tid == 64) { prof[5] = w0; prof[6] = w1; }
+  } else {
+    // ---- epilogue, thread = row 32 q + lane of the tile: both halves of the Z1 row from TMEM
+    const int q = warp & 3;
+    const int H = p.H, O = p.O;
+    for (int i = 0; i < ntiles; ++i) {
+      const int a = i & 1;
+      { ITC_T0(); ptx::mbar_wait(&afull[a], (i >> 1) & 1); ITC_ACC(w0); }
+      tc::tc_fence_after();
+      float z[32], zl[32];
+      tc::tmem_ld32(tmem + ((uint32_t)(32 * q) << 16) + 64u * a, z);
+      tc::tmem_ld32(tmem + ((uint32_t)(32 * q) << 16) + 64u * a + 32u, zl);
+      tc::tc_fence_before();
+      __syncwarp();
+      if (lane == 0) ptx::mbar_arrive(&aempty[a]);
+      const int64_t row = r0 + (int64_t)i * tx::kRows + 32 * q + lane;
+      if (row < r1) {
+        float a1[32];
+#pragma unroll
+        for (int j = 0; j < 32; ++j) a1[j] = j < H ? act_only(p.act_h, (z[j] + zl[j]) + b1s[j]) : 0.0f;
+        float *orow = p.out + row * O;
+        for (int o = 0; o < O; ++o) {
+          const float *w2 = W2s + o * 33;
+          float c0 = b2s[o], c1 = 0.0f, c2 = 0.0f, c3 = 0.0f;
+#pragma unroll
+          for (int j = 0; j < 32; j += 4) {
+            c0 = fmaf(w2[j], a1[j], c0);
+            c1 = fmaf(w2[j + 1], a1[j + 1], c1);
+            c2 = fmaf(w2[j + 2], a1[j + 2], c2);
+            c3 = fmaf(w2[j + 3], a1[j + 3], c3);
+          }
+          orow[o] = act_only(p.act_o, (c0 + c1) + (c2 + c3));
+        }
+      }
+    }
+    if (prof && q == 0 && lane == 0) { prof[7] = w0; prof[9] = clock64() - tstart; }
+  }
+  tc::tc_fence_before();
+  __syncthreads();
+  if (prof && tid == 0) { prof[8] = clock64() - tstart; prof[10] = ntiles * p.nkb; }
+  if (warp == 1) {
+    tc::tc_fence_after();
+    asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem), "r"(128u) : "memory");
+  }
+}
+
 }  // namespace
 
 bool infer_tc_applicable(const std::vector<int> &dims, const float *X) {
@@ -509,6 +976,8 @@ cudaError_t infer_tc(cudaStream_t st, const std::vector<int> &dims, int act_h, i
   {
     cudaError_t e = set_max_smem(reinterpret_cast<const void *>(infer_tc_kernel), kSmem);
     if (e == cudaSuccess) e = set_max_smem(reinterpret_cast<const void *>(infer_tcT_kernel), tt::kSmem);
+    if (e == cudaSuccess) e = set_max_smem(reinterpret_cast<const void *>(infer_tcS_kernel), ts::kSmem);
+    if (e == cudaSuccess) e = set_max_smem(reinterpret_cast<const void *>(infer_tcX_kernel), tx::kSmem);
     if (e != cudaSuccess) return e;
   }
   // tensor maps, cached per (pointer, shape): encoding costs host microseconds per call
@@ -549,8 +1018,41 @@ cudaError_t infer_tc(cudaStream_t st, const std::vector<int> &dims, int act_h, i
   p.out = out;
   p.exp = getenv("NF_ITC_EXP") ? atoi(getenv("NF_ITC_EXP")) : 0;
   const int blocks = (int)std::max<int64_t>(1, std::min<int64_t>(p.nblk, 148));
-  static const int form = getenv("NF_INFER_TC_FORM") ? atoi(getenv("NF_INFER_TC_FORM")) : 1;
-  if (form == 1) {  // transposed: Z1^T = W1 X^T, N = 128 rows per MMA (default)
+  static const bool want_prof = getenv("NF_ITC_PROF") != nullptr;
+  static long long *dprof = nullptr;
+  if (want_prof && !dprof) cudaMalloc(&dprof, 148 * 16 * sizeof(long long));
+  if (want_prof) cudaMemsetAsync(dprof, 0, 148 * 16 * sizeof(long long), st);
+  p.prof = want_prof ? dprof : nullptr;
+  auto report = [&]() {  // wait-time counters (clocks), mean over CTAs, to stderr
+    if (!want_prof) return;
+    std::vector<long long> h(148 * 16);
+    cudaStreamSynchronize(st);
+    cudaMemcpy(h.data(), dprof, h.size() * sizeof(long long), cudaMemcpyDeviceToHost);
+    static const char *nm[11] = {"xTMA wait xempty", "wTMA wait mdone", "MMA wait wfull", "MMA wait x ready", "MMA wait aempty",
+                                 "cvt wait xfull", "cvt wait slot", "epi wait afull", "CTA total", "epi done", "K-blocks"};
+    for (int k = 0; k < 11; ++k) {
+      double m = 0, mx = 0;
+      for (int b = 0; b < blocks; ++b) { m += (double)h[b * 16 + k]; mx = std::max(mx, (double)h[b * 16 + k]); }
+      fprintf(stderr, "[itc] %-18s mean %9.0f  max %9.0f\n", nm[k], m / blocks, mx);
+    }
+  };
+  // 0 (default): x from TMEM, W1 hi | lo stacked along N; 1: transposed, 3 MMAs per k-step; 2: transposed, stacked along M
+  const int form = getenv("NF_INFER_TC_FORM") ? atoi(getenv("NF_INFER_TC_FORM")) : 0;
+  if (form == 3) {  // x as the shared-memory A operand, W1 hi | lo stacked along N
+    infer_tcX_kernel<<<blocks, tx::kThreads, tx::kSmem, st>>>(p, mX, mWh, mWl);
+    count_launch();
+    log_launch(reinterpret_cast<const void *>(infer_tcX_kernel), dim3(blocks), dim3(tx::kThreads), tx::kSmem);
+    report();
+    return cudaGetLastError();
+  }
+  if (form == 2) {  // transposed, W1 hi / lo stacked along M: 2 MMAs per k-step
+    infer_tcS_kernel<<<blocks, ts::kThreads, ts::kSmem, st>>>(p, mX, mWh, mWl);
+    count_launch();
+    log_launch(reinterpret_cast<const void *>(infer_tcS_kernel), dim3(blocks), dim3(ts::kThreads), ts::kSmem);
+    report();
+    return cudaGetLastError();
+  }
+  if (form == 1) {  // transposed: Z1^T = W1 X^T, N = 128 rows per MMA, 3 MMAs per k-step
     infer_tcT_kernel<<<blocks, tt::kThreads, tt::kSmem, st>>>(p, mX, mWh, mWl);
     count_launch();
     log_launch(reinterpret_cast<const void *>(infer_tcT_kernel), dim3(blocks), dim3(tt::kThreads), tt::kSmem);
@@ -559,6 +1061,7 @@ cudaError_t infer_tc(cudaStream_t st, const std::vector<int> &dims, int act_h, i
   infer_tc_kernel<<<blocks, kThreads, kSmem, st>>>(p, mX, mWh, mWl);
   count_launch();
   log_launch(reinterpret_cast<const void *>(infer_tc_kernel), dim3(blocks), dim3(kThreads), kSmem);
+  report();
   return cudaGetLastError();
 }
 

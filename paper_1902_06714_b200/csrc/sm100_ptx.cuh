@@ -44,6 +44,24 @@ __device__ __forceinline__ void mbar_wait(uint64_t *bar, uint32_t parity) {
   }
 }
 
+// ---- warp-uniform issue of single-thread instructions ------------------------------------------
+// tcgen05.mma / commit and TMA loads are issued by ONE thread, but their operands (descriptors,
+// tensor-memory addresses, barriers) must reach the uniform datapath: in code the compiler cannot
+// prove warp-uniform (`if (lane == 0)` around the whole loop) every such instruction is wrapped in an
+// ELECT / R2UR.BROADCAST / BRA.U.ANY loop (~12 extra instructions and the R2UR latencies per MMA).
+// So: branch on warp_uniform() (a shuffle result the compiler treats as uniform), let all 32 lanes
+// run the loop and its barrier waits, and put only the instruction itself under elect_one().
+__device__ __forceinline__ int warp_uniform(int v) { return __shfl_sync(0xffffffffu, v, 0); }
+__device__ __forceinline__ bool elect_one() {
+  uint32_t pred;
+  asm volatile(
+      "{\n\t.reg .pred p;\n\t"
+      "elect.sync _|p, 0xffffffff;\n\t"
+      "selp.u32 %0, 1, 0, p;\n\t}"
+      : "=r"(pred));
+  return pred != 0;
+}
+
 // ---- proxy fences -------------------------------------------------------------
 // generic-proxy writes to shared memory -> visible to the async proxy (bulk copies / TMA / MMA)
 __device__ __forceinline__ void fence_proxy_async_smem() {

@@ -421,11 +421,15 @@ def test_fused_inference_equals_generic_path(monkeypatch):
                                         ([784, 30, 10], "sigmoid", 33), ([784, 30, 10], "sigmoid", 4767),
                                         ([100, 17, 3], "tanh,sigmoid", 777), ([64, 32, 32], "relu,tanh", 300),
                                         ([36, 8, 1], "gaussian,sigmoid", 129)])
-def test_tensor_core_inference(dims, act, n, monkeypatch):
-    """nf_output of two-layer nets with narrow layers on the tcgen05 inference kernel (3xTF32,
-    infer_tc.cu): ragged 32-row TMA boxes and 128-row tiles, a ragged last 32-pixel K-block (n0 =
-    100, 36), every width up to 32, against the oracle at the fp32 bar; the launch log proves the
-    kernel ran, and the FFMA2 kernel (NF_INFER_SIMT=1) agrees."""
+@pytest.mark.parametrize("form", [0, 1, 2, 3])
+def test_tensor_core_inference(dims, act, n, form, monkeypatch):
+    """nf_output of two-layer nets with narrow layers on the tcgen05 inference kernels (split TF32,
+    infer_tc.cu; form 0 = the default: x from TMEM against W1 hi | lo stacked along N; 1 =
+    transposed, three MMAs per k-step; 2 = transposed, W1 hi | lo stacked along M): ragged 32-row
+    TMA boxes and 128-row tiles, a ragged last 32-pixel K-block (n0 = 100, 36), every width up to
+    32, against the oracle at the fp32 bar; the launch log proves the kernel ran, and the FFMA2
+    kernel (NF_INFER_SIMT=1) agrees."""
+    monkeypatch.setenv("NF_INFER_TC_FORM", str(form))
     p = synth.random_params(n + 3, dims, 0.5)
     x, _ = synth.random_batch(n + 5, n, dims[0], dims[-1], "uniform")
     net = make_net(dims, act, p)
@@ -433,7 +437,7 @@ def test_tensor_core_inference(dims, act, n, monkeypatch):
     out = net.output(dev(x)).cpu().numpy()
     log = nf.nf_debug_log_read()
     nf.nf_debug_log_enable(False)
-    assert any("infer_tc" in l for l in log), log
+    assert any(("infer_tc_kernel", "infer_tcT_kernel", "infer_tcS_kernel", "infer_tcX_kernel")[form] in l for l in log), log
     rows = np.arange(n) if n <= 5000 else np.random.default_rng(0).choice(n, 4000, replace=False)
     ref = oracle.Oracle(dims, act).output(p, np.ascontiguousarray(x[rows]))
     assert rel_err(out[rows], ref) <= FP32_BAR
