@@ -171,7 +171,7 @@ gemm_tc_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ 
   uint64_t *accum = conv + C::STAGES;
   uint32_t *tmem_slot = reinterpret_cast<uint32_t *>(accum + 1);
 
-  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int warp = ptx::warp_uniform(threadIdx.x >> 5), lane = threadIdx.x & 31;
   const int n0 = blockIdx.x * BN, m0 = blockIdx.y * BM;
   const int kbeg = blockIdx.z * g.kchunk;
   const int kend = min(g.K, kbeg + g.kchunk);
@@ -203,15 +203,17 @@ gemm_tc_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ 
   const uint32_t tmem = *tmem_slot;
   ptx::pdl_wait();  // prologue above overlaps the previous kernel
 
-  if (warp == 0) {
-    if (lane == 0) {  // ---- TMA producer
-      for (int it = 0; it < nkb; ++it) {
-        const int s = it % C::STAGES;
-        if (it >= C::STAGES) ptx::mbar_wait(&empty[s], (uint32_t)(((it / C::STAGES) - 1) & 1));
-        uint8_t *sa = smem + s * C::STAGE_BYTES;
-        uint8_t *sb = sa + C::A_BYTES;
-        const int k = kbeg + it * BK;
-        const bool pre = SPLIT == 3 && g.pre;
+  // The TMA and MMA warps run their loops and barrier waits with all 32 lanes (warp-uniform control
+  // flow, operands in uniform registers) and issue through one elected lane (ptx::elect_one).
+  if (warp == 0) {  // ---- TMA producer
+    int s = 0;
+    for (int it = 0; it < nkb; ++it) {
+      if (it >= C::STAGES) ptx::mbar_wait(&empty[s], (uint32_t)(((it / C::STAGES) - 1) & 1));
+      uint8_t *sa = smem + s * C::STAGE_BYTES;
+      uint8_t *sb = sa + C::A_BYTES;
+      const int k = kbeg + it * BK;
+      const bool pre = SPLIT == 3 && g.pre;
+      if (ptx::elect_one()) {
         ptx::mbar_arrive_expect_tx(&full[s], (uint32_t)(pre ? 2 * C::RAW_BYTES : C::RAW_BYTES));
         // (pre: a second pass with the lo maps into the lo half of the stage)
         for (int half = 0; half < (pre ? 2 : 1); ++half) {
@@ -231,21 +233,24 @@ gemm_tc_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ 
           }
         }
       }
+      __syncwarp();
+      if (++s == C::STAGES) s = 0;
     }
-  } else if (warp == 1) {
-    if (lane == 0) {  // ---- MMA issuer
-      constexpr uint32_t idesc = idesc_tf32(BM, BN, A_MN, B_MN);
-      for (int it = 0; it < nkb; ++it) {
-        const int s = it % C::STAGES;
-        const uint32_t par = (uint32_t)((it / C::STAGES) & 1);
-        ptx::mbar_wait((SPLIT == 3 && !g.pre) ? &conv[s] : &full[s], par);
-        tc_fence_after();
-        const uint32_t sa = ptx::smem_u32(smem + s * C::STAGE_BYTES);
-        const uint32_t sb = sa + C::A_BYTES;
+  } else if (warp == 1) {  // ---- MMA issuer
+    constexpr uint32_t idesc = idesc_tf32(BM, BN, A_MN, B_MN);
+    const uint32_t tmem_u = (uint32_t)ptx::warp_uniform((int)tmem), smem_u = ptx::smem_u32(smem);
+    int s = 0;
+    uint32_t par = 0;
+    for (int it = 0; it < nkb; ++it) {
+      ptx::mbar_wait((SPLIT == 3 && !g.pre) ? &conv[s] : &full[s], par);
+      tc_fence_after();
+      const uint32_t sa = smem_u + (uint32_t)(s * C::STAGE_BYTES);
+      const uint32_t sb = sa + C::A_BYTES;
+      if (ptx::elect_one()) {
 #pragma unroll
         for (int ks = 0; ks < BK / 8; ++ks) {
           const int t = it * (BK / 8) + ks;                  // global K-step
-          const uint32_t d = tmem + (uint32_t)((t % C::NACC) * BN);
+          const uint32_t d = tmem_u + (uint32_t)((t % C::NACC) * BN);
           const uint32_t acc = t >= C::NACC ? 1u : 0u;       // first use of each accumulator
           const uint64_t ah = op_desc<A_MN>(sa, ks), bh = op_desc<B_MN>(sb, ks);
           mma_tf32(d, ah, bh, idesc, acc);
@@ -256,8 +261,10 @@ gemm_tc_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ 
           }
         }
         mma_commit(&empty[s]);
+        if (it == nkb - 1) mma_commit(accum);
       }
-      mma_commit(accum);
+      __syncwarp();
+      if (++s == C::STAGES) { s = 0; par ^= 1; }
     }
   } else {
     const int t = threadIdx.x - 64;  // 0 .. 32 EW - 1
@@ -362,7 +369,7 @@ gemm_tc_persistent(const __grid_constant__ CUtensorMap tmA, const __grid_constan
   uint64_t *tempty = tfull + 2;          // [2] accumulator stage drained (kEpiWarps arrivals)
   uint32_t *tmem_slot = reinterpret_cast<uint32_t *>(tempty + 2);
 
-  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int warp = ptx::warp_uniform(threadIdx.x >> 5), lane = threadIdx.x & 31;
   const int tn = (N + BN - 1) / BN, ntiles = ((M + BM - 1) / BM) * tn;
   const int nkb = (K + BK - 1) / BK;
 
@@ -390,17 +397,16 @@ gemm_tc_persistent(const __grid_constant__ CUtensorMap tmA, const __grid_constan
   const uint32_t tmem = *tmem_slot;
   ptx::pdl_wait();  // prologue above overlaps the previous kernel
 
-  if (warp == 0) {
-    if (lane == 0) {  // ---- TMA producer, continuous over tiles
-      int it = 0;
-      for (int tile = blockIdx.x; tile < ntiles; tile += gridDim.x) {
-        const int m0 = (tile / tn) * BM, n0 = (tile % tn) * BN;
-        for (int kb = 0; kb < nkb; ++kb, ++it) {
-          const int s = it % C::STAGES;
-          if (it >= C::STAGES) ptx::mbar_wait(&empty[s], (uint32_t)(((it / C::STAGES) - 1) & 1));
-          uint8_t *sa = smem + s * C::STAGE_BYTES;
-          uint8_t *sb = sa + C::A_BYTES;
-          const int k = kb * BK;
+  if (warp == 0) {  // ---- TMA producer, continuous over tiles (all lanes loop, one elected lane issues)
+    int it = 0, s = 0;
+    for (int tile = blockIdx.x; tile < ntiles; tile += gridDim.x) {
+      const int m0 = (tile / tn) * BM, n0 = (tile % tn) * BN;
+      for (int kb = 0; kb < nkb; ++kb, ++it) {
+        if (it >= C::STAGES) ptx::mbar_wait(&empty[s], (uint32_t)(((it / C::STAGES) - 1) & 1));
+        uint8_t *sa = smem + s * C::STAGE_BYTES;
+        uint8_t *sb = sa + C::A_BYTES;
+        const int k = kb * BK;
+        if (ptx::elect_one()) {
           ptx::mbar_arrive_expect_tx(&full[s], (uint32_t)C::RAW_BYTES);
           if (A_MN) {
 #pragma unroll
@@ -415,29 +421,34 @@ gemm_tc_persistent(const __grid_constant__ CUtensorMap tmA, const __grid_constan
             ptx::tma_load_2d(sb, &tmB, &full[s], k, n0);
           }
         }
+        __syncwarp();
+        if (++s == C::STAGES) s = 0;
       }
     }
-  } else if (warp == 1) {
-    if (lane == 0) {  // ---- MMA issuer
-      constexpr uint32_t idesc = idesc_tf32(BM, BN, A_MN, B_MN);
-      int it = 0, lt = 0;
-      for (int tile = blockIdx.x; tile < ntiles; tile += gridDim.x, ++lt) {
-        const int as = lt & 1;
-        if (lt >= 2) ptx::mbar_wait(&tempty[as], (uint32_t)(((lt >> 1) - 1) & 1));
+  } else if (warp == 1) {  // ---- MMA issuer (all lanes loop and wait, one elected lane issues)
+    constexpr uint32_t idesc = idesc_tf32(BM, BN, A_MN, B_MN);
+    const uint32_t tmem_u = (uint32_t)ptx::warp_uniform((int)tmem), smem_u = ptx::smem_u32(smem);
+    int s = 0, lt = 0;
+    uint32_t par = 0;
+    for (int tile = blockIdx.x; tile < ntiles; tile += gridDim.x, ++lt) {
+      const int as = lt & 1;
+      if (lt >= 2) ptx::mbar_wait(&tempty[as], (uint32_t)(((lt >> 1) - 1) & 1));
+      tc_fence_after();
+      const uint32_t d = tmem_u + (uint32_t)(as * BN);
+      for (int kb = 0; kb < nkb; ++kb) {
+        ptx::mbar_wait(&full[s], par);
         tc_fence_after();
-        const uint32_t d = tmem + (uint32_t)(as * BN);
-        for (int kb = 0; kb < nkb; ++kb, ++it) {
-          const int s = it % C::STAGES;
-          ptx::mbar_wait(&full[s], (uint32_t)((it / C::STAGES) & 1));
-          tc_fence_after();
-          const uint32_t sa = ptx::smem_u32(smem + s * C::STAGE_BYTES);
-          const uint32_t sb = sa + C::A_BYTES;
+        const uint32_t sa = smem_u + (uint32_t)(s * C::STAGE_BYTES);
+        const uint32_t sb = sa + C::A_BYTES;
+        if (ptx::elect_one()) {
 #pragma unroll
           for (int ks = 0; ks < BK / 8; ++ks)
             mma_tf32(d, op_desc<A_MN>(sa, ks), op_desc<B_MN>(sb, ks), idesc, (kb | ks) != 0 ? 1u : 0u);
           mma_commit(&empty[s]);
+          if (kb == nkb - 1) mma_commit(&tfull[as]);
         }
-        mma_commit(&tfull[as]);
+        __syncwarp();
+        if (++s == C::STAGES) { s = 0; par ^= 1; }
       }
     }
   } else {  // ---- epilogue warps: TMEM lane quadrant = warp % 4, even / odd 32-column chunks
