@@ -129,7 +129,17 @@ infer_tc_kernel(const InferTcParams p, const __grid_constant__ CUtensorMap tmX,
       ptx::mbar_init(&aempty[i], 4);
     }
     ptx::fence_mbar_init();
-    ptx::prefetch_tensormap(&tmX);
+    // the first ring-full of x K-blocks (all of tile 0) goes out before the rest of the prologue
+    // (TMEM allocation, W2 / bias staging): its HBM latency overlaps the set-up
+    if (ntiles > 0) {
+      const int64_t rows_here = r1 - r0 < kTileRows ? r1 - r0 : kTileRows;
+      const int nbox = (int)((rows_here + kBoxRows - 1) / kBoxRows);
+      for (int g = 0; g < kStages && g < p.nkb; ++g) {
+        ptx::mbar_arrive_expect_tx(&full[g], (uint32_t)(nbox * kBoxRows * kKB * 4));
+        for (int b = 0; b < nbox; ++b)
+          ptx::tma_load_2d(ring + g * kXBytes + b * (kBoxRows * 128), &tmX, &full[g], g * kKB, (int)(r0 + b * kBoxRows));
+      }
+    }
     ptx::prefetch_tensormap(&tmWh);
     ptx::prefetch_tensormap(&tmWl);
   }
@@ -155,24 +165,29 @@ infer_tc_kernel(const InferTcParams p, const __grid_constant__ CUtensorMap tmX,
   long long *prof = p.prof ? p.prof + 16 * blockIdx.x : nullptr;
 
   if (warp == 0) {
-    // ---- TMA producer of the x tiles
-    if (lane == 0) {
-      int g = 0;
-      for (int i = 0; i < ntiles; ++i) {
-        const int64_t row = r0 + (int64_t)i * kTileRows;
-        const int64_t rows_here = r1 - row < kTileRows ? r1 - row : kTileRows;
-        const int nbox = (int)((rows_here + kBoxRows - 1) / kBoxRows);
-        for (int kb = 0; kb < p.nkb; ++kb, ++g) {
-          const int s = g % kStages;
-          { ITC_T0(); ptx::mbar_wait(&empty[s], ((g / kStages) & 1) ^ 1); ITC_ACC(w0); }
-          uint8_t *st = ring + s * kXBytes;
-          ptx::mbar_arrive_expect_tx(&full[s], (uint32_t)(nbox * kBoxRows * kKB * 4));
-          for (int b = 0; b < nbox; ++b)
-            ptx::tma_load_2d(st + b * (kBoxRows * 128), &tmX, &full[s], kb * kKB, (int)(row + b * kBoxRows));
+    // ---- TMA producer of the x tiles (all lanes run the loop, one elected lane issues; the first
+    //      kStages K-blocks went out in the prologue)
+    int g = 0, s = 0;
+    uint32_t par = 1;  // parity of the 'empty' phase to wait for (first pass: passes at once)
+    for (int i = 0; i < ntiles; ++i) {
+      const int64_t row = r0 + (int64_t)i * kTileRows;
+      const int64_t rows_here = r1 - row < kTileRows ? r1 - row : kTileRows;
+      const int nbox = (int)((rows_here + kBoxRows - 1) / kBoxRows);
+      for (int kb = 0; kb < p.nkb; ++kb, ++g) {
+        if (g >= kStages || g >= p.nkb) {
+          { ITC_T0(); ptx::mbar_wait(&empty[s], par); ITC_ACC(w0); }
+          if (ptx::elect_one()) {
+            uint8_t *st = ring + s * kXBytes;
+            ptx::mbar_arrive_expect_tx(&full[s], (uint32_t)(nbox * kBoxRows * kKB * 4));
+            for (int b = 0; b < nbox; ++b)
+              ptx::tma_load_2d(st + b * (kBoxRows * 128), &tmX, &full[s], kb * kKB, (int)(row + b * kBoxRows));
+          }
+          __syncwarp();
         }
+        if (++s == kStages) { s = 0; par ^= 1; }
       }
-      if (prof) prof[0] = w0;
     }
+    if (prof && lane == 0) prof[0] = w0;
   } else if (warp == kThreads / 32 - 1) {
     // ---- TMA producer of the W1 hi | lo K-blocks (L2-resident)
     if (lane == 0 && !(p.exp & 8)) {
