@@ -192,6 +192,9 @@ __host__ __device__ inline Smem smem_layout(int wpad, int nSmax, int nOwnMax, in
 
 // byte offset of element (row r, column c < 32) inside a 32-column atom of 128-B rows
 __device__ __forceinline__ int sw128_k(int r, int c) { return r * 128 + ((((c >> 2) ^ (r & 7))) << 4) + ((c & 3) << 2); }
+// W1 slice of the TC variant: per 32-pixel atom 8 KB = hi rows 0..31 | lo rows 32..63, so one K-major
+// B descriptor of N = 64 rows reads W_hi and W_lo stacked along N
+__device__ __forceinline__ int tc_w_off(int j, int k) { return (k >> 5) * 8192 + sw128_k(j, k & 31); }
 __device__ __forceinline__ int sw128_32b(int r, int c) { return r * 128 + ((((c >> 3) ^ (r & 3))) << 5) + ((c & 7) << 2); }
 // in-place TF32 split of `bytes` of staged fp32 data: hi = rn_tf32(x) in place, lo = x - hi (exact)
 __device__ __forceinline__ void tc_split(uint8_t *hi, uint8_t *lo, int bytes, int tid) {
@@ -381,23 +384,29 @@ fused_small_kernel(const FusedParams p, const __grid_constant__ CUtensorMap tmX,
       ptx::prefetch_tensormap(&tmXM);
     }
   }
-  if (TC && warp == 0) {  // 64 TMEM columns: Z1 partial accumulator | dW1 accumulator
+  if (TC && warp == 0) {  // 128 TMEM columns: Z1 partial accumulator (x W_hi | x W_lo) | dW1 accumulator (x^T d_hi | x^T d_lo)
     asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;"
-                 ::"r"(ptx::smem_u32(tmem_slot)), "r"(64u) : "memory");
+                 ::"r"(ptx::smem_u32(tmem_slot)), "r"(128u) : "memory");
     asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;" ::: "memory");
   }
   tc::tc_fence_before();
   __syncthreads();
   tc::tc_fence_after();
   const uint32_t tmem = TC ? *tmem_slot : 0u;
+  if (TC && tid == 0 && p.n_steps > 0) {  // step 0's K-layout x tile: its HBM latency overlaps the parameter staging below
+    const int64_t row00 = (p.starts ? p.starts[0] : ist.v[0]) + r0;
+    ptx::mbar_arrive_expect_tx(&bar_x[0], 4u * kTcAS);
+#pragma unroll
+    for (int a = 0; a < 4; ++a) ptx::tma_load_2d(X + a * kTcAS, &tmXK, &bar_x[0], k0 + 32 * a, (int)row00);
+  }
   if (TC) {  // W1 slice as TF32 hi + fp32 lo in the K-major SWIZZLE_128B B-operand layout
     for (int i = tid; i < 32 * 128; i += kThreads) {
       const int j = i >> 7, k = i & 127;
       const float v = (j < H && k < w) ? p.params[oW1 + (int64_t)j * n0 + k0 + k] : 0.0f;
       const float h = tc::tf32_hi(v);
-      const int off = (k >> 5) * 4096 + sw128_k(j, k & 31);
+      const int off = tc_w_off(j, k);
       *reinterpret_cast<float *>(Wt + off) = h;
-      *reinterpret_cast<float *>(Wt + 16384 + off) = v - h;
+      *reinterpret_cast<float *>(Wt + 4096 + off) = v - h;
     }
   } else if (MM) {  // fragment order: [j][nb][lane][4] = W1[8 nb + lane / 4][k0 + 16 j + 4 (lane % 4) + e]
     for (int i = tid; i < nj * 512; i += kThreads) {
@@ -450,7 +459,12 @@ fused_small_kernel(const FusedParams p, const __grid_constant__ CUtensorMap tmX,
     next_start = s + 1 < p.n_steps ? start_of(s + 1) : 0;
     float *xs = xs0 + buf * xstride;
     if (TC) {
-      // x tiles are staged by tc_issue (two layouts per step)
+      // x tiles are staged by tc_issue (two layouts per step); the rows are pulled into L2 a step
+      // ahead, so both tile loads of the step hit L2
+      if (tid == kThreads - 32) {
+#pragma unroll
+        for (int a = 0; a < 4; ++a) ptx::tma_prefetch_2d(&tmXK, k0 + 32 * a, (int)row0);
+      }
     } else if (p.aligned) {
       // issued by the last warp, which has no P1 task: the issue latency stays off the P1 path
       if (tid == kThreads - 32) {
@@ -479,8 +493,7 @@ fused_small_kernel(const FusedParams p, const __grid_constant__ CUtensorMap tmX,
   };
   int64_t row_s = next_start + r0;  // first row of step s's batch slice for this cluster
   prefetch(0);
-  if (TC && p.n_steps > 0) {  // step 0's K-layout tile
-    if (tid == 0) tc_issue(&tmXK, &bar_x[0], row_s);
+  if (TC && p.n_steps > 0) {  // step 0's K-layout tile (issued at the top of the kernel)
     ptx::mbar_wait(&bar_x[0], 0);
     tc_split(X, X + kTcXLoK, 4 * kTcAS, tid);
     ptx::fence_proxy_async_smem();
@@ -514,28 +527,36 @@ fused_small_kernel(const FusedParams p, const __grid_constant__ CUtensorMap tmX,
     // ---- P1. partial Z1: P[i][j] = sum_{k<w} x[i][k] W1[j][k0+k]
     if constexpr (TC) {
       // 3xTF32 on the tensor core: D[row][j] (TMEM cols 0..31), M = 128 rows, N = 32, K = pixels
-      if (tid == 0) {
+      if (ptx::warp_uniform(warp) == 0) {  // warp-uniform loop and operands, one elected lane issues
         tc::tc_fence_after();
-        constexpr uint32_t idK = tc::idesc_tf32(128, 32, false, false);
+        // B = 64 rows per atom: W_hi | W_lo stacked along N -> columns 0..31 x W_hi, 32..63 x W_lo; two
+        // MMAs per k-step (x_lo, x_hi) give all four partial products
+        constexpr uint32_t idK = tc::idesc_tf32(128, 64, false, false);
         const int nks = (p.ws + 7) / 8;
-        for (int ks = 0; ks < nks; ++ks) {
-          const uint32_t ao = (ks >> 2) * kTcAS + (ks & 3) * 32, bo = (ks >> 2) * 4096 + (ks & 3) * 32;
-          const uint64_t ah = tc::smem_desc(sX + ao, 16, 1024, 2), al = tc::smem_desc(sX + kTcXLoK + ao, 16, 1024, 2);
-          const uint64_t bh = tc::smem_desc(sW + bo, 16, 1024, 2), bl = tc::smem_desc(sW + 16384 + bo, 16, 1024, 2);
-          tc::mma_tf32(tmem, ah, bh, idK, ks > 0 ? 1u : 0u);
-          tc::mma_tf32(tmem, ah, bl, idK, 1u);
-          tc::mma_tf32(tmem, al, bh, idK, 1u);
+        const uint32_t tm = (uint32_t)ptx::warp_uniform((int)tmem);
+        if (ptx::elect_one()) {
+          for (int ks = 0; ks < nks; ++ks) {
+            const uint32_t ao = (ks >> 2) * kTcAS + (ks & 3) * 32, bo = (ks >> 2) * 8192 + (ks & 3) * 32;
+            const uint64_t ah = tc::smem_desc(sX + ao, 16, 1024, 2), al = tc::smem_desc(sX + kTcXLoK + ao, 16, 1024, 2);
+            const uint64_t bw = tc::smem_desc(sW + bo, 16, 1024, 2);
+            tc::mma_tf32(tm, al, bw, idK, ks > 0 ? 1u : 0u);
+            tc::mma_tf32(tm, ah, bw, idK, 1u);
+          }
+          tc::mma_commit(bar_mma);
         }
-        tc::mma_commit(bar_mma);
+        __syncwarp();
       }
       PROF(13);
       ptx::mbar_wait(bar_mma, 0);
       tc::tc_fence_after();
       PROF(14);
-      if (tid == 0) tc_issue(&tmXM, &bar_x[1], row_s);  // the MMAs are done with the K-layout tile
+      if (tid == 128) tc_issue(&tmXM, &bar_x[1], row_s);  // the MMAs are done with the K-layout tile (warp 4: not an epilogue warp)
       if (warp < 4) {
-        float v[32];
+        float v[32], vl[32];
         tc::tmem_ld32(tmem + ((uint32_t)(32 * warp) << 16), v);
+        tc::tmem_ld32(tmem + ((uint32_t)(32 * warp) << 16) + 32u, vl);
+#pragma unroll
+        for (int j = 0; j < 32; ++j) v[j] += vl[j];
         const int r = 32 * warp + lane;
         if (r < nS) {
 #pragma unroll
@@ -607,11 +628,17 @@ fused_small_kernel(const FusedParams p, const __grid_constant__ CUtensorMap tmX,
     PROF(2);
 
     // ---- P2. push the partial rows each peer owns into its Pown[rank] slot
-    if (warp == 0 && lane < C && lane != rank) {
-      const int c = lane;
+    // (one push per warp, lane 0 of warps 0..C-1: a single warp would issue its lanes' bulk copies
+    // one after the other, each behind an ELECT / R2UR.BROADCAST sequence)
+    if (lane == 0 && warp < C && warp != rank) {
+      const int c = warp;
       const int a0 = own_begin(c, nS, C), na = own_begin(c + 1, nS, C) - a0;
       if (na > 0)
         ptx::bulk_s2peer(Pown + rank * p.nOwnMax * 32, Pfull + a0 * 32, (uint32_t)(na * 128), bar_P, c);
+    }
+    if constexpr (TC) {  // the M-layout x tile of this step (issued after P1's MMAs) is split for P5
+      ptx::mbar_wait(&bar_x[1], par);   // here, while the peers' partial rows are still in flight
+      tc_split(X, X + kTcXLoM, 4 * kTcAS, tid);
     }
     ptx::mbar_wait(bar_P, par);
     PROF(3);
@@ -682,8 +709,8 @@ fused_small_kernel(const FusedParams p, const __grid_constant__ CUtensorMap tmX,
     // ---- P4. push the owned delta_1 rows to every peer at once; then this CTA's W2/b1/b2
     //      tendency partial over its owned rows (a 10x30x9 contraction) and its slices to
     //      the ranks that reduce them
-    if (warp == 0 && lane < C && lane != rank && nOwn > 0)
-      ptx::bulk_s2peer(D1 + o0 * ds, D1 + o0 * ds, (uint32_t)(nOwn * ds * 4), bar_D, lane);
+    if (lane == 0 && warp < C && warp != rank && nOwn > 0)
+      ptx::bulk_s2peer(D1 + o0 * ds, D1 + o0 * ds, (uint32_t)(nOwn * ds * 4), bar_D, warp);
     for (int t = tid; t < nsmp; t += kThreads) {
       float v = 0.0f;
       if (t < O * H) {
@@ -703,8 +730,8 @@ fused_small_kernel(const FusedParams p, const __grid_constant__ CUtensorMap tmX,
     }
     ptx::fence_proxy_async_smem();
     __syncthreads();
-    if (warp == 0 && lane < C && lane != rank) {
-      const int c = lane;
+    if (lane == 0 && warp < C && warp != rank) {
+      const int c = warp;
       const int ce0 = e_begin(c, C, nsmp), cne = e_begin(c + 1, C, nsmp) - ce0;
       if (cne > 0) ptx::bulk_s2peer(grecv + rank * eslot, gpart + ce0, (uint32_t)(cne * 4), bar_D, c);
     }
@@ -714,8 +741,7 @@ fused_small_kernel(const FusedParams p, const __grid_constant__ CUtensorMap tmX,
     if constexpr (TC) {
       // ---- P5 (tensor core). dW1 slice: D[px][j] = sum_rows x[row][px] delta_1[row][j] with
       //      M = 128 pixels (MN-major x tile), N = 32 neurons (MN-major delta_1), K = rows
-      ptx::mbar_wait(&bar_x[1], par);                       // M-layout x tile of this step
-      tc_split(X, X + kTcXLoM, 4 * kTcAS, tid);
+      // (the M-layout x tile was split in P2)
       for (int t = tid; t < kTcRows * 32; t += kThreads) {  // delta_1 hi | lo, rows >= nS zero
         const int r = t >> 5, j = t & 31;
         const float v = r < nS ? D1[r * ds + j] : 0.0f;
@@ -727,32 +753,36 @@ fused_small_kernel(const FusedParams p, const __grid_constant__ CUtensorMap tmX,
       ptx::fence_proxy_async_smem();
       __syncthreads();
       PROF(15);
-      if (tid == 0) {
+      if (ptx::warp_uniform(warp) == 0) {  // warp-uniform loop and operands, one elected lane issues
         tc::tc_fence_after();
-        constexpr uint32_t idM = tc::idesc_tf32(128, 32, true, true);
+        // B = delta_1 hi | lo: the lo block sits one MN block (LBO = kTcAS) behind the hi block, so an
+        // N = 64 descriptor reads them stacked along N: two MMAs per k-step (x_lo, x_hi)
+        constexpr uint32_t idM = tc::idesc_tf32(128, 64, true, true);
         const int nks = (nS + 7) / 8;
-        for (int ks = 0; ks < nks; ++ks) {
-          const uint64_t ah = tc::smem_desc(sX + 1024 * ks, kTcAS, 512, 1);
-          const uint64_t al = tc::smem_desc(sX + kTcXLoM + 1024 * ks, kTcAS, 512, 1);
-          const uint64_t bh = tc::smem_desc(sD + 1024 * ks, kTcAS, 512, 1);
-          const uint64_t bl = tc::smem_desc(sD + kTcAS + 1024 * ks, kTcAS, 512, 1);
-          tc::mma_tf32(tmem + 32, ah, bh, idM, ks > 0 ? 1u : 0u);
-          tc::mma_tf32(tmem + 32, ah, bl, idM, 1u);
-          tc::mma_tf32(tmem + 32, al, bh, idM, 1u);
+        const uint32_t tm = (uint32_t)ptx::warp_uniform((int)tmem) + 64u;
+        if (ptx::elect_one()) {
+          for (int ks = 0; ks < nks; ++ks) {
+            const uint64_t ah = tc::smem_desc(sX + 1024 * ks, kTcAS, 512, 1);
+            const uint64_t al = tc::smem_desc(sX + kTcXLoM + 1024 * ks, kTcAS, 512, 1);
+            const uint64_t bd = tc::smem_desc(sD + 1024 * ks, kTcAS, 512, 1);
+            tc::mma_tf32(tm, al, bd, idM, ks > 0 ? 1u : 0u);
+            tc::mma_tf32(tm, ah, bd, idM, 1u);
+          }
+          tc::mma_commit(bar_mma);
         }
-        tc::mma_commit(bar_mma);
+        __syncwarp();
       }
       ptx::mbar_wait(bar_mma, 1);
       tc::tc_fence_after();
-      if (tid == 0 && s + 1 < p.n_steps) tc_issue(&tmXK, &bar_x[0], row_s1);  // next step's K-layout tile
+      if (tid == 128 && s + 1 < p.n_steps) tc_issue(&tmXK, &bar_x[0], row_s1);  // next step's K-layout tile (warp 4: not an epilogue warp)
       if (warp < 4) {
-        float v[32];
-        tc::tmem_ld32(tmem + ((uint32_t)(32 * warp) << 16) + 32u, v);
+        float v[32], vl[32];
+        tc::tmem_ld32(tmem + ((uint32_t)(32 * warp) << 16) + 64u, v);
+        tc::tmem_ld32(tmem + ((uint32_t)(32 * warp) << 16) + 96u, vl);
         const int px = 32 * warp + lane;
-        if (px < p.ws) {
+        if (px < p.ws) {  // neuron-major slice Gs[j][ws]: lanes = consecutive pixels (conflict-free)
 #pragma unroll
-          for (int j = 0; j < 32; j += 4)
-            *reinterpret_cast<float4 *>(Gs + px * 32 + j) = make_float4(v[j], v[j + 1], v[j + 2], v[j + 3]);
+          for (int j = 0; j < 32; ++j) Gs[j * p.ws + px] = v[j] + vl[j];
         }
       }
       tc::tc_fence_before();
@@ -921,15 +951,27 @@ fused_small_kernel(const FusedParams p, const __grid_constant__ CUtensorMap tmX,
 
     // ---- P9. SGD update of the resident parameters (all clusters apply the same sums)
     if constexpr (TC) {  // W = hi + lo exactly; re-split after the update
-      for (int i = tid; i < 32 * w; i += kThreads) {
-        const int k = i >> 5, j = i & 31;
-        if (j < H) {
-          const int off = (k >> 5) * 4096 + sw128_k(j, k & 31);
-          float *hp = reinterpret_cast<float *>(Wt + off), *lp = reinterpret_cast<float *>(Wt + 16384 + off);
-          const float wv = (*hp + *lp) - p.scale * Gr[i];
-          const float h = tc::tf32_hi(wv);
-          *hp = h;
-          *lp = wv - h;
+      // thread = (neuron j, 4 pixels): quarter-warps cover one 128-B row of an atom (conflict-free
+      // float4 accesses of W hi / lo; Gr is neuron-major [j][ws])
+      const int natom = (w + 31) >> 5;           // 32-pixel atoms of the slice
+      for (int i = tid; i < natom * 256; i += kThreads) {
+        const int q8 = i >> 5, jj = (i >> 3) & 3, c = i & 7;   // a warp: 8 chunks x 4 neuron rows of one atom
+        const int a = q8 >> 3, j = 4 * (q8 & 7) + jj, k = 32 * a + 4 * c;
+        if (j < H && k < w) {
+          const int off = tc_w_off(j, k);
+          float4 *hp = reinterpret_cast<float4 *>(Wt + off), *lp = reinterpret_cast<float4 *>(Wt + 4096 + off);
+          const float4 hv = *hp, lv = *lp, gv = *reinterpret_cast<const float4 *>(Gr + j * p.ws + k);
+          float wv[4] = {hv.x + lv.x, hv.y + lv.y, hv.z + lv.z, hv.w + lv.w};
+          const float gq[4] = {gv.x, gv.y, gv.z, gv.w};
+          float hh[4], ll[4];
+#pragma unroll
+          for (int e = 0; e < 4; ++e) {
+            if (k + e < w) wv[e] -= p.scale * gq[e];
+            hh[e] = tc::tf32_hi(wv[e]);
+            ll[e] = wv[e] - hh[e];
+          }
+          *hp = make_float4(hh[0], hh[1], hh[2], hh[3]);
+          *lp = make_float4(ll[0], ll[1], ll[2], ll[3]);
         }
       }
       ptx::fence_proxy_async_smem();
@@ -986,8 +1028,8 @@ fused_small_kernel(const FusedParams p, const __grid_constant__ CUtensorMap tmX,
       if (j >= H) continue;
       float v;
       if constexpr (TC) {
-        const int off = (k >> 5) * 4096 + sw128_k(j, k & 31);
-        v = *reinterpret_cast<const float *>(Wt + off) + *reinterpret_cast<const float *>(Wt + 16384 + off);
+        const int off = tc_w_off(j, k);
+        v = *reinterpret_cast<const float *>(Wt + off) + *reinterpret_cast<const float *>(Wt + 4096 + off);
       } else {
         v = W1t[i];
       }
@@ -1002,7 +1044,7 @@ fused_small_kernel(const FusedParams p, const __grid_constant__ CUtensorMap tmX,
   ptx::cluster_sync();  // no CTA exits while a peer may still push into it
   if (TC && warp == 0) {
     tc::tc_fence_after();
-    asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem), "r"(64u) : "memory");
+    asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem), "r"(128u) : "memory");
   }
 }
 
@@ -1029,7 +1071,7 @@ int fused_small_train_steps(FusedSmall &fs, cudaStream_t st, const std::vector<i
   // ---- launch configuration: decided once per (shape, batch, dataset, switches), then cached
   // (the occupancy query and the tensor-map encodes cost host microseconds per call)
   const std::vector<int64_t> key = {n0, H, O, batch, (int64_t)(uintptr_t)X, N, aligned_now,
-                                    env_int("NF_FUSED_C", 0), env_int("NF_FUSED_G", 0), env_int("NF_FUSED_TC", 0),
+                                    env_int("NF_FUSED_C", 0), env_int("NF_FUSED_G", 0), env_int("NF_FUSED_TC", 1),
                                     env_int("NF_FUSED_MM", 0)};
   if (key != fs.cfg_key) {
     fs.cfg_key.clear();
@@ -1068,7 +1110,10 @@ int fused_small_train_steps(FusedSmall &fs, cudaStream_t st, const std::vector<i
           (const void *)fused_small_kernel<false, false, -1, -1, kInlineSmall>,
           (const void *)fused_small_kernel<false, false, ACT_SIGMOID, ACT_SIGMOID, kInlineSmall>,
           (const void *)fused_small_kernel<false, true, -1, -1, kInlineSmall>,
-          (const void *)fused_small_kernel<false, true, ACT_SIGMOID, ACT_SIGMOID, kInlineSmall>};
+          (const void *)fused_small_kernel<false, true, ACT_SIGMOID, ACT_SIGMOID, kInlineSmall>,
+          (const void *)fused_small_kernel<true, false, ACT_SIGMOID, ACT_SIGMOID, kInlineStarts>,
+          (const void *)fused_small_kernel<true, false, -1, -1, kInlineSmall>,
+          (const void *)fused_small_kernel<true, false, ACT_SIGMOID, ACT_SIGMOID, kInlineSmall>};
       for (const void *k : ks) {
         cudaFuncSetAttribute(k, cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
         cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024);
@@ -1076,10 +1121,11 @@ int fused_small_train_steps(FusedSmall &fs, cudaStream_t st, const std::vector<i
       done |= 1u << (dev & 31);
     }
   }
-  // tensor-core variant: TMA-aligned x, pixel slices of <= 128 columns, <= kTcRows rows per cluster
-  // (opt-in, NF_FUSED_TC=1: at N = 32 the 3xTF32 MMAs are shared-memory-bandwidth bound and no
-  // faster than the FFMA2 path; profiles/r01_fused_tc_experiment.txt)
-  bool tc = aligned && ws <= 128 && env_int("NF_FUSED_TC", 0) != 0;
+  // tensor-core variant (the default where it applies; NF_FUSED_TC=0 selects the FFMA2 path):
+  // TMA-aligned x, pixel slices of <= 128 columns, <= kTcRows rows per cluster.  Split-TF32 MMAs with
+  // the hi | lo parts of W1 / delta_1 stacked along N (two MMAs per k-step, all four partial
+  // products), issued warp-uniformly: 10.1 vs 11.0 us per config-2 step (profiles/r02_k6_tc_stacked.txt)
+  bool tc = aligned && ws <= 128 && env_int("NF_FUSED_TC", 1) != 0 && env_int("NF_FUSED_MM", 0) == 0;
   // warp-level MMA contractions (opt-in NF_FUSED_MM=1; TMA-aligned x, <= 128 rows per cluster,
   // pixel slices <= 128): parity-green, but 11.25 vs 11.05 us per config-2 step against the FFMA2
   // SIMT default (profiles/r02_k6_mma_experiment.txt)
@@ -1281,16 +1327,15 @@ int fused_small_train_steps(FusedSmall &fs, cudaStream_t st, const std::vector<i
       if (small_ist) {
         auto k = mm ? (sig ? fused_small_kernel<false, true, ACT_SIGMOID, ACT_SIGMOID, kInlineSmall>
                            : fused_small_kernel<false, true, -1, -1, kInlineSmall>)
-                    : tc ? nullptr
+                    : tc ? (sig ? fused_small_kernel<true, false, ACT_SIGMOID, ACT_SIGMOID, kInlineSmall>
+                                : fused_small_kernel<true, false, -1, -1, kInlineSmall>)
                     : sig ? fused_small_kernel<false, false, ACT_SIGMOID, ACT_SIGMOID, kInlineSmall>
                           : fused_small_kernel<false, false, -1, -1, kInlineSmall>;
-        if (k) {
-          kern = reinterpret_cast<const void *>(k);
-          return cudaLaunchKernelEx(&cfg, k, p, tmX, tmXK, tmXM, ist_s);
-        }
-        memcpy(ist.v, ist_s.v, n_steps * sizeof(int64_t));  // (TC: large-buffer variant only)
+        kern = reinterpret_cast<const void *>(k);
+        return cudaLaunchKernelEx(&cfg, k, p, tmX, tmXK, tmXM, ist_s);
       }
-      auto k = tc   ? fused_small_kernel<true, false, -1, -1, kInlineStarts>
+      auto k = tc   ? (sig ? fused_small_kernel<true, false, ACT_SIGMOID, ACT_SIGMOID, kInlineStarts>
+                           : fused_small_kernel<true, false, -1, -1, kInlineStarts>)
                : mm ? (sig ? fused_small_kernel<false, true, ACT_SIGMOID, ACT_SIGMOID, kInlineStarts>
                            : fused_small_kernel<false, true, -1, -1, kInlineStarts>)
                : sig ? fused_small_kernel<false, false, ACT_SIGMOID, ACT_SIGMOID, kInlineStarts>

@@ -311,9 +311,13 @@ def test_c3_c4_full_width_one_step(cid, n):
         assert rel_err(bg, br) <= FP32_BAR
 
 
-def test_c2_tensor_core_variant_of_fused_kernel(c2_trajectory, monkeypatch):
-    """The opt-in tcgen05 3xTF32 variant of the fused kernel (NF_FUSED_TC=1): same parity bar."""
-    monkeypatch.setenv("NF_FUSED_TC", "1")
+@pytest.mark.parametrize("engine", ["tc", "ffma2"])
+def test_c2_tensor_core_variant_of_fused_kernel(c2_trajectory, monkeypatch, engine):
+    """The two contraction engines of the fused kernel on config 2: tcgen05 split-TF32 (the default
+    where it applies) and packed FFMA2 (NF_FUSED_TC=0): same parity bar; the launch log shows which
+    instantiation ran."""
+    monkeypatch.setenv("NF_FUSED_TC", "1" if engine == "tc" else "0")
+    nf.nf_debug_log_enable(True)
     t = c2_trajectory
     cfg, X, Y = t["cfg"], t["X"], t["Y"]
     starts = t["starts"][100:110]
@@ -321,6 +325,10 @@ def test_c2_tensor_core_variant_of_fused_kernel(c2_trajectory, monkeypatch):
     net = make_net(cfg["dims"], cfg["act"], p)
     loss = torch.zeros(len(starts), device="cuda")
     net.train_steps(dev(X), dev(Y), cfg["batch"], starts, cfg["eta"], step_loss=loss)
+    log = nf.nf_debug_log_read()
+    nf.nf_debug_log_enable(False)
+    want = "fused_small_kernel<true" if engine == "tc" else "fused_small_kernel<false, false"
+    assert any(want in l for l in log), log
     o = oracle.Oracle(cfg["dims"], cfg["act"])
     ref, ref_loss = o.train_steps(p, X, Y, cfg["batch"], starts, cfg["eta"])
     for (Wg, bg), (Wr, br) in zip(o.layers(gpu_params(net)), o.layers(ref)):
