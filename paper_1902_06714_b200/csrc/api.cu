@@ -232,9 +232,12 @@ int ensure_ws(nf_net *net, int64_t rows) {
 // Which weight-gradient contractions read transposed (K-major) copies of their operands, written
 // by the producing epilogues: the big tensor-core ones (a wave of 128 x 256 tiles or more: config
 // 5's), whose MN-major smem operands cost ~16 % of the tensor rate.
-// NF_MATH_TF32 by default (NF_TPOSE=0 off, NF_TPOSE=2 also in the 3xTF32 fp32 mode).
+// Off by default since the tensor-core instructions are issued warp-uniformly (the MN/MN kernel no
+// longer pays the per-instruction issue overhead and the transposed copies' extra HBM writes cost
+// more than they save: config 5 TF32 7.73 -> 7.36 ms per step, profiles/r02_uniform_issue.txt);
+// NF_TPOSE=1 turns it on for NF_MATH_TF32, NF_TPOSE=2 also in the 3xTF32 fp32 mode.
 int ensure_tpose(nf_net *net, const float *x, int64_t n) {
-  static const int mode = getenv("NF_TPOSE") ? atoi(getenv("NF_TPOSE")) : 1;
+  const int mode = getenv("NF_TPOSE") ? atoi(getenv("NF_TPOSE")) : 0;  // (read per call: tests toggle it)
   const int L = net->L;
   std::vector<char> tp(L + 1, 0);
   const bool on = mode == 2 ? net->math != NF_MATH_FP64 : (mode == 1 && net->math == NF_MATH_TF32);

@@ -161,3 +161,35 @@ def test_full_batch_grad_split_invariance(cid, math):
     for (Wa, ba), (Wb, bb) in zip(o.layers(g), o.layers(g1 + g2)):
         check(Wa, Wb, math)
         check(ba, bb, math)
+
+
+def test_transposed_gradient_operands(monkeypatch, engine):
+    """NF_TPOSE=1 (opt-in since the warp-uniform MMA issue): the forward / delta epilogues also store
+    A_l^T / delta_l^T so that the weight-gradient contraction reads K-major operands (store_t, the
+    K/K persistent EpiGrad).  One TF32 SGD step at config-5 widths (a wave or more of 128 x 256
+    tiles per GEMM) against the batched fp64 oracle, tanh hidden layers (reading R20)."""
+    if engine != "tcgen05":
+        pytest.skip("tcgen05 path only")
+    from oracle.batched import BatchedOracle
+    monkeypatch.setenv("NF_TPOSE", "1")
+    dims, act, B = [4096, 4096, 4096, 1024], "tanh,sigmoid", 2048
+    p = synth.init_params(5, dims)
+    X, Y = synth.dataset(5, N=B)
+    X = np.ascontiguousarray(X[:, :dims[0]])
+    Y = np.ascontiguousarray(Y[:, :dims[-1]])
+    o = BatchedOracle(dims, act)
+    eta = 5.0
+    ref, _, _ = o.train_batch(p, X, Y, eta)
+    net = make_net(dims, act, p, nf.NF_MATH_TF32)
+    nf.nf_debug_log_enable(True)
+    net.train_steps(dev(X), dev(Y), B, [0], eta)
+    torch.cuda.synchronize()
+    log = nf.nf_debug_log_read()
+    nf.nf_debug_log_enable(False)
+    # the K-major / K-major weight-gradient instantiation ran (MN / MN without the transposed copies)
+    assert any("gemm_tc_persistent<256, false, false, nf::EpiGrad" in l.replace("(bool)0", "false").replace("<256, 0, 0,", "<256, false, false,")
+               for l in log), log
+    got = gpu_params(net)
+    for (Wg, bg), (Wr, br), (W0, b0) in zip(o.layers(got), o.layers(ref), o.layers(p.astype(np.float64))):
+        assert rel_err(Wg - W0, Wr - W0, tau=1.0) <= TF32_BAR
+        assert rel_err(bg - b0, br - b0, tau=1.0) <= TF32_BAR
