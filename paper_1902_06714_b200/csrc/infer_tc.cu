@@ -106,9 +106,9 @@ infer_tc_kernel(const InferTcParams p, const __grid_constant__ CUtensorMap tmX,
   uint32_t *tslot = reinterpret_cast<uint32_t *>(wempty + kWStages);
   const int tid = threadIdx.x, warp = ptx::warp_uniform(tid >> 5), lane = tid & 31;
 
-  // this CTA's rows: an equal share of whole 32-row blocks
-  const int64_t bb = (int64_t)blockIdx.x * p.nblk / gridDim.x, be = (int64_t)(blockIdx.x + 1) * p.nblk / gridDim.x;
-  const int64_t r0 = bb * kBoxRows, r1 = min(p.n, be * kBoxRows);
+  // this CTA's rows: an equal share of the rows (+-1; a TMA box may start at any row, and the rows a
+  // last box reads past r1 -- the next CTA's, or zero fill past n -- are computed and not stored)
+  const int64_t r0 = (int64_t)blockIdx.x * p.n / gridDim.x, r1 = (int64_t)(blockIdx.x + 1) * p.n / gridDim.x;
   const int ntiles = r1 > r0 ? (int)((r1 - r0 + kTileRows - 1) / kTileRows) : 0;
 
   if (tid == 0) {
