@@ -558,10 +558,12 @@ fused_small_kernel(const FusedParams p, const __grid_constant__ CUtensorMap tmX,
 #pragma unroll
         for (int j = 0; j < 32; ++j) v[j] += vl[j];
         const int r = 32 * warp + lane;
-        if (r < nS) {
+        if (r < nS) {  // 16-B chunk c of row r at chunk c ^ (r % 8): the eight lanes of a store phase
+                       // hit eight different bank groups (P3 reads the rows back with the same key)
 #pragma unroll
           for (int j = 0; j < 32; j += 4)
-            *reinterpret_cast<float4 *>(Pfull + r * 32 + j) = make_float4(v[j], v[j + 1], v[j + 2], v[j + 3]);
+            *reinterpret_cast<float4 *>(Pfull + r * 32 + ((((j >> 2) ^ (r & 7))) << 2)) =
+                make_float4(v[j], v[j + 1], v[j + 2], v[j + 3]);
         }
       }
       tc::tc_fence_before();
@@ -650,10 +652,12 @@ fused_small_kernel(const FusedParams p, const __grid_constant__ CUtensorMap tmX,
     float lacc = 0.0f;
     for (int t = tid; t < nOwn * 32; t += kThreads) {
       const int q = t >> 5, j = t & 31, i = o0 + q;
+      // (TC: the partial rows are stored with their 16-B chunks permuted by the row index)
+      const int jc = TC ? ((((j >> 2) ^ (i & 7)) << 2) | (j & 3)) : j;
       float z = b1s[j];
 #pragma unroll
       for (int c = 0; c < kMaxC; ++c)
-        if (c < C) z += (c == rank) ? Pfull[i * 32 + j] : Pown[(c * p.nOwnMax + q) * 32 + j];
+        if (c < C) z += (c == rank) ? Pfull[i * 32 + jc] : Pown[(c * p.nOwnMax + q) * 32 + jc];
       float a1, s1;
       act_sel<AH, AO>(p.act_h, z, a1, s1);
       A1own[t] = j < H ? a1 : 0.0f;

@@ -20,3 +20,10 @@ starts = synth.batch_starts(2, steps=steps)
 for _ in range(2):
     net.train_steps(Xd, Yd, cfg["batch"], starts, cfg["eta"])
 torch.cuda.synchronize()
+if os.environ.get("PP_FRESH"):  # a third call on fresh batch starts after an L2 flush: x from HBM, as in bench.py
+    flush = torch.empty(64 * 1024 * 1024, dtype=torch.float32, device="cuda")
+    flush.fill_(1.0)
+    torch.cuda.synchronize()
+    print("---- fresh starts, L2 flushed", file=sys.stderr, flush=True)
+    net.train_steps(Xd, Yd, cfg["batch"], synth.batch_starts(2, steps=2 * steps)[steps:], cfg["eta"])
+    torch.cuda.synchronize()
