@@ -370,6 +370,13 @@ fused_small_kernel(const FusedParams p, const __grid_constant__ CUtensorMap tmX,
 
   // ---- one-time setup: zero smem, barriers, resident parameters
   for (int i = 32 + tid; i < L.total; i += kThreads) sm[i] = 0.0f;
+  if (TC) {  // rows >= nS of P5's delta_1 operand (hi and lo blocks) are never written: zero for all steps
+             // (the 1024-B alignment pad of the operand area may reach past the loop above)
+    for (int t = tid; t < (kTcRows - nS) * 64; t += kThreads) {
+      const int r = nS + (t >> 6), c = t & 63;
+      *reinterpret_cast<float *>(Dt + (c >= 32 ? kTcAS : 0) + r * 128 + (c & 31) * 4) = 0.0f;
+    }
+  }
   if (tid == 0) {
     ptx::mbar_init(&bar_x[0], 1);
     ptx::mbar_init(&bar_x[1], 1);
@@ -444,7 +451,7 @@ fused_small_kernel(const FusedParams p, const __grid_constant__ CUtensorMap tmX,
   for (int c = 0; c < C; ++c) {
     if (c == rank) continue;
     bytesP += nOwn * 128;
-    bytesD += (own_begin(c + 1, nS, C) - own_begin(c, nS, C)) * ds * 4 + ne * 4;
+    bytesD += (own_begin(c + 1, nS, C) - own_begin(c, nS, C)) * (TC ? 256 : ds * 4) + ne * 4;  // (TC: hi + lo rows of the MMA operand)
   }
   const uint32_t bytesG = (uint32_t)(p.gsl * 4 + nsmp * 4);
 
@@ -700,7 +707,15 @@ fused_small_kernel(const FusedParams p, const __grid_constant__ CUtensorMap tmX,
           t1 = fmaf(W2s[(o + 1) * 33 + j], vd[o + 1], t1);
         }
       }
-      D1[i * ds + j] = j < H ? (t0 + t1) * D1[i * ds + j] : 0.0f;
+      const float d1 = j < H ? (t0 + t1) * D1[i * ds + j] : 0.0f;
+      D1[i * ds + j] = d1;
+      if constexpr (TC) {  // the owner writes its rows of P5's B operand (delta_1 hi | lo, MN-major, a
+        // row = 128 contiguous bytes permuted inside) and pushes those rows: no peer rebuilds them
+        const float h = tc::tf32_hi(d1);
+        const int off = sw128_32b(i, j);
+        *reinterpret_cast<float *>(Dt + off) = h;
+        *reinterpret_cast<float *>(Dt + kTcAS + off) = d1 - h;
+      }
     }
     {
       const float l = warp_sum(lacc);
@@ -713,8 +728,14 @@ fused_small_kernel(const FusedParams p, const __grid_constant__ CUtensorMap tmX,
     // ---- P4. push the owned delta_1 rows to every peer at once; then this CTA's W2/b1/b2
     //      tendency partial over its owned rows (a 10x30x9 contraction) and its slices to
     //      the ranks that reduce them
-    if (lane == 0 && warp < C && warp != rank && nOwn > 0)
-      ptx::bulk_s2peer(D1 + o0 * ds, D1 + o0 * ds, (uint32_t)(nOwn * ds * 4), bar_D, warp);
+    if (lane == 0 && warp < C && warp != rank && nOwn > 0) {
+      if constexpr (TC) {
+        ptx::bulk_s2peer(Dt + o0 * 128, Dt + o0 * 128, (uint32_t)(nOwn * 128), bar_D, warp);
+        ptx::bulk_s2peer(Dt + kTcAS + o0 * 128, Dt + kTcAS + o0 * 128, (uint32_t)(nOwn * 128), bar_D, warp);
+      } else {
+        ptx::bulk_s2peer(D1 + o0 * ds, D1 + o0 * ds, (uint32_t)(nOwn * ds * 4), bar_D, warp);
+      }
+    }
     for (int t = tid; t < nsmp; t += kThreads) {
       float v = 0.0f;
       if (t < O * H) {
@@ -745,17 +766,8 @@ fused_small_kernel(const FusedParams p, const __grid_constant__ CUtensorMap tmX,
     if constexpr (TC) {
       // ---- P5 (tensor core). dW1 slice: D[px][j] = sum_rows x[row][px] delta_1[row][j] with
       //      M = 128 pixels (MN-major x tile), N = 32 neurons (MN-major delta_1), K = rows
-      // (the M-layout x tile was split in P2)
-      for (int t = tid; t < kTcRows * 32; t += kThreads) {  // delta_1 hi | lo, rows >= nS zero
-        const int r = t >> 5, j = t & 31;
-        const float v = r < nS ? D1[r * ds + j] : 0.0f;
-        const float h = tc::tf32_hi(v);
-        const int off = sw128_32b(r, j);
-        *reinterpret_cast<float *>(Dt + off) = h;
-        *reinterpret_cast<float *>(Dt + kTcAS + off) = v - h;
-      }
-      ptx::fence_proxy_async_smem();
-      __syncthreads();
+      // (the M-layout x tile was split in P2; the delta_1 hi | lo rows were written by their owners in
+      //  P3 and pushed in P4: rows >= nS of the operand stay zero from the kernel's set-up)
       PROF(15);
       if (ptx::warp_uniform(warp) == 0) {  // warp-uniform loop and operands, one elected lane issues
         tc::tc_fence_after();
