@@ -196,13 +196,16 @@ __device__ __forceinline__ int sw128_k(int r, int c) { return r * 128 + ((((c >>
 // B descriptor of N = 64 rows reads W_hi and W_lo stacked along N
 __device__ __forceinline__ int tc_w_off(int j, int k) { return (k >> 5) * 8192 + sw128_k(j, k & 31); }
 __device__ __forceinline__ int sw128_32b(int r, int c) { return r * 128 + ((((c >> 3) ^ (r & 3))) << 5) + ((c & 7) << 2); }
-// in-place TF32 split of `bytes` of staged fp32 data: hi = rn_tf32(x) in place, lo = x - hi (exact)
-__device__ __forceinline__ void tc_split(uint8_t *hi, uint8_t *lo, int bytes, int tid) {
-  for (int i = tid; i < bytes / 16; i += kThreads) {
+// TF32 split of `bytes` of staged fp32 data (the x tiles)
+__device__ __forceinline__ void tc_split(const uint8_t *hi, uint8_t *lo, int bytes, int tid, int nthreads = kThreads,
+                                         int part = 0, int nparts = 1) {
+  // truncation split: the tensor core reads the staged fp32 tile itself as the hi part (it drops the
+  // low 13 mantissa bits), so only lo = rn_tf32(x - trunc(x)) is written -- no in-place store, and the
+  // loads of successive chunks are independent of the stores
+  const int n16 = bytes / 16, i0 = (int)((int64_t)n16 * part / nparts), i1 = (int)((int64_t)n16 * (part + 1) / nparts);
+  for (int i = i0 + tid; i < i1; i += nthreads) {
     const float4 x = reinterpret_cast<const float4 *>(hi)[i];
-    const float4 h = make_float4(tc::tf32_hi(x.x), tc::tf32_hi(x.y), tc::tf32_hi(x.z), tc::tf32_hi(x.w));
-    reinterpret_cast<float4 *>(hi)[i] = h;
-    reinterpret_cast<float4 *>(lo)[i] = make_float4(x.x - h.x, x.y - h.y, x.z - h.z, x.w - h.w);
+    reinterpret_cast<float4 *>(lo)[i] = make_float4(tf32_lo(x.x), tf32_lo(x.y), tf32_lo(x.z), tf32_lo(x.w));
   }
 }
 
@@ -645,9 +648,15 @@ fused_small_kernel(const FusedParams p, const __grid_constant__ CUtensorMap tmX,
       if (na > 0)
         ptx::bulk_s2peer(Pown + rank * p.nOwnMax * 32, Pfull + a0 * 32, (uint32_t)(na * 128), bar_P, c);
     }
-    if constexpr (TC) {  // the M-layout x tile of this step (issued after P1's MMAs) is split for P5
-      ptx::mbar_wait(&bar_x[1], par);   // here, while the peers' partial rows are still in flight
-      tc_split(X, X + kTcXLoM, 4 * kTcAS, tid);
+    // TC: the M-layout x tile of this step (issued after P1's MMAs) is split for P5 by the warps that
+    // have no P3 task (warps >= 9 when a CTA owns <= 9 rows), a third per P3 pass; otherwise here,
+    // while the peers' partial rows are still in flight
+    const bool split_in_p3 = TC && p.nOwnMax <= 9;
+    if constexpr (TC) {
+      if (!split_in_p3) {
+        ptx::mbar_wait(&bar_x[1], par);
+        tc_split(X, X + kTcXLoM, 4 * kTcAS, tid);
+      }
     }
     ptx::mbar_wait(bar_P, par);
     PROF(3);
@@ -657,6 +666,12 @@ fused_small_kernel(const FusedParams p, const __grid_constant__ CUtensorMap tmX,
     //      (b) thread (q, o): z2 = b2 + W2 a1, a2, delta_2 = (a2 - y) sigma'(z2), cost
     //      (c) thread (q, j): delta_1 = sigma'(z1) * W2^T delta_2
     float lacc = 0.0f;
+    if constexpr (TC) {
+      if (split_in_p3 && warp >= 9) {
+        ptx::mbar_wait(&bar_x[1], par);
+        tc_split(X, X + kTcXLoM, 4 * kTcAS, tid - 288, kThreads - 288, 0, 3);
+      }
+    }
     for (int t = tid; t < nOwn * 32; t += kThreads) {
       const int q = t >> 5, j = t & 31, i = o0 + q;
       // (TC: the partial rows are stored with their 16-B chunks permuted by the row index)
@@ -672,6 +687,9 @@ fused_small_kernel(const FusedParams p, const __grid_constant__ CUtensorMap tmX,
     }
     __syncthreads();
     PROF(11);
+    if constexpr (TC) {
+      if (split_in_p3 && warp >= 9) tc_split(X, X + kTcXLoM, 4 * kTcAS, tid - 288, kThreads - 288, 1, 3);
+    }
     for (int t = tid; t < nOwn * O; t += kThreads) {
       const int q = t / O, o = t - q * O;
       const float *va = A1own + q * 32, *w2 = W2s + o * 33;
@@ -696,6 +714,9 @@ fused_small_kernel(const FusedParams p, const __grid_constant__ CUtensorMap tmX,
     }
     __syncthreads();
     PROF(12);
+    if constexpr (TC) {
+      if (split_in_p3 && warp >= 9) tc_split(X, X + kTcXLoM, 4 * kTcAS, tid - 288, kThreads - 288, 2, 3);
+    }
     for (int t = tid; t < nOwn * 32; t += kThreads) {
       const int q = t >> 5, j = t & 31, i = o0 + q;
       const float *vd = D2own + q * 32;
