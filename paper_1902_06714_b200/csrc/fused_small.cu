@@ -29,12 +29,17 @@
 //       P9  W -= (eta/B) G on the resident parameters; zero this CTA's share of the
 //           accumulator used two steps ahead
 //
-// Contraction engines of P1 / P5 (template MM, chosen per launch): packed FFMA2 SIMT (default), or
-// the warp-level tensor-core MMA (mma.sync m16n8k8 TF32, 3xTF32 = hi*hi + hi*lo + lo*hi, fp32
-// accumulate; NF_FUSED_MM=1).  HMMA runs 511 MAC/clk/SM at ~21 cycles latency with register
-// operands, while tcgen05's issue -> commit -> mbarrier round trip alone is 1.3-3 K cycles at these
-// 128 x 32 shapes (profiles/r02_micro_small_mma_launch.txt); but 3xTF32 needs three HMMAs per
-// product and the m16 / k8 tiles pad config 2's 67 rows x 100 pixels, so MM measured no faster.
+// Contraction engines of P1 / P5 (templates TC / MM, chosen per launch):
+//   * tcgen05 split-TF32 (TC, the default where it applies: TMA-aligned x, pixel slices <= 128, <= 72
+//     rows per cluster): x tiles staged by TMA in the K-major and the MN-major operand layouts, the
+//     tensor core truncates them to their hi part, lo = rn_tf32(x - trunc(x)) written beside them;
+//     W1 hi | lo and delta_1 hi | lo stacked along N, so two N = 64 MMAs per k-step (x_lo, x_hi)
+//     give all four partial products; warp-uniform issue (ptx::warp_uniform / ptx::elect_one);
+//     delta_1's operand rows written by their owners in P3 and pushed in P4; neuron-major dW1 slice.
+//     9.9 us per config-2 step;
+//   * packed FFMA2 SIMT (NF_FUSED_TC=0 and every other shape): 11.0 us;
+//   * warp-level tensor-core MMA (mma.sync m16n8k8 TF32, 3xTF32, NF_FUSED_MM=1): three HMMAs per
+//     product and m16 / k8 padding of 67 rows x 100 pixels: 11.25 us (profiles/r02_k6_mma_experiment.txt).
 #include <algorithm>
 #include <cstdio>
 #include <cstdlib>
@@ -1161,7 +1166,7 @@ int fused_small_train_steps(FusedSmall &fs, cudaStream_t st, const std::vector<i
   // tensor-core variant (the default where it applies; NF_FUSED_TC=0 selects the FFMA2 path):
   // TMA-aligned x, pixel slices of <= 128 columns, <= kTcRows rows per cluster.  Split-TF32 MMAs with
   // the hi | lo parts of W1 / delta_1 stacked along N (two MMAs per k-step, all four partial
-  // products), issued warp-uniformly: 10.1 vs 11.0 us per config-2 step (profiles/r02_k6_tc_stacked.txt)
+  // products), issued warp-uniformly: 9.9 vs 11.0 us per config-2 step (profiles/r02_k6_tc_stacked.txt)
   bool tc = aligned && ws <= 128 && env_int("NF_FUSED_TC", 1) != 0 && env_int("NF_FUSED_MM", 0) == 0;
   // warp-level MMA contractions (opt-in NF_FUSED_MM=1; TMA-aligned x, <= 128 rows per cluster,
   // pixel slices <= 128): parity-green, but 11.25 vs 11.05 us per config-2 step against the FFMA2
