@@ -62,8 +62,23 @@ struct Cfg {
   static constexpr int B_BYTES = BN * BK * 4;
   static constexpr int RAW_BYTES = A_BYTES + B_BYTES;
   static constexpr int STAGE_BYTES = SPLIT == 3 ? 2 * RAW_BYTES : RAW_BYTES;  // raw(hi) | lo
-  static constexpr int STAGES_FIT = (kSmemBudget - EPI_BYTES - 1024 - 512) / STAGE_BYTES;
-  static constexpr int STAGES = STAGES_FIT > MAXST ? MAXST : STAGES_FIT;
+  // The per-tile kernel's epilogue transpose buffers may overlay the operand ring (the ring is dead
+  // once the accumulator barrier fires: every stage has been consumed): used where that buys a
+  // stage (the one-wave 128 x 256 tiles with 16 epilogue warps, config 3: 3 -> 4 stages).  The
+  // persistent kernel drains tile i while tile i+1 streams and keeps them apart.
+  static constexpr int FIT_SEP = (kSmemBudget - EPI_BYTES - 1024 - 512) / STAGE_BYTES;
+  static constexpr int FIT_OVL = (kSmemBudget - 1024 - 512) / STAGE_BYTES;
+  static constexpr int ST_SEP = FIT_SEP > MAXST ? MAXST : FIT_SEP;
+  static constexpr int ST_OVL = FIT_OVL > MAXST ? MAXST : FIT_OVL;
+#ifdef NF_TC_NO_OVERLAY
+  static constexpr bool OVL = false;
+#else
+  static constexpr bool OVL = ST_OVL > ST_SEP;
+#endif
+  static constexpr int STAGES = OVL ? ST_OVL : ST_SEP;
+  static constexpr int RING_BYTES = STAGES * STAGE_BYTES;
+  static constexpr int EPI_OFF = OVL ? 0 : RING_BYTES;                                  // epilogue buffers
+  static constexpr int BAR_OFF = OVL ? (RING_BYTES > EPI_BYTES ? RING_BYTES : EPI_BYTES) : RING_BYTES + EPI_BYTES;
   // NACC accumulators (all 512 TMEM columns): K-step t accumulates into t % NACC, and
   // the epilogue sums them in fp32.  The tensor core's fp32 accumulation truncates
   // (measured error linear in K, micro/tc_major_test.cu); spreading the K-steps over
@@ -73,7 +88,7 @@ struct Cfg {
   // take its TMEM while this one drains.
   static constexpr int NACC = SPLIT == 3 ? 512 / BN : 1;
   static constexpr int TMEM_COLS = SPLIT == 3 ? 512 : (BN < 32 ? 32 : BN);
-  static constexpr int SMEM = STAGES * STAGE_BYTES + EPI_BYTES + 1024 /*align*/ + 512 /*barriers*/;
+  static constexpr int SMEM = BAR_OFF + 1024 /*align*/ + 512 /*barriers*/;
   static_assert(STAGES >= 2, "ring too shallow");
 };
 
@@ -164,8 +179,8 @@ gemm_tc_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ 
   ptx::pdl_trigger();
   extern __shared__ uint8_t smem_raw[];
   uint8_t *smem = reinterpret_cast<uint8_t *>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
-  float *epibuf = reinterpret_cast<float *>(smem + C::STAGES * C::STAGE_BYTES);
-  uint64_t *full = reinterpret_cast<uint64_t *>(smem + C::STAGES * C::STAGE_BYTES + C::EPI_BYTES);
+  float *epibuf = reinterpret_cast<float *>(smem + C::EPI_OFF);
+  uint64_t *full = reinterpret_cast<uint64_t *>(smem + C::BAR_OFF);
   uint64_t *empty = full + C::STAGES;
   uint64_t *conv = empty + C::STAGES;
   uint64_t *accum = conv + C::STAGES;
@@ -359,6 +374,7 @@ gemm_tc_persistent(const __grid_constant__ CUtensorMap tmA, const __grid_constan
                    int K, Epi epi) {
   using C = Cfg<BN, 1>;
   static_assert(2 * BN <= 512, "two accumulator stages must fit in TMEM");
+  static_assert(!C::OVL, "the persistent kernel's epilogue buffers live beside the ring");
   ptx::pdl_trigger();
   extern __shared__ uint8_t smem_raw[];
   uint8_t *smem = reinterpret_cast<uint8_t *>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
